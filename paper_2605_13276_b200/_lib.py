@@ -1,0 +1,125 @@
+"""ctypes binding of libdvla_b200.so (the C-ABI in include/dvla_b200.h).
+
+This is the only place Python touches native code.  There is no fallback:
+if the shared library is missing or fails to load, importing the package's
+compute modules raises immediately (the product path must never route
+through a CPU implementation).  ctypes releases the GIL for the duration of
+every call, which gives the four swimlane threads the same concurrency the
+reference gets from numba's nogil kernels (reference
+kernels/numba_backend.py:1-5).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+from .core import ConfigError, UsageError
+
+_LIB_PATH = Path(__file__).resolve().parent / "libdvla_b200.so"
+
+# status codes (include/dvla_b200.h: enum dvla_status)
+OK = 0
+ERR_USAGE = 1
+ERR_CONFIG = 2
+ERR_GRPO_ABORT = 3
+ERR_ALLOC_FAILURE = 4
+ERR_POOL_USAGE = 5
+ERR_CUDA = 6
+ERR_DECODE = 7
+ERR_TIMEOUT = 8
+
+F32, BF16, U8, F64 = 0, 1, 2, 3
+TL_WRITE_DLOGITS = 1
+TL_UNFUSED = 2
+
+ST_LOSS, ST_RATIO_SUM, ST_CLIP_COUNT, ST_CHUNK_COUNT = 0, 1, 2, 3
+ST_ABORT, ST_ABORT_GROUP, ST_KERNEL_ERR, ST_RESERVED, ST_LEN = 4, 5, 6, 7, 8
+
+
+class NativeError(RuntimeError):
+    """CUDA-level failure inside libdvla_b200 (no reference analogue)."""
+
+
+class ReplicationTimeout(RuntimeError):
+    """A replication flag wait exceeded its deadline (peer never delivered)."""
+
+
+def _load():
+    if not _LIB_PATH.exists():
+        raise ImportError(
+            f"{_LIB_PATH} is missing: build it with `python -m paper_2605_13276_b200.build` "
+            "(there is no CPU fallback)")
+    return C.CDLL(str(_LIB_PATH), mode=os.RTLD_LOCAL)
+
+
+lib = _load()
+
+_vp = C.c_void_p
+_i64 = C.c_int64
+_i32 = C.c_int
+_f64 = C.c_double
+_sz = C.c_size_t
+
+
+def _proto(name, args, res=C.c_int):
+    fn = getattr(lib, name)
+    fn.argtypes = args
+    fn.restype = res
+    return fn
+
+
+dvla_last_error = _proto("dvla_last_error", [], C.c_char_p)
+dvla_abi_version = _proto("dvla_abi_version", [], C.c_int)
+
+dvla_profile_enable = _proto("dvla_profile_enable", [_i32])
+dvla_profile_collect = _proto("dvla_profile_collect", [C.POINTER(C.c_double), C.POINTER(_i64)])
+dvla_advantages = _proto("dvla_advantages", [_vp, _i64, _i64, _f64, _vp, _vp])
+dvla_group_advantages = _proto("dvla_group_advantages", [_vp, _i64, _i64, _f64, _vp, _vp, _vp])
+dvla_token_loss_workspace_bytes = _proto(
+    "dvla_token_loss_workspace_bytes", [_i64, _i64, _i64, _i64], _sz)
+dvla_token_loss_fwd_bwd = _proto("dvla_token_loss_fwd_bwd", [
+    _vp, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64,
+    _f64, _f64, _f64, _i32, _vp, _vp, _vp, _vp, _sz, _vp])
+dvla_grpo_epilogue = _proto("dvla_grpo_epilogue", [
+    _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _f64, _f64, _vp, _vp, _vp])
+
+
+def last_error() -> str:
+    msg = dvla_last_error()
+    return msg.decode("utf-8", "replace") if msg else ""
+
+
+def check(status: int, what: str = "") -> None:
+    """Map a dvla status onto the reference's exception types."""
+    if status == OK:
+        return
+    msg = last_error() or what
+    if status == ERR_CONFIG:
+        raise ConfigError(msg)
+    if status == ERR_USAGE:
+        raise UsageError(msg)
+    if status == ERR_POOL_USAGE:
+        from .pools import PoolUsageError
+        raise PoolUsageError(msg)
+    if status == ERR_TIMEOUT:
+        raise ReplicationTimeout(msg)
+    if status == ERR_DECODE:
+        from .wire import DecodeError
+        raise DecodeError(-1, msg)
+    raise NativeError(f"{what}: {msg} (status {status})")
+
+
+def profile_collect() -> tuple[float, int]:
+    ms = C.c_double(0.0)
+    n = _i64(0)
+    check(dvla_profile_collect(C.byref(ms), C.byref(n)), "dvla_profile_collect")
+    return ms.value, n.value
+
+
+def exported_symbols() -> list[str]:
+    """Every dvla_* symbol the header declares (parsed from include/)."""
+    import re
+    hdr = (Path(__file__).resolve().parent.parent / "include" / "dvla_b200.h").read_text()
+    return sorted(set(re.findall(r"\b(dvla_[a-z0-9_]+)\s*\(", hdr)))

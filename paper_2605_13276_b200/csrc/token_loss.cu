@@ -1,0 +1,801 @@
+// Fused GRPO action-token loss: log-softmax gather (forward) + clipped-ratio
+// surrogate with group-normalised advantages + d loss / d logits (backward).
+//
+// Reference semantics (the per-chunk joint log-prob analogue of
+// kernels/numba_backend.py:49-61 chunk_log_prob, with "one Gaussian dim"
+// -> "one action token"):
+//   lp_tok[r]  = x[r, tgt_r] - logsumexp_v x[r, v]                 (f64)
+//   lp[q]      = sum_{t=0..T-1} lp_tok[q*T + t]   (sequential, f64)
+//   rho, loss, coeff per chunk           <- grpo.py:252-268 (grpo_math.cuh)
+//   dlogits[r, v] = coeff[q] * (1[v == tgt_r] - softmax(x[r])_v)
+// i.e. the chain rule of policy.backward_batch (grpo.py:277) through the
+// token head instead of the Gaussian head (numba_backend.py:92-99).
+//
+// Kernels
+//   tok_adv_kernel        advantages per group (bit-exact, grpo.py:89-99)
+//   tok_fused_bf16_kernel persistent, 1 CTA/SM, warp-specialised: a producer
+//                         warp streams logits rows HBM->SMEM with TMA bulk
+//                         copies (cp.async.bulk), 16 compute warps do
+//                         max / sum-exp (MUFU ex2) / gather on the SMEM row,
+//                         publish lp_tok, and the last CTA to finish a chunk
+//                         computes that chunk's coefficient; dlogits are then
+//                         written in place in SMEM and TMA-stored back.
+//                         Logits are read from HBM exactly once:
+//                         compulsory traffic 2*N*2 bytes.
+//   tok_rows_kernel<T>    unfused forward (any dtype / alignment / V)
+//   tok_chunk_kernel      unfused per-chunk coefficient
+//   tok_bwd_kernel<T>     unfused backward (re-reads logits: 3*N*s traffic)
+//   grpo_epilogue_kernel  loss / stats / abort detection in canonical order
+#include "common.cuh"
+#include "grpo_math.cuh"
+
+namespace dvla {
+
+constexpr int kFusedComputeWarps = 16;
+constexpr int kFusedComputeThreads = kFusedComputeWarps * 32;
+constexpr int kFusedThreads = kFusedComputeThreads + 32;  // + producer warp
+constexpr int kFusedStages = 3;
+constexpr uint64_t kSpinTimeoutNs = 4000000000ull;  // 4 s: report, never hang
+
+struct TokParams {
+  const void* logits;
+  const int32_t* tokens;
+  const float* blp;
+  const double* adv;
+  void* dlogits;
+  double* lp_tok;
+  double* lse;
+  double* lp_chunk;
+  double* coeff;
+  uint32_t* cnt;
+  uint32_t* err;
+  int64_t R, V, T, C, n_chunks;
+  double w, clip_eps, kl_coeff;
+};
+
+enum : uint32_t { kErrToken = 1u, kErrTimeout = 2u };
+
+// ------------------------------------------------------------ advantages
+__global__ void tok_adv_kernel(const float* __restrict__ rewards, int64_t n_groups, int64_t G,
+                               double delta, double* __restrict__ adv,
+                               uint32_t* __restrict__ reward_bad) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= n_groups) return;
+  const float* r = rewards + g * G;
+  double* a = adv + g * G;
+  auto get = [&](int64_t i) { return static_cast<double>(r[i]); };
+  group_advantages(get, G, delta, [&](int64_t i, double v) { a[i] = v; });
+  uint32_t bad = 0;
+  for (int64_t i = 0; i < G; ++i) bad |= !isfinite(r[i]);
+  reward_bad[g] = bad;
+}
+
+__global__ void adv_f64_kernel(const double* __restrict__ rewards, int64_t n_groups, int64_t G,
+                               double delta, double* __restrict__ adv) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= n_groups) return;
+  const double* r = rewards + g * G;
+  double* a = adv + g * G;
+  group_advantages([&](int64_t i) { return r[i]; }, G, delta,
+                   [&](int64_t i, double v) { a[i] = v; });
+}
+
+// Sequential (t = 0..T-1) f64 sum of a chunk's token log-probs by one warp;
+// result valid in lane 0.  Loads are issued 32 at a time.
+__device__ __forceinline__ double warp_chunk_lp(const double* __restrict__ lp_tok, int64_t T,
+                                                int lane) {
+  double acc = 0.0;
+  for (int64_t m0 = 0; m0 < T; m0 += 32) {
+    double v = (m0 + lane < T) ? __ldcg(lp_tok + m0 + lane) : 0.0;
+    const int lim = (T - m0 < 32) ? static_cast<int>(T - m0) : 32;
+    for (int l = 0; l < lim; ++l) {
+      double x = __shfl_sync(0xffffffffu, v, l);
+      acc = __dadd_rn(acc, x);
+    }
+  }
+  return acc;
+}
+
+// ---------------------------------------------------- fused bf16 kernel
+struct FusedSmem {
+  uint64_t full[kFusedStages];
+  uint64_t done[kFusedStages];
+  double lse[kFusedStages];
+  double coeff_s;
+  double redd[kFusedComputeWarps];
+  float redf[kFusedComputeWarps];
+  int32_t tgt[kFusedStages];
+};
+
+__device__ __forceinline__ void spin_until_ready(const uint32_t* cnt, uint32_t target,
+                                                 uint32_t* err) {
+  if (ld_acquire_gpu(cnt) == target) return;
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t ns = 32;
+  while (ld_acquire_gpu(cnt) != target) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+    if (globaltimer_ns() - t0 > kSpinTimeoutNs) {
+      atomicOr(err, kErrTimeout);
+      return;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kFusedThreads, 1)
+    tok_fused_bf16_kernel(TokParams p, uint32_t stage_bytes, int write_dl) {
+  extern __shared__ __align__(128) uint8_t dyn_smem[];
+  FusedSmem& S = *reinterpret_cast<FusedSmem*>(dyn_smem);
+  uint8_t* bufs = dyn_smem + ((sizeof(FusedSmem) + 127) / 128) * 128;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int64_t V = p.V;
+  const uint32_t row_bytes = static_cast<uint32_t>(V * 2);
+  const int64_t G = gridDim.x;
+  const int64_t nloc = (p.R > blockIdx.x) ? (p.R - blockIdx.x + G - 1) / G : 0;
+  auto row_of = [&](int64_t k) { return blockIdx.x + k * G; };
+  auto buf = [&](int s) { return bufs + static_cast<size_t>(s) * stage_bytes; };
+
+  if (tid == 0) {
+    for (int s = 0; s < kFusedStages; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.done[s], kFusedComputeWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const __nv_bfloat16* logits = static_cast<const __nv_bfloat16*>(p.logits);
+  __nv_bfloat16* dl = static_cast<__nv_bfloat16*>(p.dlogits);
+
+  // ------------------------------------------------------- producer warp
+  if (warp == kFusedComputeWarps) {
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();
+      const int64_t pro = nloc < kFusedStages ? nloc : kFusedStages;
+      for (int64_t k = 0; k < pro; ++k) {
+        mbar_arrive_expect_tx(&S.full[k], row_bytes);
+        tma_load_1d_evict_first(buf(k), logits + row_of(k) * V, row_bytes, &S.full[k], pol);
+      }
+      for (int64_t k = 0; k < nloc; ++k) {
+        const int s = static_cast<int>(k % kFusedStages);
+        const uint32_t ph = static_cast<uint32_t>((k / kFusedStages) & 1);
+        mbar_wait(&S.done[s], ph);
+        if (write_dl) {
+          tma_store_1d_evict_first(dl + row_of(k) * V, buf(s), row_bytes, pol);
+          bulk_commit();
+        }
+        if (k + kFusedStages < nloc) {
+          if (write_dl) bulk_wait_read<0>();
+          mbar_arrive_expect_tx(&S.full[s], row_bytes);
+          tma_load_1d_evict_first(buf(s), logits + row_of(k + kFusedStages) * V, row_bytes,
+                                  &S.full[s], pol);
+        }
+      }
+      if (write_dl) bulk_wait<0>();
+    }
+    return;
+  }
+
+  // ------------------------------------------------------- compute warps
+  const int nvec = static_cast<int>(V >> 3);  // uint4 = 8 bf16
+  const int64_t T = p.T;
+
+  // phase A: row statistics, lp_tok, chunk completion
+  auto phaseA = [&](int64_t k) {
+    const int s = static_cast<int>(k % kFusedStages);
+    const uint32_t ph = static_cast<uint32_t>((k / kFusedStages) & 1);
+    const int64_t r = row_of(k);
+    mbar_wait(&S.full[s], ph);
+    const uint4* v = reinterpret_cast<const uint4*>(buf(s));
+    uint32_t mx0 = 0xff80ff80u, mx1 = 0xff80ff80u;
+    for (int i = tid; i < nvec; i += kFusedComputeThreads) {
+      uint4 x = v[i];
+      mx0 = bf16x2_max(mx0, bf16x2_max(x.x, x.y));
+      mx1 = bf16x2_max(mx1, bf16x2_max(x.z, x.w));
+    }
+    uint32_t mx = bf16x2_max(mx0, mx1);
+    float m = fmaxf(bf16lo(mx), bf16hi(mx));
+    m = warp_max_f32(m);
+    if (lane == 0) S.redf[warp] = m;
+    named_bar_sync(1, kFusedComputeThreads);
+    m = S.redf[0];
+#pragma unroll
+    for (int w = 1; w < kFusedComputeWarps; ++w) m = fmaxf(m, S.redf[w]);
+    const float mL = m * kLog2e;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    for (int i = tid; i < nvec; i += kFusedComputeThreads) {
+      uint4 x = v[i];
+      s0 += ex2f(fmaf(bf16lo(x.x), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.x), kLog2e, -mL));
+      s1 += ex2f(fmaf(bf16lo(x.y), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.y), kLog2e, -mL));
+      s2 += ex2f(fmaf(bf16lo(x.z), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.z), kLog2e, -mL));
+      s3 += ex2f(fmaf(bf16lo(x.w), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.w), kLog2e, -mL));
+    }
+    double part = (static_cast<double>(s0) + static_cast<double>(s1)) +
+                  (static_cast<double>(s2) + static_cast<double>(s3));
+    part = warp_sum_f64(part);
+    if (lane == 0) S.redd[warp] = part;
+    named_bar_sync(1, kFusedComputeThreads);
+    if (warp == 0) {
+      uint32_t old = 0;
+      if (lane == 0) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < kFusedComputeWarps; ++w) sum += S.redd[w];
+        const double lse = static_cast<double>(m) + log(sum);
+        int32_t tgt = p.tokens[r];
+        double xt;
+        if (tgt < 0 || tgt >= V) {
+          atomicOr(p.err, kErrToken);
+          xt = __longlong_as_double(0x7ff8000000000000ll);  // NaN -> abort
+          tgt = -1;
+        } else {
+          xt = static_cast<double>(__bfloat162float(
+              reinterpret_cast<const __nv_bfloat16*>(buf(s))[tgt]));
+        }
+        S.lse[s] = lse;
+        S.tgt[s] = tgt;
+        p.lp_tok[r] = xt - lse;
+        if (write_dl) old = atom_add_acq_rel_gpu(p.cnt + r / T, 1u);
+      }
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if (write_dl && old == static_cast<uint32_t>(T - 1)) {
+        // last row of this chunk: the chunk coefficient (grpo.py:252-268)
+        const int64_t q = r / T;
+        const double lp = warp_chunk_lp(p.lp_tok + q * T, T, lane);
+        if (lane == 0) {
+          ChunkTerms ct = chunk_terms(lp, static_cast<double>(p.blp[q]), p.adv[q / p.C], p.w,
+                                      p.clip_eps, p.kl_coeff);
+          p.lp_chunk[q] = lp;
+          p.coeff[q] = ct.coeff;
+          red_release_gpu_add(p.cnt + q, 1u);  // T + 1 == coefficient ready
+        }
+      }
+    }
+  };
+
+  // phase B: dlogits of row k, in place in SMEM, then hand to the producer
+  auto phaseB = [&](int64_t k) {
+    const int s = static_cast<int>(k % kFusedStages);
+    const int64_t r = row_of(k);
+    const int64_t q = r / T;
+    if (tid == 0) {
+      spin_until_ready(p.cnt + q, static_cast<uint32_t>(T + 1), p.err);
+      S.coeff_s = __ldcg(p.coeff + q);
+    }
+    named_bar_sync(1, kFusedComputeThreads);
+    const double c = S.coeff_s;
+    const double lse = S.lse[s];
+    const int32_t tgt = S.tgt[s];
+    uint4* v = reinterpret_cast<uint4*>(buf(s));
+    if (c == 0.0 || !isfinite(c)) {
+      // zero gradient rows (A == 0 or clipped chunks): 0 * (onehot - p)
+      const uint32_t z = (c == 0.0) ? 0u : 0x7fc07fc0u;
+      for (int i = tid; i < nvec; i += kFusedComputeThreads) v[i] = make_uint4(z, z, z, z);
+    } else {
+      // -c * p_v = -sign(c) * 2^(x*log2e - (lse*log2e - log2|c|))
+      const float K = static_cast<float>(lse * 1.4426950408889634 - log2(fabs(c)));
+      const uint32_t sgn = (c > 0.0) ? 0x80008000u : 0u;
+      const int tv = tgt >> 3;
+      for (int i = tid; i < nvec; i += kFusedComputeThreads) {
+        uint4 x = v[i];
+        uint4 o;
+        o.x = pack_bf16x2(ex2f(fmaf(bf16lo(x.x), kLog2e, -K)), ex2f(fmaf(bf16hi(x.x), kLog2e, -K))) ^ sgn;
+        o.y = pack_bf16x2(ex2f(fmaf(bf16lo(x.y), kLog2e, -K)), ex2f(fmaf(bf16hi(x.y), kLog2e, -K))) ^ sgn;
+        o.z = pack_bf16x2(ex2f(fmaf(bf16lo(x.z), kLog2e, -K)), ex2f(fmaf(bf16hi(x.z), kLog2e, -K))) ^ sgn;
+        o.w = pack_bf16x2(ex2f(fmaf(bf16lo(x.w), kLog2e, -K)), ex2f(fmaf(bf16hi(x.w), kLog2e, -K))) ^ sgn;
+        if (i == tv) {
+          // target column: c * (1 - p_t)
+          const int e = tgt & 7;
+          const uint32_t word = (&x.x)[e >> 1];
+          const float xt = (e & 1) ? bf16hi(word) : bf16lo(word);
+          const float pt = ex2f(fmaf(xt, kLog2e, -static_cast<float>(lse * 1.4426950408889634)));
+          const float val = static_cast<float>(c) * (1.0f - pt);
+          const uint32_t b = pack_bf16x2(val, val) & 0xffffu;
+          uint32_t& ow = (&o.x)[e >> 1];
+          ow = (e & 1) ? ((ow & 0x0000ffffu) | (b << 16)) : ((ow & 0xffff0000u) | b);
+        }
+        v[i] = o;
+      }
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.done[s]);
+  };
+
+  if (!write_dl) {
+    for (int64_t k = 0; k < nloc; ++k) {
+      phaseA(k);
+      named_bar_sync(1, kFusedComputeThreads);  // everyone done reading buf
+      if (lane == 0) mbar_arrive(&S.done[k % kFusedStages]);
+    }
+    return;
+  }
+  if (nloc > 0) phaseA(0);
+  for (int64_t k = 0; k < nloc; ++k) {
+    if (k + 1 < nloc) phaseA(k + 1);
+    phaseB(k);
+  }
+}
+
+// ------------------------------------------------------ unfused kernels
+template <class T>
+struct Elem;
+template <>
+struct Elem<float> {
+  static constexpr int kVec = 4;
+  __device__ static float get(const float* p, int64_t i) { return p[i]; }
+};
+template <>
+struct Elem<__nv_bfloat16> {
+  static constexpr int kVec = 8;
+  __device__ static float get(const __nv_bfloat16* p, int64_t i) { return __bfloat162float(p[i]); }
+};
+
+__device__ __forceinline__ void unpack_vec(const uint4& u, float* f, float) {
+  f[0] = __uint_as_float(u.x);
+  f[1] = __uint_as_float(u.y);
+  f[2] = __uint_as_float(u.z);
+  f[3] = __uint_as_float(u.w);
+}
+__device__ __forceinline__ void unpack_vec(const uint4& u, float* f, __nv_bfloat16) {
+  f[0] = bf16lo(u.x); f[1] = bf16hi(u.x);
+  f[2] = bf16lo(u.y); f[3] = bf16hi(u.y);
+  f[4] = bf16lo(u.z); f[5] = bf16hi(u.z);
+  f[6] = bf16lo(u.w); f[7] = bf16hi(u.w);
+}
+__device__ __forceinline__ uint4 pack_vec(const float* f, float) {
+  return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
+                    __float_as_uint(f[3]));
+}
+__device__ __forceinline__ uint4 pack_vec(const float* f, __nv_bfloat16) {
+  return make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                    pack_bf16x2(f[6], f[7]));
+}
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+__device__ __forceinline__ void from_f(float v, float* d) { *d = v; }
+__device__ __forceinline__ void from_f(float v, __nv_bfloat16* d) { *d = __float2bfloat16_rn(v); }
+
+constexpr int kRowThreads = 256;
+
+// online (max, sum-exp) with per-vector rescale; one CTA per row
+template <class T>
+__global__ void __launch_bounds__(kRowThreads) tok_rows_kernel(TokParams p, int vec_ok) {
+  const int64_t r = blockIdx.x;
+  const int64_t V = p.V;
+  const T* row = static_cast<const T*>(p.logits) + r * V;
+  const int tid = threadIdx.x;
+  float m = -INFINITY, s = 0.f;
+  auto add = [&](const float* f, int n) {
+    float vm = f[0];
+    for (int e = 1; e < n; ++e) vm = fmaxf(vm, f[e]);
+    if (vm > m) {
+      s = (m == -INFINITY) ? 0.f : s * ex2f((m - vm) * kLog2e);
+      m = vm;
+    }
+    if (m == -INFINITY) return;
+    const float mL = m * kLog2e;
+    for (int e = 0; e < n; ++e) s += ex2f(fmaf(f[e], kLog2e, -mL));
+  };
+  constexpr int E = Elem<T>::kVec;
+  if (vec_ok) {
+    const uint4* v = reinterpret_cast<const uint4*>(row);
+    const int64_t nvec = V / E;
+    for (int64_t i = tid; i < nvec; i += kRowThreads) {
+      float f[E];
+      unpack_vec(__ldcs(v + i), f, T());
+      add(f, E);
+    }
+    for (int64_t i = nvec * E + tid; i < V; i += kRowThreads) {
+      float f = to_f(row[i]);
+      add(&f, 1);
+    }
+  } else {
+    for (int64_t i = tid; i < V; i += kRowThreads) {
+      float f = to_f(row[i]);
+      add(&f, 1);
+    }
+  }
+  __shared__ float sm[kRowThreads / 32];
+  __shared__ double ss[kRowThreads / 32];
+  const int warp = tid >> 5, lane = tid & 31;
+  float M = warp_max_f32(m);
+  if (lane == 0) sm[warp] = M;
+  __syncthreads();
+  M = sm[0];
+  for (int w = 1; w < kRowThreads / 32; ++w) M = fmaxf(M, sm[w]);
+  double part = (m == -INFINITY) ? 0.0 : static_cast<double>(s) * exp2(static_cast<double>((m - M) * kLog2e));
+  part = warp_sum_f64(part);
+  if (lane == 0) ss[warp] = part;
+  __syncthreads();
+  if (tid == 0) {
+    double sum = 0.0;
+    for (int w = 0; w < kRowThreads / 32; ++w) sum += ss[w];
+    const double lse = static_cast<double>(M) + log(sum);
+    const int32_t tgt = p.tokens[r];
+    double xt;
+    if (tgt < 0 || tgt >= V) {
+      atomicOr(p.err, kErrToken);
+      xt = __longlong_as_double(0x7ff8000000000000ll);
+    } else {
+      xt = static_cast<double>(to_f(row[tgt]));
+    }
+    p.lse[r] = lse;
+    p.lp_tok[r] = xt - lse;
+  }
+}
+
+__global__ void tok_chunk_kernel(TokParams p) {
+  const int64_t warps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < p.n_chunks;
+       q += warps) {
+    const double lp = warp_chunk_lp(p.lp_tok + q * p.T, p.T, lane);
+    if (lane == 0) {
+      ChunkTerms ct = chunk_terms(lp, static_cast<double>(p.blp[q]), p.adv[q / p.C], p.w,
+                                  p.clip_eps, p.kl_coeff);
+      p.lp_chunk[q] = lp;
+      p.coeff[q] = ct.coeff;
+    }
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kRowThreads) tok_bwd_kernel(TokParams p, int vec_ok) {
+  const int64_t r = blockIdx.x;
+  const int64_t V = p.V;
+  const T* row = static_cast<const T*>(p.logits) + r * V;
+  T* out = static_cast<T*>(p.dlogits) + r * V;
+  const double c = p.coeff[r / p.T];
+  const double lse = p.lse[r];
+  const int32_t tgt = p.tokens[r];
+  const int tid = threadIdx.x;
+  constexpr int E = Elem<T>::kVec;
+  const float cf = static_cast<float>(c);
+  const float lseL = static_cast<float>(lse * 1.4426950408889634);
+  auto val = [&](float x, int64_t col) {
+    const float pv = ex2f(fmaf(x, kLog2e, -lseL));
+    return (col == tgt) ? cf * (1.0f - pv) : -cf * pv;
+  };
+  if (vec_ok) {
+    const uint4* v = reinterpret_cast<const uint4*>(row);
+    uint4* o = reinterpret_cast<uint4*>(out);
+    const int64_t nvec = V / E;
+    for (int64_t i = tid; i < nvec; i += kRowThreads) {
+      float f[E];
+      unpack_vec(__ldcs(v + i), f, T());
+#pragma unroll
+      for (int e = 0; e < E; ++e) f[e] = val(f[e], i * E + e);
+      __stcs(o + i, pack_vec(f, T()));
+    }
+    for (int64_t i = nvec * E + tid; i < V; i += kRowThreads) from_f(val(to_f(row[i]), i), out + i);
+  } else {
+    for (int64_t i = tid; i < V; i += kRowThreads) from_f(val(to_f(row[i]), i), out + i);
+  }
+}
+
+// ------------------------------------------------------------- epilogue
+struct EpiParams {
+  const double* lp_chunk;   // [n_traj*C] input order
+  const float* blp;         // [n_traj*C]
+  const double* blp64;      // optional f64 behaviour log-probs (overrides blp)
+  const double* adv;        // [n_traj]
+  const uint32_t* reward_bad;  // [n_groups] or null
+  const int64_t* order;     // [n_groups] canonical order (null = identity)
+  const int64_t* group_ids; // [n_groups] (null = position)
+  double* coeff_out;        // [n_traj*C] or null
+  double* stats;            // [DVLA_ST_LEN]
+  const uint32_t* kerr;     // kernel error word or null
+  int64_t n_groups, G, C;
+  double w, clip_eps, kl_coeff;
+};
+
+constexpr int kEpiThreads = 512;
+
+__global__ void __launch_bounds__(kEpiThreads) grpo_epilogue_kernel(EpiParams e) {
+  __shared__ double s_loss[kEpiThreads], s_rho[kEpiThreads];
+  __shared__ unsigned char s_clip[kEpiThreads];
+  __shared__ unsigned long long s_first_reward, s_first_traj;
+  const int tid = threadIdx.x;
+  const int64_t GC = e.G * e.C;
+  const int64_t n_entries = e.n_groups * GC;
+  auto gin = [&](int64_t k) { return e.order ? e.order[k] : k; };
+  auto gid = [&](int64_t g) { return e.group_ids ? e.group_ids[g] : g; };
+  if (tid == 0) {
+    s_first_reward = ~0ull;
+    s_first_traj = ~0ull;
+  }
+  __syncthreads();
+  if (e.reward_bad) {
+    for (int64_t k = tid; k < e.n_groups; k += kEpiThreads)
+      if (e.reward_bad[gin(k)]) atomicMin(&s_first_reward, (unsigned long long)k);
+  }
+  double loss = 0.0, ratio_sum = 0.0, clip_count = 0.0;
+  for (int64_t base = 0; base < n_entries; base += kEpiThreads) {
+    const int64_t idx = base + tid;
+    if (idx < n_entries) {
+      const int64_t k = idx / GC, rem = idx % GC;
+      const int64_t i = rem / e.C, c = rem % e.C;
+      const int64_t j = gin(k) * e.G + i;  // input-order trajectory
+      const int64_t q = j * e.C + c;
+      const double lp = e.lp_chunk[q];
+      const double blp = e.blp64 ? e.blp64[q] : static_cast<double>(e.blp[q]);
+      ChunkTerms ct = chunk_terms(lp, blp, e.adv[j], e.w, e.clip_eps, e.kl_coeff);
+      if (e.coeff_out) e.coeff_out[q] = ct.coeff;
+      s_loss[tid] = ct.loss;
+      s_rho[tid] = ct.rho;
+      s_clip[tid] = ct.clipped;
+      if (!isfinite(lp) || !isfinite(ct.rho))
+        atomicMin(&s_first_traj, (unsigned long long)(idx / e.C));
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const int64_t lim = (n_entries - base < kEpiThreads) ? n_entries - base : kEpiThreads;
+      for (int64_t t = 0; t < lim; ++t) {
+        loss = __dadd_rn(loss, s_loss[t]);
+        ratio_sum = __dadd_rn(ratio_sum, s_rho[t]);
+        clip_count += s_clip[t];
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    double code = 0.0, group = 0.0;
+    if (s_first_reward != ~0ull) {
+      code = 1.0;
+      group = static_cast<double>(gid(gin(static_cast<int64_t>(s_first_reward))));
+    } else if (s_first_traj != ~0ull) {
+      const int64_t ct = static_cast<int64_t>(s_first_traj);  // canonical traj index
+      const int64_t k = ct / e.G, i = ct % e.G;
+      const int64_t j = gin(k) * e.G + i;
+      bool lp_bad = false;
+      for (int64_t c = 0; c < e.C; ++c) lp_bad |= !isfinite(e.lp_chunk[j * e.C + c]);
+      code = lp_bad ? 2.0 : 3.0;
+      group = static_cast<double>(gid(gin(k)));
+    } else if (!isfinite(loss)) {
+      code = 4.0;
+      group = static_cast<double>(gid(gin(0)));
+    }
+    e.stats[DVLA_ST_LOSS] = loss;
+    e.stats[DVLA_ST_RATIO_SUM] = ratio_sum;
+    e.stats[DVLA_ST_CLIP_COUNT] = clip_count;
+    e.stats[DVLA_ST_CHUNK_COUNT] = static_cast<double>(n_entries);
+    e.stats[DVLA_ST_ABORT] = code;
+    e.stats[DVLA_ST_ABORT_GROUP] = group;
+    e.stats[DVLA_ST_KERNEL_ERR] = e.kerr ? static_cast<double>(*e.kerr) : 0.0;
+    e.stats[DVLA_ST_RESERVED] = 0.0;
+  }
+}
+
+// ------------------------------------------------------------ workspace
+struct TokWorkspace {
+  double* adv;
+  double* lp_tok;
+  double* lse;
+  double* coeff;
+  uint32_t* cnt;
+  uint32_t* reward_bad;
+  uint32_t* err;
+  size_t bytes;
+  size_t zero_off, zero_bytes;  // region memset every call (cnt, err)
+};
+
+static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static TokWorkspace carve(void* base, int64_t n_groups, int64_t G, int64_t C, int64_t T) {
+  const int64_t n_traj = n_groups * G, nq = n_traj * C, R = nq * T;
+  TokWorkspace w{};
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    size_t o = off;
+    off += al256(b);
+    return static_cast<uint8_t*>(base) + o;
+  };
+  w.adv = reinterpret_cast<double*>(take(n_traj * 8));
+  w.lp_tok = reinterpret_cast<double*>(take(R * 8));
+  w.lse = reinterpret_cast<double*>(take(R * 8));
+  w.coeff = reinterpret_cast<double*>(take(nq * 8));
+  w.reward_bad = reinterpret_cast<uint32_t*>(take(n_groups * 4));
+  w.zero_off = off;
+  w.cnt = reinterpret_cast<uint32_t*>(take(nq * 4));
+  w.err = reinterpret_cast<uint32_t*>(take(16));
+  w.zero_bytes = off - w.zero_off;
+  w.bytes = off;
+  return w;
+}
+
+static size_t fused_smem_bytes(int64_t V) {
+  const size_t hdr = ((sizeof(FusedSmem) + 127) / 128) * 128;
+  const size_t stage = ((static_cast<size_t>(V) * 2 + 127) / 128) * 128;
+  return hdr + kFusedStages * stage;
+}
+
+}  // namespace dvla
+
+using namespace dvla;
+
+extern "C" size_t dvla_token_loss_workspace_bytes(int64_t n_groups, int64_t G, int64_t C,
+                                                  int64_t T) {
+  if (n_groups < 0 || G < 0 || C < 0 || T < 0) return 0;
+  return carve(nullptr, n_groups, G, C, T).bytes;
+}
+
+extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int32_t* tokens,
+                                       const float* blp, const float* rewards,
+                                       const int64_t* group_order, const int64_t* group_ids,
+                                       int64_t n_groups, int64_t G, int64_t C, int64_t T,
+                                       int64_t V, double clip_eps, double adv_eps,
+                                       double kl_coeff, int flags, void* dlogits,
+                                       double* lp_chunk, double* stats, void* workspace,
+                                       size_t workspace_bytes, void* stream_) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (n_groups < 1) return fail(DVLA_ERR_CONFIG, "grpo update needs at least one group");
+  if (G < 2) return fail(DVLA_ERR_CONFIG, "group_size must be >= 2, got %lld", (long long)G);
+  if (C < 1 || T < 1 || V < 1)
+    return fail(DVLA_ERR_USAGE, "C, T, V must be >= 1 (got %lld, %lld, %lld)", (long long)C,
+                (long long)T, (long long)V);
+  if (dtype != DVLA_F32 && dtype != DVLA_BF16)
+    return fail(DVLA_ERR_USAGE, "dtype must be DVLA_F32 or DVLA_BF16");
+  if (!logits || !tokens || !blp || !rewards || !lp_chunk || !stats || !workspace)
+    return fail(DVLA_ERR_USAGE, "null pointer argument");
+  const bool want_dl = (flags & DVLA_TL_WRITE_DLOGITS) != 0;
+  if (want_dl && !dlogits) return fail(DVLA_ERR_USAGE, "dlogits requested but null");
+  TokWorkspace ws = carve(workspace, n_groups, G, C, T);
+  if (workspace_bytes < ws.bytes)
+    return fail(DVLA_ERR_USAGE, "workspace too small: %zu < %zu", workspace_bytes, ws.bytes);
+
+  const int64_t n_traj = n_groups * G, nq = n_traj * C, R = nq * T;
+  TokParams p{};
+  p.logits = logits;
+  p.tokens = tokens;
+  p.blp = blp;
+  p.adv = ws.adv;
+  p.dlogits = dlogits;
+  p.lp_tok = ws.lp_tok;
+  p.lse = ws.lse;
+  p.lp_chunk = lp_chunk;
+  p.coeff = ws.coeff;
+  p.cnt = ws.cnt;
+  p.err = ws.err;
+  p.R = R;
+  p.V = V;
+  p.T = T;
+  p.C = C;
+  p.n_chunks = nq;
+  p.w = 1.0 / static_cast<double>(n_traj * C);
+  p.clip_eps = clip_eps;
+  p.kl_coeff = kl_coeff;
+
+  DVLA_CUDA_TRY(cudaMemsetAsync(static_cast<uint8_t*>(workspace) + ws.zero_off, 0,
+                                ws.zero_bytes, stream));
+  {
+    const int thr = 128;
+    tok_adv_kernel<<<(unsigned)((n_groups + thr - 1) / thr), thr, 0, stream>>>(
+        rewards, n_groups, G, adv_eps, ws.adv, ws.reward_bad);
+    if (int rc = launch_check("tok_adv_kernel")) return rc;
+  }
+
+  const int dev = current_device();
+  const int sms = num_sms(dev);
+  const size_t esz = dtype == DVLA_BF16 ? 2 : 4;
+  const bool aligned16 = (reinterpret_cast<uintptr_t>(logits) % 16 == 0) &&
+                         (!want_dl || reinterpret_cast<uintptr_t>(dlogits) % 16 == 0) &&
+                         ((V * esz) % 16 == 0);
+  const size_t fsmem = fused_smem_bytes(V);
+  const bool fused = !(flags & DVLA_TL_UNFUSED) && dtype == DVLA_BF16 && aligned16 &&
+                     fsmem <= 227 * 1024 && T <= sms && R >= 1;
+  if (fused) {
+    static bool attr_set[64] = {false};
+    if (!attr_set[dev & 63]) {
+      DVLA_CUDA_TRY(cudaFuncSetAttribute(tok_fused_bf16_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024));
+      attr_set[dev & 63] = true;
+    }
+    const unsigned grid = static_cast<unsigned>(R < sms ? R : sms);
+    const uint32_t stage_bytes = static_cast<uint32_t>(((V * 2 + 127) / 128) * 128);
+    cudaEvent_t stop;
+    prof_begin(stream, &stop);
+    tok_fused_bf16_kernel<<<grid, kFusedThreads, fsmem, stream>>>(p, stage_bytes, want_dl ? 1 : 0);
+    prof_end(stream, stop);
+    if (int rc = launch_check("tok_fused_bf16_kernel")) return rc;
+    if (!want_dl) {
+      tok_chunk_kernel<<<(unsigned)((nq * 32 + 255) / 256), 256, 0, stream>>>(p);
+      if (int rc = launch_check("tok_chunk_kernel")) return rc;
+    }
+  } else {
+    const int vec_ok = aligned16 ? 1 : 0;
+    cudaEvent_t stop;
+    prof_begin(stream, &stop);
+    if (dtype == DVLA_BF16)
+      tok_rows_kernel<__nv_bfloat16><<<(unsigned)R, kRowThreads, 0, stream>>>(p, vec_ok);
+    else
+      tok_rows_kernel<float><<<(unsigned)R, kRowThreads, 0, stream>>>(p, vec_ok);
+    if (int rc = launch_check("tok_rows_kernel")) return rc;
+    tok_chunk_kernel<<<(unsigned)((nq * 32 + 255) / 256), 256, 0, stream>>>(p);
+    if (int rc = launch_check("tok_chunk_kernel")) return rc;
+    if (want_dl) {
+      if (dtype == DVLA_BF16)
+        tok_bwd_kernel<__nv_bfloat16><<<(unsigned)R, kRowThreads, 0, stream>>>(p, vec_ok);
+      else
+        tok_bwd_kernel<float><<<(unsigned)R, kRowThreads, 0, stream>>>(p, vec_ok);
+      if (int rc = launch_check("tok_bwd_kernel")) return rc;
+    }
+    prof_end(stream, stop);
+  }
+
+  EpiParams e{};
+  e.lp_chunk = lp_chunk;
+  e.blp = blp;
+  e.adv = ws.adv;
+  e.reward_bad = ws.reward_bad;
+  e.order = group_order;
+  e.group_ids = group_ids;
+  e.stats = stats;
+  e.kerr = ws.err;
+  e.n_groups = n_groups;
+  e.G = G;
+  e.C = C;
+  e.w = p.w;
+  e.clip_eps = clip_eps;
+  e.kl_coeff = kl_coeff;
+  grpo_epilogue_kernel<<<1, kEpiThreads, 0, stream>>>(e);
+  return launch_check("grpo_epilogue_kernel");
+}
+
+extern "C" int dvla_advantages(const double* rewards, int64_t n_groups, int64_t G, double delta,
+                               double* out, void* stream) {
+  if (G < 2) return fail(DVLA_ERR_CONFIG, "a reward group needs >= 2 entries, got shape (%lld,)",
+                         (long long)G);
+  if (n_groups < 1) return DVLA_OK;
+  if (!rewards || !out) return fail(DVLA_ERR_USAGE, "null pointer argument");
+  const int thr = 128;
+  adv_f64_kernel<<<(unsigned)((n_groups + thr - 1) / thr), thr, 0,
+                   static_cast<cudaStream_t>(stream)>>>(rewards, n_groups, G, delta, out);
+  return launch_check("adv_f64_kernel");
+}
+
+extern "C" int dvla_group_advantages(const float* rewards, int64_t n_groups, int64_t G,
+                                     double delta, double* adv, uint32_t* reward_bad,
+                                     void* stream) {
+  if (G < 2) return fail(DVLA_ERR_CONFIG, "a reward group needs >= 2 entries, got shape (%lld,)",
+                         (long long)G);
+  if (n_groups < 1) return DVLA_OK;
+  if (!rewards || !adv || !reward_bad) return fail(DVLA_ERR_USAGE, "null pointer argument");
+  const int thr = 128;
+  tok_adv_kernel<<<(unsigned)((n_groups + thr - 1) / thr), thr, 0,
+                   static_cast<cudaStream_t>(stream)>>>(rewards, n_groups, G, delta, adv,
+                                                        reward_bad);
+  return launch_check("tok_adv_kernel");
+}
+
+extern "C" int dvla_grpo_epilogue(const double* lp_chunk, const float* blp, const double* blp64,
+                                  const double* adv, const uint32_t* reward_bad,
+                                  const int64_t* group_order,
+                                  const int64_t* group_ids, int64_t n_groups, int64_t G,
+                                  int64_t C, double clip_eps, double kl_coeff, double* coeff_out,
+                                  double* stats, void* stream) {
+  if (n_groups < 1) return fail(DVLA_ERR_CONFIG, "grpo update needs at least one group");
+  if (!lp_chunk || (!blp && !blp64) || !adv || !stats)
+    return fail(DVLA_ERR_USAGE, "null pointer argument");
+  EpiParams e{};
+  e.lp_chunk = lp_chunk;
+  e.blp = blp;
+  e.blp64 = blp64;
+  e.adv = adv;
+  e.reward_bad = reward_bad;
+  e.order = group_order;
+  e.group_ids = group_ids;
+  e.coeff_out = coeff_out;
+  e.stats = stats;
+  e.n_groups = n_groups;
+  e.G = G;
+  e.C = C;
+  e.w = 1.0 / static_cast<double>(n_groups * G * C);
+  e.clip_eps = clip_eps;
+  e.kl_coeff = kl_coeff;
+  grpo_epilogue_kernel<<<1, kEpiThreads, 0, static_cast<cudaStream_t>(stream)>>>(e);
+  return launch_check("grpo_epilogue_kernel");
+}

@@ -1,0 +1,372 @@
+"""Group-relative policy optimisation on B200: the learner's hot path.
+
+Same public API as reference pkg/src/dvla/grpo.py (GrpoConfig :23-52,
+GroupBatch :55-78, GrpoAbort :81-86, compute_advantages :89-99,
+group_advantages :102-108, clipped_surrogate :111-119, AdamState :122-134,
+adam_step :137-150, UpdateStats :153-174, grpo_loss :194-214, grpo_grad
+:217-294, clip_grad_norm :297-301, grpo_update :304-320), with every
+array-sized computation done by sm_100a kernels through the C-ABI.
+
+Two policy heads share one learner epilogue (csrc/grpo_math.cuh):
+  * the action-token head (the north-star path): `grpo_token_grad` /
+    `TokenLoss` -- fused log-softmax gather + clipped surrogate + dlogits
+    over logits [rows, V] in one pass (csrc/token_loss.cu);
+  * the reference's Gaussian tanh-MLP chunk policy: `grpo_grad` on
+    PolicyParams, bit-for-bit the reference's arithmetic contract
+    (csrc/gauss.cu).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .core import ConfigError, UsageError
+
+VALID_RATIO_GRANULARITY = ("chunk",)
+
+
+@dataclass(frozen=True)
+class GrpoConfig:
+    group_size: int = 8
+    clip_eps: float = 0.2
+    adv_epsilon: float = 1e-8
+    micro_batch: int = 8
+    lr: float = 3e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    opt_eps: float = 1e-8
+    max_grad_norm: float | None = None
+    kl_coeff: float = 0.0
+    ratio_granularity: str = "chunk"
+
+    def validate(self):
+        if self.group_size < 2:
+            raise ConfigError(f"group_size must be >= 2, got {self.group_size}")
+        if not (0.0 < self.clip_eps < 1.0):
+            raise ConfigError(f"clip_eps must be in (0, 1), got {self.clip_eps}")
+        if self.micro_batch < 1:
+            raise ConfigError("micro_batch must be >= 1")
+        if self.adv_epsilon <= 0:
+            raise ConfigError("adv_epsilon must be > 0")
+        if self.kl_coeff < 0:
+            raise ConfigError("kl_coeff must be >= 0")
+        if self.ratio_granularity not in VALID_RATIO_GRANULARITY:
+            raise ConfigError(
+                "ratio_granularity must be 'chunk'; per-sub-step ratios are "
+                "unrepresentable (one behavior log-prob is stored per chunk)"
+            )
+
+
+@dataclass
+class GroupBatch:
+    """G trajectories sharing one initial condition and one behaviour version.
+
+    obs: (G, C, obs_dim); actions: (G, C, chunk*act_dim);
+    behavior_log_prob: (G, C); rewards: (G,).  Arrays may be numpy (host)
+    or torch tensors (device).  For the action-token head `tokens`
+    (G, C, T) int32 holds the target action-token ids.
+    """
+
+    group_id: int
+    horizon: int
+    chunk: int
+    obs: object
+    actions: object
+    behavior_log_prob: object
+    rewards: object
+    behavior_version: int
+    tokens: object = None
+
+    @property
+    def g(self) -> int:
+        return self.obs.shape[0]
+
+    @property
+    def n_chunks(self) -> int:
+        return self.obs.shape[1]
+
+
+class GrpoAbort(RuntimeError):
+    """Non-finite loss or gradient; carries the offending group id."""
+
+    def __init__(self, group_id: int, detail: str):
+        super().__init__(f"update aborted on group {group_id}: {detail}")
+        self.group_id = group_id
+
+
+ABORT_DETAILS = {
+    1: "non-finite reward",
+    2: "non-finite log-prob",
+    3: "non-finite importance ratio",
+    4: "non-finite loss or gradient",
+}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dev(device=None):
+    torch = _torch()
+    if device is not None:
+        return torch.device(device)
+    if not torch.cuda.is_available():
+        raise RuntimeError("dvla_b200 kernels need a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream_ptr(stream=None):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def compute_advantages(rewards, delta: float):
+    """A_i = (r_i - mean(r)) / (popstd(r) + delta); all-zero when var == 0.
+
+    Computed on the GPU (csrc/grpo_math.cuh group_advantages), bit-identical
+    to reference grpo.py:89-99 including numpy's pairwise mean order.
+    Returns the input's kind: numpy in -> numpy f64 out, tensor -> tensor.
+    """
+    from . import _lib
+    torch = _torch()
+    is_t = isinstance(rewards, torch.Tensor)
+    r = rewards if is_t else np.asarray(rewards, dtype=np.float64)
+    if r.ndim != 1 or r.shape[0] < 2:
+        raise ConfigError(f"a reward group needs >= 2 entries, got shape {tuple(r.shape)}")
+    dev = rewards.device if (is_t and rewards.is_cuda) else _dev()
+    rd = (r if is_t else torch.from_numpy(np.ascontiguousarray(r))).to(
+        device=dev, dtype=torch.float64).contiguous()
+    out = torch.empty_like(rd)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.dvla_advantages(rd.data_ptr(), 1, rd.shape[0], float(delta),
+                                        out.data_ptr(), _stream_ptr()), "dvla_advantages")
+    if is_t:
+        return out if rewards.is_cuda else out.cpu()
+    return out.cpu().numpy()
+
+
+def group_advantages(batch: GroupBatch, cfg: GrpoConfig):
+    if batch.g != cfg.group_size:
+        raise ConfigError(
+            f"group {batch.group_id} has {batch.g} trajectories, "
+            f"expected G={cfg.group_size}"
+        )
+    return compute_advantages(batch.rewards, cfg.adv_epsilon)
+
+
+def clipped_surrogate(ratio: float, adv: float, clip_eps: float):
+    """-min(ratio*A, clip(ratio)*A) and its d/d ratio; ties take the
+    unclipped derivative (reference grpo.py:111-119).  Scalar helper only:
+    the batched path evaluates the same expression on the device
+    (grpo_math.cuh chunk_terms)."""
+    clipped_ratio = min(max(ratio, 1.0 - clip_eps), 1.0 + clip_eps)
+    unclipped = ratio * adv
+    clipped = clipped_ratio * adv
+    if unclipped <= clipped:
+        return -unclipped, -adv
+    return -clipped, 0.0
+
+
+@dataclass
+class UpdateStats:
+    version: int
+    loss: float
+    mean_ratio: float
+    clip_fraction: float
+    grad_norm: float
+    mean_reward: float
+    n_traj: int
+    n_groups: int
+    n_chunks: int
+    quarantined: int = 0
+    group_ids: list = field(default_factory=list)
+
+    def to_dict(self) -> dict:
+        return {
+            "version": self.version, "loss": self.loss,
+            "mean_ratio": self.mean_ratio, "clip_fraction": self.clip_fraction,
+            "grad_norm": self.grad_norm, "mean_reward": self.mean_reward,
+            "n_traj": self.n_traj, "n_groups": self.n_groups,
+            "n_chunks": self.n_chunks, "quarantined": self.quarantined,
+        }
+
+
+def canonical_order(group_ids) -> np.ndarray:
+    """Stable sort by group_id (reference grpo.py:177-178 _ordered)."""
+    ids = np.asarray(group_ids, dtype=np.int64)
+    return np.argsort(ids, kind="stable").astype(np.int64)
+
+
+def _mean_reward(rewards_2d: np.ndarray, order: np.ndarray) -> float:
+    """float(np.mean([b.rewards.mean() for b in batches])) in canonical order
+    (reference grpo.py:291); host f32 arithmetic, bit-identical."""
+    per = [np.asarray(rewards_2d[k], dtype=np.float32).mean() for k in order]
+    return float(np.mean(per))
+
+
+def stats_from_vector(sv: np.ndarray, group_ids: np.ndarray, order: np.ndarray,
+                      n_traj: int, rewards_2d=None) -> dict:
+    """Host view of the device stats vector + the abort contract."""
+    from . import _lib
+    code = int(sv[_lib.ST_ABORT])
+    if int(sv[_lib.ST_KERNEL_ERR]) & 1:
+        raise UsageError("target token id outside [0, V)")
+    if int(sv[_lib.ST_KERNEL_ERR]) & 2:
+        raise _lib.NativeError("fused loss kernel timed out waiting for a chunk")
+    if code:
+        raise GrpoAbort(int(sv[_lib.ST_ABORT_GROUP]), ABORT_DETAILS[code])
+    n_chunks = int(sv[_lib.ST_CHUNK_COUNT])
+    out = {
+        "loss": float(sv[_lib.ST_LOSS]),
+        "mean_ratio": float(sv[_lib.ST_RATIO_SUM]) / max(n_chunks, 1),
+        "clip_fraction": float(sv[_lib.ST_CLIP_COUNT]) / max(n_chunks, 1),
+        "n_traj": int(n_traj),
+        "n_groups": int(len(group_ids)),
+        "n_chunks": n_chunks,
+        "group_ids": [int(group_ids[k]) for k in order],
+    }
+    if rewards_2d is not None:
+        out["mean_reward"] = _mean_reward(rewards_2d, order)
+    return out
+
+
+class TokenLoss:
+    """Reusable launcher for the fused action-token GRPO loss.
+
+    Holds the device workspace, stats vector and canonical group order for
+    one batch shape so the trainer lane (and bench.py) can launch the fused
+    kernel repeatedly without allocations:
+
+        tl = TokenLoss(n_groups, G, C, T, V, cfg, dtype=torch.bfloat16)
+        tl.set_groups(group_ids)                 # host ids -> canonical order
+        tl.launch(logits, tokens, blp, rewards, dlogits)   # async
+        stats = tl.stats(rewards)                # sync + GrpoAbort mapping
+
+    Shapes (device tensors, input group order):
+      logits  [n_groups*G*C*T, V] (bf16 or f32), tokens int32 [rows],
+      blp f32 [n_groups*G*C], rewards f32 [n_groups*G],
+      dlogits same shape/dtype as logits.
+    """
+
+    def __init__(self, n_groups: int, G: int, C: int, T: int, V: int, cfg: GrpoConfig,
+                 dtype=None, device=None, fused: bool = True):
+        from . import _lib
+        torch = _torch()
+        cfg.validate()
+        if n_groups < 1:
+            raise ConfigError("grpo update needs at least one group")
+        if G != cfg.group_size:
+            raise ConfigError(f"group has {G} trajectories, expected G={cfg.group_size}")
+        self.cfg = cfg
+        self.n_groups, self.G, self.C, self.T, self.V = n_groups, G, C, T, V
+        self.dtype = dtype if dtype is not None else torch.bfloat16
+        if self.dtype not in (torch.bfloat16, torch.float32):
+            raise UsageError(f"logits dtype must be bf16 or f32, got {self.dtype}")
+        self.code = _lib.BF16 if self.dtype == torch.bfloat16 else _lib.F32
+        self.device = _dev(device)
+        self.fused = fused
+        self.rows = n_groups * G * C * T
+        nbytes = _lib.dvla_token_loss_workspace_bytes(n_groups, G, C, T)
+        self.workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=self.device)
+        self.lp_chunk = torch.empty(n_groups * G * C, dtype=torch.float64, device=self.device)
+        self.stats_dev = torch.zeros(_lib.ST_LEN, dtype=torch.float64, device=self.device)
+        self.set_groups(np.arange(n_groups, dtype=np.int64))
+
+    def set_groups(self, group_ids):
+        torch = _torch()
+        ids = np.asarray(group_ids, dtype=np.int64)
+        if ids.shape != (self.n_groups,):
+            raise UsageError(f"expected {self.n_groups} group ids, got shape {ids.shape}")
+        self.group_ids = ids
+        self.order = canonical_order(ids)
+        self.order_dev = torch.from_numpy(self.order).to(self.device)
+        self.ids_dev = torch.from_numpy(ids).to(self.device)
+
+    def _check_tensor(self, t, shape, dtype, name):
+        torch = _torch()
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise UsageError(f"{name} must be a CUDA tensor")
+        if t.dtype != dtype:
+            raise UsageError(f"{name} must be {dtype}, got {t.dtype}")
+        if t.numel() != int(np.prod(shape)):
+            raise UsageError(f"{name} has {t.numel()} elements, expected shape {shape}")
+        if not t.is_contiguous():
+            raise UsageError(f"{name} must be contiguous")
+
+    def launch(self, logits, tokens, blp, rewards, dlogits=None, stream=None):
+        """Enqueue the fused forward+backward on `stream` (default: current)."""
+        from . import _lib
+        torch = _torch()
+        R, V = self.rows, self.V
+        self._check_tensor(logits, (R, V), self.dtype, "logits")
+        self._check_tensor(tokens, (R,), torch.int32, "tokens")
+        self._check_tensor(blp, (self.n_groups * self.G * self.C,), torch.float32,
+                           "behavior_log_prob")
+        self._check_tensor(rewards, (self.n_groups * self.G,), torch.float32, "rewards")
+        flags = 0 if self.fused else _lib.TL_UNFUSED
+        dptr = None
+        if dlogits is not None:
+            self._check_tensor(dlogits, (R, V), self.dtype, "dlogits")
+            flags |= _lib.TL_WRITE_DLOGITS
+            dptr = dlogits.data_ptr()
+        c = self.cfg
+        with torch.cuda.device(self.device):
+            st = _lib.dvla_token_loss_fwd_bwd(
+                logits.data_ptr(), self.code, tokens.data_ptr(), blp.data_ptr(),
+                rewards.data_ptr(), self.order_dev.data_ptr(), self.ids_dev.data_ptr(),
+                self.n_groups, self.G, self.C, self.T, V, float(c.clip_eps),
+                float(c.adv_epsilon), float(c.kl_coeff), flags, dptr,
+                self.lp_chunk.data_ptr(), self.stats_dev.data_ptr(),
+                self.workspace.data_ptr(), self.workspace.numel(), _stream_ptr(stream))
+        _lib.check(st, "dvla_token_loss_fwd_bwd")
+
+    def stats(self, rewards=None) -> dict:
+        """Synchronise on the stats vector (64 B D2H) and apply the abort
+        contract (GrpoAbort with the reference's group id and message)."""
+        sv = self.stats_dev.cpu().numpy()
+        r2d = None
+        if rewards is not None:
+            r = rewards.detach().cpu().numpy() if hasattr(rewards, "detach") else np.asarray(rewards)
+            r2d = r.reshape(self.n_groups, self.G)
+        return stats_from_vector(sv, self.group_ids, self.order, self.n_groups * self.G, r2d)
+
+
+def grpo_token_grad(logits, tokens, behavior_log_prob, rewards, group_ids, cfg: GrpoConfig,
+                    dlogits=None, write_dlogits: bool = True, fused: bool = True):
+    """Token-head grpo_grad: (loss, dlogits, stats) for one learner batch.
+
+    logits [n_groups, G, C, T, V] (or [rows, V]) bf16/f32 CUDA tensor in the
+    same group order as `group_ids`; tokens int32 [n_groups, G, C, T];
+    behavior_log_prob f32 [n_groups, G, C]; rewards f32 [n_groups, G].
+    Canonical (sorted-by-group_id) order governs the loss accumulation and
+    the abort group exactly as reference grpo.py:226-294.
+    """
+    torch = _torch()
+    ids = np.asarray(group_ids, dtype=np.int64)
+    n_groups = len(ids)
+    if n_groups == 0:
+        raise ConfigError("grpo update needs at least one group")
+    tok = tokens
+    if tok.dim() != 4:
+        raise UsageError("tokens must be (n_groups, G, C, T)")
+    _, G, C, T = tok.shape
+    if G != cfg.group_size:
+        k = 0
+        raise ConfigError(f"group {int(ids[k])} has {G} trajectories, expected G={cfg.group_size}")
+    V = logits.shape[-1]
+    tl = TokenLoss(n_groups, G, C, T, V, cfg, dtype=logits.dtype, device=logits.device,
+                   fused=fused)
+    tl.set_groups(ids)
+    lg = logits.reshape(-1, V)
+    if write_dlogits and dlogits is None:
+        dlogits = torch.empty_like(lg)
+    tl.launch(lg, tok.reshape(-1).contiguous(), behavior_log_prob.reshape(-1).contiguous(),
+              rewards.reshape(-1).contiguous(),
+              dlogits.reshape(-1, V) if write_dlogits else None)
+    st = tl.stats(rewards)
+    st["lp_chunk"] = tl.lp_chunk.view(n_groups, G, C)
+    return st["loss"], (dlogits if write_dlogits else None), st

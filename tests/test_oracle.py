@@ -1,0 +1,127 @@
+"""Pin the CPU oracle against golden vectors produced by the reference itself
+(tests/golden/make_golden.py).  CPU only."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import grpo_oracle as O
+
+
+def test_oracle_advantages_bitwise_against_reference():
+    g = golden("advantages")
+    offs = g["offsets"]
+    for a, b in zip(offs[:-1], offs[1:]):
+        got = O.compute_advantages(g["rewards"][a:b], float(g["delta"]))
+        assert np.array_equal(got, g["adv"][a:b]), (a, b)
+
+
+def test_oracle_reproduces_nondyadic_constant_quirk():
+    # three identical non-dyadic rewards give A != 0
+    g = golden("advantages")
+    kinds = g["kinds"]
+    idx = int(np.flatnonzero(kinds == 9)[0])
+    a, b = g["offsets"][idx], g["offsets"][idx + 1]
+    adv = g["adv"][a:b]
+    assert np.all(adv != 0.0) and np.all(np.abs(adv) < 1e-4)
+
+
+@pytest.mark.parametrize("ratio,adv,eps,want", [
+    (1.3, 1.0, 0.2, (-1.2, 0.0)),
+    (0.7, -1.0, 0.2, (0.8, 0.0)),
+    (0.95, 2.0, 0.2, (-1.9, -2.0)),
+    (1.0, 1.5, 0.2, (-1.5, -1.5)),
+    (1.0, -1.5, 0.2, (1.5, 1.5)),
+])
+def test_oracle_surrogate_kats(ratio, adv, eps, want):
+    loss, d = O.clipped_surrogate(ratio, adv, eps)
+    assert loss == pytest.approx(want[0]) and d == want[1]
+
+
+def _gauss_case(g, tag):
+    return dict(w1=g[f"{tag}_w1"], b1=g[f"{tag}_b1"], w2=g[f"{tag}_w2"], b2=g[f"{tag}_b2"],
+                log_std=g[f"{tag}_log_std"], group_ids=g[f"{tag}_group_ids"],
+                obs=g[f"{tag}_obs"], actions=g[f"{tag}_actions"], blp=g[f"{tag}_blp"],
+                rewards=g[f"{tag}_rewards"])
+
+
+def test_oracle_grpo_grad_gauss_matches_reference():
+    g = golden("grpo_gauss")
+    tags = sorted({k.rsplit("_", 1)[0] for k in g.files if k.endswith("_loss")})
+    assert len(tags) == 12
+    for tag in tags:
+        case = _gauss_case(g, tag)
+        loss, grad, st = O.grpo_grad_gauss(**case, kl_coeff=float(g[f"{tag}_kl"]))
+        # The reference's default numba backend evaluates float(x) of f32
+        # array elements in f32 (its jitted chunk_log_prob differs from its own
+        # py_func by ~4e-8 rel), its numpy backend in f64; the two agree only
+        # to rtol 1e-6 (reference tests/test_kernels.py:59,79).  The oracle
+        # follows the documented f64 contract, so the pin is that tolerance.
+        assert loss == pytest.approx(float(g[f"{tag}_loss"]), abs=1e-6)
+        ref = g[f"{tag}_grad"]
+        assert np.abs(grad - ref).max() <= 1e-5 * np.abs(ref).max()
+        rs = g[f"{tag}_stats"]
+        assert st["mean_ratio"] == pytest.approx(rs[1], rel=1e-6)
+        assert st["clip_fraction"] == rs[2] and st["n_chunks"] == rs[3]
+
+
+def test_oracle_adam_matches_reference_update():
+    g = golden("grpo_gauss")
+    for seed in range(10):
+        tag = f"s{seed}_kl0"
+        case = _gauss_case(g, tag)
+        _, grad, _ = O.grpo_grad_gauss(**case)
+        flat = np.concatenate([case[k].ravel() for k in ("w1", "b1", "w2", "b2", "log_std")])
+        norm, grad = O.clip_grad_norm(grad, None)
+        assert norm == pytest.approx(float(g[f"{tag}_grad_norm"]), rel=1e-6)
+        new, *_ = O.adam_step(flat, g[f"{tag}_grad"], np.zeros(flat.size), np.zeros(flat.size),
+                              0, 1e-3, 0.9, 0.999, 1e-8)
+        assert np.array_equal(new, g[f"{tag}_updated"])  # bitwise on the reference grad
+
+
+def test_oracle_kernels_match_reference_backend():
+    g = golden("kernels")
+    lp = O.chunk_log_prob(g["means"], g["log_std"], g["actions"])
+    np.testing.assert_allclose(lp, g["lp"], rtol=1e-6)
+    mf = O.mlp_forward(g["w1"], g["b1"], g["w2"], g["b2"], g["obs"])
+    np.testing.assert_allclose(mf, g["mlp_out"], rtol=1e-6, atol=1e-7)
+    out = np.zeros_like(g["backward"])
+    O.policy_backward(g["w1"], g["b1"], g["w2"], g["b2"], g["ls2"], g["obs"], g["act"],
+                      g["coeffs"], out)
+    np.testing.assert_allclose(out, g["backward"], rtol=1e-5, atol=1e-6 * np.abs(out).max())
+
+
+def test_token_oracle_epilogue_equals_gaussian_epilogue():
+    """Cross-check of the unpinned token head: feed the token
+    restatement's epilogue the Gaussian chunk log-probs of a pinned case and
+    require the reference loss/stats."""
+    g = golden("grpo_gauss")
+    tag = "s2_kl0"
+    case = _gauss_case(g, tag)
+    n_groups, G, C = case["blp"].shape
+    lp = np.zeros((n_groups, G, C))
+    for k in range(n_groups):
+        for i in range(G):
+            means = O.mlp_forward(case["w1"], case["b1"], case["w2"], case["b2"], case["obs"][k, i])
+            lp[k, i] = O.chunk_log_prob(means, case["log_std"], case["actions"][k, i])
+    order, entries = O._entries(case["group_ids"], case["rewards"], case["blp"], G, 1e-8)
+    loss, ratio_sum, clip, n, _ = O._epilogue(lambda key: lp[key], entries, n_groups * G, 0.2, 0.0)
+    assert loss == pytest.approx(float(g[f"{tag}_loss"]), abs=1e-6)
+    assert n == int(g[f"{tag}_stats"][3])
+
+
+def test_token_oracle_small_case_properties():
+    rng = np.random.default_rng(0)
+    n_groups, G, C, T, V = 2, 4, 2, 3, 17
+    logits = rng.normal(0, 2, (n_groups, G, C, T, V)).astype(np.float32)
+    tokens = rng.integers(0, V, (n_groups, G, C, T))
+    blp = rng.normal(-8, 1, (n_groups, G, C)).astype(np.float32)
+    rewards = rng.integers(0, 2, (n_groups, G)).astype(np.float32)
+    loss, dl, st = O.grpo_token_grad(logits, tokens, blp, rewards, np.array([5, 2]))
+    assert st["group_ids"] == [2, 5]
+    # each dlogits row sums to zero (softmax Jacobian rows) times coeff
+    np.testing.assert_allclose(dl.sum(axis=-1), 0.0, atol=1e-12)
+    # lp_tok <= 0 and lp_chunk is the sequential sum
+    assert np.all(st["lp_tok"] <= 0)
+    np.testing.assert_allclose(st["lp_chunk"].reshape(-1), st["lp_tok"].reshape(-1, T).sum(1),
+                               rtol=1e-13)

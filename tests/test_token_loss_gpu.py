@@ -1,0 +1,207 @@
+"""GPU parity of the fused action-token GRPO loss (csrc/token_loss.cu) against
+the numpy oracle (oracle/grpo_oracle.py), through the C-ABI.
+
+Tolerances (north star): loss and gradients within 1e-5 relative in fp32,
+1e-2 in bf16; chunk indexing / advantage grouping / canonical order exact.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import grpo_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(seed, n_groups, G, C, T, V, dtype, spread=0.05, binary=True, ids=None):
+    import torch
+    rng = np.random.default_rng(seed)
+    x = rng.normal(0.0, 2.0, (n_groups, G, C, T, V)).astype(np.float32)
+    if dtype == torch.bfloat16:
+        x = torch.from_numpy(x).to(torch.bfloat16).float().numpy()  # exact bf16 values
+    tokens = rng.integers(0, V, (n_groups, G, C, T)).astype(np.int32)
+    # behaviour log-probs near the current policy (ratios inside the clip box)
+    _, _, st0 = O.grpo_token_grad(x, tokens, np.zeros((n_groups, G, C), np.float32),
+                                  np.tile(np.arange(G, dtype=np.float32), (n_groups, 1)),
+                                  np.arange(n_groups), want_dlogits=False)
+    blp = (st0["lp_chunk"] + rng.uniform(-spread, spread, (n_groups, G, C))).astype(np.float32)
+    if binary:
+        rewards = rng.integers(0, 2, (n_groups, G)).astype(np.float32)
+    else:
+        rewards = rng.uniform(0, 1, (n_groups, G)).astype(np.float32)
+    if ids is None:
+        ids = rng.permutation(n_groups * 3)[:n_groups]
+    return x, tokens, blp, rewards, np.asarray(ids)
+
+
+def _run_gpu(x, tokens, blp, rewards, ids, dtype, fused=True, cfg=None):
+    import torch
+    from paper_2605_13276_b200 import grpo
+    cfg = cfg or grpo.GrpoConfig(group_size=x.shape[1])
+    dev = torch.device("cuda", 0)
+    lg = torch.from_numpy(x).to(dev, dtype)
+    loss, dl, st = grpo.grpo_token_grad(
+        lg, torch.from_numpy(tokens).to(dev), torch.from_numpy(blp).to(dev),
+        torch.from_numpy(rewards).to(dev), ids, cfg, fused=fused)
+    torch.cuda.synchronize()
+    return loss, dl.float().cpu().numpy(), st
+
+
+def _check(x, tokens, blp, rewards, ids, dtype, fused, rtol, cfg_kw=None):
+    from paper_2605_13276_b200 import grpo
+    cfg = grpo.GrpoConfig(group_size=x.shape[1], **(cfg_kw or {}))
+    loss, dl, st = _run_gpu(x, tokens, blp, rewards, ids, dtype, fused, cfg)
+    oloss, odl, ost = O.grpo_token_grad(x, tokens, blp, rewards, ids, clip_eps=cfg.clip_eps,
+                                        kl_coeff=cfg.kl_coeff)
+    # chunk log-probs (f64 accumulate on both sides)
+    lp = st["lp_chunk"].cpu().numpy()
+    np.testing.assert_allclose(lp, ost["lp_chunk"], rtol=1e-9, atol=2e-6)
+    assert st["group_ids"] == ost["group_ids"]            # canonical order, exact
+    assert st["n_chunks"] == ost["n_chunks"]
+    scale = sum(abs(v) for v in ost["coeff"].ravel()) / max(ost["coeff"].size, 1)
+    assert abs(loss - oloss) <= 1e-5 * max(abs(oloss), scale, 1e-12)
+    assert st["mean_ratio"] == pytest.approx(ost["mean_ratio"], rel=1e-5)
+    assert st["clip_fraction"] == pytest.approx(ost["clip_fraction"], abs=1.5 / ost["n_chunks"])
+    odl = odl.reshape(dl.shape)
+    err = np.abs(dl - odl)
+    tol = rtol * np.abs(odl) + rtol * np.abs(odl).max()
+    assert np.all(err <= tol), float((err / (np.abs(odl) + np.abs(odl).max())).max())
+    return st, ost
+
+
+def test_f32_unfused_odd_vocab_matches_oracle():
+    import torch
+    case = _case(0, 3, 4, 2, 3, 257, torch.float32)
+    _check(*case, torch.float32, fused=False, rtol=1e-5)
+
+
+def test_f32_vectorised_rows_match_oracle():
+    import torch
+    case = _case(1, 2, 4, 2, 5, 1024, torch.float32, binary=False)
+    _check(*case, torch.float32, fused=True, rtol=1e-5)   # f32 takes the unfused kernels
+
+
+def test_bf16_fused_matches_oracle():
+    import torch
+    case = _case(2, 4, 8, 1, 56, 4096, torch.bfloat16)
+    _check(*case, torch.bfloat16, fused=True, rtol=1e-2)
+
+
+def test_bf16_fused_multi_chunk_kl_matches_oracle():
+    import torch
+    case = _case(3, 5, 4, 3, 7, 2048, torch.bfloat16, spread=0.5, binary=False)
+    _check(*case, torch.bfloat16, fused=True, rtol=1e-2, cfg_kw={"kl_coeff": 0.3})
+
+
+def test_bf16_unfused_matches_oracle():
+    import torch
+    case = _case(4, 2, 8, 1, 56, 4096, torch.bfloat16)
+    _check(*case, torch.bfloat16, fused=False, rtol=1e-2)
+
+
+def test_bf16_openvla_vocab_rows():
+    """V = 32,064 (OpenVLA/Llama-2 padded vocab): the C2 row shape."""
+    import torch
+    case = _case(5, 2, 8, 1, 56, 32064, torch.bfloat16)
+    _check(*case, torch.bfloat16, fused=True, rtol=1e-2)
+
+
+def test_group_order_is_canonicalised_bitwise():
+    import torch
+    x, tokens, blp, rewards, ids = _case(6, 4, 8, 1, 56, 2048, torch.bfloat16)
+    perm = np.array([2, 0, 3, 1])
+    loss_a, dl_a, st_a = _run_gpu(x, tokens, blp, rewards, ids, torch.bfloat16)
+    loss_b, dl_b, st_b = _run_gpu(x[perm], tokens[perm], blp[perm], rewards[perm], ids[perm],
+                                  torch.bfloat16)
+    assert loss_a == loss_b
+    assert st_a["group_ids"] == st_b["group_ids"] == sorted(ids.tolist())
+    assert np.array_equal(dl_a[perm], dl_b)
+
+
+def test_fused_equals_unfused_forward_stats():
+    import torch
+    case = _case(7, 3, 8, 2, 9, 4096, torch.bfloat16, binary=False)
+    la, _, sa = _run_gpu(*case, torch.bfloat16, fused=True)
+    lb, _, sb = _run_gpu(*case, torch.bfloat16, fused=False)
+    assert la == pytest.approx(lb, rel=1e-12, abs=1e-15)
+    np.testing.assert_allclose(sa["lp_chunk"].cpu().numpy(), sb["lp_chunk"].cpu().numpy(),
+                               rtol=1e-9)
+
+
+def test_abort_on_nonfinite_reward_names_group():
+    import torch
+    from paper_2605_13276_b200.grpo import GrpoAbort
+    x, tokens, blp, rewards, ids = _case(8, 3, 4, 1, 4, 512, torch.bfloat16, ids=[7, 3, 5])
+    rewards[2, 1] = np.nan
+    with pytest.raises(GrpoAbort, match="group 5.*non-finite reward") as exc:
+        _run_gpu(x, tokens, blp, rewards, ids, torch.bfloat16)
+    assert exc.value.group_id == 5
+
+
+def test_abort_on_overflowing_ratio():
+    import torch
+    from paper_2605_13276_b200.grpo import GrpoAbort
+    x, tokens, blp, rewards, ids = _case(9, 3, 4, 1, 4, 512, torch.bfloat16, ids=[7, 3, 5])
+    blp[0, :, :] = -1e6
+    with pytest.raises(GrpoAbort, match="group 7.*non-finite importance ratio"):
+        _run_gpu(x, tokens, blp, rewards, ids, torch.bfloat16)
+
+
+def test_abort_on_nonfinite_logit():
+    import torch
+    from paper_2605_13276_b200.grpo import GrpoAbort
+    x, tokens, blp, rewards, ids = _case(10, 3, 4, 1, 4, 512, torch.float32, ids=[7, 3, 5])
+    x[1, 2, 0, 1, 5] = np.inf
+    with pytest.raises(GrpoAbort, match="group 3.*non-finite log-prob"):
+        _run_gpu(x, tokens, blp, rewards, ids, torch.float32)
+
+
+def test_token_out_of_range_is_usage_error():
+    import torch
+    from paper_2605_13276_b200.core import UsageError
+    x, tokens, blp, rewards, ids = _case(11, 2, 4, 1, 4, 512, torch.bfloat16)
+    tokens[0, 0, 0, 0] = 512
+    with pytest.raises(UsageError, match="token"):
+        _run_gpu(x, tokens, blp, rewards, ids, torch.bfloat16)
+
+
+def test_full_c2_batch_properties():
+    """BASELINE config 2 at full size (512 traj x 56 tokens x V=32,064, bf16):
+    size-independent properties plus an oracle check on a sample of groups."""
+    import torch
+    from paper_2605_13276_b200 import grpo
+    n_groups, G, C, T, V = 64, 8, 1, 56, 32064
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(0)
+    logits = (torch.randn(n_groups * G * C * T, V, device=dev, generator=g) * 2).to(torch.bfloat16)
+    tokens = torch.randint(31744, 32000, (n_groups * G * C * T,), device=dev, generator=g,
+                           dtype=torch.int32)
+    rewards = torch.randint(0, 2, (n_groups * G,), device=dev, generator=g).float()
+    cfg = grpo.GrpoConfig(group_size=G)
+    tl = grpo.TokenLoss(n_groups, G, C, T, V, cfg, dtype=torch.bfloat16)
+    blp0 = torch.zeros(n_groups * G * C, device=dev)
+    tl.launch(logits, tokens, blp0, rewards, None)
+    lp = tl.lp_chunk.clone()
+    blp = (lp + (torch.rand(lp.shape, device=dev, generator=g, dtype=torch.float64) - 0.5) * 0.1).float()
+    dl = torch.empty_like(logits)
+    tl.launch(logits, tokens, blp, rewards, dl)
+    st = tl.stats(rewards)
+    torch.cuda.synchronize()
+    assert st["n_chunks"] == n_groups * G * C
+    # rows of d loss / d logits sum to ~0 (softmax Jacobian), bf16 rounding only
+    rs = dl.float().sum(dim=1).abs().max().item()
+    assert rs <= 1e-2 * dl.float().abs().max().item()
+    # oracle on 2 groups: same coefficients up to the 1/(n_traj*C) weight
+    sel = [5, 40]
+    rows = torch.cat([torch.arange(k * G * T, (k + 1) * G * T, device=dev) for k in sel])
+    xs = logits[rows].float().cpu().numpy().reshape(len(sel), G, C, T, V)
+    ts = tokens[rows].cpu().numpy().reshape(len(sel), G, C, T)
+    bs = blp.view(n_groups, G, C)[sel].cpu().numpy()
+    rw = rewards.view(n_groups, G)[sel].cpu().numpy()
+    _, odl, ost = O.grpo_token_grad(xs, ts, bs, rw, np.array(sel))
+    np.testing.assert_allclose(tl.lp_chunk.view(n_groups, G, C)[sel].cpu().numpy(),
+                               ost["lp_chunk"], rtol=1e-9, atol=2e-6)
+    odl = odl.reshape(-1, V) * (len(sel) / n_groups)
+    got = dl[rows].float().cpu().numpy()
+    err = np.abs(got - odl)
+    assert np.all(err <= 1e-2 * np.abs(odl) + 1e-2 * np.abs(odl).max())
