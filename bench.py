@@ -41,7 +41,7 @@ UNIT = "samples/s"
 def _args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -214,13 +214,17 @@ def run_ours(a):
     dl = torch.empty_like(logits)
     stream = torch.cuda.current_stream()
 
-    for _ in range(max(a.warmup, 3)):
+    clocks = Clocks(dev.index if dev.index is not None else 0)
+    clocks.start()  # samples the warm-up tail and the whole timed region
+    t_warm = time.perf_counter()
+    w = 0
+    while w < max(a.warmup, 3) or time.perf_counter() - t_warm < 0.5:
         tl.launch(logits, tokens, blp, rewards, dl)
+        w += 1
+        if w % 16 == 0:
+            torch.cuda.synchronize()
     st = tl.stats(rewards)  # raises GrpoAbort on bad data
     barrier()
-
-    clocks = Clocks(dev.index if dev.index is not None else 0)
-    clocks.start()
     _lib.dvla_profile_enable(1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()

@@ -11,8 +11,8 @@ Follows reference pkg/src/dvla/grpo.py and kernels/numpy_backend.py:
                           policy_backward (:52-93)
   grpo_grad (token head)  the same epilogue with the action-token head
                           ("one Gaussian dim" -> "one
-                          action token"; chunk lp = sequential sum over the
-                          chunk's T token log-probs, f64)
+                          action token"; chunk lp = numpy pairwise sum over
+                          the chunk's T token log-probs, f64)
 """
 
 from __future__ import annotations
@@ -262,11 +262,9 @@ def grpo_token_grad(logits, tokens, blp, rewards, group_ids, clip_eps=0.2, adv_e
         lse[a:b], lp_tok[a:b] = token_row_stats(x2d[a:b], tok[a:b])
 
     _rows_parallel(rows, R, threads)
-    lp_chunk = np.zeros((n_groups * G * C,))
-    lpt = lp_tok.reshape(-1, T)
-    for t in range(T):  # sequential over the chunk's tokens, f64
-        lp_chunk += lpt[:, t]
-    lp_chunk = lp_chunk.reshape(n_groups, G, C)
+    # chunk-joint log-prob: numpy pairwise sum over the chunk's T tokens (the
+    # order numpy_backend.chunk_log_prob's .sum(axis=1) uses over D dims)
+    lp_chunk = lp_tok.reshape(-1, T).sum(axis=1).reshape(n_groups, G, C)
     n_traj = n_groups * G
     order, entries = _entries(group_ids, rewards, blp, G, adv_eps)
     loss, ratio_sum, clip_count, chunk_count, coeffs = _epilogue(

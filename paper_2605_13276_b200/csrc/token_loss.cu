@@ -5,7 +5,7 @@
 // kernels/numba_backend.py:49-61 chunk_log_prob, with "one Gaussian dim"
 // -> "one action token"):
 //   lp_tok[r]  = x[r, tgt_r] - logsumexp_v x[r, v]                 (f64)
-//   lp[q]      = sum_{t=0..T-1} lp_tok[q*T + t]   (sequential, f64)
+//   lp[q]      = sum_{t=0..T-1} lp_tok[q*T + t]   (numpy pairwise order, f64)
 //   rho, loss, coeff per chunk           <- grpo.py:252-268 (grpo_math.cuh)
 //   dlogits[r, v] = coeff[q] * (1[v == tgt_r] - softmax(x[r])_v)
 // i.e. the chain rule of policy.backward_batch (grpo.py:277) through the
@@ -33,7 +33,6 @@ namespace dvla {
 
 constexpr int kFusedComputeWarps = 16;
 constexpr int kFusedComputeThreads = kFusedComputeWarps * 32;
-constexpr int kFusedThreads = kFusedComputeThreads + 32;  // + producer warp
 constexpr int kFusedStages = 3;
 constexpr uint64_t kSpinTimeoutNs = 4000000000ull;  // 4 s: report, never hang
 
@@ -80,49 +79,106 @@ __global__ void adv_f64_kernel(const double* __restrict__ rewards, int64_t n_gro
                    [&](int64_t i, double v) { a[i] = v; });
 }
 
-// Sequential (t = 0..T-1) f64 sum of a chunk's token log-probs by one warp;
-// result valid in lane 0.  Loads are issued 32 at a time.
-__device__ __forceinline__ double warp_chunk_lp(const double* __restrict__ lp_tok, int64_t T,
-                                                int lane) {
-  double acc = 0.0;
-  for (int64_t m0 = 0; m0 < T; m0 += 32) {
-    double v = (m0 + lane < T) ? __ldcg(lp_tok + m0 + lane) : 0.0;
-    const int lim = (T - m0 < 32) ? static_cast<int>(T - m0) : 32;
-    for (int l = 0; l < lim; ++l) {
-      double x = __shfl_sync(0xffffffffu, v, l);
-      acc = __dadd_rn(acc, x);
-    }
+// Chunk-joint log-prob: numpy pairwise order over the chunk's T token
+// log-probs (the order numpy_backend.chunk_log_prob's .sum(axis=1) uses for
+// the Gaussian head, numpy_backend.py:39-49).  One warp, T <= 128; the
+// result is valid in every lane.  vals[m] holds lp_tok[32*m + lane].
+__device__ __forceinline__ double warp_pairwise_small(const double (&vals)[4], int T, int lane) {
+  double res;
+  if (T < 8) {
+    res = 0.0;
+    for (int t = 0; t < T; ++t) res = __dadd_rn(res, __shfl_sync(0xffffffffu, vals[0], t));
+    return res;
   }
-  return acc;
+  const int n8 = T - (T % 8);
+  // lanes 0..7: r_j = a[j] + a[j+8] + ... (sequential), j = lane
+  double r = 0.0;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    if (8 * m >= n8) break;
+    const int src = 8 * (m & 3) + (lane & 7);
+    double x = 0.0;
+    switch (m >> 2) {
+      case 0: x = __shfl_sync(0xffffffffu, vals[0], src); break;
+      case 1: x = __shfl_sync(0xffffffffu, vals[1], src); break;
+      case 2: x = __shfl_sync(0xffffffffu, vals[2], src); break;
+      default: x = __shfl_sync(0xffffffffu, vals[3], src); break;
+    }
+    r = (m == 0) ? x : __dadd_rn(r, x);
+  }
+  // ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7))
+  double p1 = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+  double p2 = __dadd_rn(p1, __shfl_xor_sync(0xffffffffu, p1, 2));
+  double p4 = __dadd_rn(p2, __shfl_xor_sync(0xffffffffu, p2, 4));
+  res = __shfl_sync(0xffffffffu, p4, 0);
+  for (int t = n8; t < T; ++t) {
+    double x;
+    switch (t >> 5) {
+      case 0: x = __shfl_sync(0xffffffffu, vals[0], t & 31); break;
+      case 1: x = __shfl_sync(0xffffffffu, vals[1], t & 31); break;
+      case 2: x = __shfl_sync(0xffffffffu, vals[2], t & 31); break;
+      default: x = __shfl_sync(0xffffffffu, vals[3], t & 31); break;
+    }
+    res = __dadd_rn(res, x);
+  }
+  return res;
+}
+
+// Chunk lp for any T from global memory (numpy pairwise order), one thread.
+__device__ __forceinline__ double chunk_lp_pairwise(const double* __restrict__ lp_tok, int64_t T) {
+  return pairwise_sum([&](int64_t i) { return __ldcg(lp_tok + i); }, 0, T);
 }
 
 // ---------------------------------------------------- fused bf16 kernel
+//
+// Warp roles (1 CTA per SM, persistent, rows assigned round-robin):
+//   warps 0..15  compute: per row, phase A (warp max, warp sum-exp, publish
+//                (m_w, s_w) to SMEM) and, one row later, phase B (dlogits in
+//                place in the SMEM row).  No CTA-wide barriers.
+//   warp 16      producer: TMA bulk loads of logits rows into a 3-stage SMEM
+//                ring, TMA bulk stores of finished dlogits rows.
+//   warp 17      coefficient: per row, combines the 16 warp partials into lse
+//                (f64), gathers the target logit, publishes lp_tok and bumps
+//                the chunk counter (red.release.gpu); one row later waits for
+//                the chunk to complete (other CTAs), sums its T token
+//                log-probs and evaluates the GRPO coefficient for phase B.
+// Ordering A(k+1) before B(k) on every CTA makes the cross-CTA chunk wait
+// deadlock-free while all CTAs are co-resident (grid <= #SMs, T <= grid).
+constexpr int kCoefWarp = kFusedComputeWarps + 1;
+constexpr int kFusedThreadsWS = (kFusedComputeWarps + 2) * 32;
+
 struct FusedSmem {
   uint64_t full[kFusedStages];
+  uint64_t adone[kFusedStages];
+  uint64_t cfull[kFusedStages];
   uint64_t done[kFusedStages];
+  double ws[kFusedStages][kFusedComputeWarps];
+  float wm[kFusedStages][kFusedComputeWarps];
+  float kval[kFusedStages];   // lse*log2e - log2|c|
+  float lseL[kFusedStages];   // lse*log2e
+  float cf[kFusedStages];     // coefficient (f32)
   double lse[kFusedStages];
-  double coeff_s;
-  double redd[kFusedComputeWarps];
-  float redf[kFusedComputeWarps];
+  uint32_t mode[kFusedStages];  // 0 zero row, 1 finite c (bit 31: c > 0), 2 non-finite c
   int32_t tgt[kFusedStages];
 };
 
-__device__ __forceinline__ void spin_until_ready(const uint32_t* cnt, uint32_t target,
-                                                 uint32_t* err) {
-  if (ld_acquire_gpu(cnt) == target) return;
+__device__ __forceinline__ bool spin_until_at_least(const uint32_t* cnt, uint32_t target,
+                                                    uint32_t* err) {
+  if (ld_acquire_gpu(cnt) >= target) return true;
   const uint64_t t0 = globaltimer_ns();
   uint32_t ns = 32;
-  while (ld_acquire_gpu(cnt) != target) {
+  while (ld_acquire_gpu(cnt) < target) {
     __nanosleep(ns);
     if (ns < 256) ns <<= 1;
     if (globaltimer_ns() - t0 > kSpinTimeoutNs) {
       atomicOr(err, kErrTimeout);
-      return;
+      return false;
     }
   }
+  return true;
 }
 
-__global__ void __launch_bounds__(kFusedThreads, 1)
+__global__ void __launch_bounds__(kFusedThreadsWS, 1)
     tok_fused_bf16_kernel(TokParams p, uint32_t stage_bytes, int write_dl) {
   extern __shared__ __align__(128) uint8_t dyn_smem[];
   FusedSmem& S = *reinterpret_cast<FusedSmem*>(dyn_smem);
@@ -136,11 +192,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   const int64_t nloc = (p.R > blockIdx.x) ? (p.R - blockIdx.x + G - 1) / G : 0;
   auto row_of = [&](int64_t k) { return blockIdx.x + k * G; };
   auto buf = [&](int s) { return bufs + static_cast<size_t>(s) * stage_bytes; };
+  const int64_t T = p.T;
 
   if (tid == 0) {
     for (int s = 0; s < kFusedStages; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.done[s], kFusedComputeWarps);
+      mbar_init(&S.adone[s], kFusedComputeWarps);
+      mbar_init(&S.cfull[s], 1);
+      mbar_init(&S.done[s], write_dl ? kFusedComputeWarps : 1);
     }
     fence_mbar_init();
   }
@@ -178,35 +237,111 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     return;
   }
 
+  // ---------------------------------------------------- coefficient warp
+  if (warp == kCoefWarp) {
+    int32_t tgt_next = (nloc > 0 && lane == 0) ? __ldg(p.tokens + row_of(0)) : 0;
+    auto tail = [&](int64_t k) {  // lse, lp_tok, chunk counter
+      const int s = static_cast<int>(k % kFusedStages);
+      const uint32_t ph = static_cast<uint32_t>((k / kFusedStages) & 1);
+      const int64_t r = row_of(k);
+      int32_t tgt = tgt_next;
+      if (lane == 0 && k + 1 < nloc) tgt_next = __ldg(p.tokens + row_of(k + 1));
+      mbar_wait(&S.adone[s], ph);
+      // combine the 16 warp partials: M = max m_w, S = sum s_w 2^((m_w - M) log2e)
+      float mw = (lane < kFusedComputeWarps) ? S.wm[s][lane] : -INFINITY;
+      double sw = (lane < kFusedComputeWarps) ? S.ws[s][lane] : 0.0;
+      const float M = warp_max_f32(mw);
+      double term = (lane < kFusedComputeWarps && sw > 0.0)
+                        ? sw * exp2(static_cast<double>(mw - M) * 1.4426950408889634)
+                        : 0.0;
+      term = warp_sum_f64(term);
+      if (lane == 0) {
+        const double lse = static_cast<double>(M) + log(term);
+        double xt;
+        if (tgt < 0 || tgt >= V) {
+          atomicOr(p.err, kErrToken);
+          xt = __longlong_as_double(0x7ff8000000000000ll);
+          tgt = -1;
+        } else {
+          xt = static_cast<double>(__bfloat162float(
+              reinterpret_cast<const __nv_bfloat16*>(buf(s))[tgt]));
+        }
+        S.tgt[s] = tgt;
+        S.lseL[s] = static_cast<float>(lse * 1.4426950408889634);
+        S.lse[s] = lse;
+        p.lse[r] = lse;
+        p.lp_tok[r] = xt - lse;
+        if (write_dl) red_release_gpu_add(p.cnt + r / T, 1u);
+      }
+      __syncwarp();
+      if (!write_dl && lane == 0) mbar_arrive(&S.done[s]);
+    };
+    auto coef = [&](int64_t k) {  // chunk coefficient for phase B of row k
+      const int s = static_cast<int>(k % kFusedStages);
+      const int64_t r = row_of(k);
+      const int64_t q = r / T;
+      if (lane == 0) spin_until_at_least(p.cnt + q, static_cast<uint32_t>(T), p.err);
+      __syncwarp();
+      const double* lt = p.lp_tok + q * T;
+      double vals[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int64_t t = 32 * m + lane;
+        vals[m] = (t < T) ? __ldcg(lt + t) : 0.0;
+      }
+      const double lp = warp_pairwise_small(vals, static_cast<int>(T), lane);
+      if (lane == 0) {
+        ChunkTerms ct = chunk_terms(lp, static_cast<double>(p.blp[q]), p.adv[q / p.C], p.w,
+                                    p.clip_eps, p.kl_coeff);
+        const double c = ct.coeff;
+        if (r % T == 0) {
+          p.lp_chunk[q] = lp;
+          p.coeff[q] = c;
+        }
+        uint32_t mode;
+        if (c == 0.0) {
+          mode = 0u;
+        } else if (!isfinite(c)) {
+          mode = 2u;
+        } else {
+          mode = 1u | ((c > 0.0) ? 0x80000000u : 0u);
+          S.kval[s] = static_cast<float>(S.lse[s] * 1.4426950408889634 - log2(fabs(c)));
+        }
+        S.mode[s] = mode;
+        S.cf[s] = static_cast<float>(c);
+        mbar_arrive(&S.cfull[s]);
+      }
+      __syncwarp();
+    };
+    if (nloc > 0) tail(0);
+    for (int64_t k = 0; k < nloc; ++k) {
+      if (k + 1 < nloc) tail(k + 1);
+      if (write_dl) coef(k);
+    }
+    return;
+  }
+
   // ------------------------------------------------------- compute warps
   const int nvec = static_cast<int>(V >> 3);  // uint4 = 8 bf16
-  const int64_t T = p.T;
-
-  // phase A: row statistics, lp_tok, chunk completion
   auto phaseA = [&](int64_t k) {
     const int s = static_cast<int>(k % kFusedStages);
     const uint32_t ph = static_cast<uint32_t>((k / kFusedStages) & 1);
-    const int64_t r = row_of(k);
     mbar_wait(&S.full[s], ph);
     const uint4* v = reinterpret_cast<const uint4*>(buf(s));
     uint32_t mx0 = 0xff80ff80u, mx1 = 0xff80ff80u;
+#pragma unroll 4
     for (int i = tid; i < nvec; i += kFusedComputeThreads) {
-      uint4 x = v[i];
+      const uint4 x = v[i];
       mx0 = bf16x2_max(mx0, bf16x2_max(x.x, x.y));
       mx1 = bf16x2_max(mx1, bf16x2_max(x.z, x.w));
     }
-    uint32_t mx = bf16x2_max(mx0, mx1);
-    float m = fmaxf(bf16lo(mx), bf16hi(mx));
-    m = warp_max_f32(m);
-    if (lane == 0) S.redf[warp] = m;
-    named_bar_sync(1, kFusedComputeThreads);
-    m = S.redf[0];
-#pragma unroll
-    for (int w = 1; w < kFusedComputeWarps; ++w) m = fmaxf(m, S.redf[w]);
+    const uint32_t mx = bf16x2_max(mx0, mx1);
+    const float m = warp_max_f32(fmaxf(bf16lo(mx), bf16hi(mx)));
     const float mL = m * kLog2e;
     float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll 2
     for (int i = tid; i < nvec; i += kFusedComputeThreads) {
-      uint4 x = v[i];
+      const uint4 x = v[i];
       s0 += ex2f(fmaf(bf16lo(x.x), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.x), kLog2e, -mL));
       s1 += ex2f(fmaf(bf16lo(x.y), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.y), kLog2e, -mL));
       s2 += ex2f(fmaf(bf16lo(x.z), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.z), kLog2e, -mL));
@@ -215,71 +350,32 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     double part = (static_cast<double>(s0) + static_cast<double>(s1)) +
                   (static_cast<double>(s2) + static_cast<double>(s3));
     part = warp_sum_f64(part);
-    if (lane == 0) S.redd[warp] = part;
-    named_bar_sync(1, kFusedComputeThreads);
-    if (warp == 0) {
-      uint32_t old = 0;
-      if (lane == 0) {
-        double sum = 0.0;
-#pragma unroll
-        for (int w = 0; w < kFusedComputeWarps; ++w) sum += S.redd[w];
-        const double lse = static_cast<double>(m) + log(sum);
-        int32_t tgt = p.tokens[r];
-        double xt;
-        if (tgt < 0 || tgt >= V) {
-          atomicOr(p.err, kErrToken);
-          xt = __longlong_as_double(0x7ff8000000000000ll);  // NaN -> abort
-          tgt = -1;
-        } else {
-          xt = static_cast<double>(__bfloat162float(
-              reinterpret_cast<const __nv_bfloat16*>(buf(s))[tgt]));
-        }
-        S.lse[s] = lse;
-        S.tgt[s] = tgt;
-        p.lp_tok[r] = xt - lse;
-        if (write_dl) old = atom_add_acq_rel_gpu(p.cnt + r / T, 1u);
-      }
-      old = __shfl_sync(0xffffffffu, old, 0);
-      if (write_dl && old == static_cast<uint32_t>(T - 1)) {
-        // last row of this chunk: the chunk coefficient (grpo.py:252-268)
-        const int64_t q = r / T;
-        const double lp = warp_chunk_lp(p.lp_tok + q * T, T, lane);
-        if (lane == 0) {
-          ChunkTerms ct = chunk_terms(lp, static_cast<double>(p.blp[q]), p.adv[q / p.C], p.w,
-                                      p.clip_eps, p.kl_coeff);
-          p.lp_chunk[q] = lp;
-          p.coeff[q] = ct.coeff;
-          red_release_gpu_add(p.cnt + q, 1u);  // T + 1 == coefficient ready
-        }
-      }
+    if (lane == 0) {
+      S.wm[s][warp] = m;
+      S.ws[s][warp] = part;
+      mbar_arrive(&S.adone[s]);
     }
   };
 
-  // phase B: dlogits of row k, in place in SMEM, then hand to the producer
   auto phaseB = [&](int64_t k) {
     const int s = static_cast<int>(k % kFusedStages);
-    const int64_t r = row_of(k);
-    const int64_t q = r / T;
-    if (tid == 0) {
-      spin_until_ready(p.cnt + q, static_cast<uint32_t>(T + 1), p.err);
-      S.coeff_s = __ldcg(p.coeff + q);
-    }
-    named_bar_sync(1, kFusedComputeThreads);
-    const double c = S.coeff_s;
-    const double lse = S.lse[s];
-    const int32_t tgt = S.tgt[s];
+    const uint32_t ph = static_cast<uint32_t>((k / kFusedStages) & 1);
+    mbar_wait(&S.cfull[s], ph);
+    const uint32_t mode = S.mode[s];
     uint4* v = reinterpret_cast<uint4*>(buf(s));
-    if (c == 0.0 || !isfinite(c)) {
-      // zero gradient rows (A == 0 or clipped chunks): 0 * (onehot - p)
-      const uint32_t z = (c == 0.0) ? 0u : 0x7fc07fc0u;
+    if ((mode & 3u) != 1u) {
+      // zero-gradient rows (A == 0 or clipped chunk): 0 * (onehot - p)
+      const uint32_t z = (mode == 0u) ? 0u : 0x7fc07fc0u;
       for (int i = tid; i < nvec; i += kFusedComputeThreads) v[i] = make_uint4(z, z, z, z);
     } else {
       // -c * p_v = -sign(c) * 2^(x*log2e - (lse*log2e - log2|c|))
-      const float K = static_cast<float>(lse * 1.4426950408889634 - log2(fabs(c)));
-      const uint32_t sgn = (c > 0.0) ? 0x80008000u : 0u;
+      const float K = S.kval[s];
+      const uint32_t sgn = (mode & 0x80000000u) ? 0x80008000u : 0u;
+      const int32_t tgt = S.tgt[s];
       const int tv = tgt >> 3;
+#pragma unroll 2
       for (int i = tid; i < nvec; i += kFusedComputeThreads) {
-        uint4 x = v[i];
+        const uint4 x = v[i];
         uint4 o;
         o.x = pack_bf16x2(ex2f(fmaf(bf16lo(x.x), kLog2e, -K)), ex2f(fmaf(bf16hi(x.x), kLog2e, -K))) ^ sgn;
         o.y = pack_bf16x2(ex2f(fmaf(bf16lo(x.y), kLog2e, -K)), ex2f(fmaf(bf16hi(x.y), kLog2e, -K))) ^ sgn;
@@ -288,13 +384,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         if (i == tv) {
           // target column: c * (1 - p_t)
           const int e = tgt & 7;
-          const uint32_t word = (&x.x)[e >> 1];
+          const uint32_t word = (e >> 1) == 0 ? x.x : (e >> 1) == 1 ? x.y : (e >> 1) == 2 ? x.z : x.w;
           const float xt = (e & 1) ? bf16hi(word) : bf16lo(word);
-          const float pt = ex2f(fmaf(xt, kLog2e, -static_cast<float>(lse * 1.4426950408889634)));
-          const float val = static_cast<float>(c) * (1.0f - pt);
+          const float pt = ex2f(fmaf(xt, kLog2e, -S.lseL[s]));
+          const float val = S.cf[s] * (1.0f - pt);
           const uint32_t b = pack_bf16x2(val, val) & 0xffffu;
-          uint32_t& ow = (&o.x)[e >> 1];
+          uint32_t ow = (e >> 1) == 0 ? o.x : (e >> 1) == 1 ? o.y : (e >> 1) == 2 ? o.z : o.w;
           ow = (e & 1) ? ((ow & 0x0000ffffu) | (b << 16)) : ((ow & 0xffff0000u) | b);
+          if ((e >> 1) == 0) o.x = ow;
+          else if ((e >> 1) == 1) o.y = ow;
+          else if ((e >> 1) == 2) o.z = ow;
+          else o.w = ow;
         }
         v[i] = o;
       }
@@ -305,11 +405,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   };
 
   if (!write_dl) {
-    for (int64_t k = 0; k < nloc; ++k) {
-      phaseA(k);
-      named_bar_sync(1, kFusedComputeThreads);  // everyone done reading buf
-      if (lane == 0) mbar_arrive(&S.done[k % kFusedStages]);
-    }
+    for (int64_t k = 0; k < nloc; ++k) phaseA(k);
     return;
   }
   if (nloc > 0) phaseA(0);
@@ -432,8 +528,8 @@ __global__ void tok_chunk_kernel(TokParams p) {
   const int lane = threadIdx.x & 31;
   for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < p.n_chunks;
        q += warps) {
-    const double lp = warp_chunk_lp(p.lp_tok + q * p.T, p.T, lane);
     if (lane == 0) {
+      const double lp = chunk_lp_pairwise(p.lp_tok + q * p.T, p.T);
       ChunkTerms ct = chunk_terms(lp, static_cast<double>(p.blp[q]), p.adv[q / p.C], p.w,
                                   p.clip_eps, p.kl_coeff);
       p.lp_chunk[q] = lp;
@@ -685,7 +781,7 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
                          ((V * esz) % 16 == 0);
   const size_t fsmem = fused_smem_bytes(V);
   const bool fused = !(flags & DVLA_TL_UNFUSED) && dtype == DVLA_BF16 && aligned16 &&
-                     fsmem <= 227 * 1024 && T <= sms && R >= 1;
+                     fsmem <= 227 * 1024 && T <= sms && T <= 128 && R >= 1;
   if (fused) {
     static bool attr_set[64] = {false};
     if (!attr_set[dev & 63]) {
@@ -698,7 +794,7 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
     const uint32_t stage_bytes = static_cast<uint32_t>(((V * 2 + 127) / 128) * 128);
     cudaEvent_t stop;
     prof_begin(stream, &stop);
-    tok_fused_bf16_kernel<<<grid, kFusedThreads, fsmem, stream>>>(p, stage_bytes, want_dl ? 1 : 0);
+    tok_fused_bf16_kernel<<<grid, kFusedThreadsWS, fsmem, stream>>>(p, stage_bytes, want_dl ? 1 : 0);
     prof_end(stream, stop);
     if (int rc = launch_check("tok_fused_bf16_kernel")) return rc;
     if (!want_dl) {

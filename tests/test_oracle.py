@@ -121,7 +121,41 @@ def test_token_oracle_small_case_properties():
     assert st["group_ids"] == [2, 5]
     # each dlogits row sums to zero (softmax Jacobian rows) times coeff
     np.testing.assert_allclose(dl.sum(axis=-1), 0.0, atol=1e-12)
-    # lp_tok <= 0 and lp_chunk is the sequential sum
+    # lp_tok <= 0 and lp_chunk is the per-chunk sum
     assert np.all(st["lp_tok"] <= 0)
     np.testing.assert_allclose(st["lp_chunk"].reshape(-1), st["lp_tok"].reshape(-1, T).sum(1),
                                rtol=1e-13)
+
+
+def _pairwise(a):
+    """numpy pairwise_sum restated (loops_utils.h) -- used by the GPU kernels."""
+    n = len(a)
+    if n < 8:
+        s = 0.0
+        for x in a:
+            s += x
+        return s
+    if n <= 128:
+        r = list(a[:8])
+        i = 8
+        while i < n - n % 8:
+            for j in range(8):
+                r[j] += a[i + j]
+            i += 8
+        s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+        for x in a[i:]:
+            s += x
+        return s
+    n2 = n // 2
+    n2 -= n2 % 8
+    return _pairwise(a[:n2]) + _pairwise(a[n2:])
+
+
+@pytest.mark.parametrize("T", [1, 3, 7, 8, 9, 15, 16, 56, 57, 100, 128, 129, 300])
+def test_row_sum_is_numpy_pairwise_bitwise(T):
+    """The chunk-lp order the kernels implement (numpy pairwise) is what
+    ndarray.sum(axis=1) computes on contiguous rows."""
+    x = np.random.default_rng(T).normal(-10, 3, (5, T))
+    got = x.sum(axis=1)
+    for i in range(5):
+        assert got[i] == _pairwise(list(x[i])), T
