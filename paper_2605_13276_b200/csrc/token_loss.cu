@@ -131,33 +131,46 @@ __device__ __forceinline__ double chunk_lp_pairwise(const double* __restrict__ l
 
 // ---------------------------------------------------- fused bf16 kernel
 //
-// Warp roles (1 CTA per SM, persistent, rows assigned round-robin):
-//   warps 0..15  compute: per row, phase A (warp max, warp sum-exp, publish
-//                (m_w, s_w) to SMEM) and, one row later, phase B (dlogits in
-//                place in the SMEM row).  No CTA-wide barriers.
-//   warp 16      producer: TMA bulk loads of logits rows into a 3-stage SMEM
-//                ring, TMA bulk stores of finished dlogits rows.
-//   warp 17      coefficient: per row, combines the 16 warp partials into lse
-//                (f64), gathers the target logit, publishes lp_tok and bumps
-//                the chunk counter (red.release.gpu); one row later waits for
-//                the chunk to complete (other CTAs), sums its T token
-//                log-probs and evaluates the GRPO coefficient for phase B.
-// Ordering A(k+1) before B(k) on every CTA makes the cross-CTA chunk wait
-// deadlock-free while all CTAs are co-resident (grid <= #SMs, T <= grid).
+// One CTA per SM (persistent), rows assigned round-robin (row = cta + k*grid).
+// Every CTA walks one op sequence: A(0..L-1), then A(k), B(k-L), ..., B(n-1):
+//   A(k)  row k streamed HBM -> SMEM by TMA; 16 compute warps take warp
+//         max / sum-exp (MUFU ex2) and publish (m_w, s_w); the coefficient
+//         warp combines them into lse (f64), gathers the target logit,
+//         publishes lp_tok and bumps the chunk counter (red.release.gpu).
+//   B(k)  row k streamed again -- from L2, L rounds (~L*148*64 KB) after
+//         A(k) -- the coefficient warp waits for the chunk to be complete on
+//         all CTAs (long done by then), sums its T token log-probs (numpy
+//         pairwise order) and evaluates the GRPO coefficient; the compute
+//         warps write d loss / d logits in place and the store warp streams
+//         the row back with a TMA bulk store.
+// HBM traffic stays at the compulsory 2*N*2 bytes while the L-round lag
+// hides the cross-CTA chunk dependency.  A(k+L) precedes B(k) on every CTA,
+// so the chunk wait is deadlock-free while all CTAs are co-resident
+// (grid <= #SMs, T <= grid).
+//
+// Warp roles: 0..15 compute, 16 loader, 17 coefficient, 18 store.
+// Barriers per SMEM stage s (each completes exactly once per op on s, so the
+// parity of op n is (n / kStages) & 1 everywhere):
+//   full   loader -> compute, coef         (TMA tx bytes)
+//   adone  compute -> coef (A) / store (B) (16 arrivals)
+//   cfull  coef -> compute                 (1 arrival; dummy for A ops)
+//   empty  coef (A) / store (B) -> loader  (1 arrival)
+constexpr int kWarpLoader = kFusedComputeWarps;
 constexpr int kCoefWarp = kFusedComputeWarps + 1;
-constexpr int kFusedThreadsWS = (kFusedComputeWarps + 2) * 32;
+constexpr int kWarpStore = kFusedComputeWarps + 2;
+constexpr int kFusedThreadsWS = (kFusedComputeWarps + 3) * 32;
+constexpr int kLagRounds = 3;
 
 struct FusedSmem {
   uint64_t full[kFusedStages];
   uint64_t adone[kFusedStages];
   uint64_t cfull[kFusedStages];
-  uint64_t done[kFusedStages];
+  uint64_t empty[kFusedStages];
   double ws[kFusedStages][kFusedComputeWarps];
   float wm[kFusedStages][kFusedComputeWarps];
   float kval[kFusedStages];   // lse*log2e - log2|c|
   float lseL[kFusedStages];   // lse*log2e
   float cf[kFusedStages];     // coefficient (f32)
-  double lse[kFusedStages];
   uint32_t mode[kFusedStages];  // 0 zero row, 1 finite c (bit 31: c > 0), 2 non-finite c
   int32_t tgt[kFusedStages];
 };
@@ -178,6 +191,25 @@ __device__ __forceinline__ bool spin_until_at_least(const uint32_t* cnt, uint32_
   return true;
 }
 
+// op n of a CTA with nloc rows and lag L: (is_B, local row)
+__device__ __forceinline__ void op_of(int64_t n, int64_t nloc, int L, bool* isB, int64_t* k) {
+  const int64_t Le = nloc < L ? nloc : L;  // effective lag
+  if (n < Le) {
+    *isB = false;
+    *k = n;
+    return;
+  }
+  const int64_t m = n - Le;  // pairs (A(Le + j), B(j)) for j < nloc - Le, then B tail
+  const int64_t pairs = nloc - Le;
+  if (m < 2 * pairs) {
+    *isB = (m & 1) != 0;
+    *k = (m & 1) ? (m >> 1) : (Le + (m >> 1));
+    return;
+  }
+  *isB = true;
+  *k = pairs + (m - 2 * pairs);
+}
+
 __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     tok_fused_bf16_kernel(TokParams p, uint32_t stage_bytes, int write_dl) {
   extern __shared__ __align__(128) uint8_t dyn_smem[];
@@ -190,6 +222,8 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   const uint32_t row_bytes = static_cast<uint32_t>(V * 2);
   const int64_t G = gridDim.x;
   const int64_t nloc = (p.R > blockIdx.x) ? (p.R - blockIdx.x + G - 1) / G : 0;
+  const int64_t nops = write_dl ? 2 * nloc : nloc;
+  const int L = write_dl ? kLagRounds : 1 << 30;  // forward-only: A ops only
   auto row_of = [&](int64_t k) { return blockIdx.x + k * G; };
   auto buf = [&](int s) { return bufs + static_cast<size_t>(s) * stage_bytes; };
   const int64_t T = p.T;
@@ -199,7 +233,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       mbar_init(&S.full[s], 1);
       mbar_init(&S.adone[s], kFusedComputeWarps);
       mbar_init(&S.cfull[s], 1);
-      mbar_init(&S.done[s], write_dl ? kFusedComputeWarps : 1);
+      mbar_init(&S.empty[s], 1);
     }
     fence_mbar_init();
   }
@@ -208,31 +242,44 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   const __nv_bfloat16* logits = static_cast<const __nv_bfloat16*>(p.logits);
   __nv_bfloat16* dl = static_cast<__nv_bfloat16*>(p.dlogits);
 
-  // ------------------------------------------------------- producer warp
-  if (warp == kFusedComputeWarps) {
+  // --------------------------------------------------------- loader warp
+  if (warp == kWarpLoader) {
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
-      const int64_t pro = nloc < kFusedStages ? nloc : kFusedStages;
-      for (int64_t k = 0; k < pro; ++k) {
-        mbar_arrive_expect_tx(&S.full[k], row_bytes);
-        tma_load_1d_evict_first(buf(k), logits + row_of(k) * V, row_bytes, &S.full[k], pol);
+      for (int64_t n = 0; n < nops; ++n) {
+        const int s = static_cast<int>(n % kFusedStages);
+        if (n >= kFusedStages)
+          mbar_wait(&S.empty[s], static_cast<uint32_t>(((n / kFusedStages) - 1) & 1));
+        bool isB;
+        int64_t k;
+        op_of(n, nloc, L, &isB, &k);
+        mbar_arrive_expect_tx(&S.full[s], row_bytes);
+        if (isB)  // second (last) read of the row: from L2, then evict
+          tma_load_1d_evict_first(buf(s), logits + row_of(k) * V, row_bytes, &S.full[s], pol);
+        else
+          tma_load_1d(buf(s), logits + row_of(k) * V, row_bytes, &S.full[s]);
       }
-      for (int64_t k = 0; k < nloc; ++k) {
-        const int s = static_cast<int>(k % kFusedStages);
-        const uint32_t ph = static_cast<uint32_t>((k / kFusedStages) & 1);
-        mbar_wait(&S.done[s], ph);
-        if (write_dl) {
-          tma_store_1d_evict_first(dl + row_of(k) * V, buf(s), row_bytes, pol);
-          bulk_commit();
-        }
-        if (k + kFusedStages < nloc) {
-          if (write_dl) bulk_wait_read<0>();
-          mbar_arrive_expect_tx(&S.full[s], row_bytes);
-          tma_load_1d_evict_first(buf(s), logits + row_of(k + kFusedStages) * V, row_bytes,
-                                  &S.full[s], pol);
-        }
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------- store warp
+  if (warp == kWarpStore) {
+    if (lane == 0 && write_dl) {
+      const uint64_t pol = l2_policy_evict_first();
+      for (int64_t n = 0; n < nops; ++n) {
+        bool isB;
+        int64_t k;
+        op_of(n, nloc, L, &isB, &k);
+        if (!isB) continue;
+        const int s = static_cast<int>(n % kFusedStages);
+        mbar_wait(&S.adone[s], static_cast<uint32_t>((n / kFusedStages) & 1));
+        tma_store_1d_evict_first(dl + row_of(k) * V, buf(s), row_bytes, pol);
+        bulk_commit();
+        bulk_wait_read<0>();
+        mbar_arrive(&S.empty[s]);
       }
-      if (write_dl) bulk_wait<0>();
+      bulk_wait<0>();
     }
     return;
   }
@@ -240,126 +287,129 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   // ---------------------------------------------------- coefficient warp
   if (warp == kCoefWarp) {
     int32_t tgt_next = (nloc > 0 && lane == 0) ? __ldg(p.tokens + row_of(0)) : 0;
-    auto tail = [&](int64_t k) {  // lse, lp_tok, chunk counter
-      const int s = static_cast<int>(k % kFusedStages);
-      const uint32_t ph = static_cast<uint32_t>((k / kFusedStages) & 1);
+    int64_t next_a = 1;  // next A row whose token id to prefetch
+    for (int64_t n = 0; n < nops; ++n) {
+      const int s = static_cast<int>(n % kFusedStages);
+      const uint32_t ph = static_cast<uint32_t>((n / kFusedStages) & 1);
+      bool isB;
+      int64_t k;
+      op_of(n, nloc, L, &isB, &k);
       const int64_t r = row_of(k);
-      int32_t tgt = tgt_next;
-      if (lane == 0 && k + 1 < nloc) tgt_next = __ldg(p.tokens + row_of(k + 1));
-      mbar_wait(&S.adone[s], ph);
-      // combine the 16 warp partials: M = max m_w, S = sum s_w 2^((m_w - M) log2e)
-      float mw = (lane < kFusedComputeWarps) ? S.wm[s][lane] : -INFINITY;
-      double sw = (lane < kFusedComputeWarps) ? S.ws[s][lane] : 0.0;
-      const float M = warp_max_f32(mw);
-      double term = (lane < kFusedComputeWarps && sw > 0.0)
-                        ? sw * exp2(static_cast<double>(mw - M) * 1.4426950408889634)
-                        : 0.0;
-      term = warp_sum_f64(term);
-      if (lane == 0) {
-        const double lse = static_cast<double>(M) + log(term);
-        double xt;
-        if (tgt < 0 || tgt >= V) {
-          atomicOr(p.err, kErrToken);
-          xt = __longlong_as_double(0x7ff8000000000000ll);
-          tgt = -1;
-        } else {
-          xt = static_cast<double>(__bfloat162float(
-              reinterpret_cast<const __nv_bfloat16*>(buf(s))[tgt]));
+      if (!isB) {
+        // ---- tail of A(k): lse, lp_tok, chunk counter
+        int32_t tgt = tgt_next;
+        if (lane == 0 && next_a < nloc) tgt_next = __ldg(p.tokens + row_of(next_a));
+        ++next_a;
+        mbar_wait(&S.adone[s], ph);
+        const float mw = (lane < kFusedComputeWarps) ? S.wm[s][lane] : -INFINITY;
+        const double sw = (lane < kFusedComputeWarps) ? S.ws[s][lane] : 0.0;
+        const float M = warp_max_f32(mw);
+        double term = (lane < kFusedComputeWarps && sw > 0.0)
+                          ? sw * exp2(static_cast<double>(mw - M) * 1.4426950408889634)
+                          : 0.0;
+        term = warp_sum_f64(term);
+        if (lane == 0) {
+          const double lse = static_cast<double>(M) + log(term);
+          double xt;
+          if (tgt < 0 || tgt >= V) {
+            atomicOr(p.err, kErrToken);
+            xt = __longlong_as_double(0x7ff8000000000000ll);
+          } else {
+            xt = static_cast<double>(__bfloat162float(
+                reinterpret_cast<const __nv_bfloat16*>(buf(s))[tgt]));
+          }
+          p.lse[r] = lse;
+          p.lp_tok[r] = xt - lse;
+          if (write_dl) red_release_gpu_add(p.cnt + r / T, 1u);
+          mbar_arrive(&S.cfull[s]);  // keeps the per-stage phases aligned
+          mbar_arrive(&S.empty[s]);
         }
-        S.tgt[s] = tgt;
-        S.lseL[s] = static_cast<float>(lse * 1.4426950408889634);
-        S.lse[s] = lse;
-        p.lse[r] = lse;
-        p.lp_tok[r] = xt - lse;
-        if (write_dl) red_release_gpu_add(p.cnt + r / T, 1u);
-      }
-      __syncwarp();
-      if (!write_dl && lane == 0) mbar_arrive(&S.done[s]);
-    };
-    auto coef = [&](int64_t k) {  // chunk coefficient for phase B of row k
-      const int s = static_cast<int>(k % kFusedStages);
-      const int64_t r = row_of(k);
-      const int64_t q = r / T;
-      if (lane == 0) spin_until_at_least(p.cnt + q, static_cast<uint32_t>(T), p.err);
-      __syncwarp();
-      const double* lt = p.lp_tok + q * T;
-      double vals[4];
+        __syncwarp();
+      } else {
+        // ---- coefficient for B(k)
+        mbar_wait(&S.full[s], ph);  // stage reuse ordering (see header)
+        const int64_t q = r / T;
+        if (lane == 0) spin_until_at_least(p.cnt + q, static_cast<uint32_t>(T), p.err);
+        __syncwarp();
+        const double* lt = p.lp_tok + q * T;
+        double vals[4];
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int64_t t = 32 * m + lane;
-        vals[m] = (t < T) ? __ldcg(lt + t) : 0.0;
-      }
-      const double lp = warp_pairwise_small(vals, static_cast<int>(T), lane);
-      if (lane == 0) {
-        ChunkTerms ct = chunk_terms(lp, static_cast<double>(p.blp[q]), p.adv[q / p.C], p.w,
-                                    p.clip_eps, p.kl_coeff);
-        const double c = ct.coeff;
-        if (r % T == 0) {
-          p.lp_chunk[q] = lp;
-          p.coeff[q] = c;
+        for (int m = 0; m < 4; ++m) {
+          const int64_t t = 32 * m + lane;
+          vals[m] = (t < T) ? __ldcg(lt + t) : 0.0;
         }
-        uint32_t mode;
-        if (c == 0.0) {
-          mode = 0u;
-        } else if (!isfinite(c)) {
-          mode = 2u;
-        } else {
-          mode = 1u | ((c > 0.0) ? 0x80000000u : 0u);
-          S.kval[s] = static_cast<float>(S.lse[s] * 1.4426950408889634 - log2(fabs(c)));
+        const double lp = warp_pairwise_small(vals, static_cast<int>(T), lane);
+        if (lane == 0) {
+          const double lse = __ldcg(p.lse + r);
+          const int32_t tgt = __ldg(p.tokens + r);
+          ChunkTerms ct = chunk_terms(lp, static_cast<double>(p.blp[q]), p.adv[q / p.C], p.w,
+                                      p.clip_eps, p.kl_coeff);
+          const double c = ct.coeff;
+          if (r % T == 0) {
+            p.lp_chunk[q] = lp;
+            p.coeff[q] = c;
+          }
+          uint32_t mode;
+          if (c == 0.0) {
+            mode = 0u;
+          } else if (!isfinite(c)) {
+            mode = 2u;
+          } else {
+            mode = 1u | ((c > 0.0) ? 0x80000000u : 0u);
+            S.kval[s] = static_cast<float>(lse * 1.4426950408889634 - log2(fabs(c)));
+          }
+          S.mode[s] = mode;
+          S.cf[s] = static_cast<float>(c);
+          S.lseL[s] = static_cast<float>(lse * 1.4426950408889634);
+          S.tgt[s] = (tgt >= 0 && tgt < V) ? tgt : -1;
+          mbar_arrive(&S.cfull[s]);
         }
-        S.mode[s] = mode;
-        S.cf[s] = static_cast<float>(c);
-        mbar_arrive(&S.cfull[s]);
+        __syncwarp();
       }
-      __syncwarp();
-    };
-    if (nloc > 0) tail(0);
-    for (int64_t k = 0; k < nloc; ++k) {
-      if (k + 1 < nloc) tail(k + 1);
-      if (write_dl) coef(k);
     }
     return;
   }
 
   // ------------------------------------------------------- compute warps
   const int nvec = static_cast<int>(V >> 3);  // uint4 = 8 bf16
-  auto phaseA = [&](int64_t k) {
-    const int s = static_cast<int>(k % kFusedStages);
-    const uint32_t ph = static_cast<uint32_t>((k / kFusedStages) & 1);
+  for (int64_t n = 0; n < nops; ++n) {
+    const int s = static_cast<int>(n % kFusedStages);
+    const uint32_t ph = static_cast<uint32_t>((n / kFusedStages) & 1);
+    bool isB;
+    int64_t k;
+    op_of(n, nloc, L, &isB, &k);
     mbar_wait(&S.full[s], ph);
-    const uint4* v = reinterpret_cast<const uint4*>(buf(s));
-    uint32_t mx0 = 0xff80ff80u, mx1 = 0xff80ff80u;
+    if (!isB) {
+      const uint4* v = reinterpret_cast<const uint4*>(buf(s));
+      uint32_t mx0 = 0xff80ff80u, mx1 = 0xff80ff80u;
 #pragma unroll 4
-    for (int i = tid; i < nvec; i += kFusedComputeThreads) {
-      const uint4 x = v[i];
-      mx0 = bf16x2_max(mx0, bf16x2_max(x.x, x.y));
-      mx1 = bf16x2_max(mx1, bf16x2_max(x.z, x.w));
-    }
-    const uint32_t mx = bf16x2_max(mx0, mx1);
-    const float m = warp_max_f32(fmaxf(bf16lo(mx), bf16hi(mx)));
-    const float mL = m * kLog2e;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      for (int i = tid; i < nvec; i += kFusedComputeThreads) {
+        const uint4 x = v[i];
+        mx0 = bf16x2_max(mx0, bf16x2_max(x.x, x.y));
+        mx1 = bf16x2_max(mx1, bf16x2_max(x.z, x.w));
+      }
+      const uint32_t mx = bf16x2_max(mx0, mx1);
+      const float m = warp_max_f32(fmaxf(bf16lo(mx), bf16hi(mx)));
+      const float mL = m * kLog2e;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll 2
-    for (int i = tid; i < nvec; i += kFusedComputeThreads) {
-      const uint4 x = v[i];
-      s0 += ex2f(fmaf(bf16lo(x.x), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.x), kLog2e, -mL));
-      s1 += ex2f(fmaf(bf16lo(x.y), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.y), kLog2e, -mL));
-      s2 += ex2f(fmaf(bf16lo(x.z), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.z), kLog2e, -mL));
-      s3 += ex2f(fmaf(bf16lo(x.w), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.w), kLog2e, -mL));
+      for (int i = tid; i < nvec; i += kFusedComputeThreads) {
+        const uint4 x = v[i];
+        s0 += ex2f(fmaf(bf16lo(x.x), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.x), kLog2e, -mL));
+        s1 += ex2f(fmaf(bf16lo(x.y), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.y), kLog2e, -mL));
+        s2 += ex2f(fmaf(bf16lo(x.z), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.z), kLog2e, -mL));
+        s3 += ex2f(fmaf(bf16lo(x.w), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.w), kLog2e, -mL));
+      }
+      double part = (static_cast<double>(s0) + static_cast<double>(s1)) +
+                    (static_cast<double>(s2) + static_cast<double>(s3));
+      part = warp_sum_f64(part);
+      if (lane == 0) {
+        S.wm[s][warp] = m;
+        S.ws[s][warp] = part;
+        mbar_arrive(&S.adone[s]);
+      }
+      continue;
     }
-    double part = (static_cast<double>(s0) + static_cast<double>(s1)) +
-                  (static_cast<double>(s2) + static_cast<double>(s3));
-    part = warp_sum_f64(part);
-    if (lane == 0) {
-      S.wm[s][warp] = m;
-      S.ws[s][warp] = part;
-      mbar_arrive(&S.adone[s]);
-    }
-  };
-
-  auto phaseB = [&](int64_t k) {
-    const int s = static_cast<int>(k % kFusedStages);
-    const uint32_t ph = static_cast<uint32_t>((k / kFusedStages) & 1);
     mbar_wait(&S.cfull[s], ph);
     const uint32_t mode = S.mode[s];
     uint4* v = reinterpret_cast<uint4*>(buf(s));
@@ -401,17 +451,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     }
     fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&S.done[s]);
-  };
-
-  if (!write_dl) {
-    for (int64_t k = 0; k < nloc; ++k) phaseA(k);
-    return;
-  }
-  if (nloc > 0) phaseA(0);
-  for (int64_t k = 0; k < nloc; ++k) {
-    if (k + 1 < nloc) phaseA(k + 1);
-    phaseB(k);
+    if (lane == 0) mbar_arrive(&S.adone[s]);
   }
 }
 
