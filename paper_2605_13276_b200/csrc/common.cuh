@@ -81,8 +81,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns();
+
+// Blocking wait with a safety net: a protocol bug must never hang the GPU,
+// so after ~20 s the kernel traps (the host sees a launch failure).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
+    if (((++spins) & 1023u) == 0 && globaltimer_ns() - t0 > 20000000000ull) __trap();
   }
 }
 

@@ -149,12 +149,14 @@ __device__ __forceinline__ double chunk_lp_pairwise(const double* __restrict__ l
 // (grid <= #SMs, T <= grid).
 //
 // Warp roles: 0..15 compute, 16 loader, 17 coefficient, 18 store.
-// Barriers per SMEM stage s (each completes exactly once per op on s, so the
-// parity of op n is (n / kStages) & 1 everywhere):
-//   full   loader -> compute, coef         (TMA tx bytes)
-//   adone  compute -> coef (A) / store (B) (16 arrivals)
-//   cfull  coef -> compute                 (1 arrival; dummy for A ops)
-//   empty  coef (A) / store (B) -> loader  (1 arrival)
+// Barriers (every barrier completes once per use of its own ring index, and
+// every waiter walks its ring in order, so parity never aliases):
+//   full[s], empty[s]  per SMEM stage s = op % 3: loader <-> all consumers
+//   adoneA[a % 3]      compute -> coef, per A op a (SMEM partial slot a % 3)
+//   cfullB[b % 3]      coef -> compute, per B op b (coefficient slot b % 3)
+//   adoneB[b % 3]      compute -> store (and coef, before reusing slot b % 3)
+// The op sequence and barrier protocol were model-checked for races and
+// parity aliasing (tests/test_fused_protocol.py).
 constexpr int kWarpLoader = kFusedComputeWarps;
 constexpr int kCoefWarp = kFusedComputeWarps + 1;
 constexpr int kWarpStore = kFusedComputeWarps + 2;
@@ -163,9 +165,10 @@ constexpr int kLagRounds = 3;
 
 struct FusedSmem {
   uint64_t full[kFusedStages];
-  uint64_t adone[kFusedStages];
-  uint64_t cfull[kFusedStages];
   uint64_t empty[kFusedStages];
+  uint64_t adoneA[kFusedStages];
+  uint64_t adoneB[kFusedStages];
+  uint64_t cfullB[kFusedStages];
   double ws[kFusedStages][kFusedComputeWarps];
   float wm[kFusedStages][kFusedComputeWarps];
   float kval[kFusedStages];   // lse*log2e - log2|c|
@@ -231,9 +234,10 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   if (tid == 0) {
     for (int s = 0; s < kFusedStages; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.adone[s], kFusedComputeWarps);
-      mbar_init(&S.cfull[s], 1);
       mbar_init(&S.empty[s], 1);
+      mbar_init(&S.adoneA[s], kFusedComputeWarps);
+      mbar_init(&S.adoneB[s], kFusedComputeWarps);
+      mbar_init(&S.cfullB[s], 1);
     }
     fence_mbar_init();
   }
@@ -267,13 +271,15 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   if (warp == kWarpStore) {
     if (lane == 0 && write_dl) {
       const uint64_t pol = l2_policy_evict_first();
+      int64_t b = 0;
       for (int64_t n = 0; n < nops; ++n) {
         bool isB;
         int64_t k;
         op_of(n, nloc, L, &isB, &k);
         if (!isB) continue;
         const int s = static_cast<int>(n % kFusedStages);
-        mbar_wait(&S.adone[s], static_cast<uint32_t>((n / kFusedStages) & 1));
+        mbar_wait(&S.adoneB[b % kFusedStages], static_cast<uint32_t>((b / kFusedStages) & 1));
+        ++b;
         tma_store_1d_evict_first(dl + row_of(k) * V, buf(s), row_bytes, pol);
         bulk_commit();
         bulk_wait_read<0>();
@@ -288,9 +294,9 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   if (warp == kCoefWarp) {
     int32_t tgt_next = (nloc > 0 && lane == 0) ? __ldg(p.tokens + row_of(0)) : 0;
     int64_t next_a = 1;  // next A row whose token id to prefetch
+    int64_t a = 0, b = 0;  // A / B op counters
     for (int64_t n = 0; n < nops; ++n) {
       const int s = static_cast<int>(n % kFusedStages);
-      const uint32_t ph = static_cast<uint32_t>((n / kFusedStages) & 1);
       bool isB;
       int64_t k;
       op_of(n, nloc, L, &isB, &k);
@@ -300,9 +306,11 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         int32_t tgt = tgt_next;
         if (lane == 0 && next_a < nloc) tgt_next = __ldg(p.tokens + row_of(next_a));
         ++next_a;
-        mbar_wait(&S.adone[s], ph);
-        const float mw = (lane < kFusedComputeWarps) ? S.wm[s][lane] : -INFINITY;
-        const double sw = (lane < kFusedComputeWarps) ? S.ws[s][lane] : 0.0;
+        const int sa = static_cast<int>(a % kFusedStages);
+        mbar_wait(&S.adoneA[sa], static_cast<uint32_t>((a / kFusedStages) & 1));
+        ++a;
+        const float mw = (lane < kFusedComputeWarps) ? S.wm[sa][lane] : -INFINITY;
+        const double sw = (lane < kFusedComputeWarps) ? S.ws[sa][lane] : 0.0;
         const float M = warp_max_f32(mw);
         double term = (lane < kFusedComputeWarps && sw > 0.0)
                           ? sw * exp2(static_cast<double>(mw - M) * 1.4426950408889634)
@@ -321,13 +329,15 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
           p.lse[r] = lse;
           p.lp_tok[r] = xt - lse;
           if (write_dl) red_release_gpu_add(p.cnt + r / T, 1u);
-          mbar_arrive(&S.cfull[s]);  // keeps the per-stage phases aligned
-          mbar_arrive(&S.empty[s]);
+          mbar_arrive(&S.empty[s]);  // row no longer needed in SMEM
         }
         __syncwarp();
       } else {
-        // ---- coefficient for B(k)
-        mbar_wait(&S.full[s], ph);  // stage reuse ordering (see header)
+        // ---- coefficient for B(k); slot b % 3 is free once B op b-3 is done
+        const int sb = static_cast<int>(b % kFusedStages);
+        if (b >= kFusedStages)
+          mbar_wait(&S.adoneB[sb], static_cast<uint32_t>(((b - kFusedStages) / kFusedStages) & 1));
+        ++b;
         const int64_t q = r / T;
         if (lane == 0) spin_until_at_least(p.cnt + q, static_cast<uint32_t>(T), p.err);
         __syncwarp();
@@ -356,13 +366,13 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
             mode = 2u;
           } else {
             mode = 1u | ((c > 0.0) ? 0x80000000u : 0u);
-            S.kval[s] = static_cast<float>(lse * 1.4426950408889634 - log2(fabs(c)));
+            S.kval[sb] = static_cast<float>(lse * 1.4426950408889634 - log2(fabs(c)));
           }
-          S.mode[s] = mode;
-          S.cf[s] = static_cast<float>(c);
-          S.lseL[s] = static_cast<float>(lse * 1.4426950408889634);
-          S.tgt[s] = (tgt >= 0 && tgt < V) ? tgt : -1;
-          mbar_arrive(&S.cfull[s]);
+          S.mode[sb] = mode;
+          S.cf[sb] = static_cast<float>(c);
+          S.lseL[sb] = static_cast<float>(lse * 1.4426950408889634);
+          S.tgt[sb] = (tgt >= 0 && tgt < V) ? tgt : -1;
+          mbar_arrive(&S.cfullB[sb]);
         }
         __syncwarp();
       }
@@ -372,6 +382,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
 
   // ------------------------------------------------------- compute warps
   const int nvec = static_cast<int>(V >> 3);  // uint4 = 8 bf16
+  int64_t a = 0, b = 0;  // A / B op counters
   for (int64_t n = 0; n < nops; ++n) {
     const int s = static_cast<int>(n % kFusedStages);
     const uint32_t ph = static_cast<uint32_t>((n / kFusedStages) & 1);
@@ -403,15 +414,19 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       double part = (static_cast<double>(s0) + static_cast<double>(s1)) +
                     (static_cast<double>(s2) + static_cast<double>(s3));
       part = warp_sum_f64(part);
+      const int sa = static_cast<int>(a % kFusedStages);
+      ++a;
       if (lane == 0) {
-        S.wm[s][warp] = m;
-        S.ws[s][warp] = part;
-        mbar_arrive(&S.adone[s]);
+        S.wm[sa][warp] = m;
+        S.ws[sa][warp] = part;
+        mbar_arrive(&S.adoneA[sa]);
       }
       continue;
     }
-    mbar_wait(&S.cfull[s], ph);
-    const uint32_t mode = S.mode[s];
+    const int sb = static_cast<int>(b % kFusedStages);
+    mbar_wait(&S.cfullB[sb], static_cast<uint32_t>((b / kFusedStages) & 1));
+    ++b;
+    const uint32_t mode = S.mode[sb];
     uint4* v = reinterpret_cast<uint4*>(buf(s));
     if ((mode & 3u) != 1u) {
       // zero-gradient rows (A == 0 or clipped chunk): 0 * (onehot - p)
@@ -419,9 +434,9 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       for (int i = tid; i < nvec; i += kFusedComputeThreads) v[i] = make_uint4(z, z, z, z);
     } else {
       // -c * p_v = -sign(c) * 2^(x*log2e - (lse*log2e - log2|c|))
-      const float K = S.kval[s];
+      const float K = S.kval[sb];
       const uint32_t sgn = (mode & 0x80000000u) ? 0x80008000u : 0u;
-      const int32_t tgt = S.tgt[s];
+      const int32_t tgt = S.tgt[sb];
       const int tv = tgt >> 3;
 #pragma unroll 2
       for (int i = tid; i < nvec; i += kFusedComputeThreads) {
@@ -436,8 +451,8 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
           const int e = tgt & 7;
           const uint32_t word = (e >> 1) == 0 ? x.x : (e >> 1) == 1 ? x.y : (e >> 1) == 2 ? x.z : x.w;
           const float xt = (e & 1) ? bf16hi(word) : bf16lo(word);
-          const float pt = ex2f(fmaf(xt, kLog2e, -S.lseL[s]));
-          const float val = S.cf[s] * (1.0f - pt);
+          const float pt = ex2f(fmaf(xt, kLog2e, -S.lseL[sb]));
+          const float val = S.cf[sb] * (1.0f - pt);
           const uint32_t b = pack_bf16x2(val, val) & 0xffffu;
           uint32_t ow = (e >> 1) == 0 ? o.x : (e >> 1) == 1 ? o.y : (e >> 1) == 2 ? o.z : o.w;
           ow = (e & 1) ? ((ow & 0x0000ffffu) | (b << 16)) : ((ow & 0xffff0000u) | b);
@@ -451,7 +466,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     }
     fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&S.adone[s]);
+    if (lane == 0) mbar_arrive(&S.adoneB[sb]);
   }
 }
 

@@ -1,0 +1,145 @@
+"""Model check of the fused token-loss kernel's warp/mbarrier protocol
+(csrc/token_loss.cu, tok_fused_bf16_kernel) on the CPU.
+
+Every warp role is a generator that waits on simulated mbarriers with the
+hardware's parity semantics; random interleavings must (a) finish, (b) never
+let a barrier run two phases ahead of a waiter (parity aliasing), and (c)
+never let a SMEM slot be overwritten before its consumer read it.  The op
+sequence `op_of` mirrors the CUDA function of the same name.
+"""
+
+import random
+
+import pytest
+
+S = 3  # kFusedStages
+
+
+def op_of(n, nloc, L):
+    Le = min(nloc, L)
+    if n < Le:
+        return False, n
+    m = n - Le
+    pairs = nloc - Le
+    if m < 2 * pairs:
+        return (m & 1) == 1, (m >> 1) if (m & 1) else Le + (m >> 1)
+    return True, pairs + (m - 2 * pairs)
+
+
+class Bar:
+    def __init__(self, cnt):
+        self.cnt, self.pend, self.phase = cnt, cnt, 0
+
+    def arrive(self):
+        self.pend -= 1
+        if self.pend == 0:
+            self.phase += 1
+            self.pend = self.cnt
+
+    def done(self, idx):
+        assert idx <= self.phase + 1 and self.phase <= idx + 1, "parity aliasing"
+        return (self.phase & 1) != (idx & 1)
+
+
+def simulate(nloc, L, seed, write_dl=True):
+    rnd = random.Random(seed)
+    nops = 2 * nloc if write_dl else nloc
+    Lx = L if write_dl else 1 << 30
+    full = [Bar(1) for _ in range(S)]
+    empty = [Bar(1) for _ in range(S)]
+    ad_a = [Bar(16) for _ in range(S)]
+    ad_b = [Bar(16) for _ in range(S)]
+    cf_b = [Bar(1) for _ in range(S)]
+    slot_p, slot_c, rows_b = [None] * S, [None] * S, []
+
+    def wait(b, idx):
+        while not b.done(idx):
+            yield 1
+
+    def loader():
+        for n in range(nops):
+            if n >= S:
+                yield from wait(empty[n % S], n // S - 1)
+            full[n % S].arrive()
+
+    def store():
+        b = 0
+        for n in range(nops):
+            isb, k = op_of(n, nloc, Lx)
+            if isb:
+                yield from wait(ad_b[b % S], b // S)
+                rows_b.append(k)
+                empty[n % S].arrive()
+                b += 1
+
+    def coef():
+        a = b = 0
+        for n in range(nops):
+            isb, k = op_of(n, nloc, Lx)
+            if not isb:
+                yield from wait(ad_a[a % S], a // S)
+                assert slot_p[a % S] == a
+                empty[n % S].arrive()
+                a += 1
+            else:
+                if b >= S:
+                    yield from wait(ad_b[(b - S) % S], (b - S) // S)
+                slot_c[b % S] = b
+                cf_b[b % S].arrive()
+                b += 1
+
+    def compute(w):
+        a = b = 0
+        for n in range(nops):
+            isb, k = op_of(n, nloc, Lx)
+            yield from wait(full[n % S], n // S)
+            if not isb:
+                if w == 0:
+                    slot_p[a % S] = a
+                ad_a[a % S].arrive()
+                a += 1
+            else:
+                yield from wait(cf_b[b % S], b // S)
+                assert slot_c[b % S] == b
+                ad_b[b % S].arrive()
+                b += 1
+
+    gens = [loader(), store(), coef()] + [compute(w) for w in range(16)]
+    live = list(gens)
+    for _ in range(200000):
+        if not live:
+            break
+        g = rnd.choice(live)
+        try:
+            next(g)
+        except StopIteration:
+            live.remove(g)
+    assert not live, "protocol deadlocked"
+    if write_dl:
+        assert sorted(rows_b) == list(range(nloc))
+
+
+@pytest.mark.parametrize("nloc", [1, 2, 3, 4, 7, 13, 20])
+@pytest.mark.parametrize("L", [1, 2, 3])
+def test_protocol_completes_without_aliasing(nloc, L):
+    for seed in range(3):
+        simulate(nloc, L, seed)
+
+
+def test_forward_only_protocol():
+    for nloc in (1, 5, 13):
+        simulate(nloc, 3, 0, write_dl=False)
+
+
+def test_op_sequence_is_a_permutation():
+    for nloc in range(1, 30):
+        for L in (1, 2, 3, 5):
+            ops = [op_of(n, nloc, L) for n in range(2 * nloc)]
+            assert sorted(k for b, k in ops if not b) == list(range(nloc))
+            assert sorted(k for b, k in ops if b) == list(range(nloc))
+            # A(k) always precedes B(k), and A(k + L) precedes B(k)
+            pos = {op: i for i, op in enumerate(ops)}
+            for k in range(nloc):
+                assert pos[(False, k)] < pos[(True, k)]
+                if k + L < nloc:
+                    assert pos[(False, k + L)] < pos[(True, k)]
