@@ -162,6 +162,7 @@ constexpr int kCoefWarp = kFusedComputeWarps + 1;
 constexpr int kWarpStore = kFusedComputeWarps + 2;
 constexpr int kFusedThreadsWS = (kFusedComputeWarps + 3) * 32;
 constexpr int kLagRounds = 3;
+constexpr int kRing = 8;  // > kLagRounds + 1 rows of (lse, target) in flight
 
 struct FusedSmem {
   uint64_t full[kFusedStages];
@@ -176,7 +177,29 @@ struct FusedSmem {
   float cf[kFusedStages];     // coefficient (f32)
   uint32_t mode[kFusedStages];  // 0 zero row, 1 finite c (bit 31: c > 0), 2 non-finite c
   int32_t tgt[kFusedStages];
+  double ring_lse[kRing];
+  int32_t ring_tgt[kRing];
 };
+
+// coefficient not yet published (the workspace is memset to 0xff)
+constexpr unsigned long long kCoeffPending = 0xffffffffffffffffull;
+
+__device__ __forceinline__ unsigned long long spin_coeff(const unsigned long long* c,
+                                                         uint32_t* err) {
+  unsigned long long v = ld_acquire_gpu_u64(c);
+  if (v != kCoeffPending) return v;
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t ns = 32;
+  while ((v = ld_acquire_gpu_u64(c)) == kCoeffPending) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+    if (globaltimer_ns() - t0 > kSpinTimeoutNs) {
+      atomicOr(err, kErrTimeout);
+      return 0x7ff8000000000000ull;
+    }
+  }
+  return v;
+}
 
 __device__ __forceinline__ bool spin_until_at_least(const uint32_t* cnt, uint32_t target,
                                                     uint32_t* err) {
@@ -292,15 +315,46 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
 
   // ---------------------------------------------------- coefficient warp
   if (warp == kCoefWarp) {
+    // Per-row ring (lse, target id) carried from A(k) to B(k), L ops later.
+    double* ring_lse = S.ring_lse;
+    int32_t* ring_tgt = S.ring_tgt;
     int32_t tgt_next = (nloc > 0 && lane == 0) ? __ldg(p.tokens + row_of(0)) : 0;
-    int64_t next_a = 1;  // next A row whose token id to prefetch
-    int64_t a = 0, b = 0;  // A / B op counters
+    int64_t next_a = 1;          // next A row whose token id to prefetch
+    int64_t a = 0, b = 0;        // A / B op counters
+    uint32_t pend_old = 0;       // chunk counter value returned to the last tail
+    int64_t pend_q = -1;         // ... for this chunk (finalised lazily)
+    unsigned long long pref = kCoeffPending;  // prefetched coefficient bits
+    int64_t pref_q = -1;
+    auto finalize = [&](int64_t q) {
+      // last row of chunk q published: lp, rho, coefficient (grpo.py:252-268)
+      const double* lt = p.lp_tok + q * T;
+      double vals[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int64_t t = 32 * m + lane;
+        vals[m] = (t < T) ? __ldcg(lt + t) : 0.0;
+      }
+      const double lp = warp_pairwise_small(vals, static_cast<int>(T), lane);
+      if (lane == 0) {
+        ChunkTerms ct = chunk_terms(lp, static_cast<double>(p.blp[q]), p.adv[q / p.C], p.w,
+                                    p.clip_eps, p.kl_coeff);
+        p.lp_chunk[q] = lp;
+        st_release_gpu_u64(reinterpret_cast<unsigned long long*>(p.coeff + q),
+                           static_cast<unsigned long long>(__double_as_longlong(ct.coeff)));
+      }
+      __syncwarp();
+    };
     for (int64_t n = 0; n < nops; ++n) {
       const int s = static_cast<int>(n % kFusedStages);
       bool isB;
       int64_t k;
       op_of(n, nloc, L, &isB, &k);
       const int64_t r = row_of(k);
+      // the previous tail's atomic result is consumed one op later, so its
+      // round trip overlaps this op's waits
+      const int64_t chk_q = pend_q;
+      const uint32_t chk_old = pend_old;
+      pend_q = -1;
       if (!isB) {
         // ---- tail of A(k): lse, lp_tok, chunk counter
         int32_t tgt = tgt_next;
@@ -322,15 +376,22 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
           if (tgt < 0 || tgt >= V) {
             atomicOr(p.err, kErrToken);
             xt = __longlong_as_double(0x7ff8000000000000ll);
+            tgt = -1;
           } else {
             xt = static_cast<double>(__bfloat162float(
                 reinterpret_cast<const __nv_bfloat16*>(buf(s))[tgt]));
           }
-          p.lse[r] = lse;
-          p.lp_tok[r] = xt - lse;
-          if (write_dl) red_release_gpu_add(p.cnt + r / T, 1u);
           mbar_arrive(&S.empty[s]);  // row no longer needed in SMEM
+          p.lp_tok[r] = xt - lse;
+          if (write_dl) {
+            ring_lse[k % kRing] = lse;
+            ring_tgt[k % kRing] = tgt;
+            pend_old = atom_add_acq_rel_gpu(p.cnt + r / T, 1u);  // consumed next op
+          } else {
+            p.lse[r] = lse;
+          }
         }
+        if (write_dl) pend_q = r / T;
         __syncwarp();
       } else {
         // ---- coefficient for B(k); slot b % 3 is free once B op b-3 is done
@@ -339,26 +400,13 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
           mbar_wait(&S.adoneB[sb], static_cast<uint32_t>(((b - kFusedStages) / kFusedStages) & 1));
         ++b;
         const int64_t q = r / T;
-        if (lane == 0) spin_until_at_least(p.cnt + q, static_cast<uint32_t>(T), p.err);
-        __syncwarp();
-        const double* lt = p.lp_tok + q * T;
-        double vals[4];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const int64_t t = 32 * m + lane;
-          vals[m] = (t < T) ? __ldcg(lt + t) : 0.0;
-        }
-        const double lp = warp_pairwise_small(vals, static_cast<int>(T), lane);
         if (lane == 0) {
-          const double lse = __ldcg(p.lse + r);
-          const int32_t tgt = __ldg(p.tokens + r);
-          ChunkTerms ct = chunk_terms(lp, static_cast<double>(p.blp[q]), p.adv[q / p.C], p.w,
-                                      p.clip_eps, p.kl_coeff);
-          const double c = ct.coeff;
-          if (r % T == 0) {
-            p.lp_chunk[q] = lp;
-            p.coeff[q] = c;
-          }
+          unsigned long long bits = (pref_q == q) ? pref : kCoeffPending;
+          if (bits == kCoeffPending)
+            bits = spin_coeff(reinterpret_cast<const unsigned long long*>(p.coeff + q), p.err);
+          const double c = __longlong_as_double(static_cast<long long>(bits));
+          const double lse = ring_lse[k % kRing];
+          const int32_t tgt = ring_tgt[k % kRing];
           uint32_t mode;
           if (c == 0.0) {
             mode = 0u;
@@ -371,11 +419,24 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
           S.mode[sb] = mode;
           S.cf[sb] = static_cast<float>(c);
           S.lseL[sb] = static_cast<float>(lse * 1.4426950408889634);
-          S.tgt[sb] = (tgt >= 0 && tgt < V) ? tgt : -1;
+          S.tgt[sb] = tgt;
           mbar_arrive(&S.cfullB[sb]);
+          // prefetch the next B row's chunk coefficient (ready long before use)
+          if (k + 1 < nloc) {
+            pref_q = row_of(k + 1) / T;
+            pref = ld_acquire_gpu_u64(reinterpret_cast<const unsigned long long*>(p.coeff + pref_q));
+          }
         }
         __syncwarp();
       }
+      if (write_dl && chk_q >= 0) {
+        const uint32_t old = __shfl_sync(0xffffffffu, chk_old, 0);
+        if (old == static_cast<uint32_t>(T - 1)) finalize(chk_q);
+      }
+    }
+    if (write_dl && pend_q >= 0) {
+      const uint32_t old = __shfl_sync(0xffffffffu, pend_old, 0);
+      if (old == static_cast<uint32_t>(T - 1)) finalize(pend_q);
     }
     return;
   }
@@ -845,6 +906,8 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
                                          227 * 1024));
       attr_set[dev & 63] = true;
     }
+    if (want_dl)  // chunk coefficients start as "pending" (all-ones bit pattern)
+      DVLA_CUDA_TRY(cudaMemsetAsync(ws.coeff, 0xff, static_cast<size_t>(nq) * 8, stream));
     const unsigned grid = static_cast<unsigned>(R < sms ? R : sms);
     const uint32_t stage_bytes = static_cast<uint32_t>(((V * 2 + 127) / 128) * 128);
     cudaEvent_t stop;
