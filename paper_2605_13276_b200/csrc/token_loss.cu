@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       }
       __syncwarp();
     };
-    for (int64_t n = 0; n < nops; ++n) {
+    auto process = [&](int64_t n) {
       const int s = static_cast<int>(n % kFusedStages);
       bool isB;
       int64_t k;
@@ -355,6 +355,12 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       const int64_t chk_q = pend_q;
       const uint32_t chk_old = pend_old;
       pend_q = -1;
+      auto check_pending = [&]() {
+        if (write_dl && chk_q >= 0) {
+          const uint32_t old = __shfl_sync(0xffffffffu, chk_old, 0);
+          if (old == static_cast<uint32_t>(T - 1)) finalize(chk_q);
+        }
+      };
       if (!isB) {
         // ---- tail of A(k): lse, lp_tok, chunk counter
         int32_t tgt = tgt_next;
@@ -393,12 +399,14 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         }
         if (write_dl) pend_q = r / T;
         __syncwarp();
+        check_pending();
       } else {
         // ---- coefficient for B(k); slot b % 3 is free once B op b-3 is done
         const int sb = static_cast<int>(b % kFusedStages);
         if (b >= kFusedStages)
           mbar_wait(&S.adoneB[sb], static_cast<uint32_t>(((b - kFusedStages) / kFusedStages) & 1));
         ++b;
+        check_pending();  // before any cross-CTA wait: finalisers never block
         const int64_t q = r / T;
         if (lane == 0) {
           unsigned long long bits = (pref_q == q) ? pref : kCoeffPending;
@@ -429,9 +437,22 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         }
         __syncwarp();
       }
-      if (write_dl && chk_q >= 0) {
-        const uint32_t old = __shfl_sync(0xffffffffu, chk_old, 0);
-        if (old == static_cast<uint32_t>(T - 1)) finalize(chk_q);
+    };
+    // B(k) is handled before the A(k+L) that precedes it in the op sequence:
+    // its coefficient does not depend on that A, so the compute warps find
+    // it ready when they finish A(k+L) (tests/test_fused_protocol.py).
+    for (int64_t n = 0; n < nops;) {
+      bool isB0, isB1 = false;
+      int64_t k0, k1;
+      op_of(n, nloc, L, &isB0, &k0);
+      if (n + 1 < nops) op_of(n + 1, nloc, L, &isB1, &k1);
+      if (!isB0 && isB1) {
+        process(n + 1);
+        process(n);
+        n += 2;
+      } else {
+        process(n);
+        n += 1;
       }
     }
     if (write_dl && pend_q >= 0) {

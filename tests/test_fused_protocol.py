@@ -41,6 +41,24 @@ class Bar:
         return (self.phase & 1) != (idx & 1)
 
 
+def coef_order(nops, nloc, L):
+    """The coefficient warp handles B(k) before the A(k+L) that precedes it
+    in the op sequence (its coefficient never depends on that A), so the
+    compute warps never wait for the tail of the row they just finished."""
+    order = []
+    n = 0
+    while n < nops:
+        isb, _ = op_of(n, nloc, L)
+        nxt = op_of(n + 1, nloc, L)[0] if n + 1 < nops else None
+        if not isb and nxt:
+            order += [n + 1, n]
+            n += 2
+        else:
+            order.append(n)
+            n += 1
+    return order
+
+
 def simulate(nloc, L, seed, write_dl=True):
     rnd = random.Random(seed)
     nops = 2 * nloc if write_dl else nloc
@@ -74,7 +92,7 @@ def simulate(nloc, L, seed, write_dl=True):
 
     def coef():
         a = b = 0
-        for n in range(nops):
+        for n in coef_order(nops, nloc, Lx):
             isb, k = op_of(n, nloc, Lx)
             if not isb:
                 yield from wait(ad_a[a % S], a // S)
@@ -129,6 +147,12 @@ def test_protocol_completes_without_aliasing(nloc, L):
 def test_forward_only_protocol():
     for nloc in (1, 5, 13):
         simulate(nloc, 3, 0, write_dl=False)
+
+
+def test_coef_order_is_a_permutation():
+    for nloc in range(1, 20):
+        for L in (1, 2, 3):
+            assert sorted(coef_order(2 * nloc, nloc, L)) == list(range(2 * nloc))
 
 
 def test_op_sequence_is_a_permutation():
