@@ -161,7 +161,7 @@ constexpr int kWarpLoader = kFusedComputeWarps;
 constexpr int kCoefWarp = kFusedComputeWarps + 1;
 constexpr int kWarpStore = kFusedComputeWarps + 2;
 constexpr int kFusedThreadsWS = (kFusedComputeWarps + 3) * 32;
-constexpr int kLagRounds = 3;
+constexpr int kLagRounds = 4;
 constexpr int kRing = 8;  // > kLagRounds + 1 rows of (lse, target) in flight
 
 struct FusedSmem {
@@ -321,8 +321,8 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     int32_t tgt_next = (nloc > 0 && lane == 0) ? __ldg(p.tokens + row_of(0)) : 0;
     int64_t next_a = 1;          // next A row whose token id to prefetch
     int64_t a = 0, b = 0;        // A / B op counters
-    uint32_t pend_old = 0;       // chunk counter value returned to the last tail
-    int64_t pend_q = -1;         // ... for this chunk (finalised lazily)
+    uint32_t pend_old = 0;       // chunk counter value returned to the last A tail
+    int64_t pend_q = -1;         // ... for this chunk (finalised at the next A op)
     unsigned long long pref = kCoeffPending;  // prefetched coefficient bits
     int64_t pref_q = -1;
     auto finalize = [&](int64_t q) {
@@ -339,8 +339,12 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         ChunkTerms ct = chunk_terms(lp, static_cast<double>(p.blp[q]), p.adv[q / p.C], p.w,
                                     p.clip_eps, p.kl_coeff);
         p.lp_chunk[q] = lp;
-        st_release_gpu_u64(reinterpret_cast<unsigned long long*>(p.coeff + q),
-                           static_cast<unsigned long long>(__double_as_longlong(ct.coeff)));
+        // the GPU's default f64 NaN is all-ones == the "pending" sentinel:
+        // publish non-finite coefficients as a quiet NaN with another payload
+        const unsigned long long bits =
+            isnan(ct.coeff) ? 0x7ff8000000000000ull
+                            : static_cast<unsigned long long>(__double_as_longlong(ct.coeff));
+        st_release_gpu_u64(reinterpret_cast<unsigned long long*>(p.coeff + q), bits);
       }
       __syncwarp();
     };
@@ -352,13 +356,11 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       const int64_t r = row_of(k);
       // the previous tail's atomic result is consumed one op later, so its
       // round trip overlaps this op's waits
-      const int64_t chk_q = pend_q;
-      const uint32_t chk_old = pend_old;
-      pend_q = -1;
       auto check_pending = [&]() {
-        if (write_dl && chk_q >= 0) {
-          const uint32_t old = __shfl_sync(0xffffffffu, chk_old, 0);
-          if (old == static_cast<uint32_t>(T - 1)) finalize(chk_q);
+        if (write_dl && pend_q >= 0) {
+          const uint32_t old = __shfl_sync(0xffffffffu, pend_old, 0);
+          if (old == static_cast<uint32_t>(T - 1)) finalize(pend_q);
+          pend_q = -1;
         }
       };
       if (!isB) {
@@ -369,6 +371,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         const int sa = static_cast<int>(a % kFusedStages);
         mbar_wait(&S.adoneA[sa], static_cast<uint32_t>((a / kFusedStages) & 1));
         ++a;
+        check_pending();  // atomic of the previous A tail: returned long ago
         const float mw = (lane < kFusedComputeWarps) ? S.wm[sa][lane] : -INFINITY;
         const double sw = (lane < kFusedComputeWarps) ? S.ws[sa][lane] : 0.0;
         const float M = warp_max_f32(mw);
@@ -392,22 +395,28 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
           if (write_dl) {
             ring_lse[k % kRing] = lse;
             ring_tgt[k % kRing] = tgt;
-            pend_old = atom_add_acq_rel_gpu(p.cnt + r / T, 1u);  // consumed next op
+            pend_old = atom_add_acq_rel_gpu(p.cnt + r / T, 1u);  // consumed next A op
           } else {
             p.lse[r] = lse;
           }
         }
-        if (write_dl) pend_q = r / T;
         __syncwarp();
-        check_pending();
+        if (write_dl) pend_q = r / T;
+        // re-issue a coefficient prefetch that found the chunk still pending
+        if (write_dl && lane == 0 && pref_q >= 0 && pref == kCoeffPending)
+          pref = ld_acquire_gpu_u64(reinterpret_cast<const unsigned long long*>(p.coeff + pref_q));
       } else {
         // ---- coefficient for B(k); slot b % 3 is free once B op b-3 is done
         const int sb = static_cast<int>(b % kFusedStages);
         if (b >= kFusedStages)
           mbar_wait(&S.adoneB[sb], static_cast<uint32_t>(((b - kFusedStages) / kFusedStages) & 1));
         ++b;
-        check_pending();  // before any cross-CTA wait: finalisers never block
         const int64_t q = r / T;
+        // a finaliser must never block on another chunk: settle any pending
+        // finalisation duty before a (rare) spin on this chunk's coefficient
+        const bool need_spin =
+            __shfl_sync(0xffffffffu, (pref_q == q) ? (pref == kCoeffPending ? 1 : 0) : 1, 0) != 0;
+        if (need_spin) check_pending();
         if (lane == 0) {
           unsigned long long bits = (pref_q == q) ? pref : kCoeffPending;
           if (bits == kCoeffPending)
