@@ -54,6 +54,13 @@ struct TokParams {
 
 enum : uint32_t { kErrToken = 1u, kErrTimeout = 2u };
 
+// Optional per-role cycle counters for the fused kernel (set by
+// dvla_debug_fused_counters; null in normal runs -> no clock reads).
+__device__ unsigned long long* g_dbg = nullptr;
+#define DBG_T0() const long long _t0 = dbg ? clock64() : 0
+#define DBG_ADD(i) \
+  if (dbg) atomicAdd(dbg + (i), static_cast<unsigned long long>(clock64() - _t0))
+
 // ------------------------------------------------------------ advantages
 __global__ void tok_adv_kernel(const float* __restrict__ rewards, int64_t n_groups, int64_t G,
                                double delta, double* __restrict__ adv,
@@ -253,6 +260,8 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   auto row_of = [&](int64_t k) { return blockIdx.x + k * G; };
   auto buf = [&](int s) { return bufs + static_cast<size_t>(s) * stage_bytes; };
   const int64_t T = p.T;
+  unsigned long long* dbg = g_dbg;
+  const long long t_kernel = dbg ? clock64() : 0;
 
   if (tid == 0) {
     for (int s = 0; s < kFusedStages; ++s) {
@@ -275,8 +284,11 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       const uint64_t pol = l2_policy_evict_first();
       for (int64_t n = 0; n < nops; ++n) {
         const int s = static_cast<int>(n % kFusedStages);
-        if (n >= kFusedStages)
+        if (n >= kFusedStages) {
+          DBG_T0();
           mbar_wait(&S.empty[s], static_cast<uint32_t>(((n / kFusedStages) - 1) & 1));
+          DBG_ADD(8);
+        }
         bool isB;
         int64_t k;
         op_of(n, nloc, L, &isB, &k);
@@ -301,7 +313,11 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         op_of(n, nloc, L, &isB, &k);
         if (!isB) continue;
         const int s = static_cast<int>(n % kFusedStages);
-        mbar_wait(&S.adoneB[b % kFusedStages], static_cast<uint32_t>((b / kFusedStages) & 1));
+        {
+          DBG_T0();
+          mbar_wait(&S.adoneB[b % kFusedStages], static_cast<uint32_t>((b / kFusedStages) & 1));
+          DBG_ADD(9);
+        }
         ++b;
         tma_store_1d_evict_first(dl + row_of(k) * V, buf(s), row_bytes, pol);
         bulk_commit();
@@ -359,7 +375,11 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       auto check_pending = [&]() {
         if (write_dl && pend_q >= 0) {
           const uint32_t old = __shfl_sync(0xffffffffu, pend_old, 0);
-          if (old == static_cast<uint32_t>(T - 1)) finalize(pend_q);
+          if (old == static_cast<uint32_t>(T - 1)) {
+            DBG_T0();
+            finalize(pend_q);
+            if (lane == 0) { DBG_ADD(7); }
+          }
           pend_q = -1;
         }
       };
@@ -369,7 +389,12 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         if (lane == 0 && next_a < nloc) tgt_next = __ldg(p.tokens + row_of(next_a));
         ++next_a;
         const int sa = static_cast<int>(a % kFusedStages);
-        mbar_wait(&S.adoneA[sa], static_cast<uint32_t>((a / kFusedStages) & 1));
+        {
+          DBG_T0();
+          mbar_wait(&S.adoneA[sa], static_cast<uint32_t>((a / kFusedStages) & 1));
+          if (lane == 0) { DBG_ADD(2); }
+        }
+        const long long t_tail = dbg ? clock64() : 0;
         ++a;
         check_pending();  // atomic of the previous A tail: returned long ago
         const float mw = (lane < kFusedComputeWarps) ? S.wm[sa][lane] : -INFINITY;
@@ -402,14 +427,19 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         }
         __syncwarp();
         if (write_dl) pend_q = r / T;
+        if (dbg && lane == 0) atomicAdd(dbg + 3, static_cast<unsigned long long>(clock64() - t_tail));
         // re-issue a coefficient prefetch that found the chunk still pending
         if (write_dl && lane == 0 && pref_q >= 0 && pref == kCoeffPending)
           pref = ld_acquire_gpu_u64(reinterpret_cast<const unsigned long long*>(p.coeff + pref_q));
       } else {
         // ---- coefficient for B(k); slot b % 3 is free once B op b-3 is done
         const int sb = static_cast<int>(b % kFusedStages);
-        if (b >= kFusedStages)
+        if (b >= kFusedStages) {
+          DBG_T0();
           mbar_wait(&S.adoneB[sb], static_cast<uint32_t>(((b - kFusedStages) / kFusedStages) & 1));
+          if (lane == 0) { DBG_ADD(4); }
+        }
+        const long long t_prep = dbg ? clock64() : 0;
         ++b;
         const int64_t q = r / T;
         // a finaliser must never block on another chunk: settle any pending
@@ -419,8 +449,12 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         if (need_spin) check_pending();
         if (lane == 0) {
           unsigned long long bits = (pref_q == q) ? pref : kCoeffPending;
-          if (bits == kCoeffPending)
+          if (bits == kCoeffPending) {
+            DBG_T0();
             bits = spin_coeff(reinterpret_cast<const unsigned long long*>(p.coeff + q), p.err);
+            DBG_ADD(6);
+            if (dbg) atomicAdd(dbg + 11, 1ull);
+          }
           const double c = __longlong_as_double(static_cast<long long>(bits));
           const double lse = ring_lse[k % kRing];
           const int32_t tgt = ring_tgt[k % kRing];
@@ -438,6 +472,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
           S.lseL[sb] = static_cast<float>(lse * 1.4426950408889634);
           S.tgt[sb] = tgt;
           mbar_arrive(&S.cfullB[sb]);
+          if (dbg) atomicAdd(dbg + 5, static_cast<unsigned long long>(clock64() - t_prep));
           // prefetch the next B row's chunk coefficient (ready long before use)
           if (k + 1 < nloc) {
             pref_q = row_of(k + 1) / T;
@@ -450,12 +485,16 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     // B(k) is handled before the A(k+L) that precedes it in the op sequence:
     // its coefficient does not depend on that A, so the compute warps find
     // it ready when they finish A(k+L) (tests/test_fused_protocol.py).
+    // Only inside the paired region and with a lag >= 2: B(k) depends on the
+    // tails of rows k and k+1 (a chunk spans <= 2 rounds), never on A(k+Le).
+    const int64_t Le = nloc < L ? nloc : L;
+    const int64_t pair_end = Le + 2 * (nloc - Le);
     for (int64_t n = 0; n < nops;) {
       bool isB0, isB1 = false;
       int64_t k0, k1;
       op_of(n, nloc, L, &isB0, &k0);
       if (n + 1 < nops) op_of(n + 1, nloc, L, &isB1, &k1);
-      if (!isB0 && isB1) {
+      if (!isB0 && isB1 && Le >= 2 && n + 1 < pair_end) {
         process(n + 1);
         process(n);
         n += 2;
@@ -480,7 +519,11 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     bool isB;
     int64_t k;
     op_of(n, nloc, L, &isB, &k);
-    mbar_wait(&S.full[s], ph);
+    {
+      DBG_T0();
+      mbar_wait(&S.full[s], ph);
+      if (tid == 0) { DBG_ADD(0); }
+    }
     if (!isB) {
       const uint4* v = reinterpret_cast<const uint4*>(buf(s));
       uint32_t mx0 = 0xff80ff80u, mx1 = 0xff80ff80u;
@@ -515,7 +558,11 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       continue;
     }
     const int sb = static_cast<int>(b % kFusedStages);
-    mbar_wait(&S.cfullB[sb], static_cast<uint32_t>((b / kFusedStages) & 1));
+    {
+      DBG_T0();
+      mbar_wait(&S.cfullB[sb], static_cast<uint32_t>((b / kFusedStages) & 1));
+      if (tid == 0) { DBG_ADD(1); }
+    }
     ++b;
     const uint32_t mode = S.mode[sb];
     uint4* v = reinterpret_cast<uint4*>(buf(s));
@@ -559,6 +606,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.adoneB[sb]);
   }
+  if (dbg && tid == 0) atomicAdd(dbg + 12, static_cast<unsigned long long>(clock64() - t_kernel));
 }
 
 // ------------------------------------------------------ unfused kernels
@@ -987,6 +1035,14 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
   e.kl_coeff = kl_coeff;
   grpo_epilogue_kernel<<<1, kEpiThreads, 0, stream>>>(e);
   return launch_check("grpo_epilogue_kernel");
+}
+
+// Debug only (not part of the header): point the fused kernel's per-role
+// cycle counters at a device buffer of 16 u64 (or null to disable).
+extern "C" int dvla_debug_fused_counters(void* dev_buf) {
+  unsigned long long* p = static_cast<unsigned long long*>(dev_buf);
+  DVLA_CUDA_TRY(cudaMemcpyToSymbol(g_dbg, &p, sizeof(p)));
+  return DVLA_OK;
 }
 
 extern "C" int dvla_advantages(const double* rewards, int64_t n_groups, int64_t G, double delta,

@@ -47,10 +47,12 @@ def coef_order(nops, nloc, L):
     compute warps never wait for the tail of the row they just finished."""
     order = []
     n = 0
+    Le = min(nloc, L)
+    pair_end = Le + 2 * (nloc - Le)
     while n < nops:
         isb, _ = op_of(n, nloc, L)
         nxt = op_of(n + 1, nloc, L)[0] if n + 1 < nops else None
-        if not isb and nxt:
+        if not isb and nxt and Le >= 2 and n + 1 < pair_end:
             order += [n + 1, n]
             n += 2
         else:
@@ -90,10 +92,18 @@ def simulate(nloc, L, seed, write_dl=True):
                 empty[n % S].arrive()
                 b += 1
 
+    tails = set()
+
     def coef():
         a = b = 0
         for n in coef_order(nops, nloc, Lx):
             isb, k = op_of(n, nloc, Lx)
+            if isb:
+                # the chunk of row k spans rounds k and k+1: both tails of this
+                # CTA must already be published (else: cross-CTA deadlock)
+                assert k in tails and (k + 1 >= nloc or k + 1 in tails), (k, sorted(tails))
+            else:
+                tails.add(k)
             if not isb:
                 yield from wait(ad_a[a % S], a // S)
                 assert slot_p[a % S] == a
