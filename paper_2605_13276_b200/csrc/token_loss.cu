@@ -155,7 +155,8 @@ __device__ __forceinline__ double chunk_lp_pairwise(const double* __restrict__ l
 // so the chunk wait is deadlock-free while all CTAs are co-resident
 // (grid <= #SMs, T <= grid).
 //
-// Warp roles: 0..15 compute, 16 loader, 17 coefficient, 18 store.
+// Warp roles: 0..15 compute, 16 loader, 17 coefficient, 18 store,
+// 19 publisher (lp_tok + chunk counters + chunk finalisation).
 // Barriers (every barrier completes once per use of its own ring index, and
 // every waiter walks its ring in order, so parity never aliases):
 //   full[s], empty[s]  per SMEM stage s = op % 3: loader <-> all consumers
@@ -167,7 +168,9 @@ __device__ __forceinline__ double chunk_lp_pairwise(const double* __restrict__ l
 constexpr int kWarpLoader = kFusedComputeWarps;
 constexpr int kCoefWarp = kFusedComputeWarps + 1;
 constexpr int kWarpStore = kFusedComputeWarps + 2;
-constexpr int kFusedThreadsWS = (kFusedComputeWarps + 3) * 32;
+constexpr int kWarpPublish = kFusedComputeWarps + 3;
+constexpr int kFusedThreadsWS = (kFusedComputeWarps + 4) * 32;
+constexpr int kPubRing = 8;
 constexpr int kLagRounds = 4;
 constexpr int kRing = 8;  // > kLagRounds + 1 rows of (lse, target) in flight
 
@@ -186,6 +189,9 @@ struct FusedSmem {
   int32_t tgt[kFusedStages];
   double ring_lse[kRing];
   int32_t ring_tgt[kRing];
+  uint64_t pubfull[kPubRing];
+  uint64_t pubempty[kPubRing];
+  double pub_lp[kPubRing];
 };
 
 // coefficient not yet published (the workspace is memset to 0xff)
@@ -271,6 +277,10 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       mbar_init(&S.adoneB[s], kFusedComputeWarps);
       mbar_init(&S.cfullB[s], 1);
     }
+    for (int j = 0; j < kPubRing; ++j) {
+      mbar_init(&S.pubfull[j], 1);
+      mbar_init(&S.pubempty[j], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -329,62 +339,76 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     return;
   }
 
-  // ---------------------------------------------------- coefficient warp
-  if (warp == kCoefWarp) {
-    // Per-row ring (lse, target id) carried from A(k) to B(k), L ops later.
-    double* ring_lse = S.ring_lse;
-    int32_t* ring_tgt = S.ring_tgt;
-    int32_t tgt_next = (nloc > 0 && lane == 0) ? __ldg(p.tokens + row_of(0)) : 0;
-    int64_t next_a = 1;          // next A row whose token id to prefetch
-    int64_t a = 0, b = 0;        // A / B op counters
-    uint32_t pend_old = 0;       // chunk counter value returned to the last A tail
-    int64_t pend_q = -1;         // ... for this chunk (finalised at the next A op)
-    unsigned long long pref = kCoeffPending;  // prefetched coefficient bits
-    int64_t pref_q = -1;
-    auto finalize = [&](int64_t q) {
-      // last row of chunk q published: lp, rho, coefficient (grpo.py:252-268)
-      const double* lt = p.lp_tok + q * T;
-      double vals[4];
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int64_t t = 32 * m + lane;
-        vals[m] = (t < T) ? __ldcg(lt + t) : 0.0;
-      }
-      const double lp = warp_pairwise_small(vals, static_cast<int>(T), lane);
+  // ------------------------------------------------------ publisher warp
+  // Publishes each row's lp_tok and bumps its chunk counter (acq_rel: the
+  // release fence and the atomic round trip stall only this warp); the last
+  // arrival of a chunk finalises it: lp (pairwise over T), rho, coefficient
+  // (grpo.py:252-268), published with st.release for the B ops of all CTAs.
+  if (warp == kWarpPublish) {
+    if (!write_dl) return;
+    int64_t na = 0;  // A ops seen
+    for (int64_t n = 0; n < nops; ++n) {
+      bool isB;
+      int64_t k;
+      op_of(n, nloc, L, &isB, &k);
+      if (isB) continue;
+      const int j = static_cast<int>(na % kPubRing);
+      mbar_wait(&S.pubfull[j], static_cast<uint32_t>((na / kPubRing) & 1));
+      ++na;
+      const double lp = S.pub_lp[j];
+      const int64_t r = row_of(k);
+      const int64_t q = r / T;
+      __syncwarp();
+      uint32_t old = 0;
       if (lane == 0) {
-        ChunkTerms ct = chunk_terms(lp, static_cast<double>(p.blp[q]), p.adv[q / p.C], p.w,
-                                    p.clip_eps, p.kl_coeff);
-        p.lp_chunk[q] = lp;
-        // the GPU's default f64 NaN is all-ones == the "pending" sentinel:
-        // publish non-finite coefficients as a quiet NaN with another payload
-        const unsigned long long bits =
-            isnan(ct.coeff) ? 0x7ff8000000000000ull
-                            : static_cast<unsigned long long>(__double_as_longlong(ct.coeff));
-        st_release_gpu_u64(reinterpret_cast<unsigned long long*>(p.coeff + q), bits);
+        mbar_arrive(&S.pubempty[j]);
+        p.lp_tok[r] = lp;
+        old = atom_add_acq_rel_gpu(p.cnt + q, 1u);
+      }
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if (old == static_cast<uint32_t>(T - 1)) {
+        DBG_T0();
+        const double* lt = p.lp_tok + q * T;
+        double vals[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int64_t t = 32 * m + lane;
+          vals[m] = (t < T) ? __ldcg(lt + t) : 0.0;
+        }
+        const double lpc = warp_pairwise_small(vals, static_cast<int>(T), lane);
+        if (lane == 0) {
+          ChunkTerms ct = chunk_terms(lpc, static_cast<double>(p.blp[q]), p.adv[q / p.C], p.w,
+                                      p.clip_eps, p.kl_coeff);
+          p.lp_chunk[q] = lpc;
+          // the GPU's default f64 NaN is all-ones == the "pending" sentinel:
+          // publish non-finite coefficients as a quiet NaN with another payload
+          const unsigned long long bits =
+              isnan(ct.coeff) ? 0x7ff8000000000000ull
+                              : static_cast<unsigned long long>(__double_as_longlong(ct.coeff));
+          st_release_gpu_u64(reinterpret_cast<unsigned long long*>(p.coeff + q), bits);
+          DBG_ADD(7);
+        }
       }
       __syncwarp();
-    };
+    }
+    return;
+  }
+
+  // ---------------------------------------------------- coefficient warp
+  if (warp == kCoefWarp) {
+    int32_t tgt_next = (nloc > 0 && lane == 0) ? __ldg(p.tokens + row_of(0)) : 0;
+    int64_t next_a = 1;  // next A row whose token id to prefetch
+    int64_t a = 0, b = 0;  // A / B op counters
+    unsigned long long pref = kCoeffPending;  // prefetched coefficient bits
+    int64_t pref_q = -1;
     auto process = [&](int64_t n) {
       const int s = static_cast<int>(n % kFusedStages);
       bool isB;
       int64_t k;
       op_of(n, nloc, L, &isB, &k);
       const int64_t r = row_of(k);
-      // the previous tail's atomic result is consumed one op later, so its
-      // round trip overlaps this op's waits
-      auto check_pending = [&]() {
-        if (write_dl && pend_q >= 0) {
-          const uint32_t old = __shfl_sync(0xffffffffu, pend_old, 0);
-          if (old == static_cast<uint32_t>(T - 1)) {
-            DBG_T0();
-            finalize(pend_q);
-            if (lane == 0) { DBG_ADD(7); }
-          }
-          pend_q = -1;
-        }
-      };
       if (!isB) {
-        // ---- tail of A(k): lse, lp_tok, chunk counter
+        // ---- tail of A(k): lse (f64) and the target's log-prob
         int32_t tgt = tgt_next;
         if (lane == 0 && next_a < nloc) tgt_next = __ldg(p.tokens + row_of(next_a));
         ++next_a;
@@ -395,13 +419,15 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
           if (lane == 0) { DBG_ADD(2); }
         }
         const long long t_tail = dbg ? clock64() : 0;
+        const int j = static_cast<int>(a % kPubRing);
+        const uint32_t pe_ph = static_cast<uint32_t>(((a / kPubRing) - 1) & 1);
+        const bool pub_reuse = write_dl && a >= kPubRing;
         ++a;
-        check_pending();  // atomic of the previous A tail: returned long ago
         const float mw = (lane < kFusedComputeWarps) ? S.wm[sa][lane] : -INFINITY;
         const double sw = (lane < kFusedComputeWarps) ? S.ws[sa][lane] : 0.0;
         const float M = warp_max_f32(mw);
         double term = (lane < kFusedComputeWarps && sw > 0.0)
-                          ? sw * exp2(static_cast<double>(mw - M) * 1.4426950408889634)
+                          ? sw * static_cast<double>(ex2f((mw - M) * kLog2e))
                           : 0.0;
         term = warp_sum_f64(term);
         if (lane == 0) {
@@ -416,21 +442,22 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
                 reinterpret_cast<const __nv_bfloat16*>(buf(s))[tgt]));
           }
           mbar_arrive(&S.empty[s]);  // row no longer needed in SMEM
-          p.lp_tok[r] = xt - lse;
           if (write_dl) {
-            ring_lse[k % kRing] = lse;
-            ring_tgt[k % kRing] = tgt;
-            pend_old = atom_add_acq_rel_gpu(p.cnt + r / T, 1u);  // consumed next A op
+            S.ring_lse[k % kRing] = lse;
+            S.ring_tgt[k % kRing] = tgt;
+            if (pub_reuse) mbar_wait(&S.pubempty[j], pe_ph);
+            S.pub_lp[j] = xt - lse;
+            mbar_arrive(&S.pubfull[j]);
           } else {
             p.lse[r] = lse;
+            p.lp_tok[r] = xt - lse;
           }
+          if (dbg) atomicAdd(dbg + 3, static_cast<unsigned long long>(clock64() - t_tail));
+          // re-issue a coefficient prefetch that found the chunk still pending
+          if (write_dl && pref_q >= 0 && pref == kCoeffPending)
+            pref = ld_acquire_gpu_u64(reinterpret_cast<const unsigned long long*>(p.coeff + pref_q));
         }
         __syncwarp();
-        if (write_dl) pend_q = r / T;
-        if (dbg && lane == 0) atomicAdd(dbg + 3, static_cast<unsigned long long>(clock64() - t_tail));
-        // re-issue a coefficient prefetch that found the chunk still pending
-        if (write_dl && lane == 0 && pref_q >= 0 && pref == kCoeffPending)
-          pref = ld_acquire_gpu_u64(reinterpret_cast<const unsigned long long*>(p.coeff + pref_q));
       } else {
         // ---- coefficient for B(k); slot b % 3 is free once B op b-3 is done
         const int sb = static_cast<int>(b % kFusedStages);
@@ -442,11 +469,6 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         const long long t_prep = dbg ? clock64() : 0;
         ++b;
         const int64_t q = r / T;
-        // a finaliser must never block on another chunk: settle any pending
-        // finalisation duty before a (rare) spin on this chunk's coefficient
-        const bool need_spin =
-            __shfl_sync(0xffffffffu, (pref_q == q) ? (pref == kCoeffPending ? 1 : 0) : 1, 0) != 0;
-        if (need_spin) check_pending();
         if (lane == 0) {
           unsigned long long bits = (pref_q == q) ? pref : kCoeffPending;
           if (bits == kCoeffPending) {
@@ -456,8 +478,8 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
             if (dbg) atomicAdd(dbg + 11, 1ull);
           }
           const double c = __longlong_as_double(static_cast<long long>(bits));
-          const double lse = ring_lse[k % kRing];
-          const int32_t tgt = ring_tgt[k % kRing];
+          const double lse = S.ring_lse[k % kRing];
+          const int32_t tgt = S.ring_tgt[k % kRing];
           uint32_t mode;
           if (c == 0.0) {
             mode = 0u;
@@ -482,11 +504,10 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         __syncwarp();
       }
     };
-    // B(k) is handled before the A(k+L) that precedes it in the op sequence:
-    // its coefficient does not depend on that A, so the compute warps find
-    // it ready when they finish A(k+L) (tests/test_fused_protocol.py).
-    // Only inside the paired region and with a lag >= 2: B(k) depends on the
-    // tails of rows k and k+1 (a chunk spans <= 2 rounds), never on A(k+Le).
+    // B(k) is handled before the A(k+L) that precedes it in the op sequence
+    // (its coefficient depends only on the tails of rows k and k+1), so the
+    // compute warps find it ready when they finish A(k+L).  Only inside the
+    // paired region and with an effective lag >= 2 (tests/test_fused_protocol.py).
     const int64_t Le = nloc < L ? nloc : L;
     const int64_t pair_end = Le + 2 * (nloc - Le);
     for (int64_t n = 0; n < nops;) {
@@ -502,10 +523,6 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         process(n);
         n += 1;
       }
-    }
-    if (write_dl && pend_q >= 0) {
-      const uint32_t old = __shfl_sync(0xffffffffu, pend_old, 0);
-      if (old == static_cast<uint32_t>(T - 1)) finalize(pend_q);
     }
     return;
   }
