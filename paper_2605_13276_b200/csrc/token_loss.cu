@@ -156,7 +156,7 @@ __device__ __forceinline__ double chunk_lp_pairwise(const double* __restrict__ l
 // (grid <= #SMs, T <= grid).
 //
 // Warp roles: 0..15 compute, 16 loader, 17 coefficient, 18 store,
-// 19 publisher (lp_tok + chunk counters + chunk finalisation).
+// 19 publisher (lp_tok + release of the chunk counters).
 // Barriers (every barrier completes once per use of its own ring index, and
 // every waiter walks its ring in order, so parity never aliases):
 //   full[s], empty[s]  per SMEM stage s = op % 3: loader <-> all consumers
@@ -340,12 +340,10 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   }
 
   // ------------------------------------------------------ publisher warp
-  // Publishes each row's lp_tok and bumps its chunk counter (acq_rel: the
-  // release fence and the atomic round trip stall only this warp); the last
-  // arrival of a chunk finalises it: lp (pairwise over T), rho, coefficient
-  // (grpo.py:252-268), published with st.release for the B ops of all CTAs.
+  // Publishes each row's lp_tok and bumps its chunk counter with a release
+  // reduction; the release fence's wait for the store stalls only this warp.
   if (warp == kWarpPublish) {
-    if (!write_dl) return;
+    if (!write_dl || lane != 0) return;
     int64_t na = 0;  // A ops seen
     for (int64_t n = 0; n < nops; ++n) {
       bool isB;
@@ -353,43 +351,19 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       op_of(n, nloc, L, &isB, &k);
       if (isB) continue;
       const int j = static_cast<int>(na % kPubRing);
-      mbar_wait(&S.pubfull[j], static_cast<uint32_t>((na / kPubRing) & 1));
+      {
+        DBG_T0();
+        mbar_wait(&S.pubfull[j], static_cast<uint32_t>((na / kPubRing) & 1));
+        DBG_ADD(13);
+      }
+      const long long t_pub = dbg ? clock64() : 0;
       ++na;
       const double lp = S.pub_lp[j];
+      mbar_arrive(&S.pubempty[j]);
       const int64_t r = row_of(k);
-      const int64_t q = r / T;
-      __syncwarp();
-      uint32_t old = 0;
-      if (lane == 0) {
-        mbar_arrive(&S.pubempty[j]);
-        p.lp_tok[r] = lp;
-        old = atom_add_acq_rel_gpu(p.cnt + q, 1u);
-      }
-      old = __shfl_sync(0xffffffffu, old, 0);
-      if (old == static_cast<uint32_t>(T - 1)) {
-        DBG_T0();
-        const double* lt = p.lp_tok + q * T;
-        double vals[4];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const int64_t t = 32 * m + lane;
-          vals[m] = (t < T) ? __ldcg(lt + t) : 0.0;
-        }
-        const double lpc = warp_pairwise_small(vals, static_cast<int>(T), lane);
-        if (lane == 0) {
-          ChunkTerms ct = chunk_terms(lpc, static_cast<double>(p.blp[q]), p.adv[q / p.C], p.w,
-                                      p.clip_eps, p.kl_coeff);
-          p.lp_chunk[q] = lpc;
-          // the GPU's default f64 NaN is all-ones == the "pending" sentinel:
-          // publish non-finite coefficients as a quiet NaN with another payload
-          const unsigned long long bits =
-              isnan(ct.coeff) ? 0x7ff8000000000000ull
-                              : static_cast<unsigned long long>(__double_as_longlong(ct.coeff));
-          st_release_gpu_u64(reinterpret_cast<unsigned long long*>(p.coeff + q), bits);
-          DBG_ADD(7);
-        }
-      }
-      __syncwarp();
+      p.lp_tok[r] = lp;
+      red_release_gpu_add(p.cnt + r / T, 1u);
+      if (dbg) atomicAdd(dbg + 14, static_cast<unsigned long long>(clock64() - t_pub));
     }
     return;
   }
@@ -399,8 +373,35 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     int32_t tgt_next = (nloc > 0 && lane == 0) ? __ldg(p.tokens + row_of(0)) : 0;
     int64_t next_a = 1;  // next A row whose token id to prefetch
     int64_t a = 0, b = 0;  // A / B op counters
-    unsigned long long pref = kCoeffPending;  // prefetched coefficient bits
-    int64_t pref_q = -1;
+    // Prefetched inputs of the next B row's chunk coefficient.  Every CTA
+    // evaluates the coefficients of its own B rows from the published token
+    // log-probs (same inputs, same code: bitwise identical across CTAs), so
+    // no CTA ever waits on another CTA's finaliser -- only on its rows.
+    int64_t pq = -1;       // chunk being prefetched
+    uint32_t pc = 0;       // acquired counter value (this lane)
+    bool pv_ok = false;    // pv[] holds the chunk's token log-probs
+    double pv[4] = {0.0, 0.0, 0.0, 0.0};
+    float pblp = 0.f;
+    double padv = 0.0;
+    auto prefetch_vals = [&]() {
+      // called with pc acquired on every lane; loads ordered after the acquire
+      const double* lt = p.lp_tok + pq * T;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int64_t t = 32 * m + lane;
+        pv[m] = (t < T) ? __ldcg(lt + t) : 0.0;
+      }
+      pblp = __ldg(p.blp + pq);
+      padv = __ldg(p.adv + pq / p.C);
+      pv_ok = true;
+    };
+    auto poll = [&]() {  // advance the prefetch state machine without blocking
+      if (pq < 0 || pv_ok) return;
+      if (__all_sync(0xffffffffu, pc >= static_cast<uint32_t>(T)))
+        prefetch_vals();
+      else
+        pc = ld_acquire_gpu(p.cnt + pq);
+    };
     auto process = [&](int64_t n) {
       const int s = static_cast<int>(n % kFusedStages);
       bool isB;
@@ -453,11 +454,9 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
             p.lp_tok[r] = xt - lse;
           }
           if (dbg) atomicAdd(dbg + 3, static_cast<unsigned long long>(clock64() - t_tail));
-          // re-issue a coefficient prefetch that found the chunk still pending
-          if (write_dl && pref_q >= 0 && pref == kCoeffPending)
-            pref = ld_acquire_gpu_u64(reinterpret_cast<const unsigned long long*>(p.coeff + pref_q));
         }
         __syncwarp();
+        if (write_dl) poll();
       } else {
         // ---- coefficient for B(k); slot b % 3 is free once B op b-3 is done
         const int sb = static_cast<int>(b % kFusedStages);
@@ -469,15 +468,37 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         const long long t_prep = dbg ? clock64() : 0;
         ++b;
         const int64_t q = r / T;
-        if (lane == 0) {
-          unsigned long long bits = (pref_q == q) ? pref : kCoeffPending;
-          if (bits == kCoeffPending) {
-            DBG_T0();
-            bits = spin_coeff(reinterpret_cast<const unsigned long long*>(p.coeff + q), p.err);
-            DBG_ADD(6);
-            if (dbg) atomicAdd(dbg + 11, 1ull);
+        if (pq != q) {  // no prefetch for this chunk (first B op)
+          pq = q;
+          pv_ok = false;
+          pc = ld_acquire_gpu(p.cnt + q);
+        }
+        if (!pv_ok) {
+          DBG_T0();
+          if (dbg && lane == 0) atomicAdd(dbg + 11, 1ull);
+          const uint64_t t0 = globaltimer_ns();
+          uint32_t ns = 32;
+          while (!__all_sync(0xffffffffu, pc >= static_cast<uint32_t>(T))) {
+            __nanosleep(ns);
+            if (ns < 256) ns <<= 1;
+            pc = ld_acquire_gpu(p.cnt + q);
+            if (globaltimer_ns() - t0 > kSpinTimeoutNs) {
+              if (lane == 0) atomicOr(p.err, kErrTimeout);
+              break;
+            }
           }
-          const double c = __longlong_as_double(static_cast<long long>(bits));
+          prefetch_vals();
+          if (lane == 0) { DBG_ADD(6); }
+        }
+        const double lp = warp_pairwise_small(pv, static_cast<int>(T), lane);
+        if (lane == 0) {
+          ChunkTerms ct = chunk_terms(lp, static_cast<double>(pblp), padv, p.w, p.clip_eps,
+                                      p.kl_coeff);
+          const double c = ct.coeff;
+          if (r % T == 0) {  // one writer per chunk for the epilogue
+            p.lp_chunk[q] = lp;
+            p.coeff[q] = c;
+          }
           const double lse = S.ring_lse[k % kRing];
           const int32_t tgt = S.ring_tgt[k % kRing];
           uint32_t mode;
@@ -495,13 +516,17 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
           S.tgt[sb] = tgt;
           mbar_arrive(&S.cfullB[sb]);
           if (dbg) atomicAdd(dbg + 5, static_cast<unsigned long long>(clock64() - t_prep));
-          // prefetch the next B row's chunk coefficient (ready long before use)
-          if (k + 1 < nloc) {
-            pref_q = row_of(k + 1) / T;
-            pref = ld_acquire_gpu_u64(reinterpret_cast<const unsigned long long*>(p.coeff + pref_q));
-          }
         }
         __syncwarp();
+        // start prefetching the next B row's chunk (same chunk: reuse)
+        if (k + 1 < nloc) {
+          const int64_t nq = row_of(k + 1) / T;
+          if (nq != pq) {
+            pq = nq;
+            pv_ok = false;
+            pc = ld_acquire_gpu(p.cnt + nq);
+          }
+        }
       }
     };
     // B(k) is handled before the A(k+L) that precedes it in the op sequence
@@ -1001,8 +1026,6 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
                                          227 * 1024));
       attr_set[dev & 63] = true;
     }
-    if (want_dl)  // chunk coefficients start as "pending" (all-ones bit pattern)
-      DVLA_CUDA_TRY(cudaMemsetAsync(ws.coeff, 0xff, static_cast<size_t>(nq) * 8, stream));
     const unsigned grid = static_cast<unsigned>(R < sms ? R : sms);
     const uint32_t stage_bytes = static_cast<uint32_t>(((V * 2 + 127) / 128) * 128);
     cudaEvent_t stop;
