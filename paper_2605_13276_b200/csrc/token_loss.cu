@@ -187,6 +187,8 @@ struct FusedSmem {
   float cf[kFusedStages];     // coefficient (f32)
   uint32_t mode[kFusedStages];  // 0 zero row, 1 finite c (bit 31: c > 0), 2 non-finite c
   int32_t tgt[kFusedStages];
+  float xt[kFusedStages];       // gathered target logit of A slot
+  int32_t tgta[kFusedStages];   // its token id (-1: out of range)
   double ring_lse[kRing];
   int32_t ring_tgt[kRing];
   uint64_t pubfull[kPubRing];
@@ -370,8 +372,6 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
 
   // ---------------------------------------------------- coefficient warp
   if (warp == kCoefWarp) {
-    int32_t tgt_next = (nloc > 0 && lane == 0) ? __ldg(p.tokens + row_of(0)) : 0;
-    int64_t next_a = 1;  // next A row whose token id to prefetch
     int64_t a = 0, b = 0;  // A / B op counters
     // Prefetched inputs of the next B row's chunk coefficient.  Every CTA
     // evaluates the coefficients of its own B rows from the published token
@@ -410,22 +410,25 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       const int64_t r = row_of(k);
       if (!isB) {
         // ---- tail of A(k): lse (f64) and the target's log-prob
-        int32_t tgt = tgt_next;
-        if (lane == 0 && next_a < nloc) tgt_next = __ldg(p.tokens + row_of(next_a));
-        ++next_a;
         const int sa = static_cast<int>(a % kFusedStages);
         {
           DBG_T0();
           mbar_wait(&S.adoneA[sa], static_cast<uint32_t>((a / kFusedStages) & 1));
           if (lane == 0) { DBG_ADD(2); }
         }
+        // read everything this tail needs from slot sa, then free the stage
+        // (the compute warps already gathered the target logit)
+        const int32_t tgt = S.tgta[sa];
+        const float xt_f = S.xt[sa];
+        const float mw = (lane < kFusedComputeWarps) ? S.wm[sa][lane] : -INFINITY;
+        const double sw = (lane < kFusedComputeWarps) ? S.ws[sa][lane] : 0.0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[s]);
         const long long t_tail = dbg ? clock64() : 0;
         const int j = static_cast<int>(a % kPubRing);
         const uint32_t pe_ph = static_cast<uint32_t>(((a / kPubRing) - 1) & 1);
         const bool pub_reuse = write_dl && a >= kPubRing;
         ++a;
-        const float mw = (lane < kFusedComputeWarps) ? S.wm[sa][lane] : -INFINITY;
-        const double sw = (lane < kFusedComputeWarps) ? S.ws[sa][lane] : 0.0;
         const float M = warp_max_f32(mw);
         double term = (lane < kFusedComputeWarps && sw > 0.0)
                           ? sw * static_cast<double>(ex2f((mw - M) * kLog2e))
@@ -433,16 +436,8 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         term = warp_sum_f64(term);
         if (lane == 0) {
           const double lse = static_cast<double>(M) + log(term);
-          double xt;
-          if (tgt < 0 || tgt >= V) {
-            atomicOr(p.err, kErrToken);
-            xt = __longlong_as_double(0x7ff8000000000000ll);
-            tgt = -1;
-          } else {
-            xt = static_cast<double>(__bfloat162float(
-                reinterpret_cast<const __nv_bfloat16*>(buf(s))[tgt]));
-          }
-          mbar_arrive(&S.empty[s]);  // row no longer needed in SMEM
+          const double xt = static_cast<double>(xt_f);
+          if (tgt < 0) atomicOr(p.err, kErrToken);
           if (write_dl) {
             S.ring_lse[k % kRing] = lse;
             S.ring_tgt[k % kRing] = tgt;
@@ -567,6 +562,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       if (tid == 0) { DBG_ADD(0); }
     }
     if (!isB) {
+      const int32_t tg = (tid == 0) ? __ldg(p.tokens + row_of(k)) : 0;  // used at the end
       const uint4* v = reinterpret_cast<const uint4*>(buf(s));
       uint32_t mx0 = 0xff80ff80u, mx1 = 0xff80ff80u;
 #pragma unroll 4
@@ -592,6 +588,12 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       part = warp_sum_f64(part);
       const int sa = static_cast<int>(a % kFusedStages);
       ++a;
+      if (tid == 0) {  // gather the target logit while the row is in SMEM
+        const bool ok = tg >= 0 && tg < V;
+        S.tgta[sa] = ok ? tg : -1;
+        S.xt[sa] = ok ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(buf(s))[tg])
+                      : __int_as_float(0x7fc00000);
+      }
       if (lane == 0) {
         S.wm[sa][warp] = m;
         S.ws[sa][warp] = part;
