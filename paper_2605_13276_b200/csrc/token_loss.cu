@@ -26,6 +26,8 @@
 //   tok_chunk_kernel      unfused per-chunk coefficient
 //   tok_bwd_kernel<T>     unfused backward (re-reads logits: 3*N*s traffic)
 //   grpo_epilogue_kernel  loss / stats / abort detection in canonical order
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "grpo_math.cuh"
 
@@ -171,7 +173,7 @@ constexpr int kWarpStore = kFusedComputeWarps + 2;
 constexpr int kWarpPublish = kFusedComputeWarps + 3;
 constexpr int kFusedThreadsWS = (kFusedComputeWarps + 4) * 32;
 constexpr int kPubRing = 8;
-constexpr int kLagRounds = 4;
+constexpr int kLagRounds = 3;
 constexpr int kRing = 8;  // > kLagRounds + 1 rows of (lse, target) in flight
 
 struct FusedSmem {
@@ -252,7 +254,7 @@ __device__ __forceinline__ void op_of(int64_t n, int64_t nloc, int L, bool* isB,
 }
 
 __global__ void __launch_bounds__(kFusedThreadsWS, 1)
-    tok_fused_bf16_kernel(TokParams p, uint32_t stage_bytes, int write_dl) {
+    tok_fused_bf16_kernel(TokParams p, uint32_t stage_bytes, int write_dl, int lag, int a_evict_last) {
   extern __shared__ __align__(128) uint8_t dyn_smem[];
   FusedSmem& S = *reinterpret_cast<FusedSmem*>(dyn_smem);
   uint8_t* bufs = dyn_smem + ((sizeof(FusedSmem) + 127) / 128) * 128;
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   const int64_t G = gridDim.x;
   const int64_t nloc = (p.R > blockIdx.x) ? (p.R - blockIdx.x + G - 1) / G : 0;
   const int64_t nops = write_dl ? 2 * nloc : nloc;
-  const int L = write_dl ? kLagRounds : 1 << 30;  // forward-only: A ops only
+  const int L = write_dl ? lag : 1 << 30;  // forward-only: A ops only
   auto row_of = [&](int64_t k) { return blockIdx.x + k * G; };
   auto buf = [&](int s) { return bufs + static_cast<size_t>(s) * stage_bytes; };
   const int64_t T = p.T;
@@ -294,6 +296,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   if (warp == kWarpLoader) {
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
+      const uint64_t pol_keep = l2_policy_evict_last();
       for (int64_t n = 0; n < nops; ++n) {
         const int s = static_cast<int>(n % kFusedStages);
         if (n >= kFusedStages) {
@@ -307,6 +310,8 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         mbar_arrive_expect_tx(&S.full[s], row_bytes);
         if (isB)  // second (last) read of the row: from L2, then evict
           tma_load_1d_evict_first(buf(s), logits + row_of(k) * V, row_bytes, &S.full[s], pol);
+        else if (a_evict_last && write_dl)  // keep in L2 until B re-reads it
+          tma_load_1d_evict_first(buf(s), logits + row_of(k) * V, row_bytes, &S.full[s], pol_keep);
         else
           tma_load_1d(buf(s), logits + row_of(k) * V, row_bytes, &S.full[s]);
       }
@@ -1032,7 +1037,16 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
     const uint32_t stage_bytes = static_cast<uint32_t>(((V * 2 + 127) / 128) * 128);
     cudaEvent_t stop;
     prof_begin(stream, &stop);
-    tok_fused_bf16_kernel<<<grid, kFusedThreadsWS, fsmem, stream>>>(p, stage_bytes, want_dl ? 1 : 0);
+    static const int lag = [] {
+      const char* e = getenv("DVLA_FUSED_LAG");
+      return e ? atoi(e) : kLagRounds;
+    }();
+    static const int a_keep = [] {
+      const char* e = getenv("DVLA_FUSED_KEEP");
+      return e ? atoi(e) : 1;
+    }();
+    tok_fused_bf16_kernel<<<grid, kFusedThreadsWS, fsmem, stream>>>(p, stage_bytes, want_dl ? 1 : 0,
+                                                                     lag < 2 ? 2 : lag, a_keep);
     prof_end(stream, stop);
     if (int rc = launch_check("tok_fused_bf16_kernel")) return rc;
     if (!want_dl) {
