@@ -173,7 +173,7 @@ constexpr int kWarpStore = kFusedComputeWarps + 2;
 constexpr int kWarpPublish = kFusedComputeWarps + 3;
 constexpr int kFusedThreadsWS = (kFusedComputeWarps + 4) * 32;
 constexpr int kPubRing = 8;
-constexpr int kLagRounds = 3;
+constexpr int kLagRounds = 2;  // measured best on B200 (lag 2..4 x L2 policy sweep)
 constexpr int kRing = 8;  // > kLagRounds + 1 rows of (lse, target) in flight
 
 struct FusedSmem {
@@ -1043,7 +1043,7 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
     }();
     static const int a_keep = [] {
       const char* e = getenv("DVLA_FUSED_KEEP");
-      return e ? atoi(e) : 1;
+      return e ? atoi(e) : 0;
     }();
     tok_fused_bf16_kernel<<<grid, kFusedThreadsWS, fsmem, stream>>>(p, stage_bytes, want_dl ? 1 : 0,
                                                                      lag < 2 ? 2 : lag, a_keep);
