@@ -126,6 +126,94 @@ int dvla_grpo_epilogue(const double* lp_chunk, const float* blp, const double* b
                        int64_t G, int64_t C, double clip_eps, double kl_coeff,
                        double* coeff_out, double* stats, void* stream);
 
+/* --------------------------------------------------- dual-pool arena */
+
+/* PoolKind (pools.py:23-26) */
+enum dvla_pool_kind {
+  DVLA_POOL_MODEL_COMPUTE = 0, /* long-lived: params, grads, optimizer, replicas */
+  DVLA_POOL_ENV_AUX = 1,       /* epoch-scoped: rollout staging, activations/KV */
+  DVLA_POOL_UNIFIED_BASELINE = 2
+};
+
+/* Opaque arena: host-side first-fit bookkeeping over a device slab
+ * (Pool, pools.py:72-212).  Offsets are bit-identical to the reference. */
+typedef struct dvla_arena dvla_arena;
+
+int dvla_arena_create(int kind, int64_t capacity, dvla_arena** out, int64_t* pool_id_out);
+int dvla_arena_destroy(dvla_arena* arena);
+/* Pool.alloc (pools.py:92-128); DVLA_ERR_ALLOC_FAILURE when nothing fits. */
+int dvla_arena_alloc(dvla_arena* arena, int64_t size, int64_t align, int64_t* offset_out,
+                     int64_t* serial_out, int64_t* generation_out);
+/* Pool.free (pools.py:130-141); DVLA_ERR_POOL_USAGE for foreign, stale or
+ * double-freed handles (messages as the reference). */
+int dvla_arena_free(dvla_arena* arena, int64_t pool_id, int64_t offset, int64_t size,
+                    int64_t generation, int64_t serial);
+/* Pool.epoch_reset (pools.py:160-170): ENV_AUX only. */
+int dvla_arena_epoch_reset(dvla_arena* arena);
+int dvla_arena_is_live(dvla_arena* arena, int64_t generation, int64_t serial, int* out);
+/* out[9] = live_bytes, total_free, largest_free, failed_allocs, alloc_count,
+ * free_count, churn_bytes, generation, n_free_extents (Pool.stats). */
+int dvla_arena_stats(dvla_arena* arena, int64_t* out);
+/* kernels.alloc_trace_run (numba_backend.py:139-247), host memory in/out;
+ * final_out[3] = (total_free, largest_free, n_extents). */
+int dvla_arena_trace(int64_t capacity, int64_t n, const uint8_t* is_alloc, const int64_t* size,
+                     const int64_t* align, const uint64_t* pick, uint8_t* out_ok,
+                     int64_t* out_off, int64_t* final_out);
+
+/* -------------------------------------------------- weight replication */
+
+/* Device slabs (cudaMalloc, so they can be shared over CUDA IPC); backing
+ * store of the dual-pool allocator's regions. */
+int dvla_dev_alloc(int device, size_t bytes, void** out);
+int dvla_dev_free(void* ptr);
+
+/* CUDA IPC for cross-process NVLink mappings of a peer's replica region
+ * (handle: 64 bytes).  The mapping is the B200 analogue of the reference
+ * Transport's WIRE link (planes.py:101-128): a peer pointer instead of a
+ * byte stream. */
+int dvla_ipc_handle(void* dev_ptr, uint8_t* handle_out);
+int dvla_ipc_open(const uint8_t* handle, void** out);
+int dvla_ipc_close(void* ptr);
+int dvla_enable_peer_access(int device, int peer);
+
+/* One hop of a replication chain: copy nbytes from src to dst (dst may be a
+ * peer mapping; NULL = wait only).  Chunk c is read only after
+ * wait_flags[c] >= epoch (NULL = source is ready) and signal_flags[c] is set
+ * to epoch (release, system scope) once chunk c has landed in dst. */
+typedef struct dvla_hop {
+  const void* src;
+  void* dst;
+  const uint32_t* wait_flags;
+  uint32_t* signal_flags;
+} dvla_hop;
+
+/* Chunked, pipelined chain broadcast (ControlPlane.broadcast, planes.py:294-321,
+ * without serialisation): TMA bulk copies HBM -> SMEM -> (peer) HBM, every
+ * receiver forwarding each chunk as soon as it landed.  All hops of one call
+ * run concurrently in one launch (ctas_per_hop CTAs each).  nbytes and
+ * chunk_bytes must be multiples of 16; pointers 16-byte aligned.  A flag wait
+ * longer than timeout_ns sets *err_dev (device u32) instead of hanging. */
+int dvla_replicate_chain(const dvla_hop* hops, int n_hops, int64_t nbytes, int64_t chunk_bytes,
+                         uint32_t epoch, int ctas_per_hop, uint64_t timeout_ns,
+                         uint32_t* err_dev, void* stream);
+
+/* snapshot_from_params on the device (core.py:120-129): copy nbytes from src
+ * to dst and write the first non-finite element index (dtype DVLA_F32 /
+ * DVLA_BF16 / DVLA_F64; DVLA_U8 = no check) to *bad_index_dev (device u64;
+ * UINT64_MAX when all finite). */
+int dvla_snapshot_copy(const void* src, void* dst, int64_t nbytes, int dtype,
+                       uint64_t* bad_index_dev, void* stream);
+
+/* Bitwise compare (messages_equal on parameter bytes, wire.py:279-281):
+ * out_dev[0] = number of differing 16-byte words, out_dev[1] = first
+ * differing byte offset (UINT64_MAX if equal). */
+int dvla_bytes_equal(const void* a, const void* b, int64_t nbytes, uint64_t* out_dev,
+                     void* stream);
+
+/* Copy-engine copy (cudaMemcpyAsync, UVA): the baseline replication path
+ * the TMA chain is measured against. */
+int dvla_memcpy_async(void* dst, const void* src, int64_t nbytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -123,3 +123,34 @@ def exported_symbols() -> list[str]:
     import re
     hdr = (Path(__file__).resolve().parent.parent / "include" / "dvla_b200.h").read_text()
     return sorted(set(re.findall(r"\b(dvla_[a-z0-9_]+)\s*\(", hdr)))
+
+
+# ------------------------------------------------------------- arena / pools
+POOL_MODEL_COMPUTE, POOL_ENV_AUX, POOL_UNIFIED_BASELINE = 0, 1, 2
+_pp = C.c_void_p
+_i64p = C.POINTER(_i64)
+dvla_arena_create = _proto("dvla_arena_create", [_i32, _i64, C.POINTER(_pp), _i64p])
+dvla_arena_destroy = _proto("dvla_arena_destroy", [_pp])
+dvla_arena_alloc = _proto("dvla_arena_alloc", [_pp, _i64, _i64, _i64p, _i64p, _i64p])
+dvla_arena_free = _proto("dvla_arena_free", [_pp, _i64, _i64, _i64, _i64, _i64])
+dvla_arena_epoch_reset = _proto("dvla_arena_epoch_reset", [_pp])
+dvla_arena_is_live = _proto("dvla_arena_is_live", [_pp, _i64, _i64, C.POINTER(C.c_int)])
+dvla_arena_stats = _proto("dvla_arena_stats", [_pp, _i64p])
+dvla_arena_trace = _proto("dvla_arena_trace", [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp])
+
+# ------------------------------------------------------- weight replication
+class Hop(C.Structure):
+    _fields_ = [("src", _vp), ("dst", _vp), ("wait_flags", _vp), ("signal_flags", _vp)]
+
+
+dvla_dev_alloc = _proto("dvla_dev_alloc", [_i32, _sz, C.POINTER(_pp)])
+dvla_dev_free = _proto("dvla_dev_free", [_pp])
+dvla_ipc_handle = _proto("dvla_ipc_handle", [_vp, C.c_char_p])
+dvla_ipc_open = _proto("dvla_ipc_open", [C.c_char_p, C.POINTER(_pp)])
+dvla_ipc_close = _proto("dvla_ipc_close", [_pp])
+dvla_enable_peer_access = _proto("dvla_enable_peer_access", [_i32, _i32])
+dvla_replicate_chain = _proto("dvla_replicate_chain", [
+    C.POINTER(Hop), _i32, _i64, _i64, C.c_uint32, _i32, C.c_uint64, _vp, _vp])
+dvla_snapshot_copy = _proto("dvla_snapshot_copy", [_vp, _vp, _i64, _i32, _vp, _vp])
+dvla_bytes_equal = _proto("dvla_bytes_equal", [_vp, _vp, _i64, _vp, _vp])
+dvla_memcpy_async = _proto("dvla_memcpy_async", [_vp, _vp, _i64, _vp])

@@ -1,0 +1,402 @@
+// Weight replication: learner -> rollout replicas over NVLink (K5/K6).
+//
+// Replaces the reference's weight control plane data path:
+//   TrainerWorker.snapshot -> core.snapshot_from_params (core.py:120-129,
+//   deep copy + isfinite), ControlPlane.broadcast (planes.py:294-321) ->
+//   Transport.outbound/inbound -> wire weight frame encode/decode
+//   (wire.py:144-147, 227-237) -> WeightMailbox.deliver/take_newest.
+// On B200 the parameters never leave device memory: a snapshot is a fused
+// copy + isfinite into a MODEL_COMPUTE pool region, and a broadcast is a
+// chunked, pipelined chain of TMA bulk copies (HBM -> SMEM -> peer HBM over
+// NVLink/NVSwitch) in which every receiver forwards each chunk to the next
+// receiver as soon as it has landed (per-chunk flags, release/acquire at
+// system scope).  Bit-exactness is by construction (byte copies) and is
+// checked by dvla_bytes_equal on every bench run.
+#include <stdlib.h>
+
+#include "common.cuh"
+
+namespace dvla {
+
+constexpr int kRepThreads = 32;  // one warp; lane 0 drives the TMA pipeline
+constexpr int kRepStages = 4;
+constexpr uint32_t kRepPiece = 32 * 1024;  // bytes per TMA bulk copy
+
+struct RepSmem {
+  uint64_t full[kRepStages];
+};
+
+struct HopDev {
+  const uint8_t* src;
+  uint8_t* dst;                  // may be an NVLink peer mapping; null = wait only
+  const uint32_t* wait_flags;    // local flags to wait on before reading a chunk
+  uint32_t* signal_flags;        // flags (often on the peer) to set after a chunk
+};
+
+constexpr int kMaxHops = 16;
+struct HopTable {
+  HopDev h[kMaxHops];
+};
+
+__device__ __forceinline__ bool wait_flag_sys(const uint32_t* f, uint32_t epoch, uint64_t timeout,
+                                              uint32_t* err) {
+  if (ld_acquire_sys(f) >= epoch) return true;
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t ns = 64;
+  while (ld_acquire_sys(f) < epoch) {
+    __nanosleep(ns);
+    if (ns < 1024) ns <<= 1;
+    if (globaltimer_ns() - t0 > timeout) {
+      atomicOr(err, 1u);
+      return false;
+    }
+  }
+  return true;
+}
+
+// One CTA group per hop; CTA j of a hop moves chunks j, j + ctas, ...
+__global__ void __launch_bounds__(kRepThreads) replicate_chain_kernel(
+    HopTable tab, int n_hops, int ctas_per_hop, int64_t nbytes, int64_t chunk_bytes,
+    uint32_t epoch, uint64_t timeout_ns, uint32_t* err) {
+  extern __shared__ __align__(128) uint8_t dyn[];
+  RepSmem& S = *reinterpret_cast<RepSmem*>(dyn);
+  uint8_t* stage = dyn + 128;
+  const int hop = blockIdx.x / ctas_per_hop;
+  const int j = blockIdx.x % ctas_per_hop;
+  if (hop >= n_hops) return;
+  const HopDev H = tab.h[hop];
+  if (threadIdx.x != 0) return;  // pure data movement: one elected thread
+  for (int s = 0; s < kRepStages; ++s) mbar_init(&S.full[s], 1);
+  fence_mbar_init();
+  const int64_t n_chunks = (nbytes + chunk_bytes - 1) / chunk_bytes;
+  uint32_t uses[kRepStages] = {0, 0, 0, 0};
+  for (int64_t c = j; c < n_chunks; c += ctas_per_hop) {
+    if (H.wait_flags && !wait_flag_sys(H.wait_flags + c, epoch, timeout_ns, err)) return;
+    if (!H.dst) continue;
+    const int64_t base = c * chunk_bytes;
+    const int64_t len = (nbytes - base < chunk_bytes) ? nbytes - base : chunk_bytes;
+    const int64_t npieces = (len + kRepPiece - 1) / kRepPiece;
+    fence_proxy_async_global();  // generic acquire above -> async-proxy reads below
+    auto piece_len = [&](int64_t i) {
+      const int64_t off = i * kRepPiece;
+      return static_cast<uint32_t>((len - off < kRepPiece) ? len - off : kRepPiece);
+    };
+    auto issue_load = [&](int64_t i) {
+      const int s = static_cast<int>(i % kRepStages);
+      mbar_arrive_expect_tx(&S.full[s], piece_len(i));
+      tma_load_1d(stage + s * kRepPiece, H.src + base + i * kRepPiece, piece_len(i), &S.full[s]);
+    };
+    const int64_t pro = npieces < kRepStages ? npieces : kRepStages;
+    for (int64_t i = 0; i < pro; ++i) issue_load(i);
+    for (int64_t i = 0; i < npieces; ++i) {
+      const int s = static_cast<int>(i % kRepStages);
+      mbar_wait(&S.full[s], uses[s] & 1);
+      ++uses[s];
+      tma_store_1d(H.dst + base + i * kRepPiece, stage + s * kRepPiece, piece_len(i));
+      bulk_commit();
+      if (i >= 1 && i - 1 + kRepStages < npieces) {
+        bulk_wait_read<1>();  // store i-1 has finished reading its stage
+        issue_load(i - 1 + kRepStages);
+      }
+    }
+    bulk_wait<0>();  // this chunk's writes are performed (visible at the peer)
+    if (H.signal_flags) {
+      fence_proxy_async_global();
+      __threadfence_system();
+      st_release_sys(H.signal_flags + c, epoch);
+    }
+  }
+  bulk_wait<0>();
+}
+
+// ------------------------------------------------ snapshot copy + isfinite
+constexpr int kSnapThreads = 256;
+
+template <int DT>
+__device__ __forceinline__ int first_nonfinite_in16(const uint4& v) {
+  if (DT == DVLA_F32) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if ((w[e] & 0x7f800000u) == 0x7f800000u) return e;
+  } else if (DT == DVLA_BF16) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t h = (e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xffffu);
+      if ((h & 0x7f80u) == 0x7f80u) return e;
+    }
+  } else if (DT == DVLA_F64) {
+    const unsigned long long d0 = (static_cast<unsigned long long>(v.y) << 32) | v.x;
+    const unsigned long long d1 = (static_cast<unsigned long long>(v.w) << 32) | v.z;
+    if ((d0 & 0x7ff0000000000000ull) == 0x7ff0000000000000ull) return 0;
+    if ((d1 & 0x7ff0000000000000ull) == 0x7ff0000000000000ull) return 1;
+  }
+  return -1;
+}
+
+// Grid-stride 16-byte copy with a fused finiteness scan; first bad element
+// index via atomicMin.  (HBM-bound: 2 bytes moved per byte snapshotted.)
+template <int DT>
+__global__ void __launch_bounds__(kSnapThreads) snapshot_kernel(const uint4* __restrict__ src,
+                                                                uint4* __restrict__ dst,
+                                                                int64_t nvec,
+                                                                unsigned long long* bad) {
+  constexpr int epv = DT == DVLA_F32 ? 4 : DT == DVLA_BF16 ? 8 : DT == DVLA_F64 ? 2 : 16;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  for (; i + 3 * stride < nvec; i += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(src + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      __stcs(dst + i + u * stride, v[u]);
+      if (DT != DVLA_U8) {
+        const int e = first_nonfinite_in16<DT>(v[u]);
+        if (e >= 0) atomicMin(bad, static_cast<unsigned long long>((i + u * stride) * epv + e));
+      }
+    }
+  }
+  for (; i < nvec; i += stride) {
+    const uint4 v = __ldcs(src + i);
+    __stcs(dst + i, v);
+    if (DT != DVLA_U8) {
+      const int e = first_nonfinite_in16<DT>(v);
+      if (e >= 0) atomicMin(bad, static_cast<unsigned long long>(i * epv + e));
+    }
+  }
+}
+
+__global__ void snapshot_tail_kernel(const uint8_t* src, uint8_t* dst, int64_t from, int64_t n,
+                                     int dtype, unsigned long long* bad) {
+  const int64_t i = from + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  dst[i] = src[i];
+  if (dtype == DVLA_F32 && (i % 4) == 3) {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(src + i - 3);
+    if ((w & 0x7f800000u) == 0x7f800000u) atomicMin(bad, static_cast<unsigned long long>(i / 4));
+  } else if (dtype == DVLA_BF16 && (i % 2) == 1) {
+    const uint32_t h = src[i - 1] | (static_cast<uint32_t>(src[i]) << 8);
+    if ((h & 0x7f80u) == 0x7f80u) atomicMin(bad, static_cast<unsigned long long>(i / 2));
+  }
+}
+
+// ------------------------------------------------------------ bytes_equal
+__global__ void bytes_equal_kernel(const uint4* __restrict__ a, const uint4* __restrict__ b,
+                                   int64_t nvec, unsigned long long* out) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  unsigned long long mism = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nvec;
+       i += stride) {
+    const uint4 x = __ldcs(a + i), y = __ldcs(b + i);
+    if (x.x != y.x || x.y != y.y || x.z != y.z || x.w != y.w) {
+      ++mism;
+      const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+      for (int e = 0; e < 4; ++e)
+        if (xs[e] != ys[e]) {
+          const uint32_t d = xs[e] ^ ys[e];
+          const int byte = (__ffs(static_cast<int>(d)) - 1) >> 3;
+          atomicMin(out + 1, static_cast<unsigned long long>(i * 16 + e * 4 + byte));
+          break;
+        }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) mism += __shfl_xor_sync(0xffffffffu, mism, o);
+  if ((threadIdx.x & 31) == 0 && mism) atomicAdd(out, mism);
+}
+
+__global__ void bytes_equal_tail_kernel(const uint8_t* a, const uint8_t* b, int64_t from,
+                                        int64_t n, unsigned long long* out) {
+  const int64_t i = from + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n && a[i] != b[i]) {
+    atomicAdd(out, 1ull);
+    atomicMin(out + 1, static_cast<unsigned long long>(i));
+  }
+}
+
+__global__ void init_u64_kernel(unsigned long long* p, unsigned long long v0,
+                                unsigned long long v1) {
+  p[0] = v0;
+  if (v1 != 0) p[1] = v1;
+}
+
+static int grid_for(int64_t nvec, int threads) {
+  const int sms = num_sms(current_device());
+  int64_t g = (nvec + threads - 1) / threads;
+  const int64_t cap = static_cast<int64_t>(sms) * 8;
+  if (g > cap) g = cap;
+  return static_cast<int>(g < 1 ? 1 : g);
+}
+
+}  // namespace dvla
+
+using namespace dvla;
+
+extern "C" int dvla_dev_alloc(int device, size_t bytes, void** out) {
+  if (!out) return fail(DVLA_ERR_USAGE, "null out pointer");
+  int prev = 0;
+  DVLA_CUDA_TRY(cudaGetDevice(&prev));
+  DVLA_CUDA_TRY(cudaSetDevice(device));
+  cudaError_t e = cudaMalloc(out, bytes ? bytes : 1);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess)
+    return fail(DVLA_ERR_CUDA, "cudaMalloc(%zu) on device %d failed: %s", bytes, device,
+                cudaGetErrorString(e));
+  return DVLA_OK;
+}
+
+extern "C" int dvla_dev_free(void* p) {
+  if (p) DVLA_CUDA_TRY(cudaFree(p));
+  return DVLA_OK;
+}
+
+extern "C" int dvla_ipc_handle(void* dev_ptr, uint8_t* handle_out) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  if (!dev_ptr || !handle_out) return fail(DVLA_ERR_USAGE, "null pointer argument");
+  cudaIpcMemHandle_t h;
+  DVLA_CUDA_TRY(cudaIpcGetMemHandle(&h, dev_ptr));
+  memcpy(handle_out, &h, 64);
+  return DVLA_OK;
+}
+
+extern "C" int dvla_ipc_open(const uint8_t* handle, void** out) {
+  if (!handle || !out) return fail(DVLA_ERR_USAGE, "null pointer argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  DVLA_CUDA_TRY(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+  return DVLA_OK;
+}
+
+extern "C" int dvla_ipc_close(void* p) {
+  if (p) DVLA_CUDA_TRY(cudaIpcCloseMemHandle(p));
+  return DVLA_OK;
+}
+
+extern "C" int dvla_enable_peer_access(int device, int peer) {
+  int prev = 0, can = 0;
+  DVLA_CUDA_TRY(cudaGetDevice(&prev));
+  DVLA_CUDA_TRY(cudaDeviceCanAccessPeer(&can, device, peer));
+  if (!can) return fail(DVLA_ERR_CUDA, "device %d cannot access peer %d", device, peer);
+  DVLA_CUDA_TRY(cudaSetDevice(device));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  cudaSetDevice(prev);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return DVLA_OK;
+  }
+  if (e != cudaSuccess)
+    return fail(DVLA_ERR_CUDA, "enable peer access %d->%d: %s", device, peer,
+                cudaGetErrorString(e));
+  return DVLA_OK;
+}
+
+extern "C" int dvla_replicate_chain(const dvla_hop* hops, int n_hops, int64_t nbytes,
+                                    int64_t chunk_bytes, uint32_t epoch, int ctas_per_hop,
+                                    uint64_t timeout_ns, uint32_t* err_dev, void* stream) {
+  if (n_hops < 1 || n_hops > kMaxHops)
+    return fail(DVLA_ERR_USAGE, "n_hops must be in [1, %d], got %d", kMaxHops, n_hops);
+  if (nbytes < 0 || chunk_bytes < 16 || (chunk_bytes % 16) != 0 || (nbytes % 16) != 0)
+    return fail(DVLA_ERR_USAGE,
+                "nbytes must be a multiple of 16 and chunk_bytes a positive multiple of 16");
+  if (ctas_per_hop < 1) return fail(DVLA_ERR_USAGE, "ctas_per_hop must be >= 1");
+  if (!err_dev) return fail(DVLA_ERR_USAGE, "null err pointer");
+  if (epoch == 0) return fail(DVLA_ERR_USAGE, "epoch must be >= 1 (flags start at 0)");
+  HopTable tab{};
+  for (int i = 0; i < n_hops; ++i) {
+    const dvla_hop& h = hops[i];
+    if (h.dst && !h.src) return fail(DVLA_ERR_USAGE, "hop %d has a destination but no source", i);
+    if ((h.src && reinterpret_cast<uintptr_t>(h.src) % 16) ||
+        (h.dst && reinterpret_cast<uintptr_t>(h.dst) % 16))
+      return fail(DVLA_ERR_USAGE, "hop %d pointers must be 16-byte aligned", i);
+    tab.h[i].src = static_cast<const uint8_t*>(h.src);
+    tab.h[i].dst = static_cast<uint8_t*>(h.dst);
+    tab.h[i].wait_flags = h.wait_flags;
+    tab.h[i].signal_flags = h.signal_flags;
+  }
+  if (nbytes == 0) return DVLA_OK;
+  const size_t smem = 128 + static_cast<size_t>(kRepStages) * kRepPiece;
+  static bool attr = false;
+  if (!attr) {
+    DVLA_CUDA_TRY(cudaFuncSetAttribute(replicate_chain_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+    attr = true;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaEvent_t stop;
+  prof_begin(st, &stop);
+  replicate_chain_kernel<<<n_hops * ctas_per_hop, kRepThreads, smem, st>>>(
+      tab, n_hops, ctas_per_hop, nbytes, chunk_bytes, epoch, timeout_ns, err_dev);
+  prof_end(st, stop);
+  return launch_check("replicate_chain_kernel");
+}
+
+extern "C" int dvla_snapshot_copy(const void* src, void* dst, int64_t nbytes, int dtype,
+                                  uint64_t* bad_index_dev, void* stream) {
+  if (nbytes < 0) return fail(DVLA_ERR_USAGE, "nbytes must be >= 0");
+  if ((!src || !dst || !bad_index_dev) && nbytes > 0)
+    return fail(DVLA_ERR_USAGE, "null pointer argument");
+  if (dtype != DVLA_F32 && dtype != DVLA_BF16 && dtype != DVLA_U8 && dtype != DVLA_F64)
+    return fail(DVLA_ERR_USAGE, "unsupported dtype %d", dtype);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* bad = reinterpret_cast<unsigned long long*>(bad_index_dev);
+  init_u64_kernel<<<1, 1, 0, st>>>(bad, ~0ull, 0);
+  if (nbytes == 0) return launch_check("init_u64_kernel");
+  const bool al = (reinterpret_cast<uintptr_t>(src) % 16 == 0) &&
+                  (reinterpret_cast<uintptr_t>(dst) % 16 == 0);
+  const int64_t nvec = al ? nbytes / 16 : 0;
+  cudaEvent_t stop;
+  prof_begin(st, &stop);
+  if (nvec > 0) {
+    const int g = grid_for(nvec, kSnapThreads);
+    const uint4* s4 = static_cast<const uint4*>(src);
+    uint4* d4 = static_cast<uint4*>(dst);
+    switch (dtype) {
+      case DVLA_F32: snapshot_kernel<DVLA_F32><<<g, kSnapThreads, 0, st>>>(s4, d4, nvec, bad); break;
+      case DVLA_BF16: snapshot_kernel<DVLA_BF16><<<g, kSnapThreads, 0, st>>>(s4, d4, nvec, bad); break;
+      case DVLA_F64: snapshot_kernel<DVLA_F64><<<g, kSnapThreads, 0, st>>>(s4, d4, nvec, bad); break;
+      default: snapshot_kernel<DVLA_U8><<<g, kSnapThreads, 0, st>>>(s4, d4, nvec, bad); break;
+    }
+  }
+  const int64_t from = nvec * 16;
+  if (from < nbytes) {
+    const int64_t rem = nbytes - from;
+    snapshot_tail_kernel<<<static_cast<unsigned>((rem + 255) / 256), 256, 0, st>>>(
+        static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), from, nbytes, dtype, bad);
+  }
+  prof_end(st, stop);
+  return launch_check("snapshot_kernel");
+}
+
+extern "C" int dvla_bytes_equal(const void* a, const void* b, int64_t nbytes, uint64_t* out_dev,
+                                void* stream) {
+  if (nbytes < 0) return fail(DVLA_ERR_USAGE, "nbytes must be >= 0");
+  if (!out_dev || ((!a || !b) && nbytes > 0)) return fail(DVLA_ERR_USAGE, "null pointer argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* out = reinterpret_cast<unsigned long long*>(out_dev);
+  init_u64_kernel<<<1, 1, 0, st>>>(out, 0ull, ~0ull);
+  if (nbytes == 0) return launch_check("init_u64_kernel");
+  const bool al = (reinterpret_cast<uintptr_t>(a) % 16 == 0) &&
+                  (reinterpret_cast<uintptr_t>(b) % 16 == 0);
+  const int64_t nvec = al ? nbytes / 16 : 0;
+  if (nvec > 0)
+    bytes_equal_kernel<<<grid_for(nvec, 256), 256, 0, st>>>(
+        static_cast<const uint4*>(a), static_cast<const uint4*>(b), nvec, out);
+  const int64_t from = nvec * 16;
+  if (from < nbytes)
+    bytes_equal_tail_kernel<<<static_cast<unsigned>((nbytes - from + 255) / 256), 256, 0, st>>>(
+        static_cast<const uint8_t*>(a), static_cast<const uint8_t*>(b), from, nbytes, out);
+  return launch_check("bytes_equal_kernel");
+}
+
+extern "C" int dvla_memcpy_async(void* dst, const void* src, int64_t nbytes, void* stream) {
+  if (nbytes < 0) return fail(DVLA_ERR_USAGE, "nbytes must be >= 0");
+  if (nbytes == 0) return DVLA_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaEvent_t stop;
+  prof_begin(st, &stop);
+  DVLA_CUDA_TRY(cudaMemcpyAsync(dst, src, static_cast<size_t>(nbytes), cudaMemcpyDefault, st));
+  prof_end(st, stop);
+  return DVLA_OK;
+}
