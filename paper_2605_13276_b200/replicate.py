@@ -1,0 +1,263 @@
+"""Weight snapshots and learner -> replica replication on B200.
+
+B200 replacement of the reference weight plane's data path:
+  core.snapshot_from_params (core.py:120-129)  -> device_snapshot (fused copy
+      + isfinite into a MODEL_COMPUTE region, csrc/replicate.cu)
+  ControlPlane.broadcast + Transport WIRE + wire weight frames
+      (planes.py:294-321, 101-128; wire.py:144-147, 227-237)
+      -> a chunked, pipelined TMA chain over NVLink into every replica's
+         pre-allocated region (ChainReplicator, LocalChain)
+  messages_equal on parameter bytes (wire.py:279-281) -> bytes_equal
+
+Process model: one process per GPU (torchrun).  Each rank owns its replica
+region(s) and a per-chunk flag array in device slabs; CUDA IPC handles are
+exchanged once over torch.distributed, after which a broadcast is one kernel
+per rank: the root streams its parameters into the first receiver, every
+receiver forwards each chunk to the next as soon as it landed, and the last
+receiver just waits for its flags.  n_buffers = staleness_limit + 1 replica
+regions per receiver give the latest-wins mailbox its double buffer.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from .core import ConfigError, ParamSnapshot, UsageError
+
+_DTYPE_CODE = None
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _code(t) -> int:
+    torch = _torch()
+    from . import _lib
+    return {torch.float32: _lib.F32, torch.bfloat16: _lib.BF16, torch.float64: _lib.F64}.get(
+        t.dtype, _lib.U8)
+
+
+def _stream_ptr(stream=None):
+    torch = _torch()
+    return (stream or torch.cuda.current_stream()).cuda_stream
+
+
+def device_snapshot(params, version: int, out=None, stream=None) -> ParamSnapshot:
+    """snapshot_from_params for a device tensor: fused copy + isfinite.
+
+    Raises ConfigError("non-finite parameter at flat index {i}") exactly as
+    the reference (core.py:123-125).  `out` may be a pool region view of at
+    least params.nbytes bytes (same dtype or uint8)."""
+    from . import _lib
+    torch = _torch()
+    if version < 0:
+        raise ConfigError(f"snapshot version must be >= 0, got {version}")
+    src = params.detach().reshape(-1)
+    if not src.is_contiguous():
+        src = src.contiguous()
+    nbytes = src.numel() * src.element_size()
+    dst = torch.empty_like(src) if out is None else out
+    if dst.numel() * dst.element_size() < nbytes:
+        raise UsageError(f"snapshot destination holds {dst.numel() * dst.element_size()} bytes, "
+                         f"need {nbytes}")
+    bad = torch.empty(1, dtype=torch.int64, device=src.device)
+    with torch.cuda.device(src.device):
+        _lib.check(_lib.dvla_snapshot_copy(src.data_ptr(), dst.data_ptr(), nbytes, _code(src),
+                                           bad.data_ptr(), _stream_ptr(stream)),
+                   "dvla_snapshot_copy")
+    b = int(bad.item()) & 0xFFFFFFFFFFFFFFFF
+    if b != 0xFFFFFFFFFFFFFFFF:
+        raise ConfigError(f"non-finite parameter at flat index {b}")
+    if out is not None and dst.dtype != src.dtype:
+        dst = dst[:nbytes].view(src.dtype)
+    return ParamSnapshot(version=int(version), params=dst[:src.numel()] if out is not None
+                         else dst)
+
+
+def bytes_equal(a, b, stream=None) -> tuple[int, int]:
+    """(number of differing 16-byte words, first differing byte or -1)."""
+    from . import _lib
+    torch = _torch()
+    na = a.numel() * a.element_size()
+    nb = b.numel() * b.element_size()
+    if na != nb:
+        return 1, min(na, nb)
+    out = torch.empty(2, dtype=torch.int64, device=a.device)
+    with torch.cuda.device(a.device):
+        _lib.check(_lib.dvla_bytes_equal(a.data_ptr(), b.data_ptr(), na, out.data_ptr(),
+                                         _stream_ptr(stream)), "dvla_bytes_equal")
+    mism, first = (int(x) for x in out.cpu().tolist())
+    return mism, (-1 if mism == 0 else first)
+
+
+def _hops(specs):
+    from . import _lib
+    arr = (_lib.Hop * len(specs))()
+    for i, (src, dst, wait, sig) in enumerate(specs):
+        arr[i].src, arr[i].dst, arr[i].wait_flags, arr[i].signal_flags = src, dst, wait, sig
+    return arr
+
+
+class _Slab:
+    """Device slab (cudaMalloc) + torch view; IPC-shareable."""
+
+    def __init__(self, nbytes: int, device: int):
+        torch = _torch()
+        from .pools import _DeviceSlab
+        self.slab = _DeviceSlab(nbytes, device)
+        self.t = torch.as_tensor(self.slab, device=torch.device("cuda", device))
+        self.ptr = self.slab.ptr
+
+    def ipc(self) -> bytes:
+        from . import _lib
+        buf = C.create_string_buffer(64)
+        _lib.check(_lib.dvla_ipc_handle(self.ptr, buf), "dvla_ipc_handle")
+        return buf.raw
+
+
+def _open_ipc(handle: bytes) -> int:
+    from . import _lib
+    p = C.c_void_p()
+    _lib.check(_lib.dvla_ipc_open(handle, C.byref(p)), "dvla_ipc_open")
+    return p.value
+
+
+class LocalChain:
+    """Chain replication between regions of ONE process (one GPU, or several
+    GPUs with peer access): all hops run in a single launch, so hops that
+    wait on each other are co-resident by construction.  Used for the
+    1-GPU parity tests and the co-located (N=1) replica."""
+
+    def __init__(self, nbytes: int, n_dst: int, device=None, chunk_bytes: int = 8 << 20,
+                 ctas_per_hop: int = 16, dsts=None):
+        torch = _torch()
+        if nbytes % 16:
+            raise UsageError("replicated regions must be a multiple of 16 bytes")
+        self.nbytes, self.n_dst = int(nbytes), int(n_dst)
+        self.chunk = int(chunk_bytes)
+        self.ctas = int(ctas_per_hop)
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.device = dev
+        self.n_chunks = (self.nbytes + self.chunk - 1) // self.chunk
+        self.dsts = dsts if dsts is not None else [
+            torch.empty(self.nbytes, dtype=torch.uint8, device=dev) for _ in range(n_dst)]
+        self.flags = torch.zeros((max(n_dst, 1), self.n_chunks), dtype=torch.int32, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.epoch = 0
+
+    def broadcast(self, src, stream=None, timeout_s: float = 10.0):
+        """Copy src's bytes into every destination through the chain."""
+        from . import _lib
+        if src.numel() * src.element_size() != self.nbytes:
+            raise UsageError("source size differs from the replicated region")
+        self.epoch += 1
+        specs = []
+        prev = src.data_ptr()
+        for i, d in enumerate(self.dsts):
+            wait = None if i == 0 else self.flags[i - 1].data_ptr()
+            specs.append((prev, d.data_ptr(), wait, self.flags[i].data_ptr()))
+            prev = d.data_ptr()
+        hops = _hops(specs)
+        torch = _torch()
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.dvla_replicate_chain(hops, len(specs), self.nbytes, self.chunk,
+                                                 self.epoch, self.ctas, int(timeout_s * 1e9),
+                                                 self.err.data_ptr(), _stream_ptr(stream)),
+                       "dvla_replicate_chain")
+
+    def check(self):
+        if int(self.err.item()):
+            from ._lib import ReplicationTimeout
+            raise ReplicationTimeout("replication chain flag wait timed out")
+
+
+class ChainReplicator:
+    """Cross-process chain broadcast over NVLink (one process per GPU).
+
+    Collective construction: every rank of `ranks` (default: all) calls it.
+    ranks[0] is the source; the others hold `n_buffers` replica regions of
+    `nbytes` each in device slabs (or in a MODEL_COMPUTE pool's slab).
+    """
+
+    def __init__(self, nbytes: int, ranks=None, n_buffers: int = 2, chunk_bytes: int = 16 << 20,
+                 ctas_per_hop: int = 32, group=None):
+        import torch.distributed as dist
+        torch = _torch()
+        if nbytes % 16:
+            raise UsageError("replicated regions must be a multiple of 16 bytes")
+        self.rank = dist.get_rank()
+        world = dist.get_world_size()
+        self.ranks = list(range(world)) if ranks is None else list(ranks)
+        self.nbytes, self.nb = int(nbytes), int(n_buffers)
+        self.chunk, self.ctas = int(chunk_bytes), int(ctas_per_hop)
+        self.n_chunks = (self.nbytes + self.chunk - 1) // self.chunk
+        self.dev = torch.cuda.current_device()
+        self.pos = self.ranks.index(self.rank) if self.rank in self.ranks else -1
+        self.err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.buf = None
+        self.flags = None
+        handles = None
+        if self.pos > 0:
+            self.buf = _Slab(self.nb * self.nbytes, self.dev)
+            flag_bytes = ((self.nb * self.n_chunks * 4 + 255) // 256) * 256
+            self.flags = _Slab(flag_bytes, self.dev)
+            self.flags.t.zero_()
+            torch.cuda.synchronize()
+            handles = (self.buf.ipc(), self.flags.ipc())
+        allh = [None] * world
+        dist.all_gather_object(allh, handles, group=group)
+        self.next_buf = self.next_flags = None
+        if 0 <= self.pos < len(self.ranks) - 1:
+            nxt = self.ranks[self.pos + 1]
+            bh, fh = allh[nxt]
+            self.next_buf = _open_ipc(bh)
+            self.next_flags = _open_ipc(fh)
+        self.epochs = [0] * self.nb
+
+    def replica(self, version: int):
+        """This receiver's region holding `version` (after broadcast)."""
+        if self.buf is None:
+            raise UsageError("the source rank holds no replica region")
+        b = version % self.nb
+        return self.buf.t[b * self.nbytes:(b + 1) * self.nbytes]
+
+    def broadcast(self, src, version: int, stream=None, timeout_s: float = 30.0):
+        """Enqueue this rank's hop of the chain for `version` (all ranks)."""
+        from . import _lib
+        torch = _torch()
+        if self.pos < 0:
+            return
+        b = version % self.nb
+        epoch = version + 1
+        off = b * self.nbytes
+        fl_off = b * self.n_chunks * 4
+        if self.pos == 0:
+            if src.numel() * src.element_size() != self.nbytes:
+                raise UsageError("source size differs from the replicated region")
+            s_ptr, wait = src.data_ptr(), None
+        else:
+            s_ptr, wait = self.buf.ptr + off, self.flags.ptr + fl_off
+        if self.next_buf is not None:
+            spec = (s_ptr, self.next_buf + off, wait, self.next_flags + fl_off)
+        else:  # last receiver: wait until every chunk landed
+            spec = (None, None, wait, None)
+        hops = _hops([spec])
+        _lib.check(_lib.dvla_replicate_chain(hops, 1, self.nbytes, self.chunk, epoch, self.ctas,
+                                             int(timeout_s * 1e9), self.err.data_ptr(),
+                                             _stream_ptr(stream)), "dvla_replicate_chain")
+
+    def check(self):
+        if int(self.err.item()):
+            from ._lib import ReplicationTimeout
+            raise ReplicationTimeout(f"rank {self.rank}: replication flag wait timed out")
+
+    def close(self):
+        from . import _lib
+        for p in (self.next_buf, self.next_flags):
+            if p:
+                _lib.dvla_ipc_close(p)
+        self.next_buf = self.next_flags = None
