@@ -47,6 +47,7 @@ def _args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--unfused", action="store_true")
+    ap.add_argument("--no-repl", action="store_true")
     return ap.parse_args()
 
 
@@ -171,6 +172,123 @@ def run_reference(a):
     return 0
 
 
+NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction
+NVLINK_NOMINAL_GBS = 900.0
+REPL_BYTES = 6_600_000_000  # pi0-3B-shaped bf16 weights (BASELINE config 3)
+
+
+def _bench_replication(world, rank, dev, barrier, max_over_ranks, iters=5):
+    """Weight replication GB/s: chain broadcast of REPL_BYTES from rank 0 to
+    every other rank (N >= 2), or into a co-located replica region (N = 1).
+    Bit-exactness is verified on every receiver."""
+    import torch
+    from paper_2605_13276_b200 import _lib
+    from paper_2605_13276_b200.replicate import ChainReplicator, LocalChain, bytes_equal
+    S = REPL_BYTES
+    gen = torch.Generator(device=dev).manual_seed(4242)
+    src = torch.randint(0, 256, (S,), dtype=torch.uint8, device=dev, generator=gen)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    out = {"bytes": S, "iters": iters}
+    if world == 1:
+        ch = LocalChain(S, 1, device=dev, chunk_bytes=64 << 20, ctas_per_hop=148)
+        ch.broadcast(src)
+        torch.cuda.synchronize()
+        ch.check()
+        mism, _ = bytes_equal(src, ch.dsts[0])
+        _lib.dvla_profile_enable(1)
+        e0.record(stream)
+        for _ in range(iters):
+            ch.broadcast(src)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        kms, kn = _lib.profile_collect()
+        _lib.dvla_profile_enable(0)
+        ms = e0.elapsed_time(e1) / iters
+        dst_ce = ch.dsts[0]
+        e0.record(stream)
+        for _ in range(iters):
+            _lib.dvla_memcpy_async(dst_ce.data_ptr(), src.data_ptr(), S, stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ce_ms = e0.elapsed_time(e1) / iters
+        peak, kind = _peaks()
+        out.update({"mode": "co-located replica (intra-HBM chain hop, TMA)",
+                    "gbs": S / (ms / 1e3) / 1e9, "ms": ms,
+                    "roofline": {"bound": "hbm", "achieved": 2 * S / (ms / 1e3) / 1e9,
+                                 "peak": peak, "unit": "GB/s",
+                                 "frac": 2 * S / (ms / 1e3) / 1e9 / peak,
+                                 "note": "2 bytes moved per replicated byte"},
+                    "ce_memcpy_gbs": S / (ce_ms / 1e3) / 1e9, "bit_exact": mism == 0,
+                    "kernel_ms": kms / max(kn, 1)})
+        del ch
+        return out
+    rep = ChainReplicator(S, n_buffers=2, chunk_bytes=32 << 20, ctas_per_hop=32)
+    expect = src  # every rank generated the same bytes (same seed)
+    rep.broadcast(src, 0)
+    torch.cuda.synchronize()
+    barrier()
+    rep.check()
+    ok = True if rank == 0 else bytes_equal(expect, rep.replica(0))[0] == 0
+    times = []
+    for it in range(1, iters + 1):
+        barrier()
+        e0.record(stream)
+        rep.broadcast(src, it)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(max_over_ranks(e0.elapsed_time(e1)))
+    rep.check()
+    if rank != 0:
+        ok = ok and bytes_equal(expect, rep.replica(iters))[0] == 0
+    ok_all = max_over_ranks(0.0 if ok else 1.0) == 0.0
+    ms = sorted(times)[len(times) // 2]
+    # copy-engine fan-out baseline (root pushes to every receiver)
+    ce = []
+    for it in range(3):
+        barrier()
+        e0.record(stream)
+        rep.ce_fanout(src, 0)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ce.append(max_over_ranks(e0.elapsed_time(e1)))
+    barrier()
+    rep.close()
+    gbs = S / (ms / 1e3) / 1e9
+    out.update({"mode": f"TMA chain 0->{'->'.join(str(r) for r in range(1, world))}",
+                "gbs": gbs, "ms": ms, "bit_exact": ok_all,
+                "roofline": {"bound": "nvlink", "achieved": gbs, "peak": NVLINK_PEER_GBS,
+                             "unit": "GB/s", "frac": gbs / NVLINK_PEER_GBS,
+                             "frac_of_nominal_900": gbs / NVLINK_NOMINAL_GBS,
+                             "peak_source": "B200_PROFILING.md measured peer copy (770 GB/s/dir)"},
+                "ce_fanout_gbs_per_receiver": S / (sorted(ce)[1] / 1e3) / 1e9})
+    return out
+
+
+def _bench_allreduce(world, dev, barrier, max_over_ranks, nbytes=1 << 30, iters=5):
+    """NCCL all-reduce of a learner gradient bucket (f32), busbw."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return None
+    g = torch.ones(nbytes // 4, dtype=torch.float32, device=dev)
+    dist.all_reduce(g)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(iters):
+        barrier()
+        e0.record(stream)
+        dist.all_reduce(g)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(max_over_ranks(e0.elapsed_time(e1)))
+    ms = sorted(ts)[len(ts) // 2]
+    busbw = nbytes * 2 * (world - 1) / world / (ms / 1e3) / 1e9
+    return {"bytes": nbytes, "ms": ms, "busbw_gbs": busbw, "dtype": "f32",
+            "frac_of_nominal_900": busbw / NVLINK_NOMINAL_GBS}
+
+
 def run_ours(a):
     import numpy as np
     import torch
@@ -291,6 +409,10 @@ def run_ours(a):
                "steps": e_steps, "ms_per_step": ems / e_steps}
         del h_logits, d_logits
 
+    del dl
+    repl = None if a.no_repl else _bench_replication(world, rank, dev, barrier, max_over_ranks)
+    allreduce = _bench_allreduce(world, dev, barrier, max_over_ranks)
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         threads = len(os.sched_getaffinity(0))
@@ -311,6 +433,7 @@ def run_ours(a):
                        "parallelism": f"dp{world} (group-sharded learner)",
                        "l2": "inputs 1.84 GB/rank > 126 MB L2 (no flush needed)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "replication": repl, "grad_allreduce": allreduce,
             "gpu_launches": 3 * a.steps, "clocks": clk,
             "loss": st["loss"], "mean_ratio": st["mean_ratio"],
             "clip_fraction": st["clip_fraction"],

@@ -217,6 +217,23 @@ class ChainReplicator:
             self.next_buf = _open_ipc(bh)
             self.next_flags = _open_ipc(fh)
         self.epochs = [0] * self.nb
+        # root also maps every receiver region (copy-engine fan-out baseline)
+        self.fan_bufs = []
+        if self.pos == 0:
+            for r in self.ranks[1:]:
+                self.fan_bufs.append(self.next_buf if r == self.ranks[1] else _open_ipc(allh[r][0]))
+
+    def ce_fanout(self, src, version: int, stream=None):
+        """Baseline: root copies into every receiver with cudaMemcpyAsync
+        (copy engines, 1 -> k direct fan-out).  No flags: time it with a
+        barrier + synchronize.  Root only."""
+        from . import _lib
+        if self.pos != 0:
+            return
+        off = (version % self.nb) * self.nbytes
+        for p in self.fan_bufs:
+            _lib.check(_lib.dvla_memcpy_async(p + off, src.data_ptr(), self.nbytes,
+                                              _stream_ptr(stream)), "dvla_memcpy_async")
 
     def replica(self, version: int):
         """This receiver's region holding `version` (after broadcast)."""
@@ -257,7 +274,8 @@ class ChainReplicator:
 
     def close(self):
         from . import _lib
-        for p in (self.next_buf, self.next_flags):
+        for p in set([self.next_buf, self.next_flags] + list(self.fan_bufs)):
             if p:
                 _lib.dvla_ipc_close(p)
         self.next_buf = self.next_flags = None
+        self.fan_bufs = []
