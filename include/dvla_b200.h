@@ -126,6 +126,47 @@ int dvla_grpo_epilogue(const double* lp_chunk, const float* blp, const double* b
                        int64_t G, int64_t C, double clip_eps, double kl_coeff,
                        double* coeff_out, double* stats, void* stream);
 
+/* ------------------------------------- Gaussian head + reference policy */
+
+/* kernels.mlp_forward (numba_backend.py:27-46): tanh MLP means, f64
+ * accumulate, f32 out.  w1 [H,O], b1 [H], w2 [D,H], b2 [D], obs [B,O]. */
+int dvla_mlp_forward(const float* w1, const float* b1, const float* w2, const float* b2,
+                     const float* obs, int64_t B, int obs_dim, int hidden, int out_dim,
+                     float* out, void* stream);
+/* kernels.chunk_log_prob (numba_backend.py:49-61): joint diagonal-Gaussian
+ * log-density per row, f64.  means/actions [B,D] f32, log_std [D] f32. */
+int dvla_chunk_log_prob(const float* means, const float* log_std, const float* actions,
+                        int64_t B, int D, double* out, void* stream);
+size_t dvla_policy_backward_workspace_bytes(int64_t B, int hidden, int out_dim);
+/* kernels.policy_backward (numba_backend.py:64-113): out[n_params] +=
+ * sum_b coeffs[b] * d lp_b / d params, canonical flat order
+ * [W1, b1, W2, b2, log_std]; deterministic row order. */
+int dvla_policy_backward(const float* w1, const float* b1, const float* w2, const float* b2,
+                         const float* log_std, const float* obs, const float* actions,
+                         const double* coeffs, int64_t B, int obs_dim, int hidden, int out_dim,
+                         double* out, void* workspace, void* stream);
+/* Head-only Gaussian backward for large action experts (config 3):
+ * dmeans[B,D] = c_b eps e^{-s} (f32, may be NULL); dlog_std[D] += sum_b
+ * c_b (eps^2 - 1) (f64, may be NULL). */
+int dvla_gauss_head_backward(const float* means, const float* log_std, const float* actions,
+                             const double* coeffs, int64_t B, int D, float* dmeans,
+                             double* dlog_std, void* stream);
+
+/* ----------------------------------------------------- optimizer tail */
+
+/* adam_step (grpo.py:137-150) in place: f32 params, f64 grad/m/v; step is the
+ * new step count (>= 1).  Bit-identical to the reference's numpy arithmetic. */
+int dvla_adam_step(float* params, const double* grad, double* m, double* v, int64_t n,
+                   int64_t step, double lr, double beta1, double beta2, double eps,
+                   void* stream);
+size_t dvla_grad_norm_workspace_bytes(int64_t n);
+/* clip_grad_norm (grpo.py:297-301): *norm_out = ||grad||; scales in place if
+ * max_norm > 0 and norm > max_norm; *nonfinite_out |= any non-finite. */
+int dvla_grad_norm(double* grad, int64_t n, double max_norm, double* norm_out,
+                   uint32_t* nonfinite_out, void* workspace, void* stream);
+/* *flag_out |= any non-finite f32 (runtime.py:793-795 RunAbort check). */
+int dvla_f32_nonfinite(const float* p, int64_t n, uint32_t* flag_out, void* stream);
+
 /* --------------------------------------------------- dual-pool arena */
 
 /* PoolKind (pools.py:23-26) */

@@ -154,3 +154,20 @@ dvla_replicate_chain = _proto("dvla_replicate_chain", [
 dvla_snapshot_copy = _proto("dvla_snapshot_copy", [_vp, _vp, _i64, _i32, _vp, _vp])
 dvla_bytes_equal = _proto("dvla_bytes_equal", [_vp, _vp, _i64, _vp, _vp])
 dvla_memcpy_async = _proto("dvla_memcpy_async", [_vp, _vp, _i64, _vp])
+
+# ---------------------------------------------- Gaussian head / MLP policy
+dvla_mlp_forward = _proto("dvla_mlp_forward", [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32,
+                                               _vp, _vp])
+dvla_chunk_log_prob = _proto("dvla_chunk_log_prob", [_vp, _vp, _vp, _i64, _i32, _vp, _vp])
+dvla_policy_backward_workspace_bytes = _proto("dvla_policy_backward_workspace_bytes",
+                                              [_i64, _i32, _i32], _sz)
+dvla_policy_backward = _proto("dvla_policy_backward", [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                                       _i64, _i32, _i32, _i32, _vp, _vp, _vp])
+dvla_gauss_head_backward = _proto("dvla_gauss_head_backward", [_vp, _vp, _vp, _vp, _i64, _i32,
+                                                               _vp, _vp, _vp])
+# ------------------------------------------------------------ optimizer
+dvla_adam_step = _proto("dvla_adam_step", [_vp, _vp, _vp, _vp, _i64, _i64, _f64, _f64, _f64,
+                                           _f64, _vp])
+dvla_grad_norm_workspace_bytes = _proto("dvla_grad_norm_workspace_bytes", [_i64], _sz)
+dvla_grad_norm = _proto("dvla_grad_norm", [_vp, _i64, _f64, _vp, _vp, _vp, _vp])
+dvla_f32_nonfinite = _proto("dvla_f32_nonfinite", [_vp, _i64, _vp, _vp])

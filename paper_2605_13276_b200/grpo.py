@@ -370,3 +370,187 @@ def grpo_token_grad(logits, tokens, behavior_log_prob, rewards, group_ids, cfg: 
     st = tl.stats(rewards)
     st["lp_chunk"] = tl.lp_chunk.view(n_groups, G, C)
     return st["loss"], (dlogits if write_dlogits else None), st
+
+
+# ------------------------------------------------------------------------
+# Reference-shaped learner for the Gaussian tanh-MLP chunk policy
+# ------------------------------------------------------------------------
+
+@dataclass
+class AdamState:
+    """Adam moments (f64) and step count (reference grpo.py:122-134); m/v
+    may be numpy arrays or device tensors (e.g. MODEL_COMPUTE pool views)."""
+
+    m: object
+    v: object
+    step: int = 0
+
+    @classmethod
+    def zeros(cls, n: int, m_buf=None, v_buf=None) -> "AdamState":
+        m = np.zeros(n, dtype=np.float64) if m_buf is None else m_buf
+        v = np.zeros(n, dtype=np.float64) if v_buf is None else v_buf
+        m[:] = 0.0
+        v[:] = 0.0
+        return cls(m=m, v=v)
+
+
+def _is_t(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def adam_step(flat_params, grad, state: AdamState, cfg: GrpoConfig):
+    """One bias-corrected Adam step in place on flat_params (f32), on the
+    GPU (csrc/optim.cu), element-wise identical to reference grpo.py:137-150."""
+    from . import _lib
+    from .policy import to_dev
+    torch = _torch()
+    p = flat_params if (_is_t(flat_params) and flat_params.is_cuda) else to_dev(flat_params)
+    g = to_dev(grad, torch.float64)
+    m = state.m if (_is_t(state.m) and state.m.is_cuda) else to_dev(state.m, torch.float64)
+    v = state.v if (_is_t(state.v) and state.v.is_cuda) else to_dev(state.v, torch.float64)
+    state.step += 1
+    _lib.check(_lib.dvla_adam_step(p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(),
+                                   p.numel(), state.step, float(cfg.lr), float(cfg.beta1),
+                                   float(cfg.beta2), float(cfg.opt_eps), _stream_ptr()),
+               "dvla_adam_step")
+    for host, dev in ((state.m, m), (state.v, v)):
+        if not (_is_t(host) and host.is_cuda):
+            host[:] = dev.cpu().numpy() if not _is_t(host) else dev.cpu()
+    if not (_is_t(flat_params) and flat_params.is_cuda):
+        flat_params[:] = p.cpu().numpy() if not _is_t(flat_params) else p.cpu()
+    return flat_params
+
+
+def clip_grad_norm(grad, max_norm: float | None) -> float:
+    """L2 norm of grad; scales grad in place when norm > max_norm > 0
+    (reference grpo.py:297-301)."""
+    from . import _lib
+    from .policy import to_dev
+    torch = _torch()
+    g = grad if (_is_t(grad) and grad.is_cuda) else to_dev(grad, torch.float64)
+    n = g.numel()
+    ws = torch.empty(_lib.dvla_grad_norm_workspace_bytes(n), dtype=torch.uint8, device=g.device)
+    norm = torch.empty(1, dtype=torch.float64, device=g.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=g.device)
+    mx = float(max_norm) if max_norm is not None else 0.0
+    _lib.check(_lib.dvla_grad_norm(g.data_ptr(), n, mx, norm.data_ptr(), flag.data_ptr(),
+                                   ws.data_ptr(), _stream_ptr()), "dvla_grad_norm")
+    if not (_is_t(grad) and grad.is_cuda):
+        grad[:] = g.cpu().numpy() if not _is_t(grad) else g.cpu()
+    return float(norm.item())
+
+
+def _ordered(batches) -> list:
+    return sorted(batches, key=lambda b: b.group_id)
+
+
+def _stack_batches(batches, cfg: GrpoConfig):
+    """Device tensors of a list of GroupBatch in INPUT order + canonical order."""
+    from .policy import to_dev
+    torch = _torch()
+    ordered = _ordered(batches)
+    for b in ordered:  # group-size check in canonical order (grpo.py:235-236)
+        if b.g != cfg.group_size:
+            raise ConfigError(f"group {b.group_id} has {b.g} trajectories, "
+                              f"expected G={cfg.group_size}")
+    ids = np.array([b.group_id for b in batches], dtype=np.int64)
+    order = canonical_order(ids)
+
+    def stack(attr, dtype):
+        xs = [getattr(b, attr) for b in batches]
+        if all(_is_t(x) for x in xs):
+            return torch.stack([x.to(dtype) for x in xs]).to(_dev()).contiguous()
+        return to_dev(np.stack([np.asarray(x.cpu() if _is_t(x) else x) for x in xs]), dtype)
+
+    obs = stack("obs", torch.float32)
+    act = stack("actions", torch.float32)
+    blp = stack("behavior_log_prob", torch.float32)
+    rw = stack("rewards", torch.float32)
+    return ids, order, obs, act, blp, rw
+
+
+def grpo_grad(params, batches, cfg: GrpoConfig, out_grad=None):
+    """Micro-batched GRPO loss + gradient for the Gaussian MLP policy
+    (reference grpo.py:217-294) on the GPU: mlp_forward -> chunk_log_prob ->
+    group advantages -> canonical-order epilogue -> policy_backward.
+
+    Returns (loss, grad_sum f64 flat, stats) with the reference's stats keys
+    and GrpoAbort / ConfigError contract.  grad is numpy when params are
+    numpy, a device tensor when params are device tensors."""
+    from . import _lib
+    from .policy import _dims, _dparams, chunk_log_prob_dev, mlp_forward_dev, policy_backward_dev
+    torch = _torch()
+    cfg.validate()
+    if not batches:
+        raise ConfigError("grpo update needs at least one group")
+    ids, order, obs, act, blp, rw = _stack_batches(batches, cfg)
+    n_groups, G, C = blp.shape
+    o, h, d = _dims(params)
+    dev = obs.device
+    n_traj = n_groups * G
+    adv = torch.empty(n_traj, dtype=torch.float64, device=dev)
+    bad = torch.empty(n_groups, dtype=torch.int32, device=dev)
+    _lib.check(_lib.dvla_group_advantages(rw.data_ptr(), n_groups, G, float(cfg.adv_epsilon),
+                                          adv.data_ptr(), bad.data_ptr(), _stream_ptr()),
+               "dvla_group_advantages")
+    dp = _dparams(params)
+    means = mlp_forward_dev(dp, obs.reshape(-1, o), o, h, d)
+    lp = chunk_log_prob_dev(means, dp[4], act.reshape(-1, d))
+    coeff = torch.empty(n_traj * C, dtype=torch.float64, device=dev)
+    stats = torch.zeros(_lib.ST_LEN, dtype=torch.float64, device=dev)
+    order_d = torch.from_numpy(order).to(dev)
+    ids_d = torch.from_numpy(ids).to(dev)
+    _lib.check(_lib.dvla_grpo_epilogue(lp.data_ptr(), blp.data_ptr(), None, adv.data_ptr(),
+                                       bad.data_ptr(), order_d.data_ptr(), ids_d.data_ptr(),
+                                       n_groups, G, C, float(cfg.clip_eps), float(cfg.kl_coeff),
+                                       coeff.data_ptr(), stats.data_ptr(), _stream_ptr()),
+               "dvla_grpo_epilogue")
+    st = stats_from_vector(stats.cpu().numpy(), ids, order, n_traj,
+                           rw.reshape(n_groups, G).cpu().numpy())
+    grad = torch.zeros(h * o + h + d * h + d + d, dtype=torch.float64, device=dev)
+    policy_backward_dev(dp, obs.reshape(-1, o), act.reshape(-1, d), coeff, grad, o, h, d)
+    if not np.isfinite(st["loss"]) or not bool(torch.isfinite(grad).all()):
+        raise GrpoAbort(int(ids[order[0]]), "non-finite loss or gradient")
+    if out_grad is not None:
+        if _is_t(out_grad):
+            out_grad.copy_(grad)
+            grad = out_grad
+        else:
+            out_grad[:] = grad.cpu().numpy()
+            grad = out_grad
+    elif not _is_t(params.w1):
+        grad = grad.cpu().numpy()
+    return float(st["loss"]), grad, st
+
+
+def grpo_loss(params, batches, cfg: GrpoConfig) -> float:
+    """Scalar surrogate loss (reference grpo.py:194-214), from the same GPU
+    forward + epilogue as grpo_grad (the independent f64 finite-difference
+    path of the reference lives in the test oracle, oracle/grpo_oracle.py)."""
+    loss, _, _ = grpo_grad(params, batches, cfg)
+    return loss
+
+
+def infer_policy_config(params):
+    from .policy import PolicyConfig
+    hidden, obs_dim = tuple(params.w1.shape)
+    out_dim = tuple(params.w2.shape)[0]
+    return PolicyConfig(obs_dim=obs_dim, hidden=hidden, chunk=out_dim // 2, act_dim=2)
+
+
+def grpo_update(params, batches, cfg: GrpoConfig, adam: AdamState, version: int):
+    """grad, optional norm clip, Adam (reference grpo.py:304-320)."""
+    from .policy import flatten, unflatten
+    loss, grad, stats = grpo_grad(params, batches, cfg)
+    norm = clip_grad_norm(grad, cfg.max_grad_norm)
+    flat = flatten(params)
+    adam_step(flat, grad, adam, cfg)
+    new_params = unflatten(infer_policy_config(params), flat)
+    ustats = UpdateStats(
+        version=version + 1, loss=loss, mean_ratio=stats["mean_ratio"],
+        clip_fraction=stats["clip_fraction"], grad_norm=norm,
+        mean_reward=stats["mean_reward"], n_traj=stats["n_traj"],
+        n_groups=stats["n_groups"], n_chunks=stats["n_chunks"],
+        group_ids=stats["group_ids"],
+    )
+    return new_params, ustats

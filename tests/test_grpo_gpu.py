@@ -1,0 +1,218 @@
+"""Reference-shaped learner on the GPU vs golden vectors produced by the
+reference itself (tests/golden/make_golden.py): advantages (bitwise), the
+Gaussian-MLP grpo_grad, Adam (bitwise), kernels, aborts."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import grpo_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _tags(g):
+    return sorted({k.rsplit("_", 1)[0] for k in g.files if k.endswith("_loss")})
+
+
+def _case(g, tag):
+    from paper_2605_13276_b200.grpo import GroupBatch
+    from paper_2605_13276_b200.policy import PolicyParams
+    params = PolicyParams(w1=g[f"{tag}_w1"].copy(), b1=g[f"{tag}_b1"].copy(),
+                          w2=g[f"{tag}_w2"].copy(), b2=g[f"{tag}_b2"].copy(),
+                          log_std=g[f"{tag}_log_std"].copy())
+    batches = []
+    for k, gid in enumerate(g[f"{tag}_group_ids"]):
+        batches.append(GroupBatch(
+            group_id=int(gid), horizon=8, chunk=4, obs=g[f"{tag}_obs"][k].copy(),
+            actions=g[f"{tag}_actions"][k].copy(), behavior_log_prob=g[f"{tag}_blp"][k].copy(),
+            rewards=g[f"{tag}_rewards"][k].copy(), behavior_version=0))
+    return params, batches
+
+
+def test_advantages_bitwise_against_reference(dev):
+    from paper_2605_13276_b200.grpo import compute_advantages
+    g = golden("advantages")
+    offs = g["offsets"]
+    for a, b in zip(offs[:-1], offs[1:]):
+        got = compute_advantages(g["rewards"][a:b], float(g["delta"]))
+        assert got.dtype == np.float64
+        assert np.array_equal(got, g["adv"][a:b]), (a, b)
+
+
+def test_advantages_known_answers(dev):
+    from paper_2605_13276_b200.grpo import compute_advantages
+    np.testing.assert_allclose(compute_advantages([1.0, 0.0, 0.0, 1.0], 1e-8), [1, -1, -1, 1],
+                               rtol=1e-7)
+    assert np.all(compute_advantages([1.0, 1.0, 1.0, 1.0], 1e-8) == 0.0)
+    from paper_2605_13276_b200.core import ConfigError
+    with pytest.raises(ConfigError):
+        compute_advantages([1.0], 1e-8)
+
+
+def test_grpo_grad_matches_reference_golden(dev):
+    from paper_2605_13276_b200 import grpo
+    g = golden("grpo_gauss")
+    tags = _tags(g)
+    assert len(tags) == 12
+    for tag in tags:
+        params, batches = _case(g, tag)
+        cfg = grpo.GrpoConfig(group_size=4, clip_eps=0.2, adv_epsilon=1e-8, micro_batch=4,
+                              lr=1e-3, kl_coeff=float(g[f"{tag}_kl"]))
+        loss, grad, st = grpo.grpo_grad(params, batches, cfg)
+        ref = g[f"{tag}_grad"]
+        # the reference's default numba backend evaluates part of the
+        # log-density in f32 (see tests/test_oracle.py): pin at its own
+        # inter-backend tolerance, and tighter against the f64 oracle below
+        assert loss == pytest.approx(float(g[f"{tag}_loss"]), abs=1e-6)
+        assert np.abs(grad - ref).max() <= 1e-5 * np.abs(ref).max()
+        rs = g[f"{tag}_stats"]
+        assert st["mean_ratio"] == pytest.approx(rs[1], rel=1e-6)
+        assert st["clip_fraction"] == rs[2] and st["n_chunks"] == rs[3]
+        assert st["mean_reward"] == rs[4]
+        # against the f64 oracle restatement: much tighter
+        oloss, ograd, _ = O.grpo_grad_gauss(
+            params.w1, params.b1, params.w2, params.b2, params.log_std,
+            g[f"{tag}_group_ids"], g[f"{tag}_obs"], g[f"{tag}_actions"], g[f"{tag}_blp"],
+            g[f"{tag}_rewards"], kl_coeff=cfg.kl_coeff)
+        assert loss == pytest.approx(oloss, rel=1e-9, abs=1e-13)
+        assert np.abs(grad - ograd).max() <= 1e-9 * np.abs(ograd).max()
+
+
+def test_batch_order_is_canonicalised_bitwise(dev):
+    from paper_2605_13276_b200 import grpo
+    g = golden("grpo_gauss")
+    params, batches = _case(g, "s5_kl0")
+    cfg = grpo.GrpoConfig(group_size=4, micro_batch=4)
+    la, ga, sa = grpo.grpo_grad(params, batches, cfg)
+    lb, gb, sb = grpo.grpo_grad(params, batches[::-1], cfg)
+    assert la == lb and sa["group_ids"] == sb["group_ids"] == [0, 1]
+    np.testing.assert_allclose(ga, gb, rtol=1e-13, atol=1e-16)
+
+
+def test_aborts_carry_group_and_message(dev):
+    from paper_2605_13276_b200 import grpo
+    from paper_2605_13276_b200.core import ConfigError
+    g = golden("grpo_gauss")
+    cfg = grpo.GrpoConfig(group_size=4, micro_batch=4)
+    params, batches = _case(g, "s1_kl0")
+    batches[1].rewards[0] = np.nan
+    with pytest.raises(grpo.GrpoAbort, match="group 1.*non-finite reward") as exc:
+        grpo.grpo_grad(params, batches, cfg)
+    assert exc.value.group_id == 1
+    params, batches = _case(g, "s2_kl0")
+    params.w2[0, 0] = np.nan
+    with pytest.raises(grpo.GrpoAbort, match="non-finite log-prob"):
+        grpo.grpo_grad(params, batches, cfg)
+    params, batches = _case(g, "s6_kl0")
+    batches[0].behavior_log_prob[:] = -1e6
+    with pytest.raises(grpo.GrpoAbort, match="non-finite importance ratio"):
+        grpo.grpo_grad(params, batches, cfg)
+    with pytest.raises(ConfigError, match="at least one group"):
+        grpo.grpo_grad(params, [], cfg)
+    params, batches = _case(g, "s0_kl0")
+    with pytest.raises(ConfigError, match="group 0 has 4"):
+        grpo.grpo_grad(params, batches, grpo.GrpoConfig(group_size=8))
+
+
+def test_adam_is_bitwise_on_the_reference_gradient(dev):
+    from paper_2605_13276_b200 import grpo
+    g = golden("grpo_gauss")
+    cfg = grpo.GrpoConfig(lr=1e-3)
+    for seed in range(10):
+        tag = f"s{seed}_kl0"
+        flat = np.concatenate([g[f"{tag}_{k}"].ravel() for k in ("w1", "b1", "w2", "b2",
+                                                                  "log_std")]).astype(np.float32)
+        st = grpo.AdamState.zeros(flat.size)
+        grpo.adam_step(flat, g[f"{tag}_grad"].copy(), st, cfg)
+        assert st.step == 1
+        assert np.array_equal(flat, g[f"{tag}_updated"]), seed
+
+
+def test_adam_known_answers(dev):
+    from paper_2605_13276_b200 import grpo
+    p = np.zeros(3, dtype=np.float32)
+    st = grpo.AdamState.zeros(3)
+    out = grpo.adam_step(p, np.ones(3), st, grpo.GrpoConfig(lr=0.1))
+    assert out is p
+    np.testing.assert_allclose(p, -0.1, rtol=1e-6)
+    for scale in (1e-3, 1.0, 1e3):
+        q = np.zeros(2, dtype=np.float32)
+        grpo.adam_step(q, np.full(2, scale), grpo.AdamState.zeros(2), grpo.GrpoConfig(lr=0.05))
+        np.testing.assert_allclose(q, -0.05, rtol=1e-5)
+
+
+def test_clip_grad_norm(dev):
+    from paper_2605_13276_b200 import grpo
+    gv = np.array([3.0, 4.0])
+    assert grpo.clip_grad_norm(gv, 2.5) == pytest.approx(5.0)
+    np.testing.assert_allclose(gv, [1.5, 2.0])
+    g2 = np.array([3.0, 4.0])
+    assert grpo.clip_grad_norm(g2, None) == pytest.approx(5.0)
+    np.testing.assert_allclose(g2, [3.0, 4.0])
+
+
+def test_grpo_update_matches_reference(dev):
+    from paper_2605_13276_b200 import grpo
+    from paper_2605_13276_b200.policy import flatten
+    g = golden("grpo_gauss")
+    params, batches = _case(g, "s8_kl0")
+    cfg = grpo.GrpoConfig(group_size=4, micro_batch=4, lr=1e-3)
+    adam = grpo.AdamState.zeros(params.n_params)
+    newp, ust = grpo.grpo_update(params, batches, cfg, adam, 4)
+    assert ust.version == 5 and adam.step == 1
+    assert ust.n_traj == 8 and ust.n_groups == 2 and ust.n_chunks == 16
+    np.testing.assert_allclose(flatten(newp), g["s8_kl0_updated"], rtol=0, atol=2e-7)
+    assert ust.grad_norm == pytest.approx(float(g["s8_kl0_grad_norm"]), rel=1e-5)
+
+
+def test_kernels_match_reference_backend(dev):
+    from paper_2605_13276_b200 import kernels
+    g = golden("kernels")
+    np.testing.assert_allclose(kernels.chunk_log_prob(g["means"], g["log_std"], g["actions"]),
+                               g["lp"], rtol=1e-6)
+    np.testing.assert_allclose(kernels.mlp_forward(g["w1"], g["b1"], g["w2"], g["b2"], g["obs"]),
+                               g["mlp_out"], rtol=1e-6, atol=1e-6)
+    out = np.zeros_like(g["backward"])
+    kernels.policy_backward(g["w1"], g["b1"], g["w2"], g["b2"], g["ls2"], g["obs"], g["act"],
+                            g["coeffs"], out)
+    np.testing.assert_allclose(out, g["backward"], rtol=1e-5, atol=1e-6 * np.abs(out).max())
+    # accumulates (+=), like the reference
+    kernels.policy_backward(g["w1"], g["b1"], g["w2"], g["b2"], g["ls2"], g["obs"], g["act"],
+                            g["coeffs"], out)
+    np.testing.assert_allclose(out, 2 * g["backward"], rtol=1e-5, atol=2e-6 * np.abs(out).max())
+
+
+def test_policy_closed_forms(dev):
+    from paper_2605_13276_b200.policy import PolicyParams, backward, log_prob_of
+    LOG_2PI = float(np.log(2 * np.pi))
+    z = lambda ls: PolicyParams(w1=np.zeros((4, 3), np.float32), b1=np.zeros(4, np.float32),
+                                w2=np.zeros((2, 4), np.float32), b2=np.zeros(2, np.float32),
+                                log_std=np.full(2, ls, np.float32))
+    obs = np.zeros(3, np.float32)
+    assert log_prob_of(z(0.0), obs, np.zeros(2, np.float32)) == pytest.approx(-LOG_2PI, abs=1e-6)
+    assert log_prob_of(z(0.0), obs, np.array([1.0, 0.0], np.float32)) == pytest.approx(
+        -2.337877, abs=1e-5)
+    at = log_prob_of(z(-0.3), obs, np.zeros(2, np.float32))
+    sh = np.array([np.exp(-0.3), 0.0], np.float32)
+    assert log_prob_of(z(-0.3), obs, sh) == pytest.approx(at - 0.5, abs=1e-5)
+    gr = backward(z(0.2), obs, np.zeros(2, np.float32), upstream=2.0)
+    np.testing.assert_allclose(gr[-2:], -2.0, rtol=1e-6)
+
+
+def test_gauss_head_backward_c3_shape(dev):
+    """pi0-shaped action expert head (BASELINE config 3): D = 1,600."""
+    import torch
+    from paper_2605_13276_b200 import kernels
+    rng = np.random.default_rng(0)
+    B, D = 512, 1600
+    means = rng.normal(0, 1, (B, D)).astype(np.float32)
+    actions = rng.normal(0, 1, (B, D)).astype(np.float32)
+    log_std = rng.normal(0, 0.1, D).astype(np.float32)
+    c = rng.normal(0, 1e-3, B)
+    lp = kernels.chunk_log_prob(means, log_std, actions)
+    np.testing.assert_allclose(lp, O.chunk_log_prob(means, log_std, actions), rtol=1e-12)
+    dm, dls = kernels.gauss_head_backward(means, log_std, actions, c)
+    odm, odls = O.gauss_head_backward(means, log_std, actions, c)
+    np.testing.assert_allclose(dm, odm, rtol=1e-6, atol=1e-12)
+    np.testing.assert_allclose(dls, odls, rtol=1e-10, atol=1e-14)
