@@ -1,0 +1,551 @@
+"""The four-lane swimlane on B200: sampler, weight-receive, trainer and
+weight-distribution lanes as host threads, each driving its own CUDA stream.
+
+Mirrors the coordination of reference pkg/src/dvla/runtime.py (LaneId :53-57,
+RunAbort :65-79, Monitor :120-156, VersionBoard busy-mode gate :211-564,
+GradReducer :569-637, SamplerWorker :655-729, TrainerWorker :732-800,
+_run_async lanes :1157-1318) with the data plane kept on the device:
+
+  * rollouts are produced on the SAMPLER stream and handed to the trainer as
+    device-resident GroupBatch objects through a bounded Channel (zero copy);
+  * the TRAINER stream runs the fused token loss (csrc/token_loss.cu), the
+    head-gradient GEMM (cuBLAS), the NCCL gradient all-reduce (multi-GPU) and
+    Adam (csrc/optim.cu);
+  * the WEIGHT_DIST stream snapshots the parameters into a double-buffered
+    MODEL_COMPUTE region (fused copy + isfinite) and broadcasts it;
+  * the WEIGHT_RECV lane installs the newest snapshot at epoch boundaries
+    (latest-wins mailbox + staleness gate), a pointer swap -- no copy.
+Cross-stream ordering uses CUDA events; cross-lane ordering uses the same
+three host primitives as the reference (bounded channel, latest-wins
+mailbox, two-ended staleness gate).
+
+The policy is an action-token head: logits = features @ W^T with W the
+[V, H] head matrix (OpenVLA-style: the last 256 of V ids are action bins);
+features are a fixed random projection of synthetic LIBERO-shaped
+observations (224x224x3 uint8 + 8-d proprio summarised to H dims).  The VLA
+body is out of scope; the hot path is everything after it.
+"""
+
+from __future__ import annotations
+
+import logging
+import math
+import threading
+import time
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+
+from .core import ConfigError, ParamSnapshot
+from .grpo import GroupBatch, GrpoAbort, GrpoConfig, TokenLoss
+
+log = logging.getLogger("dvla_b200.runtime")
+
+
+class LaneId(Enum):
+    SAMPLER = "Sampler"
+    WEIGHT_RECV = "WeightRecv"
+    TRAINER = "Trainer"
+    WEIGHT_DIST = "WeightDist"
+
+
+class RunAbort(RuntimeError):
+    """Run-level failure: watchdog timeout or a poisoned update."""
+
+    def __init__(self, reason: str, lane: str = "", epoch: int = -1,
+                 lane_states: dict | None = None):
+        self.reason = reason
+        self.lane = lane
+        self.epoch = epoch
+        self.lane_states = lane_states or {}
+        super().__init__(f"{reason} (lane={lane or 'n/a'}, epoch={epoch}); "
+                         f"lanes: {self.lane_states}")
+
+
+class Monitor:
+    """Lane heartbeat registry; the watchdog aborts silent runs."""
+
+    def __init__(self, abort: threading.Event):
+        self.abort = abort
+        self._lock = threading.Lock()
+        self._lanes: dict = {}
+        self.abort_reason: str | None = None
+        self.abort_lane = ""
+        self.abort_epoch = -1
+
+    def beat(self, lane: str, state: str | None = None):
+        with self._lock:
+            prev = self._lanes.get(lane)
+            self._lanes[lane] = (time.perf_counter(),
+                                 state if state is not None else (prev[1] if prev else "run"))
+
+    def fail(self, reason: str, lane: str, epoch: int):
+        with self._lock:
+            if self.abort_reason is None:
+                self.abort_reason, self.abort_lane, self.abort_epoch = reason, lane, epoch
+        self.abort.set()
+
+    def dump(self) -> dict:
+        with self._lock:
+            now = time.perf_counter()
+            return {ln: f"{st} (last beat {now - ts:.2f}s ago)"
+                    for ln, (ts, st) in self._lanes.items()}
+
+    def stale_lanes(self, timeout: float) -> list:
+        with self._lock:
+            now = time.perf_counter()
+            return [ln for ln, (ts, st) in self._lanes.items()
+                    if st != "done" and now - ts > timeout]
+
+
+class VersionBoard:
+    """Two-ended staleness gate (reference runtime.py:211-564, busy mode).
+
+    Sampler end: an epoch may start iff version + produced - processed -
+    installed <= limit (wait_gate).  Trainer end: version V+1 may be
+    published iff the sampler is between epochs or has installed at least
+    V+1-limit (wait_pacing).  Deliveries older than the installed version
+    are ignored and counted (deposit)."""
+
+    def __init__(self, limit: int, monitor: Monitor, snap0: ParamSnapshot):
+        self.limit = limit
+        self.monitor = monitor
+        self._c = threading.Condition()
+        self.version = 0
+        self.produced = 0
+        self.processed = 0
+        self.installed = 0
+        self.snap = snap0
+        self.at_boundary = True
+        self.sampler_done = False
+        self.staleness_max = 0
+        self.regressions_ignored = 0
+        self.delivered: dict = {}
+        self.epoch_meta: dict = {}
+
+    def deposit(self, snap: ParamSnapshot):
+        with self._c:
+            if snap.version <= self.installed or snap.version in self.delivered:
+                self.regressions_ignored += 1
+                log.warning("ignoring stale weight snapshot v%d (installed v%d)", snap.version,
+                            self.installed)
+                return
+            self.delivered[snap.version] = snap
+            self._c.notify_all()
+
+    def boundary(self):
+        with self._c:
+            self.at_boundary = True
+            self._c.notify_all()
+
+    def produce(self, epoch: int, meta: dict):
+        with self._c:
+            self.epoch_meta[epoch] = meta
+            self.produced += 1
+            self._c.notify_all()
+
+    def take_meta(self, epoch: int) -> dict:
+        with self._c:
+            return self.epoch_meta.pop(epoch)
+
+    def mark_sampler_done(self):
+        with self._c:
+            self.sampler_done = True
+            self.at_boundary = True
+            self._c.notify_all()
+
+    def wait_gate(self):
+        """Block until the gate admits the next epoch; installs the newest
+        delivered snapshot first (epoch-boundary install).  Returns
+        (snapshot, staleness)."""
+        with self._c:
+            while True:
+                if self.monitor.abort.is_set():
+                    from .planes import RunAborted
+                    raise RunAborted("abort in gate wait")
+                newest = max(self.delivered, default=0)
+                if newest > self.installed:
+                    self.installed = newest
+                    self.snap = self.delivered[newest]
+                    for v in [k for k in self.delivered if k <= newest]:
+                        del self.delivered[v]
+                    self._c.notify_all()
+                if self.version + self.produced - self.processed - self.installed <= self.limit:
+                    stal = self.version - self.installed
+                    self.staleness_max = max(self.staleness_max, stal)
+                    self.at_boundary = False
+                    return self.snap, stal
+                self.monitor.beat(LaneId.SAMPLER.value, "gate-wait")
+                self._c.wait(0.05)
+
+    def wait_pacing(self, next_version: int):
+        with self._c:
+            while True:
+                if self.monitor.abort.is_set():
+                    from .planes import RunAborted
+                    raise RunAborted("abort in pacing wait")
+                if self.sampler_done or self.at_boundary or \
+                        self.installed >= next_version - self.limit:
+                    return
+                self.monitor.beat(LaneId.TRAINER.value, "pacing-wait")
+                self._c.wait(0.05)
+
+    def publish(self) -> int:
+        with self._c:
+            self.version += 1
+            self.processed += 1
+            if not self.at_boundary:
+                self.staleness_max = max(self.staleness_max, self.version - self.installed)
+            self._c.notify_all()
+            return self.version
+
+    def quarantine(self):
+        with self._c:
+            self.processed += 1
+            self._c.notify_all()
+
+
+class GradReducer:
+    """Cross-node gradient mean (reference runtime.py:569-637) over NCCL.
+
+    The reference ships every node's gradient as an f32 frame, sums the
+    decoded frames in f64 in node order and divides by `nodes`.  Here the
+    gradient is quantised to f32 exactly as the frame would be, then
+    all-reduced: `exact=True` sums the f32 values in f64 (the reference's
+    arithmetic up to summation order), `exact=False` sums in f32 on the wire
+    (half the NVLink bytes; NCCL ring/NVLS order).  Single-node runs are a
+    no-op, as in the reference."""
+
+    def __init__(self, nodes: int, group=None, exact: bool = False):
+        self.nodes = nodes
+        self.group = group
+        self.exact = exact
+
+    def reduce(self, grad):
+        import torch
+        import torch.distributed as dist
+        if self.nodes == 1:
+            return grad
+        q = grad.to(torch.float32)
+        if self.exact:
+            q = q.to(torch.float64)
+        dist.all_reduce(q, op=dist.ReduceOp.SUM, group=self.group)
+        return q.to(grad.dtype) / self.nodes if q.dtype != grad.dtype else q / self.nodes
+
+
+# --------------------------------------------------------------- workers
+@dataclass
+class SwimlaneConfig:
+    """Shapes of the token-head swimlane (defaults: small enough to run in
+    seconds; BASELINE config 4 uses V=32064, T=56, 64 groups/GPU)."""
+
+    n_groups: int = 8            # groups per epoch per GPU
+    group_size: int = 8
+    chunks: int = 1
+    tokens: int = 56             # action tokens per chunk (8 steps x 7 DoF)
+    vocab: int = 32064
+    action_bins: int = 256       # OpenVLA: the last 256 token ids
+    hidden: int = 1024
+    epochs: int = 6
+    staleness_limit: int = 1
+    queue_capacity: int = 2      # epochs of groups buffered in the channel
+    lr: float = 1e-4
+    seed: int = 0
+    watchdog_s: float = 60.0
+
+    def validate(self):
+        if self.group_size < 2:
+            raise ConfigError("group_size must be >= 2")
+        if self.action_bins > self.vocab:
+            raise ConfigError("action_bins must be <= vocab")
+        if self.staleness_limit < 0:
+            raise ConfigError("staleness_limit must be >= 0")
+
+
+class TokenPolicy:
+    """Action-token head W [V, H] (bf16 on the device) with f32 master
+    weights and f64 Adam moments in a MODEL_COMPUTE pool."""
+
+    def __init__(self, cfg: SwimlaneConfig, pool, device):
+        import torch
+        V, H = cfg.vocab, cfg.hidden
+        n = V * H
+        g = torch.Generator(device=device).manual_seed(cfg.seed)
+        self.hm = pool.alloc(n * 4, align=256)
+        self.hmm = pool.alloc(n * 8, align=256)
+        self.hmv = pool.alloc(n * 8, align=256)
+        self.master = pool.view(self.hm, torch.float32)
+        self.master.copy_(torch.randn(n, device=device, generator=g) * (H ** -0.5))
+        self.m = pool.view(self.hmm, torch.float64)
+        self.v = pool.view(self.hmv, torch.float64)
+        self.m.zero_()
+        self.v.zero_()
+        self.step = 0
+        self.V, self.H = V, H
+
+    def weight_bf16(self):
+        import torch
+        return self.master.view(self.V, self.H).to(torch.bfloat16)
+
+
+class RunResult:
+    def __init__(self):
+        self.reports: list = []
+        self.update_stats: list = []
+        self.counters: dict = {}
+        self.staleness_max = 0
+        self.wall = 0.0
+        self.lane_busy: dict = {}
+
+    def summary(self) -> dict:
+        post = self.reports[1:] if len(self.reports) > 1 else self.reports
+        trans = sum(r["transitions"] for r in post)
+        span = sum(r["step_time"] for r in post)
+        traj = sum(r["trajectories"] for r in post)
+        return {"transitions_per_s": trans / max(span, 1e-12),
+                "trajectories_per_s": traj / max(span, 1e-12),
+                "wall": self.wall, "staleness_max": self.staleness_max,
+                "updates": len(self.update_stats)}
+
+
+def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=frozenset()):
+    """Asynchronous swimlane on one GPU (and, under torch.distributed, one
+    closed loop per GPU with NCCL gradient reduction: topology replication,
+    reference placement.py:197-205)."""
+    import torch
+    import torch.distributed as dist
+
+    from . import _lib
+    from .grpo import _stream_ptr
+    from .planes import Channel, ControlPlane, Plane, RunAborted, Transport, TransportMode
+    from .pools import Pool, PoolKind
+    from .replicate import device_snapshot
+
+    cfg.validate()
+    dev = torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+    torch.cuda.set_device(dev)
+    nodes = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    V, H, G, C, T = cfg.vocab, cfg.hidden, cfg.group_size, cfg.chunks, cfg.tokens
+    n_traj = cfg.n_groups * G
+    R = n_traj * C * T
+
+    # ---- dual pools: long-lived model state vs epoch-recycled rollout staging
+    model_bytes = V * H * (4 + 8 + 8) + 2 * V * H * 2 + (64 << 20)
+    model_pool = Pool(PoolKind.MODEL_COMPUTE, model_bytes, device=dev)
+    env_bytes = R * (H * 2 + V * 2 + 64) + (64 << 20)
+    env_pool = Pool(PoolKind.ENV_AUX, env_bytes, device=dev)
+    policy = TokenPolicy(cfg, model_pool, dev)
+    gcfg = GrpoConfig(group_size=G, lr=cfg.lr)
+    abort = threading.Event()
+    monitor = Monitor(abort)
+
+    s_sample, s_train, s_dist = (torch.cuda.Stream(device=dev) for _ in range(3))
+    ctrl = ControlPlane(Transport(TransportMode.INPROC, Plane.CONTROL, name="ctrl"))
+    mailbox = ctrl.subscribe("weights", abort_event=abort)
+    chan = Channel(cfg.queue_capacity * cfg.n_groups,
+                   Transport(TransportMode.INPROC, Plane.DATA, name="data"), abort_event=abort)
+    # double-buffered published weights (bf16) in the MODEL_COMPUTE pool
+    wbuf = [model_pool.view(model_pool.alloc(V * H * 2, align=256), torch.bfloat16)
+            for _ in range(cfg.staleness_limit + 1)]
+    w0 = policy.weight_bf16().reshape(-1)
+    snap0 = device_snapshot(w0, 0, out=wbuf[0])
+    board = VersionBoard(cfg.staleness_limit, monitor, snap0)
+    reducer = GradReducer(nodes, group)
+    proj = torch.randn(224 * 224 * 3 // 64 + 8, H, device=dev,
+                       generator=torch.Generator(device=dev).manual_seed(cfg.seed + 1)) * 0.05
+    result = RunResult()
+    busy = {"sampler": 0.0, "trainer": 0.0}
+    dist_q: list = []
+    dist_cv = threading.Condition()
+
+    def sampler_lane():
+        try:
+            rng = torch.Generator(device=dev).manual_seed(cfg.seed * 7919 + rank)
+            probe = TokenLoss(cfg.n_groups, G, C, T, V, gcfg, dtype=torch.bfloat16, device=dev)
+            for epoch in range(cfg.epochs):
+                snap, stal = board.wait_gate()
+                monitor.beat(LaneId.SAMPLER.value, "rolling")
+                t0 = time.perf_counter()
+                with torch.cuda.stream(s_sample):
+                    W = snap.params.view(V, H)  # installed replica, zero copy
+                    # synthetic LIBERO-shaped observations -> features
+                    img = torch.randint(0, 256, (n_traj * C, 224 * 224 * 3 // 64), device=dev,
+                                        generator=rng, dtype=torch.uint8)
+                    prop = torch.randn(n_traj * C, 8, device=dev, generator=rng)
+                    obs = torch.cat([img.float() / 255.0, prop], dim=1)
+                    feats = (obs @ proj).to(torch.bfloat16)                     # [n_traj*C, H]
+                    logits = feats.repeat_interleave(T, dim=0) @ W.t()          # [R, V] bf16
+                    # action-token sampling over the action bins (Gumbel-max)
+                    lo = V - cfg.action_bins
+                    gum = -torch.log(-torch.log(torch.rand(R, cfg.action_bins, device=dev,
+                                                           generator=rng) + 1e-20) + 1e-20)
+                    tokens = (torch.argmax(logits[:, lo:].float() + gum, dim=1) + lo).to(torch.int32)
+                    rewards = torch.randint(0, 2, (n_traj,), device=dev, generator=rng).float()
+                    if epoch in poison_epochs:
+                        rewards[0] = float("nan")
+                    # behaviour log-probs: forward-only pass of the fused kernel
+                    probe.launch(logits, tokens, torch.zeros(n_traj * C, device=dev), rewards, None)
+                    blp = probe.lp_chunk.float().clone()
+                ev = torch.cuda.Event()
+                ev.record(s_sample)
+                msgs = []
+                for gi in range(cfg.n_groups):
+                    gid = (epoch * nodes + rank) * cfg.n_groups + gi
+                    sl = slice(gi * G, (gi + 1) * G)
+                    toks = tokens.view(n_traj, C, T)[sl]
+                    b = GroupBatch(
+                        group_id=gid, horizon=C * T, chunk=T,
+                        obs=feats.view(n_traj, C, H)[sl], actions=toks,
+                        behavior_log_prob=blp.view(n_traj, C)[sl],
+                        rewards=rewards[sl], behavior_version=snap.version, tokens=toks)
+                    b.ready = ev  # device-resident handoff: consumer waits on the event
+                    msgs.append(b)
+                ev.synchronize()
+                busy["sampler"] += time.perf_counter() - t0
+                board.produce(epoch, {"roll_wall": time.perf_counter() - t0, "epoch": epoch,
+                                      "behavior_version": snap.version, "staleness": stal})
+                for m in msgs:
+                    chan.put(m)
+                board.boundary()
+            board.mark_sampler_done()
+            monitor.beat(LaneId.SAMPLER.value, "done")
+        except RunAborted:
+            pass
+        except Exception as e:  # surface the failure through the watchdog
+            monitor.fail(f"sampler: {e!r}", LaneId.SAMPLER.value, -1)
+
+    def trainer_lane():
+        try:
+            tl = TokenLoss(cfg.n_groups, G, C, T, V, gcfg, dtype=torch.bfloat16, device=dev)
+            dl = torch.empty(R, V, dtype=torch.bfloat16, device=dev)
+            logits = torch.empty(R, V, dtype=torch.bfloat16, device=dev)
+            for epoch in range(cfg.epochs):
+                batches = [chan.take() for _ in range(cfg.n_groups)]
+                meta = board.take_meta(epoch)
+                monitor.beat(LaneId.TRAINER.value, "train")
+                t0 = time.perf_counter()
+                with torch.cuda.stream(s_train):
+                    batches[0].ready.wait(s_train)
+                    W = policy.weight_bf16().view(V, H)
+                    feats = torch.cat([b.obs for b in batches]).reshape(n_traj * C, H)
+                    feats = feats.repeat_interleave(T, dim=0).contiguous()     # [R, H]
+                    torch.matmul(feats, W.t(), out=logits)
+                    tl.set_groups([b.group_id for b in batches])
+                    toks = torch.cat([b.actions.reshape(-1) for b in batches])
+                    blp = torch.cat([b.behavior_log_prob.reshape(-1) for b in batches])
+                    rw = torch.cat([b.rewards for b in batches])
+                    tl.launch(logits, toks, blp, rw, dl)
+                st_ev = torch.cuda.Event()
+                st_ev.record(s_train)
+                st_ev.synchronize()
+                try:
+                    stats = tl.stats(rw)
+                except GrpoAbort as e:
+                    log.warning("quarantined update: %s", e)
+                    board.quarantine()
+                    result.counters["quarantined_updates"] = \
+                        result.counters.get("quarantined_updates", 0) + 1
+                    continue
+                with torch.cuda.stream(s_train):
+                    grad = (dl.t() @ feats).reshape(-1).double()  # dW = dl^T x (cuBLAS, f32 acc)
+                    grad = reducer.reduce(grad)
+                    policy.step += 1
+                    _lib.check(_lib.dvla_adam_step(
+                        policy.master.data_ptr(), grad.data_ptr(), policy.m.data_ptr(),
+                        policy.v.data_ptr(), V * H, policy.step, gcfg.lr, gcfg.beta1,
+                        gcfg.beta2, gcfg.opt_eps, s_train.cuda_stream), "dvla_adam_step")
+                    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+                    _lib.check(_lib.dvla_f32_nonfinite(policy.master.data_ptr(), V * H,
+                                                       flag.data_ptr(), s_train.cuda_stream),
+                               "dvla_f32_nonfinite")
+                done = torch.cuda.Event()
+                done.record(s_train)
+                done.synchronize()
+                if int(flag.item()):
+                    raise RunAbort("non-finite parameters after update",
+                                   lane=LaneId.TRAINER.value, epoch=epoch)
+                board.wait_pacing(board.version + 1)
+                v = board.publish()
+                busy["trainer"] += time.perf_counter() - t0
+                result.update_stats.append({"version": v, **{k: stats[k] for k in (
+                    "loss", "mean_ratio", "clip_fraction", "n_chunks")}})
+                with dist_cv:
+                    dist_q.append((v, done))
+                    dist_cv.notify_all()
+                step_time = max(meta["roll_wall"], time.perf_counter() - t0)
+                result.reports.append({"epoch": epoch, "policy_version": meta["behavior_version"],
+                                       "version_after": v, "step_time": step_time,
+                                       "transitions": n_traj * C * T,
+                                       "trajectories": n_traj, "staleness": meta["staleness"]})
+            with dist_cv:
+                dist_q.append((None, None))
+                dist_cv.notify_all()
+            monitor.beat(LaneId.TRAINER.value, "done")
+        except RunAborted:
+            pass
+        except Exception as e:
+            monitor.fail(f"trainer: {e!r}", LaneId.TRAINER.value, -1)
+
+    def dist_lane():
+        try:
+            while True:
+                with dist_cv:
+                    while not dist_q:
+                        if abort.is_set():
+                            return
+                        dist_cv.wait(0.05)
+                    v, ev = dist_q.pop(0)
+                if v is None:
+                    break
+                with torch.cuda.stream(s_dist):
+                    s_dist.wait_event(ev)
+                    w = policy.weight_bf16().reshape(-1)
+                    snap = device_snapshot(w, v, out=wbuf[v % len(wbuf)], stream=s_dist)
+                ctrl.broadcast(snap, stream=s_dist)
+                monitor.beat(LaneId.WEIGHT_DIST.value)
+            monitor.beat(LaneId.WEIGHT_DIST.value, "done")
+        except RunAborted:
+            pass
+        except Exception as e:
+            monitor.fail(f"dist: {e!r}", LaneId.WEIGHT_DIST.value, -1)
+
+    def recv_lane():
+        try:
+            while not (board.sampler_done and mailbox._slot is None):
+                snap = mailbox.take_newest(timeout=0.2)
+                if snap is not None:
+                    board.deposit(snap)
+                    monitor.beat(LaneId.WEIGHT_RECV.value)
+            monitor.beat(LaneId.WEIGHT_RECV.value, "done")
+        except RunAborted:
+            pass
+
+    t_start = time.perf_counter()
+    lanes = [threading.Thread(target=f, name=n, daemon=True) for f, n in (
+        (sampler_lane, "sampler"), (recv_lane, "recv"), (trainer_lane, "trainer"),
+        (dist_lane, "dist"))]
+    for t in lanes:
+        t.start()
+    while any(t.is_alive() for t in lanes):
+        time.sleep(0.05)
+        stale = monitor.stale_lanes(cfg.watchdog_s)
+        if stale:
+            monitor.fail(f"watchdog: lanes silent for > {cfg.watchdog_s}s", stale[0], -1)
+        if abort.is_set():
+            for t in lanes:
+                t.join(timeout=2.0)
+            raise RunAbort(monitor.abort_reason or "aborted", lane=monitor.abort_lane,
+                           epoch=monitor.abort_epoch, lane_states=monitor.dump())
+    torch.cuda.synchronize(dev)
+    result.wall = time.perf_counter() - t_start
+    result.staleness_max = board.staleness_max
+    result.lane_busy = busy
+    result.counters.update({"updates": board.version, "produced": board.produced,
+                            "regressions_ignored": board.regressions_ignored})
+    return result
+
+
+_ = (math, field)
