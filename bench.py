@@ -48,6 +48,8 @@ def _args():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--unfused", action="store_true")
     ap.add_argument("--no-repl", action="store_true")
+    ap.add_argument("--fixed-warmup", action="store_true",
+                    help="exactly --warmup warm-up steps (for ncu launch lists)")
     return ap.parse_args()
 
 
@@ -336,7 +338,8 @@ def run_ours(a):
     clocks.start()  # samples the warm-up tail and the whole timed region
     t_warm = time.perf_counter()
     w = 0
-    while w < max(a.warmup, 3) or time.perf_counter() - t_warm < 0.5:
+    min_warm_s = 0.0 if a.fixed_warmup else 0.5
+    while w < max(a.warmup, 3) or time.perf_counter() - t_warm < min_warm_s:
         tl.launch(logits, tokens, blp, rewards, dl)
         w += 1
         if w % 16 == 0:
