@@ -81,16 +81,31 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
-__device__ __forceinline__ uint64_t globaltimer_ns();
+// try_wait with a suspend-time hint: the warp sleeps in hardware (up to
+// hint_ns) instead of re-issuing the probe, so waiting warps do not steal
+// issue slots from working warps on the same SM sub-partition.
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity,
+                                                   uint32_t hint_ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns)
+      : "memory");
+  return ok != 0;
+}
 
-// Blocking wait with a safety net: a protocol bug must never hang the GPU,
-// so after ~20 s the kernel traps (the host sees a launch failure).
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  if (mbar_try_wait(bar, parity)) return;
-  const uint64_t t0 = globaltimer_ns();
-  uint32_t spins = 0;
-  while (!mbar_try_wait(bar, parity)) {
-    if (((++spins) & 1023u) == 0 && globaltimer_ns() - t0 > 20000000000ull) __trap();
+// Blocking wait with a safety net: a protocol bug must never hang the GPU.
+// The suspended warp wakes as soon as the phase completes (HW sleep, not a
+// poll), so the hint only bounds the sleep; after 2^14 probes of <= 1 ms
+// (>= ~16 s) the kernel traps (the host sees a launch failure).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity,
+                                          uint32_t hint_ns = 1000000) {
+  uint32_t n = 0;
+  while (!mbar_try_wait_hint(bar, parity, hint_ns)) {
+    if (++n > (1u << 14)) __trap();
   }
 }
 
