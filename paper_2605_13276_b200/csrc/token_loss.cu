@@ -35,9 +35,7 @@ namespace dvla {
 
 constexpr int kFusedComputeWarps = 16;
 constexpr int kFusedComputeThreads = kFusedComputeWarps * 32;
-constexpr int kFusedStages = 3;    // row-level slot rings (partials, coefficients)
-constexpr int kPieceStages = 6;    // SMEM ring of row pieces
-constexpr int kPieceElems = 16384; // 32 KB of bf16 per piece
+constexpr int kFusedStages = 3;
 constexpr uint64_t kSpinTimeoutNs = 4000000000ull;  // 4 s: report, never hang
 
 struct TokParams {
@@ -163,10 +161,8 @@ __device__ __forceinline__ double chunk_lp_pairwise(const double* __restrict__ l
 // 19 publisher (lp_tok + release of the chunk counters).
 // Barriers (every barrier completes once per use of its own ring index, and
 // every waiter walks its ring in order, so parity never aliases):
-//   full/empty/pdone[s] per SMEM piece stage s = piece op % 6: loader ->
-//                      compute -> store (which recycles every stage)
+//   full[s], empty[s]  per SMEM stage s = op % 3: loader <-> all consumers
 //   adoneA[a % 3]      compute -> coef, per A op a (SMEM partial slot a % 3)
-//   afree[a % 3]       coef -> compute, partial slot a % 3 consumed
 //   cfullB[b % 3]      coef -> compute, per B op b (coefficient slot b % 3)
 //   adoneB[b % 3]      compute -> store (and coef, before reusing slot b % 3)
 // The op sequence and barrier protocol were model-checked for races and
@@ -181,11 +177,9 @@ constexpr int kLagRounds = 2;  // measured best on B200 (lag 2..4 x L2 policy sw
 constexpr int kRing = 8;  // > kLagRounds + 1 rows of (lse, target) in flight
 
 struct FusedSmem {
-  uint64_t full[kPieceStages];
-  uint64_t empty[kPieceStages];
-  uint64_t pdone[kPieceStages];
+  uint64_t full[kFusedStages];
+  uint64_t empty[kFusedStages];
   uint64_t adoneA[kFusedStages];
-  uint64_t afree[kFusedStages];   // coef -> compute: A slot consumed
   uint64_t adoneB[kFusedStages];
   uint64_t cfullB[kFusedStages];
   double ws[kFusedStages][kFusedComputeWarps];
@@ -275,23 +269,14 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   const int L = write_dl ? lag : 1 << 30;  // forward-only: A ops only
   auto row_of = [&](int64_t k) { return blockIdx.x + k * G; };
   auto buf = [&](int s) { return bufs + static_cast<size_t>(s) * stage_bytes; };
-  (void)row_bytes;
   const int64_t T = p.T;
-  const int64_t PE = V < kPieceElems ? V : kPieceElems;  // elements per piece
-  const int64_t NP = (V + PE - 1) / PE;                   // pieces per row
-  const int64_t nj = nops * NP;                           // piece ops
-  auto piece_elems = [&](int64_t pc) { return (pc + 1 < NP) ? PE : V - pc * PE; };
   unsigned long long* dbg = g_dbg;
   const long long t_kernel = dbg ? clock64() : 0;
 
   if (tid == 0) {
-    for (int s = 0; s < kPieceStages; ++s) {
+    for (int s = 0; s < kFusedStages; ++s) {
       mbar_init(&S.full[s], 1);
       mbar_init(&S.empty[s], 1);
-      mbar_init(&S.pdone[s], kFusedComputeWarps);
-    }
-    for (int s = 0; s < kFusedStages; ++s) {
-      mbar_init(&S.afree[s], 1);
       mbar_init(&S.adoneA[s], kFusedComputeWarps);
       mbar_init(&S.adoneB[s], kFusedComputeWarps);
       mbar_init(&S.cfullB[s], 1);
@@ -312,54 +297,48 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
       const uint64_t pol_keep = l2_policy_evict_last();
-      for (int64_t j = 0; j < nj; ++j) {
-        const int s = static_cast<int>(j % kPieceStages);
-        if (j >= kPieceStages) {
+      for (int64_t n = 0; n < nops; ++n) {
+        const int s = static_cast<int>(n % kFusedStages);
+        if (n >= kFusedStages) {
           DBG_T0();
-          mbar_wait(&S.empty[s], static_cast<uint32_t>(((j / kPieceStages) - 1) & 1));
+          mbar_wait(&S.empty[s], static_cast<uint32_t>(((n / kFusedStages) - 1) & 1));
           DBG_ADD(8);
         }
         bool isB;
         int64_t k;
-        op_of(j / NP, nloc, L, &isB, &k);
-        const int64_t pc = j % NP;
-        const uint32_t bytes = static_cast<uint32_t>(piece_elems(pc) * 2);
-        const __nv_bfloat16* src = logits + row_of(k) * V + pc * PE;
-        mbar_arrive_expect_tx(&S.full[s], bytes);
+        op_of(n, nloc, L, &isB, &k);
+        mbar_arrive_expect_tx(&S.full[s], row_bytes);
         if (isB)  // second (last) read of the row: from L2, then evict
-          tma_load_1d_evict_first(buf(s), src, bytes, &S.full[s], pol);
+          tma_load_1d_evict_first(buf(s), logits + row_of(k) * V, row_bytes, &S.full[s], pol);
         else if (a_evict_last && write_dl)  // keep in L2 until B re-reads it
-          tma_load_1d_evict_first(buf(s), src, bytes, &S.full[s], pol_keep);
+          tma_load_1d_evict_first(buf(s), logits + row_of(k) * V, row_bytes, &S.full[s], pol_keep);
         else
-          tma_load_1d(buf(s), src, bytes, &S.full[s]);
+          tma_load_1d(buf(s), logits + row_of(k) * V, row_bytes, &S.full[s]);
       }
     }
     return;
   }
 
   // ---------------------------------------------------------- store warp
-  // Recycles every SMEM piece: A pieces as soon as the compute warps have
-  // read them, B pieces once their TMA store has finished reading SMEM.
   if (warp == kWarpStore) {
-    if (lane == 0) {
+    if (lane == 0 && write_dl) {
       const uint64_t pol = l2_policy_evict_first();
-      for (int64_t j = 0; j < nj; ++j) {
-        const int s = static_cast<int>(j % kPieceStages);
-        {
-          DBG_T0();
-          mbar_wait(&S.pdone[s], static_cast<uint32_t>((j / kPieceStages) & 1));
-          DBG_ADD(9);
-        }
+      int64_t b = 0;
+      for (int64_t n = 0; n < nops; ++n) {
         bool isB;
         int64_t k;
-        op_of(j / NP, nloc, L, &isB, &k);
-        if (isB) {
-          const int64_t pc = j % NP;
-          tma_store_1d_evict_first(dl + row_of(k) * V + pc * PE, buf(s),
-                                   static_cast<uint32_t>(piece_elems(pc) * 2), pol);
-          bulk_commit();
-          bulk_wait_read<0>();
+        op_of(n, nloc, L, &isB, &k);
+        if (!isB) continue;
+        const int s = static_cast<int>(n % kFusedStages);
+        {
+          DBG_T0();
+          mbar_wait(&S.adoneB[b % kFusedStages], static_cast<uint32_t>((b / kFusedStages) & 1));
+          DBG_ADD(9);
         }
+        ++b;
+        tma_store_1d_evict_first(dl + row_of(k) * V, buf(s), row_bytes, pol);
+        bulk_commit();
+        bulk_wait_read<0>();
         mbar_arrive(&S.empty[s]);
       }
       bulk_wait<0>();
@@ -429,6 +408,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         pc = ld_acquire_gpu(p.cnt + pq);
     };
     auto process = [&](int64_t n) {
+      const int s = static_cast<int>(n % kFusedStages);
       bool isB;
       int64_t k;
       op_of(n, nloc, L, &isB, &k);
@@ -441,14 +421,14 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
           mbar_wait(&S.adoneA[sa], static_cast<uint32_t>((a / kFusedStages) & 1));
           if (lane == 0) { DBG_ADD(2); }
         }
-        // everything this tail needs is in slot sa (the compute warps
-        // gathered the target logit while the row streamed through SMEM)
+        // read everything this tail needs from slot sa, then free the stage
+        // (the compute warps already gathered the target logit)
         const int32_t tgt = S.tgta[sa];
         const float xt_f = S.xt[sa];
         const float mw = (lane < kFusedComputeWarps) ? S.wm[sa][lane] : -INFINITY;
         const double sw = (lane < kFusedComputeWarps) ? S.ws[sa][lane] : 0.0;
         __syncwarp();
-        if (lane == 0) mbar_arrive(&S.afree[sa]);  // slot sa may be rewritten
+        if (lane == 0) mbar_arrive(&S.empty[s]);
         const long long t_tail = dbg ? clock64() : 0;
         const int j = static_cast<int>(a % kPubRing);
         const uint32_t pe_ph = static_cast<uint32_t>(((a / kPubRing) - 1) & 1);
@@ -573,36 +553,21 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   }
 
   // ------------------------------------------------------- compute warps
-  int64_t a = 0, b = 0;  // A / B row counters
-  float m_run = -INFINITY, s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // A row state
-  int32_t tg = 0;
-  float xt_keep = __int_as_float(0x7fc00000);
-  int sb = 0;            // B row state (from the coefficient slot)
-  uint32_t mode = 0u, sgn = 0u;
-  float K = 0.f, lseL = 0.f, cfv = 0.f;
-  int32_t tgt = -1;
-  for (int64_t j = 0; j < nj; ++j) {
-    const int s = static_cast<int>(j % kPieceStages);
+  const int nvec = static_cast<int>(V >> 3);  // uint4 = 8 bf16
+  int64_t a = 0, b = 0;  // A / B op counters
+  for (int64_t n = 0; n < nops; ++n) {
+    const int s = static_cast<int>(n % kFusedStages);
+    const uint32_t ph = static_cast<uint32_t>((n / kFusedStages) & 1);
     bool isB;
     int64_t k;
-    op_of(j / NP, nloc, L, &isB, &k);
-    const int64_t pc = j % NP;
-    const int64_t off = pc * PE;
-    const int nvec = static_cast<int>(piece_elems(pc) >> 3);  // uint4 = 8 bf16
+    op_of(n, nloc, L, &isB, &k);
     {
       DBG_T0();
-      mbar_wait(&S.full[s], static_cast<uint32_t>((j / kPieceStages) & 1));
+      mbar_wait(&S.full[s], ph);
       if (tid == 0) { DBG_ADD(0); }
     }
     if (!isB) {
-      if (pc == 0) {
-        m_run = -INFINITY;
-        s0 = s1 = s2 = s3 = 0.f;
-        if (tid == 0) {
-          tg = __ldg(p.tokens + row_of(k));
-          xt_keep = __int_as_float(0x7fc00000);
-        }
-      }
+      const int32_t tg = (tid == 0) ? __ldg(p.tokens + row_of(k)) : 0;  // used at the end
       const uint4* v = reinterpret_cast<const uint4*>(buf(s));
       uint32_t mx0 = 0xff80ff80u, mx1 = 0xff80ff80u;
 #pragma unroll 4
@@ -612,15 +577,9 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         mx1 = bf16x2_max(mx1, bf16x2_max(x.z, x.w));
       }
       const uint32_t mx = bf16x2_max(mx0, mx1);
-      const float pm = warp_max_f32(fmaxf(bf16lo(mx), bf16hi(mx)));
-      if (pm > m_run) {  // online softmax across pieces (warp-uniform)
-        if (m_run != -INFINITY) {
-          const float f = ex2f((m_run - pm) * kLog2e);
-          s0 *= f; s1 *= f; s2 *= f; s3 *= f;
-        }
-        m_run = pm;
-      }
-      const float mL = m_run * kLog2e;
+      const float m = warp_max_f32(fmaxf(bf16lo(mx), bf16hi(mx)));
+      const float mL = m * kLog2e;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll 2
       for (int i = tid; i < nvec; i += kFusedComputeThreads) {
         const uint4 x = v[i];
@@ -629,46 +588,32 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         s2 += ex2f(fmaf(bf16lo(x.z), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.z), kLog2e, -mL));
         s3 += ex2f(fmaf(bf16lo(x.w), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.w), kLog2e, -mL));
       }
-      if (tid == 0 && tg >= off && tg < off + piece_elems(pc))  // gather the target
-        xt_keep = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(buf(s))[tg - off]);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.pdone[s]);  // piece fully read
-      if (pc == NP - 1) {
-        double part = (static_cast<double>(s0) + static_cast<double>(s1)) +
-                      (static_cast<double>(s2) + static_cast<double>(s3));
-        part = warp_sum_f64(part);
-        const int sa = static_cast<int>(a % kFusedStages);
-        if (a >= kFusedStages)  // the coefficient warp has read A row a-3's slot
-          mbar_wait(&S.afree[sa], static_cast<uint32_t>(((a - kFusedStages) / kFusedStages) & 1));
-        ++a;
-        if (tid == 0) {
-          const bool ok = tg >= 0 && tg < V;
-          S.tgta[sa] = ok ? tg : -1;
-          S.xt[sa] = ok ? xt_keep : __int_as_float(0x7fc00000);
-        }
-        if (lane == 0) {
-          S.wm[sa][warp] = m_run;
-          S.ws[sa][warp] = part;
-          mbar_arrive(&S.adoneA[sa]);
-        }
+      double part = (static_cast<double>(s0) + static_cast<double>(s1)) +
+                    (static_cast<double>(s2) + static_cast<double>(s3));
+      part = warp_sum_f64(part);
+      const int sa = static_cast<int>(a % kFusedStages);
+      ++a;
+      if (tid == 0) {  // gather the target logit while the row is in SMEM
+        const bool ok = tg >= 0 && tg < V;
+        S.tgta[sa] = ok ? tg : -1;
+        S.xt[sa] = ok ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(buf(s))[tg])
+                      : __int_as_float(0x7fc00000);
+      }
+      if (lane == 0) {
+        S.wm[sa][warp] = m;
+        S.ws[sa][warp] = part;
+        mbar_arrive(&S.adoneA[sa]);
       }
       continue;
     }
-    if (pc == 0) {
-      sb = static_cast<int>(b % kFusedStages);
-      {
-        DBG_T0();
-        mbar_wait(&S.cfullB[sb], static_cast<uint32_t>((b / kFusedStages) & 1));
-        if (tid == 0) { DBG_ADD(1); }
-      }
-      ++b;
-      mode = S.mode[sb];
-      K = S.kval[sb];
-      sgn = (mode & 0x80000000u) ? 0x80008000u : 0u;
-      tgt = S.tgt[sb];
-      lseL = S.lseL[sb];
-      cfv = S.cf[sb];
+    const int sb = static_cast<int>(b % kFusedStages);
+    {
+      DBG_T0();
+      mbar_wait(&S.cfullB[sb], static_cast<uint32_t>((b / kFusedStages) & 1));
+      if (tid == 0) { DBG_ADD(1); }
     }
+    ++b;
+    const uint32_t mode = S.mode[sb];
     uint4* v = reinterpret_cast<uint4*>(buf(s));
     if ((mode & 3u) != 1u) {
       // zero-gradient rows (A == 0 or clipped chunk): 0 * (onehot - p)
@@ -676,8 +621,10 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       for (int i = tid; i < nvec; i += kFusedComputeThreads) v[i] = make_uint4(z, z, z, z);
     } else {
       // -c * p_v = -sign(c) * 2^(x*log2e - (lse*log2e - log2|c|))
-      const int64_t tl = static_cast<int64_t>(tgt) - off;  // target within the piece
-      const int tv = (tl >= 0 && tl < piece_elems(pc)) ? static_cast<int>(tl >> 3) : -1;
+      const float K = S.kval[sb];
+      const uint32_t sgn = (mode & 0x80000000u) ? 0x80008000u : 0u;
+      const int32_t tgt = S.tgt[sb];
+      const int tv = tgt >> 3;
 #pragma unroll 2
       for (int i = tid; i < nvec; i += kFusedComputeThreads) {
         const uint4 x = v[i];
@@ -688,14 +635,14 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         o.w = pack_bf16x2(ex2f(fmaf(bf16lo(x.w), kLog2e, -K)), ex2f(fmaf(bf16hi(x.w), kLog2e, -K))) ^ sgn;
         if (i == tv) {
           // target column: c * (1 - p_t)
-          const int e = static_cast<int>(tl & 7);
+          const int e = tgt & 7;
           const uint32_t word = (e >> 1) == 0 ? x.x : (e >> 1) == 1 ? x.y : (e >> 1) == 2 ? x.z : x.w;
-          const float xv = (e & 1) ? bf16hi(word) : bf16lo(word);
-          const float pt = ex2f(fmaf(xv, kLog2e, -lseL));
-          const float val = cfv * (1.0f - pt);
-          const uint32_t bb = pack_bf16x2(val, val) & 0xffffu;
+          const float xt = (e & 1) ? bf16hi(word) : bf16lo(word);
+          const float pt = ex2f(fmaf(xt, kLog2e, -S.lseL[sb]));
+          const float val = S.cf[sb] * (1.0f - pt);
+          const uint32_t b = pack_bf16x2(val, val) & 0xffffu;
           uint32_t ow = (e >> 1) == 0 ? o.x : (e >> 1) == 1 ? o.y : (e >> 1) == 2 ? o.z : o.w;
-          ow = (e & 1) ? ((ow & 0x0000ffffu) | (bb << 16)) : ((ow & 0xffff0000u) | bb);
+          ow = (e & 1) ? ((ow & 0x0000ffffu) | (b << 16)) : ((ow & 0xffff0000u) | b);
           if ((e >> 1) == 0) o.x = ow;
           else if ((e >> 1) == 1) o.y = ow;
           else if ((e >> 1) == 2) o.z = ow;
@@ -706,10 +653,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     }
     fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0) {
-      mbar_arrive(&S.pdone[s]);
-      if (pc == NP - 1) mbar_arrive(&S.adoneB[sb]);
-    }
+    if (lane == 0) mbar_arrive(&S.adoneB[sb]);
   }
   if (dbg && tid == 0) atomicAdd(dbg + 12, static_cast<unsigned long long>(clock64() - t_kernel));
 }
@@ -1001,14 +945,10 @@ static TokWorkspace carve(void* base, int64_t n_groups, int64_t G, int64_t C, in
   return w;
 }
 
-static size_t fused_stage_bytes(int64_t V) {
-  const int64_t pe = V < kPieceElems ? V : kPieceElems;
-  return ((static_cast<size_t>(pe) * 2 + 127) / 128) * 128;
-}
-
 static size_t fused_smem_bytes(int64_t V) {
   const size_t hdr = ((sizeof(FusedSmem) + 127) / 128) * 128;
-  return hdr + kPieceStages * fused_stage_bytes(V);
+  const size_t stage = ((static_cast<size_t>(V) * 2 + 127) / 128) * 128;
+  return hdr + kFusedStages * stage;
 }
 
 }  // namespace dvla
@@ -1094,7 +1034,7 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
       attr_set[dev & 63] = true;
     }
     const unsigned grid = static_cast<unsigned>(R < sms ? R : sms);
-    const uint32_t stage_bytes = static_cast<uint32_t>(fused_stage_bytes(V));
+    const uint32_t stage_bytes = static_cast<uint32_t>(((V * 2 + 127) / 128) * 128);
     cudaEvent_t stop;
     prof_begin(stream, &stop);
     static const int lag = [] {

@@ -12,8 +12,7 @@ import random
 
 import pytest
 
-S = 3   # kFusedStages: row-level slot rings
-PS = 6  # kPieceStages: SMEM piece ring
+S = 3  # kFusedStages
 
 
 def op_of(n, nloc, L):
@@ -62,43 +61,36 @@ def coef_order(nops, nloc, L):
     return order
 
 
-def simulate(nloc, L, seed, write_dl=True, NP=2):
-    """Roles as generators; each row op is split into NP SMEM pieces."""
+def simulate(nloc, L, seed, write_dl=True):
     rnd = random.Random(seed)
     nops = 2 * nloc if write_dl else nloc
     Lx = L if write_dl else 1 << 30
-    nj = nops * NP
-    full = [Bar(1) for _ in range(PS)]
-    empty = [Bar(1) for _ in range(PS)]
-    pdone = [Bar(16) for _ in range(PS)]
+    full = [Bar(1) for _ in range(S)]
+    empty = [Bar(1) for _ in range(S)]
     ad_a = [Bar(16) for _ in range(S)]
-    a_free = [Bar(1) for _ in range(S)]
     ad_b = [Bar(16) for _ in range(S)]
     cf_b = [Bar(1) for _ in range(S)]
     slot_p, slot_c, rows_b = [None] * S, [None] * S, []
-    stage_owner = [None] * PS
 
     def wait(b, idx):
         while not b.done(idx):
             yield 1
 
     def loader():
-        for j in range(nj):
-            if j >= PS:
-                yield from wait(empty[j % PS], j // PS - 1)
-            assert stage_owner[j % PS] is None, "stage overwritten while in use"
-            stage_owner[j % PS] = j
-            full[j % PS].arrive()
+        for n in range(nops):
+            if n >= S:
+                yield from wait(empty[n % S], n // S - 1)
+            full[n % S].arrive()
 
     def store():
-        for j in range(nj):
-            yield from wait(pdone[j % PS], j // PS)
-            isb, k = op_of(j // NP, nloc, Lx)
-            if isb and j % NP == NP - 1:
+        b = 0
+        for n in range(nops):
+            isb, k = op_of(n, nloc, Lx)
+            if isb:
+                yield from wait(ad_b[b % S], b // S)
                 rows_b.append(k)
-            assert stage_owner[j % PS] == j
-            stage_owner[j % PS] = None
-            empty[j % PS].arrive()
+                empty[n % S].arrive()
+                b += 1
 
     tails = set()
 
@@ -110,46 +102,39 @@ def simulate(nloc, L, seed, write_dl=True, NP=2):
                 # the chunk of row k spans rounds k and k+1: both tails of this
                 # CTA must already be published (else: cross-CTA deadlock)
                 assert k in tails and (k + 1 >= nloc or k + 1 in tails), (k, sorted(tails))
+            else:
+                tails.add(k)
+            if not isb:
+                yield from wait(ad_a[a % S], a // S)
+                assert slot_p[a % S] == a
+                empty[n % S].arrive()
+                a += 1
+            else:
                 if b >= S:
                     yield from wait(ad_b[(b - S) % S], (b - S) // S)
                 slot_c[b % S] = b
                 cf_b[b % S].arrive()
                 b += 1
-            else:
-                yield from wait(ad_a[a % S], a // S)
-                assert slot_p[a % S] == a
-                a_free[a % S].arrive()
-                tails.add(k)
-                a += 1
 
     def compute(w):
         a = b = 0
-        for j in range(nj):
-            isb, k = op_of(j // NP, nloc, Lx)
-            pc = j % NP
-            yield from wait(full[j % PS], j // PS)
-            assert stage_owner[j % PS] == j
+        for n in range(nops):
+            isb, k = op_of(n, nloc, Lx)
+            yield from wait(full[n % S], n // S)
             if not isb:
-                pdone[j % PS].arrive()
-                if pc == NP - 1:
-                    if a >= S:
-                        yield from wait(a_free[a % S], (a - S) // S)
-                    if w == 0:
-                        slot_p[a % S] = a
-                    ad_a[a % S].arrive()
-                    a += 1
+                if w == 0:
+                    slot_p[a % S] = a
+                ad_a[a % S].arrive()
+                a += 1
             else:
-                if pc == 0:
-                    yield from wait(cf_b[b % S], b // S)
-                    assert slot_c[b % S] == b
-                pdone[j % PS].arrive()
-                if pc == NP - 1:
-                    ad_b[b % S].arrive()
-                    b += 1
+                yield from wait(cf_b[b % S], b // S)
+                assert slot_c[b % S] == b
+                ad_b[b % S].arrive()
+                b += 1
 
     gens = [loader(), store(), coef()] + [compute(w) for w in range(16)]
     live = list(gens)
-    for _ in range(400000):
+    for _ in range(200000):
         if not live:
             break
         g = rnd.choice(live)
@@ -166,8 +151,7 @@ def simulate(nloc, L, seed, write_dl=True, NP=2):
 @pytest.mark.parametrize("L", [1, 2, 3])
 def test_protocol_completes_without_aliasing(nloc, L):
     for seed in range(3):
-        for NP in (1, 2, 3):
-            simulate(nloc, L, seed, NP=NP)
+        simulate(nloc, L, seed)
 
 
 def test_forward_only_protocol():
