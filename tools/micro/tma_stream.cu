@@ -12,8 +12,8 @@ __global__ void __launch_bounds__(544, 1) ring(const uint8_t* src, uint8_t* dst,
                                                int S, int P, int write_mode) {
   extern __shared__ __align__(128) uint8_t sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
-  uint64_t* empty = full + 16;
-  uint8_t* buf = sm + 256;
+  uint64_t* empty = full + 32;
+  uint8_t* buf = sm + 512;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t npieces = nbytes / P;
   if (tid == 0) {
@@ -58,12 +58,12 @@ int main() {
   cudaMemset(a, 1, N);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaFuncSetAttribute(ring, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  int cfg[][2] = {{3, 65536}, {2, 65536}, {6, 32768}, {12, 16384}, {4, 49152}, {24, 8192}};
+  int cfg[][2] = {{3, 65536}, {2, 65536}, {6, 32768}, {12, 16384}, {4, 49152}, {16, 8192}};
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (int wm = 0; wm < 2; ++wm)
     for (auto& c : cfg) {
       const int S = c[0], P = c[1];
-      const size_t smem = 256 + (size_t)S * P;
+      const size_t smem = 512 + (size_t)S * P;
       for (int it = 0; it < 2; ++it) ring<<<sms, 544, smem>>>(a, b, N, S, P, wm);
       cudaEventRecord(e0);
       const int R = 5;
