@@ -35,7 +35,8 @@ namespace dvla {
 
 constexpr int kFusedComputeWarps = 16;
 constexpr int kFusedComputeThreads = kFusedComputeWarps * 32;
-constexpr int kFusedStages = 3;
+constexpr int kFusedStages = 3;    // SMEM row stages and B coefficient slots
+constexpr int kASlots = 8;         // A-row partial slots (coef-warp slack)
 constexpr uint64_t kSpinTimeoutNs = 4000000000ull;  // 4 s: report, never hang
 
 struct TokParams {
@@ -157,14 +158,17 @@ __device__ __forceinline__ double chunk_lp_pairwise(const double* __restrict__ l
 // so the chunk wait is deadlock-free while all CTAs are co-resident
 // (grid <= #SMs, T <= grid).
 //
-// Warp roles: 0..15 compute, 16 loader, 17 coefficient, 18 store,
+// Warp roles: 0..15 compute (they also store dlogits, 16-byte streaming
+// stores from registers), 16 loader, 17 coefficient, 18 idle,
 // 19 publisher (lp_tok + release of the chunk counters).
 // Barriers (every barrier completes once per use of its own ring index, and
 // every waiter walks its ring in order, so parity never aliases):
-//   full[s], empty[s]  per SMEM stage s = op % 3: loader <-> all consumers
-//   adoneA[a % 3]      compute -> coef, per A op a (SMEM partial slot a % 3)
+//   full[s], empty[s]  per SMEM stage s = op % 3: loader <-> compute warps
+//                      (a stage is free as soon as its row has been read)
+//   adoneA[a % 8]      compute -> coef, per A op a (SMEM partial slot a % 8)
+//   afree[a % 8]       coef -> compute, partial slot consumed
 //   cfullB[b % 3]      coef -> compute, per B op b (coefficient slot b % 3)
-//   adoneB[b % 3]      compute -> store (and coef, before reusing slot b % 3)
+//   adoneB[b % 3]      compute -> coef (coefficient slot b % 3 consumed)
 // The op sequence and barrier protocol were model-checked for races and
 // parity aliasing (tests/test_fused_protocol.py).
 constexpr int kWarpLoader = kFusedComputeWarps;
@@ -173,24 +177,25 @@ constexpr int kWarpStore = kFusedComputeWarps + 2;
 constexpr int kWarpPublish = kFusedComputeWarps + 3;
 constexpr int kFusedThreadsWS = (kFusedComputeWarps + 4) * 32;
 constexpr int kPubRing = 8;
-constexpr int kLagRounds = 2;  // measured best on B200 (lag 2..4 x L2 policy sweep)
+constexpr int kLagRounds = 4;  // measured best on B200 (lag 2..4 sweep, tools/fused_variants.py)
 constexpr int kRing = 8;  // > kLagRounds + 1 rows of (lse, target) in flight
 
 struct FusedSmem {
   uint64_t full[kFusedStages];
   uint64_t empty[kFusedStages];
-  uint64_t adoneA[kFusedStages];
+  uint64_t adoneA[kASlots];
+  uint64_t afree[kASlots];
   uint64_t adoneB[kFusedStages];
   uint64_t cfullB[kFusedStages];
-  double ws[kFusedStages][kFusedComputeWarps];
-  float wm[kFusedStages][kFusedComputeWarps];
+  double ws[kASlots][kFusedComputeWarps];
+  float wm[kASlots][kFusedComputeWarps];
   float kval[kFusedStages];   // lse*log2e - log2|c|
   float lseL[kFusedStages];   // lse*log2e
   float cf[kFusedStages];     // coefficient (f32)
   uint32_t mode[kFusedStages];  // 0 zero row, 1 finite c (bit 31: c > 0), 2 non-finite c
   int32_t tgt[kFusedStages];
-  float xt[kFusedStages];       // gathered target logit of A slot
-  int32_t tgta[kFusedStages];   // its token id (-1: out of range)
+  float xt[kASlots];       // gathered target logit of A slot
+  int32_t tgta[kASlots];   // its token id (-1: out of range)
   double ring_lse[kRing];
   int32_t ring_tgt[kRing];
   uint64_t pubfull[kPubRing];
@@ -276,10 +281,13 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   if (tid == 0) {
     for (int s = 0; s < kFusedStages; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], 1);
-      mbar_init(&S.adoneA[s], kFusedComputeWarps);
+      mbar_init(&S.empty[s], kFusedComputeWarps);
       mbar_init(&S.adoneB[s], kFusedComputeWarps);
       mbar_init(&S.cfullB[s], 1);
+    }
+    for (int s = 0; s < kASlots; ++s) {
+      mbar_init(&S.adoneA[s], kFusedComputeWarps);
+      mbar_init(&S.afree[s], 1);
     }
     for (int j = 0; j < kPubRing; ++j) {
       mbar_init(&S.pubfull[j], 1);
@@ -319,32 +327,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     return;
   }
 
-  // ---------------------------------------------------------- store warp
-  if (warp == kWarpStore) {
-    if (lane == 0 && write_dl) {
-      const uint64_t pol = l2_policy_evict_first();
-      int64_t b = 0;
-      for (int64_t n = 0; n < nops; ++n) {
-        bool isB;
-        int64_t k;
-        op_of(n, nloc, L, &isB, &k);
-        if (!isB) continue;
-        const int s = static_cast<int>(n % kFusedStages);
-        {
-          DBG_T0();
-          mbar_wait(&S.adoneB[b % kFusedStages], static_cast<uint32_t>((b / kFusedStages) & 1));
-          DBG_ADD(9);
-        }
-        ++b;
-        tma_store_1d_evict_first(dl + row_of(k) * V, buf(s), row_bytes, pol);
-        bulk_commit();
-        bulk_wait_read<0>();
-        mbar_arrive(&S.empty[s]);
-      }
-      bulk_wait<0>();
-    }
-    return;
-  }
+  if (warp == kWarpStore) return;  // dlogits are stored by the compute warps
 
   // ------------------------------------------------------ publisher warp
   // Publishes each row's lp_tok and bumps its chunk counter with a release
@@ -408,17 +391,16 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         pc = ld_acquire_gpu(p.cnt + pq);
     };
     auto process = [&](int64_t n) {
-      const int s = static_cast<int>(n % kFusedStages);
       bool isB;
       int64_t k;
       op_of(n, nloc, L, &isB, &k);
       const int64_t r = row_of(k);
       if (!isB) {
         // ---- tail of A(k): lse (f64) and the target's log-prob
-        const int sa = static_cast<int>(a % kFusedStages);
+        const int sa = static_cast<int>(a % kASlots);
         {
           DBG_T0();
-          mbar_wait(&S.adoneA[sa], static_cast<uint32_t>((a / kFusedStages) & 1));
+          mbar_wait(&S.adoneA[sa], static_cast<uint32_t>((a / kASlots) & 1));
           if (lane == 0) { DBG_ADD(2); }
         }
         // read everything this tail needs from slot sa, then free the stage
@@ -428,7 +410,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         const float mw = (lane < kFusedComputeWarps) ? S.wm[sa][lane] : -INFINITY;
         const double sw = (lane < kFusedComputeWarps) ? S.ws[sa][lane] : 0.0;
         __syncwarp();
-        if (lane == 0) mbar_arrive(&S.empty[s]);
+        if (lane == 0) mbar_arrive(&S.afree[sa]);  // partial slot sa consumed
         const long long t_tail = dbg ? clock64() : 0;
         const int j = static_cast<int>(a % kPubRing);
         const uint32_t pe_ph = static_cast<uint32_t>(((a / kPubRing) - 1) & 1);
@@ -588,16 +570,23 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         s2 += ex2f(fmaf(bf16lo(x.z), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.z), kLog2e, -mL));
         s3 += ex2f(fmaf(bf16lo(x.w), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.w), kLog2e, -mL));
       }
+      // gather the target logit while the row is in SMEM, then free the stage
+      const bool tok_ok = tg >= 0 && tg < V;
+      const float xt_v = (tid == 0 && tok_ok)
+                             ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(buf(s))[tg])
+                             : __int_as_float(0x7fc00000);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[s]);
       double part = (static_cast<double>(s0) + static_cast<double>(s1)) +
                     (static_cast<double>(s2) + static_cast<double>(s3));
       part = warp_sum_f64(part);
-      const int sa = static_cast<int>(a % kFusedStages);
+      const int sa = static_cast<int>(a % kASlots);
+      if (a >= kASlots)  // the coefficient warp has read A row a-8's partials
+        mbar_wait(&S.afree[sa], static_cast<uint32_t>(((a - kASlots) / kASlots) & 1));
       ++a;
-      if (tid == 0) {  // gather the target logit while the row is in SMEM
-        const bool ok = tg >= 0 && tg < V;
-        S.tgta[sa] = ok ? tg : -1;
-        S.xt[sa] = ok ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(buf(s))[tg])
-                      : __int_as_float(0x7fc00000);
+      if (tid == 0) {
+        S.tgta[sa] = tok_ok ? tg : -1;
+        S.xt[sa] = xt_v;
       }
       if (lane == 0) {
         S.wm[sa][warp] = m;
@@ -614,11 +603,12 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     }
     ++b;
     const uint32_t mode = S.mode[sb];
-    uint4* v = reinterpret_cast<uint4*>(buf(s));
+    const uint4* v = reinterpret_cast<const uint4*>(buf(s));
+    uint4* dst = reinterpret_cast<uint4*>(dl + row_of(k) * V);
     if ((mode & 3u) != 1u) {
       // zero-gradient rows (A == 0 or clipped chunk): 0 * (onehot - p)
       const uint32_t z = (mode == 0u) ? 0u : 0x7fc07fc0u;
-      for (int i = tid; i < nvec; i += kFusedComputeThreads) v[i] = make_uint4(z, z, z, z);
+      for (int i = tid; i < nvec; i += kFusedComputeThreads) __stcs(dst + i, make_uint4(z, z, z, z));
     } else {
       // -c * p_v = -sign(c) * 2^(x*log2e - (lse*log2e - log2|c|))
       const float K = S.kval[sb];
@@ -648,12 +638,14 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
           else if ((e >> 1) == 2) o.z = ow;
           else o.w = ow;
         }
-        v[i] = o;
+        __stcs(dst + i, o);
       }
     }
-    fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&S.adoneB[sb]);
+    if (lane == 0) {
+      mbar_arrive(&S.empty[s]);   // B row read: the stage may be reloaded
+      mbar_arrive(&S.adoneB[sb]);
+    }
   }
   if (dbg && tid == 0) atomicAdd(dbg + 12, static_cast<unsigned long long>(clock64() - t_kernel));
 }

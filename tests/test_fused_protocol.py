@@ -62,15 +62,23 @@ def coef_order(nops, nloc, L):
 
 
 def simulate(nloc, L, seed, write_dl=True):
+    """Roles as generators (v8 protocol): the loader streams every op's row
+    into a 3-stage SMEM ring; compute warps free a stage as soon as they have
+    read it (dlogits leave through 16-byte stores from registers); A-row
+    partials go through an 8-slot ring guarded by afree; B coefficients
+    through a 3-slot ring guarded by adoneB."""
+    AS = 8
     rnd = random.Random(seed)
     nops = 2 * nloc if write_dl else nloc
     Lx = L if write_dl else 1 << 30
     full = [Bar(1) for _ in range(S)]
-    empty = [Bar(1) for _ in range(S)]
-    ad_a = [Bar(16) for _ in range(S)]
+    empty = [Bar(16) for _ in range(S)]
+    ad_a = [Bar(16) for _ in range(AS)]
+    a_free = [Bar(1) for _ in range(AS)]
     ad_b = [Bar(16) for _ in range(S)]
     cf_b = [Bar(1) for _ in range(S)]
-    slot_p, slot_c, rows_b = [None] * S, [None] * S, []
+    slot_p, slot_c, rows_b = [None] * AS, [None] * S, []
+    stage_owner = [None] * S
 
     def wait(b, idx):
         while not b.done(idx):
@@ -80,19 +88,12 @@ def simulate(nloc, L, seed, write_dl=True):
         for n in range(nops):
             if n >= S:
                 yield from wait(empty[n % S], n // S - 1)
+            assert stage_owner[n % S] is None, "stage reloaded while in use"
+            stage_owner[n % S] = n
             full[n % S].arrive()
 
-    def store():
-        b = 0
-        for n in range(nops):
-            isb, k = op_of(n, nloc, Lx)
-            if isb:
-                yield from wait(ad_b[b % S], b // S)
-                rows_b.append(k)
-                empty[n % S].arrive()
-                b += 1
-
     tails = set()
+    readers = {}
 
     def coef():
         a = b = 0
@@ -102,39 +103,47 @@ def simulate(nloc, L, seed, write_dl=True):
                 # the chunk of row k spans rounds k and k+1: both tails of this
                 # CTA must already be published (else: cross-CTA deadlock)
                 assert k in tails and (k + 1 >= nloc or k + 1 in tails), (k, sorted(tails))
-            else:
-                tails.add(k)
-            if not isb:
-                yield from wait(ad_a[a % S], a // S)
-                assert slot_p[a % S] == a
-                empty[n % S].arrive()
-                a += 1
-            else:
                 if b >= S:
                     yield from wait(ad_b[(b - S) % S], (b - S) // S)
                 slot_c[b % S] = b
                 cf_b[b % S].arrive()
                 b += 1
+            else:
+                yield from wait(ad_a[a % AS], a // AS)
+                assert slot_p[a % AS] == a
+                a_free[a % AS].arrive()
+                tails.add(k)
+                a += 1
 
     def compute(w):
         a = b = 0
         for n in range(nops):
             isb, k = op_of(n, nloc, Lx)
             yield from wait(full[n % S], n // S)
+            assert stage_owner[n % S] == n
+            readers[n] = readers.get(n, 0) + 1
+            if readers[n] == 16:
+                stage_owner[n % S] = None  # last reader done (arrives below)
             if not isb:
+                empty[n % S].arrive()
+                if a >= AS:
+                    yield from wait(a_free[a % AS], (a - AS) // AS)
                 if w == 0:
-                    slot_p[a % S] = a
-                ad_a[a % S].arrive()
+                    slot_p[a % AS] = a
+                ad_a[a % AS].arrive()
                 a += 1
             else:
                 yield from wait(cf_b[b % S], b // S)
                 assert slot_c[b % S] == b
+                if w == 0:
+                    rows_b.append(k)
+                empty[n % S].arrive()
                 ad_b[b % S].arrive()
                 b += 1
 
-    gens = [loader(), store(), coef()] + [compute(w) for w in range(16)]
+    gens = [loader(), coef()] + [compute(w) for w in range(16)]
     live = list(gens)
-    for _ in range(200000):
+    for _ in range(400000):
         if not live:
             break
         g = rnd.choice(live)
@@ -148,7 +157,7 @@ def simulate(nloc, L, seed, write_dl=True):
 
 
 @pytest.mark.parametrize("nloc", [1, 2, 3, 4, 7, 13, 20])
-@pytest.mark.parametrize("L", [1, 2, 3])
+@pytest.mark.parametrize("L", [1, 2, 3, 4])
 def test_protocol_completes_without_aliasing(nloc, L):
     for seed in range(3):
         simulate(nloc, L, seed)
