@@ -117,6 +117,17 @@ int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int32_t* tokens
                             double* stats, void* workspace, size_t workspace_bytes,
                             void* stream);
 
+/* Rollout-side action-token sampling (the token-head analogue of
+ * policy.sample_chunk_batch, policy.py:150-158): per row r of logits [R, V]
+ * draw tokens[r] ~ softmax(x_r) with Philox4x32-10 keyed by (seed, offset, r)
+ * (a pure function of those, never of scheduling), lp_tok[r] = x_r[token] -
+ * logsumexp(x_r) (f64, may be NULL), and per chunk of T rows the behaviour
+ * log-prob blp (f32, as the sampler stores it, runtime.py:698) and/or the
+ * f64 chunk log-prob (numpy pairwise order).  One pass over the logits. */
+int dvla_token_sample(const void* logits, int dtype, int64_t R, int64_t V, int64_t T,
+                      uint64_t seed, uint64_t offset, int32_t* tokens, double* lp_tok,
+                      float* blp, double* lp_chunk, void* stream);
+
 /* GRPO epilogue on precomputed chunk log-probs (any head): rho, clipped
  * surrogate, coefficient, loss and stats in canonical order (grpo.py:246-293).
  * blp64 (f64) overrides blp (f32) when non-NULL.  coeff_out may be NULL. */
