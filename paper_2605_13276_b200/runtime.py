@@ -321,6 +321,7 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
     from .planes import Channel, ControlPlane, Plane, RunAborted, Transport, TransportMode
     from .pools import Pool, PoolKind
     from .replicate import device_snapshot
+    from .rollout import sample_action_tokens
 
     cfg.validate()
     dev = torch.device(device) if device is not None else torch.device(
@@ -335,8 +336,11 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
     # ---- dual pools: long-lived model state vs epoch-recycled rollout staging
     model_bytes = V * H * (4 + 8 + 8) + 2 * V * H * 2 + (64 << 20)
     model_pool = Pool(PoolKind.MODEL_COMPUTE, model_bytes, device=dev)
-    env_bytes = R * (H * 2 + V * 2 + 64) + (64 << 20)
-    env_pool = Pool(PoolKind.ENV_AUX, env_bytes, device=dev)
+    # ENV_AUX: one epoch-recycled arena per epoch the staleness gate lets be in
+    # flight (limit + 2); each is reset wholesale when its epoch starts again
+    env_bytes = R * (V * 2 + 64) + n_traj * C * (H * 2 + 224 * 224 * 3 // 64 * 5) + (16 << 20)
+    env_pools = [Pool(PoolKind.ENV_AUX, env_bytes, device=dev)
+                 for _ in range(cfg.staleness_limit + 2)]
     policy = TokenPolicy(cfg, model_pool, dev)
     gcfg = GrpoConfig(group_size=G, lr=cfg.lr)
     abort = threading.Event()
@@ -364,31 +368,36 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
     def sampler_lane():
         try:
             rng = torch.Generator(device=dev).manual_seed(cfg.seed * 7919 + rank)
-            probe = TokenLoss(cfg.n_groups, G, C, T, V, gcfg, dtype=torch.bfloat16, device=dev)
             for epoch in range(cfg.epochs):
                 snap, stal = board.wait_gate()
                 monitor.beat(LaneId.SAMPLER.value, "rolling")
                 t0 = time.perf_counter()
+                pool = env_pools[epoch % len(env_pools)]
+                pool.epoch_reset()  # its previous epoch was consumed (staleness gate)
+
+                def stage(shape, dtype):
+                    n = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
+                    return pool.view(pool.alloc(n, align=256), dtype).view(*shape)
+
                 with torch.cuda.stream(s_sample):
                     W = snap.params.view(V, H)  # installed replica, zero copy
                     # synthetic LIBERO-shaped observations -> features
-                    img = torch.randint(0, 256, (n_traj * C, 224 * 224 * 3 // 64), device=dev,
-                                        generator=rng, dtype=torch.uint8)
+                    img = stage((n_traj * C, 224 * 224 * 3 // 64), torch.uint8)
+                    img.copy_(torch.randint(0, 256, img.shape, device=dev, generator=rng,
+                                            dtype=torch.uint8))
                     prop = torch.randn(n_traj * C, 8, device=dev, generator=rng)
                     obs = torch.cat([img.float() / 255.0, prop], dim=1)
-                    feats = (obs @ proj).to(torch.bfloat16)                     # [n_traj*C, H]
-                    logits = feats.repeat_interleave(T, dim=0) @ W.t()          # [R, V] bf16
-                    # action-token sampling over the action bins (Gumbel-max)
-                    lo = V - cfg.action_bins
-                    gum = -torch.log(-torch.log(torch.rand(R, cfg.action_bins, device=dev,
-                                                           generator=rng) + 1e-20) + 1e-20)
-                    tokens = (torch.argmax(logits[:, lo:].float() + gum, dim=1) + lo).to(torch.int32)
+                    feats = stage((n_traj * C, H), torch.bfloat16)
+                    feats.copy_(obs @ proj)                                     # [n_traj*C, H]
+                    logits = stage((R, V), torch.bfloat16)
+                    torch.matmul(feats.repeat_interleave(T, dim=0), W.t(), out=logits)
                     rewards = torch.randint(0, 2, (n_traj,), device=dev, generator=rng).float()
                     if epoch in poison_epochs:
                         rewards[0] = float("nan")
-                    # behaviour log-probs: forward-only pass of the fused kernel
-                    probe.launch(logits, tokens, torch.zeros(n_traj * C, device=dev), rewards, None)
-                    blp = probe.lp_chunk.float().clone()
+                    # action tokens ~ softmax(logits) + f32 behaviour log-probs in
+                    # one pass (csrc/sample.cu), Philox keyed by (seed, epoch, row)
+                    tokens, blp, _ = sample_action_tokens(
+                        logits, T, seed=cfg.seed * 1_000_003 + rank, offset=epoch)
                 ev = torch.cuda.Event()
                 ev.record(s_sample)
                 msgs = []
