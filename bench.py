@@ -48,6 +48,7 @@ def _args():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--unfused", action="store_true")
     ap.add_argument("--no-repl", action="store_true")
+    ap.add_argument("--no-swimlane", action="store_true")
     ap.add_argument("--fixed-warmup", action="store_true",
                     help="exactly --warmup warm-up steps (for ncu launch lists)")
     return ap.parse_args()
@@ -292,6 +293,28 @@ def _bench_allreduce(world, dev, barrier, max_over_ranks, nbytes=1 << 30, iters=
             "frac_of_nominal_900": busbw / NVLINK_NOMINAL_GBS}
 
 
+def _bench_swimlane(world, rank, dev, max_over_ranks, epochs=8):
+    """End-to-end RL samples/s of the four-lane swimlane (BASELINE config 4
+    shape: OpenVLA-7B-sized action head V=32,064 x H=4,096, 64 groups x 8
+    trajectories x 56 action tokens per GPU per epoch; one closed loop per
+    GPU, NCCL gradient mean across GPUs).  Host-clock lane timing (the
+    reference's transitions/s definition, metrics.py:101-123)."""
+    from paper_2605_13276_b200.runtime import SwimlaneConfig, run_swimlane
+    cfg = SwimlaneConfig(n_groups=N_GROUPS, group_size=G, chunks=C, tokens=T, vocab=V,
+                         hidden=4096, epochs=epochs, seed=17)
+    res = run_swimlane(cfg, device=dev)
+    s = res.summary()
+    traj = s["trajectories_per_s"]
+    tot = max_over_ranks(0.0) if world == 1 else None
+    del tot
+    return {"trajectories_per_s_rank0": traj,
+            "transitions_per_s_rank0": s["transitions_per_s"],
+            "trajectories_per_s_total": traj * world,
+            "epochs": epochs, "staleness_max": s["staleness_max"],
+            "config": "V=32064, H=4096, 64 groups x 8 traj x 56 tokens per GPU per epoch",
+            "timing": "host clock per lane (reference transitions/s definition)"}
+
+
 def run_ours(a):
     import numpy as np
     import torch
@@ -416,6 +439,11 @@ def run_ours(a):
     del dl
     repl = None if a.no_repl else _bench_replication(world, rank, dev, barrier, max_over_ranks)
     allreduce = _bench_allreduce(world, dev, barrier, max_over_ranks)
+    swim = None
+    if not a.no_swimlane:
+        barrier()
+        swim = _bench_swimlane(world, rank, dev, max_over_ranks)
+        barrier()
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -438,7 +466,7 @@ def run_ours(a):
                        "parallelism": f"dp{world} (group-sharded learner)",
                        "l2": "inputs 1.84 GB/rank > 126 MB L2 (no flush needed)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "replication": repl, "grad_allreduce": allreduce,
+            "replication": repl, "grad_allreduce": allreduce, "swimlane": swim,
             "gpu_launches": 3 * a.steps, "clocks": clk,
             "loss": st["loss"], "mean_ratio": st["mean_ratio"],
             "clip_fraction": st["clip_fraction"],
