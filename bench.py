@@ -300,18 +300,21 @@ def _bench_swimlane(world, rank, dev, max_over_ranks, epochs=8):
     GPU, NCCL gradient mean across GPUs).  Host-clock lane timing (the
     reference's transitions/s definition, metrics.py:101-123)."""
     from paper_2605_13276_b200.runtime import SwimlaneConfig, run_swimlane
-    cfg = SwimlaneConfig(n_groups=N_GROUPS, group_size=G, chunks=C, tokens=T, vocab=V,
-                         hidden=4096, epochs=epochs, seed=17)
-    res = run_swimlane(cfg, device=dev)
-    s = res.summary()
-    traj = s["trajectories_per_s"]
-    tot = max_over_ranks(0.0) if world == 1 else None
-    del tot
+    out = {}
+    for mode, limit in (("async", 1), ("sync", 0)):
+        cfg = SwimlaneConfig(n_groups=N_GROUPS, group_size=G, chunks=C, tokens=T, vocab=V,
+                             hidden=4096, epochs=epochs, seed=17, staleness_limit=limit)
+        s = run_swimlane(cfg, device=dev).summary()
+        out[mode] = s
+    traj = out["async"]["trajectories_per_s"]
     return {"trajectories_per_s_rank0": traj,
-            "transitions_per_s_rank0": s["transitions_per_s"],
+            "transitions_per_s_rank0": out["async"]["transitions_per_s"],
             "trajectories_per_s_total": traj * world,
-            "epochs": epochs, "staleness_max": s["staleness_max"],
-            "config": "V=32064, H=4096, 64 groups x 8 traj x 56 tokens per GPU per epoch",
+            "sync_trajectories_per_s_rank0": out["sync"]["trajectories_per_s"],
+            "async_over_sync": traj / max(out["sync"]["trajectories_per_s"], 1e-12),
+            "epochs": epochs, "staleness_max": out["async"]["staleness_max"],
+            "config": "V=32064, H=4096, 64 groups x 8 traj x 56 tokens per GPU per epoch; "
+                      "sync = the same lanes with staleness limit 0 (strict alternation)",
             "timing": "host clock per lane (reference transitions/s definition)"}
 
 
