@@ -299,12 +299,18 @@ class RunResult:
         self.lane_busy: dict = {}
 
     def summary(self) -> dict:
+        """Throughput between the first and the last published update (wall
+        clock), i.e. after the pipeline filled; the reference's per-epoch
+        step-time sum (metrics.py:101-123) is reported beside it."""
         post = self.reports[1:] if len(self.reports) > 1 else self.reports
         trans = sum(r["transitions"] for r in post)
-        span = sum(r["step_time"] for r in post)
         traj = sum(r["trajectories"] for r in post)
-        return {"transitions_per_s": trans / max(span, 1e-12),
-                "trajectories_per_s": traj / max(span, 1e-12),
+        span = sum(r["step_time"] for r in post)
+        pubs = [r["t_publish"] for r in self.reports]
+        wall = (pubs[-1] - pubs[0]) if len(pubs) > 1 else max(self.wall, 1e-12)
+        return {"transitions_per_s": trans / max(wall, 1e-12),
+                "trajectories_per_s": traj / max(wall, 1e-12),
+                "transitions_per_s_steptime": trans / max(span, 1e-12),
                 "wall": self.wall, "staleness_max": self.staleness_max,
                 "updates": len(self.update_stats)}
 
@@ -488,7 +494,8 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
                 result.reports.append({"epoch": epoch, "policy_version": meta["behavior_version"],
                                        "version_after": v, "step_time": step_time,
                                        "transitions": n_traj * C * T,
-                                       "trajectories": n_traj, "staleness": meta["staleness"]})
+                                       "trajectories": n_traj, "staleness": meta["staleness"],
+                                       "t_publish": time.perf_counter()})
             with dist_cv:
                 dist_q.append((None, None))
                 dist_cv.notify_all()
