@@ -862,17 +862,28 @@ __global__ void __launch_bounds__(kEpiThreads) grpo_epilogue_kernel(EpiParams e)
         atomicMin(&s_first_traj, (unsigned long long)(idx / e.C));
     }
     __syncthreads();
-    if (tid == 0) {
+    {
+      // three independent sequential sums in canonical entry order, one per
+      // warp (the reference accumulates total_loss / ratio_sum / clip_count
+      // in entry order, grpo.py:269-273)
       const int64_t lim = (n_entries - base < kEpiThreads) ? n_entries - base : kEpiThreads;
-      for (int64_t t = 0; t < lim; ++t) {
-        loss = __dadd_rn(loss, s_loss[t]);
-        ratio_sum = __dadd_rn(ratio_sum, s_rho[t]);
-        clip_count += s_clip[t];
+      if (tid == 0) {
+        for (int64_t t = 0; t < lim; ++t) loss = __dadd_rn(loss, s_loss[t]);
+      } else if (tid == 32) {
+        for (int64_t t = 0; t < lim; ++t) ratio_sum = __dadd_rn(ratio_sum, s_rho[t]);
+      } else if (tid == 64) {
+        for (int64_t t = 0; t < lim; ++t) clip_count += s_clip[t];
       }
     }
     __syncthreads();
   }
+  __shared__ double s_fin[2];
+  if (tid == 32) s_fin[0] = ratio_sum;
+  if (tid == 64) s_fin[1] = clip_count;
+  __syncthreads();
   if (tid == 0) {
+    ratio_sum = s_fin[0];
+    clip_count = s_fin[1];
     double code = 0.0, group = 0.0;
     if (s_first_reward != ~0ull) {
       code = 1.0;
