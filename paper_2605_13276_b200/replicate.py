@@ -183,8 +183,8 @@ class ChainReplicator:
     `nbytes` each in device slabs (or in a MODEL_COMPUTE pool's slab).
     """
 
-    def __init__(self, nbytes: int, ranks=None, n_buffers: int = 2, chunk_bytes: int = 8 << 20,
-                 ctas_per_hop: int = 64, group=None):
+    def __init__(self, nbytes: int, ranks=None, n_buffers: int = 2, chunk_bytes: int = 2 << 20,
+                 ctas_per_hop: int = 128, group=None):
         import torch.distributed as dist
         torch = _torch()
         if nbytes % 16:
