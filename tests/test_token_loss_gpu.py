@@ -208,3 +208,53 @@ def test_full_c2_batch_properties():
     got = dl[rows].float().cpu().numpy()
     err = np.abs(got - odl)
     assert np.all(err <= 1e-2 * np.abs(odl) + 1e-2 * np.abs(odl).max())
+
+
+def test_long_chunks_fall_back_to_unfused_kernels():
+    """T > 128 tokens per chunk exceeds the fused warp-pairwise path."""
+    import torch
+    case = _case(12, 2, 4, 1, 160, 1024, torch.bfloat16)
+    _check(*case, torch.bfloat16, fused=True, rtol=1e-2)
+
+
+def test_f32_openvla_vocab_matches_oracle():
+    import torch
+    case = _case(13, 2, 4, 1, 8, 32064, torch.float32, binary=False)
+    _check(*case, torch.float32, fused=True, rtol=1e-5)
+
+
+def test_misaligned_logits_take_the_scalar_path():
+    """A logits view starting one element into its storage (not 16-byte
+    aligned) must still be exact: the C-ABI picks the scalar kernels."""
+    import torch
+    from paper_2605_13276_b200 import grpo
+    x, tokens, blp, rewards, ids = _case(14, 2, 4, 1, 3, 256, torch.float32)
+    dev = torch.device("cuda", 0)
+    R, V = x.reshape(-1, 256).shape
+    store = torch.empty(R * V + 1, dtype=torch.float32, device=dev)
+    lg = store[1:].view(R, V)
+    lg.copy_(torch.from_numpy(x.reshape(R, V)).to(dev))
+    cfg = grpo.GrpoConfig(group_size=4)
+    tl = grpo.TokenLoss(2, 4, 1, 3, V, cfg, dtype=torch.float32)
+    tl.set_groups(ids)
+    dl = torch.empty(R * V + 1, dtype=torch.float32, device=dev)[1:].view(R, V)
+    tl.launch(lg, torch.from_numpy(tokens.reshape(-1)).to(dev),
+              torch.from_numpy(blp.reshape(-1)).to(dev), torch.from_numpy(rewards.reshape(-1)).to(dev),
+              dl)
+    st = tl.stats(torch.from_numpy(rewards.reshape(-1)))
+    oloss, odl, ost = O.grpo_token_grad(x, tokens, blp, rewards, ids)
+    assert st["loss"] == pytest.approx(oloss, rel=1e-6, abs=1e-12)
+    np.testing.assert_allclose(dl.cpu().numpy(), odl.reshape(R, V), rtol=1e-5,
+                               atol=1e-5 * np.abs(odl).max())
+
+
+def test_zero_advantage_groups_give_zero_gradient_rows():
+    """All-success / all-fail groups have A = 0 -> coefficient 0 -> the fused
+    kernel's zero-row fast path must write exact zeros (and count them as
+    clipped, reference grpo.py:272-273)."""
+    import torch
+    x, tokens, blp, rewards, ids = _case(15, 3, 8, 1, 56, 4096, torch.bfloat16)
+    rewards[:] = 1.0
+    loss, dl, st = _run_gpu(x, tokens, blp, rewards, ids, torch.bfloat16)
+    assert np.all(dl == 0.0)
+    assert st["clip_fraction"] == 1.0 and loss == 0.0
