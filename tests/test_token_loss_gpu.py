@@ -243,7 +243,8 @@ def test_misaligned_logits_take_the_scalar_path():
               dl)
     st = tl.stats(torch.from_numpy(rewards.reshape(-1)))
     oloss, odl, ost = O.grpo_token_grad(x, tokens, blp, rewards, ids)
-    assert st["loss"] == pytest.approx(oloss, rel=1e-6, abs=1e-12)
+    scale = np.abs(ost["coeff"]).mean()
+    assert abs(st["loss"] - oloss) <= 1e-5 * max(abs(oloss), scale)
     np.testing.assert_allclose(dl.cpu().numpy(), odl.reshape(R, V), rtol=1e-5,
                                atol=1e-5 * np.abs(odl).max())
 
