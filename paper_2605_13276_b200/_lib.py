@@ -17,7 +17,7 @@ from pathlib import Path
 
 from .core import ConfigError, UsageError
 
-_LIB_PATH = Path(__file__).resolve().parent / "libdvla_b200.so"
+_LIB_PATH = Path(os.environ["DVLA_B200_LIB"]) if os.environ.get("DVLA_B200_LIB") else Path(__file__).resolve().parent / "libdvla_b200.so"
 
 # status codes (include/dvla_b200.h: enum dvla_status)
 OK = 0

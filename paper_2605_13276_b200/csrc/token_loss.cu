@@ -13,14 +13,14 @@
 //
 // Kernels
 //   tok_adv_kernel        advantages per group (bit-exact, grpo.py:89-99)
-//   tok_fused_bf16_kernel persistent, 1 CTA/SM, warp-specialised: a producer
+//   tok_fused_bf16_kernel persistent, 1 CTA/SM, warp-specialised: a loader
 //                         warp streams logits rows HBM->SMEM with TMA bulk
-//                         copies (cp.async.bulk), 16 compute warps do
-//                         max / sum-exp (MUFU ex2) / gather on the SMEM row,
-//                         publish lp_tok, and the last CTA to finish a chunk
-//                         computes that chunk's coefficient; dlogits are then
-//                         written in place in SMEM and TMA-stored back.
-//                         Logits are read from HBM exactly once:
+//                         copies, 20 compute warps take max / sum-exp and
+//                         later write dlogits in place in SMEM, a tail /
+//                         prep / publisher warp trio turns partials into
+//                         lp_tok and chunk coefficients, a store warp streams
+//                         dlogits out with TMA bulk stores.  Each row is read
+//                         from HBM once (the second read hits L2):
 //                         compulsory traffic 2*N*2 bytes.
 //   tok_rows_kernel<T>    unfused forward (any dtype / alignment / V)
 //   tok_chunk_kernel      unfused per-chunk coefficient
@@ -33,7 +33,7 @@
 
 namespace dvla {
 
-constexpr int kFusedComputeWarps = 16;
+constexpr int kFusedComputeWarps = 20;
 constexpr int kFusedComputeThreads = kFusedComputeWarps * 32;
 constexpr int kFusedStages = 3;    // SMEM row stages and B coefficient slots
 constexpr int kASlots = 8;         // A-row partial slots (coef-warp slack)
@@ -143,42 +143,48 @@ __device__ __forceinline__ double chunk_lp_pairwise(const double* __restrict__ l
 //
 // One CTA per SM (persistent), rows assigned round-robin (row = cta + k*grid).
 // Every CTA walks one op sequence: A(0..L-1), then A(k), B(k-L), ..., B(n-1):
-//   A(k)  row k streamed HBM -> SMEM by TMA; 16 compute warps take warp
-//         max / sum-exp (MUFU ex2) and publish (m_w, s_w); the coefficient
-//         warp combines them into lse (f64), gathers the target logit,
-//         publishes lp_tok and bumps the chunk counter (red.release.gpu).
+//   A(k)  row k streamed HBM -> SMEM by TMA; the compute warps take warp
+//         max (packed bf16) / sum-exp (FFMA2 + MUFU ex2 + FADD2) partials;
+//         the tail warp combines them into lse (f64), forms lp_tok from the
+//         gathered target logit and hands it to the publisher, which stores
+//         it and bumps the chunk counter (red.release.gpu).
 //   B(k)  row k streamed again -- from L2, L rounds (~L*148*64 KB) after
-//         A(k) -- the coefficient warp waits for the chunk to be complete on
-//         all CTAs (long done by then), sums its T token log-probs (numpy
+//         A(k) -- the prep warp waits for the chunk to be complete on all
+//         CTAs (long done by then), sums its T token log-probs (numpy
 //         pairwise order) and evaluates the GRPO coefficient; the compute
-//         warps write d loss / d logits in place and the store warp streams
-//         the row back with a TMA bulk store.
+//         warps overwrite the row in SMEM with d loss / d logits and the
+//         store warp streams it out with one TMA bulk store.
 // HBM traffic stays at the compulsory 2*N*2 bytes while the L-round lag
-// hides the cross-CTA chunk dependency.  A(k+L) precedes B(k) on every CTA,
-// so the chunk wait is deadlock-free while all CTAs are co-resident
-// (grid <= #SMs, T <= grid).
+// hides the cross-CTA chunk dependency.  A(k+L) precedes B(k) on every CTA
+// and the tail warp never waits on another CTA, so the chunk wait is
+// deadlock-free while all CTAs are co-resident (grid <= #SMs, T <= grid).
 //
-// Warp roles: 0..15 compute (they also store dlogits, 16-byte streaming
-// stores from registers), 16 loader, 17 coefficient, 18 idle,
-// 19 publisher (lp_tok + release of the chunk counters).
+// Warp roles: 0..W-1 compute, W loader, W+1 tail, W+2 store, W+3 publisher
+// (lp_tok + release of the chunk counters), W+4 prep.
 // Barriers (every barrier completes once per use of its own ring index, and
 // every waiter walks its ring in order, so parity never aliases):
 //   full[s], empty[s]  per SMEM stage s = op % 3: loader <-> compute warps
-//                      (a stage is free as soon as its row has been read)
-//   adoneA[a % 8]      compute -> coef, per A op a (SMEM partial slot a % 8)
-//   afree[a % 8]       coef -> compute, partial slot consumed
-//   cfullB[b % 3]      coef -> compute, per B op b (coefficient slot b % 3)
-//   adoneB[b % 3]      compute -> coef (coefficient slot b % 3 consumed)
-// The op sequence and barrier protocol were model-checked for races and
-// parity aliasing (tests/test_fused_protocol.py).
+//                      (A: free once read; B: freed by the store warp, one
+//                      arrival worth W, once its bulk copy has read it)
+//   adoneA[a % 8]      compute -> tail, per A op a (SMEM partial slot a % 8)
+//   afree[a % 8]       tail -> compute, partial slot consumed
+//   tdone[k % 8]       tail -> prep, (lse, target) of row k in the ring
+//   cfullB[b % 3]      prep -> compute, per B op b (coefficient slot b % 3)
+//   adoneB[b % 3]      compute -> prep (coefficient slot b % 3 consumed)
+//   bdone[b % 3]       compute -> store, B row b written in SMEM
+//   pubfull/pubempty   tail <-> publisher, 8-entry lp_tok ring
+// The op sequence and barrier protocol are model-checked for deadlock,
+// races and parity aliasing (tests/test_fused_protocol.py).
 constexpr int kWarpLoader = kFusedComputeWarps;
-constexpr int kCoefWarp = kFusedComputeWarps + 1;
+constexpr int kTailWarp = kFusedComputeWarps + 1;
 constexpr int kWarpStore = kFusedComputeWarps + 2;
 constexpr int kWarpPublish = kFusedComputeWarps + 3;
-constexpr int kFusedThreadsWS = (kFusedComputeWarps + 4) * 32;
+constexpr int kPrepWarp = kFusedComputeWarps + 4;
+constexpr int kFusedThreadsWS = (kFusedComputeWarps + 5) * 32;
 constexpr int kPubRing = 8;
-constexpr int kLagRounds = 4;  // measured best on B200 (lag 2..4 sweep, tools/fused_variants.py)
-constexpr int kRing = 8;  // > kLagRounds + 1 rows of (lse, target) in flight
+constexpr int kLagRounds = 4;  // measured best on B200 (lag 2..6 sweep, tools/fused_variants.py)
+constexpr int kRing = 8;       // (lse, target) rows in flight tail -> prep; needs lag < kRing
+constexpr int kMaxLag = kRing - 1;
 
 struct FusedSmem {
   uint64_t full[kFusedStages];
@@ -187,6 +193,8 @@ struct FusedSmem {
   uint64_t afree[kASlots];
   uint64_t adoneB[kFusedStages];
   uint64_t cfullB[kFusedStages];
+  uint64_t bdone[kFusedStages];  // compute -> store warp, B row b % 3 written in SMEM
+  uint64_t tdone[kRing];         // tail -> prep warp, (lse, target) of row k % kRing
   double ws[kASlots][kFusedComputeWarps];
   float wm[kASlots][kFusedComputeWarps];
   float kval[kFusedStages];   // lse*log2e - log2|c|
@@ -203,52 +211,16 @@ struct FusedSmem {
   double pub_lp[kPubRing];
 };
 
-// coefficient not yet published (the workspace is memset to 0xff)
-constexpr unsigned long long kCoeffPending = 0xffffffffffffffffull;
-
-__device__ __forceinline__ unsigned long long spin_coeff(const unsigned long long* c,
-                                                         uint32_t* err) {
-  unsigned long long v = ld_acquire_gpu_u64(c);
-  if (v != kCoeffPending) return v;
-  const uint64_t t0 = globaltimer_ns();
-  uint32_t ns = 32;
-  while ((v = ld_acquire_gpu_u64(c)) == kCoeffPending) {
-    __nanosleep(ns);
-    if (ns < 256) ns <<= 1;
-    if (globaltimer_ns() - t0 > kSpinTimeoutNs) {
-      atomicOr(err, kErrTimeout);
-      return 0x7ff8000000000000ull;
-    }
-  }
-  return v;
-}
-
-__device__ __forceinline__ bool spin_until_at_least(const uint32_t* cnt, uint32_t target,
-                                                    uint32_t* err) {
-  if (ld_acquire_gpu(cnt) >= target) return true;
-  const uint64_t t0 = globaltimer_ns();
-  uint32_t ns = 32;
-  while (ld_acquire_gpu(cnt) < target) {
-    __nanosleep(ns);
-    if (ns < 256) ns <<= 1;
-    if (globaltimer_ns() - t0 > kSpinTimeoutNs) {
-      atomicOr(err, kErrTimeout);
-      return false;
-    }
-  }
-  return true;
-}
-
 // op n of a CTA with nloc rows and lag L: (is_B, local row)
-__device__ __forceinline__ void op_of(int64_t n, int64_t nloc, int L, bool* isB, int64_t* k) {
-  const int64_t Le = nloc < L ? nloc : L;  // effective lag
+__device__ __forceinline__ void op_of(int n, int nloc, int L, bool* isB, int* k) {
+  const int Le = nloc < L ? nloc : L;  // effective lag
   if (n < Le) {
     *isB = false;
     *k = n;
     return;
   }
-  const int64_t m = n - Le;  // pairs (A(Le + j), B(j)) for j < nloc - Le, then B tail
-  const int64_t pairs = nloc - Le;
+  const int m = n - Le;  // pairs (A(Le + j), B(j)) for j < nloc - Le, then B tail
+  const int pairs = nloc - Le;
   if (m < 2 * pairs) {
     *isB = (m & 1) != 0;
     *k = (m & 1) ? (m >> 1) : (Le + (m >> 1));
@@ -256,6 +228,23 @@ __device__ __forceinline__ void op_of(int64_t n, int64_t nloc, int L, bool* isB,
   }
   *isB = true;
   *k = pairs + (m - 2 * pairs);
+}
+
+// d loss / d logits of one B row, in place in SMEM: v = -c * p_v
+// (sgn = 0x80008000 flips both bf16 signs when c > 0)
+__device__ __forceinline__ void b_row(uint4* __restrict__ v, int nvec, int tid, float K,
+                                      uint32_t sgn) {
+  const uint64_t l2e2 = f2pack(kLog2e, kLog2e), nK2 = f2pack(-K, -K);
+  auto e2 = [&](uint32_t w) {
+    float y0, y1;
+    f2unpack(bf16x2_fma2(w, l2e2, nK2), y0, y1);
+    return pack_bf16x2(ex2f(y0), ex2f(y1)) ^ sgn;
+  };
+#pragma unroll 2
+  for (int i = tid; i < nvec; i += kFusedComputeThreads) {
+    const uint4 x = v[i];
+    v[i] = make_uint4(e2(x.x), e2(x.y), e2(x.z), e2(x.w));
+  }
 }
 
 __global__ void __launch_bounds__(kFusedThreadsWS, 1)
@@ -269,10 +258,10 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   const int64_t V = p.V;
   const uint32_t row_bytes = static_cast<uint32_t>(V * 2);
   const int64_t G = gridDim.x;
-  const int64_t nloc = (p.R > blockIdx.x) ? (p.R - blockIdx.x + G - 1) / G : 0;
-  const int64_t nops = write_dl ? 2 * nloc : nloc;
+  const int nloc = (p.R > blockIdx.x) ? static_cast<int>((p.R - blockIdx.x + G - 1) / G) : 0;
+  const int nops = write_dl ? 2 * nloc : nloc;
   const int L = write_dl ? lag : 1 << 30;  // forward-only: A ops only
-  auto row_of = [&](int64_t k) { return blockIdx.x + k * G; };
+  auto row_of = [&](int k) { return static_cast<int64_t>(blockIdx.x) + k * G; };
   auto buf = [&](int s) { return bufs + static_cast<size_t>(s) * stage_bytes; };
   const int64_t T = p.T;
   unsigned long long* dbg = g_dbg;
@@ -284,11 +273,13 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       mbar_init(&S.empty[s], kFusedComputeWarps);
       mbar_init(&S.adoneB[s], kFusedComputeWarps);
       mbar_init(&S.cfullB[s], 1);
+      mbar_init(&S.bdone[s], kFusedComputeWarps);
     }
     for (int s = 0; s < kASlots; ++s) {
       mbar_init(&S.adoneA[s], kFusedComputeWarps);
       mbar_init(&S.afree[s], 1);
     }
+    for (int j = 0; j < kRing; ++j) mbar_init(&S.tdone[j], 1);
     for (int j = 0; j < kPubRing; ++j) {
       mbar_init(&S.pubfull[j], 1);
       mbar_init(&S.pubempty[j], 1);
@@ -305,7 +296,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
       const uint64_t pol_keep = l2_policy_evict_last();
-      for (int64_t n = 0; n < nops; ++n) {
+      for (int n = 0; n < nops; ++n) {
         const int s = static_cast<int>(n % kFusedStages);
         if (n >= kFusedStages) {
           DBG_T0();
@@ -313,7 +304,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
           DBG_ADD(8);
         }
         bool isB;
-        int64_t k;
+        int k;
         op_of(n, nloc, L, &isB, &k);
         mbar_arrive_expect_tx(&S.full[s], row_bytes);
         if (isB)  // second (last) read of the row: from L2, then evict
@@ -327,17 +318,40 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     return;
   }
 
-  if (warp == kWarpStore) return;  // dlogits are stored by the compute warps
+  // ---------------------------------------------------------- store warp
+  // B rows are written in place in SMEM and streamed out with one bulk copy
+  // each; the stage returns to the loader once the copy has read it.
+  if (warp == kWarpStore) {
+    if (!write_dl || lane != 0) return;
+    int nb = 0;
+    const uint64_t pol_ef = l2_policy_evict_first();
+    for (int n = 0; n < nops; ++n) {
+      bool isB;
+      int k;
+      op_of(n, nloc, L, &isB, &k);
+      if (!isB) continue;
+      const int s = static_cast<int>(n % kFusedStages);
+      mbar_wait(&S.bdone[nb % kFusedStages], static_cast<uint32_t>((nb / kFusedStages) & 1));
+      ++nb;
+      // dlogits are not re-read here: keep L2 for the rows B still needs
+      tma_store_1d_evict_first(dl + row_of(k) * V, buf(s), row_bytes, pol_ef);
+      bulk_commit();
+      bulk_wait_read<0>();
+      mbar_arrive_cnt(&S.empty[s], kFusedComputeWarps);
+    }
+    bulk_wait<0>();
+    return;
+  }
 
   // ------------------------------------------------------ publisher warp
   // Publishes each row's lp_tok and bumps its chunk counter with a release
   // reduction; the release fence's wait for the store stalls only this warp.
   if (warp == kWarpPublish) {
     if (!write_dl || lane != 0) return;
-    int64_t na = 0;  // A ops seen
-    for (int64_t n = 0; n < nops; ++n) {
+    int na = 0;  // A ops seen
+    for (int n = 0; n < nops; ++n) {
       bool isB;
-      int64_t k;
+      int k;
       op_of(n, nloc, L, &isB, &k);
       if (isB) continue;
       const int j = static_cast<int>(na % kPubRing);
@@ -358,190 +372,126 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     return;
   }
 
-  // ---------------------------------------------------- coefficient warp
-  if (warp == kCoefWarp) {
-    int64_t a = 0, b = 0;  // A / B op counters
-    // Prefetched inputs of the next B row's chunk coefficient.  Every CTA
-    // evaluates the coefficients of its own B rows from the published token
-    // log-probs (same inputs, same code: bitwise identical across CTAs), so
-    // no CTA ever waits on another CTA's finaliser -- only on its rows.
-    int64_t pq = -1;       // chunk being prefetched
-    uint32_t pc = 0;       // acquired counter value (this lane)
-    bool pv_ok = false;    // pv[] holds the chunk's token log-probs
-    double pv[4] = {0.0, 0.0, 0.0, 0.0};
-    float pblp = 0.f;
-    double padv = 0.0;
-    auto prefetch_vals = [&]() {
-      // called with pc acquired on every lane; loads ordered after the acquire
-      const double* lt = p.lp_tok + pq * T;
+  // ----------------------------------------------------------- tail warp
+  // Turns every A row's per-warp partials into lse (f64) and lp_tok, hands
+  // lp_tok to the publisher (other CTAs' chunks wait for it, so this warp
+  // never waits on anything but its own compute warps) and leaves (lse,
+  // target) in the ring for the prep warp.
+  if (warp == kTailWarp) {
+    for (int k = 0; k < nloc; ++k) {
+      const int sa = static_cast<int>(k % kASlots);
+      const int64_t r = row_of(k);
+      mbar_wait(&S.adoneA[sa], static_cast<uint32_t>((k / kASlots) & 1));
+      const int32_t tgt = S.tgta[sa];
+      const float xt_f = S.xt[sa];
+      const float mw = (lane < kFusedComputeWarps) ? S.wm[sa][lane] : -INFINITY;
+      const double sw = (lane < kFusedComputeWarps) ? S.ws[sa][lane] : 0.0;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.afree[sa]);  // partial slot sa consumed
+      const float M = warp_max_f32(mw);
+      double term = (lane < kFusedComputeWarps && sw > 0.0)
+                        ? sw * static_cast<double>(ex2f((mw - M) * kLog2e))
+                        : 0.0;
+      term = warp_sum_f64(term);
+      if (lane == 0) {
+        const double lse = static_cast<double>(M) + log(term);
+        const double xt = static_cast<double>(xt_f);
+        if (tgt < 0) atomicOr(p.err, kErrToken);
+        if (write_dl) {
+          const int j = static_cast<int>(k % kPubRing);
+          S.ring_lse[k % kRing] = lse;
+          S.ring_tgt[k % kRing] = tgt;
+          mbar_arrive(&S.tdone[k % kRing]);
+          if (k >= kPubRing)
+            mbar_wait(&S.pubempty[j], static_cast<uint32_t>(((k / kPubRing) - 1) & 1));
+          S.pub_lp[j] = xt - lse;
+          mbar_arrive(&S.pubfull[j]);
+        } else {
+          p.lse[r] = lse;
+          p.lp_tok[r] = xt - lse;
+        }
+      }
+      __syncwarp();
+    }
+    return;
+  }
+
+  // ----------------------------------------------------------- prep warp
+  // For each B row in order: wait until the row's chunk is complete on all
+  // CTAs (acquire on its counter; L rounds after A, normally long done),
+  // sum its T published token log-probs (numpy pairwise order), evaluate
+  // rho, the clipped surrogate and the coefficient (every CTA computes the
+  // same value from the same inputs) and hand them to the compute warps.
+  if (warp == kPrepWarp) {
+    if (!write_dl) return;
+    const uint64_t t_start = globaltimer_ns();
+    for (int k = 0; k < nloc; ++k) {
+      const int sb = static_cast<int>(k % kFusedStages);
+      const int64_t r = row_of(k);
+      const int64_t q = r / T;
+      uint32_t c = (lane == 0) ? ld_acquire_gpu(p.cnt + q) : 0u;
+      c = __shfl_sync(0xffffffffu, c, 0);
+      uint32_t spins = 0;
+      while (c < static_cast<uint32_t>(T)) {
+        __nanosleep(64);
+        c = (lane == 0) ? ld_acquire_gpu(p.cnt + q) : 0u;
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if ((++spins & 1023u) == 0 && globaltimer_ns() - t_start > kSpinTimeoutNs) {
+          if (lane == 0) atomicOr(p.err, kErrTimeout);
+          break;
+        }
+      }
+      __syncwarp();  // lane 0's acquire orders the loads below for the warp
+      double pv[4];
+      const double* lt = p.lp_tok + q * T;
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         const int64_t t = 32 * m + lane;
         pv[m] = (t < T) ? __ldcg(lt + t) : 0.0;
       }
-      pblp = __ldg(p.blp + pq);
-      padv = __ldg(p.adv + pq / p.C);
-      pv_ok = true;
-    };
-    auto poll = [&]() {  // advance the prefetch state machine without blocking
-      if (pq < 0 || pv_ok) return;
-      if (__all_sync(0xffffffffu, pc >= static_cast<uint32_t>(T)))
-        prefetch_vals();
-      else
-        pc = ld_acquire_gpu(p.cnt + pq);
-    };
-    auto process = [&](int64_t n) {
-      bool isB;
-      int64_t k;
-      op_of(n, nloc, L, &isB, &k);
-      const int64_t r = row_of(k);
-      if (!isB) {
-        // ---- tail of A(k): lse (f64) and the target's log-prob
-        const int sa = static_cast<int>(a % kASlots);
-        {
-          DBG_T0();
-          mbar_wait(&S.adoneA[sa], static_cast<uint32_t>((a / kASlots) & 1));
-          if (lane == 0) { DBG_ADD(2); }
+      const float pblp = __ldg(p.blp + q);
+      const double padv = __ldg(p.adv + q / p.C);
+      const double lp = warp_pairwise_small(pv, static_cast<int>(T), lane);
+      mbar_wait(&S.tdone[k % kRing], static_cast<uint32_t>((k / kRing) & 1));  // own tail
+      if (k >= kFusedStages)  // coefficient slot sb consumed by the compute warps
+        mbar_wait(&S.adoneB[sb], static_cast<uint32_t>(((k - kFusedStages) / kFusedStages) & 1));
+      if (lane == 0) {
+        ChunkTerms ct = chunk_terms(lp, static_cast<double>(pblp), padv, p.w, p.clip_eps,
+                                    p.kl_coeff);
+        const double cc = ct.coeff;
+        if (r % T == 0) {  // one writer per chunk for the epilogue
+          p.lp_chunk[q] = lp;
+          p.coeff[q] = cc;
         }
-        // read everything this tail needs from slot sa, then free the stage
-        // (the compute warps already gathered the target logit)
-        const int32_t tgt = S.tgta[sa];
-        const float xt_f = S.xt[sa];
-        const float mw = (lane < kFusedComputeWarps) ? S.wm[sa][lane] : -INFINITY;
-        const double sw = (lane < kFusedComputeWarps) ? S.ws[sa][lane] : 0.0;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&S.afree[sa]);  // partial slot sa consumed
-        const long long t_tail = dbg ? clock64() : 0;
-        const int j = static_cast<int>(a % kPubRing);
-        const uint32_t pe_ph = static_cast<uint32_t>(((a / kPubRing) - 1) & 1);
-        const bool pub_reuse = write_dl && a >= kPubRing;
-        ++a;
-        const float M = warp_max_f32(mw);
-        double term = (lane < kFusedComputeWarps && sw > 0.0)
-                          ? sw * static_cast<double>(ex2f((mw - M) * kLog2e))
-                          : 0.0;
-        term = warp_sum_f64(term);
-        if (lane == 0) {
-          const double lse = static_cast<double>(M) + log(term);
-          const double xt = static_cast<double>(xt_f);
-          if (tgt < 0) atomicOr(p.err, kErrToken);
-          if (write_dl) {
-            S.ring_lse[k % kRing] = lse;
-            S.ring_tgt[k % kRing] = tgt;
-            if (pub_reuse) mbar_wait(&S.pubempty[j], pe_ph);
-            S.pub_lp[j] = xt - lse;
-            mbar_arrive(&S.pubfull[j]);
-          } else {
-            p.lse[r] = lse;
-            p.lp_tok[r] = xt - lse;
-          }
-          if (dbg) atomicAdd(dbg + 3, static_cast<unsigned long long>(clock64() - t_tail));
+        const double lse = S.ring_lse[k % kRing];
+        uint32_t mode;
+        if (cc == 0.0) {
+          mode = 0u;
+        } else if (!isfinite(cc)) {
+          mode = 2u;
+        } else {
+          mode = 1u | ((cc > 0.0) ? 0x80000000u : 0u);
+          S.kval[sb] = static_cast<float>(lse * 1.4426950408889634 - log2(fabs(cc)));
         }
-        __syncwarp();
-        if (write_dl) poll();
-      } else {
-        // ---- coefficient for B(k); slot b % 3 is free once B op b-3 is done
-        const int sb = static_cast<int>(b % kFusedStages);
-        if (b >= kFusedStages) {
-          DBG_T0();
-          mbar_wait(&S.adoneB[sb], static_cast<uint32_t>(((b - kFusedStages) / kFusedStages) & 1));
-          if (lane == 0) { DBG_ADD(4); }
-        }
-        const long long t_prep = dbg ? clock64() : 0;
-        ++b;
-        const int64_t q = r / T;
-        if (pq != q) {  // no prefetch for this chunk (first B op)
-          pq = q;
-          pv_ok = false;
-          pc = ld_acquire_gpu(p.cnt + q);
-        }
-        if (!pv_ok) {
-          DBG_T0();
-          if (dbg && lane == 0) atomicAdd(dbg + 11, 1ull);
-          const uint64_t t0 = globaltimer_ns();
-          uint32_t ns = 32;
-          while (!__all_sync(0xffffffffu, pc >= static_cast<uint32_t>(T))) {
-            __nanosleep(ns);
-            if (ns < 256) ns <<= 1;
-            pc = ld_acquire_gpu(p.cnt + q);
-            if (globaltimer_ns() - t0 > kSpinTimeoutNs) {
-              if (lane == 0) atomicOr(p.err, kErrTimeout);
-              break;
-            }
-          }
-          prefetch_vals();
-          if (lane == 0) { DBG_ADD(6); }
-        }
-        const double lp = warp_pairwise_small(pv, static_cast<int>(T), lane);
-        if (lane == 0) {
-          ChunkTerms ct = chunk_terms(lp, static_cast<double>(pblp), padv, p.w, p.clip_eps,
-                                      p.kl_coeff);
-          const double c = ct.coeff;
-          if (r % T == 0) {  // one writer per chunk for the epilogue
-            p.lp_chunk[q] = lp;
-            p.coeff[q] = c;
-          }
-          const double lse = S.ring_lse[k % kRing];
-          const int32_t tgt = S.ring_tgt[k % kRing];
-          uint32_t mode;
-          if (c == 0.0) {
-            mode = 0u;
-          } else if (!isfinite(c)) {
-            mode = 2u;
-          } else {
-            mode = 1u | ((c > 0.0) ? 0x80000000u : 0u);
-            S.kval[sb] = static_cast<float>(lse * 1.4426950408889634 - log2(fabs(c)));
-          }
-          S.mode[sb] = mode;
-          S.cf[sb] = static_cast<float>(c);
-          S.lseL[sb] = static_cast<float>(lse * 1.4426950408889634);
-          S.tgt[sb] = tgt;
-          mbar_arrive(&S.cfullB[sb]);
-          if (dbg) atomicAdd(dbg + 5, static_cast<unsigned long long>(clock64() - t_prep));
-        }
-        __syncwarp();
-        // start prefetching the next B row's chunk (same chunk: reuse)
-        if (k + 1 < nloc) {
-          const int64_t nq = row_of(k + 1) / T;
-          if (nq != pq) {
-            pq = nq;
-            pv_ok = false;
-            pc = ld_acquire_gpu(p.cnt + nq);
-          }
-        }
+        S.mode[sb] = mode;
+        S.cf[sb] = static_cast<float>(cc);
+        S.lseL[sb] = static_cast<float>(lse * 1.4426950408889634);
+        S.tgt[sb] = S.ring_tgt[k % kRing];
+        mbar_arrive(&S.cfullB[sb]);
       }
-    };
-    // B(k) is handled before the A(k+L) that precedes it in the op sequence
-    // (its coefficient depends only on the tails of rows k and k+1), so the
-    // compute warps find it ready when they finish A(k+L).  Only inside the
-    // paired region and with an effective lag >= 2 (tests/test_fused_protocol.py).
-    const int64_t Le = nloc < L ? nloc : L;
-    const int64_t pair_end = Le + 2 * (nloc - Le);
-    for (int64_t n = 0; n < nops;) {
-      bool isB0, isB1 = false;
-      int64_t k0, k1;
-      op_of(n, nloc, L, &isB0, &k0);
-      if (n + 1 < nops) op_of(n + 1, nloc, L, &isB1, &k1);
-      if (!isB0 && isB1 && Le >= 2 && n + 1 < pair_end) {
-        process(n + 1);
-        process(n);
-        n += 2;
-      } else {
-        process(n);
-        n += 1;
-      }
+      __syncwarp();
     }
     return;
   }
 
   // ------------------------------------------------------- compute warps
   const int nvec = static_cast<int>(V >> 3);  // uint4 = 8 bf16
-  int64_t a = 0, b = 0;  // A / B op counters
-  for (int64_t n = 0; n < nops; ++n) {
+  int a = 0, b = 0;  // A / B op counters
+  for (int n = 0; n < nops; ++n) {
     const int s = static_cast<int>(n % kFusedStages);
     const uint32_t ph = static_cast<uint32_t>((n / kFusedStages) & 1);
     bool isB;
-    int64_t k;
+    int k;
     op_of(n, nloc, L, &isB, &k);
     {
       DBG_T0();
@@ -561,14 +511,28 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       const uint32_t mx = bf16x2_max(mx0, mx1);
       const float m = warp_max_f32(fmaxf(bf16lo(mx), bf16hi(mx)));
       const float mL = m * kLog2e;
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      const uint64_t l2e2 = f2pack(kLog2e, kLog2e), nmL2 = f2pack(-mL, -mL);
+      uint64_t s01 = 0, s23 = 0, s45 = 0, s67 = 0;  // packed (0.f, 0.f)
+      auto ex2_pair = [&](uint32_t w) {
+        float y0, y1;
+        f2unpack(bf16x2_fma2(w, l2e2, nmL2), y0, y1);
+        return f2pack(ex2f(y0), ex2f(y1));
+      };
 #pragma unroll 2
       for (int i = tid; i < nvec; i += kFusedComputeThreads) {
         const uint4 x = v[i];
-        s0 += ex2f(fmaf(bf16lo(x.x), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.x), kLog2e, -mL));
-        s1 += ex2f(fmaf(bf16lo(x.y), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.y), kLog2e, -mL));
-        s2 += ex2f(fmaf(bf16lo(x.z), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.z), kLog2e, -mL));
-        s3 += ex2f(fmaf(bf16lo(x.w), kLog2e, -mL)) + ex2f(fmaf(bf16hi(x.w), kLog2e, -mL));
+        s01 = fadd2(s01, ex2_pair(x.x));
+        s23 = fadd2(s23, ex2_pair(x.y));
+        s45 = fadd2(s45, ex2_pair(x.z));
+        s67 = fadd2(s67, ex2_pair(x.w));
+      }
+      float s0, s1, s2, s3;
+      {
+        float a, b;
+        f2unpack(fadd2(s01, s23), a, b);
+        s0 = a; s1 = b;
+        f2unpack(fadd2(s45, s67), a, b);
+        s2 = a; s3 = b;
       }
       // gather the target logit while the row is in SMEM, then free the stage
       const bool tok_ok = tg >= 0 && tg < V;
@@ -581,8 +545,11 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
                     (static_cast<double>(s2) + static_cast<double>(s3));
       part = warp_sum_f64(part);
       const int sa = static_cast<int>(a % kASlots);
-      if (a >= kASlots)  // the coefficient warp has read A row a-8's partials
+      if (a >= kASlots) {  // the coefficient warp has read A row a-8's partials
+        DBG_T0();
         mbar_wait(&S.afree[sa], static_cast<uint32_t>(((a - kASlots) / kASlots) & 1));
+        if (tid == 0) { DBG_ADD(3); }
+      }
       ++a;
       if (tid == 0) {
         S.tgta[sa] = tok_ok ? tg : -1;
@@ -603,47 +570,30 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     }
     ++b;
     const uint32_t mode = S.mode[sb];
-    const uint4* v = reinterpret_cast<const uint4*>(buf(s));
-    uint4* dst = reinterpret_cast<uint4*>(dl + row_of(k) * V);
+    uint4* v = reinterpret_cast<uint4*>(buf(s));  // dlogits overwrite the row in place
     if ((mode & 3u) != 1u) {
       // zero-gradient rows (A == 0 or clipped chunk): 0 * (onehot - p)
       const uint32_t z = (mode == 0u) ? 0u : 0x7fc07fc0u;
-      for (int i = tid; i < nvec; i += kFusedComputeThreads) __stcs(dst + i, make_uint4(z, z, z, z));
+      for (int i = tid; i < nvec; i += kFusedComputeThreads) v[i] = make_uint4(z, z, z, z);
     } else {
+      // target column: c * (1 - p_t), patched by the thread that owns it
+      const int32_t tgt = S.tgt[sb];
+      const bool owner = tid == ((tgt >> 3) % kFusedComputeThreads);
+      __nv_bfloat16* row = reinterpret_cast<__nv_bfloat16*>(v);
+      float val = 0.f;
+      if (owner) {
+        const float pt = ex2f(fmaf(__bfloat162float(row[tgt]), kLog2e, -S.lseL[sb]));
+        val = S.cf[sb] * (1.0f - pt);
+      }
       // -c * p_v = -sign(c) * 2^(x*log2e - (lse*log2e - log2|c|))
       const float K = S.kval[sb];
-      const uint32_t sgn = (mode & 0x80000000u) ? 0x80008000u : 0u;
-      const int32_t tgt = S.tgt[sb];
-      const int tv = tgt >> 3;
-#pragma unroll 2
-      for (int i = tid; i < nvec; i += kFusedComputeThreads) {
-        const uint4 x = v[i];
-        uint4 o;
-        o.x = pack_bf16x2(ex2f(fmaf(bf16lo(x.x), kLog2e, -K)), ex2f(fmaf(bf16hi(x.x), kLog2e, -K))) ^ sgn;
-        o.y = pack_bf16x2(ex2f(fmaf(bf16lo(x.y), kLog2e, -K)), ex2f(fmaf(bf16hi(x.y), kLog2e, -K))) ^ sgn;
-        o.z = pack_bf16x2(ex2f(fmaf(bf16lo(x.z), kLog2e, -K)), ex2f(fmaf(bf16hi(x.z), kLog2e, -K))) ^ sgn;
-        o.w = pack_bf16x2(ex2f(fmaf(bf16lo(x.w), kLog2e, -K)), ex2f(fmaf(bf16hi(x.w), kLog2e, -K))) ^ sgn;
-        if (i == tv) {
-          // target column: c * (1 - p_t)
-          const int e = tgt & 7;
-          const uint32_t word = (e >> 1) == 0 ? x.x : (e >> 1) == 1 ? x.y : (e >> 1) == 2 ? x.z : x.w;
-          const float xt = (e & 1) ? bf16hi(word) : bf16lo(word);
-          const float pt = ex2f(fmaf(xt, kLog2e, -S.lseL[sb]));
-          const float val = S.cf[sb] * (1.0f - pt);
-          const uint32_t b = pack_bf16x2(val, val) & 0xffffu;
-          uint32_t ow = (e >> 1) == 0 ? o.x : (e >> 1) == 1 ? o.y : (e >> 1) == 2 ? o.z : o.w;
-          ow = (e & 1) ? ((ow & 0x0000ffffu) | (b << 16)) : ((ow & 0xffff0000u) | b);
-          if ((e >> 1) == 0) o.x = ow;
-          else if ((e >> 1) == 1) o.y = ow;
-          else if ((e >> 1) == 2) o.z = ow;
-          else o.w = ow;
-        }
-        __stcs(dst + i, o);
-      }
+      b_row(v, nvec, tid, K, (mode & 0x80000000u) ? 0x80008000u : 0u);
+      if (owner) row[tgt] = __float2bfloat16_rn(val);
     }
+    fence_proxy_async_smem();  // generic SMEM writes -> visible to the bulk store
     __syncwarp();
     if (lane == 0) {
-      mbar_arrive(&S.empty[s]);   // B row read: the stage may be reloaded
+      mbar_arrive(&S.bdone[sb]);  // the store warp frees the stage after its copy
       mbar_arrive(&S.adoneB[sb]);
     }
   }
@@ -1027,7 +977,8 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
                          ((V * esz) % 16 == 0);
   const size_t fsmem = fused_smem_bytes(V);
   const bool fused = !(flags & DVLA_TL_UNFUSED) && dtype == DVLA_BF16 && aligned16 &&
-                     fsmem <= 227 * 1024 && T <= sms && T <= 128 && R >= 1;
+                     fsmem <= 227 * 1024 && T <= sms && T <= 128 && R >= 1 &&
+                     R < (int64_t{1} << 31);
   if (fused) {
     static bool attr_set[64] = {false};
     if (!attr_set[dev & 63]) {
@@ -1048,8 +999,9 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
       const char* e = getenv("DVLA_FUSED_KEEP");
       return e ? atoi(e) : 0;
     }();
+
     tok_fused_bf16_kernel<<<grid, kFusedThreadsWS, fsmem, stream>>>(p, stage_bytes, want_dl ? 1 : 0,
-                                                                     lag < 2 ? 2 : lag, a_keep);
+                                                                     lag < 2 ? 2 : (lag > kMaxLag ? kMaxLag : lag), a_keep);
     prof_end(stream, stop);
     if (int rc = launch_check("tok_fused_bf16_kernel")) return rc;
     if (!want_dl) {
