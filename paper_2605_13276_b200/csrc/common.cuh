@@ -204,6 +204,17 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 }
 
 // acquire / release flag accesses
+// relaxed (strong, L1-bypassing) f64 load / store at GPU scope: a single
+// 8-byte access is single-copy atomic, so a poller sees old or new value
+__device__ __forceinline__ double ld_relaxed_gpu_f64(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu_f64(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -28,6 +28,8 @@
 //   grpo_epilogue_kernel  loss / stats / abort detection in canonical order
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "grpo_math.cuh"
 
@@ -49,7 +51,6 @@ struct TokParams {
   double* lse;
   double* lp_chunk;
   double* coeff;
-  uint32_t* cnt;
   uint32_t* err;
   int64_t R, V, T, C, n_chunks;
   double w, clip_eps, kl_coeff;
@@ -64,11 +65,20 @@ __device__ unsigned long long* g_dbg = nullptr;
 #define DBG_ADD(i) \
   if (dbg) atomicAdd(dbg + (i), static_cast<unsigned long long>(clock64() - _t0))
 
+// lp_tok not yet published (tok_adv_kernel fills it before the fused kernel;
+// a finite ~1.4e306, never a log-probability)
+constexpr long long kLpPending = 0x7f7f7f7f7f7f7f7fll;
+constexpr long long kNaN64 = 0x7ff8000000000000ll;
+
 // ------------------------------------------------------------ advantages
+// (also marks n_fill token log-probs pending for the fused kernel's polls)
 __global__ void tok_adv_kernel(const float* __restrict__ rewards, int64_t n_groups, int64_t G,
                                double delta, double* __restrict__ adv,
-                               uint32_t* __restrict__ reward_bad) {
-  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+                               uint32_t* __restrict__ reward_bad, double* __restrict__ lp_fill,
+                               int64_t n_fill) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int64_t i = g; i < n_fill; i += gridDim.x * (int64_t)blockDim.x)
+    reinterpret_cast<long long*>(lp_fill)[i] = kLpPending;
   if (g >= n_groups) return;
   const float* r = rewards + g * G;
   double* a = adv + g * G;
@@ -145,9 +155,8 @@ __device__ __forceinline__ double chunk_lp_pairwise(const double* __restrict__ l
 // Every CTA walks one op sequence: A(0..L-1), then A(k), B(k-L), ..., B(n-1):
 //   A(k)  row k streamed HBM -> SMEM by TMA; the compute warps take warp
 //         max (packed bf16) / sum-exp (FFMA2 + MUFU ex2 + FADD2) partials;
-//         the tail warp combines them into lse (f64), forms lp_tok from the
-//         gathered target logit and hands it to the publisher, which stores
-//         it and bumps the chunk counter (red.release.gpu).
+//         the tail warp combines them into lse (f64) and publishes lp_tok
+//         (target logit - lse) to global memory.
 //   B(k)  row k streamed again -- from L2, L rounds (~L*148*64 KB) after
 //         A(k) -- the prep warp waits for the chunk to be complete on all
 //         CTAs (long done by then), sums its T token log-probs (numpy
@@ -159,8 +168,11 @@ __device__ __forceinline__ double chunk_lp_pairwise(const double* __restrict__ l
 // and the tail warp never waits on another CTA, so the chunk wait is
 // deadlock-free while all CTAs are co-resident (grid <= #SMs, T <= grid).
 //
-// Warp roles: 0..W-1 compute, W loader, W+1 tail, W+2 store, W+3 publisher
-// (lp_tok + release of the chunk counters), W+4 prep.
+// Warp roles: 0..W-1 compute, W loader, W+1 tail, W+2 store, W+3 prep.
+// Cross-CTA: lp_tok values are published with single 8-byte relaxed stores
+// into a buffer pre-filled with a pending marker; the prep warp polls the
+// chunk's values themselves (one L2 round trip yields the data), so neither
+// side needs a counter or a release fence.
 // Barriers (every barrier completes once per use of its own ring index, and
 // every waiter walks its ring in order, so parity never aliases):
 //   full[s], empty[s]  per SMEM stage s = op % 3: loader <-> compute warps
@@ -172,16 +184,14 @@ __device__ __forceinline__ double chunk_lp_pairwise(const double* __restrict__ l
 //   cfullB[b % 3]      prep -> compute, per B op b (coefficient slot b % 3)
 //   adoneB[b % 3]      compute -> prep (coefficient slot b % 3 consumed)
 //   bdone[b % 3]       compute -> store, B row b written in SMEM
-//   pubfull/pubempty   tail <-> publisher, 8-entry lp_tok ring
 // The op sequence and barrier protocol are model-checked for deadlock,
 // races and parity aliasing (tests/test_fused_protocol.py).
 constexpr int kWarpLoader = kFusedComputeWarps;
 constexpr int kTailWarp = kFusedComputeWarps + 1;
 constexpr int kWarpStore = kFusedComputeWarps + 2;
-constexpr int kWarpPublish = kFusedComputeWarps + 3;
-constexpr int kPrepWarp = kFusedComputeWarps + 4;
-constexpr int kFusedThreadsWS = (kFusedComputeWarps + 5) * 32;
-constexpr int kPubRing = 8;
+constexpr int kPrepWarp = kFusedComputeWarps + 3;
+constexpr int kFusedThreadsWS = (kFusedComputeWarps + 4) * 32;
+
 constexpr int kLagRounds = 4;  // measured best on B200 (lag 2..6 sweep, tools/fused_variants.py)
 constexpr int kRing = 8;       // (lse, target) rows in flight tail -> prep; needs lag < kRing
 constexpr int kMaxLag = kRing - 1;
@@ -206,9 +216,6 @@ struct FusedSmem {
   int32_t tgta[kASlots];   // its token id (-1: out of range)
   double ring_lse[kRing];
   int32_t ring_tgt[kRing];
-  uint64_t pubfull[kPubRing];
-  uint64_t pubempty[kPubRing];
-  double pub_lp[kPubRing];
 };
 
 // op n of a CTA with nloc rows and lag L: (is_B, local row)
@@ -280,10 +287,6 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       mbar_init(&S.afree[s], 1);
     }
     for (int j = 0; j < kRing; ++j) mbar_init(&S.tdone[j], 1);
-    for (int j = 0; j < kPubRing; ++j) {
-      mbar_init(&S.pubfull[j], 1);
-      mbar_init(&S.pubempty[j], 1);
-    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -343,35 +346,6 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     return;
   }
 
-  // ------------------------------------------------------ publisher warp
-  // Publishes each row's lp_tok and bumps its chunk counter with a release
-  // reduction; the release fence's wait for the store stalls only this warp.
-  if (warp == kWarpPublish) {
-    if (!write_dl || lane != 0) return;
-    int na = 0;  // A ops seen
-    for (int n = 0; n < nops; ++n) {
-      bool isB;
-      int k;
-      op_of(n, nloc, L, &isB, &k);
-      if (isB) continue;
-      const int j = static_cast<int>(na % kPubRing);
-      {
-        DBG_T0();
-        mbar_wait(&S.pubfull[j], static_cast<uint32_t>((na / kPubRing) & 1));
-        DBG_ADD(13);
-      }
-      const long long t_pub = dbg ? clock64() : 0;
-      ++na;
-      const double lp = S.pub_lp[j];
-      mbar_arrive(&S.pubempty[j]);
-      const int64_t r = row_of(k);
-      p.lp_tok[r] = lp;
-      red_release_gpu_add(p.cnt + r / T, 1u);
-      if (dbg) atomicAdd(dbg + 14, static_cast<unsigned long long>(clock64() - t_pub));
-    }
-    return;
-  }
-
   // ----------------------------------------------------------- tail warp
   // Turns every A row's per-warp partials into lse (f64) and lp_tok, hands
   // lp_tok to the publisher (other CTAs' chunks wait for it, so this warp
@@ -395,20 +369,18 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       term = warp_sum_f64(term);
       if (lane == 0) {
         const double lse = static_cast<double>(M) + log(term);
-        const double xt = static_cast<double>(xt_f);
+        double lp = static_cast<double>(xt_f) - lse;
+        if (__double_as_longlong(lp) == kLpPending) lp = __longlong_as_double(kNaN64);
         if (tgt < 0) atomicOr(p.err, kErrToken);
+        // published with one 8-byte store: other CTAs' prep warps poll the
+        // value itself (no counter, no release fence on this path)
+        st_relaxed_gpu_f64(p.lp_tok + r, lp);
         if (write_dl) {
-          const int j = static_cast<int>(k % kPubRing);
           S.ring_lse[k % kRing] = lse;
           S.ring_tgt[k % kRing] = tgt;
           mbar_arrive(&S.tdone[k % kRing]);
-          if (k >= kPubRing)
-            mbar_wait(&S.pubempty[j], static_cast<uint32_t>(((k / kPubRing) - 1) & 1));
-          S.pub_lp[j] = xt - lse;
-          mbar_arrive(&S.pubfull[j]);
         } else {
           p.lse[r] = lse;
-          p.lp_tok[r] = xt - lse;
         }
       }
       __syncwarp();
@@ -429,25 +401,25 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       const int sb = static_cast<int>(k % kFusedStages);
       const int64_t r = row_of(k);
       const int64_t q = r / T;
-      uint32_t c = (lane == 0) ? ld_acquire_gpu(p.cnt + q) : 0u;
-      c = __shfl_sync(0xffffffffu, c, 0);
+      // poll the chunk's T published token log-probs (2 per lane at most
+      // 4 deep) until none is pending any more
+      double pv[4];
+      const double* lt = p.lp_tok + q * T;
       uint32_t spins = 0;
-      while (c < static_cast<uint32_t>(T)) {
-        __nanosleep(64);
-        c = (lane == 0) ? ld_acquire_gpu(p.cnt + q) : 0u;
-        c = __shfl_sync(0xffffffffu, c, 0);
+      for (;;) {
+        bool ready = true;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int64_t t = 32 * m + lane;
+          pv[m] = (t < T) ? ld_relaxed_gpu_f64(lt + t) : 0.0;
+          ready &= __double_as_longlong(pv[m]) != kLpPending;
+        }
+        if (__all_sync(0xffffffffu, ready)) break;
+        __nanosleep(32);
         if ((++spins & 1023u) == 0 && globaltimer_ns() - t_start > kSpinTimeoutNs) {
           if (lane == 0) atomicOr(p.err, kErrTimeout);
           break;
         }
-      }
-      __syncwarp();  // lane 0's acquire orders the loads below for the warp
-      double pv[4];
-      const double* lt = p.lp_tok + q * T;
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int64_t t = 32 * m + lane;
-        pv[m] = (t < T) ? __ldcg(lt + t) : 0.0;
       }
       const float pblp = __ldg(p.blp + q);
       const double padv = __ldg(p.adv + q / p.C);
@@ -867,11 +839,10 @@ struct TokWorkspace {
   double* lp_tok;
   double* lse;
   double* coeff;
-  uint32_t* cnt;
   uint32_t* reward_bad;
   uint32_t* err;
   size_t bytes;
-  size_t zero_off, zero_bytes;  // region memset every call (cnt, err)
+  size_t zero_off, zero_bytes;  // region memset every call (err)
 };
 
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -891,7 +862,6 @@ static TokWorkspace carve(void* base, int64_t n_groups, int64_t G, int64_t C, in
   w.coeff = reinterpret_cast<double*>(take(nq * 8));
   w.reward_bad = reinterpret_cast<uint32_t*>(take(n_groups * 4));
   w.zero_off = off;
-  w.cnt = reinterpret_cast<uint32_t*>(take(nq * 4));
   w.err = reinterpret_cast<uint32_t*>(take(16));
   w.zero_bytes = off - w.zero_off;
   w.bytes = off;
@@ -949,7 +919,6 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
   p.lse = ws.lse;
   p.lp_chunk = lp_chunk;
   p.coeff = ws.coeff;
-  p.cnt = ws.cnt;
   p.err = ws.err;
   p.R = R;
   p.V = V;
@@ -964,8 +933,10 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
                                 ws.zero_bytes, stream));
   {
     const int thr = 128;
-    tok_adv_kernel<<<(unsigned)((n_groups + thr - 1) / thr), thr, 0, stream>>>(
-        rewards, n_groups, G, adv_eps, ws.adv, ws.reward_bad);
+    const int64_t fill_blocks = std::min<int64_t>((R + thr - 1) / thr, 4 * 148);
+    const int64_t blocks = std::max<int64_t>((n_groups + thr - 1) / thr, fill_blocks);
+    tok_adv_kernel<<<(unsigned)blocks, thr, 0, stream>>>(rewards, n_groups, G, adv_eps, ws.adv,
+                                                          ws.reward_bad, ws.lp_tok, R);
     if (int rc = launch_check("tok_adv_kernel")) return rc;
   }
 
@@ -1078,7 +1049,7 @@ extern "C" int dvla_group_advantages(const float* rewards, int64_t n_groups, int
   const int thr = 128;
   tok_adv_kernel<<<(unsigned)((n_groups + thr - 1) / thr), thr, 0,
                    static_cast<cudaStream_t>(stream)>>>(rewards, n_groups, G, delta, adv,
-                                                        reward_bad);
+                                                        reward_bad, nullptr, 0);
   return launch_check("tok_adv_kernel");
 }
 
