@@ -128,6 +128,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity,
   }
 }
 
+// Polling wait with NANOSLEEP backoff: issues a handful of instructions per
+// ~100 ns instead of waking on every SYNCS event in the CTA (cheaper in issue
+// slots and power for long waits among many busy warps).
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  if (mbar_test_wait(bar, parity)) return;
+  uint32_t ns = 32, n = 0;
+  while (!mbar_test_wait(bar, parity)) {
+    __nanosleep(ns);
+    if (ns < 128) ns <<= 1;
+    if (++n > (1u << 26)) __trap();
+  }
+}
+
 // TMA bulk copy global -> shared (non-tensor, 1-D), completion on an mbarrier.
 __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src, uint32_t bytes,
                                             uint64_t* bar) {

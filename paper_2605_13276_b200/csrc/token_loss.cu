@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     const int sb = static_cast<int>(b % kFusedStages);
     {
       DBG_T0();
-      mbar_wait(&S.cfullB[sb], static_cast<uint32_t>((b / kFusedStages) & 1));
+      mbar_wait_backoff(&S.cfullB[sb], static_cast<uint32_t>((b / kFusedStages) & 1));
       if (tid == 0) { DBG_ADD(1); }
     }
     ++b;
