@@ -266,7 +266,41 @@ def _bench_replication(world, rank, dev, barrier, max_over_ranks, iters=5):
                              "frac_of_nominal_900": gbs / NVLINK_NOMINAL_GBS,
                              "peak_source": "B200_PROFILING.md measured peer copy (770 GB/s/dir)"},
                 "ce_fanout_gbs_per_receiver": S / (sorted(ce)[1] / 1e3) / 1e9})
+    out["multicast"] = _bench_multicast(S, src, rank, world, barrier, max_over_ranks)
     return out
+
+
+def _bench_multicast(S, src, rank, world, barrier, max_over_ranks, iters=4):
+    """Switch-multicast (NVLS) broadcast of the same region, beside the
+    chain: one source write per byte, replicated by the NVSwitch."""
+    import torch
+    from paper_2605_13276_b200.replicate import McReplicator, bytes_equal, multicast_supported
+    ok_local = multicast_supported()
+    if max_over_ranks(0.0 if ok_local else 1.0) != 0.0:
+        return {"unavailable": "no NVSwitch multicast / POSIX-fd handles on this box"}
+    rep = McReplicator(S, n_buffers=1)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    for it in range(iters + 1):
+        barrier()
+        e0.record(stream)
+        rep.broadcast(src, it)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = max_over_ranks(e0.elapsed_time(e1))
+        if it:
+            times.append(t)
+    rep.check()
+    ok = bytes_equal(src, rep.replica(iters))[0] == 0
+    ok_all = max_over_ranks(0.0 if ok else 1.0) == 0.0
+    barrier()
+    rep.close()
+    ms = sorted(times)[len(times) // 2]
+    gbs = S / (ms / 1e3) / 1e9
+    return {"mode": f"NVLS multicast 0->{{{','.join(str(r) for r in range(1, world))}}}",
+            "gbs": gbs, "ms": ms, "bit_exact": ok_all,
+            "frac_of_peer_copy": gbs / NVLINK_PEER_GBS}
 
 
 def _bench_allreduce(world, dev, barrier, max_over_ranks, nbytes=1 << 30, iters=5):

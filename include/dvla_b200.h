@@ -266,6 +266,33 @@ int dvla_bytes_equal(const void* a, const void* b, int64_t nbytes, uint64_t* out
  * the TMA chain is measured against. */
 int dvla_memcpy_async(void* dst, const void* src, int64_t nbytes, void* stream);
 
+/* ---- switch-multicast (NVLS) replication ---------------------------------
+ * Replaces the same ControlPlane.broadcast -> WeightMailbox.deliver data path
+ * (planes.py:294-321, 244-275) as dvla_replicate_chain: the source writes each
+ * byte once into a multicast address and the NVSwitch replicates it into the
+ * bound region of every member GPU.  One process per GPU; the multicast
+ * object is created on the source and shared as a POSIX fd (pidfd_getfd).
+ * Sequence: root dvla_mc_create; others dvla_mc_import; all
+ * dvla_mc_add_device; (barrier) all dvla_mc_bind; (barrier) writers
+ * dvla_mc_map.  Objects are opaque (void*). */
+int dvla_mc_supported(int device, int* out);
+int dvla_mc_create(int n_devices, size_t nbytes, int* fd_out, size_t* size_out, void** obj_out);
+int dvla_mc_import(int owner_pid, int owner_fd, int n_devices, size_t size, void** obj_out);
+int dvla_mc_add_device(void* obj, int device);
+int dvla_mc_bind(void* obj, int device, void** local_out);
+int dvla_mc_map(void* obj, int device, void** mc_out);
+int dvla_mc_destroy(void* obj);
+/* Root: copy nbytes (multiple of 16) from src into the multicast region,
+ * then release-store `epoch` into every member's flag word (mc_flag is the
+ * flag's multicast address).  done_ctr: device u32, zero-initialised, owned
+ * by the caller (reset by the kernel). */
+int dvla_mc_broadcast(const void* src, void* mc_dst, int64_t nbytes, void* mc_flag,
+                      uint32_t epoch, int ctas, uint32_t* done_ctr, void* stream);
+/* Receivers: stream-ordered wait until the local flag reaches `epoch`;
+ * *err_dev |= 1 on timeout (the reference's WeightMailbox wait). */
+int dvla_mc_wait(const uint32_t* local_flag, uint32_t epoch, uint64_t timeout_ns,
+                 uint32_t* err_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -154,6 +154,17 @@ dvla_replicate_chain = _proto("dvla_replicate_chain", [
 dvla_snapshot_copy = _proto("dvla_snapshot_copy", [_vp, _vp, _i64, _i32, _vp, _vp])
 dvla_bytes_equal = _proto("dvla_bytes_equal", [_vp, _vp, _i64, _vp, _vp])
 dvla_memcpy_async = _proto("dvla_memcpy_async", [_vp, _vp, _i64, _vp])
+dvla_mc_supported = _proto("dvla_mc_supported", [_i32, C.POINTER(_i32)])
+dvla_mc_create = _proto("dvla_mc_create", [_i32, _sz, C.POINTER(_i32), C.POINTER(_sz),
+                                           C.POINTER(_pp)])
+dvla_mc_import = _proto("dvla_mc_import", [_i32, _i32, _i32, _sz, C.POINTER(_pp)])
+dvla_mc_add_device = _proto("dvla_mc_add_device", [_vp, _i32])
+dvla_mc_bind = _proto("dvla_mc_bind", [_vp, _i32, C.POINTER(_pp)])
+dvla_mc_map = _proto("dvla_mc_map", [_vp, _i32, C.POINTER(_pp)])
+dvla_mc_destroy = _proto("dvla_mc_destroy", [_vp])
+dvla_mc_broadcast = _proto("dvla_mc_broadcast", [_vp, _vp, _i64, _vp, C.c_uint32, _i32, _vp,
+                                                 _vp])
+dvla_mc_wait = _proto("dvla_mc_wait", [_vp, C.c_uint32, C.c_uint64, _vp, _vp])
 
 # ---------------------------------------------- Gaussian head / MLP policy
 dvla_mlp_forward = _proto("dvla_mlp_forward", [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32,

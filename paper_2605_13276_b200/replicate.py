@@ -279,3 +279,127 @@ class ChainReplicator:
                 _lib.dvla_ipc_close(p)
         self.next_buf = self.next_flags = None
         self.fan_bufs = []
+
+
+class _CudaView:
+    """__cuda_array_interface__ over memory this module does not own."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {
+            "shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+            "strides": None,
+        }
+
+
+def multicast_supported(device=None) -> bool:
+    """NVSwitch multicast (NVLS) + POSIX-fd handle export on `device`."""
+    from . import _lib
+    torch = _torch()
+    out = C.c_int()
+    dev = torch.cuda.current_device() if device is None else int(device)
+    _lib.check(_lib.dvla_mc_supported(dev, C.byref(out)), "dvla_mc_supported")
+    return bool(out.value)
+
+
+class McReplicator:
+    """Cross-process switch-multicast (NVLS) broadcast (one process per GPU).
+
+    ranks[0] writes each byte once into a multicast mapping and the NVSwitch
+    replicates it into the bound region of every member; the root then
+    release-stores the epoch into every member's flag through the same
+    mapping and receivers acquire-poll their local copy (reference
+    ControlPlane.broadcast -> WeightMailbox.deliver, planes.py:294-321,
+    244-275).  Collective construction: every rank of `ranks` calls it.
+    The root is a member too (its own bound copy is the cost of the team).
+    """
+
+    def __init__(self, nbytes: int, ranks=None, n_buffers: int = 2, ctas: int = 0, group=None):
+        import os
+        import torch.distributed as dist
+        from . import _lib
+        torch = _torch()
+        if nbytes % 16:
+            raise UsageError("replicated regions must be a multiple of 16 bytes")
+        self.rank = dist.get_rank()
+        world = dist.get_world_size()
+        self.ranks = list(range(world)) if ranks is None else list(ranks)
+        self.pos = self.ranks.index(self.rank) if self.rank in self.ranks else -1
+        self.nbytes, self.nb, self.ctas = int(nbytes), int(n_buffers), int(ctas)
+        self.dev = torch.cuda.current_device()
+        n = len(self.ranks)
+        self.flag_off = (self.nb * self.nbytes + 255) // 256 * 256
+        total = self.flag_off + self.nb * 256
+        self.obj = self.local = self.mc = None
+        self.err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.done = torch.zeros(1, dtype=torch.int32, device="cuda")
+        info = None
+        if self.pos == 0:
+            fd, size, obj = C.c_int(), C.c_size_t(), C.c_void_p()
+            _lib.check(_lib.dvla_mc_create(n, total, C.byref(fd), C.byref(size), C.byref(obj)),
+                       "dvla_mc_create")
+            self.obj = obj.value
+            info = (os.getpid(), fd.value, size.value)
+        allinfo = [None] * world
+        dist.all_gather_object(allinfo, info, group=group)
+        pid, fd, size = allinfo[self.ranks[0]]
+        self.size = size
+        if self.pos > 0:
+            obj = C.c_void_p()
+            _lib.check(_lib.dvla_mc_import(pid, fd, n, size, C.byref(obj)), "dvla_mc_import")
+            self.obj = obj.value
+        if self.pos >= 0:
+            _lib.check(_lib.dvla_mc_add_device(self.obj, self.dev), "dvla_mc_add_device")
+        dist.barrier(group=group)
+        if self.pos >= 0:
+            local = C.c_void_p()
+            _lib.check(_lib.dvla_mc_bind(self.obj, self.dev, C.byref(local)), "dvla_mc_bind")
+            self.local = local.value
+            self.t = torch.as_tensor(_CudaView(self.local, self.size),
+                                     device=torch.device("cuda", self.dev))
+            self.t[self.flag_off:].zero_()
+            torch.cuda.synchronize()
+        dist.barrier(group=group)
+        if self.pos == 0:
+            mc = C.c_void_p()
+            _lib.check(_lib.dvla_mc_map(self.obj, self.dev, C.byref(mc)), "dvla_mc_map")
+            self.mc = mc.value
+        dist.barrier(group=group)
+
+    def replica(self, version: int):
+        """This member's bound copy of `version` (after broadcast + wait)."""
+        b = version % self.nb
+        return self.t[b * self.nbytes:(b + 1) * self.nbytes]
+
+    def broadcast(self, src, version: int, stream=None, timeout_s: float = 30.0):
+        """Root: multicast `src`; receivers: stream-ordered wait for it."""
+        from . import _lib
+        if self.pos < 0:
+            return
+        b = version % self.nb
+        epoch = version + 1
+        flag = self.flag_off + b * 256
+        if self.pos == 0:
+            if src.numel() * src.element_size() != self.nbytes:
+                raise UsageError("source size differs from the replicated region")
+            _lib.check(_lib.dvla_mc_broadcast(src.data_ptr(), self.mc + b * self.nbytes,
+                                              self.nbytes, self.mc + flag, epoch, self.ctas,
+                                              self.done.data_ptr(), _stream_ptr(stream)),
+                       "dvla_mc_broadcast")
+        else:
+            _lib.check(_lib.dvla_mc_wait(self.local + flag, epoch, int(timeout_s * 1e9),
+                                         self.err.data_ptr(), _stream_ptr(stream)),
+                       "dvla_mc_wait")
+
+    def check(self):
+        if int(self.err.item()):
+            from ._lib import ReplicationTimeout
+            raise ReplicationTimeout(f"rank {self.rank}: multicast flag wait timed out")
+
+    def close(self):
+        from . import _lib
+        torch = _torch()
+        torch.cuda.synchronize()
+        self.t = None
+        if self.obj:
+            _lib.dvla_mc_destroy(self.obj)
+        self.obj = self.local = self.mc = None

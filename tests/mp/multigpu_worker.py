@@ -1,7 +1,8 @@
 """Per-rank body of tests/test_multigpu.py (run under torch.distributed.run).
 
 Checks, on N >= 2 GPUs over NCCL/NVLink: (1) the cross-process TMA chain
-broadcast is bit-exact on every receiver for two versions (double buffer);
+broadcast is bit-exact on every receiver for two versions (double buffer),
+and so is the switch-multicast (NVLS) broadcast where the box supports it;
 (2) GradReducer's NCCL mean equals the reference semantics; (3) the
 group-sharded token loss gives every rank its own shard's result; (4) the
 swimlane runs one closed loop per GPU with NCCL gradient reduction."""
@@ -21,7 +22,8 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, world = dist.get_rank(), dist.get_world_size()
-    from paper_2605_13276_b200.replicate import ChainReplicator, bytes_equal
+    from paper_2605_13276_b200.replicate import (ChainReplicator, McReplicator, bytes_equal,
+                                                 multicast_supported)
     from paper_2605_13276_b200.runtime import GradReducer, SwimlaneConfig, run_swimlane
 
     # (1) chain replication, 2 versions, odd size
@@ -37,6 +39,23 @@ def main():
         if rank > 0:
             assert bytes_equal(src, rep.replica(v)) == (0, -1), (rank, v)
     rep.close()
+
+    # (1b) switch-multicast (NVLS) replication, 3 versions through 2 buffers
+    if multicast_supported():
+        mrep = McReplicator(S, n_buffers=2)
+        for v in (0, 1, 2):
+            src = torch.randint(0, 256, (S,), dtype=torch.uint8, device="cuda",
+                                generator=torch.Generator(device="cuda").manual_seed(200 + v))
+            dist.barrier()
+            mrep.broadcast(src, v)
+            torch.cuda.synchronize()
+            dist.barrier()
+            mrep.check()
+            assert bytes_equal(src, mrep.replica(v)) == (0, -1), ("mc", rank, v)
+        dist.barrier()
+        mrep.close()
+        if rank == 0:
+            print("MULTICAST_OK", flush=True)
 
     # (2) gradient mean over NCCL, exact mode vs host arithmetic
     g = torch.full((1000,), float(rank + 1), dtype=torch.float64, device="cuda") / 3.0
