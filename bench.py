@@ -172,7 +172,7 @@ def run_reference(a):
                                    "(oracle numpy f64, all host threads)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    _emit(line)
     return 0
 
 
@@ -259,7 +259,8 @@ def _bench_replication(world, rank, dev, barrier, max_over_ranks, iters=5):
     barrier()
     rep.close()
     gbs = S / (ms / 1e3) / 1e9
-    out.update({"mode": f"TMA chain 0->{'->'.join(str(r) for r in range(1, world))}",
+    engine = "copy-engine hop" if rep.engine == "ce" else "TMA chain"
+    out.update({"mode": f"{engine} 0->{'->'.join(str(r) for r in range(1, world))}",
                 "gbs": gbs, "ms": ms, "bit_exact": ok_all,
                 "roofline": {"bound": "nvlink", "achieved": gbs, "peak": NVLINK_PEER_GBS,
                              "unit": "GB/s", "frac": gbs / NVLINK_PEER_GBS,
@@ -508,13 +509,36 @@ def run_ours(a):
             "loss": st["loss"], "mean_ratio": st["mean_ratio"],
             "clip_fraction": st["clip_fraction"],
         }
-        print(json.dumps(line), flush=True)
+        _emit(line)
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
+_JSON_FD = None
+
+
+def _quiet_stdout():
+    """Keep stdout for the one JSON line: anything else written to fd 1 (the
+    NCCL version banner, library chatter) goes to stderr."""
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def _emit(line):
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
+
+
 def main():
+    _quiet_stdout()
     a = _args()
     if a.impl == "reference":
         return run_reference(a)

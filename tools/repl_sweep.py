@@ -12,9 +12,12 @@ S = int(float(os.environ.get("S", "6.6e9"))) // 16 * 16
 src = torch.randint(0, 256, (S,), dtype=torch.uint8, device="cuda",
                     generator=torch.Generator(device="cuda").manual_seed(1))
 res = []
-for ctas in [16, 32, 64, 128]:
-    for chunk in [2 << 20, 8 << 20, 32 << 20]:
-        rep = ChainReplicator(S, chunk_bytes=chunk, ctas_per_hop=ctas)
+CTAS = [int(x) for x in os.environ.get("CTAS", "16,32,64,128").split(",")]
+CHUNKS = [int(x) << 20 for x in os.environ.get("CHUNKS_MB", "2,8,32").split(",")]
+for ctas in CTAS:
+    for chunk in CHUNKS:
+        rep = ChainReplicator(S, chunk_bytes=chunk, ctas_per_hop=ctas,
+                              engine=os.environ.get("ENGINE", "sm"))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ts = []
         for it in range(4):
