@@ -227,7 +227,7 @@ def _bench_replication(world, rank, dev, barrier, max_over_ranks, iters=5):
                     "kernel_ms": kms / max(kn, 1)})
         del ch
         return out
-    rep = ChainReplicator(S, n_buffers=2, chunk_bytes=2 << 20, ctas_per_hop=128)
+    rep = ChainReplicator(S, n_buffers=2, ctas_per_hop=128)
     expect = src  # every rank generated the same bytes (same seed)
     rep.broadcast(src, 0)
     torch.cuda.synchronize()

@@ -175,6 +175,16 @@ class LocalChain:
             raise ReplicationTimeout("replication chain flag wait timed out")
 
 
+def chain_chunk_bytes(nbytes: int, ctas_per_hop: int = 128) -> int:
+    """Chunk size for the TMA chain: the pipeline fill costs (hops - 1) chunk
+    transfers at the per-CTA rate, so chunks shrink with the region (about 16
+    chunks per CTA), within [128 KB, 1 MB] (tools/repl_sweep.py, 4 B200:
+    6.6 GB -> 1 MB 680 GB/s vs 2 MB 659; 1 GB -> 256 KB 607 vs 2 MB 482)."""
+    target = max(1, nbytes // (ctas_per_hop * 16))
+    c = 1 << (target.bit_length() - 1)
+    return int(min(max(c, 128 << 10), 1 << 20))
+
+
 class ChainReplicator:
     """Cross-process chain broadcast over NVLink (one process per GPU).
 
@@ -183,7 +193,7 @@ class ChainReplicator:
     `nbytes` each in device slabs (or in a MODEL_COMPUTE pool's slab).
     """
 
-    def __init__(self, nbytes: int, ranks=None, n_buffers: int = 2, chunk_bytes: int = 2 << 20,
+    def __init__(self, nbytes: int, ranks=None, n_buffers: int = 2, chunk_bytes=None,
                  ctas_per_hop: int = 128, group=None, engine: str = "auto"):
         import torch.distributed as dist
         torch = _torch()
@@ -202,7 +212,8 @@ class ChainReplicator:
             engine = "ce" if len(self.ranks) == 2 else "sm"
         self.engine = engine
         self.nbytes, self.nb = int(nbytes), int(n_buffers)
-        self.chunk, self.ctas = int(chunk_bytes), int(ctas_per_hop)
+        self.ctas = int(ctas_per_hop)
+        self.chunk = int(chunk_bytes) if chunk_bytes else chain_chunk_bytes(self.nbytes, self.ctas)
         if engine == "ce" and len(self.ranks) == 2:
             self.chunk = max(16, self.nbytes)  # one copy, one flag
         self.n_chunks = (self.nbytes + self.chunk - 1) // self.chunk

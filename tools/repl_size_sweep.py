@@ -68,7 +68,7 @@ def main():
         if rank == 0:
             src = torch.randint(0, 256, (S,), dtype=torch.uint8, device="cuda",
                                 generator=torch.Generator(device="cuda").manual_seed(int(sg * 1000)))
-        rep = ChainReplicator(S, n_buffers=1, chunk_bytes=2 << 20, ctas_per_hop=128)
+        rep = ChainReplicator(S, n_buffers=1, ctas_per_hop=128)
         ms = timed(lambda it: rep.broadcast(src, it))
         rep.check()
         ok = same_as_root(src if rank == 0 else rep.replica(0))

@@ -13,7 +13,8 @@ src = torch.randint(0, 256, (S,), dtype=torch.uint8, device="cuda",
                     generator=torch.Generator(device="cuda").manual_seed(1))
 res = []
 CTAS = [int(x) for x in os.environ.get("CTAS", "16,32,64,128").split(",")]
-CHUNKS = [int(x) << 20 for x in os.environ.get("CHUNKS_MB", "2,8,32").split(",")]
+CHUNKS = ([int(x) << 10 for x in os.environ["CHUNKS_KB"].split(",")] if "CHUNKS_KB" in os.environ
+          else [int(x) << 20 for x in os.environ.get("CHUNKS_MB", "2,8,32").split(",")])
 for ctas in CTAS:
     for chunk in CHUNKS:
         rep = ChainReplicator(S, chunk_bytes=chunk, ctas_per_hop=ctas,
@@ -29,7 +30,7 @@ for ctas in CTAS:
         ok = rank == 0 or bytes_equal(src, rep.replica(3))[0] == 0
         rep.close(); del rep
         ms = sorted(ts[1:])[1]
-        res.append((ctas, chunk >> 20, round(S / ms / 1e6, 1), ok))
+        res.append((ctas, chunk >> 10, round(S / ms / 1e6, 1), ok))
 if rank == 0:
-    for r in res: print("ctas %4d chunk %3d MB  %7.1f GB/s  exact=%s" % r)
+    for r in res: print("ctas %4d chunk %6d KB  %7.1f GB/s  exact=%s" % r)
 dist.destroy_process_group()
