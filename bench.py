@@ -49,6 +49,7 @@ def _args():
     ap.add_argument("--unfused", action="store_true")
     ap.add_argument("--no-repl", action="store_true")
     ap.add_argument("--no-swimlane", action="store_true")
+    ap.add_argument("--no-gauss", action="store_true")
     ap.add_argument("--fixed-warmup", action="store_true",
                     help="exactly --warmup warm-up steps (for ncu launch lists)")
     return ap.parse_args()
@@ -304,6 +305,107 @@ def _bench_multicast(S, src, rank, world, barrier, max_over_ranks, iters=4):
             "frac_of_peer_copy": gbs / NVLINK_PEER_GBS}
 
 
+def _bench_gauss_c3(dev, rank, steps=200, cpu=True):
+    """C3 (pi0-shaped) Gaussian-head learner step on this GPU: chunk_log_prob
+    -> group advantages -> canonical-order epilogue -> head backward, B = 512
+    chunks x D = 1,600 (SURVEY §8 d: ~10 MB, latency-bound: report time).
+    Timed eagerly and as a captured CUDA graph; the f64 oracle port of the
+    same step (single host thread, like the reference's numba backend)
+    beside it on rank 0."""
+    import numpy as np
+    import torch
+    from paper_2605_13276_b200 import _lib
+    n_groups, G, C, D = 64, 8, 1, 1600
+    B = n_groups * G * C
+    g = torch.Generator(device=dev).manual_seed(0)
+    means = torch.randn(B, D, device=dev, generator=g)
+    actions = torch.randn(B, D, device=dev, generator=g)
+    log_std = torch.randn(D, device=dev, generator=g) * 0.1
+    lp0 = torch.empty(B, dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream()
+    _lib.check(_lib.dvla_chunk_log_prob(means.data_ptr(), log_std.data_ptr(), actions.data_ptr(),
+                                        B, D, lp0.data_ptr(), st.cuda_stream), "clp")
+    blp = (lp0 + (torch.rand(B, dtype=torch.float64, device=dev, generator=g) - 0.5) * 0.1).float()
+    rewards = torch.randint(0, 2, (n_groups * G,), device=dev, generator=g).float()
+    ids = np.arange(n_groups, dtype=np.int64)
+    order_d = torch.from_numpy(ids).to(dev)
+    ids_d = order_d.clone()
+    adv = torch.empty(n_groups * G, dtype=torch.float64, device=dev)
+    bad = torch.empty(n_groups, dtype=torch.int32, device=dev)
+    lp = torch.empty(B, dtype=torch.float64, device=dev)
+    coeff = torch.empty(B, dtype=torch.float64, device=dev)
+    stats = torch.zeros(_lib.ST_LEN, dtype=torch.float64, device=dev)
+    dm = torch.empty(B, D, dtype=torch.float32, device=dev)
+    dls = torch.zeros(D, dtype=torch.float64, device=dev)
+
+    def step(s):
+        _lib.dvla_group_advantages(rewards.data_ptr(), n_groups, G, 1e-8, adv.data_ptr(),
+                                   bad.data_ptr(), s)
+        _lib.dvla_chunk_log_prob(means.data_ptr(), log_std.data_ptr(), actions.data_ptr(), B, D,
+                                 lp.data_ptr(), s)
+        _lib.dvla_grpo_epilogue(lp.data_ptr(), blp.data_ptr(), None, adv.data_ptr(),
+                                bad.data_ptr(), order_d.data_ptr(), ids_d.data_ptr(), n_groups, G,
+                                C, 0.2, 0.0, coeff.data_ptr(), stats.data_ptr(), s)
+        _lib.dvla_gauss_head_backward(means.data_ptr(), log_std.data_ptr(), actions.data_ptr(),
+                                      coeff.data_ptr(), B, D, dm.data_ptr(), dls.data_ptr(), s)
+
+    for _ in range(5):
+        step(st.cuda_stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        step(st.cuda_stream)
+    e1.record(st)
+    torch.cuda.synchronize()
+    eager_us = e0.elapsed_time(e1) / steps * 1e3
+    # CUDA graph: the four launches captured once, replayed per step
+    gs = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(gs):
+        step(gs.cuda_stream)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=gs):
+            step(gs.cuda_stream)
+    torch.cuda.synchronize()
+    for _ in range(5):
+        graph.replay()
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(steps):
+        graph.replay()
+    e1.record(st)
+    torch.cuda.synchronize()
+    graph_us = e0.elapsed_time(e1) / steps * 1e3
+    out = {"workload": "C3 Gaussian head (pi0-shaped): 64 groups x 8 x 1 chunk, D = 1600, f32 "
+                       "means/actions, f64 accumulation",
+           "us_per_step_eager": eager_us, "us_per_step_graph": graph_us,
+           "loss": float(stats[_lib.ST_LOSS].item()), "launches_per_step": 4}
+    if cpu and rank == 0:
+        sys.path.insert(0, ROOT)
+        from oracle import grpo_oracle as O
+        m, a, ls = means.cpu().numpy(), actions.cpu().numpy(), log_std.cpu().numpy()
+        b3 = blp.cpu().numpy().reshape(n_groups, G, C)
+        r2 = rewards.cpu().numpy().reshape(n_groups, G)
+        t0 = time.perf_counter()
+        reps = 3
+        for _ in range(reps):
+            lpo = O.chunk_log_prob(m, ls, a)
+            _, entries = O._entries(ids, r2, b3, G, 1e-8)
+            res = O._epilogue(lambda key: lpo[(key[0] * G + key[1]) * C:(key[0] * G + key[1] + 1) * C],
+                              entries, n_groups * G, 0.2, 0.0)
+            cs = np.empty(B)
+            for (k, i), v in res[4].items():
+                cs[(k * G + i) * C:(k * G + i + 1) * C] = v
+            O.gauss_head_backward(m, ls, a, cs)
+        cpu_ms = (time.perf_counter() - t0) / reps * 1e3
+        out["cpu_oracle_ms"] = cpu_ms
+        out["cpu_cores"] = 1
+        out["gpu_over_cpu"] = cpu_ms * 1e3 / graph_us
+        out["loss_oracle"] = float(res[0])
+    return out
+
+
 def _bench_allreduce(world, dev, barrier, max_over_ranks, nbytes=1 << 30, iters=5):
     """NCCL all-reduce of a learner gradient bucket (f32), busbw."""
     import torch
@@ -477,6 +579,7 @@ def run_ours(a):
     del dl
     repl = None if a.no_repl else _bench_replication(world, rank, dev, barrier, max_over_ranks)
     allreduce = _bench_allreduce(world, dev, barrier, max_over_ranks)
+    gauss = None if a.no_gauss else _bench_gauss_c3(dev, rank, cpu=not a.no_cpu)
     swim = None
     if not a.no_swimlane:
         barrier()
@@ -505,6 +608,7 @@ def run_ours(a):
                        "l2": "inputs 1.84 GB/rank > 126 MB L2 (no flush needed)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "replication": repl, "grad_allreduce": allreduce, "swimlane": swim,
+            "gauss_c3": gauss,
             "gpu_launches": 3 * a.steps, "clocks": clk,
             "loss": st["loss"], "mean_ratio": st["mean_ratio"],
             "clip_fraction": st["clip_fraction"],

@@ -58,6 +58,32 @@ __global__ void chunk_log_prob_kernel(const float* __restrict__ means,
   if (lane == 0) out[b] = -0.5 * kLog2Pi * D + acc;
 }
 
+// one CTA per row for wide chunks (D >= 512, e.g. pi0's 1,600): 256
+// thread-strided f64 partials, fixed warp-then-CTA reduction order
+constexpr int kClpThreads = 256;
+__global__ void __launch_bounds__(kClpThreads) chunk_log_prob_wide_kernel(
+    const float* __restrict__ means, const float* __restrict__ log_std,
+    const float* __restrict__ actions, int64_t B, int D, double* __restrict__ out) {
+  __shared__ double red[kClpThreads / 32];
+  const int64_t b = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double acc = 0.0;
+  for (int d = threadIdx.x; d < D; d += kClpThreads) {
+    const double s = static_cast<double>(log_std[d]);
+    const double eps =
+        (static_cast<double>(actions[b * D + d]) - static_cast<double>(means[b * D + d])) * exp(-s);
+    acc += -0.5 * eps * eps - s;
+  }
+  acc = warp_sum_f64(acc);
+  if (lane == 0) red[w] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < kClpThreads / 32; ++i) t += red[i];
+    out[b] = -0.5 * kLog2Pi * D + t;
+  }
+}
+
 // Per-row intermediates of the MLP backward (f64, recomputed forward).
 __global__ void policy_backward_rows_kernel(
     const float* __restrict__ w1, const float* __restrict__ b1, const float* __restrict__ w2,
@@ -131,34 +157,37 @@ __global__ void policy_backward_reduce_kernel(const float* __restrict__ obs,
 
 // head-only backward: dmeans[b, d] = c_b eps e^{-s} (f32 or f64 out),
 // dlog_std[d] += sum_b c_b (eps^2 - 1)
-__global__ void gauss_head_bwd_rows_kernel(const float* __restrict__ means,
-                                           const float* __restrict__ log_std,
-                                           const float* __restrict__ actions,
-                                           const double* __restrict__ coeffs, int64_t B, int D,
-                                           float* __restrict__ dmeans) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= B * D) return;
-  const int64_t b = i / D;
-  const int d = static_cast<int>(i % D);
-  const double inv = exp(-static_cast<double>(log_std[d]));
-  const double eps = (static_cast<double>(actions[i]) - static_cast<double>(means[i])) * inv;
-  dmeans[i] = static_cast<float>(coeffs[b] * eps * inv);
-}
-
-__global__ void gauss_head_bwd_cols_kernel(const float* __restrict__ means,
-                                           const float* __restrict__ log_std,
-                                           const float* __restrict__ actions,
-                                           const double* __restrict__ coeffs, int64_t B, int D,
-                                           double* __restrict__ dlog_std) {
-  const int d = blockIdx.x * blockDim.x + threadIdx.x;
-  if (d >= D) return;
-  const double inv = exp(-static_cast<double>(log_std[d]));
+// Head backward in one pass: a CTA owns 32 columns and all rows; its 32 row
+// groups stride the rows (warp = 32 consecutive columns of one row: 128-byte
+// coalesced), write dmeans, and reduce c_b (eps^2 - 1) over their rows; the
+// 32 group partials are then combined in a fixed order (deterministic).
+constexpr int kHeadCols = 32, kHeadGroups = 32;
+__global__ void __launch_bounds__(kHeadCols * kHeadGroups) gauss_head_bwd_kernel(
+    const float* __restrict__ means, const float* __restrict__ log_std,
+    const float* __restrict__ actions, const double* __restrict__ coeffs, int64_t B, int D,
+    float* __restrict__ dmeans, double* __restrict__ dlog_std) {
+  __shared__ double part[kHeadGroups][kHeadCols];
+  const int col = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int d = blockIdx.x * kHeadCols + col;
   double acc = 0.0;
-  for (int64_t b = 0; b < B; ++b) {
-    const double eps = (static_cast<double>(actions[b * D + d]) - static_cast<double>(means[b * D + d])) * inv;
-    acc += coeffs[b] * (eps * eps - 1.0);
+  if (d < D) {
+    const double inv = exp(-static_cast<double>(log_std[d]));
+#pragma unroll 4
+    for (int64_t b = grp; b < B; b += kHeadGroups) {
+      const double c = coeffs[b];
+      const double eps =
+          (static_cast<double>(actions[b * D + d]) - static_cast<double>(means[b * D + d])) * inv;
+      if (dmeans) dmeans[b * D + d] = static_cast<float>(c * eps * inv);
+      acc += c * (eps * eps - 1.0);
+    }
   }
-  dlog_std[d] += acc;
+  part[grp][col] = acc;
+  __syncthreads();
+  if (grp == 0 && d < D && dlog_std) {
+    double t = 0.0;
+    for (int g = 0; g < kHeadGroups; ++g) t += part[g][col];
+    dlog_std[d] += t;
+  }
 }
 
 }  // namespace dvla
@@ -183,6 +212,12 @@ extern "C" int dvla_chunk_log_prob(const float* means, const float* log_std, con
                                    int64_t B, int D, double* out, void* stream) {
   if (B < 0 || D < 1) return fail(DVLA_ERR_USAGE, "bad chunk_log_prob dimensions");
   if (B == 0) return DVLA_OK;
+  if (D >= 512) {
+    chunk_log_prob_wide_kernel<<<static_cast<unsigned>(B), kClpThreads, 0,
+                                 static_cast<cudaStream_t>(stream)>>>(means, log_std, actions, B,
+                                                                      D, out);
+    return launch_check("chunk_log_prob_wide_kernel");
+  }
   const int warps = 8;
   chunk_log_prob_kernel<<<static_cast<unsigned>((B + warps - 1) / warps), warps * 32, 0,
                           static_cast<cudaStream_t>(stream)>>>(means, log_std, actions, B, D, out);
@@ -226,16 +261,10 @@ extern "C" int dvla_gauss_head_backward(const float* means, const float* log_std
   if (B < 0 || D < 1) return fail(DVLA_ERR_USAGE, "bad gauss head dimensions");
   if (B == 0) return DVLA_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (dmeans) {
-    const int64_t n = B * D;
-    gauss_head_bwd_rows_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
-        means, log_std, actions, coeffs, B, D, dmeans);
-    if (int rc = launch_check("gauss_head_bwd_rows_kernel")) return rc;
-  }
-  if (dlog_std) {
-    gauss_head_bwd_cols_kernel<<<static_cast<unsigned>((D + 127) / 128), 128, 0, st>>>(
-        means, log_std, actions, coeffs, B, D, dlog_std);
-    if (int rc = launch_check("gauss_head_bwd_cols_kernel")) return rc;
-  }
+  if (!dmeans && !dlog_std) return DVLA_OK;
+  gauss_head_bwd_kernel<<<static_cast<unsigned>((D + kHeadCols - 1) / kHeadCols),
+                          kHeadCols * kHeadGroups, 0, st>>>(means, log_std, actions, coeffs, B, D,
+                                                            dmeans, dlog_std);
+  if (int rc = launch_check("gauss_head_bwd_kernel")) return rc;
   return DVLA_OK;
 }

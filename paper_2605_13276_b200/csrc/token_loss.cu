@@ -789,10 +789,23 @@ __global__ void __launch_bounds__(kEpiThreads) grpo_epilogue_kernel(EpiParams e)
       // warp (the reference accumulates total_loss / ratio_sum / clip_count
       // in entry order, grpo.py:269-273)
       const int64_t lim = (n_entries - base < kEpiThreads) ? n_entries - base : kEpiThreads;
+      // (loads batched 8 ahead so only the dependent adds serialise)
+      auto seq_sum = [&](double acc, const double* v) {
+        int64_t t = 0;
+        for (; t + 8 <= lim; t += 8) {
+          double x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) x[u] = v[t + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, x[u]);
+        }
+        for (; t < lim; ++t) acc = __dadd_rn(acc, v[t]);
+        return acc;
+      };
       if (tid == 0) {
-        for (int64_t t = 0; t < lim; ++t) loss = __dadd_rn(loss, s_loss[t]);
+        loss = seq_sum(loss, s_loss);
       } else if (tid == 32) {
-        for (int64_t t = 0; t < lim; ++t) ratio_sum = __dadd_rn(ratio_sum, s_rho[t]);
+        ratio_sum = seq_sum(ratio_sum, s_rho);
       } else if (tid == 64) {
         for (int64_t t = 0; t < lim; ++t) clip_count += s_clip[t];
       }
