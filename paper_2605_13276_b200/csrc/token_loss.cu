@@ -195,6 +195,8 @@ constexpr int kFusedThreadsWS = (kFusedComputeWarps + 4) * 32;
 constexpr int kLagRounds = 4;  // measured best on B200 (lag 2..6 sweep, tools/fused_variants.py)
 constexpr int kRing = 8;       // (lse, target) rows in flight tail -> prep; needs lag < kRing
 constexpr int kMaxLag = kRing - 1;
+constexpr float kFrameHi = 64.f;   // fixed-frame sum-exp range of a warp max (see phase A)
+constexpr float kFrameLo = -50.f;
 
 struct FusedSmem {
   uint64_t full[kFusedStages];
@@ -362,13 +364,17 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       const double sw = (lane < kFusedComputeWarps) ? S.ws[sa][lane] : 0.0;
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.afree[sa]);  // partial slot sa consumed
-      const float M = warp_max_f32(mw);
+      // a NaN partial (NaN logit) or a +inf frame (+inf logit) poisons the row
+      const bool poison = __any_sync(0xffffffffu, lane < kFusedComputeWarps &&
+                                                      (isnan(sw) || mw == INFINITY));
+      const float M = warp_max_f32((lane < kFusedComputeWarps && sw > 0.0) ? mw : -INFINITY);
       double term = (lane < kFusedComputeWarps && sw > 0.0)
                         ? sw * static_cast<double>(ex2f((mw - M) * kLog2e))
                         : 0.0;
       term = warp_sum_f64(term);
       if (lane == 0) {
-        const double lse = static_cast<double>(M) + log(term);
+        const double lse =
+            poison ? __longlong_as_double(kNaN64) : static_cast<double>(M) + log(term);
         double lp = static_cast<double>(xt_f) - lse;
         if (__double_as_longlong(lp) == kLpPending) lp = __longlong_as_double(kNaN64);
         if (tgt < 0) atomicOr(p.err, kErrToken);
@@ -472,31 +478,48 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     }
     if (!isB) {
       const int32_t tg = (tid == 0) ? __ldg(p.tokens + row_of(k)) : 0;  // used at the end
+      // One pass: exponentials in the fixed frame 2^(x log2e) (no max
+      // subtraction) with the packed max alongside.  The frame is exact
+      // enough when the warp max lies in [kFrameLo, kFrameHi] (no f32
+      // overflow of <= 8 terms per accumulator; terms flushed below 2^-126
+      // are < e^-37 of the max); otherwise (rare: huge or very negative
+      // logits) the warp redoes its slice relative to its own max.  The tail
+      // combines (frame, sum) pairs of all warps.
       const uint4* v = reinterpret_cast<const uint4*>(buf(s));
       uint32_t mx0 = 0xff80ff80u, mx1 = 0xff80ff80u;
-#pragma unroll 4
-      for (int i = tid; i < nvec; i += kFusedComputeThreads) {
-        const uint4 x = v[i];
-        mx0 = bf16x2_max(mx0, bf16x2_max(x.x, x.y));
-        mx1 = bf16x2_max(mx1, bf16x2_max(x.z, x.w));
-      }
-      const uint32_t mx = bf16x2_max(mx0, mx1);
-      const float m = warp_max_f32(fmaxf(bf16lo(mx), bf16hi(mx)));
-      const float mL = m * kLog2e;
-      const uint64_t l2e2 = f2pack(kLog2e, kLog2e), nmL2 = f2pack(-mL, -mL);
+      const uint64_t l2e2 = f2pack(kLog2e, kLog2e);
       uint64_t s01 = 0, s23 = 0, s45 = 0, s67 = 0;  // packed (0.f, 0.f)
-      auto ex2_pair = [&](uint32_t w) {
+      auto ex2_pair = [&](uint32_t w, uint64_t off2) {
         float y0, y1;
-        f2unpack(bf16x2_fma2(w, l2e2, nmL2), y0, y1);
+        f2unpack(bf16x2_fma2(w, l2e2, off2), y0, y1);
         return f2pack(ex2f(y0), ex2f(y1));
       };
 #pragma unroll 2
       for (int i = tid; i < nvec; i += kFusedComputeThreads) {
         const uint4 x = v[i];
-        s01 = fadd2(s01, ex2_pair(x.x));
-        s23 = fadd2(s23, ex2_pair(x.y));
-        s45 = fadd2(s45, ex2_pair(x.z));
-        s67 = fadd2(s67, ex2_pair(x.w));
+        mx0 = bf16x2_max(mx0, bf16x2_max(x.x, x.y));
+        mx1 = bf16x2_max(mx1, bf16x2_max(x.z, x.w));
+        s01 = fadd2(s01, ex2_pair(x.x, 0));
+        s23 = fadd2(s23, ex2_pair(x.y, 0));
+        s45 = fadd2(s45, ex2_pair(x.z, 0));
+        s67 = fadd2(s67, ex2_pair(x.w, 0));
+      }
+      const uint32_t mx = bf16x2_max(mx0, mx1);
+      const float wmax = warp_max_f32(fmaxf(bf16lo(mx), bf16hi(mx)));
+      float m = 0.f;  // frame of this warp's partial
+      if (!(wmax <= kFrameHi) || (wmax < kFrameLo && wmax > -INFINITY)) {  // warp-uniform
+        m = wmax;
+        const float mL = m * kLog2e;
+        const uint64_t nmL2 = f2pack(-mL, -mL);
+        s01 = s23 = s45 = s67 = 0;
+#pragma unroll 2
+        for (int i = tid; i < nvec; i += kFusedComputeThreads) {
+          const uint4 x = v[i];
+          s01 = fadd2(s01, ex2_pair(x.x, nmL2));
+          s23 = fadd2(s23, ex2_pair(x.y, nmL2));
+          s45 = fadd2(s45, ex2_pair(x.z, nmL2));
+          s67 = fadd2(s67, ex2_pair(x.w, nmL2));
+        }
       }
       float s0, s1, s2, s3;
       {

@@ -159,6 +159,36 @@ def test_abort_on_nonfinite_logit():
         _run_gpu(x, tokens, blp, rewards, ids, torch.float32)
 
 
+@pytest.mark.parametrize("bad", [np.nan, np.inf])
+def test_fused_bf16_abort_on_nonfinite_logit(bad):
+    """A NaN or +inf logit anywhere in a row poisons that row's lse in the
+    fused bf16 path too (the reference's log-prob check, grpo.py:255-256)."""
+    import torch
+    from paper_2605_13276_b200.grpo import GrpoAbort
+    x, tokens, blp, rewards, ids = _case(12, 3, 4, 1, 4, 4096, torch.bfloat16, ids=[7, 3, 5])
+    x[1, 2, 0, 1, 3001] = bad   # not the target column, deep inside one warp's slice
+    tokens[1, 2, 0, 1] = 17
+    with pytest.raises(GrpoAbort, match="group 3.*non-finite log-prob"):
+        _run_gpu(x, tokens, blp, rewards, ids, torch.bfloat16, fused=True)
+
+
+def test_fused_bf16_masked_logits_match_oracle():
+    """-inf (masked) logits, including whole warp slices of -inf and rows
+    with a large dynamic range, stay finite and match the oracle."""
+    import torch
+    x, tokens, blp, rewards, ids = _case(13, 2, 4, 1, 4, 4096, torch.bfloat16)
+    x[0, 1, 0, 2, 1024:3072] = -np.inf
+    x[1, 0, 0, 0, :] += 70.0            # beyond the speculative exp frame
+    x[1, 3, 0, 3, :] -= 90.0
+    x = torch.from_numpy(x).to(torch.bfloat16).float().numpy()  # exact bf16 values again
+    tokens[0, 1, 0, 2] = 5
+    _, _, st0 = O.grpo_token_grad(x, tokens, np.zeros(blp.shape, np.float32),
+                                  np.tile(np.arange(4, dtype=np.float32), (2, 1)),
+                                  np.arange(2), want_dlogits=False)
+    blp = (st0["lp_chunk"] + 0.01).astype(np.float32)
+    _check(x, tokens, blp, rewards, ids, torch.bfloat16, True, 1e-2)
+
+
 def test_token_out_of_range_is_usage_error():
     import torch
     from paper_2605_13276_b200.core import UsageError
