@@ -159,8 +159,9 @@ def test_abort_on_nonfinite_logit():
         _run_gpu(x, tokens, blp, rewards, ids, torch.float32)
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("bad", [np.nan, np.inf])
-def test_fused_bf16_abort_on_nonfinite_logit(bad):
+def test_bf16_abort_on_nonfinite_logit(bad, fused):
     """A NaN or +inf logit anywhere in a row poisons that row's lse in the
     fused bf16 path too (the reference's log-prob check, grpo.py:255-256)."""
     import torch
@@ -169,7 +170,7 @@ def test_fused_bf16_abort_on_nonfinite_logit(bad):
     x[1, 2, 0, 1, 3001] = bad   # not the target column, deep inside one warp's slice
     tokens[1, 2, 0, 1] = 17
     with pytest.raises(GrpoAbort, match="group 3.*non-finite log-prob"):
-        _run_gpu(x, tokens, blp, rewards, ids, torch.bfloat16, fused=True)
+        _run_gpu(x, tokens, blp, rewards, ids, torch.bfloat16, fused=fused)
 
 
 def test_fused_bf16_masked_logits_match_oracle():
