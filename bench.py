@@ -330,24 +330,20 @@ def _bench_gauss_c3(dev, rank, steps=200, cpu=True):
     ids = np.arange(n_groups, dtype=np.int64)
     order_d = torch.from_numpy(ids).to(dev)
     ids_d = order_d.clone()
-    adv = torch.empty(n_groups * G, dtype=torch.float64, device=dev)
-    bad = torch.empty(n_groups, dtype=torch.int32, device=dev)
     lp = torch.empty(B, dtype=torch.float64, device=dev)
-    coeff = torch.empty(B, dtype=torch.float64, device=dev)
     stats = torch.zeros(_lib.ST_LEN, dtype=torch.float64, device=dev)
     dm = torch.empty(B, D, dtype=torch.float32, device=dev)
     dls = torch.zeros(D, dtype=torch.float64, device=dev)
 
-    def step(s):
-        _lib.dvla_group_advantages(rewards.data_ptr(), n_groups, G, 1e-8, adv.data_ptr(),
-                                   bad.data_ptr(), s)
-        _lib.dvla_chunk_log_prob(means.data_ptr(), log_std.data_ptr(), actions.data_ptr(), B, D,
-                                 lp.data_ptr(), s)
-        _lib.dvla_grpo_epilogue(lp.data_ptr(), blp.data_ptr(), None, adv.data_ptr(),
-                                bad.data_ptr(), order_d.data_ptr(), ids_d.data_ptr(), n_groups, G,
-                                C, 0.2, 0.0, coeff.data_ptr(), stats.data_ptr(), s)
-        _lib.dvla_gauss_head_backward(means.data_ptr(), log_std.data_ptr(), actions.data_ptr(),
-                                      coeff.data_ptr(), B, D, dm.data_ptr(), dls.data_ptr(), s)
+    ws = torch.empty(_lib.dvla_gauss_loss_workspace_bytes(n_groups, G, C), dtype=torch.uint8,
+                     device=dev)
+
+    def step(s):  # one C-ABI call: advantages -> lp -> epilogue -> head backward
+        _lib.dvla_gauss_loss_fwd_bwd(means.data_ptr(), log_std.data_ptr(), actions.data_ptr(),
+                                     blp.data_ptr(), rewards.data_ptr(), order_d.data_ptr(),
+                                     ids_d.data_ptr(), n_groups, G, C, D, 0.2, 1e-8, 0.0,
+                                     dm.data_ptr(), dls.data_ptr(), lp.data_ptr(),
+                                     stats.data_ptr(), ws.data_ptr(), ws.numel(), s)
 
     for _ in range(5):
         step(st.cuda_stream)

@@ -163,6 +163,22 @@ int dvla_gauss_head_backward(const float* means, const float* log_std, const flo
                              const double* coeffs, int64_t B, int D, float* dmeans,
                              double* dlog_std, void* stream);
 
+/* The whole Gaussian-head GRPO step in one call (grpo_grad, grpo.py:217-294,
+ * for an action expert whose means come from the caller's model, BASELINE
+ * config 3): group advantages (grpo.py:89-108) -> chunk_log_prob
+ * (numba_backend.py:49-61) -> canonical-order epilogue (grpo.py:242-276,
+ * stats as dvla_token_loss_fwd_bwd) -> head backward.  Rows are
+ * (group, trajectory, chunk) in input group order, B = n_groups*G*C.
+ * lp_chunk [B] f64 out; dmeans [B,D] f32 out (may be NULL); dlog_std [D] f64
+ * accumulates += (may be NULL).  Workspace: dvla_gauss_loss_workspace_bytes. */
+size_t dvla_gauss_loss_workspace_bytes(int64_t n_groups, int64_t G, int64_t C);
+int dvla_gauss_loss_fwd_bwd(const float* means, const float* log_std, const float* actions,
+                            const float* blp, const float* rewards, const int64_t* group_order,
+                            const int64_t* group_ids, int64_t n_groups, int64_t G, int64_t C,
+                            int D, double clip_eps, double adv_eps, double kl_coeff,
+                            float* dmeans, double* dlog_std, double* lp_chunk, double* stats,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
 /* ----------------------------------------------------- optimizer tail */
 
 /* adam_step (grpo.py:137-150) in place: f32 params, f64 grad/m/v; step is the

@@ -178,6 +178,11 @@ dvla_policy_backward_workspace_bytes = _proto("dvla_policy_backward_workspace_by
                                               [_i64, _i32, _i32], _sz)
 dvla_policy_backward = _proto("dvla_policy_backward", [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                                        _i64, _i32, _i32, _i32, _vp, _vp, _vp])
+dvla_gauss_loss_workspace_bytes = _proto("dvla_gauss_loss_workspace_bytes", [_i64, _i64, _i64],
+                                         _sz)
+dvla_gauss_loss_fwd_bwd = _proto("dvla_gauss_loss_fwd_bwd", [
+    _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i32, _f64, _f64, _f64, _vp, _vp, _vp,
+    _vp, _vp, _sz, _vp])
 dvla_gauss_head_backward = _proto("dvla_gauss_head_backward", [_vp, _vp, _vp, _vp, _i64, _i32,
                                                                _vp, _vp, _vp])
 # ------------------------------------------------------------ optimizer

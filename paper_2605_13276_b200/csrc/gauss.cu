@@ -268,3 +268,61 @@ extern "C" int dvla_gauss_head_backward(const float* means, const float* log_std
   if (int rc = launch_check("gauss_head_bwd_kernel")) return rc;
   return DVLA_OK;
 }
+
+// ------------------------------------------------ one-call Gaussian GRPO step
+extern "C" int dvla_group_advantages(const float* rewards, int64_t n_groups, int64_t G,
+                                     double delta, double* adv, uint32_t* reward_bad,
+                                     void* stream);
+extern "C" int dvla_grpo_epilogue(const double* lp_chunk, const float* blp, const double* blp64,
+                                  const double* adv, const uint32_t* reward_bad,
+                                  const int64_t* group_order, const int64_t* group_ids,
+                                  int64_t n_groups, int64_t G, int64_t C, double clip_eps,
+                                  double kl_coeff, double* coeff_out, double* stats,
+                                  void* stream);
+
+static size_t gauss_ws(int64_t n_groups, int64_t G, int64_t C, size_t* off_coeff,
+                       size_t* off_bad) {
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t adv = al(static_cast<size_t>(n_groups * G) * 8);
+  const size_t coeff = al(static_cast<size_t>(n_groups * G * C) * 8);
+  const size_t bad = al(static_cast<size_t>(n_groups) * 4);
+  *off_coeff = adv;
+  *off_bad = adv + coeff;
+  return adv + coeff + bad;
+}
+
+extern "C" size_t dvla_gauss_loss_workspace_bytes(int64_t n_groups, int64_t G, int64_t C) {
+  if (n_groups < 0 || G < 0 || C < 0) return 0;
+  size_t a, b;
+  return gauss_ws(n_groups, G, C, &a, &b);
+}
+
+extern "C" int dvla_gauss_loss_fwd_bwd(const float* means, const float* log_std,
+                                       const float* actions, const float* blp,
+                                       const float* rewards, const int64_t* group_order,
+                                       const int64_t* group_ids, int64_t n_groups, int64_t G,
+                                       int64_t C, int D, double clip_eps, double adv_eps,
+                                       double kl_coeff, float* dmeans, double* dlog_std,
+                                       double* lp_chunk, double* stats, void* workspace,
+                                       size_t workspace_bytes, void* stream) {
+  if (n_groups < 1) return fail(DVLA_ERR_CONFIG, "grpo update needs at least one group");
+  if (G < 2) return fail(DVLA_ERR_CONFIG, "group_size must be >= 2, got %lld", (long long)G);
+  if (C < 1 || D < 1) return fail(DVLA_ERR_USAGE, "C and D must be >= 1");
+  if (!means || !log_std || !actions || !blp || !rewards || !lp_chunk || !stats || !workspace)
+    return fail(DVLA_ERR_USAGE, "null pointer argument");
+  size_t off_coeff, off_bad;
+  const size_t need = gauss_ws(n_groups, G, C, &off_coeff, &off_bad);
+  if (workspace_bytes < need)
+    return fail(DVLA_ERR_USAGE, "workspace too small: %zu < %zu", workspace_bytes, need);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  double* adv = reinterpret_cast<double*>(ws);
+  double* coeff = reinterpret_cast<double*>(ws + off_coeff);
+  uint32_t* bad = reinterpret_cast<uint32_t*>(ws + off_bad);
+  const int64_t B = n_groups * G * C;
+  if (int rc = dvla_group_advantages(rewards, n_groups, G, adv_eps, adv, bad, stream)) return rc;
+  if (int rc = dvla_chunk_log_prob(means, log_std, actions, B, D, lp_chunk, stream)) return rc;
+  if (int rc = dvla_grpo_epilogue(lp_chunk, blp, nullptr, adv, bad, group_order, group_ids,
+                                  n_groups, G, C, clip_eps, kl_coeff, coeff, stats, stream))
+    return rc;
+  return dvla_gauss_head_backward(means, log_std, actions, coeff, B, D, dmeans, dlog_std, stream);
+}

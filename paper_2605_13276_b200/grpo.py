@@ -372,6 +372,60 @@ def grpo_token_grad(logits, tokens, behavior_log_prob, rewards, group_ids, cfg: 
     return st["loss"], (dlogits if write_dlogits else None), st
 
 
+def grpo_gauss_head_grad(means, log_std, actions, behavior_log_prob, rewards, group_ids,
+                         cfg: GrpoConfig, dlog_std=None, stream=None):
+    """Gaussian-head grpo_grad for an action expert whose chunk means come
+    from the caller's model (BASELINE config 3, pi0-shaped): one
+    `dvla_gauss_loss_fwd_bwd` call -> (loss, dmeans [.., D] f32,
+    dlog_std [D] f64 (accumulated into `dlog_std` if given), stats).
+
+    means/actions f32 [n_groups, G, C, D] CUDA tensors in `group_ids` order,
+    log_std f32 [D], behavior_log_prob f32 [n_groups, G, C], rewards f32
+    [n_groups, G]; the abort and canonical-order contract is grpo.py:226-294.
+    """
+    from . import _lib
+    torch = _torch()
+    cfg.validate()
+    ids = np.asarray(group_ids, dtype=np.int64)
+    n_groups = len(ids)
+    if n_groups == 0:
+        raise ConfigError("grpo update needs at least one group")
+    if means.dim() != 4 or actions.shape != means.shape:
+        raise UsageError("means/actions must be (n_groups, G, C, D) and equal in shape")
+    _, G, C, D = means.shape
+    if G != cfg.group_size:
+        raise ConfigError(f"group {int(ids[0])} has {G} trajectories, expected G={cfg.group_size}")
+    dev = means.device
+    for name, t, dt in (("means", means, torch.float32), ("actions", actions, torch.float32),
+                        ("log_std", log_std, torch.float32),
+                        ("behavior_log_prob", behavior_log_prob, torch.float32),
+                        ("rewards", rewards, torch.float32)):
+        if t.dtype != dt or not t.is_cuda or not t.is_contiguous():
+            raise UsageError(f"{name} must be a contiguous {dt} CUDA tensor")
+    order = canonical_order(ids)
+    order_d = torch.from_numpy(order).to(dev)
+    ids_d = torch.from_numpy(ids).to(dev)
+    B = n_groups * G * C
+    lp = torch.empty(B, dtype=torch.float64, device=dev)
+    stats = torch.zeros(_lib.ST_LEN, dtype=torch.float64, device=dev)
+    dm = torch.empty((n_groups, G, C, D), dtype=torch.float32, device=dev)
+    if dlog_std is None:
+        dlog_std = torch.zeros(D, dtype=torch.float64, device=dev)
+    ws = torch.empty(max(_lib.dvla_gauss_loss_workspace_bytes(n_groups, G, C), 8),
+                     dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.dvla_gauss_loss_fwd_bwd(
+            means.data_ptr(), log_std.data_ptr(), actions.data_ptr(), behavior_log_prob.data_ptr(),
+            rewards.data_ptr(), order_d.data_ptr(), ids_d.data_ptr(), n_groups, G, C, D,
+            float(cfg.clip_eps), float(cfg.adv_epsilon), float(cfg.kl_coeff), dm.data_ptr(),
+            dlog_std.data_ptr(), lp.data_ptr(), stats.data_ptr(), ws.data_ptr(), ws.numel(),
+            _stream_ptr(stream)), "dvla_gauss_loss_fwd_bwd")
+    st = stats_from_vector(stats.cpu().numpy(), ids, order, n_groups * G,
+                           rewards.reshape(n_groups, G).cpu().numpy())
+    st["lp_chunk"] = lp.view(n_groups, G, C)
+    return st["loss"], dm, dlog_std, st
+
+
 # ------------------------------------------------------------------------
 # Reference-shaped learner for the Gaussian tanh-MLP chunk policy
 # ------------------------------------------------------------------------

@@ -216,3 +216,55 @@ def test_gauss_head_backward_c3_shape(dev):
     odm, odls = O.gauss_head_backward(means, log_std, actions, c)
     np.testing.assert_allclose(dm, odm, rtol=1e-6, atol=1e-12)
     np.testing.assert_allclose(dls, odls, rtol=1e-10, atol=1e-14)
+
+
+@pytest.mark.parametrize("C,kl", [(1, 0.0), (3, 0.1)])
+def test_gauss_loss_one_call_matches_oracle(dev, C, kl):
+    """dvla_gauss_loss_fwd_bwd (advantages -> chunk_log_prob -> canonical
+    epilogue -> head backward in one C call) against the f64 oracle, with
+    permuted group ids, several chunks per trajectory and the KL term."""
+    import torch
+    from paper_2605_13276_b200 import grpo
+    rng = np.random.default_rng(1 + C)
+    n_groups, G, D = 6, 4, 1600
+    ids = np.array([11, 3, 7, 20, 1, 9])
+    means = rng.normal(0, 1, (n_groups, G, C, D)).astype(np.float32)
+    actions = (means + rng.normal(0, 0.5, means.shape)).astype(np.float32)
+    log_std = rng.normal(0, 0.1, D).astype(np.float32)
+    lp0 = O.chunk_log_prob(means.reshape(-1, D), log_std, actions.reshape(-1, D))
+    blp = (lp0.reshape(n_groups, G, C) + rng.uniform(-0.3, 0.3, (n_groups, G, C))).astype(np.float32)
+    rewards = rng.integers(0, 2, (n_groups, G)).astype(np.float32)
+    cfg = grpo.GrpoConfig(group_size=G, kl_coeff=kl)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    loss, dm, dls, st = grpo.grpo_gauss_head_grad(t(means), t(log_std), t(actions), t(blp),
+                                                   t(rewards), ids, cfg)
+    # oracle: same epilogue entries, coefficients -> head backward
+    order, entries = O._entries(ids, rewards, blp, G, cfg.adv_epsilon)
+    lp_flat = lp0.reshape(n_groups, G, C)
+    res = O._epilogue(lambda key: lp_flat[key[0], key[1]], entries, n_groups * G, cfg.clip_eps,
+                      kl)
+    cs = np.empty((n_groups, G, C))
+    for (k, i), v in res[4].items():
+        cs[k, i] = v
+    odm, odls = O.gauss_head_backward(means.reshape(-1, D), log_std, actions.reshape(-1, D),
+                                      cs.reshape(-1))
+    assert loss == pytest.approx(res[0], rel=1e-9, abs=1e-15)
+    assert st["group_ids"] == sorted(ids.tolist())
+    np.testing.assert_allclose(st["lp_chunk"].cpu().numpy(), lp_flat, rtol=1e-12)
+    np.testing.assert_allclose(dm.cpu().numpy().reshape(-1, D), odm, rtol=1e-5, atol=1e-12)
+    np.testing.assert_allclose(dls.cpu().numpy(), odls, rtol=1e-9, atol=1e-14)
+
+
+def test_gauss_loss_one_call_abort_on_nonfinite_reward(dev):
+    import torch
+    from paper_2605_13276_b200 import grpo
+    rng = np.random.default_rng(5)
+    n_groups, G, C, D = 3, 4, 1, 64
+    means = rng.normal(0, 1, (n_groups, G, C, D)).astype(np.float32)
+    rewards = rng.integers(0, 2, (n_groups, G)).astype(np.float32)
+    rewards[1, 2] = np.inf
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    with pytest.raises(grpo.GrpoAbort, match="group 4.*non-finite reward"):
+        grpo.grpo_gauss_head_grad(t(means), t(np.zeros(D, np.float32)), t(means),
+                                  t(np.zeros((n_groups, G, C), np.float32)), t(rewards),
+                                  [9, 4, 6], grpo.GrpoConfig(group_size=G))
