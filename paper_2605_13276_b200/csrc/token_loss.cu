@@ -257,7 +257,7 @@ __device__ __forceinline__ void b_row(uint4* __restrict__ v, int nvec, int tid, 
 }
 
 __global__ void __launch_bounds__(kFusedThreadsWS, 1)
-    tok_fused_bf16_kernel(TokParams p, uint32_t stage_bytes, int write_dl, int lag, int a_evict_last) {
+    tok_fused_bf16_kernel(TokParams p, uint32_t stage_bytes, int write_dl, int lag) {
   extern __shared__ __align__(128) uint8_t dyn_smem[];
   FusedSmem& S = *reinterpret_cast<FusedSmem*>(dyn_smem);
   uint8_t* bufs = dyn_smem + ((sizeof(FusedSmem) + 127) / 128) * 128;
@@ -300,7 +300,6 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   if (warp == kWarpLoader) {
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
-      const uint64_t pol_keep = l2_policy_evict_last();
       for (int n = 0; n < nops; ++n) {
         const int s = static_cast<int>(n % kFusedStages);
         if (n >= kFusedStages) {
@@ -314,9 +313,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
         mbar_arrive_expect_tx(&S.full[s], row_bytes);
         if (isB)  // second (last) read of the row: from L2, then evict
           tma_load_1d_evict_first(buf(s), logits + row_of(k) * V, row_bytes, &S.full[s], pol);
-        else if (a_evict_last && write_dl)  // keep in L2 until B re-reads it
-          tma_load_1d_evict_first(buf(s), logits + row_of(k) * V, row_bytes, &S.full[s], pol_keep);
-        else
+        else  // (an evict_last hint here measured no better: the lag keeps rows in L2)
           tma_load_1d(buf(s), logits + row_of(k) * V, row_bytes, &S.full[s]);
       }
     }
@@ -1002,13 +999,8 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
       const char* e = getenv("DVLA_FUSED_LAG");
       return e ? atoi(e) : kLagRounds;
     }();
-    static const int a_keep = [] {
-      const char* e = getenv("DVLA_FUSED_KEEP");
-      return e ? atoi(e) : 0;
-    }();
-
-    tok_fused_bf16_kernel<<<grid, kFusedThreadsWS, fsmem, stream>>>(p, stage_bytes, want_dl ? 1 : 0,
-                                                                     lag < 2 ? 2 : (lag > kMaxLag ? kMaxLag : lag), a_keep);
+    tok_fused_bf16_kernel<<<grid, kFusedThreadsWS, fsmem, stream>>>(
+        p, stage_bytes, want_dl ? 1 : 0, lag < 2 ? 2 : (lag > kMaxLag ? kMaxLag : lag));
     prof_end(stream, stop);
     if (int rc = launch_check("tok_fused_bf16_kernel")) return rc;
     if (!want_dl) {

@@ -19,7 +19,7 @@ f(cnt.data_ptr())
 tl.launch(logits,tokens,blp,rewards,dl); torch.cuda.synchronize()
 f(None)
 c=cnt.cpu().numpy().astype(float)
-names={0:'comp wait full (n<16)',7:'comp wait full (n>=16)',1:'comp wait cfullB (b<8)',6:'comp wait cfullB (b>=8)',9:'prep polls k<8 (count)',10:'prep polls k>=8 (count)',2:'coef tail',3:'coef chunk-load latency',4:'coef prep',5:'coef idle sleeps (count)',8:'loader wait empty',9:'store wait adoneB',10:'missing rows at spin (sum)',15:'spins with chunk complete',11:'spin count',13:'pub wait pubfull',14:'pub store+atomic',12:'kernel cycles (sum over CTAs, tid0)'}
+names={0:'compute warp 0: wait full',1:'compute warp 0: wait B coefficient',3:'compute warp 0: wait A partial slot',8:'loader: wait empty stage',12:'kernel cycles (sum over CTAs, tid0)'}
 tot=c[12]
-for i,n in names.items(): print(f'{n:40s} {c[i]:14.0f} {c[i]/tot*100 if i not in (5,9,10,11,15) else 0:6.1f}%')
+for i,n in names.items(): print(f'{n:40s} {c[i]:14.0f} {c[i]/tot*100:6.1f}%')
 print(tl.stats(rewards)['loss'])
