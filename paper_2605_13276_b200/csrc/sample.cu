@@ -6,9 +6,11 @@
 //   token_r  ~ softmax(x_r)                  (Philox4x32-10 keyed by (seed, r))
 //   lp_tok_r = x_r[token_r] - logsumexp(x_r)  (f64)
 //   blp_q    = f32( pairwise sum of the chunk's T lp_tok )
-// One pass over the logits (HBM-bound, N*s bytes): per-thread online
-// (max, sum-exp), a deterministic block scan of the per-thread masses, and an
-// inverse-CDF lookup inside the single thread whose mass interval holds u.
+// One pass over the logits (HBM-bound, N*s bytes; 0.37 ms = 5.0 TB/s at the
+// C2 shape, tools/sample_bench.py): per-thread sum-exp in a fixed exponent
+// frame with 8 16-byte loads in flight, a deterministic block scan of the
+// per-thread masses, and an inverse-CDF lookup inside the single thread whose
+// mass interval holds u.
 // Draws are a pure function of (seed, offset, row), never of scheduling.
 #include "common.cuh"
 #include "grpo_math.cuh"
@@ -38,12 +40,30 @@ __device__ __forceinline__ double philox_uniform53(uint64_t seed, uint64_t offse
 }
 
 constexpr int kSampThreads = 256;
+constexpr int kSampBatch = 8;         // uint4 loads in flight per thread
+constexpr float kSampFrameHi = 64.f;  // fixed exponent frame valid for row max in [lo, hi]
+constexpr float kSampFrameLo = -50.f;
 
 template <class T>
 struct SampElem;
 template <>
 struct SampElem<__nv_bfloat16> {
   static constexpr int kVec = 8;
+  // 2^(x log2e - fL) for the 8 elements of u, summed pairwise into acc[4]
+  __device__ static void exps(const uint4& u, uint64_t l2e2, uint64_t nf2, uint64_t (&acc)[4]) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float y0, y1;
+      f2unpack(bf16x2_fma2(w[j], l2e2, nf2), y0, y1);
+      acc[j] = fadd2(acc[j], f2pack(ex2f(y0), ex2f(y1)));
+    }
+  }
+  __device__ static uint32_t maxw(const uint4& u) {  // packed max of the 8
+    return bf16x2_max(bf16x2_max(u.x, u.y), bf16x2_max(u.z, u.w));
+  }
+  __device__ static float maxf(uint32_t packed) { return fmaxf(bf16lo(packed), bf16hi(packed)); }
+  static constexpr uint32_t kNegInf = 0xff80ff80u;
   __device__ static void unpack(const uint4& u, float* f) {
     f[0] = bf16lo(u.x); f[1] = bf16hi(u.x); f[2] = bf16lo(u.y); f[3] = bf16hi(u.y);
     f[4] = bf16lo(u.z); f[5] = bf16hi(u.z); f[6] = bf16lo(u.w); f[7] = bf16hi(u.w);
@@ -55,6 +75,19 @@ struct SampElem<__nv_bfloat16> {
 template <>
 struct SampElem<float> {
   static constexpr int kVec = 4;
+  __device__ static void exps(const uint4& u, uint64_t l2e2, uint64_t nf2, uint64_t (&acc)[4]) {
+    float y0, y1, y2, y3;
+    f2unpack(ffma2(f2pack(__uint_as_float(u.x), __uint_as_float(u.y)), l2e2, nf2), y0, y1);
+    f2unpack(ffma2(f2pack(__uint_as_float(u.z), __uint_as_float(u.w)), l2e2, nf2), y2, y3);
+    acc[0] = fadd2(acc[0], f2pack(ex2f(y0), ex2f(y1)));
+    acc[1] = fadd2(acc[1], f2pack(ex2f(y2), ex2f(y3)));
+  }
+  __device__ static uint32_t maxw(const uint4& u) {
+    return __float_as_uint(fmaxf(fmaxf(__uint_as_float(u.x), __uint_as_float(u.y)),
+                                 fmaxf(__uint_as_float(u.z), __uint_as_float(u.w))));
+  }
+  __device__ static float maxf(uint32_t packed) { return __uint_as_float(packed); }
+  static constexpr uint32_t kNegInf = 0xff800000u;
   __device__ static void unpack(const uint4& u, float* f) {
     f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
     f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
@@ -62,7 +95,57 @@ struct SampElem<float> {
   __device__ static float at(const void* row, int64_t i) { return static_cast<const float*>(row)[i]; }
 };
 
-// Requires V % kVec == 0 and 16-byte aligned rows (checked on the host).
+template <class T>
+__device__ __forceinline__ uint32_t max_merge(uint32_t a, uint32_t b);
+template <>
+__device__ __forceinline__ uint32_t max_merge<__nv_bfloat16>(uint32_t a, uint32_t b) {
+  return bf16x2_max(a, b);
+}
+template <>
+__device__ __forceinline__ uint32_t max_merge<float>(uint32_t a, uint32_t b) {
+  return __float_as_uint(fmaxf(__uint_as_float(a), __uint_as_float(b)));
+}
+
+// Sum of this thread's exponentials 2^(x log2e - frame log2e), elements
+// tid, tid + 256, ... (uint4 granules), kSampBatch loads in flight.
+template <class T>
+__device__ __forceinline__ float thread_mass(const uint4* v, int nvec, int tid, float frame,
+                                             uint32_t* mx_out) {
+  const uint64_t l2e2 = f2pack(kLog2e, kLog2e);
+  const float fL = frame * kLog2e;
+  const uint64_t nf2 = f2pack(-fL, -fL);
+  uint64_t acc[4] = {0, 0, 0, 0};
+  uint32_t mx = SampElem<T>::kNegInf;
+  for (int i0 = tid; i0 < nvec; i0 += kSampBatch * kSampThreads) {
+    uint4 x[kSampBatch];
+#pragma unroll
+    for (int b = 0; b < kSampBatch; ++b) {
+      const int i = i0 + b * kSampThreads;
+      x[b] = (i < nvec) ? __ldcs(v + i)
+                        : make_uint4(SampElem<T>::kNegInf, SampElem<T>::kNegInf,
+                                     SampElem<T>::kNegInf, SampElem<T>::kNegInf);
+    }
+#pragma unroll
+    for (int b = 0; b < kSampBatch; ++b) {
+      mx = max_merge<T>(mx, SampElem<T>::maxw(x[b]));
+      SampElem<T>::exps(x[b], l2e2, nf2, acc);
+    }
+  }
+  if (mx_out) *mx_out = mx;
+  float a0, a1, a2, a3, a4, a5, a6, a7;
+  f2unpack(acc[0], a0, a1);
+  f2unpack(acc[1], a2, a3);
+  f2unpack(acc[2], a4, a5);
+  f2unpack(acc[3], a6, a7);
+  return ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+}
+
+// One CTA per row (requires V % kVec == 0 and 16-byte aligned rows).
+// Pass 1 takes every thread's mass in a fixed exponent frame (0, or the row
+// max when the max leaves the frame's safe range) and the row max; a
+// deterministic block scan of the masses in thread order locates the thread
+// whose interval holds u * total, and that thread walks its own elements in
+// the same order and frame to find the token.  lse = frame + log(total).
 template <class T>
 __global__ void __launch_bounds__(kSampThreads) tok_sample_kernel(
     const void* __restrict__ logits, int64_t V, uint64_t seed, uint64_t offset,
@@ -73,35 +156,25 @@ __global__ void __launch_bounds__(kSampThreads) tok_sample_kernel(
   const uint4* v = reinterpret_cast<const uint4*>(rowp);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nvec = static_cast<int>(V / E);
-  // pass 1: per-thread online max / sum-exp over vectors tid, tid + 256, ...
-  float m = -INFINITY, s = 0.f;
-  for (int i = tid; i < nvec; i += kSampThreads) {
-    float f[E];
-    SampElem<T>::unpack(__ldcs(v + i), f);
-    float vm = f[0];
-#pragma unroll
-    for (int e = 1; e < E; ++e) vm = fmaxf(vm, f[e]);
-    if (vm > m) {
-      s = (m == -INFINITY) ? 0.f : s * ex2f((m - vm) * kLog2e);
-      m = vm;
-    }
-    const float mL = m * kLog2e;
-#pragma unroll
-    for (int e = 0; e < E; ++e) s += ex2f(fmaf(f[e], kLog2e, -mL));
-  }
   __shared__ float sm_m[kSampThreads / 32];
   __shared__ double sm_w[kSampThreads / 32];
   __shared__ double sm_tot;
   __shared__ int32_t sm_tok;
   __shared__ int sm_win;
-  float M = warp_max_f32(m);
+  uint32_t mxp;
+  float s = thread_mass<T>(v, nvec, tid, 0.f, &mxp);
+  float M = warp_max_f32(SampElem<T>::maxf(mxp));
   if (lane == 0) sm_m[warp] = M;
   __syncthreads();
   M = sm_m[0];
 #pragma unroll
   for (int w = 1; w < kSampThreads / 32; ++w) M = fmaxf(M, sm_m[w]);
-  // this thread's mass relative to the row max, f64
-  const double c = (m == -INFINITY) ? 0.0 : static_cast<double>(s) * exp2(static_cast<double>((m - M) * kLog2e));
+  float frame = 0.f;
+  if (!(M <= kSampFrameHi) || (M < kSampFrameLo && M > -INFINITY)) {  // block-uniform
+    frame = M;
+    s = thread_mass<T>(v, nvec, tid, frame, nullptr);
+  }
+  const double c = static_cast<double>(s);
   // deterministic inclusive scan in thread order (warp shuffles, then warps)
   double incl = c;
 #pragma unroll
@@ -127,16 +200,16 @@ __global__ void __launch_bounds__(kSampThreads) tok_sample_kernel(
   if (c > 0.0 && u < hi) atomicMin(&sm_win, tid);
   __syncthreads();
   if (tid == sm_win) {
-    // inverse CDF inside this thread's elements, in its scan order
+    // inverse CDF inside this thread's elements, in its order and frame
     double acc = lo;
     int32_t tok = -1, last = -1;
-    const double ML = static_cast<double>(M) * 1.4426950408889634;
+    const float fL = frame * kLog2e;
     for (int i = tid; i < nvec && tok < 0; i += kSampThreads) {
       float f[E];
       SampElem<T>::unpack(v[i], f);
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const double pe = exp2(static_cast<double>(f[e]) * 1.4426950408889634 - ML);
+        const double pe = static_cast<double>(ex2f(fmaf(f[e], kLog2e, -fL)));
         if (pe > 0.0) last = i * E + e;
         acc += pe;
         if (tok < 0 && u < acc) tok = i * E + e;
@@ -149,7 +222,7 @@ __global__ void __launch_bounds__(kSampThreads) tok_sample_kernel(
   if (tid == 0) {
     int32_t tok = sm_tok;
     if (tok < 0) tok = 0;  // non-finite row: reported through lp (NaN)
-    const double lse = static_cast<double>(M) + log(sm_tot);
+    const double lse = static_cast<double>(frame) + log(sm_tot);
     tokens[r] = tok;
     if (lp_tok) lp_tok[r] = static_cast<double>(SampElem<T>::at(rowp, tok)) - lse;
   }
