@@ -402,6 +402,28 @@ def _bench_gauss_c3(dev, rank, steps=200, cpu=True):
     return out
 
 
+def _bench_sampler(dev, logits, steps=20):
+    """Rollout-side action-token sampling + behaviour log-prob
+    over the same C2 logits: one read pass, HBM-bound."""
+    import torch
+    from paper_2605_13276_b200.rollout import sample_action_tokens
+    for _ in range(3):
+        sample_action_tokens(logits, T, seed=1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(steps):
+        sample_action_tokens(logits, T, seed=1, offset=i)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    nbytes = logits.numel() * logits.element_size()
+    peak, _ = _peaks()
+    return {"workload": "C2 logits [28672, 32064] bf16 -> tokens, lp_tok, blp (f32)",
+            "ms": ms, "gbs": nbytes / ms / 1e6, "frac_of_hbm_peak": nbytes / ms / 1e6 / peak,
+            "launches_per_step": 2}
+
+
 def _bench_allreduce(world, dev, barrier, max_over_ranks, nbytes=1 << 30, iters=5):
     """NCCL all-reduce of a learner gradient bucket (f32), busbw."""
     import torch
@@ -576,6 +598,7 @@ def run_ours(a):
     repl = None if a.no_repl else _bench_replication(world, rank, dev, barrier, max_over_ranks)
     allreduce = _bench_allreduce(world, dev, barrier, max_over_ranks)
     gauss = None if a.no_gauss else _bench_gauss_c3(dev, rank, cpu=not a.no_cpu)
+    sampler = None if a.no_gauss else _bench_sampler(dev, logits)
     swim = None
     if not a.no_swimlane:
         barrier()
@@ -604,7 +627,7 @@ def run_ours(a):
                        "l2": "inputs 1.84 GB/rank > 126 MB L2 (no flush needed)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "replication": repl, "grad_allreduce": allreduce, "swimlane": swim,
-            "gauss_c3": gauss,
+            "gauss_c3": gauss, "sampler": sampler,
             "gpu_launches": 3 * a.steps, "clocks": clk,
             "loss": st["loss"], "mean_ratio": st["mean_ratio"],
             "clip_fraction": st["clip_fraction"],
