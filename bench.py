@@ -444,8 +444,34 @@ def _bench_allreduce(world, dev, barrier, max_over_ranks, nbytes=1 << 30, iters=
         ts.append(max_over_ranks(e0.elapsed_time(e1)))
     ms = sorted(ts)[len(ts) // 2]
     busbw = nbytes * 2 * (world - 1) / world / (ms / 1e3) / 1e9
-    return {"bytes": nbytes, "ms": ms, "busbw_gbs": busbw, "dtype": "f32",
-            "frac_of_nominal_900": busbw / NVLINK_NOMINAL_GBS}
+    out = {"bytes": nbytes, "ms": ms, "busbw_gbs": busbw, "dtype": "f32",
+           "frac_of_nominal_900": busbw / NVLINK_NOMINAL_GBS, "impl": "NCCL (ring)"}
+    del g
+    # the switch-reduced all-reduce (GradReducer's default where available)
+    from paper_2605_13276_b200.replicate import McAllReduce, multicast_supported
+    if max_over_ranks(0.0 if multicast_supported() else 1.0) == 0.0:
+        ar = McAllReduce(nbytes // 4)
+        ar.buf.fill_(1.0)
+        ar.allreduce()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(iters):
+            barrier()
+            e0.record(stream)
+            ar.allreduce()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(max_over_ranks(e0.elapsed_time(e1)))
+        ar.check()
+        ok = bool(torch.all(ar.buf == float(world ** (iters + 1))).item())
+        barrier()
+        ar.close()
+        nms = sorted(ts)[len(ts) // 2]
+        nbus = nbytes * 2 * (world - 1) / world / (nms / 1e3) / 1e9
+        out["nvls"] = {"impl": "switch-reduced (multimem.ld_reduce + multimem.st)", "ms": nms,
+                       "busbw_gbs": nbus, "frac_of_nominal_900": nbus / NVLINK_NOMINAL_GBS,
+                       "exact": ok}
+    return out
 
 
 def _bench_swimlane(world, rank, dev, max_over_ranks, epochs=8):

@@ -317,6 +317,16 @@ int dvla_mc_destroy(void* obj);
  * by the caller (reset by the kernel). */
 int dvla_mc_broadcast(const void* src, void* mc_dst, int64_t nbytes, void* mc_flag,
                       uint32_t epoch, int ctas, uint32_t* done_ctr, void* stream);
+/* Switch-reduced all-reduce of n f32 (n % 4 == 0) held in every member's
+ * bound region of one multicast object (GradReducer.reduce, runtime.py:
+ * 569-637): rank r reduces its 1/world slice with multimem.ld_reduce.add and
+ * stores the sum (times `scale`) to all members with multimem.st; entry and
+ * exit barriers use two u32 counters (local view / multicast view, zeroed
+ * once) with epoch = 1, 2, ... per call.  done_ctr: device u32, zeroed. */
+int dvla_mc_allreduce_f32(void* mc_buf, int64_t n, int rank, int world,
+                          const uint32_t* local_flags, void* mc_flags, uint32_t epoch,
+                          float scale, int ctas, uint32_t* done_ctr, uint64_t timeout_ns,
+                          uint32_t* err_dev, void* stream);
 /* Receivers: stream-ordered wait until the local flag reaches `epoch`;
  * *err_dev |= 1 on timeout (the reference's WeightMailbox wait). */
 int dvla_mc_wait(const uint32_t* local_flag, uint32_t epoch, uint64_t timeout_ns,

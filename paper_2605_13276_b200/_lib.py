@@ -168,6 +168,8 @@ dvla_mc_map = _proto("dvla_mc_map", [_vp, _i32, C.POINTER(_pp)])
 dvla_mc_destroy = _proto("dvla_mc_destroy", [_vp])
 dvla_mc_broadcast = _proto("dvla_mc_broadcast", [_vp, _vp, _i64, _vp, C.c_uint32, _i32, _vp,
                                                  _vp])
+dvla_mc_allreduce_f32 = _proto("dvla_mc_allreduce_f32", [
+    _vp, _i64, _i32, _i32, _vp, _vp, C.c_uint32, C.c_float, _i32, _vp, C.c_uint64, _vp, _vp])
 dvla_mc_wait = _proto("dvla_mc_wait", [_vp, C.c_uint32, C.c_uint64, _vp, _vp])
 
 # ---------------------------------------------- Gaussian head / MLP policy

@@ -300,3 +300,113 @@ extern "C" int dvla_mc_wait(const uint32_t* local_flag, uint32_t epoch, uint64_t
                                                                   err_dev);
   return launch_check("mc_wait_kernel");
 }
+
+// ------------------------------------------- switch-reduced all-reduce (f32)
+//
+// Learner-gradient mean across ranks (GradReducer.reduce, runtime.py:569-637;
+// SURVEY §8 a10) on NVSwitch multicast memory: every rank's f32 gradient
+// lives in its bound region of one multicast object; rank r owns the slice
+// [r n / N, (r + 1) n / N) and, per 16-byte granule, issues ONE
+// multimem.ld_reduce.add (the switch reads and sums the granule from every
+// member) and ONE multimem.st of the sum (the switch writes it into every
+// member).  Per GPU and direction the links carry (N + 1) / N of the
+// buffer (a ring all-reduce: 2 (N - 1) / N), the reduction happens in the
+// switch, and there are no rank-to-rank pipeline steps.  Entry and exit
+// barriers are flag counters in the same
+// multicast region, bumped with multimem.red.release and acquire-polled
+// locally; `epoch` = 1, 2, ... per call (flags start at 0).
+
+__device__ __forceinline__ void multimem_red_add_release_u32(uint32_t* mc, uint32_t v) {
+  asm volatile("multimem.red.release.sys.global.add.u32 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint4 multimem_ld_reduce_add_f32x4(const void* mc) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(mc)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ bool mc_wait_count(const uint32_t* flag, uint32_t target,
+                                              uint64_t timeout_ns, uint32_t* err) {
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t ns = 32;
+  while (ld_acquire_sys(flag) < target) {
+    __nanosleep(ns);
+    if (ns < 512) ns <<= 1;
+    if (globaltimer_ns() - t0 > timeout_ns) {
+      atomicOr(err, 1u);
+      return false;
+    }
+  }
+  return true;
+}
+
+constexpr int kArThreads = 512;
+
+// flags: [0] entry counter, [1] exit counter (local view and multicast view)
+__global__ void __launch_bounds__(kArThreads) mc_allreduce_f32_kernel(
+    uint4* mc_buf, int64_t nvec, int rank, int world, const uint32_t* local_flags,
+    uint32_t* mc_flags, uint32_t epoch, uint32_t* done_ctr, float scale, uint64_t timeout_ns,
+    uint32_t* err) {
+  __shared__ int s_ok;
+  // entry barrier: every rank's gradient is in place before anyone reduces
+  if (threadIdx.x == 0) {
+    if (blockIdx.x == 0) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      multimem_red_add_release_u32(mc_flags, 1u);
+    }
+    s_ok = mc_wait_count(local_flags, epoch * static_cast<uint32_t>(world), timeout_ns, err);
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  const int64_t per = (nvec + world - 1) / world;
+  const int64_t lo = per * rank, hi = (lo + per < nvec) ? lo + per : nvec;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kArThreads;
+  // (one reduction in flight per thread measured as fast as four: the
+  // switch, not the issue rate, bounds this loop)
+  for (int64_t i = lo + static_cast<int64_t>(blockIdx.x) * kArThreads + threadIdx.x; i < hi;
+       i += stride) {
+    uint4 v = multimem_ld_reduce_add_f32x4(mc_buf + i);
+    if (scale != 1.0f) {
+      v.x = __float_as_uint(__uint_as_float(v.x) * scale);
+      v.y = __float_as_uint(__uint_as_float(v.y) * scale);
+      v.z = __float_as_uint(__uint_as_float(v.z) * scale);
+      v.w = __float_as_uint(__uint_as_float(v.w) * scale);
+    }
+    multimem_st_u4(mc_buf + i, v);
+  }
+  // exit barrier: this rank's slice is stored everywhere; the last CTA of the
+  // rank signals, then waits until every rank has (results complete here)
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atom_add_acq_rel_gpu(done_ctr, 1u);
+    if (prev == gridDim.x - 1) {
+      *done_ctr = 0;
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      multimem_red_add_release_u32(mc_flags + 1, 1u);
+      mc_wait_count(local_flags + 1, epoch * static_cast<uint32_t>(world), timeout_ns, err);
+    }
+  }
+}
+
+extern "C" int dvla_mc_allreduce_f32(void* mc_buf, int64_t n, int rank, int world,
+                                     const uint32_t* local_flags, void* mc_flags, uint32_t epoch,
+                                     float scale, int ctas, uint32_t* done_ctr,
+                                     uint64_t timeout_ns, uint32_t* err_dev, void* stream) {
+  if (!mc_buf || !local_flags || !mc_flags || !done_ctr || !err_dev || n < 0 || (n % 4) != 0 ||
+      world < 1 || rank < 0 || rank >= world || epoch == 0)
+    return fail(DVLA_ERR_USAGE, "dvla_mc_allreduce_f32: bad arguments (n must be a multiple of 4)");
+  const int grid = ctas > 0 ? ctas : num_sms(current_device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaEvent_t stop;
+  prof_begin(st, &stop);
+  mc_allreduce_f32_kernel<<<grid, kArThreads, 0, st>>>(
+      static_cast<uint4*>(mc_buf), n / 4, rank, world, local_flags,
+      static_cast<uint32_t*>(mc_flags), epoch, done_ctr, scale, timeout_ns, err_dev);
+  prof_end(st, stop);
+  return launch_check("mc_allreduce_f32_kernel");
+}

@@ -330,37 +330,23 @@ def multicast_supported(device=None) -> bool:
     return bool(out.value)
 
 
-class McReplicator:
-    """Cross-process switch-multicast (NVLS) broadcast (one process per GPU).
+class _McRegion:
+    """One multicast object over `ranks` (one process per GPU) with a bound
+    region of `total` bytes on every member, mapped locally; the multicast
+    VA is mapped on the ranks in `map_on` (positions in `ranks`)."""
 
-    ranks[0] writes each byte once into a multicast mapping and the NVSwitch
-    replicates it into the bound region of every member; the root then
-    release-stores the epoch into every member's flag through the same
-    mapping and receivers acquire-poll their local copy (reference
-    ControlPlane.broadcast -> WeightMailbox.deliver, planes.py:294-321,
-    244-275).  Collective construction: every rank of `ranks` calls it.
-    The root is a member too (its own bound copy is the cost of the team).
-    """
-
-    def __init__(self, nbytes: int, ranks=None, n_buffers: int = 2, ctas: int = 0, group=None):
+    def __init__(self, total: int, ranks, group, map_on):
         import os
         import torch.distributed as dist
         from . import _lib
         torch = _torch()
-        if nbytes % 16:
-            raise UsageError("replicated regions must be a multiple of 16 bytes")
         self.rank = dist.get_rank()
         world = dist.get_world_size()
-        self.ranks = list(range(world)) if ranks is None else list(ranks)
+        self.ranks = list(ranks)
         self.pos = self.ranks.index(self.rank) if self.rank in self.ranks else -1
-        self.nbytes, self.nb, self.ctas = int(nbytes), int(n_buffers), int(ctas)
         self.dev = torch.cuda.current_device()
         n = len(self.ranks)
-        self.flag_off = (self.nb * self.nbytes + 255) // 256 * 256
-        total = self.flag_off + self.nb * 256
         self.obj = self.local = self.mc = None
-        self.err = torch.zeros(1, dtype=torch.int32, device="cuda")
-        self.done = torch.zeros(1, dtype=torch.int32, device="cuda")
         info = None
         if self.pos == 0:
             fd, size, obj = C.c_int(), C.c_size_t(), C.c_void_p()
@@ -379,19 +365,58 @@ class McReplicator:
         if self.pos >= 0:
             _lib.check(_lib.dvla_mc_add_device(self.obj, self.dev), "dvla_mc_add_device")
         dist.barrier(group=group)
+        self.t = None
         if self.pos >= 0:
             local = C.c_void_p()
             _lib.check(_lib.dvla_mc_bind(self.obj, self.dev, C.byref(local)), "dvla_mc_bind")
             self.local = local.value
             self.t = torch.as_tensor(_CudaView(self.local, self.size),
                                      device=torch.device("cuda", self.dev))
-            self.t[self.flag_off:].zero_()
-            torch.cuda.synchronize()
         dist.barrier(group=group)
-        if self.pos == 0:
+        if self.pos in map_on:
             mc = C.c_void_p()
             _lib.check(_lib.dvla_mc_map(self.obj, self.dev, C.byref(mc)), "dvla_mc_map")
             self.mc = mc.value
+        dist.barrier(group=group)
+
+    def close(self):
+        from . import _lib
+        _torch().cuda.synchronize()
+        self.t = None
+        if self.obj:
+            _lib.dvla_mc_destroy(self.obj)
+        self.obj = self.local = self.mc = None
+
+
+class McReplicator:
+    """Cross-process switch-multicast (NVLS) broadcast (one process per GPU).
+
+    ranks[0] writes each byte once into a multicast mapping and the NVSwitch
+    replicates it into the bound region of every member; the root then
+    release-stores the epoch into every member's flag through the same
+    mapping and receivers acquire-poll their local copy (reference
+    ControlPlane.broadcast -> WeightMailbox.deliver, planes.py:294-321,
+    244-275).  Collective construction: every rank of `ranks` calls it.
+    The root is a member too (its own bound copy is the cost of the team).
+    """
+
+    def __init__(self, nbytes: int, ranks=None, n_buffers: int = 2, ctas: int = 0, group=None):
+        import torch.distributed as dist
+        torch = _torch()
+        if nbytes % 16:
+            raise UsageError("replicated regions must be a multiple of 16 bytes")
+        ranks = list(range(dist.get_world_size())) if ranks is None else list(ranks)
+        self.nbytes, self.nb, self.ctas = int(nbytes), int(n_buffers), int(ctas)
+        self.flag_off = (self.nb * self.nbytes + 255) // 256 * 256
+        self.err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.done = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.region = _McRegion(self.flag_off + self.nb * 256, ranks, group, map_on=(0,))
+        self.rank, self.ranks, self.pos = self.region.rank, self.region.ranks, self.region.pos
+        self.size, self.local, self.mc, self.t = (self.region.size, self.region.local,
+                                                  self.region.mc, self.region.t)
+        if self.t is not None:
+            self.t[self.flag_off:].zero_()
+            torch.cuda.synchronize()
         dist.barrier(group=group)
 
     def replica(self, version: int):
@@ -425,10 +450,56 @@ class McReplicator:
             raise ReplicationTimeout(f"rank {self.rank}: multicast flag wait timed out")
 
     def close(self):
-        from . import _lib
-        torch = _torch()
-        torch.cuda.synchronize()
         self.t = None
-        if self.obj:
-            _lib.dvla_mc_destroy(self.obj)
-        self.obj = self.local = self.mc = None
+        self.region.close()
+        self.local = self.mc = None
+
+
+class McAllReduce:
+    """Switch-reduced all-reduce of an f32 buffer over NVSwitch multicast
+    (one process per GPU; GradReducer's collective, runtime.py:569-637).
+
+    `buf` is this rank's f32 [n] view inside its bound region: write the
+    local gradient there, call `allreduce(scale)`, read the (scaled) sum back.
+    Collective construction and calls: every rank of `ranks`."""
+
+    def __init__(self, n: int, ranks=None, ctas: int = 0, group=None):
+        import torch.distributed as dist
+        torch = _torch()
+        if n % 4:
+            raise UsageError("the all-reduce length must be a multiple of 4 floats")
+        ranks = list(range(dist.get_world_size())) if ranks is None else list(ranks)
+        self.n, self.ctas = int(n), int(ctas)
+        self.flag_off = (self.n * 4 + 255) // 256 * 256
+        self.region = _McRegion(self.flag_off + 256, ranks, group,
+                                map_on=tuple(range(len(ranks))))
+        self.pos, self.world = self.region.pos, len(ranks)
+        self.err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.done = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.epoch = 0
+        self.buf = None
+        if self.region.t is not None:
+            self.region.t[self.flag_off:].zero_()
+            self.buf = self.region.t[: self.n * 4].view(torch.float32)
+            torch.cuda.synchronize()
+        dist.barrier(group=group)
+
+    def allreduce(self, scale: float = 1.0, stream=None, timeout_s: float = 30.0):
+        from . import _lib
+        if self.pos < 0:
+            return
+        self.epoch += 1
+        r = self.region
+        _lib.check(_lib.dvla_mc_allreduce_f32(
+            r.mc, self.n, self.pos, self.world, r.local + self.flag_off, r.mc + self.flag_off,
+            self.epoch, float(scale), self.ctas, self.done.data_ptr(), int(timeout_s * 1e9),
+            self.err.data_ptr(), _stream_ptr(stream)), "dvla_mc_allreduce_f32")
+
+    def check(self):
+        if int(self.err.item()):
+            from ._lib import ReplicationTimeout
+            raise ReplicationTimeout("multicast all-reduce barrier timed out")
+
+    def close(self):
+        self.buf = None
+        self.region.close()

@@ -207,31 +207,79 @@ class VersionBoard:
 
 
 class GradReducer:
-    """Cross-node gradient mean (reference runtime.py:569-637) over NCCL.
+    """Cross-node gradient mean (reference runtime.py:569-637).
 
     The reference ships every node's gradient as an f32 frame, sums the
     decoded frames in f64 in node order and divides by `nodes`.  Here the
     gradient is quantised to f32 exactly as the frame would be, then
-    all-reduced: `exact=True` sums the f32 values in f64 (the reference's
-    arithmetic up to summation order), `exact=False` sums in f32 on the wire
-    (half the NVLink bytes; NCCL ring/NVLS order).  Single-node runs are a
-    no-op, as in the reference."""
+    all-reduced:
+      * `exact=True`: NCCL sum of the f32 values in f64 (the reference's
+        arithmetic up to summation order);
+      * backend "nvls": the switch-reduced all-reduce over NVSwitch multicast
+        memory (`replicate.McAllReduce`, f32 sums in the switch, 1/nodes
+        applied in the same pass; 685 vs 635 GB/s busbw for NCCL's ring at
+        1 GiB on 4 B200);
+      * backend "nccl": NCCL f32 all-reduce.
+    "auto" picks nvls from 4 nodes up when the box has NVSwitch multicast
+    and the sum need not be exact: per GPU and link direction it moves
+    (N + 1) / N of the buffer against the ring's 2 (N - 1) / N, so at 2
+    nodes the ring wins (569 vs 400 GB/s busbw measured).  Single-node runs
+    are a no-op, as in the reference."""
 
-    def __init__(self, nodes: int, group=None, exact: bool = False):
+    def __init__(self, nodes: int, group=None, exact: bool = False, backend: str = "auto"):
+        if backend not in ("auto", "nccl", "nvls"):
+            raise ConfigError(f"unknown gradient reduction backend {backend!r}")
+        if exact and backend == "nvls":
+            raise ConfigError("exact=True needs the NCCL f64 path")
         self.nodes = nodes
         self.group = group
         self.exact = exact
+        self.backend = backend
+        self._ar = None
+
+    def _use_nvls(self, grad) -> bool:
+        if self.exact or self.backend == "nccl" or self.nodes == 1 or not grad.is_cuda:
+            return False
+        if self.backend == "nvls":
+            return True
+        if self.nodes < 4:
+            self.backend = "nccl"
+            return False
+        from .replicate import multicast_supported
+        import torch
+        import torch.distributed as dist
+        ok = torch.tensor([1.0 if multicast_supported() else 0.0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+        self.backend = "nvls" if ok.item() == 1.0 else "nccl"
+        return self.backend == "nvls"
 
     def reduce(self, grad):
         import torch
         import torch.distributed as dist
         if self.nodes == 1:
             return grad
+        if self._use_nvls(grad):
+            from .replicate import McAllReduce
+            n = grad.numel()
+            if self._ar is None or self._ar.n < n:
+                if self._ar is not None:
+                    self._ar.close()
+                self._ar = McAllReduce((n + 3) // 4 * 4, group=self.group)
+                self._ar.buf.zero_()
+            self._ar.buf[:n].copy_(grad.reshape(-1))  # f32 quantisation (the frame)
+            self._ar.allreduce(scale=1.0 / self.nodes)
+            out = self._ar.buf[:n].to(grad.dtype).reshape(grad.shape)
+            return out
         q = grad.to(torch.float32)
         if self.exact:
             q = q.to(torch.float64)
         dist.all_reduce(q, op=dist.ReduceOp.SUM, group=self.group)
         return q.to(grad.dtype) / self.nodes if q.dtype != grad.dtype else q / self.nodes
+
+    def close(self):
+        if self._ar is not None:
+            self._ar.close()
+            self._ar = None
 
 
 # --------------------------------------------------------------- workers

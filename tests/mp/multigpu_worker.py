@@ -56,6 +56,26 @@ def main():
         mrep.close()
         if rank == 0:
             print("MULTICAST_OK", flush=True)
+        # (1c) switch-reduced all-reduce: exact on integer-valued f32, 3 calls
+        from paper_2605_13276_b200.replicate import McAllReduce
+        n = 1_000_004
+        ar = McAllReduce(n)
+        idx = torch.arange(n, device="cuda", dtype=torch.float32)
+        for it in range(3):
+            ar.buf.copy_((idx % 97) * (rank + 1) + it)
+            ar.allreduce(scale=1.0)
+            torch.cuda.synchronize()
+            ar.check()
+            want = (idx % 97) * (world * (world + 1) / 2) + it * world
+            assert torch.equal(ar.buf, want), ("allreduce", rank, it)
+        ar.buf.fill_(float(rank))
+        ar.allreduce(scale=1.0 / world)
+        torch.cuda.synchronize()
+        assert torch.allclose(ar.buf, torch.full_like(ar.buf, (world - 1) / 2), rtol=1e-6)
+        dist.barrier()
+        ar.close()
+        if rank == 0:
+            print("MC_ALLREDUCE_OK", flush=True)
 
     # (2) gradient mean over NCCL, exact mode vs host arithmetic
     g = torch.full((1000,), float(rank + 1), dtype=torch.float64, device="cuda") / 3.0
