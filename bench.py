@@ -580,7 +580,7 @@ def run_ours(a):
     traffic = _traffic().get("tok_fused_bf16_kernel")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "tok_fused_bf16_kernel" if not a.unfused else "tok_rows+tok_bwd",
+                "kernel": "tok_fused_kernel<bf16, 1 piece>" if not a.unfused else "tok_rows+tok_bwd",
                 "kernel_ms": round(kern_avg_ms, 4), "algo_bytes": algo_bytes,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
 

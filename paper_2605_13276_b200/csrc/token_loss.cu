@@ -13,15 +13,16 @@
 //
 // Kernels
 //   tok_adv_kernel        advantages per group (bit-exact, grpo.py:89-99)
-//   tok_fused_bf16_kernel persistent, 1 CTA/SM, warp-specialised: a loader
-//                         warp streams logits rows HBM->SMEM with TMA bulk
+//   tok_fused_kernel<TE,P> persistent, 1 CTA/SM, warp-specialised: a loader
+//                         warp streams logits rows (bf16 or f32; P = 1, 2 or
+//                         4 SMEM pieces per row) HBM->SMEM with TMA bulk
 //                         copies, 20 compute warps take max / sum-exp and
 //                         later write dlogits in place in SMEM, a tail /
-//                         prep / publisher warp trio turns partials into
-//                         lp_tok and chunk coefficients, a store warp streams
-//                         dlogits out with TMA bulk stores.  Each row is read
-//                         from HBM once (the second read hits L2):
-//                         compulsory traffic 2*N*2 bytes.
+//                         prep warp pair turns partials into lp_tok and
+//                         chunk coefficients, a store warp streams dlogits
+//                         out with TMA bulk stores.  Each row is read from
+//                         HBM once (the second read hits L2): compulsory
+//                         traffic 2*N*s bytes.  C2: bf16 0.67 ms, f32 1.29 ms.
 //   tok_rows_kernel<T>    unfused forward (any dtype / alignment / V)
 //   tok_chunk_kernel      unfused per-chunk coefficient
 //   tok_bwd_kernel<T>     unfused backward (re-reads logits: 3*N*s traffic)
@@ -192,9 +193,8 @@ constexpr int kWarpStore = kFusedComputeWarps + 2;
 constexpr int kPrepWarp = kFusedComputeWarps + 3;
 constexpr int kFusedThreadsWS = (kFusedComputeWarps + 4) * 32;
 
-constexpr int kLagRounds = 4;  // measured best on B200 (lag 2..6 sweep, tools/fused_variants.py)
+constexpr int kLagRounds = 4;  // pieces; measured best on B200 (lag sweep, tools/fused_variants.py)
 constexpr int kRing = 8;       // (lse, target) rows in flight tail -> prep; needs lag < kRing
-constexpr int kMaxLag = kRing - 1;
 constexpr float kFrameHi = 64.f;   // fixed-frame sum-exp range of a warp max (see phase A)
 constexpr float kFrameLo = -50.f;
 
@@ -239,25 +239,83 @@ __device__ __forceinline__ void op_of(int n, int nloc, int L, bool* isB, int* k)
   *k = pairs + (m - 2 * pairs);
 }
 
-// d loss / d logits of one B row, in place in SMEM: v = -c * p_v
-// (sgn = 0x80008000 flips both bf16 signs when c > 0)
-__device__ __forceinline__ void b_row(uint4* __restrict__ v, int nvec, int tid, float K,
-                                      uint32_t sgn) {
-  const uint64_t l2e2 = f2pack(kLog2e, kLog2e), nK2 = f2pack(-K, -K);
-  auto e2 = [&](uint32_t w) {
-    float y0, y1;
-    f2unpack(bf16x2_fma2(w, l2e2, nK2), y0, y1);
-    return pack_bf16x2(ex2f(y0), ex2f(y1)) ^ sgn;
-  };
-#pragma unroll 2
-  for (int i = tid; i < nvec; i += kFusedComputeThreads) {
-    const uint4 x = v[i];
-    v[i] = make_uint4(e2(x.x), e2(x.y), e2(x.z), e2(x.w));
+// Element traits of the fused kernel: 16-byte granules of bf16 (8) or f32 (4)
+template <class TE>
+struct FusedElem;
+template <>
+struct FusedElem<__nv_bfloat16> {
+  static constexpr int kE = 8;
+  static constexpr uint32_t kNegInf = 0xff80ff80u;
+  static constexpr uint32_t kSign = 0x80008000u;   // both halves
+  static constexpr uint32_t kNaN = 0x7fc07fc0u;
+  __device__ static uint32_t max16(uint32_t m, const uint4& x) {
+    return bf16x2_max(m, bf16x2_max(bf16x2_max(x.x, x.y), bf16x2_max(x.z, x.w)));
   }
-}
+  __device__ static float maxf(uint32_t m) { return fmaxf(bf16lo(m), bf16hi(m)); }
+  // acc += 2^(x log2e + off) over the granule (packed f32 pairs)
+  __device__ static void exps(const uint4& x, uint64_t l2e2, uint64_t off2, uint64_t (&acc)[4]) {
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float y0, y1;
+      f2unpack(bf16x2_fma2(w[j], l2e2, off2), y0, y1);
+      acc[j] = fadd2(acc[j], f2pack(ex2f(y0), ex2f(y1)));
+    }
+  }
+  // -sign(c) 2^(x log2e - K) for the granule, in place
+  __device__ static uint4 grad(const uint4& x, uint64_t l2e2, uint64_t nK2, uint32_t sgn) {
+    auto e2 = [&](uint32_t w) {
+      float y0, y1;
+      f2unpack(bf16x2_fma2(w, l2e2, nK2), y0, y1);
+      return pack_bf16x2(ex2f(y0), ex2f(y1)) ^ sgn;
+    };
+    return make_uint4(e2(x.x), e2(x.y), e2(x.z), e2(x.w));
+  }
+  __device__ static float get(const void* base, int i) {
+    return __bfloat162float(static_cast<const __nv_bfloat16*>(base)[i]);
+  }
+  __device__ static void put(void* base, int i, float v) {
+    static_cast<__nv_bfloat16*>(base)[i] = __float2bfloat16_rn(v);
+  }
+};
+template <>
+struct FusedElem<float> {
+  static constexpr int kE = 4;
+  static constexpr uint32_t kNegInf = 0xff800000u;
+  static constexpr uint32_t kSign = 0x80000000u;
+  static constexpr uint32_t kNaN = 0x7fc00000u;
+  __device__ static uint32_t max16(uint32_t m, const uint4& x) {
+    return __float_as_uint(fmaxf(__uint_as_float(m),
+                                 fmaxf(fmaxf(__uint_as_float(x.x), __uint_as_float(x.y)),
+                                       fmaxf(__uint_as_float(x.z), __uint_as_float(x.w)))));
+  }
+  __device__ static float maxf(uint32_t m) { return __uint_as_float(m); }
+  __device__ static void exps(const uint4& x, uint64_t l2e2, uint64_t off2, uint64_t (&acc)[4]) {
+    float y0, y1, y2, y3;
+    f2unpack(ffma2(f2pack(__uint_as_float(x.x), __uint_as_float(x.y)), l2e2, off2), y0, y1);
+    f2unpack(ffma2(f2pack(__uint_as_float(x.z), __uint_as_float(x.w)), l2e2, off2), y2, y3);
+    acc[0] = fadd2(acc[0], f2pack(ex2f(y0), ex2f(y1)));
+    acc[1] = fadd2(acc[1], f2pack(ex2f(y2), ex2f(y3)));
+  }
+  __device__ static uint4 grad(const uint4& x, uint64_t l2e2, uint64_t nK2, uint32_t sgn) {
+    float y0, y1, y2, y3;
+    f2unpack(ffma2(f2pack(__uint_as_float(x.x), __uint_as_float(x.y)), l2e2, nK2), y0, y1);
+    f2unpack(ffma2(f2pack(__uint_as_float(x.z), __uint_as_float(x.w)), l2e2, nK2), y2, y3);
+    return make_uint4(__float_as_uint(ex2f(y0)) ^ sgn, __float_as_uint(ex2f(y1)) ^ sgn,
+                      __float_as_uint(ex2f(y2)) ^ sgn, __float_as_uint(ex2f(y3)) ^ sgn);
+  }
+  __device__ static float get(const void* base, int i) { return static_cast<const float*>(base)[i]; }
+  __device__ static void put(void* base, int i, float v) { static_cast<float*>(base)[i] = v; }
+};
 
+// TE: logits / dlogits element type; P: SMEM pieces per row (a row longer
+// than a stage is streamed as P consecutive pieces: "virtual rows" u = k P + p
+// in the op sequence; the tail warp combines the P pieces' partials).
+template <class TE, int P>
 __global__ void __launch_bounds__(kFusedThreadsWS, 1)
-    tok_fused_bf16_kernel(TokParams p, uint32_t stage_bytes, int write_dl, int lag) {
+    tok_fused_kernel(TokParams p, uint32_t stage_bytes, int piece_vec, int write_dl, int lag) {
+  using FE = FusedElem<TE>;
+  constexpr int E = FE::kE;
   extern __shared__ __align__(128) uint8_t dyn_smem[];
   FusedSmem& S = *reinterpret_cast<FusedSmem*>(dyn_smem);
   uint8_t* bufs = dyn_smem + ((sizeof(FusedSmem) + 127) / 128) * 128;
@@ -265,13 +323,20 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int64_t V = p.V;
-  const uint32_t row_bytes = static_cast<uint32_t>(V * 2);
+  const int64_t row_bytes = V * static_cast<int64_t>(sizeof(TE));
+  const int nvec_row = static_cast<int>(row_bytes / 16);
   const int64_t G = gridDim.x;
   const int nloc = (p.R > blockIdx.x) ? static_cast<int>((p.R - blockIdx.x + G - 1) / G) : 0;
-  const int nops = write_dl ? 2 * nloc : nloc;
-  const int L = write_dl ? lag : 1 << 30;  // forward-only: A ops only
+  const int nvr = nloc * P;                       // virtual rows (pieces) of this CTA
+  const int nops = write_dl ? 2 * nvr : nvr;
+  const int L = write_dl ? lag : 1 << 30;         // lag in pieces; forward-only: A ops only
   auto row_of = [&](int k) { return static_cast<int64_t>(blockIdx.x) + k * G; };
   auto buf = [&](int s) { return bufs + static_cast<size_t>(s) * stage_bytes; };
+  // granules [piece * piece_vec, piece * piece_vec + piece_len(piece)) of a row
+  auto piece_len = [&](int piece) {
+    const int lo = piece * piece_vec;
+    return (nvec_row - lo < piece_vec) ? nvec_row - lo : piece_vec;
+  };
   const int64_t T = p.T;
   unsigned long long* dbg = g_dbg;
   const long long t_kernel = dbg ? clock64() : 0;
@@ -293,8 +358,8 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   }
   __syncthreads();
 
-  const __nv_bfloat16* logits = static_cast<const __nv_bfloat16*>(p.logits);
-  __nv_bfloat16* dl = static_cast<__nv_bfloat16*>(p.dlogits);
+  const uint8_t* logits = static_cast<const uint8_t*>(p.logits);
+  uint8_t* dl = static_cast<uint8_t*>(p.dlogits);
 
   // --------------------------------------------------------- loader warp
   if (warp == kWarpLoader) {
@@ -308,35 +373,40 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
           DBG_ADD(8);
         }
         bool isB;
-        int k;
-        op_of(n, nloc, L, &isB, &k);
-        mbar_arrive_expect_tx(&S.full[s], row_bytes);
-        if (isB)  // second (last) read of the row: from L2, then evict
-          tma_load_1d_evict_first(buf(s), logits + row_of(k) * V, row_bytes, &S.full[s], pol);
+        int u;
+        op_of(n, nvr, L, &isB, &u);
+        const int piece = u % P;
+        const uint32_t bytes = static_cast<uint32_t>(piece_len(piece)) * 16u;
+        const uint8_t* src = logits + row_of(u / P) * row_bytes + int64_t{16} * piece * piece_vec;
+        mbar_arrive_expect_tx(&S.full[s], bytes);
+        if (isB)  // second (last) read of the piece: from L2, then evict
+          tma_load_1d_evict_first(buf(s), src, bytes, &S.full[s], pol);
         else  // (an evict_last hint here measured no better: the lag keeps rows in L2)
-          tma_load_1d(buf(s), logits + row_of(k) * V, row_bytes, &S.full[s]);
+          tma_load_1d(buf(s), src, bytes, &S.full[s]);
       }
     }
     return;
   }
 
   // ---------------------------------------------------------- store warp
-  // B rows are written in place in SMEM and streamed out with one bulk copy
-  // each; the stage returns to the loader once the copy has read it.
+  // B pieces are written in place in SMEM and streamed out with one bulk
+  // copy each; the stage returns to the loader once the copy has read it.
   if (warp == kWarpStore) {
     if (!write_dl || lane != 0) return;
     int nb = 0;
     const uint64_t pol_ef = l2_policy_evict_first();
     for (int n = 0; n < nops; ++n) {
       bool isB;
-      int k;
-      op_of(n, nloc, L, &isB, &k);
+      int u;
+      op_of(n, nvr, L, &isB, &u);
       if (!isB) continue;
       const int s = static_cast<int>(n % kFusedStages);
       mbar_wait(&S.bdone[nb % kFusedStages], static_cast<uint32_t>((nb / kFusedStages) & 1));
       ++nb;
+      const int piece = u % P;
       // dlogits are not re-read here: keep L2 for the rows B still needs
-      tma_store_1d_evict_first(dl + row_of(k) * V, buf(s), row_bytes, pol_ef);
+      tma_store_1d_evict_first(dl + row_of(u / P) * row_bytes + int64_t{16} * piece * piece_vec,
+                               buf(s), static_cast<uint32_t>(piece_len(piece)) * 16u, pol_ef);
       bulk_commit();
       bulk_wait_read<0>();
       mbar_arrive_cnt(&S.empty[s], kFusedComputeWarps);
@@ -346,28 +416,45 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   }
 
   // ----------------------------------------------------------- tail warp
-  // Turns every A row's per-warp partials into lse (f64) and lp_tok, hands
-  // lp_tok to the publisher (other CTAs' chunks wait for it, so this warp
+  // Turns every row's per-warp (and per-piece) partials into lse (f64) and
+  // lp_tok, publishes lp_tok (other CTAs' chunks wait for it, so this warp
   // never waits on anything but its own compute warps) and leaves (lse,
   // target) in the ring for the prep warp.
   if (warp == kTailWarp) {
     for (int k = 0; k < nloc; ++k) {
-      const int sa = static_cast<int>(k % kASlots);
       const int64_t r = row_of(k);
-      mbar_wait(&S.adoneA[sa], static_cast<uint32_t>((k / kASlots) & 1));
-      const int32_t tgt = S.tgta[sa];
-      const float xt_f = S.xt[sa];
-      const float mw = (lane < kFusedComputeWarps) ? S.wm[sa][lane] : -INFINITY;
-      const double sw = (lane < kFusedComputeWarps) ? S.ws[sa][lane] : 0.0;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.afree[sa]);  // partial slot sa consumed
+      float mw[P];
+      double sw[P];
+      int32_t tgt = -1;
+      float xt_f = __int_as_float(0x7fc00000);
+#pragma unroll
+      for (int pc = 0; pc < P; ++pc) {
+        const int u = k * P + pc;
+        const int sa = u % kASlots;
+        mbar_wait(&S.adoneA[sa], static_cast<uint32_t>((u / kASlots) & 1));
+        tgt = S.tgta[sa];
+        const float x = S.xt[sa];
+        if (!isnan(x)) xt_f = x;  // the piece that holds the target column
+        mw[pc] = (lane < kFusedComputeWarps) ? S.wm[sa][lane] : -INFINITY;
+        sw[pc] = (lane < kFusedComputeWarps) ? S.ws[sa][lane] : 0.0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.afree[sa]);  // partial slot sa consumed
+      }
       // a NaN partial (NaN logit) or a +inf frame (+inf logit) poisons the row
-      const bool poison = __any_sync(0xffffffffu, lane < kFusedComputeWarps &&
-                                                      (isnan(sw) || mw == INFINITY));
-      const float M = warp_max_f32((lane < kFusedComputeWarps && sw > 0.0) ? mw : -INFINITY);
-      double term = (lane < kFusedComputeWarps && sw > 0.0)
-                        ? sw * static_cast<double>(ex2f((mw - M) * kLog2e))
-                        : 0.0;
+      bool bad = false;
+      float mlane = -INFINITY;
+#pragma unroll
+      for (int pc = 0; pc < P; ++pc) {
+        bad |= lane < kFusedComputeWarps && (isnan(sw[pc]) || mw[pc] == INFINITY);
+        if (lane < kFusedComputeWarps && sw[pc] > 0.0) mlane = fmaxf(mlane, mw[pc]);
+      }
+      const bool poison = __any_sync(0xffffffffu, bad);
+      const float M = warp_max_f32(mlane);
+      double term = 0.0;
+#pragma unroll
+      for (int pc = 0; pc < P; ++pc)
+        if (lane < kFusedComputeWarps && sw[pc] > 0.0)
+          term += sw[pc] * static_cast<double>(ex2f((mw[pc] - M) * kLog2e));
       term = warp_sum_f64(term);
       if (lane == 0) {
         const double lse =
@@ -392,20 +479,19 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
   }
 
   // ----------------------------------------------------------- prep warp
-  // For each B row in order: wait until the row's chunk is complete on all
-  // CTAs (acquire on its counter; L rounds after A, normally long done),
-  // sum its T published token log-probs (numpy pairwise order), evaluate
+  // For each row in order: wait until the row's chunk is complete on all
+  // CTAs (its T published token log-probs are no longer pending; L rounds
+  // after A, normally long done), sum them (numpy pairwise order), evaluate
   // rho, the clipped surrogate and the coefficient (every CTA computes the
-  // same value from the same inputs) and hand them to the compute warps.
+  // same value from the same inputs) and hand them to the compute warps,
+  // once per piece of the row.
   if (warp == kPrepWarp) {
     if (!write_dl) return;
     const uint64_t t_start = globaltimer_ns();
     for (int k = 0; k < nloc; ++k) {
-      const int sb = static_cast<int>(k % kFusedStages);
       const int64_t r = row_of(k);
       const int64_t q = r / T;
-      // poll the chunk's T published token log-probs (2 per lane at most
-      // 4 deep) until none is pending any more
+      // poll the chunk's T published token log-probs (at most 4 per lane)
       double pv[4];
       const double* lt = p.lp_tok + q * T;
       uint32_t spins = 0;
@@ -428,8 +514,8 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
       const double padv = __ldg(p.adv + q / p.C);
       const double lp = warp_pairwise_small(pv, static_cast<int>(T), lane);
       mbar_wait(&S.tdone[k % kRing], static_cast<uint32_t>((k / kRing) & 1));  // own tail
-      if (k >= kFusedStages)  // coefficient slot sb consumed by the compute warps
-        mbar_wait(&S.adoneB[sb], static_cast<uint32_t>(((k - kFusedStages) / kFusedStages) & 1));
+      uint32_t mode = 0u;
+      float kval = 0.f, cf = 0.f;
       if (lane == 0) {
         ChunkTerms ct = chunk_terms(lp, static_cast<double>(pblp), padv, p.w, p.clip_eps,
                                     p.kl_coeff);
@@ -439,105 +525,101 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
           p.coeff[q] = cc;
         }
         const double lse = S.ring_lse[k % kRing];
-        uint32_t mode;
         if (cc == 0.0) {
           mode = 0u;
         } else if (!isfinite(cc)) {
           mode = 2u;
         } else {
           mode = 1u | ((cc > 0.0) ? 0x80000000u : 0u);
-          S.kval[sb] = static_cast<float>(lse * 1.4426950408889634 - log2(fabs(cc)));
+          kval = static_cast<float>(lse * 1.4426950408889634 - log2(fabs(cc)));
         }
-        S.mode[sb] = mode;
-        S.cf[sb] = static_cast<float>(cc);
-        S.lseL[sb] = static_cast<float>(lse * 1.4426950408889634);
-        S.tgt[sb] = S.ring_tgt[k % kRing];
-        mbar_arrive(&S.cfullB[sb]);
+        cf = static_cast<float>(cc);
       }
-      __syncwarp();
+      const float lseL = static_cast<float>(S.ring_lse[k % kRing] * 1.4426950408889634);
+      const int32_t tgt = S.ring_tgt[k % kRing];
+#pragma unroll
+      for (int pc = 0; pc < P; ++pc) {
+        const int u = k * P + pc;
+        const int sb = u % kFusedStages;
+        if (u >= kFusedStages)  // coefficient slot sb consumed by the compute warps
+          mbar_wait(&S.adoneB[sb], static_cast<uint32_t>(((u - kFusedStages) / kFusedStages) & 1));
+        if (lane == 0) {
+          S.mode[sb] = mode;
+          S.kval[sb] = kval;
+          S.cf[sb] = cf;
+          S.lseL[sb] = lseL;
+          S.tgt[sb] = tgt;
+          mbar_arrive(&S.cfullB[sb]);
+        }
+        __syncwarp();
+      }
     }
     return;
   }
 
   // ------------------------------------------------------- compute warps
-  const int nvec = static_cast<int>(V >> 3);  // uint4 = 8 bf16
-  int a = 0, b = 0;  // A / B op counters
+  int a = 0, b = 0;  // A / B op counters (virtual rows)
+  const uint64_t l2e2 = f2pack(kLog2e, kLog2e);
   for (int n = 0; n < nops; ++n) {
     const int s = static_cast<int>(n % kFusedStages);
     const uint32_t ph = static_cast<uint32_t>((n / kFusedStages) & 1);
     bool isB;
-    int k;
-    op_of(n, nloc, L, &isB, &k);
+    int u;
+    op_of(n, nvr, L, &isB, &u);
+    const int piece = u % P;
+    const int nvec = piece_len(piece);
+    const int elem0 = piece * piece_vec * E;  // first element of this piece in its row
     {
       DBG_T0();
       mbar_wait(&S.full[s], ph);
       if (tid == 0) { DBG_ADD(0); }
     }
     if (!isB) {
-      const int32_t tg = (tid == 0) ? __ldg(p.tokens + row_of(k)) : 0;  // used at the end
+      const int32_t tg = (tid == 0) ? __ldg(p.tokens + row_of(u / P)) : 0;  // used at the end
       // One pass: exponentials in the fixed frame 2^(x log2e) (no max
-      // subtraction) with the packed max alongside.  The frame is exact
-      // enough when the warp max lies in [kFrameLo, kFrameHi] (no f32
-      // overflow of <= 8 terms per accumulator; terms flushed below 2^-126
-      // are < e^-37 of the max); otherwise (rare: huge or very negative
-      // logits) the warp redoes its slice relative to its own max.  The tail
-      // combines (frame, sum) pairs of all warps.
+      // subtraction) with the max alongside.  The frame is exact enough when
+      // the warp max lies in [kFrameLo, kFrameHi] (no f32 overflow of <= 8
+      // terms per accumulator; terms flushed below 2^-126 are < e^-37 of the
+      // max); otherwise (rare: huge or very negative logits) the warp redoes
+      // its slice relative to its own max.  The tail combines (frame, sum)
+      // pairs of all warps and pieces.
       const uint4* v = reinterpret_cast<const uint4*>(buf(s));
-      uint32_t mx0 = 0xff80ff80u, mx1 = 0xff80ff80u;
-      const uint64_t l2e2 = f2pack(kLog2e, kLog2e);
-      uint64_t s01 = 0, s23 = 0, s45 = 0, s67 = 0;  // packed (0.f, 0.f)
-      auto ex2_pair = [&](uint32_t w, uint64_t off2) {
-        float y0, y1;
-        f2unpack(bf16x2_fma2(w, l2e2, off2), y0, y1);
-        return f2pack(ex2f(y0), ex2f(y1));
-      };
+      uint32_t mx = FE::kNegInf;
+      uint64_t acc[4] = {0, 0, 0, 0};  // packed (0.f, 0.f)
 #pragma unroll 2
       for (int i = tid; i < nvec; i += kFusedComputeThreads) {
         const uint4 x = v[i];
-        mx0 = bf16x2_max(mx0, bf16x2_max(x.x, x.y));
-        mx1 = bf16x2_max(mx1, bf16x2_max(x.z, x.w));
-        s01 = fadd2(s01, ex2_pair(x.x, 0));
-        s23 = fadd2(s23, ex2_pair(x.y, 0));
-        s45 = fadd2(s45, ex2_pair(x.z, 0));
-        s67 = fadd2(s67, ex2_pair(x.w, 0));
+        mx = FE::max16(mx, x);
+        FE::exps(x, l2e2, 0, acc);
       }
-      const uint32_t mx = bf16x2_max(mx0, mx1);
-      const float wmax = warp_max_f32(fmaxf(bf16lo(mx), bf16hi(mx)));
+      const float wmax = warp_max_f32(FE::maxf(mx));
       float m = 0.f;  // frame of this warp's partial
       if (!(wmax <= kFrameHi) || (wmax < kFrameLo && wmax > -INFINITY)) {  // warp-uniform
         m = wmax;
         const float mL = m * kLog2e;
         const uint64_t nmL2 = f2pack(-mL, -mL);
-        s01 = s23 = s45 = s67 = 0;
+        acc[0] = acc[1] = acc[2] = acc[3] = 0;
 #pragma unroll 2
-        for (int i = tid; i < nvec; i += kFusedComputeThreads) {
-          const uint4 x = v[i];
-          s01 = fadd2(s01, ex2_pair(x.x, nmL2));
-          s23 = fadd2(s23, ex2_pair(x.y, nmL2));
-          s45 = fadd2(s45, ex2_pair(x.z, nmL2));
-          s67 = fadd2(s67, ex2_pair(x.w, nmL2));
-        }
+        for (int i = tid; i < nvec; i += kFusedComputeThreads) FE::exps(v[i], l2e2, nmL2, acc);
       }
-      float s0, s1, s2, s3;
+      double part;
       {
-        float a, b;
-        f2unpack(fadd2(s01, s23), a, b);
-        s0 = a; s1 = b;
-        f2unpack(fadd2(s45, s67), a, b);
-        s2 = a; s3 = b;
+        float a0, a1, a2, a3;
+        f2unpack(fadd2(acc[0], acc[1]), a0, a1);
+        f2unpack(fadd2(acc[2], acc[3]), a2, a3);
+        part = (static_cast<double>(a0) + static_cast<double>(a1)) +
+               (static_cast<double>(a2) + static_cast<double>(a3));
       }
-      // gather the target logit while the row is in SMEM, then free the stage
+      // gather the target logit while the piece is in SMEM, then free the stage
       const bool tok_ok = tg >= 0 && tg < V;
-      const float xt_v = (tid == 0 && tok_ok)
-                             ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(buf(s))[tg])
-                             : __int_as_float(0x7fc00000);
+      const int li = tg - elem0;
+      const bool here = tok_ok && li >= 0 && li < nvec * E;
+      const float xt_v = (tid == 0 && here) ? FE::get(buf(s), li) : __int_as_float(0x7fc00000);
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[s]);
-      double part = (static_cast<double>(s0) + static_cast<double>(s1)) +
-                    (static_cast<double>(s2) + static_cast<double>(s3));
       part = warp_sum_f64(part);
       const int sa = static_cast<int>(a % kASlots);
-      if (a >= kASlots) {  // the coefficient warp has read A row a-8's partials
+      if (a >= kASlots) {  // the tail warp has read A piece a-8's partials
         DBG_T0();
         mbar_wait(&S.afree[sa], static_cast<uint32_t>(((a - kASlots) / kASlots) & 1));
         if (tid == 0) { DBG_ADD(3); }
@@ -562,25 +644,28 @@ __global__ void __launch_bounds__(kFusedThreadsWS, 1)
     }
     ++b;
     const uint32_t mode = S.mode[sb];
-    uint4* v = reinterpret_cast<uint4*>(buf(s));  // dlogits overwrite the row in place
+    uint4* v = reinterpret_cast<uint4*>(buf(s));  // dlogits overwrite the piece in place
     if ((mode & 3u) != 1u) {
       // zero-gradient rows (A == 0 or clipped chunk): 0 * (onehot - p)
-      const uint32_t z = (mode == 0u) ? 0u : 0x7fc07fc0u;
+      const uint32_t z = (mode == 0u) ? 0u : FE::kNaN;
       for (int i = tid; i < nvec; i += kFusedComputeThreads) v[i] = make_uint4(z, z, z, z);
     } else {
       // target column: c * (1 - p_t), patched by the thread that owns it
-      const int32_t tgt = S.tgt[sb];
-      const bool owner = tid == ((tgt >> 3) % kFusedComputeThreads);
-      __nv_bfloat16* row = reinterpret_cast<__nv_bfloat16*>(v);
+      const int li = S.tgt[sb] - elem0;
+      const bool here = li >= 0 && li < nvec * E;
+      const bool owner = here && tid == ((li / E) % kFusedComputeThreads);
       float val = 0.f;
       if (owner) {
-        const float pt = ex2f(fmaf(__bfloat162float(row[tgt]), kLog2e, -S.lseL[sb]));
+        const float pt = ex2f(fmaf(FE::get(v, li), kLog2e, -S.lseL[sb]));
         val = S.cf[sb] * (1.0f - pt);
       }
       // -c * p_v = -sign(c) * 2^(x*log2e - (lse*log2e - log2|c|))
       const float K = S.kval[sb];
-      b_row(v, nvec, tid, K, (mode & 0x80000000u) ? 0x80008000u : 0u);
-      if (owner) row[tgt] = __float2bfloat16_rn(val);
+      const uint64_t nK2 = f2pack(-K, -K);
+      const uint32_t sgn = (mode & 0x80000000u) ? FE::kSign : 0u;
+#pragma unroll 2
+      for (int i = tid; i < nvec; i += kFusedComputeThreads) v[i] = FE::grad(v[i], l2e2, nK2, sgn);
+      if (owner) FE::put(v, li, val);
     }
     fence_proxy_async_smem();  // generic SMEM writes -> visible to the bulk store
     __syncwarp();
@@ -901,10 +986,42 @@ static TokWorkspace carve(void* base, int64_t n_groups, int64_t G, int64_t C, in
   return w;
 }
 
-static size_t fused_smem_bytes(int64_t V) {
+// Stage geometry of the fused kernel: the fewest pieces per row (1, 2 or 4)
+// whose stage fits three times in SMEM next to the header.
+struct FusedGeom {
+  int pieces = 0;      // 0: does not fit
+  int piece_vec = 0;   // 16-byte granules per piece
+  uint32_t stage_bytes = 0;
+  size_t smem = 0;
+};
+
+static FusedGeom fused_geom(int64_t V, size_t esz) {
+  FusedGeom g;
+  const int64_t nvec_row = V * static_cast<int64_t>(esz) / 16;
   const size_t hdr = ((sizeof(FusedSmem) + 127) / 128) * 128;
-  const size_t stage = ((static_cast<size_t>(V) * 2 + 127) / 128) * 128;
-  return hdr + kFusedStages * stage;
+  for (int P : {1, 2, 4}) {
+    const int64_t pv = (nvec_row + P - 1) / P;
+    const size_t stage = ((static_cast<size_t>(pv) * 16 + 127) / 128) * 128;
+    if (hdr + kFusedStages * stage <= 227 * 1024) {
+      g.pieces = P;
+      g.piece_vec = static_cast<int>(pv);
+      g.stage_bytes = static_cast<uint32_t>(stage);
+      g.smem = hdr + kFusedStages * stage;
+      return g;
+    }
+  }
+  return g;
+}
+
+using FusedKernelFn = void (*)(TokParams, uint32_t, int, int, int);
+
+template <class TE>
+static FusedKernelFn fused_kernel_for(int pieces) {
+  switch (pieces) {
+    case 1: return tok_fused_kernel<TE, 1>;
+    case 2: return tok_fused_kernel<TE, 2>;
+    default: return tok_fused_kernel<TE, 4>;
+  }
 }
 
 }  // namespace dvla
@@ -979,30 +1096,34 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
   const bool aligned16 = (reinterpret_cast<uintptr_t>(logits) % 16 == 0) &&
                          (!want_dl || reinterpret_cast<uintptr_t>(dlogits) % 16 == 0) &&
                          ((V * esz) % 16 == 0);
-  const size_t fsmem = fused_smem_bytes(V);
-  const bool fused = !(flags & DVLA_TL_UNFUSED) && dtype == DVLA_BF16 && aligned16 &&
-                     fsmem <= 227 * 1024 && T <= sms && T <= 128 && R >= 1 &&
-                     R < (int64_t{1} << 31);
+  const FusedGeom geom = fused_geom(V, esz);
+  const bool fused = !(flags & DVLA_TL_UNFUSED) && aligned16 && geom.pieces > 0 && T <= sms &&
+                     T <= 128 && R >= 1 && R < (int64_t{1} << 31);
   if (fused) {
-    static bool attr_set[64] = {false};
-    if (!attr_set[dev & 63]) {
-      DVLA_CUDA_TRY(cudaFuncSetAttribute(tok_fused_bf16_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const FusedKernelFn kern = dtype == DVLA_BF16 ? fused_kernel_for<__nv_bfloat16>(geom.pieces)
+                                                  : fused_kernel_for<float>(geom.pieces);
+    static bool attr_set[64][2][3] = {};
+    bool& set = attr_set[dev & 63][dtype == DVLA_BF16 ? 0 : 1][geom.pieces >> 1];
+    if (!set) {
+      DVLA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024));
-      attr_set[dev & 63] = true;
+      set = true;
     }
     const unsigned grid = static_cast<unsigned>(R < sms ? R : sms);
-    const uint32_t stage_bytes = static_cast<uint32_t>(((V * 2 + 127) / 128) * 128);
     cudaEvent_t stop;
     prof_begin(stream, &stop);
     static const int lag = [] {
       const char* e = getenv("DVLA_FUSED_LAG");
       return e ? atoi(e) : kLagRounds;
     }();
-    tok_fused_bf16_kernel<<<grid, kFusedThreadsWS, fsmem, stream>>>(
-        p, stage_bytes, want_dl ? 1 : 0, lag < 2 ? 2 : (lag > kMaxLag ? kMaxLag : lag));
+    // lag in pieces: >= 2P - 1 so a chunk's two rounds of tails precede its
+    // B ops (deadlock freedom), <= kRing P - 1 for the (lse, target) ring
+    const int P = geom.pieces;
+    const int lag_p = std::min(std::max(lag, 2 * P - 1), kRing * P - 1);
+    kern<<<grid, kFusedThreadsWS, geom.smem, stream>>>(p, geom.stage_bytes, geom.piece_vec,
+                                                       want_dl ? 1 : 0, std::max(lag_p, 2));
     prof_end(stream, stop);
-    if (int rc = launch_check("tok_fused_bf16_kernel")) return rc;
+    if (int rc = launch_check("tok_fused_kernel")) return rc;
     if (!want_dl) {
       tok_chunk_kernel<<<(unsigned)((nq * 32 + 255) / 256), 256, 0, stream>>>(p);
       if (int rc = launch_check("tok_chunk_kernel")) return rc;

@@ -41,7 +41,7 @@ class Bar:
         return (self.phase & 1) != (idx & 1)
 
 
-def simulate(nloc, L, seed, write_dl=True, W=4):
+def simulate(nloc, L, seed, write_dl=True, W=4, P=1):
     """Roles as generators (v10 protocol): the loader streams every op's row
     into a 3-stage SMEM ring; compute warps free an A stage as soon as they
     have read it, write B rows in place and hand them to the store warp
@@ -51,11 +51,15 @@ def simulate(nloc, L, seed, write_dl=True, W=4):
     8-row ring for the prep warp (tdone); B coefficients go through a 3-slot
     ring guarded by adoneB.  The prep warp's wait for the chunk to complete
     on all CTAs is modelled by waiting for this CTA's own tails of rows k and
-    k + 1 (a chunk spans at most two consecutive rounds when T <= grid)."""
+    k + 1 (a chunk spans at most two consecutive rounds when T <= grid).
+    With P pieces per row, ops walk virtual rows u = k P + p (lag L P); the
+    tail consumes the P partial slots of a row, the prep hands the row's
+    coefficient to each of its P B ops."""
     AS, RING = 8, 8
     rnd = random.Random(seed)
-    nops = 2 * nloc if write_dl else nloc
-    Lx = L if write_dl else 1 << 30
+    nvr = nloc * P
+    nops = 2 * nvr if write_dl else nvr
+    Lx = L if write_dl else 1 << 30  # lag in pieces (>= 2P - 1, <= 8P - 1)
     full = [Bar(1) for _ in range(S)]
     empty = [Bar(W) for _ in range(S)]
     ad_a = [Bar(W) for _ in range(AS)]
@@ -85,9 +89,11 @@ def simulate(nloc, L, seed, write_dl=True, W=4):
 
     def tail():
         for k in range(nloc):
-            yield from wait(ad_a[k % AS], k // AS)
-            assert slot_p[k % AS] == k
-            a_free[k % AS].arrive()
+            for pc in range(P):
+                u = k * P + pc
+                yield from wait(ad_a[u % AS], u // AS)
+                assert slot_p[u % AS] == u
+                a_free[u % AS].arrive()
             if write_dl:
                 assert k < RING or (k - RING) in ring_read, "(lse, target) ring overrun"
                 ring[k % RING] = k
@@ -103,17 +109,19 @@ def simulate(nloc, L, seed, write_dl=True, W=4):
             yield from wait(tdone[k % RING], k // RING)
             assert ring[k % RING] == k
             ring_read.add(k)
-            if k >= S:
-                yield from wait(ad_b[k % S], (k - S) // S)
-            slot_c[k % S] = k
-            cf_b[k % S].arrive()
+            for pc in range(P):
+                u = k * P + pc
+                if u >= S:
+                    yield from wait(ad_b[u % S], (u - S) // S)
+                slot_c[u % S] = u
+                cf_b[u % S].arrive()
 
     def store():
         if not write_dl:
             return
         nb = 0
         for n in range(nops):
-            isb, k = op_of(n, nloc, Lx)
+            isb, k = op_of(n, nvr, Lx)
             if not isb:
                 continue
             yield from wait(bdone[nb % S], nb // S)
@@ -126,7 +134,7 @@ def simulate(nloc, L, seed, write_dl=True, W=4):
     def compute(w):
         a = b = 0
         for n in range(nops):
-            isb, k = op_of(n, nloc, Lx)
+            isb, k = op_of(n, nvr, Lx)
             yield from wait(full[n % S], n // S)
             assert stage_op[n % S] == n
             if not isb:
@@ -162,7 +170,7 @@ def simulate(nloc, L, seed, write_dl=True, W=4):
             live.remove(g)
     assert not live, "protocol deadlocked"
     if write_dl:
-        assert sorted(rows_b) == list(range(nloc))
+        assert sorted(rows_b) == list(range(nvr))
 
 
 @pytest.mark.parametrize("nloc", [1, 2, 3, 4, 7, 13, 20])
@@ -170,6 +178,15 @@ def simulate(nloc, L, seed, write_dl=True, W=4):
 def test_protocol_completes_without_aliasing(nloc, L):
     for seed in range(3):
         simulate(nloc, L, seed)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("nloc", [1, 2, 5, 11])
+@pytest.mark.parametrize("lag", ["min", "mid", "max"])
+def test_protocol_with_row_pieces(P, nloc, lag):
+    L = {"min": 2 * P - 1, "mid": 4 * P, "max": 8 * P - 1}[lag]
+    for seed in range(2):
+        simulate(nloc, L, seed, P=P)
 
 
 def test_forward_only_protocol():

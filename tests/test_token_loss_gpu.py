@@ -79,7 +79,7 @@ def test_f32_unfused_odd_vocab_matches_oracle():
 def test_f32_vectorised_rows_match_oracle():
     import torch
     case = _case(1, 2, 4, 2, 5, 1024, torch.float32, binary=False)
-    _check(*case, torch.float32, fused=True, rtol=1e-5)   # f32 takes the unfused kernels
+    _check(*case, torch.float32, fused=True, rtol=1e-5)   # fused f32, one piece per row
 
 
 def test_bf16_fused_matches_oracle():
@@ -252,6 +252,29 @@ def test_f32_openvla_vocab_matches_oracle():
     import torch
     case = _case(13, 2, 4, 1, 8, 32064, torch.float32, binary=False)
     _check(*case, torch.float32, fused=True, rtol=1e-5)
+
+
+@pytest.mark.parametrize("dtype_name,V", [("float32", 32064), ("bfloat16", 65536),
+                                          ("bfloat16", 128256)])
+def test_fused_rows_split_into_pieces_match_oracle(dtype_name, V):
+    """Rows longer than one SMEM stage stream as 2 or 4 pieces (f32 at the
+    C2 vocabulary; bf16 at 64K / Llama-3's 128,256): the tail warp combines
+    the pieces' partials, the target may sit in any piece."""
+    import torch
+    dtype = getattr(torch, dtype_name)
+    x, tokens, blp, rewards, ids = _case(21, 2, 4, 2, 6, V, dtype, binary=False)
+    tokens[0, 0, 0, :] = [0, V // 2 - 1, V // 2, V - 1, V // 4, 3 * V // 4]  # piece edges
+    _, _, st0 = O.grpo_token_grad(x, tokens, np.zeros(blp.shape, np.float32),
+                                  np.tile(np.arange(4, dtype=np.float32), (2, 1)),
+                                  np.arange(2), want_dlogits=False)
+    blp = (st0["lp_chunk"] + 0.02).astype(np.float32)
+    case = (x, tokens, blp, rewards, ids)
+    rtol = 1e-5 if dtype == torch.float32 else 1e-2
+    _check(*case, dtype, fused=True, rtol=rtol)
+    la, _, sa = _run_gpu(*case, dtype, fused=True)
+    lb, _, sb = _run_gpu(*case, dtype, fused=False)
+    np.testing.assert_allclose(sa["lp_chunk"].cpu().numpy(), sb["lp_chunk"].cpu().numpy(),
+                               rtol=1e-9, atol=1e-5)
 
 
 def test_misaligned_logits_take_the_scalar_path():
