@@ -102,6 +102,17 @@ def _hops(specs):
     return arr
 
 
+def _gather_by_rank(obj, group):
+    """all_gather_object over `group` (default: world), returned as a dict
+    global rank -> object."""
+    import torch.distributed as dist
+    ranks = (list(range(dist.get_world_size())) if group is None
+             else dist.get_process_group_ranks(group))
+    out = [None] * len(ranks)
+    dist.all_gather_object(out, obj, group=group)
+    return dict(zip(ranks, out))
+
+
 class _Slab:
     """Device slab (cudaMalloc) + torch view; IPC-shareable."""
 
@@ -230,8 +241,7 @@ class ChainReplicator:
             self.flags.t.zero_()
             torch.cuda.synchronize()
             handles = (self.buf.ipc(), self.flags.ipc())
-        allh = [None] * world
-        dist.all_gather_object(allh, handles, group=group)
+        allh = _gather_by_rank(handles, group)
         self.next_buf = self.next_flags = None
         if 0 <= self.pos < len(self.ranks) - 1:
             nxt = self.ranks[self.pos + 1]
@@ -341,7 +351,6 @@ class _McRegion:
         from . import _lib
         torch = _torch()
         self.rank = dist.get_rank()
-        world = dist.get_world_size()
         self.ranks = list(ranks)
         self.pos = self.ranks.index(self.rank) if self.rank in self.ranks else -1
         self.dev = torch.cuda.current_device()
@@ -354,8 +363,7 @@ class _McRegion:
                        "dvla_mc_create")
             self.obj = obj.value
             info = (os.getpid(), fd.value, size.value)
-        allinfo = [None] * world
-        dist.all_gather_object(allinfo, info, group=group)
+        allinfo = _gather_by_rank(info, group)
         pid, fd, size = allinfo[self.ranks[0]]
         self.size = size
         if self.pos > 0:
@@ -503,3 +511,96 @@ class McAllReduce:
     def close(self):
         self.buf = None
         self.region.close()
+
+
+class SplitReplicator:
+    """Several learners source one weight region (BASELINE config 3: two
+    learners, six replicas): part i of the region (1/len(chains) of it) flows
+    along chains[i], whose head holds the full source and sends only part i,
+    so every receiver takes in parts over several links at once.  Every rank
+    of the union of the chains constructs it and calls `broadcast`; each
+    rank's hops run in one kernel launch (one CTA group per hop)."""
+
+    def __init__(self, nbytes: int, chains, n_buffers: int = 2, chunk_bytes=None,
+                 ctas_per_hop: int = 64, group=None):
+        import torch.distributed as dist
+        torch = _torch()
+        parts = len(chains)
+        if parts < 1 or nbytes % (16 * parts):
+            raise UsageError("the region must split into 16-byte-aligned equal parts")
+        self.rank = dist.get_rank()
+        self.chains = [list(c) for c in chains]
+        self.nbytes, self.parts, self.nb = int(nbytes), parts, int(n_buffers)
+        self.part = self.nbytes // parts
+        self.ctas = int(ctas_per_hop)
+        self.chunk = int(chunk_bytes) if chunk_bytes else chain_chunk_bytes(self.part, self.ctas)
+        self.n_chunks = (self.part + self.chunk - 1) // self.chunk
+        receivers = sorted({r for c in self.chains for r in c[1:]})
+        self.err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.buf = self.flags = None
+        handles = None
+        if self.rank in receivers:
+            self.buf = _Slab(self.nb * self.nbytes, torch.cuda.current_device())
+            fb = ((self.nb * parts * self.n_chunks * 4 + 255) // 256) * 256
+            self.flags = _Slab(fb, torch.cuda.current_device())
+            self.flags.t.zero_()
+            torch.cuda.synchronize()
+            handles = (self.buf.ipc(), self.flags.ipc())
+        allh = _gather_by_rank(handles, group)
+        self.peer = {}
+        for c in self.chains:
+            if self.rank in c and c.index(self.rank) < len(c) - 1:
+                nxt = c[c.index(self.rank) + 1]
+                if nxt not in self.peer:
+                    self.peer[nxt] = (_open_ipc(allh[nxt][0]), _open_ipc(allh[nxt][1]))
+
+    def _flag_off(self, b: int, c: int) -> int:
+        return (b * self.parts + c) * self.n_chunks * 4
+
+    def replica(self, version: int):
+        if self.buf is None:
+            raise UsageError("this rank holds no replica region")
+        b = version % self.nb
+        return self.buf.t[b * self.nbytes:(b + 1) * self.nbytes]
+
+    def broadcast(self, src, version: int, stream=None, timeout_s: float = 30.0):
+        from . import _lib
+        b = version % self.nb
+        epoch = version + 1
+        specs = []
+        for c, chain in enumerate(self.chains):
+            if self.rank not in chain:
+                continue
+            pos = chain.index(self.rank)
+            off = c * self.part
+            if pos == 0:
+                if src is None or src.numel() * src.element_size() != self.nbytes:
+                    raise UsageError("a chain head needs the full source region")
+                s_ptr, wait = src.data_ptr() + off, None
+            else:
+                s_ptr = self.buf.ptr + b * self.nbytes + off
+                wait = self.flags.ptr + self._flag_off(b, c)
+            if pos < len(chain) - 1:
+                nb_ptr, nf_ptr = self.peer[chain[pos + 1]]
+                specs.append((s_ptr, nb_ptr + b * self.nbytes + off, wait,
+                              nf_ptr + self._flag_off(b, c)))
+            else:
+                specs.append((None, None, wait, None))
+        if not specs:
+            return
+        _lib.check(_lib.dvla_replicate_chain(_hops(specs), len(specs), self.part, self.chunk,
+                                             epoch, self.ctas, int(timeout_s * 1e9),
+                                             self.err.data_ptr(), _stream_ptr(stream)),
+                   "dvla_replicate_chain")
+
+    def check(self):
+        if int(self.err.item()):
+            from ._lib import ReplicationTimeout
+            raise ReplicationTimeout(f"rank {self.rank}: split replication timed out")
+
+    def close(self):
+        from . import _lib
+        for bp, fp in self.peer.values():
+            _lib.dvla_ipc_close(bp)
+            _lib.dvla_ipc_close(fp)
+        self.peer = {}
