@@ -77,6 +77,26 @@ def main():
         if rank == 0:
             print("MC_ALLREDUCE_OK", flush=True)
 
+    # (1d) several sources, one region (C3 layout at 4 GPUs; two parts from
+    # rank 0 along the same pair at 2)
+    from paper_2605_13276_b200.replicate import SplitReplicator
+    chains = [[0, 2, 3], [1, 3, 2]] if world >= 4 else [[0, 1], [0, 1]]
+    srep = SplitReplicator(S - S % 32, chains, n_buffers=2, ctas_per_hop=16)
+    heads = {c[0] for c in chains}
+    receivers = {r for c in chains for r in c[1:]}
+    for v in (0, 1, 2):
+        src = torch.randint(0, 256, (S - S % 32,), dtype=torch.uint8, device="cuda",
+                            generator=torch.Generator(device="cuda").manual_seed(300 + v))
+        dist.barrier()
+        srep.broadcast(src if rank in heads else None, v)
+        torch.cuda.synchronize()
+        dist.barrier()
+        srep.check()
+        if rank in receivers:
+            assert bytes_equal(src, srep.replica(v)) == (0, -1), ("split", rank, v)
+    dist.barrier()
+    srep.close()
+
     # (2) gradient mean over NCCL, exact mode vs host arithmetic
     g = torch.full((1000,), float(rank + 1), dtype=torch.float64, device="cuda") / 3.0
     out = GradReducer(world, exact=True).reduce(g.clone())
