@@ -424,6 +424,44 @@ def _bench_sampler(dev, logits, steps=20):
             "launches_per_step": 2}
 
 
+def _bench_optimizer(dev, iters=10):
+    """Learner optimizer tail on the OpenVLA action-head size:
+    Adam (f32 params, f64 grad / moments: 44 B per parameter) and the
+    gradient norm, HBM-bound."""
+    import torch
+    from paper_2605_13276_b200 import _lib
+    n = V * 4096
+    p = torch.randn(n, device=dev)
+    g = torch.randn(n, device=dev, dtype=torch.float64) * 1e-3
+    m = torch.zeros(n, device=dev, dtype=torch.float64)
+    v = torch.zeros(n, device=dev, dtype=torch.float64)
+    ws = torch.empty(_lib.dvla_grad_norm_workspace_bytes(n), dtype=torch.uint8, device=dev)
+    norm = torch.zeros(1, dtype=torch.float64, device=dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    s = torch.cuda.current_stream().cuda_stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    peak, _ = _peaks()
+    out = {"params": n}
+    for name, fn, nbytes in (
+            ("adam", lambda it: _lib.dvla_adam_step(p.data_ptr(), g.data_ptr(), m.data_ptr(),
+                                                    v.data_ptr(), n, it + 1, 1e-4, 0.9, 0.999,
+                                                    1e-8, s), n * 44),
+            ("grad_norm", lambda it: _lib.dvla_grad_norm(g.data_ptr(), n, 0.0, norm.data_ptr(),
+                                                         bad.data_ptr(), ws.data_ptr(), s),
+             n * 8)):
+        for it in range(3):
+            fn(it)
+        torch.cuda.synchronize()
+        e0.record()
+        for it in range(iters):
+            fn(it)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        out[name] = {"ms": ms, "gbs": nbytes / ms / 1e6, "frac_of_hbm_peak": nbytes / ms / 1e6 / peak}
+    return out
+
+
 def _bench_allreduce(world, dev, barrier, max_over_ranks, nbytes=1 << 30, iters=5):
     """NCCL all-reduce of a learner gradient bucket (f32), busbw."""
     import torch
@@ -625,6 +663,7 @@ def run_ours(a):
     allreduce = _bench_allreduce(world, dev, barrier, max_over_ranks)
     gauss = None if a.no_gauss else _bench_gauss_c3(dev, rank, cpu=not a.no_cpu)
     sampler = None if a.no_gauss else _bench_sampler(dev, logits)
+    optimizer = None if a.no_gauss else _bench_optimizer(dev)
     swim = None
     if not a.no_swimlane:
         barrier()
@@ -653,7 +692,7 @@ def run_ours(a):
                        "l2": "inputs 1.84 GB/rank > 126 MB L2 (no flush needed)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "replication": repl, "grad_allreduce": allreduce, "swimlane": swim,
-            "gauss_c3": gauss, "sampler": sampler,
+            "gauss_c3": gauss, "sampler": sampler, "optimizer": optimizer,
             "gpu_launches": 3 * a.steps, "clocks": clk,
             "loss": st["loss"], "mean_ratio": st["mean_ratio"],
             "clip_fraction": st["clip_fraction"],

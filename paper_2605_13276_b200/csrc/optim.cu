@@ -9,43 +9,114 @@
 
 namespace dvla {
 
+struct AdamConsts {
+  double beta1, one_m_beta1, beta2, one_m_beta2, bc1, bc2, lr, eps;
+};
+
+// one element, the reference's arithmetic in its order (grpo.py:143-150)
+__device__ __forceinline__ float adam_elem(float p, double gi, double& m, double& v,
+                                           const AdamConsts& c) {
+  double mi = __dmul_rn(m, c.beta1);
+  mi = __dadd_rn(mi, __dmul_rn(c.one_m_beta1, gi));
+  double vi = __dmul_rn(v, c.beta2);
+  vi = __dadd_rn(vi, __dmul_rn(c.one_m_beta2, __dmul_rn(gi, gi)));
+  m = mi;
+  v = vi;
+  const double mh = __ddiv_rn(mi, c.bc1);
+  const double vh = __ddiv_rn(vi, c.bc2);
+  const double upd = __dsub_rn(static_cast<double>(p),
+                               __ddiv_rn(__dmul_rn(c.lr, mh), __dadd_rn(__dsqrt_rn(vh), c.eps)));
+  return __double2float_rn(upd);
+}
+
+// HBM-bound (44 bytes per parameter): pairs of elements per thread with
+// 8-/16-byte accesses, two pairs in flight; a scalar tail for odd n or
+// misaligned arrays.
 __global__ void adam_kernel(float* __restrict__ p, const double* __restrict__ g,
                             double* __restrict__ m, double* __restrict__ v, int64_t n,
-                            double beta1, double one_m_beta1, double beta2, double one_m_beta2,
-                            double bc1, double bc2, double lr, double eps) {
+                            AdamConsts c, int vec) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += stride) {
-    const double gi = g[i];
-    double mi = __dmul_rn(m[i], beta1);
-    mi = __dadd_rn(mi, __dmul_rn(one_m_beta1, gi));
-    double vi = __dmul_rn(v[i], beta2);
-    vi = __dadd_rn(vi, __dmul_rn(one_m_beta2, __dmul_rn(gi, gi)));
+  const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t npair = n / 2;
+    float2* p2 = reinterpret_cast<float2*>(p);
+    const double2* g2 = reinterpret_cast<const double2*>(g);
+    double2* m2 = reinterpret_cast<double2*>(m);
+    double2* v2 = reinterpret_cast<double2*>(v);
+    int64_t i = t0;
+    for (; i + stride < npair; i += 2 * stride) {
+      float2 pa = p2[i], pb = p2[i + stride];
+      const double2 ga = __ldcs(g2 + i), gb = __ldcs(g2 + i + stride);
+      double2 ma = m2[i], mb = m2[i + stride], va = v2[i], vb = v2[i + stride];
+      pa.x = adam_elem(pa.x, ga.x, ma.x, va.x, c);
+      pa.y = adam_elem(pa.y, ga.y, ma.y, va.y, c);
+      pb.x = adam_elem(pb.x, gb.x, mb.x, vb.x, c);
+      pb.y = adam_elem(pb.y, gb.y, mb.y, vb.y, c);
+      p2[i] = pa;
+      p2[i + stride] = pb;
+      m2[i] = ma;
+      m2[i + stride] = mb;
+      v2[i] = va;
+      v2[i + stride] = vb;
+    }
+    for (; i < npair; i += stride) {
+      float2 pa = p2[i];
+      const double2 ga = __ldcs(g2 + i);
+      double2 ma = m2[i], va = v2[i];
+      pa.x = adam_elem(pa.x, ga.x, ma.x, va.x, c);
+      pa.y = adam_elem(pa.y, ga.y, ma.y, va.y, c);
+      p2[i] = pa;
+      m2[i] = ma;
+      v2[i] = va;
+    }
+    done = npair * 2;
+  }
+  for (int64_t i = done + t0; i < n; i += stride) {
+    double mi = m[i], vi = v[i];
+    p[i] = adam_elem(p[i], g[i], mi, vi, c);
     m[i] = mi;
     v[i] = vi;
-    const double mh = __ddiv_rn(mi, bc1);
-    const double vh = __ddiv_rn(vi, bc2);
-    const double upd = __dsub_rn(static_cast<double>(p[i]),
-                                 __ddiv_rn(__dmul_rn(lr, mh), __dadd_rn(__dsqrt_rn(vh), eps)));
-    p[i] = __double2float_rn(upd);
   }
 }
 
 constexpr int kNormThreads = 256;
 
+// Block b sums g[b * per, (b + 1) * per) (per a multiple of 2 when the
+// array is 16-byte aligned): 16-byte loads, two in flight per thread.
 __global__ void sumsq_blocks_kernel(const double* __restrict__ g, int64_t n, int64_t per_block,
                                     double* __restrict__ partial, unsigned* __restrict__ nonfinite) {
   __shared__ double red[kNormThreads / 32];
   const int64_t lo = blockIdx.x * per_block;
   const int64_t hi = (lo + per_block < n) ? lo + per_block : n;
-  double acc = 0.0;
+  double acc0 = 0.0, acc1 = 0.0;
   unsigned bad = 0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += kNormThreads) {
+  const bool vec = ((reinterpret_cast<uintptr_t>(g + lo) & 15) == 0);
+  int64_t i = lo;
+  if (vec) {
+    const double2* g2 = reinterpret_cast<const double2*>(g + lo);
+    const int64_t npair = (hi - lo) / 2;
+    int64_t j = threadIdx.x;
+    for (; j + kNormThreads < npair; j += 2 * kNormThreads) {
+      const double2 a = __ldcs(g2 + j), b = __ldcs(g2 + j + kNormThreads);
+      acc0 += a.x * a.x + b.x * b.x;
+      acc1 += a.y * a.y + b.y * b.y;
+      bad |= !isfinite(a.x) | !isfinite(a.y) | !isfinite(b.x) | !isfinite(b.y);
+    }
+    for (; j < npair; j += kNormThreads) {
+      const double2 a = __ldcs(g2 + j);
+      acc0 += a.x * a.x;
+      acc1 += a.y * a.y;
+      bad |= !isfinite(a.x) | !isfinite(a.y);
+    }
+    i = lo + npair * 2;
+  }
+  for (i += threadIdx.x; i < hi; i += kNormThreads) {
     const double x = g[i];
-    acc += x * x;
+    acc0 += x * x;
     bad |= !isfinite(x);
   }
-  acc = warp_sum_f64(acc);
+  double acc = warp_sum_f64(acc0 + acc1);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   bad = __any_sync(0xffffffffu, bad);
   if ((threadIdx.x & 31) == 0 && bad) atomicOr(nonfinite, 1u);
@@ -108,9 +179,13 @@ extern "C" int dvla_adam_step(float* params, const double* grad, double* m, doub
     b1p = pow(beta1, static_cast<double>(step));
     b2p = pow(beta2, static_cast<double>(step));
   }
-  adam_kernel<<<grid_n(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      params, grad, m, v, n, beta1, 1.0 - beta1, beta2, 1.0 - beta2, 1.0 - b1p, 1.0 - b2p, lr,
-      eps);
+  const AdamConsts c{beta1, 1.0 - beta1, beta2, 1.0 - beta2, 1.0 - b1p, 1.0 - b2p, lr, eps};
+  const int vec = ((reinterpret_cast<uintptr_t>(params) & 7) == 0 &&
+                   (reinterpret_cast<uintptr_t>(grad) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(m) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(v) & 15) == 0) ? 1 : 0;
+  adam_kernel<<<grid_n(vec ? (n + 1) / 2 : n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      params, grad, m, v, n, c, vec);
   return launch_check("adam_kernel");
 }
 
@@ -128,7 +203,7 @@ extern "C" int dvla_grad_norm(double* grad, int64_t n, double max_norm, double* 
     return fail(DVLA_ERR_USAGE, "bad grad_norm arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nblocks = 4096;
-  const int64_t per = (n + nblocks - 1) / nblocks;
+  const int64_t per = ((n + nblocks - 1) / nblocks + 1) & ~int64_t{1};  // even: aligned pairs
   double* partial = static_cast<double*>(workspace);
   DVLA_CUDA_TRY(cudaMemsetAsync(partial, 0, nblocks * sizeof(double), st));
   if (n > 0) {
