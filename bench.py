@@ -426,8 +426,9 @@ def _bench_sampler(dev, logits, steps=20):
 
 def _bench_optimizer(dev, iters=10):
     """Learner optimizer tail on the OpenVLA action-head size:
-    Adam (f32 params, f64 grad / moments: 44 B per parameter) and the
-    gradient norm, HBM-bound."""
+    Adam (f32 params, f64 grad / moments) and the
+    gradient norm, HBM-bound (Adam reads p, g, m, v and writes p, m, v: 48 B
+    per parameter)."""
     import torch
     from paper_2605_13276_b200 import _lib
     n = V * 4096
@@ -445,7 +446,7 @@ def _bench_optimizer(dev, iters=10):
     for name, fn, nbytes in (
             ("adam", lambda it: _lib.dvla_adam_step(p.data_ptr(), g.data_ptr(), m.data_ptr(),
                                                     v.data_ptr(), n, it + 1, 1e-4, 0.9, 0.999,
-                                                    1e-8, s), n * 44),
+                                                    1e-8, s), n * 48),
             ("grad_norm", lambda it: _lib.dvla_grad_norm(g.data_ptr(), n, 0.0, norm.data_ptr(),
                                                          bad.data_ptr(), ws.data_ptr(), s),
              n * 8)):

@@ -29,7 +29,7 @@ __device__ __forceinline__ float adam_elem(float p, double gi, double& m, double
   return __double2float_rn(upd);
 }
 
-// HBM-bound (44 bytes per parameter): pairs of elements per thread with
+// HBM-bound (48 bytes per parameter): pairs of elements per thread with
 // 8-/16-byte accesses, two pairs in flight; a scalar tail for odd n or
 // misaligned arrays.
 __global__ void adam_kernel(float* __restrict__ p, const double* __restrict__ g,
