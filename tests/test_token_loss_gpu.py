@@ -313,3 +313,25 @@ def test_zero_advantage_groups_give_zero_gradient_rows():
     loss, dl, st = _run_gpu(x, tokens, blp, rewards, ids, torch.bfloat16)
     assert np.all(dl == 0.0)
     assert st["clip_fraction"] == 1.0 and loss == 0.0
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_shapes_match_oracle(seed):
+    """Randomised batch shapes, dtypes, vocabularies (incl. ones that are not
+    16-byte row multiples), group ids and KL settings against the oracle,
+    through whichever kernel path the C-ABI selects."""
+    import torch
+    rng = np.random.default_rng(1000 + seed)
+    n_groups = int(rng.integers(1, 6))
+    G = int(rng.integers(2, 10))
+    C = int(rng.integers(1, 4))
+    T = int(rng.integers(1, 21))
+    V = int(rng.choice([8, 24, 200, 1000, 2048, 3001, 4096 + 8]))
+    dtype = torch.bfloat16 if rng.random() < 0.6 else torch.float32
+    fused = bool(rng.random() < 0.8)
+    kl = float(rng.choice([0.0, 0.0, 0.2]))
+    ids = rng.permutation(n_groups * 5)[:n_groups]
+    case = _case(2000 + seed, n_groups, G, C, T, V, dtype, spread=float(rng.choice([0.05, 0.5])),
+                 binary=bool(rng.random() < 0.5), ids=ids)
+    rtol = 1e-5 if dtype == torch.float32 else 1e-2
+    _check(*case, dtype, fused=fused, rtol=rtol, cfg_kw={"kl_coeff": kl})
