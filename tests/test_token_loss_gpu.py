@@ -275,6 +275,17 @@ def test_fused_rows_split_into_pieces_match_oracle(dtype_name, V):
     lb, _, sb = _run_gpu(*case, dtype, fused=False)
     np.testing.assert_allclose(sa["lp_chunk"].cpu().numpy(), sb["lp_chunk"].cpu().numpy(),
                                rtol=1e-9, atol=1e-5)
+    # forward-only (loss evaluation) through the same pieces
+    from paper_2605_13276_b200 import grpo
+    dev = torch.device("cuda", 0)
+    lf, dlf, sf = grpo.grpo_token_grad(
+        torch.from_numpy(x).to(dev, dtype), torch.from_numpy(tokens).to(dev),
+        torch.from_numpy(blp).to(dev), torch.from_numpy(rewards).to(dev), ids,
+        grpo.GrpoConfig(group_size=4), write_dlogits=False)
+    assert dlf is None
+    np.testing.assert_allclose(sf["lp_chunk"].cpu().numpy(), sa["lp_chunk"].cpu().numpy(),
+                               rtol=0, atol=1e-12)
+    assert lf == pytest.approx(la, rel=1e-12, abs=1e-15)
 
 
 def test_misaligned_logits_take_the_scalar_path():
