@@ -616,7 +616,7 @@ def run_ours(a):
     algo_bytes = 2 * N * 2 + R * 4 + N_GROUPS * G * C * (4 + 8) + N_GROUPS * G * 4
     peak, peak_kind = _peaks()
     achieved = algo_bytes / (kern_avg_ms / 1e3) / 1e9
-    traffic = _traffic().get("tok_fused_bf16_kernel")
+    traffic = _traffic().get("tok_fused_kernel<bf16,1>")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": "tok_fused_kernel<bf16, 1 piece>" if not a.unfused else "tok_rows+tok_bwd",

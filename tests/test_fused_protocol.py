@@ -1,5 +1,5 @@
 """Model check of the fused token-loss kernel's warp/mbarrier protocol
-(csrc/token_loss.cu, tok_fused_bf16_kernel) on the CPU.
+(csrc/token_loss.cu, tok_fused_kernel<TE, P>) on the CPU.
 
 Every warp role is a generator that waits on simulated mbarriers with the
 hardware's parity semantics; random interleavings must (a) finish, (b) never
