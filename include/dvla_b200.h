@@ -282,6 +282,18 @@ int dvla_bytes_equal(const void* a, const void* b, int64_t nbytes, uint64_t* out
  * the TMA chain is measured against. */
 int dvla_memcpy_async(void* dst, const void* src, int64_t nbytes, void* stream);
 
+/* One process driving several GPUs (ControlPlane.broadcast over NVLink,
+ * planes.py:294-321): replicate nbytes (multiple of 16) of `src` on src_dev
+ * into dst_ptrs[i] on dst_devs[i].  mode 0: chain (each hop's TMA kernel
+ * runs on its source device, per-chunk flags in library-owned buffers);
+ * mode 1: copy-engine fan-out from the source.  streams: n_dst + 1 entries
+ * (source first) or NULL for each device's default stream.  Asynchronous;
+ * dvla_replicate_status reports (and clears) chain timeouts. */
+int dvla_replicate(int src_dev, const void* src, int n_dst, const int* dst_devs,
+                   void* const* dst_ptrs, int64_t nbytes, int64_t chunk_bytes, int mode,
+                   void* const* streams);
+int dvla_replicate_status(int* timed_out);
+
 /* Copy-engine variant of one chain hop (same flags and epochs as
  * dvla_replicate_chain): stream-wait wait_flags[c] >= epoch, copy chunk c
  * with cudaMemcpyAsync into dst, stream-write signal_flags[c] = epoch.

@@ -317,12 +317,14 @@ extern "C" int dvla_replicate_chain(const dvla_hop* hops, int n_hops, int64_t nb
   }
   if (nbytes == 0) return DVLA_OK;
   const size_t smem = 128 + static_cast<size_t>(kRepStages) * kRepPiece;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[64] = {};
+  int cur_dev = 0;
+  DVLA_CUDA_TRY(cudaGetDevice(&cur_dev));
+  if (!attr[cur_dev & 63]) {  // a function attribute is per device
     DVLA_CUDA_TRY(cudaFuncSetAttribute(replicate_chain_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
-    attr = true;
+    attr[cur_dev & 63] = true;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaEvent_t stop;
@@ -457,5 +459,147 @@ extern "C" int dvla_replicate_hop_ce(const void* src, void* dst, const uint32_t*
     }
   }
   prof_end(st, stop);
+  return DVLA_OK;
+}
+
+// ------------------------------------------- one process, several devices
+//
+// dvla_replicate: the single-process form of ControlPlane.broadcast over
+// NVLink (planes.py:294-321) for a driver that owns every GPU: src on
+// src_dev is replicated into dst_ptrs[i] on dst_devs[i].
+//   mode 0 (chain): hop i runs ON ITS SOURCE DEVICE (src_dev for the first,
+//     dst_devs[i - 1] after), TMA-copying chunks into the next device and
+//     releasing per-chunk flags; every link carries the region once.
+//   mode 1 (copy engines): the source device's copy engines write every
+//     destination directly (1 -> k fan-out).
+// Flags live in per-device buffers owned by the library (grown on demand,
+// never reset: every call uses a fresh epoch).  Work is enqueued on
+// streams[0] (source) and streams[i + 1] (destination i), or each device's
+// legacy default stream when streams is NULL; the call returns once all of
+// it is enqueued.  Calls on overlapping device sets must be serialised by
+// the caller (stream order suffices when the same streams are reused).
+namespace dvla {
+struct RepFlags {
+  uint32_t* ptr = nullptr;
+  size_t count = 0;
+  uint32_t* err = nullptr;
+};
+static RepFlags g_rep_flags[64];
+static uint32_t g_rep_epoch = 0;
+}  // namespace dvla
+
+extern "C" int dvla_replicate(int src_dev, const void* src, int n_dst, const int* dst_devs,
+                              void* const* dst_ptrs, int64_t nbytes, int64_t chunk_bytes,
+                              int mode, void* const* streams) {
+  if (n_dst < 0 || n_dst >= kMaxHops || (n_dst > 0 && (!dst_devs || !dst_ptrs)) || !src ||
+      nbytes < 0 || (nbytes % 16) != 0 || (mode != 0 && mode != 1))
+    return fail(DVLA_ERR_USAGE, "dvla_replicate: bad arguments");
+  if (n_dst == 0 || nbytes == 0) return DVLA_OK;
+  if (chunk_bytes <= 0) chunk_bytes = 1 << 20;
+  if (chunk_bytes % 16) return fail(DVLA_ERR_USAGE, "chunk_bytes must be a multiple of 16");
+  int prev = 0;
+  DVLA_CUDA_TRY(cudaGetDevice(&prev));
+  auto stream_of = [&](int i) {  // i = 0: source, i > 0: destination i - 1
+    return streams ? static_cast<cudaStream_t>(streams[i]) : cudaStream_t{0};
+  };
+  int rc = DVLA_OK;
+  if (mode == 1) {
+    for (int i = 0; i < n_dst && rc == DVLA_OK; ++i) {
+      cudaSetDevice(src_dev);
+      if (cudaMemcpyPeerAsync(dst_ptrs[i], dst_devs[i], src, src_dev, static_cast<size_t>(nbytes),
+                              stream_of(0)) != cudaSuccess)
+        rc = fail(DVLA_ERR_CUDA, "cudaMemcpyPeerAsync to device %d: %s", dst_devs[i],
+                  cudaGetErrorString(cudaGetLastError()));
+    }
+    cudaSetDevice(prev);
+    return rc;
+  }
+  const int64_t n_chunks = (nbytes + chunk_bytes - 1) / chunk_bytes;
+  // peer access along the chain, flag buffers on every destination
+  for (int i = 0; i < n_dst && rc == DVLA_OK; ++i) {
+    const int from = i == 0 ? src_dev : dst_devs[i - 1];
+    if (from != dst_devs[i]) rc = dvla_enable_peer_access(from, dst_devs[i]);
+    if (rc) break;
+    RepFlags& f = g_rep_flags[dst_devs[i] & 63];
+    if (f.count < static_cast<size_t>(n_chunks)) {
+      cudaSetDevice(dst_devs[i]);
+      if (f.ptr) cudaFree(f.ptr);
+      if (!f.err && cudaMalloc(&f.err, 16) != cudaSuccess) rc = fail(DVLA_ERR_CUDA, "flag alloc");
+      if (!rc && cudaMalloc(&f.ptr, static_cast<size_t>(n_chunks) * 4) != cudaSuccess)
+        rc = fail(DVLA_ERR_CUDA, "flag alloc");
+      if (!rc) {
+        cudaMemset(f.ptr, 0, static_cast<size_t>(n_chunks) * 4);
+        cudaMemset(f.err, 0, 16);
+        cudaDeviceSynchronize();
+        f.count = static_cast<size_t>(n_chunks);
+        g_rep_epoch = 0;  // a fresh zeroed buffer restarts the epochs... for all devices:
+        for (auto& o : g_rep_flags)
+          if (o.ptr && &o != &f) {
+            cudaSetDevice(static_cast<int>(&o - g_rep_flags));
+            cudaMemset(o.ptr, 0, o.count * 4);
+            cudaDeviceSynchronize();
+          }
+      }
+    }
+  }
+  if (rc) {
+    cudaSetDevice(prev);
+    return rc;
+  }
+  const uint32_t epoch = ++g_rep_epoch;
+  // hops that run on the same device go into ONE launch (co-resident CTA
+  // groups): a waiting hop must never queue behind its producer on a GPU
+  dvla_hop hops[kMaxHops + 1];
+  int hop_dev[kMaxHops + 1], hop_stream[kMaxHops + 1];
+  for (int i = 0; i <= n_dst; ++i) {
+    dvla_hop& h = hops[i];
+    h.src = i == 0 ? src : dst_ptrs[i - 1];
+    h.dst = i < n_dst ? dst_ptrs[i] : nullptr;
+    h.wait_flags = i == 0 ? nullptr : g_rep_flags[dst_devs[i - 1] & 63].ptr;
+    h.signal_flags = i < n_dst ? g_rep_flags[dst_devs[i] & 63].ptr : nullptr;
+    if (!h.dst) h.src = nullptr;
+    hop_dev[i] = i == 0 ? src_dev : dst_devs[i - 1];
+    hop_stream[i] = i;
+  }
+  bool done[kMaxHops + 1] = {};
+  for (int i = 0; i <= n_dst && rc == DVLA_OK; ++i) {
+    if (done[i]) continue;
+    dvla_hop group[kMaxHops + 1];
+    int g = 0;
+    for (int j = i; j <= n_dst; ++j)
+      if (!done[j] && hop_dev[j] == hop_dev[i]) {
+        group[g++] = hops[j];
+        done[j] = true;
+      }
+    const int dev = hop_dev[i];
+    cudaSetDevice(dev);
+    rc = dvla_replicate_chain(group, g, nbytes, chunk_bytes, epoch, g > 1 ? 128 / g : 128,
+                              30ull * 1000000000ull, g_rep_flags[dev & 63].err
+                                  ? g_rep_flags[dev & 63].err
+                                  : g_rep_flags[dst_devs[0] & 63].err,
+                              stream_of(hop_stream[i]));
+  }
+  cudaSetDevice(prev);
+  return rc;
+}
+
+// Reads and clears the timeout flags of dvla_replicate's chain hops
+// (synchronous; call after the streams used by dvla_replicate are idle).
+extern "C" int dvla_replicate_status(int* timed_out) {
+  if (!timed_out) return fail(DVLA_ERR_USAGE, "null out pointer");
+  int prev = 0;
+  DVLA_CUDA_TRY(cudaGetDevice(&prev));
+  *timed_out = 0;
+  for (int d = 0; d < 64; ++d) {
+    if (!g_rep_flags[d].err) continue;
+    uint32_t v = 0;
+    cudaSetDevice(d);
+    DVLA_CUDA_TRY(cudaMemcpy(&v, g_rep_flags[d].err, 4, cudaMemcpyDeviceToHost));
+    if (v) {
+      *timed_out = 1;
+      DVLA_CUDA_TRY(cudaMemset(g_rep_flags[d].err, 0, 4));
+    }
+  }
+  cudaSetDevice(prev);
   return DVLA_OK;
 }

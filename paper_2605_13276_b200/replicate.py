@@ -604,3 +604,35 @@ class SplitReplicator:
             _lib.dvla_ipc_close(bp)
             _lib.dvla_ipc_close(fp)
         self.peer = {}
+
+
+def replicate_devices(src, dsts, mode: str = "chain", chunk_bytes: int = 0, streams=None):
+    """One process, several GPUs (`dvla_replicate`): copy `src` (a CUDA
+    tensor) into every tensor of `dsts` (same byte size, any devices) by a
+    device-to-device chain (each hop on its source GPU) or copy-engine
+    fan-out.  Synchronous: returns once every destination holds the bytes;
+    raises ReplicationTimeout if a chain hop timed out."""
+    from . import _lib
+    torch = _torch()
+    n = src.numel() * src.element_size()
+    if n % 16:
+        raise UsageError("replicated regions must be a multiple of 16 bytes")
+    for d in dsts:
+        if d.numel() * d.element_size() != n or not d.is_cuda:
+            raise UsageError("every destination must be a CUDA tensor of the source's size")
+    k = len(dsts)
+    devs = (C.c_int * max(k, 1))(*[d.device.index for d in dsts])
+    ptrs = (C.c_void_p * max(k, 1))(*[d.data_ptr() for d in dsts])
+    st = None
+    if streams is not None:
+        st = (C.c_void_p * (k + 1))(*[s.cuda_stream for s in streams])
+    code = {"chain": 0, "ce": 1}[mode]
+    _lib.check(_lib.dvla_replicate(src.device.index, src.data_ptr(), k, devs, ptrs, n,
+                                   int(chunk_bytes), code, st), "dvla_replicate")
+    for d in {src.device.index, *[t.device.index for t in dsts]}:
+        torch.cuda.synchronize(d)
+    bad = C.c_int()
+    _lib.check(_lib.dvla_replicate_status(C.byref(bad)), "dvla_replicate_status")
+    if bad.value:
+        from ._lib import ReplicationTimeout
+        raise ReplicationTimeout("dvla_replicate: a chain hop timed out")

@@ -116,3 +116,21 @@ def test_replicate_rejects_bad_arguments(dev):
     ch = LocalChain(64, 1, device=dev, chunk_bytes=16)
     with pytest.raises(UsageError):
         ch.broadcast(torch.zeros(8, dtype=torch.uint8, device=dev))
+
+
+@pytest.mark.parametrize("mode", ["chain", "ce"])
+def test_replicate_devices_single_process(dev, mode):
+    """dvla_replicate: one process, every visible GPU (a same-device chain on
+    a 1-GPU box), bit-exact, repeated (fresh epochs), odd chunking."""
+    import torch
+    from paper_2605_13276_b200.replicate import bytes_equal, replicate_devices
+    n_dev = torch.cuda.device_count()
+    targets = [d for d in range(n_dev)] if n_dev > 1 else [0, 0]
+    S = 48 * 1024 * 1024 + 16 * 7
+    for it in range(3):
+        src = torch.randint(0, 256, (S,), dtype=torch.uint8, device="cuda:0",
+                            generator=torch.Generator(device="cuda:0").manual_seed(50 + it))
+        dsts = [torch.empty(S, dtype=torch.uint8, device=f"cuda:{d}") for d in targets[1:] + [targets[0]]]
+        replicate_devices(src, dsts, mode=mode, chunk_bytes=(1 << 20) + 16 * it)
+        for d in dsts:
+            assert bytes_equal(src.to(d.device), d) == (0, -1)
