@@ -164,7 +164,7 @@ def run_reference(a):
     _cpu_sample(threads, 1)
     times = []
     for _ in range(a.steps):
-        v, dt = _cpu_sample(threads, 8)
+        _, dt = _cpu_sample(threads, 8)
         times.append(dt)
     value = a.steps * 8 * G / sum(times)
     line = {
@@ -224,7 +224,7 @@ def _bench_replication(world, rank, dev, barrier, max_over_ranks, iters=5):
         e1.record(stream)
         torch.cuda.synchronize()
         ce_ms = e0.elapsed_time(e1) / iters
-        peak, kind = _peaks()
+        peak, _ = _peaks()
         out.update({"mode": "co-located replica (intra-HBM chain hop, TMA)",
                     "gbs": S / (ms / 1e3) / 1e9, "ms": ms,
                     "roofline": {"bound": "hbm", "achieved": 2 * S / (ms / 1e3) / 1e9,

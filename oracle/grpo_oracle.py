@@ -127,8 +127,6 @@ def policy_backward(w1, b1, w2, b2, log_std, obs, actions, coeffs, out):
     g_w1 = gz.T @ x
     g_b1 = gz.sum(axis=0)
     g_s = (c[:, None] * (eps * eps - 1.0)).sum(axis=0)
-    hdim, odim = w1.shape
-    ddim = w2.shape[0]
     i = 0
     for part in (g_w1.ravel(), g_b1, g_w2.ravel(), g_b2, g_s):
         out[i:i + part.size] += part
@@ -193,7 +191,7 @@ def grpo_grad_gauss(w1, b1, w2, b2, log_std, group_ids, obs, actions, blp, rewar
     obs (n_groups, G, C, obs_dim), actions (n_groups, G, C, D), blp
     (n_groups, G, C) f32, rewards (n_groups, G) f32.  Returns
     (loss, grad f64 flat, stats)."""
-    n_groups, G, C = blp.shape
+    n_groups, G, _ = blp.shape
     if n_groups == 0:
         raise ValueError("grpo update needs at least one group")
     n_traj = n_groups * G

@@ -22,8 +22,6 @@ from __future__ import annotations
 
 import ctypes as C
 
-import numpy as np
-
 from .core import ConfigError, ParamSnapshot, UsageError
 
 _DTYPE_CODE = None
@@ -277,7 +275,6 @@ class ChainReplicator:
     def broadcast(self, src, version: int, stream=None, timeout_s: float = 30.0):
         """Enqueue this rank's hop of the chain for `version` (all ranks)."""
         from . import _lib
-        torch = _torch()
         if self.pos < 0:
             return
         b = version % self.nb
