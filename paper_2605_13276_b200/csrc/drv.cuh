@@ -70,6 +70,10 @@ inline const DrvTable& drv() {
 #define cuMulticastCreate(...) drv().p_cuMulticastCreate(__VA_ARGS__)
 #define cuMulticastGetGranularity(...) drv().p_cuMulticastGetGranularity(__VA_ARGS__)
 #define cuMulticastUnbind(...) drv().p_cuMulticastUnbind(__VA_ARGS__)
+// (cuda.h maps these two to versioned symbols; the table holds the default
+// version resolved for this CUDA_VERSION)
+#undef cuStreamWaitValue32
+#undef cuStreamWriteValue32
 #define cuStreamWaitValue32(...) drv().p_cuStreamWaitValue32(__VA_ARGS__)
 #define cuStreamWriteValue32(...) drv().p_cuStreamWriteValue32(__VA_ARGS__)
 
