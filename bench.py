@@ -287,7 +287,11 @@ def _bench_multicast(S, src, rank, world, barrier, max_over_ranks, iters=4):
     ok_local = multicast_supported()
     if max_over_ranks(0.0 if ok_local else 1.0) != 0.0:
         return {"unavailable": "no NVSwitch multicast / POSIX-fd handles on this box"}
-    rep = McReplicator(S, n_buffers=1)
+    from paper_2605_13276_b200._lib import NativeError
+    try:
+        rep = McReplicator(S, n_buffers=1)
+    except NativeError as e:  # every rank raises the same error (agreement in setup)
+        return {"unavailable": str(e)[:200]}
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     times = []
@@ -495,8 +499,14 @@ def _bench_allreduce(world, dev, barrier, max_over_ranks, nbytes=1 << 30, iters=
     del g
     # the switch-reduced all-reduce (GradReducer's default where available)
     from paper_2605_13276_b200.replicate import McAllReduce, multicast_supported
+    from paper_2605_13276_b200._lib import NativeError
+    ar = None
     if max_over_ranks(0.0 if multicast_supported() else 1.0) == 0.0:
-        ar = McAllReduce(nbytes // 4)
+        try:
+            ar = McAllReduce(nbytes // 4)
+        except NativeError as e:
+            out["nvls"] = {"unavailable": str(e)[:200]}
+    if ar is not None:
         ar.buf.fill_(1.0)
         ar.allreduce()
         torch.cuda.synchronize()

@@ -340,49 +340,82 @@ def multicast_supported(device=None) -> bool:
 class _McRegion:
     """One multicast object over `ranks` (one process per GPU) with a bound
     region of `total` bytes on every member, mapped locally; the multicast
-    VA is mapped on the ranks in `map_on` (positions in `ranks`)."""
+    VA is mapped on the ranks in `map_on` (positions in `ranks`).
+
+    Every setup phase ends with an agreement among the participating ranks:
+    if any rank fails (no multicast support, no pidfd_getfd permission, out
+    of memory ...), all of them release what they built and raise the same
+    NativeError, so callers can fall back collectively instead of hanging."""
 
     def __init__(self, total: int, ranks, group, map_on):
         import os
-        import torch.distributed as dist
         from . import _lib
         torch = _torch()
+        import torch.distributed as dist
         self.rank = dist.get_rank()
         self.ranks = list(ranks)
         self.pos = self.ranks.index(self.rank) if self.rank in self.ranks else -1
         self.dev = torch.cuda.current_device()
+        self.group = group
         n = len(self.ranks)
         self.obj = self.local = self.mc = None
-        info = None
-        if self.pos == 0:
+        self.t = None
+        self.size = 0
+
+        def phase(fn):
+            err = None
+            try:
+                out = fn()
+            except Exception as e:  # noqa: BLE001 - reported to every rank below
+                out, err = None, f"rank {self.rank}: {e}"
+            errs = [e for e in _gather_by_rank(err, group).values() if e]
+            if errs:
+                self.close()
+                raise _lib.NativeError("multicast setup failed: " + "; ".join(errs))
+            return out
+
+        def create():
+            if self.pos != 0:
+                return None
             fd, size, obj = C.c_int(), C.c_size_t(), C.c_void_p()
             _lib.check(_lib.dvla_mc_create(n, total, C.byref(fd), C.byref(size), C.byref(obj)),
                        "dvla_mc_create")
             self.obj = obj.value
-            info = (os.getpid(), fd.value, size.value)
-        allinfo = _gather_by_rank(info, group)
-        pid, fd, size = allinfo[self.ranks[0]]
+            return (os.getpid(), fd.value, size.value)
+
+        info = phase(create)
+        pid, fd, size = _gather_by_rank(info, group)[self.ranks[0]]
         self.size = size
-        if self.pos > 0:
-            obj = C.c_void_p()
-            _lib.check(_lib.dvla_mc_import(pid, fd, n, size, C.byref(obj)), "dvla_mc_import")
-            self.obj = obj.value
-        if self.pos >= 0:
-            _lib.check(_lib.dvla_mc_add_device(self.obj, self.dev), "dvla_mc_add_device")
-        dist.barrier(group=group)
-        self.t = None
-        if self.pos >= 0:
-            local = C.c_void_p()
-            _lib.check(_lib.dvla_mc_bind(self.obj, self.dev, C.byref(local)), "dvla_mc_bind")
-            self.local = local.value
-            self.t = torch.as_tensor(_CudaView(self.local, self.size),
-                                     device=torch.device("cuda", self.dev))
-        dist.barrier(group=group)
-        if self.pos in map_on:
-            mc = C.c_void_p()
-            _lib.check(_lib.dvla_mc_map(self.obj, self.dev, C.byref(mc)), "dvla_mc_map")
-            self.mc = mc.value
-        dist.barrier(group=group)
+
+        def join():
+            if os.environ.get("DVLA_TEST_MC_FAIL_RANK") == str(self.rank):
+                raise RuntimeError("injected failure (DVLA_TEST_MC_FAIL_RANK)")
+            if self.pos > 0:
+                obj = C.c_void_p()
+                _lib.check(_lib.dvla_mc_import(pid, fd, n, size, C.byref(obj)), "dvla_mc_import")
+                self.obj = obj.value
+            if self.pos >= 0:
+                _lib.check(_lib.dvla_mc_add_device(self.obj, self.dev), "dvla_mc_add_device")
+
+        phase(join)
+
+        def bind():
+            if self.pos >= 0:
+                local = C.c_void_p()
+                _lib.check(_lib.dvla_mc_bind(self.obj, self.dev, C.byref(local)), "dvla_mc_bind")
+                self.local = local.value
+                self.t = torch.as_tensor(_CudaView(self.local, self.size),
+                                         device=torch.device("cuda", self.dev))
+
+        phase(bind)
+
+        def map_mc():
+            if self.pos in map_on:
+                mc = C.c_void_p()
+                _lib.check(_lib.dvla_mc_map(self.obj, self.dev, C.byref(mc)), "dvla_mc_map")
+                self.mc = mc.value
+
+        phase(map_mc)
 
     def close(self):
         from . import _lib

@@ -264,7 +264,13 @@ class GradReducer:
             if self._ar is None or self._ar.n < n:
                 if self._ar is not None:
                     self._ar.close()
-                self._ar = McAllReduce((n + 3) // 4 * 4, group=self.group)
+                from ._lib import NativeError
+                try:
+                    self._ar = McAllReduce((n + 3) // 4 * 4, group=self.group)
+                except NativeError:  # raised on every rank alike: fall back together
+                    self._ar = None
+                    self.backend = "nccl"
+                    return self.reduce(grad)
                 self._ar.buf.zero_()
             self._ar.buf[:n].copy_(grad.reshape(-1))  # f32 quantisation (the frame)
             self._ar.allreduce(scale=1.0 / self.nodes)

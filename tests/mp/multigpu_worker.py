@@ -76,6 +76,17 @@ def main():
         ar.close()
         if rank == 0:
             print("MC_ALLREDUCE_OK", flush=True)
+        # (1e) a setup failure on one rank surfaces on every rank (no hang)
+        from paper_2605_13276_b200._lib import NativeError
+        if rank == world - 1:
+            os.environ["DVLA_TEST_MC_FAIL_RANK"] = str(rank)
+        try:
+            McAllReduce(1024)
+            raise AssertionError("injected multicast failure did not surface")
+        except NativeError as e:
+            assert "injected failure" in str(e), str(e)
+        os.environ.pop("DVLA_TEST_MC_FAIL_RANK", None)
+        dist.barrier()
 
     # (1d) several sources, one region (C3 layout at 4 GPUs; two parts from
     # rank 0 along the same pair at 2)
