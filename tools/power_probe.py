@@ -15,6 +15,10 @@ tl = grpo.TokenLoss(N_GROUPS, G, C, T, V, grpo.GrpoConfig(group_size=G))
 tl.launch(logits, tokens, torch.zeros(N_GROUPS * G, device=dev), rw, None)
 blp = (tl.lp_chunk + 0.01).float()
 dl = torch.empty_like(logits)
+MODE = os.environ.get("MODE", "normal")  # normal | c0 (zero coefficients) | fwd (no dlogits)
+if MODE == "c0":
+    rw = torch.ones_like(rw)
+out_dl = None if MODE == "fwd" else dl
 smi = subprocess.Popen(["nvidia-smi", "--id=0", "--query-gpu=clocks.sm,power.draw,power.limit,"
                         "clocks_event_reasons.sw_power_cap,temperature.gpu",
                         "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
@@ -26,13 +30,13 @@ n = 0
 t0 = time.time()
 while time.time() - t0 < 4.0:
     for _ in range(50):
-        tl.launch(logits, tokens, blp, rw, dl)
+        tl.launch(logits, tokens, blp, rw, out_dl)
     n += 50
     torch.cuda.synchronize()
 e1.record()
 torch.cuda.synchronize()
 smi.terminate()
 out = smi.communicate()[0].strip().splitlines()
-print(f"{n} steps, {e0.elapsed_time(e1) / n:.3f} ms/step")
+print(f"{MODE}: {n} steps, {e0.elapsed_time(e1) / n:.3f} ms/step")
 for line in out[2:-1:3]:
     print("  sm MHz, W, limit W, power cap, C:", line)
