@@ -49,3 +49,39 @@ def test_swimlane_quarantines_poisoned_epoch(dev):
     res = run_swimlane(cfg, device=dev, poison_epochs={2})
     assert res.counters.get("quarantined_updates", 0) == 1
     assert res.counters["updates"] == 3
+
+
+def test_nvlink_data_channel_moves_batches_to_the_consumer_gpu(dev):
+    """Data-plane NVLINK channel: a GroupBatch put on the
+    rollout GPU arrives on the learner GPU, bit-identical, with the bytes
+    counted; on a 1-GPU box the batch stays (same device, zero copy)."""
+    import numpy as np
+    import torch
+    from paper_2605_13276_b200.grpo import GroupBatch
+    from paper_2605_13276_b200.planes import Channel, Plane, Transport, TransportMode
+    src_dev = torch.device("cuda", 0)
+    dst_dev = torch.device("cuda", 1 if torch.cuda.device_count() > 1 else 0)
+    tr = Transport(TransportMode.NVLINK, Plane.DATA)
+    ch = Channel(4, tr, name="traj", device=dst_dev)
+    sent = []
+    for gid in range(3):
+        b = GroupBatch(group_id=gid, horizon=8, chunk=1,
+                       obs=torch.randn(8, 1, 16, device=src_dev),
+                       actions=torch.randn(8, 1, 7, device=src_dev),
+                       behavior_log_prob=torch.randn(8, 1, device=src_dev),
+                       rewards=torch.randint(0, 2, (8,), device=src_dev).float(),
+                       behavior_version=gid,
+                       tokens=torch.randint(0, 256, (8, 1, 56), device=src_dev, dtype=torch.int32))
+        sent.append(b)
+        ch.put(b)
+    for b in sent:
+        got = ch.take()
+        assert got.group_id == b.group_id and got.behavior_version == b.behavior_version
+        for f in ("obs", "actions", "behavior_log_prob", "rewards", "tokens"):
+            t = getattr(got, f)
+            assert t.device == dst_dev
+            assert torch.equal(t.cpu(), getattr(b, f).cpu())
+    per = sum(getattr(sent[0], f).numel() * getattr(sent[0], f).element_size()
+              for f in ("obs", "actions", "behavior_log_prob", "rewards", "tokens"))
+    assert tr.bytes_counter == (3 * per if dst_dev != src_dev else 0)
+    assert np.isfinite(per)
