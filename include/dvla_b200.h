@@ -108,7 +108,13 @@ size_t dvla_token_loss_workspace_bytes(int64_t n_groups, int64_t G, int64_t C, i
  *   stats    device f64 [DVLA_ST_LEN]
  * Aborts (non-finite reward / log-prob / ratio / loss) are reported in
  * stats[DVLA_ST_ABORT], not as a return status (they are data-dependent and
- * detected on the device). */
+ * detected on the device).
+ * Kernel choice: 16-byte-aligned rows with T <= 128 take the persistent
+ * fused kernel (one CTA per SM whose CTAs exchange chunk log-probs: do not
+ * run two such launches concurrently on one GPU; a wait that exceeds 4 s is
+ * reported through stats[DVLA_ST_KERNEL_ERR] bit 1 instead of hanging);
+ * otherwise the unfused row/chunk/backward kernels.  flags DVLA_TL_UNFUSED
+ * forces the latter.  Workspace: dvla_token_loss_workspace_bytes. */
 int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int32_t* tokens,
                             const float* blp, const float* rewards, const int64_t* group_order,
                             const int64_t* group_ids, int64_t n_groups, int64_t G, int64_t C,
