@@ -108,6 +108,40 @@ def main():
     dist.barrier()
     srep.close()
 
+    # (1f) trajectory batches rollout rank -> learner rank:
+    # 7 batches through a 3-slot ring (wraps twice), bit-identical
+    from paper_2605_13276_b200.grpo import GroupBatch
+    from paper_2605_13276_b200.planes import PeerChannel
+
+    def make_batch(gid, device):
+        g = torch.Generator(device=device).manual_seed(1000 + gid)
+        return GroupBatch(
+            group_id=gid, horizon=8, chunk=1, behavior_version=gid // 2,
+            obs=torch.randn(8, 1, 24, device=device, generator=g),
+            actions=torch.randn(8, 1, 7, device=device, generator=g),
+            behavior_log_prob=torch.randn(8, 1, device=device, generator=g),
+            rewards=torch.randint(0, 2, (8,), device=device, generator=g).float(),
+            tokens=torch.randint(0, 256, (8, 1, 56), device=device, generator=g,
+                                 dtype=torch.int32))
+
+    pc = PeerChannel(producer=0, consumer=1, slot_bytes=64 << 10, slots=3)
+    if rank == 0:
+        for gid in range(7):
+            pc.put(make_batch(gid, "cuda"))
+        torch.cuda.synchronize()
+    elif rank == 1:
+        for gid in range(7):
+            got = pc.take()
+            want = make_batch(gid, "cuda")
+            assert got.group_id == gid and got.behavior_version == gid // 2
+            for f in ("obs", "actions", "behavior_log_prob", "rewards", "tokens"):
+                assert torch.equal(getattr(got, f), getattr(want, f)), (f, gid)
+        torch.cuda.synchronize()
+    dist.barrier()
+    pc.close()
+    if rank == 0:
+        print("PEER_CHANNEL_OK", flush=True)
+
     # (2) gradient mean over NCCL, exact mode vs host arithmetic
     g = torch.full((1000,), float(rank + 1), dtype=torch.float64, device="cuda") / 3.0
     out = GradReducer(world, exact=True).reduce(g.clone())
