@@ -691,9 +691,11 @@ def run_ours(a):
     del dl
     repl = None if a.no_repl else _bench_replication(world, rank, dev, barrier, max_over_ranks)
     allreduce = _bench_allreduce(world, dev, barrier, max_over_ranks)
-    gauss = None if a.no_gauss else _bench_gauss_c3(dev, rank, cpu=not a.no_cpu)
-    sampler = None if a.no_gauss else _bench_sampler(dev, logits)
-    optimizer = None if a.no_gauss else _bench_optimizer(dev)
+    # secondary per-GPU measurements: a failure is reported, never fatal to
+    # the headline line
+    gauss = None if a.no_gauss else _guarded(_bench_gauss_c3, dev, rank, cpu=not a.no_cpu)
+    sampler = None if a.no_gauss else _guarded(_bench_sampler, dev, logits)
+    optimizer = None if a.no_gauss else _guarded(_bench_optimizer, dev)
     swim = None
     if not a.no_swimlane:
         barrier()
@@ -702,12 +704,14 @@ def run_ours(a):
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
-        threads = len(os.sched_getaffinity(0))
-        v, dt = _cpu_sample(threads, 16)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": "16 groups x 8 trajectories x 56 tokens x 32064 vocab (1/4 of the C2 "
-                         "batch; oracle numpy f64, rows split over all host threads)",
-               "seconds": round(dt, 3)}
+        def cpu_leg():
+            threads = len(os.sched_getaffinity(0))
+            v, dt = _cpu_sample(threads, 16)
+            return {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                    "sample": "16 groups x 8 trajectories x 56 tokens x 32064 vocab (1/4 of the "
+                              "C2 batch; oracle numpy f64, rows split over all host threads)",
+                    "seconds": round(dt, 3)}
+        cpu = _guarded(cpu_leg)
 
     if rank == 0:
         line = {
@@ -734,6 +738,17 @@ def run_ours(a):
 
 
 _JSON_FD = None
+
+
+def _guarded(fn, *args, **kw):
+    """Run a secondary, single-rank measurement; report its failure in the
+    JSON line instead of losing the whole line."""
+    try:
+        return fn(*args, **kw)
+    except Exception as e:  # noqa: BLE001 - any failure of a secondary leg
+        import traceback
+        traceback.print_exc()
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
 
 
 def _quiet_stdout():
