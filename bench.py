@@ -474,6 +474,29 @@ def _bench_optimizer(dev, iters=10):
     return out
 
 
+def _bench_weight_plane_cpu(n_params=250_000_000):
+    """CPU baseline of the weight plane (SURVEY §8 d, CPU item iii): the
+    reference's host path -- snapshot_from_params (copy + isfinite) ->
+    ControlPlane.broadcast in WIRE mode (weight frame encode) -> one
+    mailbox -> take_newest (decode) -- through this repo's byte-identical
+    port, single-threaded, on 1 GB of f32 parameters."""
+    import numpy as np
+    from paper_2605_13276_b200.core import snapshot_from_params
+    from paper_2605_13276_b200.planes import ControlPlane, Plane, Transport, TransportMode
+    params = np.random.default_rng(0).standard_normal(n_params, dtype=np.float32)
+    plane = ControlPlane(Transport(TransportMode.WIRE, Plane.CONTROL))
+    box = plane.subscribe(name="replica")
+    t0 = time.perf_counter()
+    snap = snapshot_from_params(params, 1)
+    plane.broadcast(snap)
+    got = box.take_newest()
+    dt = time.perf_counter() - t0
+    assert got.version == 1
+    return {"gbs": params.nbytes / dt / 1e9, "seconds": round(dt, 3), "bytes": params.nbytes,
+            "cores": 1, "kind": "port",
+            "path": "snapshot_from_params -> ControlPlane.broadcast (WIRE) -> take_newest"}
+
+
 def _bench_allreduce(world, dev, barrier, max_over_ranks, nbytes=1 << 30, iters=5):
     """NCCL all-reduce of a learner gradient bucket (f32), busbw."""
     import torch
@@ -701,6 +724,9 @@ def run_ours(a):
         barrier()
         swim = _bench_swimlane(world, rank, dev, max_over_ranks)
         barrier()
+
+    if rank == 0 and world == 1 and not a.no_cpu and isinstance(repl, dict):
+        repl["cpu_baseline"] = _guarded(_bench_weight_plane_cpu)
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
