@@ -81,6 +81,7 @@ __global__ void adam_kernel(float* __restrict__ p, const double* __restrict__ g,
 }
 
 constexpr int kNormThreads = 256;
+constexpr int kNormBlocks = 16384;  // fixed: the reduction order never depends on the launch
 
 // Block b sums g[b * per, (b + 1) * per) (per a multiple of 2 when the
 // array is 16-byte aligned): 16-byte loads, two in flight per thread.
@@ -97,11 +98,13 @@ __global__ void sumsq_blocks_kernel(const double* __restrict__ g, int64_t n, int
     const double2* g2 = reinterpret_cast<const double2*>(g + lo);
     const int64_t npair = (hi - lo) / 2;
     int64_t j = threadIdx.x;
-    for (; j + kNormThreads < npair; j += 2 * kNormThreads) {
+    for (; j + 3 * kNormThreads < npair; j += 4 * kNormThreads) {
       const double2 a = __ldcs(g2 + j), b = __ldcs(g2 + j + kNormThreads);
-      acc0 += a.x * a.x + b.x * b.x;
-      acc1 += a.y * a.y + b.y * b.y;
-      bad |= !isfinite(a.x) | !isfinite(a.y) | !isfinite(b.x) | !isfinite(b.y);
+      const double2 c = __ldcs(g2 + j + 2 * kNormThreads), d = __ldcs(g2 + j + 3 * kNormThreads);
+      acc0 += (a.x * a.x + b.x * b.x) + (c.x * c.x + d.x * d.x);
+      acc1 += (a.y * a.y + b.y * b.y) + (c.y * c.y + d.y * d.y);
+      bad |= !isfinite(a.x) | !isfinite(a.y) | !isfinite(b.x) | !isfinite(b.y) |
+             !isfinite(c.x) | !isfinite(c.y) | !isfinite(d.x) | !isfinite(d.y);
     }
     for (; j < npair; j += kNormThreads) {
       const double2 a = __ldcs(g2 + j);
@@ -128,12 +131,21 @@ __global__ void sumsq_blocks_kernel(const double* __restrict__ g, int64_t n, int
   }
 }
 
-__global__ void norm_finish_kernel(const double* __restrict__ partial, int nblocks,
-                                   double* __restrict__ out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double s = 0.0;
-    for (int b = 0; b < nblocks; ++b) s += partial[b];
-    out[0] = sqrt(s);
+// fixed-order finish: thread t sums partials t, t + 1024, ... sequentially,
+// then a warp-shuffle and a 32-entry tree (deterministic, one block)
+constexpr int kFinishThreads = 1024;
+__global__ void __launch_bounds__(kFinishThreads) norm_finish_kernel(
+    const double* __restrict__ partial, int nblocks, double* __restrict__ out) {
+  __shared__ double red[kFinishThreads / 32];
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += kFinishThreads) acc += partial[b];
+  acc = warp_sum_f64(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kFinishThreads / 32; ++w) t += red[w];
+    out[0] = sqrt(t);
   }
 }
 
@@ -191,7 +203,7 @@ extern "C" int dvla_adam_step(float* params, const double* grad, double* m, doub
 
 extern "C" size_t dvla_grad_norm_workspace_bytes(int64_t n) {
   (void)n;
-  return 4096 * sizeof(double) + 256;
+  return kNormBlocks * sizeof(double) + 256;
 }
 
 // norm_out (device f64[1]) = ||grad||_2; scales grad in place when
@@ -202,7 +214,7 @@ extern "C" int dvla_grad_norm(double* grad, int64_t n, double max_norm, double* 
   if (n < 0 || !norm_out || !nonfinite_out || !workspace)
     return fail(DVLA_ERR_USAGE, "bad grad_norm arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int nblocks = 4096;
+  const int nblocks = kNormBlocks;
   const int64_t per = ((n + nblocks - 1) / nblocks + 1) & ~int64_t{1};  // even: aligned pairs
   double* partial = static_cast<double*>(workspace);
   DVLA_CUDA_TRY(cudaMemsetAsync(partial, 0, nblocks * sizeof(double), st));
@@ -212,7 +224,7 @@ extern "C" int dvla_grad_norm(double* grad, int64_t n, double max_norm, double* 
                                                        reinterpret_cast<unsigned*>(nonfinite_out));
     if (int rc = launch_check("sumsq_blocks_kernel")) return rc;
   }
-  norm_finish_kernel<<<1, 32, 0, st>>>(partial, nblocks, norm_out);
+  norm_finish_kernel<<<1, kFinishThreads, 0, st>>>(partial, nblocks, norm_out);
   if (int rc = launch_check("norm_finish_kernel")) return rc;
   if (max_norm > 0.0 && n > 0) {
     scale_if_kernel<<<grid_n(n), 256, 0, st>>>(grad, n, norm_out, max_norm);
