@@ -308,6 +308,19 @@ int dvla_replicate_status(int* timed_out);
 int dvla_replicate_hop_ce(const void* src, void* dst, const uint32_t* wait_flags,
                           uint32_t* signal_flags, int64_t nbytes, int64_t chunk_bytes,
                           uint32_t epoch, void* stream);
+/* NCCL for a process that drives several GPUs itself (GradReducer.reduce,
+ * runtime.py:569-637, without torch.distributed; libnccl.so.2 is opened at
+ * run time): dvla_nccl_init builds one communicator per device in `devs`
+ * (index = position); dvla_nccl_allreduce_sum sums `count` elements of
+ * dtype DVLA_F32 / DVLA_F64 / DVLA_BF16 in place on communicator comm_idx.
+ * One thread issuing for several devices brackets the calls with
+ * dvla_nccl_group_start / dvla_nccl_group_end. */
+int dvla_nccl_init(int n, const int* devs);
+int dvla_nccl_group_start(void);
+int dvla_nccl_group_end(void);
+int dvla_nccl_allreduce_sum(int comm_idx, void* ptr, int64_t count, int dtype, void* stream);
+int dvla_nccl_destroy(void);
+
 /* Stream memory operations used by the hop (cuStreamWaitValue32 GEQ /
  * cuStreamWriteValue32 with a memory barrier). */
 int dvla_stream_wait_u32(const uint32_t* addr, uint32_t value, void* stream);

@@ -154,6 +154,11 @@ dvla_replicate_chain = _proto("dvla_replicate_chain", [
 dvla_snapshot_copy = _proto("dvla_snapshot_copy", [_vp, _vp, _i64, _i32, _vp, _vp])
 dvla_bytes_equal = _proto("dvla_bytes_equal", [_vp, _vp, _i64, _vp, _vp])
 dvla_memcpy_async = _proto("dvla_memcpy_async", [_vp, _vp, _i64, _vp])
+dvla_nccl_init = _proto("dvla_nccl_init", [_i32, C.POINTER(_i32)])
+dvla_nccl_group_start = _proto("dvla_nccl_group_start", [])
+dvla_nccl_group_end = _proto("dvla_nccl_group_end", [])
+dvla_nccl_allreduce_sum = _proto("dvla_nccl_allreduce_sum", [_i32, _vp, _i64, _i32, _vp])
+dvla_nccl_destroy = _proto("dvla_nccl_destroy", [])
 dvla_replicate = _proto("dvla_replicate", [_i32, _vp, _i32, C.POINTER(_i32), C.POINTER(_vp), _i64,
                                            _i64, _i32, C.POINTER(_vp)])
 dvla_replicate_status = _proto("dvla_replicate_status", [C.POINTER(_i32)])

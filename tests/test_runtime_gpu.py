@@ -85,3 +85,30 @@ def test_nvlink_data_channel_moves_batches_to_the_consumer_gpu(dev):
               for f in ("obs", "actions", "behavior_log_prob", "rewards", "tokens"))
     assert tr.bytes_counter == (3 * per if dst_dev != src_dev else 0)
     assert np.isfinite(per)
+
+
+def test_nccl_c_abi_single_process_allreduce(dev):
+    """dvla_nccl_*: one process, every visible GPU, in-place sum all-reduce
+    (f32 and f64) through the C-ABI (libnccl opened at run time)."""
+    import ctypes as C
+    import torch
+    from paper_2605_13276_b200 import _lib
+    n = torch.cuda.device_count()
+    devs = (C.c_int * n)(*range(n))
+    _lib.check(_lib.dvla_nccl_init(n, devs), "dvla_nccl_init")
+    try:
+        for dt, code in ((torch.float32, _lib.F32), (torch.float64, _lib.F64)):
+            bufs = [torch.arange(1000, dtype=dt, device=f"cuda:{d}") * (d + 1) for d in range(n)]
+            _lib.check(_lib.dvla_nccl_group_start(), "group_start")
+            for d, b in enumerate(bufs):
+                with torch.cuda.device(d):
+                    _lib.check(_lib.dvla_nccl_allreduce_sum(
+                        d, b.data_ptr(), b.numel(), code, torch.cuda.current_stream(d).cuda_stream),
+                        "dvla_nccl_allreduce_sum")
+            _lib.check(_lib.dvla_nccl_group_end(), "group_end")
+            want = torch.arange(1000, dtype=dt) * (n * (n + 1) / 2)
+            for d, b in enumerate(bufs):
+                torch.cuda.synchronize(d)
+                assert torch.equal(b.cpu(), want), (dt, d)
+    finally:
+        _lib.dvla_nccl_destroy()
