@@ -666,3 +666,23 @@ def replicate_devices(src, dsts, mode: str = "chain", chunk_bytes: int = 0, stre
     if bad.value:
         from ._lib import ReplicationTimeout
         raise ReplicationTimeout("dvla_replicate: a chain hop timed out")
+
+
+def make_replicator(nbytes: int, ranks=None, n_buffers: int = 2, group=None):
+    """The replication engine the C5 size sweep favours for this region and
+    team (profiles/r01_replication_size_sweep_n{2,4}.txt): NVSwitch
+    multicast for regions below 0.5 GB on teams of 4 or more GPUs (no
+    pipeline fill), else the chain (one copy-engine hop for 2 GPUs, the TMA
+    chain beyond).  Collective: every rank of `ranks` calls it."""
+    import torch.distributed as dist
+    team = len(ranks) if ranks is not None else dist.get_world_size()
+    if team >= 4 and nbytes < 500_000_000:
+        ok = _torch().tensor([1.0 if multicast_supported() else 0.0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if ok.item() == 1.0:
+            from ._lib import NativeError
+            try:
+                return McReplicator(nbytes, ranks=ranks, n_buffers=n_buffers, group=group)
+            except NativeError:
+                pass  # raised on every rank alike: fall back together
+    return ChainReplicator(nbytes, ranks=ranks, n_buffers=n_buffers, group=group)

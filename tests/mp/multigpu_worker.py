@@ -88,6 +88,23 @@ def main():
         os.environ.pop("DVLA_TEST_MC_FAIL_RANK", None)
         dist.barrier()
 
+    # (1c') the size-based engine choice delivers bit-exact too
+    from paper_2605_13276_b200.replicate import make_replicator
+    for nb in (64 << 20, 600 << 20):
+        r2 = make_replicator(nb)
+        src = torch.randint(0, 256, (nb,), dtype=torch.uint8, device="cuda",
+                            generator=torch.Generator(device="cuda").manual_seed(nb % 1000))
+        dist.barrier()
+        r2.broadcast(src, 0)
+        torch.cuda.synchronize()
+        dist.barrier()
+        r2.check()
+        if rank > 0:
+            assert bytes_equal(src, r2.replica(0)) == (0, -1), ("auto", type(r2).__name__, rank)
+        dist.barrier()
+        r2.close()
+        del src
+
     # (1d) several sources, one region (C3 layout at 4 GPUs; two parts from
     # rank 0 along the same pair at 2)
     from paper_2605_13276_b200.replicate import SplitReplicator
