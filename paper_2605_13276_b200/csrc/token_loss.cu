@@ -150,9 +150,11 @@ __device__ __forceinline__ double chunk_lp_pairwise(const double* __restrict__ l
   return pairwise_sum([&](int64_t i) { return __ldcg(lp_tok + i); }, 0, T);
 }
 
-// ---------------------------------------------------- fused bf16 kernel
+// ---------------------------------------------------- fused kernel
 //
 // One CTA per SM (persistent), rows assigned round-robin (row = cta + k*grid).
+// (Below, "row" = one SMEM piece: a row longer than a stage is P pieces,
+// u = k P + p, with the lag L counted in pieces; see tok_fused_kernel.)
 // Every CTA walks one op sequence: A(0..L-1), then A(k), B(k-L), ..., B(n-1):
 //   A(k)  row k streamed HBM -> SMEM by TMA; the compute warps take warp
 //         max (packed bf16) / sum-exp (FFMA2 + MUFU ex2 + FADD2) partials;
@@ -164,7 +166,7 @@ __device__ __forceinline__ double chunk_lp_pairwise(const double* __restrict__ l
 //         pairwise order) and evaluates the GRPO coefficient; the compute
 //         warps overwrite the row in SMEM with d loss / d logits and the
 //         store warp streams it out with one TMA bulk store.
-// HBM traffic stays at the compulsory 2*N*2 bytes while the L-round lag
+// HBM traffic stays at the compulsory 2*N*s bytes while the L-round lag
 // hides the cross-CTA chunk dependency.  A(k+L) precedes B(k) on every CTA
 // and the tail warp never waits on another CTA, so the chunk wait is
 // deadlock-free while all CTAs are co-resident (grid <= #SMs, T <= grid).
@@ -194,7 +196,7 @@ constexpr int kPrepWarp = kFusedComputeWarps + 3;
 constexpr int kFusedThreadsWS = (kFusedComputeWarps + 4) * 32;
 
 constexpr int kLagRounds = 4;  // pieces; measured best on B200 (lag sweep, tools/fused_variants.py)
-constexpr int kRing = 8;       // (lse, target) rows in flight tail -> prep; needs lag < kRing
+constexpr int kRing = 8;       // (lse, target) rows in flight tail -> prep; lag <= 8P - 1
 constexpr float kFrameHi = 64.f;   // fixed-frame sum-exp range of a warp max (see phase A)
 constexpr float kFrameLo = -50.f;
 
