@@ -20,6 +20,12 @@ sys.path.insert(0, str(ROOT))
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA (B200) device")
     config.addinivalue_line("markers", "multigpu: needs >= 2 CUDA devices")
+    # a fresh checkout has no libdvla_b200.so yet: build it (nvcc cross-
+    # compiles sm_100a without a GPU; incremental when it exists)
+    lib = ROOT / "paper_2605_13276_b200" / "libdvla_b200.so"
+    if not lib.exists():
+        from paper_2605_13276_b200 import build as _build
+        _build.build()
 
 
 def golden(name: str):
