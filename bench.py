@@ -235,7 +235,12 @@ def _bench_replication(world, rank, dev, barrier, max_over_ranks, iters=5):
                     "kernel_ms": kms / max(kn, 1)})
         del ch
         return out
-    rep = ChainReplicator(S, n_buffers=2, ctas_per_hop=128)
+    # receivers' replica regions live in their MODEL_COMPUTE pool (the static
+    # half of the dual-pool allocator): the chain writes straight into it
+    from paper_2605_13276_b200.pools import Pool, PoolKind
+    pool = None if rank == 0 else Pool(PoolKind.MODEL_COMPUTE, 2 * S + (64 << 20), device=dev)
+    rep = ChainReplicator(S, n_buffers=2, ctas_per_hop=128, pool=pool)
+    rep_engine = rep.engine
     expect = src  # every rank generated the same bytes (same seed)
     rep.broadcast(src, 0)
     torch.cuda.synchronize()
@@ -266,9 +271,11 @@ def _bench_replication(world, rank, dev, barrier, max_over_ranks, iters=5):
         ce.append(max_over_ranks(e0.elapsed_time(e1)))
     barrier()
     rep.close()
+    del rep, pool
     gbs = S / (ms / 1e3) / 1e9
-    engine = "copy-engine hop" if rep.engine == "ce" else "TMA chain"
+    engine = "copy-engine hop" if rep_engine == "ce" else "TMA chain"
     out.update({"mode": f"{engine} 0->{'->'.join(str(r) for r in range(1, world))}",
+                "replica_regions": "receivers' MODEL_COMPUTE pools (dual-pool allocator)",
                 "gbs": gbs, "ms": ms, "bit_exact": ok_all,
                 "roofline": {"bound": "nvlink", "achieved": gbs, "peak": NVLINK_PEER_GBS,
                              "unit": "GB/s", "frac": gbs / NVLINK_PEER_GBS,

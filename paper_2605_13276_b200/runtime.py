@@ -220,13 +220,14 @@ class GradReducer:
         applied in the same pass; 685 vs 635 GB/s busbw for NCCL's ring at
         1 GiB on 4 B200);
       * backend "nccl": NCCL f32 all-reduce.
-    "auto" picks nvls from 4 nodes up when the box has NVSwitch multicast
-    and the sum need not be exact: per GPU and link direction it moves
+    The default is NCCL (the north star's gradient path); "auto" picks nvls
+    from 4 nodes up when the box has NVSwitch multicast and the sum need not
+    be exact: per GPU and link direction it moves
     (N + 1) / N of the buffer against the ring's 2 (N - 1) / N, so at 2
     nodes the ring wins (569 vs 400 GB/s busbw measured).  Single-node runs
     are a no-op, as in the reference."""
 
-    def __init__(self, nodes: int, group=None, exact: bool = False, backend: str = "auto"):
+    def __init__(self, nodes: int, group=None, exact: bool = False, backend: str = "nccl"):
         if backend not in ("auto", "nccl", "nvls"):
             raise ConfigError(f"unknown gradient reduction backend {backend!r}")
         if exact and backend == "nvls":

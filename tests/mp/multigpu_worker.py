@@ -40,6 +40,25 @@ def main():
             assert bytes_equal(src, rep.replica(v)) == (0, -1), (rank, v)
     rep.close()
 
+    # (1a') replica regions placed by the receivers' MODEL_COMPUTE pools
+    from paper_2605_13276_b200.pools import Pool, PoolKind
+    pool = None if rank == 0 else Pool(PoolKind.MODEL_COMPUTE, 2 * S + (1 << 20), device="cuda")
+    prep = ChainReplicator(S, chunk_bytes=4 << 20, ctas_per_hop=16, pool=pool)
+    for v in (0, 1):
+        src = torch.randint(0, 256, (S,), dtype=torch.uint8, device="cuda",
+                            generator=torch.Generator(device="cuda").manual_seed(150 + v))
+        prep.broadcast(src, v)
+        torch.cuda.synchronize()
+        dist.barrier()
+        prep.check()
+        if rank > 0:
+            reg = prep.replica(v)
+            assert bytes_equal(src, reg) == (0, -1), ("pool", rank, v)
+            base = pool.data.data_ptr()
+            assert base <= reg.data_ptr() < base + pool.capacity  # inside the pool's slab
+    dist.barrier()
+    prep.close()
+
     # (1b) switch-multicast (NVLS) replication, 3 versions through 2 buffers
     if multicast_supported():
         mrep = McReplicator(S, n_buffers=2)
