@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kRepThreads) replicate_chain_kernel(
   for (int s = 0; s < kRepStages; ++s) mbar_init(&S.full[s], 1);
   fence_mbar_init();
   const int64_t n_chunks = (nbytes + chunk_bytes - 1) / chunk_bytes;
-  uint32_t uses[kRepStages] = {0, 0, 0, 0};
+  uint32_t uses[kRepStages] = {};
   for (int64_t c = j; c < n_chunks; c += ctas_per_hop) {
     if (H.wait_flags && !wait_flag_sys(H.wait_flags + c, epoch, timeout_ns, err)) return;
     if (!H.dst) continue;
