@@ -36,7 +36,15 @@
 
 namespace dvla {
 
-constexpr int kFusedComputeWarps = 20;
+#ifndef DVLA_FUSED_W
+#define DVLA_FUSED_W 20
+#endif
+#ifndef DVLA_FUSED_CTAS
+#define DVLA_FUSED_CTAS 1
+#endif
+constexpr int kFusedComputeWarps = DVLA_FUSED_W;
+constexpr int kFusedCtasPerSm = DVLA_FUSED_CTAS;  // resident fused CTAs per SM
+constexpr size_t kFusedSmemCap = (228u * 1024u) / DVLA_FUSED_CTAS - 1024u;
 constexpr int kFusedComputeThreads = kFusedComputeWarps * 32;
 constexpr int kFusedStages = 3;    // SMEM row stages and B coefficient slots
 constexpr int kASlots = 8;         // A-row partial slots (coef-warp slack)
@@ -314,7 +322,7 @@ struct FusedElem<float> {
 // than a stage is streamed as P consecutive pieces: "virtual rows" u = k P + p
 // in the op sequence; the tail warp combines the P pieces' partials).
 template <class TE, int P>
-__global__ void __launch_bounds__(kFusedThreadsWS, 1)
+__global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
     tok_fused_kernel(TokParams p, uint32_t stage_bytes, int piece_vec, int write_dl, int lag) {
   using FE = FusedElem<TE>;
   constexpr int E = FE::kE;
@@ -1004,7 +1012,7 @@ static FusedGeom fused_geom(int64_t V, size_t esz) {
   for (int P : {1, 2, 4}) {
     const int64_t pv = (nvec_row + P - 1) / P;
     const size_t stage = ((static_cast<size_t>(pv) * 16 + 127) / 128) * 128;
-    if (hdr + kFusedStages * stage <= 227 * 1024) {
+    if (hdr + kFusedStages * stage <= kFusedSmemCap) {
       g.pieces = P;
       g.piece_vec = static_cast<int>(pv);
       g.stage_bytes = static_cast<uint32_t>(stage);
@@ -1108,10 +1116,11 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
     bool& set = attr_set[dev & 63][dtype == DVLA_BF16 ? 0 : 1][geom.pieces >> 1];
     if (!set) {
       DVLA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024));
+                                         static_cast<int>(kFusedSmemCap)));
       set = true;
     }
-    const unsigned grid = static_cast<unsigned>(R < sms ? R : sms);
+    const int64_t slots = int64_t{sms} * kFusedCtasPerSm;
+    const unsigned grid = static_cast<unsigned>(R < slots ? R : slots);
     cudaEvent_t stop;
     prof_begin(stream, &stop);
     static const int lag = [] {
