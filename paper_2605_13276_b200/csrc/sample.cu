@@ -147,7 +147,7 @@ __device__ __forceinline__ float thread_mass(const uint4* v, int nvec, int tid, 
 // whose interval holds u * total, and that thread walks its own elements in
 // the same order and frame to find the token.  lse = frame + log(total).
 template <class T>
-__global__ void __launch_bounds__(kSampThreads) tok_sample_kernel(
+__global__ void __launch_bounds__(kSampThreads, 6) tok_sample_kernel(
     const void* __restrict__ logits, int64_t V, uint64_t seed, uint64_t offset,
     int32_t* __restrict__ tokens, double* __restrict__ lp_tok) {
   constexpr int E = SampElem<T>::kVec;
@@ -199,23 +199,61 @@ __global__ void __launch_bounds__(kSampThreads) tok_sample_kernel(
   const double u = philox_uniform53(seed, offset, static_cast<uint64_t>(r)) * total;
   if (c > 0.0 && u < hi) atomicMin(&sm_win, tid);
   __syncthreads();
-  if (tid == sm_win) {
-    // inverse CDF inside this thread's elements, in its order and frame
-    double acc = lo;
-    int32_t tok = -1, last = -1;
+  const int win = sm_win;
+  if (win < kSampThreads && warp == (win >> 5)) {
+    // inverse CDF inside the winner's elements (granules win + k * 256), walked
+    // by the winner's warp: lane k takes granule k of a 32-granule block, sums
+    // its E exponentials in element order, a fixed-order scan over the lanes
+    // places each granule in [start, end), and the first lane whose interval
+    // holds u walks its own elements.
+    const double base = __shfl_sync(0xffffffffu, lo, win & 31);
     const float fL = frame * kLog2e;
-    for (int i = tid; i < nvec && tok < 0; i += kSampThreads) {
-      float f[E];
-      SampElem<T>::unpack(v[i], f);
+    double run = base;
+    int32_t tok = -1, last = -1;
+    for (int k0 = 0; win + k0 * kSampThreads < nvec && tok < 0; k0 += 32) {
+      const int i = win + (k0 + lane) * kSampThreads;
+      float pe[E];
+      double g = 0.0;
+      int lpos = -1;
+      if (i < nvec) {
+        float f[E];
+        SampElem<T>::unpack(v[i], f);
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const double pe = static_cast<double>(ex2f(fmaf(f[e], kLog2e, -fL)));
-        if (pe > 0.0) last = i * E + e;
-        acc += pe;
-        if (tok < 0 && u < acc) tok = i * E + e;
+        for (int e = 0; e < E; ++e) {
+          pe[e] = ex2f(fmaf(f[e], kLog2e, -fL));
+          g += static_cast<double>(pe[e]);
+          if (pe[e] > 0.f) lpos = i * E + e;
+        }
       }
+      double incl = g;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+      if (lane == 0) excl = 0.0;
+      const unsigned hit = __ballot_sync(0xffffffffu, i < nvec && u < run + incl);
+      if (hit) {
+        const int fl = __ffs(hit) - 1;
+        int32_t t = -1;
+        if (lane == fl) {
+          double acc = run + excl;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            acc += static_cast<double>(pe[e]);
+            if (t < 0 && u < acc) t = i * E + e;
+          }
+          if (t < 0) t = lpos;  // rounding at the granule's upper edge
+        }
+        tok = __shfl_sync(0xffffffffu, t, fl);
+      }
+      // last positive element so far (u at or past the walked total)
+      const int lm = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(lpos + 1)) - 1;
+      if (lm >= 0) last = lm;
+      run += __shfl_sync(0xffffffffu, incl, 31);
     }
-    sm_tok = (tok < 0) ? last : tok;  // rounding at the interval's upper edge
+    if (lane == 0) sm_tok = (tok < 0) ? last : tok;
   }
   if (tid == kSampThreads - 1) sm_tot = total;
   __syncthreads();

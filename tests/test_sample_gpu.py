@@ -59,3 +59,35 @@ def test_behaviour_logprobs_match_oracle_and_learner(dev):
     st = tl.stats(rw)
     assert abs(st["mean_ratio"] - 1.0) < 1e-4
     assert st["clip_fraction"] <= 1.0
+
+
+@pytest.mark.parametrize("dtype_name", ["bfloat16", "float32"])
+def test_wide_rows_walk_every_granule_block(dev, dtype_name):
+    """V = 131,072: each thread owns 64 (bf16) / 128 (f32) granules, so the
+    winner's warp walks its elements in several 32-granule blocks.  Mass sits
+    on 16 columns spread over the row (many in the later blocks); one-hot rows
+    must return their column exactly."""
+    import torch
+    from paper_2605_13276_b200.rollout import sample_action_tokens
+    dt = getattr(torch, dtype_name)
+    V, R = 131072, 40_000
+    cols = torch.tensor([5, 2047, 9000, 40000, 65535, 65536, 70001, 81920,
+                         90000, 100003, 110000, 120000, 125000, 130000, 131000, 131071],
+                        device=dev)
+    w = torch.tensor([0.5, -1.0, 2.0, 0.0, 1.5, -3.0, 0.25, 1.0,
+                      -0.5, 0.75, -2.0, 1.25, 0.1, -0.2, 0.9, -1.5], device=dev)
+    x = torch.full((R, V), -80.0, device=dev, dtype=dt)
+    x[:, cols] = w.to(dt)
+    tok, _, _ = sample_action_tokens(x, 1, seed=5)
+    hit = (tok.unsqueeze(1) == cols.unsqueeze(0).int())
+    assert bool(hit.any(dim=1).all())
+    counts = hit.sum(dim=0).cpu().numpy()
+    p = torch.softmax(w.to(dt).double(), 0).cpu().numpy()
+    chi2 = float((((counts - R * p) ** 2) / (R * p)).sum())
+    assert chi2 < 45.0, (chi2, counts)
+    # one-hot rows: the only finite column wins, wherever it sits
+    oh = torch.full((len(cols), V), float("-inf"), device=dev, dtype=dt)
+    oh[torch.arange(len(cols), device=dev), cols] = 0.0
+    t1, _, lp1 = sample_action_tokens(oh, 1, seed=9)
+    assert torch.equal(t1, cols.int())
+    assert torch.all(lp1 == 0.0)

@@ -20,4 +20,11 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / n
 gb = R * V * 2 / 1e9
+import hashlib
+out = sample_action_tokens(lg, T, seed=1)
+h = hashlib.sha256()
+for t in (out if isinstance(out, (tuple, list)) else [out]):
+    if torch.is_tensor(t):
+        h.update(t.cpu().numpy().tobytes())
+print(os.environ.get("DVLA_B200_LIB", "default").split("/")[-1], h.hexdigest()[:16])
 print(f"sample C2 bf16: {ms:.3f} ms/step  {gb / ms * 1e3:.0f} GB/s  (rows {R}, V {V})")
