@@ -70,6 +70,7 @@ enum : uint32_t { kErrToken = 1u, kErrTimeout = 2u };
 // Optional per-role cycle counters for the fused kernel (set by
 // dvla_debug_fused_counters; null in normal runs -> no clock reads).
 __device__ unsigned long long* g_dbg = nullptr;
+__device__ unsigned long long* g_dbg_cta = nullptr;  // per-CTA (start, end) globaltimer ns
 #define DBG_T0() const long long _t0 = dbg ? clock64() : 0
 #define DBG_ADD(i) \
   if (dbg) atomicAdd(dbg + (i), static_cast<unsigned long long>(clock64() - _t0))
@@ -249,6 +250,47 @@ __device__ __forceinline__ void op_of(int n, int nloc, int L, bool* isB, int* k)
   *k = pairs + (m - 2 * pairs);
 }
 
+#ifndef DVLA_POLL_NS
+#define DVLA_POLL_NS 256  // prep warp: back-off between polls of a chunk's token log-probs
+#endif
+#ifndef DVLA_FULL_SPIN
+#define DVLA_FULL_SPIN 0
+#endif
+#ifndef DVLA_CFULL_WAIT
+#define DVLA_CFULL_WAIT 0
+#endif
+#ifndef DVLA_POLY_WORDS
+#define DVLA_POLY_WORDS 0
+#endif
+constexpr int kPolyWords = DVLA_POLY_WORDS;  // bf16 phase-B words per granule on the FMA pipe
+
+// 2^y on both lanes of a packed f32 pair without MUFU: y = j + f with j =
+// round(y) (1.5*2^23 shifter), 2^f by a degree-3 minimax polynomial on
+// [-1/2, 1/2] (max relative error 7.5e-5), 2^j added into the exponent
+// field.  y is clamped below at -126 (2^-126 stands in for every smaller
+// value, including 2^-inf: 1e-38 against a zero, invisible at bf16's
+// gradient scale); y is at most log2|c| here, never near overflow.
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t y2) {
+  float y0, y1;
+  f2unpack(y2, y0, y1);
+  y2 = f2pack(fmaxf(y0, -126.f), fmaxf(y1, -126.f));
+  constexpr float kShift = 12582912.f;  // 1.5 * 2^23
+  const uint64_t t2 = fadd2(y2, f2pack(kShift, kShift));
+  const uint64_t j2 = fadd2(t2, f2pack(-kShift, -kShift));
+  const uint64_t f2 = ffma2(j2, f2pack(-1.f, -1.f), y2);
+  uint64_t p2 = ffma2(f2, f2pack(0.05517134f, 0.05517134f), f2pack(0.24261035f, 0.24261035f));
+  p2 = ffma2(p2, f2, f2pack(0.69326097f, 0.69326097f));
+  p2 = ffma2(p2, f2, f2pack(0.99992812f, 0.99992812f));
+  float t0, t1, p0, p1;
+  f2unpack(t2, t0, t1);
+  f2unpack(p2, p0, p1);
+  // t's low mantissa bits hold j (two's complement); j << 23 wraps the
+  // shifter's own bits out of the word
+  const uint32_t r0 = __float_as_uint(p0) + (__float_as_uint(t0) << 23);
+  const uint32_t r1 = __float_as_uint(p1) + (__float_as_uint(t1) << 23);
+  return f2pack(__uint_as_float(r0), __uint_as_float(r1));
+}
+
 // Element traits of the fused kernel: 16-byte granules of bf16 (8) or f32 (4)
 template <class TE>
 struct FusedElem;
@@ -272,14 +314,23 @@ struct FusedElem<__nv_bfloat16> {
       acc[j] = fadd2(acc[j], f2pack(ex2f(y0), ex2f(y1)));
     }
   }
-  // -sign(c) 2^(x log2e - K) for the granule, in place
+  // -sign(c) 2^(x log2e - K) for the granule, in place.  kPolyWords of the
+  // four words take their exponentials on the FMA pipe (exp2_poly2: degree-3
+  // polynomial, 7.5e-5 relative, far below the bf16 output's 2^-9), the rest
+  // on MUFU: phase B's ex2 load moves off the XU pipe the forward shares.
   __device__ static uint4 grad(const uint4& x, uint64_t l2e2, uint64_t nK2, uint32_t sgn) {
     auto e2 = [&](uint32_t w) {
       float y0, y1;
       f2unpack(bf16x2_fma2(w, l2e2, nK2), y0, y1);
       return pack_bf16x2(ex2f(y0), ex2f(y1)) ^ sgn;
     };
-    return make_uint4(e2(x.x), e2(x.y), e2(x.z), e2(x.w));
+    auto e2p = [&](uint32_t w) {
+      float y0, y1;
+      f2unpack(exp2_poly2(bf16x2_fma2(w, l2e2, nK2)), y0, y1);
+      return pack_bf16x2(y0, y1) ^ sgn;
+    };
+    return make_uint4(kPolyWords > 0 ? e2p(x.x) : e2(x.x), kPolyWords > 2 ? e2p(x.y) : e2(x.y),
+                      kPolyWords > 1 ? e2p(x.z) : e2(x.z), kPolyWords > 3 ? e2p(x.w) : e2(x.w));
   }
   __device__ static float get(const void* base, int i) {
     return __bfloat162float(static_cast<const __nv_bfloat16*>(base)[i]);
@@ -350,6 +401,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
   const int64_t T = p.T;
   unsigned long long* dbg = g_dbg;
   const long long t_kernel = dbg ? clock64() : 0;
+  const unsigned long long t_kernel_ns = dbg ? globaltimer_ns() : 0;
 
   if (tid == 0) {
     for (int s = 0; s < kFusedStages; ++s) {
@@ -505,6 +557,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
       double pv[4];
       const double* lt = p.lp_tok + q * T;
       uint32_t spins = 0;
+      const long long t_poll = dbg ? clock64() : 0;
       for (;;) {
         bool ready = true;
 #pragma unroll
@@ -514,7 +567,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
           ready &= __double_as_longlong(pv[m]) != kLpPending;
         }
         if (__all_sync(0xffffffffu, ready)) break;
-        __nanosleep(32);
+        __nanosleep(DVLA_POLL_NS);
         if ((++spins & 1023u) == 0 && globaltimer_ns() - t_start > kSpinTimeoutNs) {
           if (lane == 0) atomicOr(p.err, kErrTimeout);
           break;
@@ -522,8 +575,13 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
       }
       const float pblp = __ldg(p.blp + q);
       const double padv = __ldg(p.adv + q / p.C);
+      if (dbg && lane == 0) atomicAdd(dbg + 4, static_cast<unsigned long long>(clock64() - t_poll));
       const double lp = warp_pairwise_small(pv, static_cast<int>(T), lane);
-      mbar_wait(&S.tdone[k % kRing], static_cast<uint32_t>((k / kRing) & 1));  // own tail
+      {
+        DBG_T0();
+        mbar_wait(&S.tdone[k % kRing], static_cast<uint32_t>((k / kRing) & 1));  // own tail
+        if (lane == 0) { DBG_ADD(5); }
+      }
       uint32_t mode = 0u;
       float kval = 0.f, cf = 0.f;
       if (lane == 0) {
@@ -551,8 +609,11 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
       for (int pc = 0; pc < P; ++pc) {
         const int u = k * P + pc;
         const int sb = u % kFusedStages;
-        if (u >= kFusedStages)  // coefficient slot sb consumed by the compute warps
+        if (u >= kFusedStages) {  // coefficient slot sb consumed by the compute warps
+          DBG_T0();
           mbar_wait(&S.adoneB[sb], static_cast<uint32_t>(((u - kFusedStages) / kFusedStages) & 1));
+          if (lane == 0) { DBG_ADD(6); }
+        }
         if (lane == 0) {
           S.mode[sb] = mode;
           S.kval[sb] = kval;
@@ -581,7 +642,12 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
     const int elem0 = piece * piece_vec * E;  // first element of this piece in its row
     {
       DBG_T0();
+#if DVLA_FULL_SPIN
+      while (!mbar_test_wait(&S.full[s], ph)) {
+      }
+#else
       mbar_wait(&S.full[s], ph);
+#endif
       if (tid == 0) { DBG_ADD(0); }
     }
     if (!isB) {
@@ -649,7 +715,11 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
     const int sb = static_cast<int>(b % kFusedStages);
     {
       DBG_T0();
+#if DVLA_CFULL_WAIT
+      mbar_wait(&S.cfullB[sb], static_cast<uint32_t>((b / kFusedStages) & 1));
+#else
       mbar_wait_backoff(&S.cfullB[sb], static_cast<uint32_t>((b / kFusedStages) & 1));
+#endif
       if (tid == 0) { DBG_ADD(1); }
     }
     ++b;
@@ -685,6 +755,10 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
     }
   }
   if (dbg && tid == 0) atomicAdd(dbg + 12, static_cast<unsigned long long>(clock64() - t_kernel));
+  if (dbg && tid == 0 && g_dbg_cta) {
+    g_dbg_cta[2 * blockIdx.x] = t_kernel_ns;
+    g_dbg_cta[2 * blockIdx.x + 1] = globaltimer_ns();
+  }
 }
 
 // ------------------------------------------------------ unfused kernels
@@ -1184,6 +1258,14 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
 extern "C" int dvla_debug_fused_counters(void* dev_buf) {
   unsigned long long* p = static_cast<unsigned long long*>(dev_buf);
   DVLA_CUDA_TRY(cudaMemcpyToSymbol(g_dbg, &p, sizeof(p)));
+  return DVLA_OK;
+}
+
+// Debug only: per-CTA (start, end) globaltimer stamps of the fused kernel
+// (2 u64 per CTA; recorded while the counters above are enabled).
+extern "C" int dvla_debug_fused_cta_times(void* dev_buf) {
+  unsigned long long* p = static_cast<unsigned long long*>(dev_buf);
+  DVLA_CUDA_TRY(cudaMemcpyToSymbol(g_dbg_cta, &p, sizeof(p)));
   return DVLA_OK;
 }
 

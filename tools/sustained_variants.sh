@@ -1,0 +1,11 @@
+#!/bin/bash
+# Sustained (power-capped) C2 step time of library variants through bench.py:
+#   bash tools/sustained_variants.sh default tools/_variants/a.so ...
+for rep in 1 2; do
+  for v in "$@"; do
+    if [ "$v" = default ]; then L=""; else L=$v; fi
+    printf '%s ' "$(basename "$v")"
+    DVLA_B200_LIB=$L python bench.py --steps 200 --warmup 20 --no-e2e --no-cpu --no-repl \
+      --no-swimlane --no-gauss 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); c=d['clocks']; print(round(d['ms_per_step'],4), d['roofline']['kernel_ms'], c['sm_mhz'], c['reasons'], c.get('power_w'))"
+  done
+done
