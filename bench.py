@@ -594,9 +594,66 @@ def _bench_swimlane(world, rank, dev, max_over_ranks, epochs=8):
             "sync_trajectories_per_s_rank0": out["sync"]["trajectories_per_s"],
             "async_over_sync": traj / max(out["sync"]["trajectories_per_s"], 1e-12),
             "epochs": epochs, "staleness_max": out["async"]["staleness_max"],
+            "lanes": {m: {k: out[m][k] for k in ("transitions_per_s", "trajectories_per_s",
+                                                 "rollout_time", "actor_time")}
+                      for m in out},
             "config": "V=32064, H=4096, 64 groups x 8 traj x 56 tokens per GPU per epoch; "
                       "sync = the same lanes with staleness limit 0 (strict alternation)",
             "timing": "host clock per lane (reference transitions/s definition)"}
+
+
+def _swim_model(swim, world, roofline, sampler, optimizer):
+    """the swimlane's discrete-event model (sim.py, the
+    reference DES rules) with lane costs from this run's measured B200
+    rates, checked against the live lanes above (fit_check)."""
+    from paper_2605_13276_b200 import sim
+    kw = {}
+    if isinstance(roofline, dict) and roofline.get("frac"):
+        kw["loss_frac"] = roofline["frac"]
+    if isinstance(sampler, dict) and sampler.get("frac_of_hbm_peak"):
+        kw["sample_frac"] = sampler["frac_of_hbm_peak"]
+    if isinstance(optimizer, dict) and isinstance(optimizer.get("adam"), dict):
+        kw["adam_frac"] = optimizer["adam"]["frac_of_hbm_peak"]
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            kw["gemm_tflops"] = float(json.load(f)["bf16_tflops"])
+    except Exception:  # noqa: BLE001 - the dataclass default stands
+        pass
+    rates = sim.B200Rates(hbm_gbs=_peaks()[0], **kw)
+    costs = sim.b200_costs(N_GROUPS, G, C, T, V, 4096, nodes=world, rates=rates)
+    R = N_GROUPS * G * C * T
+    per_traj = N_GROUPS * G / R
+    ep = swim["epochs"]
+
+    def fit(res, mode):
+        live = swim["lanes"][mode]
+        f = sim.fit_check(res, {"mode": mode, "throughput": live["transitions_per_s"],
+                                "rollout_time": live["rollout_time"],
+                                "actor_time": live["actor_time"]}, threshold=0.25)
+        return {"predicted_trajectories_per_s": res.throughput * per_traj,
+                "live_trajectories_per_s": live["trajectories_per_s"],
+                "fit": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in f.items()}}
+
+    akw = {"epochs": ep, "staleness_limit": 1, "nodes": world, "per_node_slots": True}
+    # (1) analytic: lane costs from the measured kernel / GEMM / link rates
+    out = {"analytic": {"rates": rates.__dict__, "rollout_s": costs.rollout_s,
+                        "actor_s": costs.actor_s, "reduce_s": costs.reduce_s,
+                        "sync": fit(sim.simulate(costs, "sync", epochs=ep), "sync"),
+                        "async": fit(sim.simulate(costs, "async", **akw), "async")}}
+    # (2) calibrated: the live strict-alternation (sync) lane times are the
+    # lanes' isolated costs; the model predicts the overlapped (async) run
+    sl = swim["lanes"]["sync"]
+    cal = sim.LaneCosts(rollout_s=sl["rollout_time"], actor_s=sl["actor_time"],
+                        reduce_s=costs.reduce_s, shared_slots=True, transitions_per_epoch=R)
+    out["calibrated"] = {"rollout_s": cal.rollout_s, "actor_s": cal.actor_s,
+                         "async": fit(sim.simulate(cal, "async", **akw), "async")}
+    # the calibrated lanes at 8 GPUs (one closed loop per GPU, NCCL gradient mean)
+    c8 = sim.b200_costs(N_GROUPS, G, C, T, V, 4096, nodes=8, rates=rates)
+    cal8 = sim.LaneCosts(rollout_s=cal.rollout_s, actor_s=cal.actor_s, reduce_s=c8.reduce_s,
+                         shared_slots=True, transitions_per_epoch=R)
+    r8 = sim.simulate(cal8, "async", epochs=ep, staleness_limit=1, nodes=8, per_node_slots=True)
+    out["predicted_8gpu_trajectories_per_s_total"] = r8.throughput * per_traj * 8
+    return out
 
 
 def run_ours(a):
@@ -745,6 +802,7 @@ def run_ours(a):
         barrier()
         swim = _bench_swimlane(world, rank, dev, max_over_ranks)
         barrier()
+        swim["model"] = _guarded(_swim_model, swim, world, roofline, sampler, optimizer)
 
     if rank == 0 and world == 1 and not a.no_cpu and isinstance(repl, dict):
         repl["cpu_baseline"] = _guarded(_bench_weight_plane_cpu)

@@ -363,7 +363,10 @@ class RunResult:
         span = sum(r["step_time"] for r in post)
         pubs = [r["t_publish"] for r in self.reports]
         wall = (pubs[-1] - pubs[0]) if len(pubs) > 1 else max(self.wall, 1e-12)
+        n = max(len(post), 1)
         return {"transitions_per_s": trans / max(wall, 1e-12),
+                "rollout_time": sum(r.get("roll_wall", 0.0) for r in post) / n,
+                "actor_time": sum(r.get("train_wall", 0.0) for r in post) / n,
                 "trajectories_per_s": traj / max(wall, 1e-12),
                 "transitions_per_s_steptime": trans / max(span, 1e-12),
                 "wall": self.wall, "staleness_max": self.staleness_max,
@@ -537,6 +540,7 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
                 if int(flag.item()):
                     raise RunAbort("non-finite parameters after update",
                                    lane=LaneId.TRAINER.value, epoch=epoch)
+                train_wall = time.perf_counter() - t0
                 board.wait_pacing(board.version + 1)
                 v = board.publish()
                 busy["trainer"] += time.perf_counter() - t0
@@ -550,6 +554,7 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
                                        "version_after": v, "step_time": step_time,
                                        "transitions": n_traj * C * T,
                                        "trajectories": n_traj, "staleness": meta["staleness"],
+                                       "roll_wall": meta["roll_wall"], "train_wall": train_wall,
                                        "t_publish": time.perf_counter()})
             with dist_cv:
                 dist_q.append((None, None))
