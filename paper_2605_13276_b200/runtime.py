@@ -308,6 +308,7 @@ class SwimlaneConfig:
     lr: float = 1e-4
     seed: int = 0
     watchdog_s: float = 60.0
+    max_grad_norm: float | None = None
 
     def validate(self):
         if self.group_size < 2:
@@ -342,6 +343,162 @@ class TokenPolicy:
     def weight_bf16(self):
         import torch
         return self.master.view(self.V, self.H).to(torch.bfloat16)
+
+
+class SamplerWorker:
+    """One per GPU: owns the epoch-recycled ENV_AUX pools, the observation
+    projection and the SAMPLER stream (reference runtime.py:655-729).
+    run_epoch produces one epoch of device-resident GroupBatch messages with
+    the installed weights read in place."""
+
+    def __init__(self, cfg: SwimlaneConfig, node: int, nodes: int, env_pools, stream, device):
+        import torch
+        self.cfg, self.node, self.nodes = cfg, node, nodes
+        self.env_pools, self.stream, self.device = env_pools, stream, device
+        H = cfg.hidden
+        self.proj = torch.randn(224 * 224 * 3 // 64 + 8, H, device=device,
+                                generator=torch.Generator(device=device).manual_seed(
+                                    cfg.seed + 1)) * 0.05
+        self.rng = torch.Generator(device=device).manual_seed(cfg.seed * 7919 + node)
+
+    def run_epoch(self, epoch: int, snap: ParamSnapshot, poison: bool = False):
+        """One epoch of rollouts; returns (messages, meta) like the reference."""
+        import torch
+
+        from .rollout import sample_action_tokens
+        cfg, dev = self.cfg, self.device
+        V, H, G, C, T = cfg.vocab, cfg.hidden, cfg.group_size, cfg.chunks, cfg.tokens
+        n_traj = cfg.n_groups * G
+        R = n_traj * C * T
+        t0 = time.perf_counter()
+        pool = self.env_pools[epoch % len(self.env_pools)]
+        pool.epoch_reset()  # its previous epoch was consumed (staleness gate)
+
+        def stage(shape, dtype):
+            n = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
+            return pool.view(pool.alloc(n, align=256), dtype).view(*shape)
+
+        with torch.cuda.stream(self.stream):
+            W = snap.params.view(V, H)  # installed replica, zero copy
+            # synthetic LIBERO-shaped observations -> features
+            img = stage((n_traj * C, 224 * 224 * 3 // 64), torch.uint8)
+            img.copy_(torch.randint(0, 256, img.shape, device=dev, generator=self.rng,
+                                    dtype=torch.uint8))
+            prop = torch.randn(n_traj * C, 8, device=dev, generator=self.rng)
+            obs = torch.cat([img.float() / 255.0, prop], dim=1)
+            feats = stage((n_traj * C, H), torch.bfloat16)
+            feats.copy_(obs @ self.proj)                                # [n_traj*C, H]
+            logits = stage((R, V), torch.bfloat16)
+            torch.matmul(feats.repeat_interleave(T, dim=0), W.t(), out=logits)
+            rewards = torch.randint(0, 2, (n_traj,), device=dev, generator=self.rng).float()
+            if poison:
+                rewards[0] = float("nan")
+            # action tokens ~ softmax(logits) + f32 behaviour log-probs in
+            # one pass (csrc/sample.cu), Philox keyed by (seed, epoch, row)
+            tokens, blp, _ = sample_action_tokens(
+                logits, T, seed=cfg.seed * 1_000_003 + self.node, offset=epoch)
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        msgs = []
+        for gi in range(cfg.n_groups):
+            gid = (epoch * self.nodes + self.node) * cfg.n_groups + gi
+            sl = slice(gi * G, (gi + 1) * G)
+            toks = tokens.view(n_traj, C, T)[sl]
+            b = GroupBatch(
+                group_id=gid, horizon=C * T, chunk=T,
+                obs=feats.view(n_traj, C, H)[sl], actions=toks,
+                behavior_log_prob=blp.view(n_traj, C)[sl],
+                rewards=rewards[sl], behavior_version=snap.version, tokens=toks)
+            b.ready = ev  # device-resident handoff: consumer waits on the event
+            msgs.append(b)
+        ev.synchronize()
+        meta = {"roll_wall": time.perf_counter() - t0, "epoch": epoch,
+                "behavior_version": snap.version,
+                "success_rate": float(torch.nanmean(rewards).item())}
+        return msgs, meta
+
+
+class TrainerWorker:
+    """One per GPU: owns the head parameters and Adam state (MODEL_COMPUTE
+    pool), the fused loss and the TRAINER stream (reference
+    runtime.py:732-800).  update() = fused token loss fwd+bwd -> weight
+    gradient (cuBLAS) -> GradReducer mean -> grad norm (+clip) -> Adam ->
+    non-finite check -> version + 1."""
+
+    def __init__(self, cfg: SwimlaneConfig, node: int, model_pool, reducer, stream, device):
+        import torch
+        self.cfg, self.node, self.reducer = cfg, node, reducer
+        self.stream, self.device = stream, device
+        self.policy = TokenPolicy(cfg, model_pool, device)
+        self.gcfg = GrpoConfig(group_size=cfg.group_size, lr=cfg.lr,
+                               max_grad_norm=cfg.max_grad_norm)
+        V, G, C, T = cfg.vocab, cfg.group_size, cfg.chunks, cfg.tokens
+        R = cfg.n_groups * G * C * T
+        self.loss = TokenLoss(cfg.n_groups, G, C, T, V, self.gcfg, dtype=torch.bfloat16,
+                              device=device)
+        self.dl = torch.empty(R, V, dtype=torch.bfloat16, device=device)
+        self.logits = torch.empty(R, V, dtype=torch.bfloat16, device=device)
+        self.version = 0
+
+    def snapshot(self, out=None, stream=None) -> ParamSnapshot:
+        """The bf16 head as a versioned device snapshot (fused copy +
+        first-non-finite scan; reference snapshot_from_params)."""
+        from .replicate import device_snapshot
+        return device_snapshot(self.policy.weight_bf16().reshape(-1), self.version, out=out,
+                               stream=stream)
+
+    def update(self, batches: list) -> dict:
+        """One GRPO update on one epoch of groups.  Raises GrpoAbort for a
+        poisoned batch (the caller quarantines it) and RunAbort when the
+        parameters turn non-finite."""
+        import torch
+
+        from . import _lib
+        from .grpo import clip_grad_norm
+        cfg, pol, s = self.cfg, self.policy, self.stream
+        V, H, C, T = cfg.vocab, cfg.hidden, cfg.chunks, cfg.tokens
+        n_traj = cfg.n_groups * cfg.group_size
+        t0 = time.perf_counter()
+        with torch.cuda.stream(s):
+            batches[0].ready.wait(s)
+            W = pol.weight_bf16().view(V, H)
+            feats = torch.cat([b.obs for b in batches]).reshape(n_traj * C, H)
+            feats = feats.repeat_interleave(T, dim=0).contiguous()     # [R, H]
+            torch.matmul(feats, W.t(), out=self.logits)
+            self.loss.set_groups([b.group_id for b in batches])
+            toks = torch.cat([b.actions.reshape(-1) for b in batches])
+            blp = torch.cat([b.behavior_log_prob.reshape(-1) for b in batches])
+            rw = torch.cat([b.rewards for b in batches])
+            self.loss.launch(self.logits, toks, blp, rw, self.dl)
+        ev = torch.cuda.Event()
+        ev.record(s)
+        ev.synchronize()
+        stats = self.loss.stats(rw)  # GrpoAbort -> caller quarantines
+        with torch.cuda.stream(s):
+            grad = (self.dl.t() @ feats).reshape(-1).double()  # dW = dl^T x (cuBLAS, f32 acc)
+            grad = self.reducer.reduce(grad)
+            norm = clip_grad_norm(grad, self.gcfg.max_grad_norm)
+            pol.step += 1
+            g = self.gcfg
+            _lib.check(_lib.dvla_adam_step(
+                pol.master.data_ptr(), grad.data_ptr(), pol.m.data_ptr(), pol.v.data_ptr(),
+                V * H, pol.step, g.lr, g.beta1, g.beta2, g.opt_eps, s.cuda_stream),
+                "dvla_adam_step")
+            flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+            _lib.check(_lib.dvla_f32_nonfinite(pol.master.data_ptr(), V * H, flag.data_ptr(),
+                                               s.cuda_stream), "dvla_f32_nonfinite")
+        done = torch.cuda.Event()
+        done.record(s)
+        done.synchronize()
+        if int(flag.item()):
+            raise RunAbort("non-finite parameters after update",
+                           lane=LaneId.TRAINER.value, epoch=self.version)
+        self.version += 1
+        self.done_event = done
+        return {"version": self.version, "loss": stats["loss"], "grad_norm": norm,
+                "train_wall": time.perf_counter() - t0, "mean_ratio": stats["mean_ratio"],
+                "clip_fraction": stats["clip_fraction"], "n_chunks": stats["n_chunks"],
+                "mean_reward": float(rw.mean().item())}
 
 
 class RunResult:
@@ -380,12 +537,9 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
     import torch
     import torch.distributed as dist
 
-    from . import _lib
-    from .grpo import _stream_ptr
     from .planes import Channel, ControlPlane, Plane, RunAborted, Transport, TransportMode
     from .pools import Pool, PoolKind
     from .replicate import device_snapshot
-    from .rollout import sample_action_tokens
 
     cfg.validate()
     dev = torch.device(device) if device is not None else torch.device(
@@ -405,8 +559,6 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
     env_bytes = R * (V * 2 + 64) + n_traj * C * (H * 2 + 224 * 224 * 3 // 64 * 5) + (16 << 20)
     env_pools = [Pool(PoolKind.ENV_AUX, env_bytes, device=dev)
                  for _ in range(cfg.staleness_limit + 2)]
-    policy = TokenPolicy(cfg, model_pool, dev)
-    gcfg = GrpoConfig(group_size=G, lr=cfg.lr)
     abort = threading.Event()
     monitor = Monitor(abort)
 
@@ -415,15 +567,15 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
     mailbox = ctrl.subscribe("weights", abort_event=abort)
     chan = Channel(cfg.queue_capacity * cfg.n_groups,
                    Transport(TransportMode.INPROC, Plane.DATA, name="data"), abort_event=abort)
+    reducer = GradReducer(nodes, group)
+    trainer = TrainerWorker(cfg, rank, model_pool, reducer, s_train, dev)
+    sampler = SamplerWorker(cfg, rank, nodes, env_pools, s_sample, dev)
+    policy = trainer.policy
     # double-buffered published weights (bf16) in the MODEL_COMPUTE pool
     wbuf = [model_pool.view(model_pool.alloc(V * H * 2, align=256), torch.bfloat16)
             for _ in range(cfg.staleness_limit + 1)]
-    w0 = policy.weight_bf16().reshape(-1)
-    snap0 = device_snapshot(w0, 0, out=wbuf[0])
+    snap0 = trainer.snapshot(out=wbuf[0])
     board = VersionBoard(cfg.staleness_limit, monitor, snap0)
-    reducer = GradReducer(nodes, group)
-    proj = torch.randn(224 * 224 * 3 // 64 + 8, H, device=dev,
-                       generator=torch.Generator(device=dev).manual_seed(cfg.seed + 1)) * 0.05
     result = RunResult()
     busy = {"sampler": 0.0, "trainer": 0.0}
     dist_q: list = []
@@ -431,55 +583,12 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
 
     def sampler_lane():
         try:
-            rng = torch.Generator(device=dev).manual_seed(cfg.seed * 7919 + rank)
             for epoch in range(cfg.epochs):
                 snap, stal = board.wait_gate()
                 monitor.beat(LaneId.SAMPLER.value, "rolling")
-                t0 = time.perf_counter()
-                pool = env_pools[epoch % len(env_pools)]
-                pool.epoch_reset()  # its previous epoch was consumed (staleness gate)
-
-                def stage(shape, dtype):
-                    n = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
-                    return pool.view(pool.alloc(n, align=256), dtype).view(*shape)
-
-                with torch.cuda.stream(s_sample):
-                    W = snap.params.view(V, H)  # installed replica, zero copy
-                    # synthetic LIBERO-shaped observations -> features
-                    img = stage((n_traj * C, 224 * 224 * 3 // 64), torch.uint8)
-                    img.copy_(torch.randint(0, 256, img.shape, device=dev, generator=rng,
-                                            dtype=torch.uint8))
-                    prop = torch.randn(n_traj * C, 8, device=dev, generator=rng)
-                    obs = torch.cat([img.float() / 255.0, prop], dim=1)
-                    feats = stage((n_traj * C, H), torch.bfloat16)
-                    feats.copy_(obs @ proj)                                     # [n_traj*C, H]
-                    logits = stage((R, V), torch.bfloat16)
-                    torch.matmul(feats.repeat_interleave(T, dim=0), W.t(), out=logits)
-                    rewards = torch.randint(0, 2, (n_traj,), device=dev, generator=rng).float()
-                    if epoch in poison_epochs:
-                        rewards[0] = float("nan")
-                    # action tokens ~ softmax(logits) + f32 behaviour log-probs in
-                    # one pass (csrc/sample.cu), Philox keyed by (seed, epoch, row)
-                    tokens, blp, _ = sample_action_tokens(
-                        logits, T, seed=cfg.seed * 1_000_003 + rank, offset=epoch)
-                ev = torch.cuda.Event()
-                ev.record(s_sample)
-                msgs = []
-                for gi in range(cfg.n_groups):
-                    gid = (epoch * nodes + rank) * cfg.n_groups + gi
-                    sl = slice(gi * G, (gi + 1) * G)
-                    toks = tokens.view(n_traj, C, T)[sl]
-                    b = GroupBatch(
-                        group_id=gid, horizon=C * T, chunk=T,
-                        obs=feats.view(n_traj, C, H)[sl], actions=toks,
-                        behavior_log_prob=blp.view(n_traj, C)[sl],
-                        rewards=rewards[sl], behavior_version=snap.version, tokens=toks)
-                    b.ready = ev  # device-resident handoff: consumer waits on the event
-                    msgs.append(b)
-                ev.synchronize()
-                busy["sampler"] += time.perf_counter() - t0
-                board.produce(epoch, {"roll_wall": time.perf_counter() - t0, "epoch": epoch,
-                                      "behavior_version": snap.version, "staleness": stal})
+                msgs, meta = sampler.run_epoch(epoch, snap, poison=epoch in poison_epochs)
+                busy["sampler"] += meta["roll_wall"]
+                board.produce(epoch, {**meta, "staleness": stal})
                 for m in msgs:
                     chan.put(m)
                 board.boundary()
@@ -492,69 +601,34 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
 
     def trainer_lane():
         try:
-            tl = TokenLoss(cfg.n_groups, G, C, T, V, gcfg, dtype=torch.bfloat16, device=dev)
-            dl = torch.empty(R, V, dtype=torch.bfloat16, device=dev)
-            logits = torch.empty(R, V, dtype=torch.bfloat16, device=dev)
             for epoch in range(cfg.epochs):
                 batches = [chan.take() for _ in range(cfg.n_groups)]
                 meta = board.take_meta(epoch)
                 monitor.beat(LaneId.TRAINER.value, "train")
                 t0 = time.perf_counter()
-                with torch.cuda.stream(s_train):
-                    batches[0].ready.wait(s_train)
-                    W = policy.weight_bf16().view(V, H)
-                    feats = torch.cat([b.obs for b in batches]).reshape(n_traj * C, H)
-                    feats = feats.repeat_interleave(T, dim=0).contiguous()     # [R, H]
-                    torch.matmul(feats, W.t(), out=logits)
-                    tl.set_groups([b.group_id for b in batches])
-                    toks = torch.cat([b.actions.reshape(-1) for b in batches])
-                    blp = torch.cat([b.behavior_log_prob.reshape(-1) for b in batches])
-                    rw = torch.cat([b.rewards for b in batches])
-                    tl.launch(logits, toks, blp, rw, dl)
-                st_ev = torch.cuda.Event()
-                st_ev.record(s_train)
-                st_ev.synchronize()
                 try:
-                    stats = tl.stats(rw)
+                    st = trainer.update(batches)
                 except GrpoAbort as e:
                     log.warning("quarantined update: %s", e)
                     board.quarantine()
                     result.counters["quarantined_updates"] = \
                         result.counters.get("quarantined_updates", 0) + 1
                     continue
-                with torch.cuda.stream(s_train):
-                    grad = (dl.t() @ feats).reshape(-1).double()  # dW = dl^T x (cuBLAS, f32 acc)
-                    grad = reducer.reduce(grad)
-                    policy.step += 1
-                    _lib.check(_lib.dvla_adam_step(
-                        policy.master.data_ptr(), grad.data_ptr(), policy.m.data_ptr(),
-                        policy.v.data_ptr(), V * H, policy.step, gcfg.lr, gcfg.beta1,
-                        gcfg.beta2, gcfg.opt_eps, s_train.cuda_stream), "dvla_adam_step")
-                    flag = torch.zeros(1, dtype=torch.int32, device=dev)
-                    _lib.check(_lib.dvla_f32_nonfinite(policy.master.data_ptr(), V * H,
-                                                       flag.data_ptr(), s_train.cuda_stream),
-                               "dvla_f32_nonfinite")
-                done = torch.cuda.Event()
-                done.record(s_train)
-                done.synchronize()
-                if int(flag.item()):
-                    raise RunAbort("non-finite parameters after update",
-                                   lane=LaneId.TRAINER.value, epoch=epoch)
-                train_wall = time.perf_counter() - t0
                 board.wait_pacing(board.version + 1)
                 v = board.publish()
                 busy["trainer"] += time.perf_counter() - t0
-                result.update_stats.append({"version": v, **{k: stats[k] for k in (
-                    "loss", "mean_ratio", "clip_fraction", "n_chunks")}})
+                result.update_stats.append({"version": v, **{k: st[k] for k in (
+                    "loss", "mean_ratio", "clip_fraction", "n_chunks", "grad_norm")}})
                 with dist_cv:
-                    dist_q.append((v, done))
+                    dist_q.append((v, trainer.done_event))
                     dist_cv.notify_all()
                 step_time = max(meta["roll_wall"], time.perf_counter() - t0)
                 result.reports.append({"epoch": epoch, "policy_version": meta["behavior_version"],
                                        "version_after": v, "step_time": step_time,
                                        "transitions": n_traj * C * T,
                                        "trajectories": n_traj, "staleness": meta["staleness"],
-                                       "roll_wall": meta["roll_wall"], "train_wall": train_wall,
+                                       "roll_wall": meta["roll_wall"],
+                                       "train_wall": st["train_wall"],
                                        "t_publish": time.perf_counter()})
             with dist_cv:
                 dist_q.append((None, None))
@@ -578,8 +652,8 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
                     break
                 with torch.cuda.stream(s_dist):
                     s_dist.wait_event(ev)
-                    w = policy.weight_bf16().reshape(-1)
-                    snap = device_snapshot(w, v, out=wbuf[v % len(wbuf)], stream=s_dist)
+                    snap = device_snapshot(policy.weight_bf16().reshape(-1), v,
+                                           out=wbuf[v % len(wbuf)], stream=s_dist)
                 ctrl.broadcast(snap, stream=s_dist)
                 monitor.beat(LaneId.WEIGHT_DIST.value)
             monitor.beat(LaneId.WEIGHT_DIST.value, "done")

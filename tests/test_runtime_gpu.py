@@ -112,3 +112,68 @@ def test_nccl_c_abi_single_process_allreduce(dev):
                 assert torch.equal(b.cpu(), want), (dt, d)
     finally:
         _lib.dvla_nccl_destroy()
+
+
+def test_sampler_and_trainer_workers_against_the_oracle(dev):
+    """SamplerWorker.run_epoch -> TrainerWorker.update (reference
+    runtime.py:676-800): the update's loss equals the f64 oracle on the same
+    logits, and Adam's first step moves every parameter with a clear
+    gradient by -lr * sign(grad) (m_hat / sqrt(v_hat) = sign(g) at step 1)."""
+    import torch
+    from oracle import grpo_oracle as O
+    from paper_2605_13276_b200.grpo import GrpoAbort
+    from paper_2605_13276_b200.pools import Pool, PoolKind
+    from paper_2605_13276_b200.runtime import (GradReducer, SamplerWorker, SwimlaneConfig,
+                                               TrainerWorker)
+    cfg = SwimlaneConfig(n_groups=2, group_size=4, tokens=8, vocab=1024, action_bins=256,
+                         hidden=64, seed=11, lr=1e-3)
+    V, H, G, T = cfg.vocab, cfg.hidden, cfg.group_size, cfg.tokens
+    n_traj = cfg.n_groups * G
+    model_pool = Pool(PoolKind.MODEL_COMPUTE, 64 << 20, device=dev)
+    env_pools = [Pool(PoolKind.ENV_AUX, 32 << 20, device=dev) for _ in range(2)]
+    s_sample, s_train = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    trainer = TrainerWorker(cfg, 0, model_pool, GradReducer(1, None), s_train, dev)
+    sampler = SamplerWorker(cfg, 0, 1, env_pools, s_sample, dev)
+    snap = trainer.snapshot()
+    torch.cuda.synchronize()
+    assert snap.version == 0
+    assert torch.equal(snap.params.view(torch.int16),
+                       trainer.policy.weight_bf16().reshape(-1).view(torch.int16))
+
+    msgs, meta = sampler.run_epoch(0, snap)
+    assert [m.group_id for m in msgs] == [0, 1]
+    assert meta["behavior_version"] == 0 and meta["roll_wall"] > 0
+    toks = torch.cat([m.actions.reshape(-1) for m in msgs])
+    assert int(toks.min()) >= 0 and int(toks.max()) < V   # sampled over the full vocabulary
+    feats = torch.cat([m.obs for m in msgs]).reshape(n_traj, H).clone()
+    blp = torch.cat([m.behavior_log_prob.reshape(-1) for m in msgs]).clone()
+    rw = torch.cat([m.rewards for m in msgs]).clone()
+    W = trainer.policy.weight_bf16()
+    logits = feats.repeat_interleave(T, dim=0) @ W.t()            # what update() computes
+    before = trainer.policy.master.clone()
+
+    st = trainer.update(msgs)
+    assert st["version"] == 1 and trainer.version == 1
+    x = logits.float().cpu().numpy().reshape(cfg.n_groups, G, 1, T, V)
+    loss, dl, ost = O.grpo_token_grad(
+        x, toks.cpu().numpy().reshape(cfg.n_groups, G, 1, T),
+        blp.cpu().numpy().reshape(cfg.n_groups, G, 1), rw.cpu().numpy().reshape(cfg.n_groups, G),
+        np.array([0, 1]))
+    # on-policy batch (ratio ~ 1, zero-mean advantages): the loss is a
+    # cancellation near 0, so compare it absolutely and the lp / ratio tightly
+    np.testing.assert_allclose(st["loss"], loss, atol=1e-6)
+    np.testing.assert_allclose(trainer.loss.lp_chunk.cpu().numpy().reshape(-1),
+                               ost["lp_chunk"].reshape(-1), rtol=1e-9, atol=1e-5)
+    np.testing.assert_allclose(st["mean_ratio"], ost["mean_ratio"], rtol=1e-6)
+    assert st["n_chunks"] == n_traj
+    g = dl.reshape(-1, V).T @ feats.double().repeat_interleave(T, dim=0).cpu().numpy()
+    g = g.reshape(-1)
+    np.testing.assert_allclose(st["grad_norm"], np.sqrt((g * g).sum()), rtol=2e-2)
+    delta = (trainer.policy.master - before).cpu().double().numpy()
+    clear = np.abs(g) > max(1e-2 * np.abs(g).max(), 1e-4)  # eps = 1e-8 negligible
+    assert clear.sum() > 100
+    np.testing.assert_allclose(delta[clear], -cfg.lr * np.sign(g[clear]), rtol=1e-3)
+
+    msgs2, _ = sampler.run_epoch(1, trainer.snapshot(), poison=True)
+    with pytest.raises(GrpoAbort):
+        trainer.update(msgs2)
