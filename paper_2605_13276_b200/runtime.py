@@ -530,6 +530,24 @@ class RunResult:
                 "updates": len(self.update_stats)}
 
 
+@dataclass
+class BubbleStats:
+    sampler_idle_fraction: float
+    trainer_idle_fraction: float
+    wall: float
+    warmup_dominated: bool
+
+
+def barrier_free_handoff_audit(result: RunResult) -> BubbleStats:
+    """Idle fraction of each lane over the run's wall clock (reference
+    runtime.py:881-889): the bubbles the asynchronous handoff leaves."""
+    wall = max(result.wall, 1e-12)
+    return BubbleStats(
+        sampler_idle_fraction=max(0.0, 1.0 - result.lane_busy.get("sampler", 0.0) / wall),
+        trainer_idle_fraction=max(0.0, 1.0 - result.lane_busy.get("trainer", 0.0) / wall),
+        wall=wall, warmup_dominated=len(result.reports) <= 1)
+
+
 def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=frozenset()):
     """Asynchronous swimlane on one GPU (and, under torch.distributed, one
     closed loop per GPU with NCCL gradient reduction: topology replication,

@@ -105,3 +105,16 @@ def test_single_node_reduce_is_identity():
     import torch
     g = torch.arange(4, dtype=torch.float64)
     assert GradReducer(1).reduce(g) is g
+
+
+def test_barrier_free_handoff_audit():
+    from paper_2605_13276_b200.runtime import RunResult, barrier_free_handoff_audit
+    r = RunResult()
+    r.wall = 2.0
+    r.lane_busy = {"sampler": 1.5, "trainer": 2.5}
+    r.reports = [{}, {}]
+    b = barrier_free_handoff_audit(r)
+    assert b.sampler_idle_fraction == 0.25 and b.trainer_idle_fraction == 0.0
+    assert b.wall == 2.0 and not b.warmup_dominated
+    r.reports = [{}]
+    assert barrier_free_handoff_audit(r).warmup_dominated
