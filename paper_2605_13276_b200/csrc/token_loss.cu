@@ -39,6 +39,9 @@ namespace dvla {
 #ifndef DVLA_FUSED_W
 #define DVLA_FUSED_W 20
 #endif
+#ifndef DVLA_SUB
+#define DVLA_SUB 0  // phase-B store sub-blocks, in granules per compute thread (0: one store per piece)
+#endif
 #ifndef DVLA_FUSED_CTAS
 #define DVLA_FUSED_CTAS 1
 #endif
@@ -209,6 +212,14 @@ constexpr int kRing = 8;       // (lse, target) rows in flight tail -> prep; lag
 constexpr float kFrameHi = 64.f;   // fixed-frame sum-exp range of a warp max (see phase A)
 constexpr float kFrameLo = -50.f;
 
+// Phase-B rows are handed to the store warp in sub-blocks of kSubVec
+// granules (a multiple of the compute threads, so granule g is still written
+// by thread g % threads), each with its own barrier: the bulk store of
+// sub-block j drains while the warps write j + 1, and the stage turns over
+// one sub-block after the last write instead of one whole row.
+constexpr int kSubVec = DVLA_SUB * kFusedComputeThreads;
+constexpr int kMaxSub = DVLA_SUB ? 8 : 1;
+
 struct FusedSmem {
   uint64_t full[kFusedStages];
   uint64_t empty[kFusedStages];
@@ -216,7 +227,7 @@ struct FusedSmem {
   uint64_t afree[kASlots];
   uint64_t adoneB[kFusedStages];
   uint64_t cfullB[kFusedStages];
-  uint64_t bdone[kFusedStages];  // compute -> store warp, B row b % 3 written in SMEM
+  uint64_t bdone[kFusedStages][kMaxSub];  // compute -> store warp, B row b % 3 (sub-block) written
   uint64_t tdone[kRing];         // tail -> prep warp, (lse, target) of row k % kRing
   double ws[kASlots][kFusedComputeWarps];
   float wm[kASlots][kFusedComputeWarps];
@@ -398,6 +409,13 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
     const int lo = piece * piece_vec;
     return (nvec_row - lo < piece_vec) ? nvec_row - lo : piece_vec;
   };
+  // phase-B store sub-blocks of a piece of nvec granules (the last one takes
+  // the remainder; at most kMaxSub)
+  auto n_sub = [&](int nvec) {
+    if (kSubVec == 0) return 1;
+    const int k = (nvec + kSubVec - 1) / kSubVec;
+    return k < 1 ? 1 : (k > kMaxSub ? kMaxSub : k);
+  };
   const int64_t T = p.T;
   unsigned long long* dbg = g_dbg;
   const long long t_kernel = dbg ? clock64() : 0;
@@ -409,7 +427,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
       mbar_init(&S.empty[s], kFusedComputeWarps);
       mbar_init(&S.adoneB[s], kFusedComputeWarps);
       mbar_init(&S.cfullB[s], 1);
-      mbar_init(&S.bdone[s], kFusedComputeWarps);
+      for (int j = 0; j < kMaxSub; ++j) mbar_init(&S.bdone[s][j], kFusedComputeWarps);
     }
     for (int s = 0; s < kASlots; ++s) {
       mbar_init(&S.adoneA[s], kFusedComputeWarps);
@@ -463,13 +481,21 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
       op_of(n, nvr, L, &isB, &u);
       if (!isB) continue;
       const int s = static_cast<int>(n % kFusedStages);
-      mbar_wait(&S.bdone[nb % kFusedStages], static_cast<uint32_t>((nb / kFusedStages) & 1));
+      const int sb = nb % kFusedStages;
+      const uint32_t par = static_cast<uint32_t>((nb / kFusedStages) & 1);
       ++nb;
       const int piece = u % P;
-      // dlogits are not re-read here: keep L2 for the rows B still needs
-      tma_store_1d_evict_first(dl + row_of(u / P) * row_bytes + int64_t{16} * piece * piece_vec,
-                               buf(s), static_cast<uint32_t>(piece_len(piece)) * 16u, pol_ef);
-      bulk_commit();
+      const int nvec = piece_len(piece);
+      const int nsub = n_sub(nvec);
+      uint8_t* dst = dl + row_of(u / P) * row_bytes + int64_t{16} * piece * piece_vec;
+      for (int j = 0; j < nsub; ++j) {
+        mbar_wait(&S.bdone[sb][j], par);
+        const int lo = j * kSubVec, hi = (j == nsub - 1) ? nvec : lo + kSubVec;
+        // dlogits are not re-read here: keep L2 for the rows B still needs
+        tma_store_1d_evict_first(dst + int64_t{16} * lo, buf(s) + size_t{16} * lo,
+                                 static_cast<uint32_t>(hi - lo) * 16u, pol_ef);
+        bulk_commit();
+      }
       bulk_wait_read<0>();
       mbar_arrive_cnt(&S.empty[s], kFusedComputeWarps);
     }
@@ -725,10 +751,39 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
     ++b;
     const uint32_t mode = S.mode[sb];
     uint4* v = reinterpret_cast<uint4*>(buf(s));  // dlogits overwrite the piece in place
+    const int nsub = n_sub(nvec);
+    // sub-block j written: make this warp's generic SMEM writes visible to
+    // the bulk store and count the warp in
+    auto sub_done = [&](int j) {
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.bdone[sb][j]);
+    };
     if ((mode & 3u) != 1u) {
       // zero-gradient rows (A == 0 or clipped chunk): 0 * (onehot - p)
       const uint32_t z = (mode == 0u) ? 0u : FE::kNaN;
       for (int i = tid; i < nvec; i += kFusedComputeThreads) v[i] = make_uint4(z, z, z, z);
+      for (int j = 0; j < nsub; ++j) sub_done(j);
+    } else if (kSubVec != 0) {
+      const int li = S.tgt[sb] - elem0;
+      const bool here = li >= 0 && li < nvec * E;
+      const bool owner = here && tid == ((li / E) % kFusedComputeThreads);
+      float val = 0.f;
+      if (owner) {
+        const float pt = ex2f(fmaf(FE::get(v, li), kLog2e, -S.lseL[sb]));
+        val = S.cf[sb] * (1.0f - pt);
+      }
+      const float K = S.kval[sb];
+      const uint64_t nK2 = f2pack(-K, -K);
+      const uint32_t sgn = (mode & 0x80000000u) ? FE::kSign : 0u;
+      for (int j = 0; j < nsub; ++j) {
+        const int lo = j * kSubVec, hi = (j == nsub - 1) ? nvec : lo + kSubVec;
+#pragma unroll 2
+        for (int i = lo + tid; i < hi; i += kFusedComputeThreads)
+          v[i] = FE::grad(v[i], l2e2, nK2, sgn);
+        if (owner && li / E >= lo && li / E < hi) FE::put(v, li, val);
+        sub_done(j);
+      }
     } else {
       // target column: c * (1 - p_t), patched by the thread that owns it
       const int li = S.tgt[sb] - elem0;
@@ -746,13 +801,9 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
 #pragma unroll 2
       for (int i = tid; i < nvec; i += kFusedComputeThreads) v[i] = FE::grad(v[i], l2e2, nK2, sgn);
       if (owner) FE::put(v, li, val);
+      sub_done(0);  // the store warp frees the stage after its copy
     }
-    fence_proxy_async_smem();  // generic SMEM writes -> visible to the bulk store
-    __syncwarp();
-    if (lane == 0) {
-      mbar_arrive(&S.bdone[sb]);  // the store warp frees the stage after its copy
-      mbar_arrive(&S.adoneB[sb]);
-    }
+    if (lane == 0) mbar_arrive(&S.adoneB[sb]);
   }
   if (dbg && tid == 0) atomicAdd(dbg + 12, static_cast<unsigned long long>(clock64() - t_kernel));
   if (dbg && tid == 0 && g_dbg_cta) {
