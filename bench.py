@@ -642,8 +642,11 @@ def _swim_model(swim, world, roofline, sampler, optimizer):
                         "async": fit(sim.simulate(costs, "async", **akw), "async")}}
     # (2) calibrated: the live strict-alternation (sync) lane times are the
     # lanes' isolated costs; the model predicts the overlapped (async) run
+    # (the live trainer lane's time includes its gradient all-reduce; the
+    # model applies it after the pacing barrier instead)
     sl = swim["lanes"]["sync"]
-    cal = sim.LaneCosts(rollout_s=sl["rollout_time"], actor_s=sl["actor_time"],
+    cal = sim.LaneCosts(rollout_s=sl["rollout_time"],
+                        actor_s=max(sl["actor_time"] - costs.reduce_s, 1e-6),
                         reduce_s=costs.reduce_s, shared_slots=True, transitions_per_epoch=R)
     out["calibrated"] = {"rollout_s": cal.rollout_s, "actor_s": cal.actor_s,
                          "async": fit(sim.simulate(cal, "async", **akw), "async")}
