@@ -42,6 +42,9 @@ namespace dvla {
 #ifndef DVLA_SUB
 #define DVLA_SUB 0  // phase-B store sub-blocks, in granules per compute thread (0: one store per piece)
 #endif
+#ifndef DVLA_PDL
+#define DVLA_PDL 1  // programmatic dependent launch: adv -> fused -> epilogue overlap their launches
+#endif
 #ifndef DVLA_FUSED_CTAS
 #define DVLA_FUSED_CTAS 1
 #endif
@@ -83,12 +86,23 @@ __device__ unsigned long long* g_dbg_cta = nullptr;  // per-CTA (start, end) glo
 constexpr long long kLpPending = 0x7f7f7f7f7f7f7f7fll;
 constexpr long long kNaN64 = 0x7ff8000000000000ll;
 
+// Programmatic dependent launch (PDL): a kernel launched with the
+// programmatic-serialization attribute may start while its predecessor in
+// the stream still runs; it must pass pdl_wait() before touching anything the
+// predecessor writes.  pdl_trigger() lets the successor launch early.  Both
+// are no-ops without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------------ advantages
 // (also marks n_fill token log-probs pending for the fused kernel's polls)
 __global__ void tok_adv_kernel(const float* __restrict__ rewards, int64_t n_groups, int64_t G,
                                double delta, double* __restrict__ adv,
                                uint32_t* __restrict__ reward_bad, double* __restrict__ lp_fill,
                                int64_t n_fill) {
+  pdl_trigger();  // the fused kernel waits (pdl_wait) where it reads what this writes
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   for (int64_t i = g; i < n_fill; i += gridDim.x * (int64_t)blockDim.x)
     reinterpret_cast<long long*>(lp_fill)[i] = kLpPending;
@@ -440,6 +454,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
 
   const uint8_t* logits = static_cast<const uint8_t*>(p.logits);
   uint8_t* dl = static_cast<uint8_t*>(p.dlogits);
+  pdl_trigger();  // the epilogue may launch now; it waits for this grid to finish
 
   // --------------------------------------------------------- loader warp
   if (warp == kWarpLoader) {
@@ -509,6 +524,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
   // never waits on anything but its own compute warps) and leaves (lse,
   // target) in the ring for the prep warp.
   if (warp == kTailWarp) {
+    pdl_wait();  // lp_tok's pending fill (tok_adv_kernel) precedes every publish
     for (int k = 0; k < nloc; ++k) {
       const int64_t r = row_of(k);
       float mw[P];
@@ -575,6 +591,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
   // once per piece of the row.
   if (warp == kPrepWarp) {
     if (!write_dl) return;
+    pdl_wait();  // advantages and the lp_tok pending fill
     const uint64_t t_start = globaltimer_ns();
     for (int k = 0; k < nloc; ++k) {
       const int64_t r = row_of(k);
@@ -988,6 +1005,7 @@ struct EpiParams {
 constexpr int kEpiThreads = 512;
 
 __global__ void __launch_bounds__(kEpiThreads) grpo_epilogue_kernel(EpiParams e) {
+  pdl_wait();  // everything below reads the fused kernel's results
   __shared__ double s_loss[kEpiThreads], s_rho[kEpiThreads];
   __shared__ unsigned char s_clip[kEpiThreads];
   __shared__ unsigned long long s_first_reward, s_first_traj;
@@ -1150,6 +1168,25 @@ static FusedGeom fused_geom(int64_t V, size_t esz) {
 
 using FusedKernelFn = void (*)(TokParams, uint32_t, int, int, int);
 
+// Launch with the programmatic-stream-serialization attribute (PDL) when
+// DVLA_PDL: the kernel may begin while the previous kernel in the stream is
+// still running (see pdl_wait / pdl_trigger).
+template <class... KArgs, class... Args>
+static cudaError_t launch_maybe_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                    cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = DVLA_PDL ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 template <class TE>
 static FusedKernelFn fused_kernel_for(int pieces) {
   switch (pieces) {
@@ -1256,8 +1293,9 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
     // B ops (deadlock freedom), <= kRing P - 1 for the (lse, target) ring
     const int P = geom.pieces;
     const int lag_p = std::min(std::max(lag, 2 * P - 1), kRing * P - 1);
-    kern<<<grid, kFusedThreadsWS, geom.smem, stream>>>(p, geom.stage_bytes, geom.piece_vec,
-                                                       want_dl ? 1 : 0, std::max(lag_p, 2));
+    DVLA_CUDA_TRY(launch_maybe_pdl(kern, dim3(grid), dim3(kFusedThreadsWS), geom.smem, stream,
+                                   p, geom.stage_bytes, geom.piece_vec, want_dl ? 1 : 0,
+                                   std::max(lag_p, 2)));
     prof_end(stream, stop);
     if (int rc = launch_check("tok_fused_kernel")) return rc;
     if (!want_dl) {
@@ -1300,7 +1338,11 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
   e.w = p.w;
   e.clip_eps = clip_eps;
   e.kl_coeff = kl_coeff;
-  grpo_epilogue_kernel<<<1, kEpiThreads, 0, stream>>>(e);
+  if (fused) {
+    DVLA_CUDA_TRY(launch_maybe_pdl(grpo_epilogue_kernel, dim3(1), dim3(kEpiThreads), 0, stream, e));
+  } else {
+    grpo_epilogue_kernel<<<1, kEpiThreads, 0, stream>>>(e);
+  }
   return launch_check("grpo_epilogue_kernel");
 }
 
