@@ -297,7 +297,43 @@ def _bench_replication(world, rank, dev, barrier, max_over_ranks, iters=5):
                              "peak_source": "B200_PROFILING.md measured peer copy (770 GB/s/dir)"},
                 "ce_fanout_gbs_per_receiver": S / (sorted(ce)[1] / 1e3) / 1e9})
     out["multicast"] = _bench_multicast(S, src, rank, world, barrier, max_over_ranks)
+    if world >= 4:
+        try:
+            out["c3_split"] = _bench_c3_split(S, src, rank, world, barrier, max_over_ranks)
+        except Exception as e:  # noqa: BLE001 - a secondary leg never sinks the line
+            out["c3_split"] = {"error": repr(e)[:300]}
     return out
+
+
+def _bench_c3_split(S, src, rank, world, barrier, max_over_ranks, iters=4):
+    """BASELINE config 3 layout: learners on ranks 0 and 1 each source half
+    of the weight region to the replicas on ranks 2..N-1 (the two chains run
+    the replicas in opposite orders), bit-exact on every replica."""
+    import torch
+    from paper_2605_13276_b200.replicate import SplitReplicator, bytes_equal
+    reps = list(range(2, world))
+    chains = [[0] + reps, [1] + reps[::-1]]
+    rep = SplitReplicator(S, chains, n_buffers=1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    for it in range(iters + 1):
+        barrier()
+        e0.record()
+        rep.broadcast(src if rank in (0, 1) else None, it)
+        e1.record()
+        torch.cuda.synchronize()
+        t = max_over_ranks(e0.elapsed_time(e1))
+        if it:
+            times.append(t)
+    rep.check()
+    ok = rank < 2 or bytes_equal(src, rep.replica(0))[0] == 0
+    ok_all = max_over_ranks(0.0 if ok else 1.0) == 0.0
+    barrier()
+    rep.close()
+    ms = sorted(times)[len(times) // 2]
+    return {"layout": f"learners 0,1 -> replicas {reps[0]}..{reps[-1]} (two half-region chains)",
+            "gbs_per_replica": S / (ms / 1e3) / 1e9, "ms": ms, "bit_exact": ok_all,
+            "frac_of_peer_copy": S / (ms / 1e3) / 1e9 / NVLINK_PEER_GBS}
 
 
 def _bench_multicast(S, src, rank, world, barrier, max_over_ranks, iters=4):
