@@ -101,9 +101,12 @@ __device__ __forceinline__ void pdl_trigger() {
 __global__ void tok_adv_kernel(const float* __restrict__ rewards, int64_t n_groups, int64_t G,
                                double delta, double* __restrict__ adv,
                                uint32_t* __restrict__ reward_bad, double* __restrict__ lp_fill,
-                               int64_t n_fill) {
+                               int64_t n_fill, uint32_t* __restrict__ err) {
   pdl_trigger();  // the fused kernel waits (pdl_wait) where it reads what this writes
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // the error word of this call: every writer (tail / prep warps, unfused
+  // kernels) runs after this kernel, so no separate memset is needed
+  if (g == 0 && err) *err = 0u;
   for (int64_t i = g; i < n_fill; i += gridDim.x * (int64_t)blockDim.x)
     reinterpret_cast<long long*>(lp_fill)[i] = kLpPending;
   if (g >= n_groups) return;
@@ -1113,7 +1116,6 @@ struct TokWorkspace {
   uint32_t* reward_bad;
   uint32_t* err;
   size_t bytes;
-  size_t zero_off, zero_bytes;  // region memset every call (err)
 };
 
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -1132,9 +1134,7 @@ static TokWorkspace carve(void* base, int64_t n_groups, int64_t G, int64_t C, in
   w.lse = reinterpret_cast<double*>(take(R * 8));
   w.coeff = reinterpret_cast<double*>(take(nq * 8));
   w.reward_bad = reinterpret_cast<uint32_t*>(take(n_groups * 4));
-  w.zero_off = off;
   w.err = reinterpret_cast<uint32_t*>(take(16));
-  w.zero_bytes = off - w.zero_off;
   w.bytes = off;
   return w;
 }
@@ -1251,14 +1251,12 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
   p.clip_eps = clip_eps;
   p.kl_coeff = kl_coeff;
 
-  DVLA_CUDA_TRY(cudaMemsetAsync(static_cast<uint8_t*>(workspace) + ws.zero_off, 0,
-                                ws.zero_bytes, stream));
   {
     const int thr = 128;
     const int64_t fill_blocks = std::min<int64_t>((R + thr - 1) / thr, 4 * 148);
     const int64_t blocks = std::max<int64_t>((n_groups + thr - 1) / thr, fill_blocks);
     tok_adv_kernel<<<(unsigned)blocks, thr, 0, stream>>>(rewards, n_groups, G, adv_eps, ws.adv,
-                                                          ws.reward_bad, ws.lp_tok, R);
+                                                          ws.reward_bad, ws.lp_tok, R, ws.err);
     if (int rc = launch_check("tok_adv_kernel")) return rc;
   }
 
@@ -1384,7 +1382,7 @@ extern "C" int dvla_group_advantages(const float* rewards, int64_t n_groups, int
   const int thr = 128;
   tok_adv_kernel<<<(unsigned)((n_groups + thr - 1) / thr), thr, 0,
                    static_cast<cudaStream_t>(stream)>>>(rewards, n_groups, G, delta, adv,
-                                                        reward_bad, nullptr, 0);
+                                                        reward_bad, nullptr, 0, nullptr);
   return launch_check("tok_adv_kernel");
 }
 
