@@ -554,6 +554,33 @@ def _bench_weight_plane_cpu(n_params=250_000_000):
             "path": "snapshot_from_params -> ControlPlane.broadcast (WIRE) -> take_newest"}
 
 
+def _bench_allocator(n_ops=20_000, capacity=1 << 18, reps=20):
+    """§8 d (iv): the dual-pool allocator's batched trace (csrc/arena.cpp,
+    host C++ -- integer bookkeeping, no device kernel) on the reference's
+    random workload, bitwise against the C restatement of alloc_trace_run
+    timed beside it on one host thread."""
+    import numpy as np
+
+    from oracle.arena import alloc_trace
+    from paper_2605_13276_b200.pools import arena_trace, random_workload
+    wl = random_workload(0, n_ops, capacity)
+
+    def best(fn):
+        out, ts = None, []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            out = fn(capacity, *wl)
+            ts.append(time.perf_counter() - t0)
+        return out, min(ts)
+    (ok, off, fin), t_ours = best(arena_trace)
+    (ok2, off2, fin2), t_or = best(alloc_trace)
+    same = bool(np.array_equal(ok, ok2) and np.array_equal(off, off2) and fin == fin2)
+    return {"workload": f"random_workload(0, {n_ops}, 2^18) (reference pools.py:219-231)",
+            "ops_per_s": n_ops / t_ours, "bit_exact_vs_oracle": same,
+            "cpu_baseline": {"ops_per_s": n_ops / t_or, "cores": 1, "kind": "port",
+                             "impl": "oracle/arena_oracle.c (alloc_trace_run restated)"}}
+
+
 def _bench_allreduce(world, dev, barrier, max_over_ranks, nbytes=1 << 30, iters=5):
     """NCCL all-reduce of a learner gradient bucket (f32), busbw."""
     import torch
@@ -855,6 +882,7 @@ def run_ours(a):
 
     if rank == 0 and world == 1 and not a.no_cpu and isinstance(repl, dict):
         repl["cpu_baseline"] = _guarded(_bench_weight_plane_cpu)
+    allocator = _guarded(_bench_allocator) if rank == 0 and not a.no_cpu else None
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -886,6 +914,7 @@ def run_ours(a):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "replication": repl, "grad_allreduce": allreduce, "swimlane": swim,
             "gauss_c3": gauss, "sampler": sampler, "optimizer": optimizer,
+            "allocator": allocator,
             "gpu_launches": 3 * a.steps, "clocks": clk,
             "loss": st["loss"], "mean_ratio": st["mean_ratio"],
             "clip_fraction": st["clip_fraction"],

@@ -159,3 +159,29 @@ def test_row_sum_is_numpy_pairwise_bitwise(T):
     got = x.sum(axis=1)
     for i in range(5):
         assert got[i] == _pairwise(list(x[i])), T
+
+
+def test_oracle_alloc_trace_matches_reference_golden_bitwise():
+    """The C restatement of alloc_trace_run (oracle/arena_oracle.c) against
+    the reference's own traces (tests/golden/alloc_traces.npz)."""
+    from oracle.arena import alloc_trace
+    from paper_2605_13276_b200.pools import random_workload
+    g = golden("alloc_traces")
+    for seed in (0, 1, 11, 17, 5):
+        cap, n = int(g[f"s{seed}_cap"]), int(g[f"s{seed}_n"])
+        ok, off, fin = alloc_trace(cap, *random_workload(seed, n, cap))
+        assert np.array_equal(ok, g[f"s{seed}_ok"]), seed
+        assert np.array_equal(off, g[f"s{seed}_off"]), seed
+        assert fin == tuple(int(x) for x in g[f"s{seed}_final"]), seed
+
+
+def test_oracle_alloc_trace_edge_cases():
+    from oracle.arena import alloc_trace
+    # free with nothing live, exact fit, no fit, and a full coalesce back to one extent
+    ok, off, fin = alloc_trace(256, [0, 1, 1, 1, 0, 0], [0, 128, 128, 1, 0, 0],
+                               [1, 64, 1, 1, 1, 1], [0, 0, 0, 0, 5, 0])
+    assert ok.tolist() == [2, 1, 1, 0, 3, 3]
+    assert off.tolist() == [-1, 0, 128, -1, 128, 0]
+    assert fin == (256, 256, 1)
+    ok, off, fin = alloc_trace(100, [], [], [], [])
+    assert len(ok) == 0 and fin == (100, 100, 1)
