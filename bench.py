@@ -697,27 +697,35 @@ def _swim_model(swim, world, roofline, sampler, optimizer):
                 "live_trajectories_per_s": live["trajectories_per_s"],
                 "fit": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in f.items()}}
 
-    akw = {"epochs": ep, "staleness_limit": 1, "nodes": world, "per_node_slots": True}
+    # one closed loop per GPU, coupled only through the gradient mean: each
+    # GPU is modelled as its own node with the all-reduce inside the trainer
+    # lane (the reference's multi-node pacing model counts versions, not
+    # per-GPU epochs)
+    akw = {"epochs": ep, "staleness_limit": 1}
+
+    def per_gpu(c, reduce_s):
+        return sim.LaneCosts(rollout_s=c.rollout_s, actor_s=c.actor_s + reduce_s,
+                             shared_slots=True, transitions_per_epoch=R)
+    a1 = per_gpu(costs, costs.reduce_s)
     # (1) analytic: lane costs from the measured kernel / GEMM / link rates
-    out = {"analytic": {"rates": rates.__dict__, "rollout_s": costs.rollout_s,
-                        "actor_s": costs.actor_s, "reduce_s": costs.reduce_s,
-                        "sync": fit(sim.simulate(costs, "sync", epochs=ep), "sync"),
-                        "async": fit(sim.simulate(costs, "async", **akw), "async")}}
+    out = {"analytic": {"rates": rates.__dict__, "rollout_s": a1.rollout_s,
+                        "actor_s": a1.actor_s, "reduce_s": costs.reduce_s,
+                        "sync": fit(sim.simulate(a1, "sync", epochs=ep), "sync"),
+                        "async": fit(sim.simulate(a1, "async", **akw), "async")}}
     # (2) calibrated: the live strict-alternation (sync) lane times are the
-    # lanes' isolated costs; the model predicts the overlapped (async) run
-    # (the live trainer lane's time includes its gradient all-reduce; the
-    # model applies it after the pacing barrier instead)
+    # lanes' isolated costs (the trainer's includes its all-reduce); the
+    # model predicts the overlapped (async) run
     sl = swim["lanes"]["sync"]
-    cal = sim.LaneCosts(rollout_s=sl["rollout_time"],
-                        actor_s=max(sl["actor_time"] - costs.reduce_s, 1e-6),
-                        reduce_s=costs.reduce_s, shared_slots=True, transitions_per_epoch=R)
+    cal = sim.LaneCosts(rollout_s=sl["rollout_time"], actor_s=sl["actor_time"],
+                        shared_slots=True, transitions_per_epoch=R)
     out["calibrated"] = {"rollout_s": cal.rollout_s, "actor_s": cal.actor_s,
                          "async": fit(sim.simulate(cal, "async", **akw), "async")}
-    # the calibrated lanes at 8 GPUs (one closed loop per GPU, NCCL gradient mean)
+    # the calibrated lanes at 8 GPUs: this run's all-reduce swapped for 8 GPUs'
     c8 = sim.b200_costs(N_GROUPS, G, C, T, V, 4096, nodes=8, rates=rates)
-    cal8 = sim.LaneCosts(rollout_s=cal.rollout_s, actor_s=cal.actor_s, reduce_s=c8.reduce_s,
+    cal8 = sim.LaneCosts(rollout_s=cal.rollout_s,
+                         actor_s=max(cal.actor_s - costs.reduce_s, 1e-6) + c8.reduce_s,
                          shared_slots=True, transitions_per_epoch=R)
-    r8 = sim.simulate(cal8, "async", epochs=ep, staleness_limit=1, nodes=8, per_node_slots=True)
+    r8 = sim.simulate(cal8, "async", **akw)
     out["predicted_8gpu_trajectories_per_s_total"] = r8.throughput * per_traj * 8
     return out
 
