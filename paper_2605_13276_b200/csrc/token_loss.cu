@@ -52,6 +52,25 @@ constexpr int kFusedComputeWarps = DVLA_FUSED_W;
 constexpr int kFusedCtasPerSm = DVLA_FUSED_CTAS;  // resident fused CTAs per SM
 constexpr size_t kFusedSmemCap = (228u * 1024u) / DVLA_FUSED_CTAS - 1024u;
 constexpr int kFusedComputeThreads = kFusedComputeWarps * 32;
+#ifndef DVLA_AB
+#define DVLA_AB 0  // 1: compute warps split into an A-op group and a B-op group
+#endif
+// With DVLA_AB the first half of the compute warps run only A ops and the
+// second half only B ops, so the two phases' exponentials overlap instead of
+// every warp meeting at every op boundary.  Each group arrives on the
+// per-op barriers with a count that makes up the full compute-warp total.
+constexpr int kAWarps = DVLA_AB ? kFusedComputeWarps / 2 : kFusedComputeWarps;
+constexpr int kBWarps = DVLA_AB ? kFusedComputeWarps - kAWarps : kFusedComputeWarps;
+constexpr int kAThreads = kAWarps * 32, kBThreads = kBWarps * 32;
+constexpr uint32_t kAArrive = kFusedComputeWarps / kAWarps;
+constexpr uint32_t kBArrive = kFusedComputeWarps / kBWarps;
+static_assert(kFusedComputeWarps % kAWarps == 0 && kFusedComputeWarps % kBWarps == 0,
+              "compute warps must split evenly");
+static_assert(!(DVLA_AB && DVLA_SUB), "the A/B split and B sub-blocks are exclusive");
+#ifndef DVLA_HALVES
+#define DVLA_HALVES 0  // 1: each piece lands as two TMA halves; compute starts on the first
+#endif
+static_assert(!(DVLA_HALVES && (DVLA_AB || DVLA_SUB)), "DVLA_HALVES stands alone");
 constexpr int kFusedStages = 3;    // SMEM row stages and B coefficient slots
 constexpr int kASlots = 8;         // A-row partial slots (coef-warp slack)
 constexpr uint64_t kSpinTimeoutNs = 4000000000ull;  // 4 s: report, never hang
@@ -239,6 +258,8 @@ constexpr int kMaxSub = DVLA_SUB ? 8 : 1;
 
 struct FusedSmem {
   uint64_t full[kFusedStages];
+  uint64_t fullB[kFusedStages];  // DVLA_AB: B-op arrivals (each group sees only its own phases)
+  uint64_t full2[kFusedStages];  // DVLA_HALVES: second half of the piece landed
   uint64_t empty[kFusedStages];
   uint64_t adoneA[kASlots];
   uint64_t afree[kASlots];
@@ -441,6 +462,8 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
   if (tid == 0) {
     for (int s = 0; s < kFusedStages; ++s) {
       mbar_init(&S.full[s], 1);
+      mbar_init(&S.fullB[s], 1);
+      mbar_init(&S.full2[s], 1);
       mbar_init(&S.empty[s], kFusedComputeWarps);
       mbar_init(&S.adoneB[s], kFusedComputeWarps);
       mbar_init(&S.cfullB[s], 1);
@@ -476,11 +499,29 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
         const int piece = u % P;
         const uint32_t bytes = static_cast<uint32_t>(piece_len(piece)) * 16u;
         const uint8_t* src = logits + row_of(u / P) * row_bytes + int64_t{16} * piece * piece_vec;
-        mbar_arrive_expect_tx(&S.full[s], bytes);
+        // with DVLA_AB, B ops land on their own barrier: a group that skips
+        // the other group's ops must never see a phase of them (parity)
+        uint64_t* fb = (DVLA_AB && isB) ? &S.fullB[s] : &S.full[s];
+#if DVLA_HALVES
+        // two halves on two barriers: the compute warps start on the first
+        const uint32_t h0 = (bytes / 32u) * 16u;
+        if (h0) {
+          mbar_arrive_expect_tx(fb, h0);
+          if (isB) tma_load_1d_evict_first(buf(s), src, h0, fb, pol);
+          else tma_load_1d(buf(s), src, h0, fb);
+        } else {
+          mbar_arrive(fb);
+        }
+        mbar_arrive_expect_tx(&S.full2[s], bytes - h0);
+        if (isB) tma_load_1d_evict_first(buf(s) + h0, src + h0, bytes - h0, &S.full2[s], pol);
+        else tma_load_1d(buf(s) + h0, src + h0, bytes - h0, &S.full2[s]);
+#else
+        mbar_arrive_expect_tx(fb, bytes);
         if (isB)  // second (last) read of the piece: from L2, then evict
-          tma_load_1d_evict_first(buf(s), src, bytes, &S.full[s], pol);
+          tma_load_1d_evict_first(buf(s), src, bytes, fb, pol);
         else  // (an evict_last hint here measured no better: the lag keeps rows in L2)
-          tma_load_1d(buf(s), src, bytes, &S.full[s]);
+          tma_load_1d(buf(s), src, bytes, fb);
+#endif
       }
     }
     return;
@@ -542,8 +583,8 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
         tgt = S.tgta[sa];
         const float x = S.xt[sa];
         if (!isnan(x)) xt_f = x;  // the piece that holds the target column
-        mw[pc] = (lane < kFusedComputeWarps) ? S.wm[sa][lane] : -INFINITY;
-        sw[pc] = (lane < kFusedComputeWarps) ? S.ws[sa][lane] : 0.0;
+        mw[pc] = (lane < kAWarps) ? S.wm[sa][lane] : -INFINITY;
+        sw[pc] = (lane < kAWarps) ? S.ws[sa][lane] : 0.0;
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.afree[sa]);  // partial slot sa consumed
       }
@@ -552,15 +593,15 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
       float mlane = -INFINITY;
 #pragma unroll
       for (int pc = 0; pc < P; ++pc) {
-        bad |= lane < kFusedComputeWarps && (isnan(sw[pc]) || mw[pc] == INFINITY);
-        if (lane < kFusedComputeWarps && sw[pc] > 0.0) mlane = fmaxf(mlane, mw[pc]);
+        bad |= lane < kAWarps && (isnan(sw[pc]) || mw[pc] == INFINITY);
+        if (lane < kAWarps && sw[pc] > 0.0) mlane = fmaxf(mlane, mw[pc]);
       }
       const bool poison = __any_sync(0xffffffffu, bad);
       const float M = warp_max_f32(mlane);
       double term = 0.0;
 #pragma unroll
       for (int pc = 0; pc < P; ++pc)
-        if (lane < kFusedComputeWarps && sw[pc] > 0.0)
+        if (lane < kAWarps && sw[pc] > 0.0)
           term += sw[pc] * static_cast<double>(ex2f((mw[pc] - M) * kLog2e));
       term = warp_sum_f64(term);
       if (lane == 0) {
@@ -676,6 +717,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
 
   // ------------------------------------------------------- compute warps
   int a = 0, b = 0;  // A / B op counters (virtual rows)
+  int uses[kFusedStages] = {};  // DVLA_AB: this group's uses of each stage so far
   const uint64_t l2e2 = f2pack(kLog2e, kLog2e);
   for (int n = 0; n < nops; ++n) {
     const int s = static_cast<int>(n % kFusedStages);
@@ -683,12 +725,15 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
     bool isB;
     int u;
     op_of(n, nvr, L, &isB, &u);
+    if (DVLA_AB && (isB != (warp >= kAWarps))) continue;  // the other group's op
     const int piece = u % P;
     const int nvec = piece_len(piece);
     const int elem0 = piece * piece_vec * E;  // first element of this piece in its row
     {
       DBG_T0();
-#if DVLA_FULL_SPIN
+#if DVLA_AB
+      mbar_wait(isB ? &S.fullB[s] : &S.full[s], static_cast<uint32_t>(uses[s]++ & 1));
+#elif DVLA_FULL_SPIN
       while (!mbar_test_wait(&S.full[s], ph)) {
       }
 #else
@@ -708,12 +753,29 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
       const uint4* v = reinterpret_cast<const uint4*>(buf(s));
       uint32_t mx = FE::kNegInf;
       uint64_t acc[4] = {0, 0, 0, 0};  // packed (0.f, 0.f)
+#if DVLA_HALVES
+      const int half = nvec / 2;
 #pragma unroll 2
-      for (int i = tid; i < nvec; i += kFusedComputeThreads) {
+      for (int i = tid; i < half; i += kAThreads) {
         const uint4 x = v[i];
         mx = FE::max16(mx, x);
         FE::exps(x, l2e2, 0, acc);
       }
+      mbar_wait(&S.full2[s], ph);
+#pragma unroll 2
+      for (int i = half + tid; i < nvec; i += kAThreads) {
+        const uint4 x = v[i];
+        mx = FE::max16(mx, x);
+        FE::exps(x, l2e2, 0, acc);
+      }
+#else
+#pragma unroll 2
+      for (int i = tid; i < nvec; i += kAThreads) {
+        const uint4 x = v[i];
+        mx = FE::max16(mx, x);
+        FE::exps(x, l2e2, 0, acc);
+      }
+#endif
       const float wmax = warp_max_f32(FE::maxf(mx));
       float m = 0.f;  // frame of this warp's partial
       if (!(wmax <= kFrameHi) || (wmax < kFrameLo && wmax > -INFINITY)) {  // warp-uniform
@@ -721,8 +783,13 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
         const float mL = m * kLog2e;
         const uint64_t nmL2 = f2pack(-mL, -mL);
         acc[0] = acc[1] = acc[2] = acc[3] = 0;
+#if DVLA_HALVES
+        for (int i = tid; i < nvec / 2; i += kAThreads) FE::exps(v[i], l2e2, nmL2, acc);
+        for (int i = nvec / 2 + tid; i < nvec; i += kAThreads) FE::exps(v[i], l2e2, nmL2, acc);
+#else
 #pragma unroll 2
-        for (int i = tid; i < nvec; i += kFusedComputeThreads) FE::exps(v[i], l2e2, nmL2, acc);
+        for (int i = tid; i < nvec; i += kAThreads) FE::exps(v[i], l2e2, nmL2, acc);
+#endif
       }
       double part;
       {
@@ -738,7 +805,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
       const bool here = tok_ok && li >= 0 && li < nvec * E;
       const float xt_v = (tid == 0 && here) ? FE::get(buf(s), li) : __int_as_float(0x7fc00000);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[s]);
+      if (lane == 0) mbar_arrive_cnt(&S.empty[s], kAArrive);
       part = warp_sum_f64(part);
       const int sa = static_cast<int>(a % kASlots);
       if (a >= kASlots) {  // the tail warp has read A piece a-8's partials
@@ -754,7 +821,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
       if (lane == 0) {
         S.wm[sa][warp] = m;
         S.ws[sa][warp] = part;
-        mbar_arrive(&S.adoneA[sa]);
+        mbar_arrive_cnt(&S.adoneA[sa], kAArrive);
       }
       continue;
     }
@@ -769,6 +836,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
       if (tid == 0) { DBG_ADD(1); }
     }
     ++b;
+    const int gt = DVLA_AB ? tid - kAThreads : tid;  // thread index within the B group
     const uint32_t mode = S.mode[sb];
     uint4* v = reinterpret_cast<uint4*>(buf(s));  // dlogits overwrite the piece in place
     const int nsub = n_sub(nvec);
@@ -777,12 +845,13 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
     auto sub_done = [&](int j) {
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.bdone[sb][j]);
+      if (lane == 0) mbar_arrive_cnt(&S.bdone[sb][j], kBArrive);
     };
     if ((mode & 3u) != 1u) {
       // zero-gradient rows (A == 0 or clipped chunk): 0 * (onehot - p)
       const uint32_t z = (mode == 0u) ? 0u : FE::kNaN;
-      for (int i = tid; i < nvec; i += kFusedComputeThreads) v[i] = make_uint4(z, z, z, z);
+      if (DVLA_HALVES) mbar_wait(&S.full2[s], ph);  // the second half must land first
+      for (int i = gt; i < nvec; i += kBThreads) v[i] = make_uint4(z, z, z, z);
       for (int j = 0; j < nsub; ++j) sub_done(j);
     } else if (kSubVec != 0) {
       const int li = S.tgt[sb] - elem0;
@@ -808,22 +877,35 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
       // target column: c * (1 - p_t), patched by the thread that owns it
       const int li = S.tgt[sb] - elem0;
       const bool here = li >= 0 && li < nvec * E;
-      const bool owner = here && tid == ((li / E) % kFusedComputeThreads);
-      float val = 0.f;
-      if (owner) {
-        const float pt = ex2f(fmaf(FE::get(v, li), kLog2e, -S.lseL[sb]));
-        val = S.cf[sb] * (1.0f - pt);
-      }
       // -c * p_v = -sign(c) * 2^(x*log2e - (lse*log2e - log2|c|))
       const float K = S.kval[sb];
       const uint64_t nK2 = f2pack(-K, -K);
       const uint32_t sgn = (mode & 0x80000000u) ? FE::kSign : 0u;
+      float val = 0.f;
+      auto target_val = [&]() {
+        const float pt = ex2f(fmaf(FE::get(v, li), kLog2e, -S.lseL[sb]));
+        return S.cf[sb] * (1.0f - pt);
+      };
+#if DVLA_HALVES
+      const int half = nvec / 2, g = li / E;
+      const bool owner = here && gt == ((g < half ? g : g - half) % kBThreads);
+      if (owner && g < half) val = target_val();
 #pragma unroll 2
-      for (int i = tid; i < nvec; i += kFusedComputeThreads) v[i] = FE::grad(v[i], l2e2, nK2, sgn);
+      for (int i = gt; i < half; i += kBThreads) v[i] = FE::grad(v[i], l2e2, nK2, sgn);
+      mbar_wait(&S.full2[s], ph);
+      if (owner && g >= half) val = target_val();
+#pragma unroll 2
+      for (int i = half + gt; i < nvec; i += kBThreads) v[i] = FE::grad(v[i], l2e2, nK2, sgn);
+#else
+      const bool owner = here && gt == ((li / E) % kBThreads);
+      if (owner) val = target_val();
+#pragma unroll 2
+      for (int i = gt; i < nvec; i += kBThreads) v[i] = FE::grad(v[i], l2e2, nK2, sgn);
+#endif
       if (owner) FE::put(v, li, val);
       sub_done(0);  // the store warp frees the stage after its copy
     }
-    if (lane == 0) mbar_arrive(&S.adoneB[sb]);
+    if (lane == 0) mbar_arrive_cnt(&S.adoneB[sb], kBArrive);
   }
   if (dbg && tid == 0) atomicAdd(dbg + 12, static_cast<unsigned long long>(clock64() - t_kernel));
   if (dbg && tid == 0 && g_dbg_cta) {
