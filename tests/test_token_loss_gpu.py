@@ -346,3 +346,42 @@ def test_random_shapes_match_oracle(seed):
                  binary=bool(rng.random() < 0.5), ids=ids)
     rtol = 1e-5 if dtype == torch.float32 else 1e-2
     _check(*case, dtype, fused=fused, rtol=rtol, cfg_kw={"kl_coeff": kl})
+
+
+def test_back_to_back_launches_see_their_own_inputs():
+    """The fused kernel and the epilogue are launched with programmatic
+    dependent launch: three calls queued back to back on one stream (no
+    host sync between them) with different rewards / behaviour log-probs /
+    logits must each match the oracle on their own inputs -- no call may
+    read the previous call's advantages, pending markers or chunk lps."""
+    import torch
+    from paper_2605_13276_b200 import grpo
+    dev = torch.device("cuda", 0)
+    n_groups, G, C, T, V = 6, 4, 1, 8, 4096
+    cases = [_case(40 + k, n_groups, G, C, T, V, torch.bfloat16, ids=np.arange(n_groups))
+             for k in range(3)]
+    tl = grpo.TokenLoss(n_groups, G, C, T, V, grpo.GrpoConfig(group_size=G),
+                        dtype=torch.bfloat16, device=dev)
+    tl.set_groups(np.arange(n_groups))
+    outs = []
+    for x, tokens, blp, rewards, _ in cases:
+        lg = torch.from_numpy(x).to(dev, torch.bfloat16).reshape(-1, V)
+        dl = torch.empty_like(lg)
+        rw = torch.from_numpy(rewards.reshape(-1)).to(dev)
+        tl.launch(lg, torch.from_numpy(tokens.reshape(-1)).to(dev),
+                  torch.from_numpy(blp.reshape(-1)).to(dev), rw, dl)
+        outs.append((dl, tl.lp_chunk.clone(), tl.stats_dev.clone(), rw))
+    torch.cuda.synchronize()
+    from paper_2605_13276_b200 import _lib
+    for (x, tokens, blp, rewards, ids), (dl, lp, st, _) in zip(cases, outs):
+        oloss, odl, ost = O.grpo_token_grad(x, tokens, blp, rewards, ids)
+        np.testing.assert_allclose(lp.cpu().numpy(), ost["lp_chunk"].reshape(-1),
+                                   rtol=1e-9, atol=1e-5)
+        sv = st.cpu().numpy()
+        assert sv[_lib.ST_ABORT] == 0 and sv[_lib.ST_KERNEL_ERR] == 0
+        assert sv[_lib.ST_CHUNK_COUNT] == ost["n_chunks"]
+        scale = sum(abs(v) for v in ost["coeff"].ravel()) / max(ost["coeff"].size, 1)
+        assert abs(sv[_lib.ST_LOSS] - oloss) <= 1e-5 * max(abs(oloss), scale, 1e-12)
+        odl = odl.reshape(dl.shape)
+        err = np.abs(dl.float().cpu().numpy() - odl)
+        assert np.all(err <= 1e-2 * np.abs(odl) + 1e-2 * np.abs(odl).max())
