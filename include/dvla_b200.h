@@ -92,6 +92,14 @@ int dvla_group_advantages(const float* rewards, int64_t n_groups, int64_t G, dou
 /* Workspace bytes for dvla_token_loss_fwd_bwd. */
 size_t dvla_token_loss_workspace_bytes(int64_t n_groups, int64_t G, int64_t C, int64_t T);
 
+/* Byte offsets inside that workspace of what the last dvla_token_loss_fwd_bwd
+ * left there: offsets[0] adv f64 [n_groups*G] (input group order),
+ * offsets[1] lp_tok f64 [rows] (x[r, tok_r] - lse_r), offsets[2] lse f64
+ * [rows] (forward-only / unfused paths), offsets[3] coeff f64 [n_groups*G*C]
+ * (d loss / d lp_chunk, the weight w included).  For parity checks. */
+int dvla_token_loss_workspace_layout(int64_t n_groups, int64_t G, int64_t C, int64_t T,
+                                     size_t* offsets);
+
 /* Fused action-token GRPO loss forward + backward (the north-star kernel).
  * Replaces, for the token head, the chain grpo.grpo_grad (grpo.py:217-294)
  * -> policy.log_prob_of (policy.py:161-172) -> kernels.chunk_log_prob

@@ -79,6 +79,8 @@ dvla_advantages = _proto("dvla_advantages", [_vp, _i64, _i64, _f64, _vp, _vp])
 dvla_group_advantages = _proto("dvla_group_advantages", [_vp, _i64, _i64, _f64, _vp, _vp, _vp])
 dvla_token_loss_workspace_bytes = _proto(
     "dvla_token_loss_workspace_bytes", [_i64, _i64, _i64, _i64], _sz)
+dvla_token_loss_workspace_layout = _proto(
+    "dvla_token_loss_workspace_layout", [_i64, _i64, _i64, _i64, C.POINTER(_sz)])
 dvla_token_loss_fwd_bwd = _proto("dvla_token_loss_fwd_bwd", [
     _vp, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64,
     _f64, _f64, _f64, _i32, _vp, _vp, _vp, _vp, _sz, _vp])

@@ -238,13 +238,13 @@ struct FusedSmem {
   double ws[kASlots][kFusedComputeWarps];
   float wm[kASlots][kFusedComputeWarps];
   float kval[kFusedStages];   // lse*log2e - log2|c|
-  float lseL[kFusedStages];   // lse*log2e
-  float cf[kFusedStages];     // coefficient (f32)
+  float tval[kFusedStages];   // target column c (1 - p_t) = -c expm1(lp_tok), f64 -> f32
   uint32_t mode[kFusedStages];  // 0 zero row, 1 finite c (bit 31: c > 0), 2 non-finite c
   int32_t tgt[kFusedStages];
   float xt[kASlots];       // gathered target logit of A slot
   int32_t tgta[kASlots];   // its token id (-1: out of range)
   double ring_lse[kRing];
+  double ring_lp[kRing];   // the row's lp_tok (target column of phase B)
   int32_t ring_tgt[kRing];
 };
 
@@ -548,6 +548,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
         st_relaxed_gpu_f64(p.lp_tok + r, lp);
         if (write_dl) {
           S.ring_lse[k % kRing] = lse;
+          S.ring_lp[k % kRing] = lp;
           S.ring_tgt[k % kRing] = tgt;
           mbar_arrive(&S.tdone[k % kRing]);
         } else {
@@ -603,7 +604,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
         if (lane == 0) { DBG_ADD(5); }
       }
       uint32_t mode = 0u;
-      float kval = 0.f, cf = 0.f;
+      float kval = 0.f, tval = 0.f;
       if (lane == 0) {
         ChunkTerms ct = chunk_terms(lp, static_cast<double>(pblp), padv, p.w, p.clip_eps,
                                     p.kl_coeff);
@@ -621,9 +622,9 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
           mode = 1u | ((cc > 0.0) ? 0x80000000u : 0u);
           kval = static_cast<float>(lse * 1.4426950408889634 - log2(fabs(cc)));
         }
-        cf = static_cast<float>(cc);
+        // 1 - p_t = -expm1(lp_tok) in f64: no cancellation when p_t -> 1
+        tval = static_cast<float>(-cc * expm1(S.ring_lp[k % kRing]));
       }
-      const float lseL = static_cast<float>(S.ring_lse[k % kRing] * 1.4426950408889634);
       const int32_t tgt = S.ring_tgt[k % kRing];
 #pragma unroll
       for (int pc = 0; pc < P; ++pc) {
@@ -637,8 +638,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
         if (lane == 0) {
           S.mode[sb] = mode;
           S.kval[sb] = kval;
-          S.cf[sb] = cf;
-          S.lseL[sb] = lseL;
+          S.tval[sb] = tval;
           S.tgt[sb] = tgt;
           mbar_arrive(&S.cfullB[sb]);
         }
@@ -750,15 +750,12 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
       const uint32_t z = (mode == 0u) ? 0u : FE::kNaN;
       for (int i = tid; i < nvec; i += kFusedComputeThreads) v[i] = make_uint4(z, z, z, z);
     } else {
-      // target column: c * (1 - p_t), patched by the thread that owns it
+      // target column: c * (1 - p_t) (prep warp, f64), patched by the
+      // thread that owns it
       const int li = S.tgt[sb] - elem0;
       const bool here = li >= 0 && li < nvec * E;
       const bool owner = here && tid == ((li / E) % kFusedComputeThreads);
-      float val = 0.f;
-      if (owner) {
-        const float pt = ex2f(fmaf(FE::get(v, li), kLog2e, -S.lseL[sb]));
-        val = S.cf[sb] * (1.0f - pt);
-      }
+      const float val = S.tval[sb];
       // -c * p_v = -sign(c) * 2^(x*log2e - (lse*log2e - log2|c|))
       const float K = S.kval[sb];
       const uint64_t nK2 = f2pack(-K, -K);
@@ -917,9 +914,11 @@ __global__ void __launch_bounds__(kRowThreads) tok_bwd_kernel(TokParams p, int v
   constexpr int E = Elem<T>::kVec;
   const float cf = static_cast<float>(c);
   const float lseL = static_cast<float>(lse * 1.4426950408889634);
+  // target column c (1 - p_t) = -c expm1(lp_tok) in f64 (no cancellation)
+  const float tv = static_cast<float>(-c * expm1(p.lp_tok[r]));
   auto val = [&](float x, int64_t col) {
     const float pv = ex2f(fmaf(x, kLog2e, -lseL));
-    return (col == tgt) ? cf * (1.0f - pv) : -cf * pv;
+    return (col == tgt) ? tv : -cf * pv;
   };
   if (vec_ok) {
     const uint4* v = reinterpret_cast<const uint4*>(row);
@@ -1153,6 +1152,19 @@ extern "C" size_t dvla_token_loss_workspace_bytes(int64_t n_groups, int64_t G, i
                                                   int64_t T) {
   if (n_groups < 0 || G < 0 || C < 0 || T < 0) return 0;
   return carve(nullptr, n_groups, G, C, T).bytes;
+}
+
+extern "C" int dvla_token_loss_workspace_layout(int64_t n_groups, int64_t G, int64_t C,
+                                                int64_t T, size_t* offsets) {
+  if (n_groups < 0 || G < 0 || C < 0 || T < 0 || !offsets)
+    return fail(DVLA_ERR_USAGE, "bad workspace layout query");
+  const TokWorkspace w = carve(nullptr, n_groups, G, C, T);
+  const auto off = [](const void* q) { return reinterpret_cast<size_t>(q); };
+  offsets[0] = off(w.adv);
+  offsets[1] = off(w.lp_tok);
+  offsets[2] = off(w.lse);
+  offsets[3] = off(w.coeff);
+  return DVLA_OK;
 }
 
 extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int32_t* tokens,

@@ -274,6 +274,15 @@ class TokenLoss:
         self.workspace = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=self.device)
         self.lp_chunk = torch.empty(n_groups * G * C, dtype=torch.float64, device=self.device)
         self.stats_dev = torch.zeros(_lib.ST_LEN, dtype=torch.float64, device=self.device)
+        offs = (_lib.C.c_size_t * 4)()
+        _lib.check(_lib.dvla_token_loss_workspace_layout(n_groups, G, C, T, offs),
+                   "dvla_token_loss_workspace_layout")
+        ws64 = self.workspace.view(torch.float64)
+        n_traj, nq = n_groups * G, n_groups * G * C
+        # views of what the last launch left in the workspace (parity checks)
+        self.adv = ws64[offs[0] // 8: offs[0] // 8 + n_traj]
+        self.lp_tok = ws64[offs[1] // 8: offs[1] // 8 + self.rows]
+        self.coeff = ws64[offs[3] // 8: offs[3] // 8 + nq]
         self.set_groups(np.arange(n_groups, dtype=np.int64))
 
     def set_groups(self, group_ids):
@@ -369,6 +378,8 @@ def grpo_token_grad(logits, tokens, behavior_log_prob, rewards, group_ids, cfg: 
               dlogits.reshape(-1, V) if write_dlogits else None)
     st = tl.stats(rewards)
     st["lp_chunk"] = tl.lp_chunk.view(n_groups, G, C)
+    st["coeff"] = tl.coeff.view(n_groups, G, C)
+    st["lp_tok"] = tl.lp_tok.view(n_groups, G, C, T)
     return st["loss"], (dlogits if write_dlogits else None), st
 
 

@@ -185,3 +185,42 @@ def test_oracle_alloc_trace_edge_cases():
     assert fin == (256, 256, 1)
     ok, off, fin = alloc_trace(100, [], [], [], [])
     assert len(ok) == 0 and fin == (100, 100, 1)
+
+
+def test_dlogits_criterion_sees_off_target_errors():
+    """The row-wise criterion (oracle/check.py) must reject a systematic
+    10 % error on every off-target softmax entry at V = 32,064 -- the error a
+    max-scaled tolerance cannot see -- and accept the exact gradient."""
+    from oracle.check import dlogits_errors, dlogits_rows
+    rng = np.random.default_rng(0)
+    V = 32064
+    x = rng.normal(0, 2, (4, V))
+    tok = rng.integers(0, V, 4)
+    lse = np.log(np.exp(x).sum(axis=1))
+    want = dlogits_rows(x, tok, lse, np.array([1e-3, -2e-3, 0.0, 5e-4]))
+    assert dlogits_errors(want, want) == (0.0, 0.0, 0)
+    bad = want.copy()
+    off = np.ones_like(bad, dtype=bool)
+    off[np.arange(4), tok] = False
+    bad[off] *= 1.1
+    row_l2, elem, nz = dlogits_errors(bad, want)
+    assert nz == 0 and elem > 0.05
+    # max-scaled check would pass this
+    assert np.all(np.abs(bad - want) <= 1e-2 * (np.abs(want) + np.abs(want).max()))
+    # a nonzero value in a zero-coefficient row is counted
+    bad2 = want.copy()
+    bad2[2, 0] = 1e-30
+    assert dlogits_errors(bad2, want)[2] == 1
+
+
+def test_coefficient_condition_widens_only_cancelling_rows():
+    from oracle.check import coeff_term_scale, row_condition
+    lp = np.full((1, 2, 1), -10.0)
+    blp = np.array([[[-10.0], [-10.0]]], np.float32)
+    rw = np.array([[0.0, 1.0]], np.float32)
+    s = coeff_term_scale(lp, blp, rw, kl_coeff=0.0)
+    # w = 1/2; A = -+1/(0.5 + 1e-8); rho = 1
+    np.testing.assert_allclose(s.ravel(), 0.5 * 0.5 / (0.5 + 1e-8))
+    coeff = np.array([s.ravel()[0], 1e-6 * s.ravel()[1]])
+    rc = row_condition(coeff, s, 3)
+    assert rc.shape == (6,) and np.all(rc[:3] == 1.0) and np.allclose(rc[3:], 1e6)
