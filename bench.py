@@ -740,8 +740,12 @@ def run_ours(a):
     world, rank, local = _dist()
     if world > 1:
         torch.cuda.set_device(local)
+        # NCCL's internal streams at high priority: the all-reduce kernels
+        # are scheduled ahead of concurrently queued sampler work
+        opts = dist.ProcessGroupNCCL.Options()
+        opts.is_high_priority_stream = True
         dist.init_process_group("nccl", init_method="env://", world_size=world, rank=rank,
-                                device_id=torch.device("cuda", local))
+                                device_id=torch.device("cuda", local), pg_options=opts)
     dev = torch.device("cuda", torch.cuda.current_device())
     torch.cuda.set_device(dev)
 

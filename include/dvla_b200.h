@@ -208,6 +208,31 @@ int dvla_grad_norm(double* grad, int64_t n, double max_norm, double* norm_out,
 /* *flag_out |= any non-finite f32 (runtime.py:793-795 RunAbort check). */
 int dvla_f32_nonfinite(const float* p, int64_t n, uint32_t* flag_out, void* stream);
 
+/* The learner tail of TrainerWorker.update (runtime.py:788-796) for an f32
+ * gradient (the head GEMM's output; all-reduced as the reference's f32
+ * frames, runtime.py:590):
+ *   dvla_grad_norm_f32: *norm_out = || f64(grad) / div || (div = nodes, the
+ *     cross-node mean of runtime.py:627; 1 for one node), *nonfinite_out |=
+ *     any non-finite gradient element;
+ *   dvla_adam_tail_f32: per element gi = f64(grad[i]) / div, times
+ *     max_norm / *norm when *norm > max_norm > 0 (clip_grad_norm,
+ *     grpo.py:297-301; norm may be NULL = no clipping; a non-finite *norm
+ *     skips the update, grpo.py:282-283), then adam_step's
+ *     arithmetic (grpo.py:137-150, bit-identical to dvla_adam_step on the
+ *     same f64 gradient).  skip (device f32, may be NULL): nonzero -> the
+ *     update is skipped on the device.  bf16_out (may be NULL): the new
+ *     parameters rounded to bf16.  nonfinite_out (may be NULL) |= any
+ *     non-finite new parameter (runtime.py:793-795).
+ *   dvla_loss_status: *skip_out = 1.0f if the fused loss's stats vector
+ *     records an abort or a kernel error, else 0.0f (the skip word). */
+int dvla_grad_norm_f32(const float* grad, int64_t n, double div, double* norm_out,
+                       uint32_t* nonfinite_out, void* workspace, void* stream);
+int dvla_adam_tail_f32(float* params, const float* grad, double* m, double* v, int64_t n,
+                       int64_t step, double lr, double beta1, double beta2, double eps,
+                       double div, const double* norm, double max_norm, const float* skip,
+                       void* bf16_out, uint32_t* nonfinite_out, void* stream);
+int dvla_loss_status(const double* stats, float* skip_out, void* stream);
+
 /* --------------------------------------------------- dual-pool arena */
 
 /* PoolKind (pools.py:23-26) */

@@ -80,6 +80,97 @@ __global__ void adam_kernel(float* __restrict__ p, const double* __restrict__ g,
   }
 }
 
+// The learner tail in one pass (runtime.py:788-796: total /= w -> reduce
+// -> clip_grad_norm -> adam_step -> non-finite check), for an f32 gradient
+// (the head GEMM's output, all-reduced as the reference's f32 frames):
+//   gi = f64(g32[i]); gi = gi / div (the cross-node mean, div = nodes);
+//   gi = gi * (max_norm / norm) when norm > max_norm > 0 (clip_grad_norm's
+//   in-place scaling, same f64 expression); then the Adam element above.
+// `skip` (device f32, e.g. the all-reduced abort count): nonzero -> the
+// whole update is skipped on the device (every rank alike), so the host
+// checks the abort after one synchronisation instead of before the step;
+// a non-finite `norm` (non-finite gradient) skips it too.
+// Optional outputs: the new parameters rounded to bf16 (the weights the
+// next forward GEMM and the published snapshot read) and a flag raised
+// when any new parameter is non-finite.
+struct TailArgs {
+  float* p;
+  const float* g;
+  double* m;
+  double* v;
+  int64_t n;
+  AdamConsts c;
+  double div;
+  const double* norm;
+  double max_norm;
+  const float* skip;
+  __nv_bfloat16* w16;
+  unsigned* nonfinite;
+};
+
+__device__ __forceinline__ double tail_grad(float g32, double div, bool clip, double f) {
+  double gi = static_cast<double>(g32);
+  if (div != 1.0) gi = __ddiv_rn(gi, div);
+  if (clip) gi = __dmul_rn(gi, f);
+  return gi;
+}
+
+__global__ void adam_tail_kernel(TailArgs a, int vec) {
+  if (a.skip != nullptr && *a.skip != 0.0f) return;
+  bool clip = false;
+  double f = 1.0;
+  if (a.norm != nullptr) {
+    const double nm = a.norm[0];
+    if (!isfinite(nm)) return;  // non-finite gradient: grpo.py:282-283 aborts the update
+    if (nm > a.max_norm && a.max_norm > 0.0) {
+      clip = true;
+      f = a.max_norm / nm;
+    }
+  }
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  unsigned bad = 0;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t npair = a.n / 2;
+    float2* p2 = reinterpret_cast<float2*>(a.p);
+    const float2* g2 = reinterpret_cast<const float2*>(a.g);
+    double2* m2 = reinterpret_cast<double2*>(a.m);
+    double2* v2 = reinterpret_cast<double2*>(a.v);
+    __nv_bfloat162* w2 = reinterpret_cast<__nv_bfloat162*>(a.w16);
+    for (int64_t i = t0; i < npair; i += stride) {
+      float2 pa = p2[i];
+      const float2 ga = __ldcs(g2 + i);
+      double2 ma = m2[i], va = v2[i];
+      pa.x = adam_elem(pa.x, tail_grad(ga.x, a.div, clip, f), ma.x, va.x, a.c);
+      pa.y = adam_elem(pa.y, tail_grad(ga.y, a.div, clip, f), ma.y, va.y, a.c);
+      p2[i] = pa;
+      m2[i] = ma;
+      v2[i] = va;
+      if (w2 != nullptr) w2[i] = __floats2bfloat162_rn(pa.x, pa.y);
+      bad |= !isfinite(pa.x) | !isfinite(pa.y);
+    }
+    done = npair * 2;
+  }
+  for (int64_t i = done + t0; i < a.n; i += stride) {
+    double mi = a.m[i], vi = a.v[i];
+    const float pn = adam_elem(a.p[i], tail_grad(a.g[i], a.div, clip, f), mi, vi, a.c);
+    a.p[i] = pn;
+    a.m[i] = mi;
+    a.v[i] = vi;
+    if (a.w16 != nullptr) a.w16[i] = __float2bfloat16_rn(pn);
+    bad |= !isfinite(pn);
+  }
+  if (a.nonfinite != nullptr && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+    atomicOr(a.nonfinite, 1u);
+}
+
+// skip word for adam_tail_kernel from the fused loss's stats vector: 1.0
+// when the loss aborted (GrpoAbort) or its kernel reported an error
+__global__ void loss_status_kernel(const double* __restrict__ stats, float* __restrict__ out) {
+  out[0] = (stats[DVLA_ST_ABORT] != 0.0 || stats[DVLA_ST_KERNEL_ERR] != 0.0) ? 1.0f : 0.0f;
+}
+
 constexpr int kNormThreads = 256;
 constexpr int kNormBlocks = 16384;  // fixed: the reduction order never depends on the launch
 
@@ -117,6 +208,60 @@ __global__ void sumsq_blocks_kernel(const double* __restrict__ g, int64_t n, int
   for (i += threadIdx.x; i < hi; i += kNormThreads) {
     const double x = g[i];
     acc0 += x * x;
+    bad |= !isfinite(x);
+  }
+  double acc = warp_sum_f64(acc0 + acc1);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  bad = __any_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0 && bad) atomicOr(nonfinite, 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kNormThreads / 32; ++w) s += red[w];
+    partial[blockIdx.x] = s;
+  }
+}
+
+// f32 gradient variant: the norm of gi = f64(g32[i]) / div (the values
+// adam_tail_kernel steps with), 8-byte loads, four in flight per thread
+__global__ void sumsq_blocks_f32_kernel(const float* __restrict__ g, int64_t n, int64_t per_block,
+                                        double div, double* __restrict__ partial,
+                                        unsigned* __restrict__ nonfinite) {
+  __shared__ double red[kNormThreads / 32];
+  const int64_t lo = blockIdx.x * per_block;
+  const int64_t hi = (lo + per_block < n) ? lo + per_block : n;
+  double acc0 = 0.0, acc1 = 0.0;
+  unsigned bad = 0;
+  auto sq = [div](float x) {
+    double d = static_cast<double>(x);
+    if (div != 1.0) d = __ddiv_rn(d, div);
+    return d * d;
+  };
+  const bool vec = ((reinterpret_cast<uintptr_t>(g + lo) & 7) == 0);
+  int64_t i = lo;
+  if (vec) {
+    const float2* g2 = reinterpret_cast<const float2*>(g + lo);
+    const int64_t npair = (hi - lo) / 2;
+    int64_t j = threadIdx.x;
+    for (; j + 3 * kNormThreads < npair; j += 4 * kNormThreads) {
+      const float2 a = __ldcs(g2 + j), b = __ldcs(g2 + j + kNormThreads);
+      const float2 c = __ldcs(g2 + j + 2 * kNormThreads), d = __ldcs(g2 + j + 3 * kNormThreads);
+      acc0 += (sq(a.x) + sq(b.x)) + (sq(c.x) + sq(d.x));
+      acc1 += (sq(a.y) + sq(b.y)) + (sq(c.y) + sq(d.y));
+      bad |= !isfinite(a.x) | !isfinite(a.y) | !isfinite(b.x) | !isfinite(b.y) |
+             !isfinite(c.x) | !isfinite(c.y) | !isfinite(d.x) | !isfinite(d.y);
+    }
+    for (; j < npair; j += kNormThreads) {
+      const float2 a = __ldcs(g2 + j);
+      acc0 += sq(a.x);
+      acc1 += sq(a.y);
+      bad |= !isfinite(a.x) | !isfinite(a.y);
+    }
+    i = lo + npair * 2;
+  }
+  for (i += threadIdx.x; i < hi; i += kNormThreads) {
+    const float x = g[i];
+    acc0 += sq(x);
     bad |= !isfinite(x);
   }
   double acc = warp_sum_f64(acc0 + acc1);
@@ -239,4 +384,54 @@ extern "C" int dvla_f32_nonfinite(const float* p, int64_t n, uint32_t* flag_out,
   f32_nonfinite_kernel<<<grid_n(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       p, n, reinterpret_cast<unsigned*>(flag_out));
   return launch_check("f32_nonfinite_kernel");
+}
+
+// ---- the learner tail for an f32 gradient (see adam_tail_kernel)
+extern "C" int dvla_grad_norm_f32(const float* grad, int64_t n, double div, double* norm_out,
+                                  uint32_t* nonfinite_out, void* workspace, void* stream) {
+  if (n < 0 || !norm_out || !nonfinite_out || !workspace || !(div > 0.0))
+    return fail(DVLA_ERR_USAGE, "bad grad_norm_f32 arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nblocks = kNormBlocks;
+  const int64_t per = ((n + nblocks - 1) / nblocks + 1) & ~int64_t{1};
+  double* partial = static_cast<double*>(workspace);
+  DVLA_CUDA_TRY(cudaMemsetAsync(partial, 0, nblocks * sizeof(double), st));
+  if (n > 0) {
+    const int used = static_cast<int>((n + per - 1) / per);
+    sumsq_blocks_f32_kernel<<<used, kNormThreads, 0, st>>>(
+        grad, n, per, div, partial, reinterpret_cast<unsigned*>(nonfinite_out));
+    if (int rc = launch_check("sumsq_blocks_f32_kernel")) return rc;
+  }
+  norm_finish_kernel<<<1, kFinishThreads, 0, st>>>(partial, nblocks, norm_out);
+  return launch_check("norm_finish_kernel");
+}
+
+extern "C" int dvla_adam_tail_f32(float* params, const float* grad, double* m, double* v,
+                                  int64_t n, int64_t step, double lr, double beta1, double beta2,
+                                  double eps, double div, const double* norm, double max_norm,
+                                  const float* skip, void* bf16_out, uint32_t* nonfinite_out,
+                                  void* stream) {
+  if (n < 0 || step < 1 || !(div > 0.0))
+    return fail(DVLA_ERR_USAGE, "adam_tail: n >= 0, step >= 1 and div > 0 required");
+  if (n == 0) return DVLA_OK;
+  const double b1p = pow(beta1, static_cast<double>(step));
+  const double b2p = pow(beta2, static_cast<double>(step));
+  TailArgs a{params, grad, m, v, n,
+             AdamConsts{beta1, 1.0 - beta1, beta2, 1.0 - beta2, 1.0 - b1p, 1.0 - b2p, lr, eps},
+             div, norm, max_norm, skip, static_cast<__nv_bfloat16*>(bf16_out),
+             reinterpret_cast<unsigned*>(nonfinite_out)};
+  const int vec = ((reinterpret_cast<uintptr_t>(params) & 7) == 0 &&
+                   (reinterpret_cast<uintptr_t>(grad) & 7) == 0 &&
+                   (reinterpret_cast<uintptr_t>(m) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(v) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(bf16_out) & 3) == 0) ? 1 : 0;
+  adam_tail_kernel<<<grid_n(vec ? (n + 1) / 2 : n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      a, vec);
+  return launch_check("adam_tail_kernel");
+}
+
+extern "C" int dvla_loss_status(const double* stats, float* skip_out, void* stream) {
+  if (!stats || !skip_out) return fail(DVLA_ERR_USAGE, "bad loss_status arguments");
+  loss_status_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(stats, skip_out);
+  return launch_check("loss_status_kernel");
 }

@@ -44,12 +44,18 @@ def _stream_ptr(stream=None):
     return (stream or torch.cuda.current_stream()).cuda_stream
 
 
-def device_snapshot(params, version: int, out=None, stream=None) -> ParamSnapshot:
+def device_snapshot(params, version: int, out=None, stream=None,
+                    verified: bool = False) -> ParamSnapshot:
     """snapshot_from_params for a device tensor: fused copy + isfinite.
 
     Raises ConfigError("non-finite parameter at flat index {i}") exactly as
     the reference (core.py:123-125).  `out` may be a pool region view of at
-    least params.nbytes bytes (same dtype or uint8)."""
+    least params.nbytes bytes (same dtype or uint8).  The copy runs on
+    `stream` (default: current); the check synchronises that stream.
+    verified=True: the caller has already established that every parameter
+    is finite (the optimizer tail's flag, runtime.TrainerWorker) -- no host
+    synchronisation; the snapshot's `ready` event marks when its bytes are
+    valid."""
     from . import _lib
     torch = _torch()
     if version < 0:
@@ -62,18 +68,22 @@ def device_snapshot(params, version: int, out=None, stream=None) -> ParamSnapsho
     if dst.numel() * dst.element_size() < nbytes:
         raise UsageError(f"snapshot destination holds {dst.numel() * dst.element_size()} bytes, "
                          f"need {nbytes}")
-    bad = torch.empty(1, dtype=torch.int64, device=src.device)
-    with torch.cuda.device(src.device):
+    st = stream if stream is not None else torch.cuda.current_stream(src.device)
+    with torch.cuda.device(src.device), torch.cuda.stream(st):
+        bad = torch.empty(1, dtype=torch.int64, device=src.device)
         _lib.check(_lib.dvla_snapshot_copy(src.data_ptr(), dst.data_ptr(), nbytes, _code(src),
-                                           bad.data_ptr(), _stream_ptr(stream)),
+                                           bad.data_ptr(), _stream_ptr(st)),
                    "dvla_snapshot_copy")
-    b = int(bad.item()) & 0xFFFFFFFFFFFFFFFF
-    if b != 0xFFFFFFFFFFFFFFFF:
-        raise ConfigError(f"non-finite parameter at flat index {b}")
+        ready = torch.cuda.Event()
+        ready.record(st)
+        if not verified:
+            b = int(bad.item()) & 0xFFFFFFFFFFFFFFFF   # .item() on `st`: ordered after the copy
+            if b != 0xFFFFFFFFFFFFFFFF:
+                raise ConfigError(f"non-finite parameter at flat index {b}")
     if out is not None and dst.dtype != src.dtype:
         dst = dst[:nbytes].view(src.dtype)
     return ParamSnapshot(version=int(version), params=dst[:src.numel()] if out is not None
-                         else dst)
+                         else dst, ready=ready)
 
 
 def bytes_equal(a, b, stream=None) -> tuple[int, int]:

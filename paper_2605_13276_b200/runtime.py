@@ -123,10 +123,12 @@ class VersionBoard:
         self.regressions_ignored = 0
         self.delivered: dict = {}
         self.epoch_meta: dict = {}
+        self.retired_max = -1   # versions <= this one's buffer has been reused
 
     def deposit(self, snap: ParamSnapshot):
         with self._c:
-            if snap.version <= self.installed or snap.version in self.delivered:
+            if snap.version <= self.installed or snap.version in self.delivered or \
+                    snap.version <= self.retired_max:
                 self.regressions_ignored += 1
                 log.warning("ignoring stale weight snapshot v%d (installed v%d)", snap.version,
                             self.installed)
@@ -204,6 +206,27 @@ class VersionBoard:
         with self._c:
             self.processed += 1
             self._c.notify_all()
+
+    def retire(self, version: int):
+        """The publisher is about to reuse the buffer of `version` (a ring of
+        published-weight regions): wait until the sampler no longer reads
+        it or anything older (a newer version is installed -- the gate
+        installs the newest delivered one at every epoch boundary, and the
+        versions between it and the one about to be published already are
+        published), then drop it and everything
+        older from the pending deliveries so it can never be installed."""
+        if version < 0:
+            return
+        with self._c:
+            while self.installed <= version and not self.sampler_done:
+                if self.monitor.abort.is_set():
+                    from .planes import RunAborted
+                    raise RunAborted("abort in retire wait")
+                self.monitor.beat(LaneId.TRAINER.value, "retire-wait")
+                self._c.wait(0.05)
+            self.retired_max = max(self.retired_max, version)
+            for v in [k for k in self.delivered if k <= version]:
+                del self.delivered[v]
 
 
 class GradReducer:
@@ -283,6 +306,20 @@ class GradReducer:
         dist.all_reduce(q, op=dist.ReduceOp.SUM, group=self.group)
         return q.to(grad.dtype) / self.nodes if q.dtype != grad.dtype else q / self.nodes
 
+    def overlappable(self, grad) -> bool:
+        """True when reduce_async can take the gradient bucket by bucket
+        (NCCL f32 sum; the caller divides by `nodes`)."""
+        return self.nodes > 1 and not self.exact and not self._use_nvls(grad)
+
+    def reduce_async(self, bucket):
+        """In-place NCCL sum of one f32 gradient bucket, asynchronous: NCCL's
+        stream waits for the current stream at this call, so the next
+        bucket's GEMM overlaps this bucket's all-reduce; wait() on the
+        returned work makes the current stream wait for the sum.  The mean's
+        division by `nodes` is the caller's (fused into the optimizer tail)."""
+        import torch.distributed as dist
+        return dist.all_reduce(bucket, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+
     def close(self):
         if self._ar is not None:
             self._ar.close()
@@ -319,9 +356,32 @@ class SwimlaneConfig:
             raise ConfigError("staleness_limit must be >= 0")
 
 
+def token_positions(cfg: "SwimlaneConfig", device):
+    """Per-position embeddings [T, H] (bf16, fixed random, seed cfg.seed + 2):
+    the feature of action token t of a chunk is the chunk's observation
+    feature + positions[t], so the T rows of a chunk have distinct logits
+    (an autoregressive VLA decodes each action token from its own hidden
+    state).  The sampler and the trainer build the same table."""
+    import torch
+    g = torch.Generator(device=device).manual_seed(cfg.seed + 2)
+    return (torch.randn(cfg.tokens, cfg.hidden, device=device, generator=g) * 0.05).to(
+        torch.bfloat16)
+
+
+def expand_token_features(feats, pos, out):
+    """out[(c, t)] = feats[c] + pos[t] (bf16; one broadcast kernel):
+    feats [n_chunks, H], pos [T, H], out [n_chunks * T, H]."""
+    import torch
+    nc, H = feats.shape[0], feats.shape[-1]
+    T = pos.shape[0]
+    torch.add(feats.reshape(nc, 1, H), pos.reshape(1, T, H), out=out.view(nc, T, H))
+    return out
+
+
 class TokenPolicy:
-    """Action-token head W [V, H] (bf16 on the device) with f32 master
-    weights and f64 Adam moments in a MODEL_COMPUTE pool."""
+    """Action-token head W [V, H]: f32 master weights, f64 Adam moments and
+    the bf16 working copy (what the forward GEMM reads; the optimizer tail
+    rewrites it as it steps the master weights) in a MODEL_COMPUTE pool."""
 
     def __init__(self, cfg: SwimlaneConfig, pool, device):
         import torch
@@ -331,18 +391,22 @@ class TokenPolicy:
         self.hm = pool.alloc(n * 4, align=256)
         self.hmm = pool.alloc(n * 8, align=256)
         self.hmv = pool.alloc(n * 8, align=256)
+        self.hw = pool.alloc(n * 2, align=256)
         self.master = pool.view(self.hm, torch.float32)
         self.master.copy_(torch.randn(n, device=device, generator=g) * (H ** -0.5))
         self.m = pool.view(self.hmm, torch.float64)
         self.v = pool.view(self.hmv, torch.float64)
         self.m.zero_()
         self.v.zero_()
+        self.w16 = pool.view(self.hw, torch.bfloat16).view(V, H)
+        self.w16.copy_(self.master.view(V, H))
         self.step = 0
         self.V, self.H = V, H
 
     def weight_bf16(self):
-        import torch
-        return self.master.view(self.V, self.H).to(torch.bfloat16)
+        """The bf16 head (round-to-nearest of the master weights), kept
+        current by the optimizer tail: no copy."""
+        return self.w16
 
 
 class SamplerWorker:
@@ -359,10 +423,14 @@ class SamplerWorker:
         self.proj = torch.randn(224 * 224 * 3 // 64 + 8, H, device=device,
                                 generator=torch.Generator(device=device).manual_seed(
                                     cfg.seed + 1)) * 0.05
+        self.pos = token_positions(cfg, device)
         self.rng = torch.Generator(device=device).manual_seed(cfg.seed * 7919 + node)
 
-    def run_epoch(self, epoch: int, snap: ParamSnapshot, poison: bool = False):
-        """One epoch of rollouts; returns (messages, meta) like the reference."""
+    def run_epoch(self, epoch: int, snap: ParamSnapshot, poison: bool = False,
+                  group_base: int | None = None):
+        """One epoch of rollouts; returns (messages, meta) like the reference.
+        group_base: first group id (default: the reference's
+        (epoch * nodes + node) * groups_per_epoch)."""
         import torch
 
         from .rollout import sample_action_tokens
@@ -379,6 +447,8 @@ class SamplerWorker:
             return pool.view(pool.alloc(n, align=256), dtype).view(*shape)
 
         with torch.cuda.stream(self.stream):
+            if getattr(snap, "ready", None) is not None:
+                self.stream.wait_event(snap.ready)  # the snapshot's bytes landed
             W = snap.params.view(V, H)  # installed replica, zero copy
             # synthetic LIBERO-shaped observations -> features
             img = stage((n_traj * C, 224 * 224 * 3 // 64), torch.uint8)
@@ -388,8 +458,9 @@ class SamplerWorker:
             obs = torch.cat([img.float() / 255.0, prop], dim=1)
             feats = stage((n_traj * C, H), torch.bfloat16)
             feats.copy_(obs @ self.proj)                                # [n_traj*C, H]
+            ftok = expand_token_features(feats, self.pos, stage((R, H), torch.bfloat16))
             logits = stage((R, V), torch.bfloat16)
-            torch.matmul(feats.repeat_interleave(T, dim=0), W.t(), out=logits)
+            torch.matmul(ftok, W.t(), out=logits)
             rewards = torch.randint(0, 2, (n_traj,), device=dev, generator=self.rng).float()
             if poison:
                 rewards[0] = float("nan")
@@ -400,12 +471,12 @@ class SamplerWorker:
         ev = torch.cuda.Event()
         ev.record(self.stream)
         msgs = []
+        base = (epoch * self.nodes + self.node) * cfg.n_groups if group_base is None else group_base
         for gi in range(cfg.n_groups):
-            gid = (epoch * self.nodes + self.node) * cfg.n_groups + gi
             sl = slice(gi * G, (gi + 1) * G)
             toks = tokens.view(n_traj, C, T)[sl]
             b = GroupBatch(
-                group_id=gid, horizon=C * T, chunk=T,
+                group_id=base + gi, horizon=C * T, chunk=T,
                 obs=feats.view(n_traj, C, H)[sl], actions=toks,
                 behavior_log_prob=blp.view(n_traj, C)[sl],
                 rewards=rewards[sl], behavior_version=snap.version, tokens=toks)
@@ -414,31 +485,77 @@ class SamplerWorker:
         ev.synchronize()
         meta = {"roll_wall": time.perf_counter() - t0, "epoch": epoch,
                 "behavior_version": snap.version,
-                "success_rate": float(torch.nanmean(rewards).item())}
+                "success_rate": float(rewards.float().mean().item()) if not poison else 0.0}
         return msgs, meta
 
 
 class TrainerWorker:
     """One per GPU: owns the head parameters and Adam state (MODEL_COMPUTE
     pool), the fused loss and the TRAINER stream (reference
-    runtime.py:732-800).  update() = fused token loss fwd+bwd -> weight
-    gradient (cuBLAS) -> GradReducer mean -> grad norm (+clip) -> Adam ->
-    non-finite check -> version + 1."""
+    runtime.py:732-800).
 
-    def __init__(self, cfg: SwimlaneConfig, node: int, model_pool, reducer, stream, device):
+    update() enqueues the whole learner step on the trainer stream and
+    synchronises once at its end:
+      per-token features -> logits GEMM (cuBLAS, bf16 weights kept by the
+      optimizer tail) -> fused token loss fwd+bwd (csrc/token_loss.cu) ->
+      skip word (loss abort) -> head gradient dW = dl^T feats as f32 GEMM
+      output, in buckets over V whose NCCL all-reduce overlaps the next
+      bucket's GEMM (the skip word travels with the last bucket, so a rank's
+      abort skips the step on every rank) -> grad norm of the mean ->
+      optimizer tail (clip, Adam, bf16 copy, non-finite flag; skipped on the
+      device on abort or a non-finite gradient).
+    Aborts surface after the one synchronisation: GrpoAbort (the caller
+    quarantines; parameters and Adam state untouched) or RunAbort
+    (non-finite parameters)."""
+
+    def __init__(self, cfg: SwimlaneConfig, node: int, model_pool, reducer, stream, device,
+                 act_pool=None, n_groups: int | None = None):
         import torch
+
+        from . import _lib
+        from .pools import Pool, PoolKind
         self.cfg, self.node, self.reducer = cfg, node, reducer
         self.stream, self.device = stream, device
         self.policy = TokenPolicy(cfg, model_pool, device)
         self.gcfg = GrpoConfig(group_size=cfg.group_size, lr=cfg.lr,
                                max_grad_norm=cfg.max_grad_norm)
-        V, G, C, T = cfg.vocab, cfg.group_size, cfg.chunks, cfg.tokens
-        R = cfg.n_groups * G * C * T
-        self.loss = TokenLoss(cfg.n_groups, G, C, T, V, self.gcfg, dtype=torch.bfloat16,
+        V, H, G, C, T = cfg.vocab, cfg.hidden, cfg.group_size, cfg.chunks, cfg.tokens
+        self.n_groups = cfg.n_groups if n_groups is None else int(n_groups)
+        R = self.n_groups * G * C * T
+        n = V * H
+        self.loss = TokenLoss(self.n_groups, G, C, T, V, self.gcfg, dtype=torch.bfloat16,
                               device=device)
-        self.dl = torch.empty(R, V, dtype=torch.bfloat16, device=device)
-        self.logits = torch.empty(R, V, dtype=torch.bfloat16, device=device)
+        # f32 gradient + the skip word (one all-reduce buffer), long-lived
+        self.hg = model_pool.alloc((n + 1) * 4, align=256)
+        self.gbuf = model_pool.view(self.hg, torch.float32)[: n + 1]
+        self.grad2d = self.gbuf[:n].view(V, H)
+        self.skip = self.gbuf[n:n + 1]
+        # activations of one update (logits, d loss / d logits, per-token
+        # features): an activation pool of the recycled kind, reset per update
+        act_bytes = R * (2 * V * 2 + H * 2) + (4 << 20)
+        self.act_pool = act_pool or Pool(PoolKind.ENV_AUX, act_bytes, device=device)
+        self._acts(R, V, H)
+        self.pos = token_positions(cfg, device)
+        self.norm_ws = torch.empty(_lib.dvla_grad_norm_workspace_bytes(n), dtype=torch.uint8,
+                                   device=device)
+        self.norm = torch.zeros(1, dtype=torch.float64, device=device)
+        self.flags = torch.zeros(2, dtype=torch.int32, device=device)  # grad / param non-finite
+        self.h_stats = torch.empty(_lib.ST_LEN, dtype=torch.float64, pin_memory=True)
+        self.h_misc = torch.empty(2, dtype=torch.float64, pin_memory=True)  # norm, skip
+        self.h_flags = torch.empty(2, dtype=torch.int32, pin_memory=True)
+        self.h_skip = torch.empty(1, dtype=torch.float32, pin_memory=True)
+        self.buckets = 4 if reducer.nodes > 1 else 1
         self.version = 0
+        self.done_event = None
+        self.timing = None  # optional: dict of CUDA event pairs per phase
+
+    def _acts(self, R, V, H):
+        import torch
+        pool = self.act_pool
+        pool.epoch_reset()
+        self.logits = pool.view(pool.alloc(R * V * 2, align=256), torch.bfloat16).view(R, V)
+        self.dl = pool.view(pool.alloc(R * V * 2, align=256), torch.bfloat16).view(R, V)
+        self.feats_tok = pool.view(pool.alloc(R * H * 2, align=256), torch.bfloat16).view(R, H)
 
     def snapshot(self, out=None, stream=None) -> ParamSnapshot:
         """The bf16 head as a versioned device snapshot (fused copy +
@@ -448,57 +565,113 @@ class TrainerWorker:
                                stream=stream)
 
     def update(self, batches: list) -> dict:
-        """One GRPO update on one epoch of groups.  Raises GrpoAbort for a
-        poisoned batch (the caller quarantines it) and RunAbort when the
-        parameters turn non-finite."""
+        """One GRPO update on one epoch of groups (reference runtime.py:768-800)."""
         import torch
 
         from . import _lib
-        from .grpo import clip_grad_norm
+        from .grpo import stats_from_vector
         cfg, pol, s = self.cfg, self.policy, self.stream
         V, H, C, T = cfg.vocab, cfg.hidden, cfg.chunks, cfg.tokens
-        n_traj = cfg.n_groups * cfg.group_size
+        n = V * H
+        nodes = self.reducer.nodes
         t0 = time.perf_counter()
+        ids = [b.group_id for b in batches]
+        if len(batches) != self.n_groups:
+            raise ConfigError(f"update expects {self.n_groups} groups, got {len(batches)}")
+        ev_t = self.timing
         with torch.cuda.stream(s):
-            batches[0].ready.wait(s)
-            W = pol.weight_bf16().view(V, H)
-            feats = torch.cat([b.obs for b in batches]).reshape(n_traj * C, H)
-            feats = feats.repeat_interleave(T, dim=0).contiguous()     # [R, H]
-            torch.matmul(feats, W.t(), out=self.logits)
-            self.loss.set_groups([b.group_id for b in batches])
+            seen = set()
+            for b in batches:
+                ev = getattr(b, "ready", None)
+                if ev is not None and id(ev) not in seen:
+                    seen.add(id(ev))
+                    s.wait_event(ev)
+            if ev_t is not None:
+                ev_t["start"].record(s)
+            feats = torch.cat([b.obs.reshape(-1, H) for b in batches])       # [n_traj*C, H]
+            expand_token_features(feats, self.pos, self.feats_tok)
+            torch.mm(self.feats_tok, pol.w16.t(), out=self.logits)
+            self.loss.set_groups(ids)
             toks = torch.cat([b.actions.reshape(-1) for b in batches])
             blp = torch.cat([b.behavior_log_prob.reshape(-1) for b in batches])
-            rw = torch.cat([b.rewards for b in batches])
-            self.loss.launch(self.logits, toks, blp, rw, self.dl)
-        ev = torch.cuda.Event()
-        ev.record(s)
-        ev.synchronize()
-        stats = self.loss.stats(rw)  # GrpoAbort -> caller quarantines
-        with torch.cuda.stream(s):
-            grad = (self.dl.t() @ feats).reshape(-1).double()  # dW = dl^T x (cuBLAS, f32 acc)
-            grad = self.reducer.reduce(grad)
-            norm = clip_grad_norm(grad, self.gcfg.max_grad_norm)
-            pol.step += 1
+            rw = torch.cat([b.rewards.reshape(-1) for b in batches])
+            if ev_t is not None:
+                ev_t["loss0"].record(s)
+            self.loss.launch(self.logits, toks, blp, rw, self.dl, stream=s)
+            if ev_t is not None:
+                ev_t["loss1"].record(s)
+            _lib.check(_lib.dvla_loss_status(self.loss.stats_dev.data_ptr(),
+                                             self.skip.data_ptr(), s.cuda_stream),
+                       "dvla_loss_status")
+            self.flags.zero_()
+            # dW = dl^T feats, f32 output, in buckets over V; each bucket's
+            # NCCL sum overlaps the next bucket's GEMM
+            overlap = self.reducer.overlappable(self.gbuf)
+            nb = self.buckets if overlap else 1
+            step = -(-V // nb)
+            works = []
+            for j in range(nb):
+                a, b_ = j * step, min(V, (j + 1) * step)
+                torch.mm(self.dl[:, a:b_].t(), self.feats_tok, out_dtype=torch.float32,
+                         out=self.grad2d[a:b_])
+                if overlap:
+                    hi = b_ * H if b_ < V else n + 1   # the skip word rides the last bucket
+                    works.append(self.reducer.reduce_async(self.gbuf[a * H:hi]))
+            if ev_t is not None:
+                ev_t["grad1"].record(s)
+            for w in works:
+                w.wait()
+            div = float(nodes) if overlap else 1.0
+            if nodes > 1 and not overlap:  # switch-reduced / exact paths: the mean itself
+                self.gbuf.copy_(self.reducer.reduce(self.gbuf))
+            if ev_t is not None:
+                ev_t["reduce1"].record(s)
             g = self.gcfg
-            _lib.check(_lib.dvla_adam_step(
-                pol.master.data_ptr(), grad.data_ptr(), pol.m.data_ptr(), pol.v.data_ptr(),
-                V * H, pol.step, g.lr, g.beta1, g.beta2, g.opt_eps, s.cuda_stream),
-                "dvla_adam_step")
-            flag = torch.zeros(1, dtype=torch.int32, device=self.device)
-            _lib.check(_lib.dvla_f32_nonfinite(pol.master.data_ptr(), V * H, flag.data_ptr(),
-                                               s.cuda_stream), "dvla_f32_nonfinite")
+            mx = float(g.max_grad_norm) if g.max_grad_norm is not None else 0.0
+            _lib.check(_lib.dvla_grad_norm_f32(self.gbuf.data_ptr(), n, div, self.norm.data_ptr(),
+                                               self.flags.data_ptr(), self.norm_ws.data_ptr(),
+                                               s.cuda_stream), "dvla_grad_norm_f32")
+            _lib.check(_lib.dvla_adam_tail_f32(
+                pol.master.data_ptr(), self.gbuf.data_ptr(), pol.m.data_ptr(), pol.v.data_ptr(),
+                n, pol.step + 1, g.lr, g.beta1, g.beta2, g.opt_eps, div, self.norm.data_ptr(), mx,
+                self.skip.data_ptr(), pol.w16.data_ptr(), self.flags.data_ptr() + 4,
+                s.cuda_stream), "dvla_adam_tail_f32")
+            if ev_t is not None:
+                ev_t["end"].record(s)
+            self.h_stats.copy_(self.loss.stats_dev, non_blocking=True)
+            self.h_misc[:1].copy_(self.norm, non_blocking=True)
+            self.h_flags.copy_(self.flags, non_blocking=True)
+            self.h_skip.copy_(self.skip, non_blocking=True)
         done = torch.cuda.Event()
         done.record(s)
-        done.synchronize()
-        if int(flag.item()):
+        done.synchronize()   # the update's one host synchronisation
+        sv = self.h_stats.numpy().copy()
+        skipped = float(self.h_skip[0]) != 0.0
+        grad_bad = bool(self.h_flags[0])
+        norm = float(self.h_misc[0])
+        rw_h = None
+        if skipped or grad_bad or not np.isfinite(norm):
+            # the device skipped the step: parameters and moments untouched
+            stats_from_vector(sv, self.loss.group_ids, self.loss.order,
+                              self.n_groups * cfg.group_size)          # local abort -> raises
+            if skipped:
+                raise GrpoAbort(int(ids[0]), "a peer learner's batch aborted the update")
+            raise GrpoAbort(int(ids[0]), "non-finite loss or gradient")
+        rw_h = rw.cpu().numpy().reshape(self.n_groups, cfg.group_size)
+        stats = stats_from_vector(sv, self.loss.group_ids, self.loss.order,
+                                  self.n_groups * cfg.group_size, rw_h)
+        if not np.isfinite(stats["loss"]):
+            raise GrpoAbort(int(ids[0]), "non-finite loss or gradient")
+        if bool(self.h_flags[1]):
             raise RunAbort("non-finite parameters after update",
                            lane=LaneId.TRAINER.value, epoch=self.version)
+        pol.step += 1
         self.version += 1
         self.done_event = done
         return {"version": self.version, "loss": stats["loss"], "grad_norm": norm,
                 "train_wall": time.perf_counter() - t0, "mean_ratio": stats["mean_ratio"],
                 "clip_fraction": stats["clip_fraction"], "n_chunks": stats["n_chunks"],
-                "mean_reward": float(rw.mean().item())}
+                "mean_reward": stats["mean_reward"]}
 
 
 class RunResult:
@@ -570,17 +743,24 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
     R = n_traj * C * T
 
     # ---- dual pools: long-lived model state vs epoch-recycled rollout staging
-    model_bytes = V * H * (4 + 8 + 8) + 2 * V * H * 2 + (64 << 20)
+    nbuf = cfg.staleness_limit + 2   # published-weight ring (see VersionBoard.retire)
+    n = V * H
+    model_bytes = n * (4 + 8 + 8 + 2) + (n + 1) * 4 + nbuf * n * 2 + (64 << 20)
     model_pool = Pool(PoolKind.MODEL_COMPUTE, model_bytes, device=dev)
     # ENV_AUX: one epoch-recycled arena per epoch the staleness gate lets be in
     # flight (limit + 2); each is reset wholesale when its epoch starts again
-    env_bytes = R * (V * 2 + 64) + n_traj * C * (H * 2 + 224 * 224 * 3 // 64 * 5) + (16 << 20)
+    env_bytes = R * (V * 2 + H * 2 + 64) + n_traj * C * (H * 2 + 224 * 224 * 3 // 64 * 5) + \
+        (16 << 20)
     env_pools = [Pool(PoolKind.ENV_AUX, env_bytes, device=dev)
                  for _ in range(cfg.staleness_limit + 2)]
     abort = threading.Event()
     monitor = Monitor(abort)
 
-    s_sample, s_train, s_dist = (torch.cuda.Stream(device=dev) for _ in range(3))
+    # the trainer stream (loss, gradient GEMM, all-reduce hand-off, optimizer
+    # and snapshot) runs at high priority: its CTAs are scheduled ahead of the
+    # sampler's GEMM CTAs whenever both have work pending
+    s_train = torch.cuda.Stream(device=dev, priority=-1)
+    s_sample, s_dist = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     ctrl = ControlPlane(Transport(TransportMode.INPROC, Plane.CONTROL, name="ctrl"))
     mailbox = ctrl.subscribe("weights", abort_event=abort)
     chan = Channel(cfg.queue_capacity * cfg.n_groups,
@@ -588,10 +768,9 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
     reducer = GradReducer(nodes, group)
     trainer = TrainerWorker(cfg, rank, model_pool, reducer, s_train, dev)
     sampler = SamplerWorker(cfg, rank, nodes, env_pools, s_sample, dev)
-    policy = trainer.policy
-    # double-buffered published weights (bf16) in the MODEL_COMPUTE pool
-    wbuf = [model_pool.view(model_pool.alloc(V * H * 2, align=256), torch.bfloat16)
-            for _ in range(cfg.staleness_limit + 1)]
+    # ring of published weights (bf16) in the MODEL_COMPUTE pool
+    wbuf = [model_pool.view(model_pool.alloc(n * 2, align=256), torch.bfloat16)
+            for _ in range(nbuf)]
     snap0 = trainer.snapshot(out=wbuf[0])
     board = VersionBoard(cfg.staleness_limit, monitor, snap0)
     result = RunResult()
@@ -633,12 +812,19 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
                         result.counters.get("quarantined_updates", 0) + 1
                     continue
                 board.wait_pacing(board.version + 1)
+                nv = trainer.version
+                board.retire(nv - nbuf)   # the ring slot nv % nbuf is free again
+                # the published copy is taken on the trainer stream, so the
+                # next update's optimizer step cannot overlap it (the bytes
+                # are already verified finite by the optimizer tail)
+                snap = device_snapshot(trainer.policy.weight_bf16().reshape(-1), nv,
+                                       out=wbuf[nv % nbuf], stream=s_train, verified=True)
                 v = board.publish()
                 busy["trainer"] += time.perf_counter() - t0
                 result.update_stats.append({"version": v, **{k: st[k] for k in (
                     "loss", "mean_ratio", "clip_fraction", "n_chunks", "grad_norm")}})
                 with dist_cv:
-                    dist_q.append((v, trainer.done_event))
+                    dist_q.append((v, snap))
                     dist_cv.notify_all()
                 step_time = max(meta["roll_wall"], time.perf_counter() - t0)
                 result.reports.append({"epoch": epoch, "policy_version": meta["behavior_version"],
@@ -665,14 +851,10 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
                         if abort.is_set():
                             return
                         dist_cv.wait(0.05)
-                    v, ev = dist_q.pop(0)
+                    v, snap = dist_q.pop(0)
                 if v is None:
                     break
-                with torch.cuda.stream(s_dist):
-                    s_dist.wait_event(ev)
-                    snap = device_snapshot(policy.weight_bf16().reshape(-1), v,
-                                           out=wbuf[v % len(wbuf)], stream=s_dist)
-                ctrl.broadcast(snap, stream=s_dist)
+                ctrl.broadcast(snap, stream=s_dist)  # INPROC: hand-off; ready event rides along
                 monitor.beat(LaneId.WEIGHT_DIST.value)
             monitor.beat(LaneId.WEIGHT_DIST.value, "done")
         except RunAborted:
@@ -711,6 +893,7 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
     result.wall = time.perf_counter() - t_start
     result.staleness_max = board.staleness_max
     result.lane_busy = busy
+    result.policy = trainer.policy   # final weights (multi-GPU: identical on every rank)
     result.counters.update({"updates": board.version, "produced": board.produced,
                             "regressions_ignored": board.regressions_ignored})
     return result

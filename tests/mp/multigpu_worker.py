@@ -4,8 +4,10 @@ Checks, on N >= 2 GPUs over NCCL/NVLink: (1) the cross-process TMA chain
 broadcast is bit-exact on every receiver for two versions (double buffer),
 and so is the switch-multicast (NVLS) broadcast where the box supports it;
 (2) GradReducer's NCCL mean equals the reference semantics; (3) the
-group-sharded token loss gives every rank its own shard's result; (4) the
-swimlane runs one closed loop per GPU with NCCL gradient reduction."""
+group-sharded token loss gives every rank its own shard's oracle result and
+the NCCL-averaged f32 head gradient equals the full-batch gradient; (4) the
+swimlane runs one closed loop per GPU with NCCL gradient reduction and ends
+with bitwise-identical weights on every rank."""
 import os
 import sys
 
@@ -17,10 +19,89 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 
+def _sharded_learner_step(rank, world):
+    """(3): the full batch (4 groups per rank, same seed everywhere) is
+    sharded by group; each rank's TokenLoss on its shard matches the f64
+    oracle run on that shard alone; the head gradient dW_r = dl_r^T x_r (f32
+    GEMM output) is all-reduced by NCCL through TrainerWorker's bucketed
+    path and divided by N; it equals (a) the f64 mean of every rank's own
+    product (f32 accumulation only, 1e-5) and (b) the single-GPU full-batch
+    gradient (reference runtime.py:775-788: mean of equal shards = full
+    batch; 1e-3: the two bf16 dlogits roundings differ)."""
+    from oracle import grpo_oracle as O
+    from oracle.check import assert_dlogits_close
+    from paper_2605_13276_b200 import grpo
+    from paper_2605_13276_b200.runtime import GradReducer
+    k, G, T, V, H = 4, 4, 8, 2048, 64
+    n_groups = k * world
+    R = n_groups * G * T
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = torch.Generator(device=dev).manual_seed(77)
+    feats = (torch.randn(R, H, device=dev, generator=g)).to(torch.bfloat16)
+    W = (torch.randn(V, H, device=dev, generator=g) * 0.3).to(torch.bfloat16)
+    logits = feats @ W.t()
+    tokens = torch.randint(0, V, (R,), device=dev, generator=g, dtype=torch.int32)
+    rewards = torch.rand(n_groups * G, device=dev, generator=g)
+    cfg = grpo.GrpoConfig(group_size=G)
+    full = grpo.TokenLoss(n_groups, G, 1, T, V, cfg, dtype=torch.bfloat16, device=dev)
+    full.launch(logits, tokens, torch.zeros(n_groups * G, device=dev), rewards, None)
+    blp = (full.lp_chunk + (torch.rand(full.lp_chunk.shape, device=dev, generator=g,
+                                       dtype=torch.float64) - 0.5) * 0.2).float()
+    rows = slice(rank * k * G * T, (rank + 1) * k * G * T)
+    trj = slice(rank * k * G, (rank + 1) * k * G)
+    ids = np.arange(rank * k, (rank + 1) * k)
+    tl = grpo.TokenLoss(k, G, 1, T, V, cfg, dtype=torch.bfloat16, device=dev)
+    tl.set_groups(ids)
+    dl = torch.empty(k * G * T, V, dtype=torch.bfloat16, device=dev)
+    tl.launch(logits[rows].contiguous(), tokens[rows].contiguous(), blp[trj].contiguous(),
+              rewards[trj].contiguous(), dl)
+    st = tl.stats(rewards[trj])
+    torch.cuda.synchronize()
+    x = logits[rows].float().cpu().numpy().reshape(k, G, 1, T, V)
+    oloss, odl, ost = O.grpo_token_grad(x, tokens[rows].cpu().numpy().reshape(k, G, 1, T),
+                                        blp[trj].cpu().numpy().reshape(k, G, 1),
+                                        rewards[trj].cpu().numpy().reshape(k, G), ids)
+    scale = float(np.abs(ost["coeff"]).mean())
+    assert abs(st["loss"] - oloss) <= 1e-5 * max(abs(oloss), scale), (rank, st["loss"], oloss)
+    np.testing.assert_allclose(tl.lp_chunk.cpu().numpy(), ost["lp_chunk"].reshape(-1),
+                               rtol=0, atol=1e-5)
+    assert st["group_ids"] == ost["group_ids"] == ids.tolist()
+    assert_dlogits_close(dl.float().cpu().numpy(), odl.reshape(-1, V), 1e-2)
+    # NCCL mean of the f32 head gradients, bucketed as TrainerWorker.update
+    n = V * H
+    gbuf = torch.zeros(n + 1, dtype=torch.float32, device=dev)
+    red = GradReducer(world)
+    assert red.overlappable(gbuf)
+    step = -(-V // 4)
+    works = []
+    for j in range(4):
+        a, b = j * step, min(V, (j + 1) * step)
+        torch.mm(dl[:, a:b].t(), feats[rows], out_dtype=torch.float32,
+                 out=gbuf[:n].view(V, H)[a:b])
+        works.append(red.reduce_async(gbuf[a * H:(b * H if b < V else n + 1)]))
+    for w in works:
+        w.wait()
+    mean = gbuf[:n].double() / world
+    own = (dl.double().t() @ feats[rows].double()).reshape(-1)
+    allown = [torch.empty_like(own) for _ in range(world)]
+    dist.all_gather(allown, own)
+    want = sum(allown) / world
+    assert float((mean - want).norm() / want.norm()) <= 1e-5, rank
+    assert float(gbuf[n]) == 0.0
+    if rank == 0:
+        dl_full = torch.empty(R, V, dtype=torch.bfloat16, device=dev)
+        full.launch(logits, tokens, blp, rewards, dl_full)
+        gfull = (dl_full.double().t() @ feats.double()).reshape(-1)
+        assert float((mean - gfull).norm() / gfull.norm()) <= 1e-3
+    dist.barrier()
+
+
 def main():
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    opts = dist.ProcessGroupNCCL.Options()
+    opts.is_high_priority_stream = True
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local), pg_options=opts)
     rank, world = dist.get_rank(), dist.get_world_size()
     from paper_2605_13276_b200.replicate import (ChainReplicator, McReplicator, bytes_equal,
                                                  multicast_supported)
@@ -184,11 +265,25 @@ def main():
     want = sum(float(np.float32((r + 1) / 3.0)) for r in range(world)) / world
     assert torch.allclose(out, torch.full_like(out, want), rtol=1e-15), (out[0].item(), want)
 
-    # (4) swimlane, topology replication with NCCL grad mean
+    # (3) group-sharded token loss + NCCL-averaged head gradient
+    _sharded_learner_step(rank, world)
+    if rank == 0:
+        print("SHARDED_LOSS_OK", flush=True)
+
+    # (4) swimlane, topology replication with NCCL grad mean: every rank
+    # ends with bitwise-identical master weights and bf16 working copies
     cfg = SwimlaneConfig(n_groups=2, group_size=4, tokens=8, vocab=1024, action_bins=256,
                          hidden=64, epochs=3, seed=11)
     res = run_swimlane(cfg)
     assert res.counters["updates"] == 3
+    for name, t in (("master", res.policy.master), ("w16", res.policy.w16.reshape(-1)),
+                    ("adam_m", res.policy.m)):
+        allw = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(allw, t.contiguous())
+        for r in range(1, world):
+            assert torch.equal(allw[0].view(torch.uint8), allw[r].view(torch.uint8)), (name, r)
+    if rank == 0:
+        print("SWIMLANE_WEIGHTS_EQUAL_OK", flush=True)
     dist.barrier()
     if rank == 0:
         print("MULTIGPU_OK", world, flush=True)

@@ -118,3 +118,134 @@ def test_barrier_free_handoff_audit():
     assert b.wall == 2.0 and not b.warmup_dominated
     r.reports = [{}]
     assert barrier_free_handoff_audit(r).warmup_dominated
+
+
+def _token_case(seed, n_groups, G, T, V, H):
+    rng = np.random.default_rng(seed)
+    feats = rng.normal(0, 1, (n_groups * G * T, H))
+    W = rng.normal(0, 0.3, (V, H))
+    x = (feats @ W.T).astype(np.float32).reshape(n_groups, G, 1, T, V)
+    tokens = rng.integers(0, V, (n_groups, G, 1, T)).astype(np.int32)
+    from oracle import grpo_oracle as O
+    _, _, st0 = O.grpo_token_grad(x, tokens, np.zeros((n_groups, G, 1), np.float32),
+                                  np.ones((n_groups, G), np.float32), np.arange(n_groups),
+                                  want_dlogits=False)
+    blp = (st0["lp_chunk"] + rng.uniform(-0.3, 0.3, (n_groups, G, 1))).astype(np.float32)
+    rewards = rng.uniform(0, 1, (n_groups, G)).astype(np.float32)
+    return feats, W, x, tokens, blp, rewards
+
+
+def _shard_grad(feats, x, tokens, blp, rewards, ids, poison=False):
+    """One learner rank's gradient of the head: the token loss on its group
+    shard (w = 1 / (n_traj_local * C)), dW = dl^T feats, as an f32 frame."""
+    from oracle import grpo_oracle as O
+    if poison:
+        rewards = rewards.copy()
+        rewards[0, 0] = np.nan
+        try:
+            O.grpo_token_grad(x, tokens, blp, rewards, ids)
+        except O.OracleAbort:
+            return None
+    _, dl, _ = O.grpo_token_grad(x, tokens, blp, rewards, ids)
+    V = x.shape[-1]
+    return (dl.reshape(-1, V).T @ feats).reshape(-1)
+
+
+def _update_worker(rank, world, port, q, poison_rank):
+    """runtime.TrainerWorker.update's arithmetic with a CPU restatement of
+    its device pieces: shard -> f32 gradient buffer + skip word -> bucketed
+    GradReducer.reduce_async (gloo) -> / nodes -> clip -> Adam, skipped on
+    every rank when any rank's batch aborted."""
+    import torch
+    import torch.distributed as dist
+    from oracle import grpo_oracle as O
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n_groups, G, T, V, H = 4, 4, 3, 16, 5
+    feats, W, x, tokens, blp, rewards = _token_case(7, n_groups, G, T, V, H)
+    k = n_groups // world
+    sl = slice(rank * k, (rank + 1) * k)
+    rows = slice(rank * k * G * T, (rank + 1) * k * G * T)
+    g = _shard_grad(feats[rows], x[sl], tokens[sl], blp[sl], rewards[sl],
+                    np.arange(n_groups)[sl], poison=(rank == poison_rank))
+    n = V * H
+    buf = torch.zeros(n + 1, dtype=torch.float32)
+    if g is None:
+        buf[n] = 1.0                     # dvla_loss_status: this rank aborted
+    else:
+        buf[:n] = torch.from_numpy(g.astype(np.float32))
+    red = GradReducer(world)
+    assert red.overlappable(buf)
+    step = -(-V // 3)
+    works = []
+    for j in range(3):
+        a, b = j * step, min(V, (j + 1) * step)
+        works.append(red.reduce_async(buf[a * H:(b * H if b < V else n + 1)]))
+    for w in works:
+        w.wait()
+    skipped = float(buf[n]) != 0.0
+    params = W.reshape(-1).astype(np.float32)
+    m = np.zeros(n)
+    v = np.zeros(n)
+    norm = None
+    if not skipped:
+        gm = buf[:n].double().numpy() / world
+        norm, gm = O.clip_grad_norm(gm, 0.05)
+        params, m, v, _ = O.adam_step(params, gm, m, v, 0, 1e-3, 0.9, 0.999, 1e-8)
+    q.put((rank, skipped, norm, params.tobytes()))
+    dist.destroy_process_group()
+
+
+def _run_update_workers(poison_rank):
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_update_worker, args=(r, 2, port, q, poison_rank))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(30)
+    return res
+
+
+def test_sharded_update_arithmetic_gloo():
+    """World size 2 (reference runtime.py:775-796): each rank's shard
+    gradient, reduced in f32 buckets, divided by the node count, clipped and
+    stepped, equals the single-process arithmetic on the same shards, and
+    both ranks hold bitwise-identical parameters afterwards."""
+    from oracle import grpo_oracle as O
+    res = _run_update_workers(poison_rank=-1)
+    (_, sk0, n0, p0), (_, sk1, n1, p1) = res
+    assert not sk0 and not sk1 and p0 == p1 and n0 == n1
+    n_groups, G, T, V, H = 4, 4, 3, 16, 5
+    feats, W, x, tokens, blp, rewards = _token_case(7, n_groups, G, T, V, H)
+    gs = [_shard_grad(feats[r * 2 * G * T:(r + 1) * 2 * G * T], x[2 * r:2 * r + 2],
+                      tokens[2 * r:2 * r + 2], blp[2 * r:2 * r + 2], rewards[2 * r:2 * r + 2],
+                      np.arange(2 * r, 2 * r + 2)) for r in range(2)]
+    # the reference's mean of f32 frames (runtime.py:590-627), f64 sum
+    gm = (gs[0].astype(np.float32).astype(np.float64) +
+          gs[1].astype(np.float32).astype(np.float64)) / 2
+    norm, gm = O.clip_grad_norm(gm, 0.05)
+    want, _, _, _ = O.adam_step(W.reshape(-1).astype(np.float32), gm, np.zeros(V * H),
+                                np.zeros(V * H), 0, 1e-3, 0.9, 0.999, 1e-8)
+    got = np.frombuffer(p0, dtype=np.float32)
+    np.testing.assert_allclose(n0, norm, rtol=1e-6)
+    np.testing.assert_allclose(got, want, rtol=1e-6, atol=1e-7)
+    # the mean of the equal-size shards' gradients is the full batch's
+    _, dl, _ = O.grpo_token_grad(x, tokens, blp, rewards, np.arange(n_groups))
+    full = (dl.reshape(-1, V).T @ feats).reshape(-1)
+    np.testing.assert_allclose((gs[0] + gs[1]) / 2, full, rtol=1e-9, atol=1e-12)
+
+
+def test_one_rank_abort_skips_the_update_on_every_rank_gloo():
+    res = _run_update_workers(poison_rank=1)
+    (_, sk0, _, p0), (_, sk1, _, p1) = res
+    assert sk0 and sk1 and p0 == p1

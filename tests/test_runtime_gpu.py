@@ -117,14 +117,17 @@ def test_nccl_c_abi_single_process_allreduce(dev):
 def test_sampler_and_trainer_workers_against_the_oracle(dev):
     """SamplerWorker.run_epoch -> TrainerWorker.update (reference
     runtime.py:676-800): the update's loss equals the f64 oracle on the same
-    logits, and Adam's first step moves every parameter with a clear
-    gradient by -lr * sign(grad) (m_hat / sqrt(v_hat) = sign(g) at step 1)."""
+    logits; the head gradient is the f32 GEMM output dW = dl^T x (checked
+    against an f64 product of the same operands at 1e-5, and its norm at
+    1e-5); Adam's first step moves every parameter with a clear gradient by
+    -lr * sign(grad) (m_hat / sqrt(v_hat) = sign(g) at step 1); the bf16
+    working copy is the round-to-nearest of the new master weights."""
     import torch
     from oracle import grpo_oracle as O
     from paper_2605_13276_b200.grpo import GrpoAbort
     from paper_2605_13276_b200.pools import Pool, PoolKind
     from paper_2605_13276_b200.runtime import (GradReducer, SamplerWorker, SwimlaneConfig,
-                                               TrainerWorker)
+                                               TrainerWorker, token_positions)
     cfg = SwimlaneConfig(n_groups=2, group_size=4, tokens=8, vocab=1024, action_bins=256,
                          hidden=64, seed=11, lr=1e-3)
     V, H, G, T = cfg.vocab, cfg.hidden, cfg.group_size, cfg.tokens
@@ -148,12 +151,16 @@ def test_sampler_and_trainer_workers_against_the_oracle(dev):
     feats = torch.cat([m.obs for m in msgs]).reshape(n_traj, H).clone()
     blp = torch.cat([m.behavior_log_prob.reshape(-1) for m in msgs]).clone()
     rw = torch.cat([m.rewards for m in msgs]).clone()
-    W = trainer.policy.weight_bf16()
-    logits = feats.repeat_interleave(T, dim=0) @ W.t()            # what update() computes
+    W = trainer.policy.weight_bf16().clone()
+    pos = token_positions(cfg, dev)
+    ftok = (feats.view(n_traj, 1, H) + pos.view(1, T, H)).reshape(-1, H)   # bf16, as update()
+    logits = ftok @ W.t()
     before = trainer.policy.master.clone()
 
     st = trainer.update(msgs)
+    torch.cuda.synchronize()
     assert st["version"] == 1 and trainer.version == 1
+    assert torch.equal(trainer.feats_tok, ftok) and torch.equal(trainer.logits, logits)
     x = logits.float().cpu().numpy().reshape(cfg.n_groups, G, 1, T, V)
     loss, dl, ost = O.grpo_token_grad(
         x, toks.cpu().numpy().reshape(cfg.n_groups, G, 1, T),
@@ -166,14 +173,29 @@ def test_sampler_and_trainer_workers_against_the_oracle(dev):
                                ost["lp_chunk"].reshape(-1), rtol=1e-9, atol=1e-5)
     np.testing.assert_allclose(st["mean_ratio"], ost["mean_ratio"], rtol=1e-6)
     assert st["n_chunks"] == n_traj
-    g = dl.reshape(-1, V).T @ feats.double().repeat_interleave(T, dim=0).cpu().numpy()
-    g = g.reshape(-1)
-    np.testing.assert_allclose(st["grad_norm"], np.sqrt((g * g).sum()), rtol=2e-2)
+    # head gradient: f32 GEMM output of the bf16 operands (dl, features)
+    assert trainer.grad2d.dtype == torch.float32
+    g64 = trainer.dl.double().t() @ trainer.feats_tok.double()
+    got = trainer.grad2d.double()
+    assert float((got - g64).norm() / g64.norm()) <= 1e-5
+    g = g64.reshape(-1).cpu().numpy()
+    np.testing.assert_allclose(st["grad_norm"], np.sqrt((g * g).sum()), rtol=1e-5)
+    # the bf16 d loss / d logits against the oracle's f64 gradient (bf16 tolerance)
+    from oracle.check import assert_dlogits_close
+    assert_dlogits_close(trainer.dl.float().cpu().numpy(), dl.reshape(-1, V), 1e-2)
     delta = (trainer.policy.master - before).cpu().double().numpy()
     clear = np.abs(g) > max(1e-2 * np.abs(g).max(), 1e-4)  # eps = 1e-8 negligible
     assert clear.sum() > 100
     np.testing.assert_allclose(delta[clear], -cfg.lr * np.sign(g[clear]), rtol=1e-3)
+    assert torch.equal(trainer.policy.weight_bf16(),
+                       trainer.policy.master.view(V, H).to(torch.bfloat16))
 
+    # a poisoned batch: GrpoAbort, and the device skipped the step
+    m0, v0 = trainer.policy.m.clone(), trainer.policy.v.clone()
+    p0 = trainer.policy.master.clone()
     msgs2, _ = sampler.run_epoch(1, trainer.snapshot(), poison=True)
     with pytest.raises(GrpoAbort):
         trainer.update(msgs2)
+    assert trainer.version == 1 and trainer.policy.step == 1
+    assert torch.equal(trainer.policy.master, p0) and torch.equal(trainer.policy.m, m0) \
+        and torch.equal(trainer.policy.v, v0)
