@@ -64,6 +64,19 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _nvlink_traffic():
+    """NVLink bytes the chain kernel puts on the wire per replicated byte
+    (ncu nvltx__bytes_data_user.sum of one 1 GiB hop, profiles/)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "nvlink_traffic.json")) as f:
+            t = json.load(f)["replicate_chain_kernel"]
+        return {"nvltx_user_bytes_per_byte": t["user_over_S"],
+                "nvltx_bytes_per_byte_incl_protocol": t["nvltx_bytes"] / t["S"],
+                "source": t["source"]}
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def _traffic():
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -198,7 +211,12 @@ def run_reference(a):
     return 0
 
 
-NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction
+NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction (fallback)
+_LIVE_NVL_PEAK = [None]   # this run's measured copy-engine peer copy (N >= 2)
+
+
+def _nvl_peak():
+    return _LIVE_NVL_PEAK[0] or NVLINK_PEER_GBS
 NVLINK_NOMINAL_GBS = 900.0
 REPL_BYTES = 6_600_000_000  # pi0-3B-shaped bf16 weights (BASELINE config 3)
 
@@ -274,6 +292,20 @@ def _bench_replication(world, rank, dev, barrier, max_over_ranks, iters=5):
         ok = ok and bytes_equal(expect, rep.replica(iters))[0] == 0
     ok_all = max_over_ranks(0.0 if ok else 1.0) == 0.0
     ms = sorted(times)[len(times) // 2]
+    # the NVLink peak of this box, measured live: copy-engine peer copy
+    # rank 0 -> rank 1, 1 GiB, best of 10 (SURVEY §8(d) replication roofline)
+    peak_ms = []
+    for it in range(10):
+        barrier()
+        if rank == 0:
+            e0.record(stream)
+            _lib.check(_lib.dvla_memcpy_async(rep.fan_bufs[0], src.data_ptr(), 1 << 30,
+                                              stream.cuda_stream), "dvla_memcpy_async")
+            e1.record(stream)
+        torch.cuda.synchronize()
+        peak_ms.append(max_over_ranks(e0.elapsed_time(e1) if rank == 0 else 0.0))
+    ce_peak = (1 << 30) / (min(peak_ms) / 1e3) / 1e9
+    _LIVE_NVL_PEAK[0] = ce_peak
     # copy-engine fan-out baseline (root pushes to every receiver)
     ce = []
     for it in range(3):
@@ -291,10 +323,12 @@ def _bench_replication(world, rank, dev, barrier, max_over_ranks, iters=5):
     out.update({"mode": f"{engine} 0->{'->'.join(str(r) for r in range(1, world))}",
                 "replica_regions": "receivers' MODEL_COMPUTE pools (dual-pool allocator)",
                 "gbs": gbs, "ms": ms, "bit_exact": ok_all,
-                "roofline": {"bound": "nvlink", "achieved": gbs, "peak": NVLINK_PEER_GBS,
-                             "unit": "GB/s", "frac": gbs / NVLINK_PEER_GBS,
+                "roofline": {"bound": "nvlink", "achieved": gbs, "peak": round(ce_peak, 1),
+                             "unit": "GB/s", "frac": gbs / ce_peak,
                              "frac_of_nominal_900": gbs / NVLINK_NOMINAL_GBS,
-                             "peak_source": "B200_PROFILING.md measured peer copy (770 GB/s/dir)"},
+                             "peak_source": "measured in this run: copy-engine peer copy "
+                                            "rank 0 -> 1, 1 GiB, best of 10",
+                             "traffic": _nvlink_traffic()},
                 "ce_fanout_gbs_per_receiver": S / (sorted(ce)[1] / 1e3) / 1e9})
     out["multicast"] = _bench_multicast(S, src, rank, world, barrier, max_over_ranks)
     if world >= 4:
@@ -333,7 +367,7 @@ def _bench_c3_split(S, src, rank, world, barrier, max_over_ranks, iters=4):
     ms = sorted(times)[len(times) // 2]
     return {"layout": f"learners 0,1 -> replicas {reps[0]}..{reps[-1]} (two half-region chains)",
             "gbs_per_replica": S / (ms / 1e3) / 1e9, "ms": ms, "bit_exact": ok_all,
-            "frac_of_peer_copy": S / (ms / 1e3) / 1e9 / NVLINK_PEER_GBS}
+            "frac_of_peer_copy": S / (ms / 1e3) / 1e9 / _nvl_peak()}
 
 
 def _bench_multicast(S, src, rank, world, barrier, max_over_ranks, iters=4):
@@ -370,7 +404,7 @@ def _bench_multicast(S, src, rank, world, barrier, max_over_ranks, iters=4):
     gbs = S / (ms / 1e3) / 1e9
     return {"mode": f"NVLS multicast 0->{{{','.join(str(r) for r in range(1, world))}}}",
             "gbs": gbs, "ms": ms, "bit_exact": ok_all,
-            "frac_of_peer_copy": gbs / NVLINK_PEER_GBS}
+            "frac_of_peer_copy": gbs / _nvl_peak()}
 
 
 def _bench_gauss_c3(dev, rank, steps=200, cpu=True):
@@ -637,6 +671,140 @@ def _bench_allreduce(world, dev, barrier, max_over_ranks, nbytes=1 << 30, iters=
     return out
 
 
+def _bench_c2_f32(dev, rank, world, barrier, max_over_ranks, steps=20):
+    """The C2 step with f32 logits (the north star's 1e-5 parity dtype):
+    the fused kernel streams each 128 KB row as two pieces.  Same timing
+    rules as the headline (CUDA events on the launching stream, the fused
+    kernel's own events in an interleaved profiled run, max over ranks)."""
+    import numpy as np
+    import torch
+
+    from paper_2605_13276_b200 import _lib, grpo
+    R = N_GROUPS * G * C * T
+    gen = torch.Generator(device=dev).manual_seed(99 + rank)
+    logits = torch.randn(R, V, device=dev, generator=gen) * 2.0
+    tokens = torch.randint(31744, 32000, (R,), device=dev, generator=gen, dtype=torch.int32)
+    rewards = torch.randint(0, 2, (N_GROUPS * G,), device=dev, generator=gen).float()
+    tl = grpo.TokenLoss(N_GROUPS, G, C, T, V, grpo.GrpoConfig(group_size=G),
+                        dtype=torch.float32, device=dev)
+    tl.set_groups(np.arange(N_GROUPS) + rank * N_GROUPS)
+    tl.launch(logits, tokens, torch.zeros(N_GROUPS * G * C, device=dev), rewards, None)
+    blp = (tl.lp_chunk + (torch.rand(tl.lp_chunk.shape, device=dev, generator=gen,
+                                     dtype=torch.float64) - 0.5) * 0.1).float()
+    dl = torch.empty_like(logits)
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        tl.launch(logits, tokens, blp, rewards, dl)
+    tl.stats(rewards)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        tl.launch(logits, tokens, blp, rewards, dl)
+    e1.record(stream)
+    _lib.dvla_profile_enable(1)
+    for _ in range(steps):
+        tl.launch(logits, tokens, blp, rewards, dl)
+    torch.cuda.synchronize()
+    km, kn = _lib.profile_collect()
+    _lib.dvla_profile_enable(0)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps)
+    kms = max_over_ranks(km / max(kn, 1))
+    st = tl.stats(rewards)
+    N = R * V
+    algo = 2 * N * 4 + R * 4 + N_GROUPS * G * C * (4 + 8) + N_GROUPS * G * 4
+    peak, kind = _peaks()
+    ach = algo / (kms / 1e3) / 1e9
+    del logits, dl
+    torch.cuda.empty_cache()
+    return {"value": world * N_GROUPS * G / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+            "dtype": "f32", "target_ms_70pct": 1.633,
+            "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(ach / peak, 4), "kernel": "tok_fused_kernel<f32, 2 pieces>",
+                         "kernel_ms": round(kms, 4), "algo_bytes": algo,
+                         "traffic": _traffic().get("tok_fused_kernel<f32,2>"),
+                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({kind})"},
+            "loss": st["loss"]}
+
+
+SWIM_H = 4096                        # OpenVLA-7B hidden size (the action head's K)
+
+
+def _bench_learner_step(world, rank, dev, barrier, max_over_ranks, steps=10, warmup=3):
+    """The learner step of BASELINE config 4 per GPU, timed as a unit with
+    its collective (reference TrainerWorker.update, runtime.py:768-800):
+    per-token features -> logits GEMM (V=32,064 x H=4,096 bf16 head) ->
+    fused token loss fwd+bwd -> f32 head-gradient GEMM in 4 buckets whose
+    NCCL all-reduce overlaps the next bucket -> grad norm -> optimizer tail
+    (clip + Adam + bf16 copy + non-finite flag), one host sync per step.
+    CUDA events on the trainer stream, max over ranks; the same 512
+    trajectories every step (inputs 1.84 GB of logits > L2)."""
+    import torch
+
+    from paper_2605_13276_b200.pools import Pool, PoolKind
+    from paper_2605_13276_b200.runtime import (GradReducer, SamplerWorker, SwimlaneConfig,
+                                               TrainerWorker)
+    cfg = SwimlaneConfig(n_groups=N_GROUPS, group_size=G, chunks=C, tokens=T, vocab=V,
+                         hidden=SWIM_H, seed=23)
+    n = V * SWIM_H
+    R = N_GROUPS * G * C * T
+    model_pool = Pool(PoolKind.MODEL_COMPUTE, n * 26 + (64 << 20), device=dev)
+    env_pool = Pool(PoolKind.ENV_AUX, R * (V * 2 + SWIM_H * 2 + 64) + (256 << 20), device=dev)
+    s_train = torch.cuda.Stream(device=dev, priority=-1)
+    s_sample = torch.cuda.Stream(device=dev)
+    import torch.distributed as dist
+    reducer = GradReducer(world, None)
+    trainer = TrainerWorker(cfg, rank, model_pool, reducer, s_train, dev)
+    sampler = SamplerWorker(cfg, rank, world, [env_pool], s_sample, dev)
+    msgs, _ = sampler.run_epoch(0, trainer.snapshot())
+    names = ("start", "loss0", "loss1", "grad1", "reduce1", "end")
+    phases = {k: 0.0 for k in ("feats_logits_gemm", "loss", "grad_gemm_and_reduce",
+                               "reduce_wait", "norm_adam_tail")}
+    for _ in range(warmup):
+        trainer.update(msgs)
+    barrier()
+    walls, devs = [], []
+    for _ in range(steps):
+        ev = {k: torch.cuda.Event(enable_timing=True) for k in names}
+        trainer.timing = ev
+        t0 = time.perf_counter()
+        trainer.update(msgs)       # ends with its one host sync
+        walls.append(time.perf_counter() - t0)
+        devs.append(ev["start"].elapsed_time(ev["end"]))
+        phases["feats_logits_gemm"] += ev["start"].elapsed_time(ev["loss0"])
+        phases["loss"] += ev["loss0"].elapsed_time(ev["loss1"])
+        phases["grad_gemm_and_reduce"] += ev["loss1"].elapsed_time(ev["grad1"])
+        phases["reduce_wait"] += ev["grad1"].elapsed_time(ev["reduce1"])
+        phases["norm_adam_tail"] += ev["reduce1"].elapsed_time(ev["end"])
+    trainer.timing = None
+    barrier()
+    dev_ms = max_over_ranks(sum(devs) / steps)
+    wall_ms = max_over_ranks(1e3 * sum(walls) / steps)
+    flops = 2 * 2 * R * SWIM_H * V            # logits GEMM + head-gradient GEMM
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            tf_peak = float(json.load(f)["bf16_tflops_sustained"])
+    except Exception:  # noqa: BLE001
+        tf_peak = 1394.0
+    out = {"metric": "learner step (RL samples/s through update(), incl. the all-reduce)",
+           "value": world * N_GROUPS * G / (wall_ms / 1e3), "unit": UNIT,
+           "ms_per_step_wall": wall_ms, "ms_per_step_device": dev_ms,
+           "phases_ms_rank0": {k: round(v / steps, 4) for k, v in phases.items()},
+           "gemm_tflop_per_step": flops / 1e12,
+           "gemm_roofline": {"bound": "tensor", "peak_tflops": tf_peak,
+                             "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
+                             "achieved_tflops_step": round(flops / (dev_ms / 1e3) / 1e12, 1),
+                             "frac_step": round(flops / (dev_ms / 1e3) / 1e12 / tf_peak, 4)},
+           "config": f"V={V} x H={SWIM_H} bf16 head, {N_GROUPS}x{G} traj x {T} tokens per GPU; "
+                     f"grad f32 {n * 4 / 1e9:.2f} GB all-reduced over {world} GPU(s)",
+           "steps": steps}
+    del trainer, sampler, model_pool, env_pool, msgs
+    torch.cuda.empty_cache()
+    _ = dist
+    return out
+
+
 def _bench_swimlane(world, rank, dev, max_over_ranks, epochs=8):
     """End-to-end RL samples/s of the four-lane swimlane (BASELINE config 4
     shape: OpenVLA-7B-sized action head V=32,064 x H=4,096, 64 groups x 8
@@ -647,7 +815,7 @@ def _bench_swimlane(world, rank, dev, max_over_ranks, epochs=8):
     out = {}
     for mode, limit in (("async", 1), ("sync", 0)):
         cfg = SwimlaneConfig(n_groups=N_GROUPS, group_size=G, chunks=C, tokens=T, vocab=V,
-                             hidden=4096, epochs=epochs, seed=17, staleness_limit=limit)
+                             hidden=SWIM_H, epochs=epochs, seed=17, staleness_limit=limit)
         s = run_swimlane(cfg, device=dev).summary()
         out[mode] = s
     traj = out["async"]["trajectories_per_s"]
@@ -888,8 +1056,11 @@ def run_ours(a):
         del h_logits, d_logits
 
     del dl
+    c2_f32 = _guarded(_bench_c2_f32, dev, rank, world, barrier, max_over_ranks)
     repl = None if a.no_repl else _bench_replication(world, rank, dev, barrier, max_over_ranks)
     allreduce = _bench_allreduce(world, dev, barrier, max_over_ranks)
+    learner = None if a.no_swimlane else _guarded(_bench_learner_step, world, rank, dev, barrier,
+                                                  max_over_ranks)
     # secondary per-GPU measurements: a failure is reported, never fatal to
     # the headline line
     gauss = None if a.no_gauss else _guarded(_bench_gauss_c3, dev, rank, cpu=not a.no_cpu)
@@ -901,6 +1072,13 @@ def run_ours(a):
         swim = _bench_swimlane(world, rank, dev, max_over_ranks)
         barrier()
         swim["model"] = _guarded(_swim_model, swim, world, roofline, sampler, optimizer)
+        # the GPU-work bound of one epoch on one GPU: the sampler's device
+        # work (the strict-alternation rollout lane) + the learner step
+        if isinstance(learner, dict) and "ms_per_step_device" in learner:
+            t_epoch = swim["lanes"]["sync"]["rollout_time"] + learner["ms_per_step_device"] / 1e3
+            bound = N_GROUPS * G / t_epoch
+            swim["gpu_work_bound_trajectories_per_s_rank0"] = bound
+            swim["async_frac_of_gpu_work_bound"] = swim["trajectories_per_s_rank0"] / bound
 
     if rank == 0 and world == 1 and not a.no_cpu and isinstance(repl, dict):
         repl["cpu_baseline"] = _guarded(_bench_weight_plane_cpu)
@@ -934,6 +1112,8 @@ def run_ours(a):
                        "parallelism": f"dp{world} (group-sharded learner)",
                        "l2": "inputs 1.84 GB/rank > 126 MB L2 (no flush needed)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "c2_f32": c2_f32, "learner_step": learner,
+            "rl_samples_per_s_end_to_end": (swim or {}).get("trajectories_per_s_total"),
             "replication": repl, "grad_allreduce": allreduce, "swimlane": swim,
             "gauss_c3": gauss, "sampler": sampler, "optimizer": optimizer,
             "allocator": allocator,

@@ -224,9 +224,14 @@ int dvla_f32_nonfinite(const float* p, int64_t n, uint32_t* flag_out, void* stre
  *     parameters rounded to bf16.  nonfinite_out (may be NULL) |= any
  *     non-finite new parameter (runtime.py:793-795).
  *   dvla_loss_status: *skip_out = 1.0f if the fused loss's stats vector
- *     records an abort or a kernel error, else 0.0f (the skip word). */
+ *     records an abort, a non-finite loss or a kernel error, else 0.0f (the
+ *     skip word). */
 int dvla_grad_norm_f32(const float* grad, int64_t n, double div, double* norm_out,
                        uint32_t* nonfinite_out, void* workspace, void* stream);
+/* The sum of squares instead of its root (a shard's share of the global
+ * norm: the shards' sums are all-reduced, then the root taken). */
+int dvla_grad_sumsq_f32(const float* grad, int64_t n, double div, double* sumsq_out,
+                        uint32_t* nonfinite_out, void* workspace, void* stream);
 int dvla_adam_tail_f32(float* params, const float* grad, double* m, double* v, int64_t n,
                        int64_t step, double lr, double beta1, double beta2, double eps,
                        double div, const double* norm, double max_norm, const float* skip,

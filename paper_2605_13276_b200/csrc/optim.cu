@@ -138,7 +138,29 @@ __global__ void adam_tail_kernel(TailArgs a, int vec) {
     double2* m2 = reinterpret_cast<double2*>(a.m);
     double2* v2 = reinterpret_cast<double2*>(a.v);
     __nv_bfloat162* w2 = reinterpret_cast<__nv_bfloat162*>(a.w16);
-    for (int64_t i = t0; i < npair; i += stride) {
+    // two pairs in flight per thread (the loads of both before any math)
+    int64_t i = t0;
+    for (; i + stride < npair; i += 2 * stride) {
+      float2 pa = p2[i], pb = p2[i + stride];
+      const float2 ga = __ldcs(g2 + i), gb = __ldcs(g2 + i + stride);
+      double2 ma = m2[i], mb = m2[i + stride], va = v2[i], vb = v2[i + stride];
+      pa.x = adam_elem(pa.x, tail_grad(ga.x, a.div, clip, f), ma.x, va.x, a.c);
+      pa.y = adam_elem(pa.y, tail_grad(ga.y, a.div, clip, f), ma.y, va.y, a.c);
+      pb.x = adam_elem(pb.x, tail_grad(gb.x, a.div, clip, f), mb.x, vb.x, a.c);
+      pb.y = adam_elem(pb.y, tail_grad(gb.y, a.div, clip, f), mb.y, vb.y, a.c);
+      p2[i] = pa;
+      p2[i + stride] = pb;
+      m2[i] = ma;
+      m2[i + stride] = mb;
+      v2[i] = va;
+      v2[i + stride] = vb;
+      if (w2 != nullptr) {
+        w2[i] = __floats2bfloat162_rn(pa.x, pa.y);
+        w2[i + stride] = __floats2bfloat162_rn(pb.x, pb.y);
+      }
+      bad |= !isfinite(pa.x) | !isfinite(pa.y) | !isfinite(pb.x) | !isfinite(pb.y);
+    }
+    for (; i < npair; i += stride) {
       float2 pa = p2[i];
       const float2 ga = __ldcs(g2 + i);
       double2 ma = m2[i], va = v2[i];
@@ -166,9 +188,11 @@ __global__ void adam_tail_kernel(TailArgs a, int vec) {
 }
 
 // skip word for adam_tail_kernel from the fused loss's stats vector: 1.0
-// when the loss aborted (GrpoAbort) or its kernel reported an error
+// when the loss aborted (GrpoAbort), is non-finite (grpo.py:282-283) or its
+// kernel reported an error
 __global__ void loss_status_kernel(const double* __restrict__ stats, float* __restrict__ out) {
-  out[0] = (stats[DVLA_ST_ABORT] != 0.0 || stats[DVLA_ST_KERNEL_ERR] != 0.0) ? 1.0f : 0.0f;
+  out[0] = (stats[DVLA_ST_ABORT] != 0.0 || stats[DVLA_ST_KERNEL_ERR] != 0.0 ||
+            !isfinite(stats[DVLA_ST_LOSS])) ? 1.0f : 0.0f;
 }
 
 constexpr int kNormThreads = 256;
@@ -280,7 +304,7 @@ __global__ void sumsq_blocks_f32_kernel(const float* __restrict__ g, int64_t n, 
 // then a warp-shuffle and a 32-entry tree (deterministic, one block)
 constexpr int kFinishThreads = 1024;
 __global__ void __launch_bounds__(kFinishThreads) norm_finish_kernel(
-    const double* __restrict__ partial, int nblocks, double* __restrict__ out) {
+    const double* __restrict__ partial, int nblocks, double* __restrict__ out, int want_sqrt = 1) {
   __shared__ double red[kFinishThreads / 32];
   double acc = 0.0;
   for (int b = threadIdx.x; b < nblocks; b += kFinishThreads) acc += partial[b];
@@ -290,7 +314,7 @@ __global__ void __launch_bounds__(kFinishThreads) norm_finish_kernel(
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int w = 0; w < kFinishThreads / 32; ++w) t += red[w];
-    out[0] = sqrt(t);
+    out[0] = want_sqrt ? sqrt(t) : t;
   }
 }
 
@@ -387,9 +411,9 @@ extern "C" int dvla_f32_nonfinite(const float* p, int64_t n, uint32_t* flag_out,
 }
 
 // ---- the learner tail for an f32 gradient (see adam_tail_kernel)
-extern "C" int dvla_grad_norm_f32(const float* grad, int64_t n, double div, double* norm_out,
-                                  uint32_t* nonfinite_out, void* workspace, void* stream) {
-  if (n < 0 || !norm_out || !nonfinite_out || !workspace || !(div > 0.0))
+static int grad_sumsq_f32(const float* grad, int64_t n, double div, double* out,
+                          uint32_t* nonfinite_out, void* workspace, void* stream, int want_sqrt) {
+  if (n < 0 || !out || !nonfinite_out || !workspace || !(div > 0.0))
     return fail(DVLA_ERR_USAGE, "bad grad_norm_f32 arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nblocks = kNormBlocks;
@@ -402,8 +426,18 @@ extern "C" int dvla_grad_norm_f32(const float* grad, int64_t n, double div, doub
         grad, n, per, div, partial, reinterpret_cast<unsigned*>(nonfinite_out));
     if (int rc = launch_check("sumsq_blocks_f32_kernel")) return rc;
   }
-  norm_finish_kernel<<<1, kFinishThreads, 0, st>>>(partial, nblocks, norm_out);
+  norm_finish_kernel<<<1, kFinishThreads, 0, st>>>(partial, nblocks, out, want_sqrt);
   return launch_check("norm_finish_kernel");
+}
+
+extern "C" int dvla_grad_norm_f32(const float* grad, int64_t n, double div, double* norm_out,
+                                  uint32_t* nonfinite_out, void* workspace, void* stream) {
+  return grad_sumsq_f32(grad, n, div, norm_out, nonfinite_out, workspace, stream, 1);
+}
+
+extern "C" int dvla_grad_sumsq_f32(const float* grad, int64_t n, double div, double* sumsq_out,
+                                   uint32_t* nonfinite_out, void* workspace, void* stream) {
+  return grad_sumsq_f32(grad, n, div, sumsq_out, nonfinite_out, workspace, stream, 0);
 }
 
 extern "C" int dvla_adam_tail_f32(float* params, const float* grad, double* m, double* v,

@@ -381,27 +381,40 @@ def expand_token_features(feats, pos, out):
 class TokenPolicy:
     """Action-token head W [V, H]: f32 master weights, f64 Adam moments and
     the bf16 working copy (what the forward GEMM reads; the optimizer tail
-    rewrites it as it steps the master weights) in a MODEL_COMPUTE pool."""
+    rewrites it as it steps the master weights) in a MODEL_COMPUTE pool.
 
-    def __init__(self, cfg: SwimlaneConfig, pool, device):
+    shard=(rank, N): ZeRO-1 layout for N learner GPUs -- the head's rows are
+    cut into N blocks of Vs = ceil(V / N) rows; this rank keeps the master
+    weights and moments of block `rank` only (the rows past V are zero
+    padding), the bf16 working copy of all blocks (all-gathered after each
+    step, so every rank holds the same bytes)."""
+
+    def __init__(self, cfg: SwimlaneConfig, pool, device, shard=None):
         import torch
         V, H = cfg.vocab, cfg.hidden
-        n = V * H
+        r, N = shard if shard is not None else (0, 1)
+        Vs = -(-V // N)
+        nloc = Vs * H
         g = torch.Generator(device=device).manual_seed(cfg.seed)
-        self.hm = pool.alloc(n * 4, align=256)
-        self.hmm = pool.alloc(n * 8, align=256)
-        self.hmv = pool.alloc(n * 8, align=256)
-        self.hw = pool.alloc(n * 2, align=256)
-        self.master = pool.view(self.hm, torch.float32)
-        self.master.copy_(torch.randn(n, device=device, generator=g) * (H ** -0.5))
-        self.m = pool.view(self.hmm, torch.float64)
-        self.v = pool.view(self.hmv, torch.float64)
+        self.hm = pool.alloc(nloc * 4, align=256)
+        self.hmm = pool.alloc(nloc * 8, align=256)
+        self.hmv = pool.alloc(nloc * 8, align=256)
+        self.hw = pool.alloc(N * nloc * 2, align=256)
+        full = torch.zeros(N * nloc, dtype=torch.float32, device=device)
+        full[:V * H] = torch.randn(V * H, device=device, generator=g) * (H ** -0.5)
+        self.master = pool.view(self.hm, torch.float32)[:nloc]
+        self.master.copy_(full[r * nloc:(r + 1) * nloc])
+        self.m = pool.view(self.hmm, torch.float64)[:nloc]
+        self.v = pool.view(self.hmv, torch.float64)[:nloc]
         self.m.zero_()
         self.v.zero_()
-        self.w16 = pool.view(self.hw, torch.bfloat16).view(V, H)
-        self.w16.copy_(self.master.view(V, H))
+        self.w16pad = pool.view(self.hw, torch.bfloat16)[:N * nloc]
+        self.w16pad.copy_(full)
+        self.w16 = self.w16pad[:V * H].view(V, H)
+        self.w16_own = self.w16pad[r * nloc:(r + 1) * nloc]
+        del full
         self.step = 0
-        self.V, self.H = V, H
+        self.V, self.H, self.Vs, self.rank, self.N = V, H, Vs, r, N
 
     def weight_bf16(self):
         """The bf16 head (round-to-nearest of the master weights), kept
@@ -516,20 +529,50 @@ class TrainerWorker:
         from .pools import Pool, PoolKind
         self.cfg, self.node, self.reducer = cfg, node, reducer
         self.stream, self.device = stream, device
-        self.policy = TokenPolicy(cfg, model_pool, device)
+        V, H, G, C, T = cfg.vocab, cfg.hidden, cfg.group_size, cfg.chunks, cfg.tokens
+        nodes = reducer.nodes
+        # ZeRO-1 over the learner GPUs when the gradient travels as NCCL f32
+        # sums: reduce-scatter the gradient, step this rank's row block,
+        # all-gather the bf16 weights (less traffic than all-reduce, and the
+        # optimizer tail runs on 1/N of the parameters)
+        self.sharded = nodes > 1 and reducer.backend == "nccl" and not reducer.exact
+        if self.sharded:
+            import torch.distributed as dist
+            shard = (dist.get_rank(reducer.group), nodes)
+        else:
+            shard = None
+        self.policy = TokenPolicy(cfg, model_pool, device, shard=shard)
         self.gcfg = GrpoConfig(group_size=cfg.group_size, lr=cfg.lr,
                                max_grad_norm=cfg.max_grad_norm)
-        V, H, G, C, T = cfg.vocab, cfg.hidden, cfg.group_size, cfg.chunks, cfg.tokens
         self.n_groups = cfg.n_groups if n_groups is None else int(n_groups)
         R = self.n_groups * G * C * T
         n = V * H
         self.loss = TokenLoss(self.n_groups, G, C, T, V, self.gcfg, dtype=torch.bfloat16,
                               device=device)
-        # f32 gradient + the skip word (one all-reduce buffer), long-lived
-        self.hg = model_pool.alloc((n + 1) * 4, align=256)
-        self.gbuf = model_pool.view(self.hg, torch.float32)[: n + 1]
-        self.grad2d = self.gbuf[:n].view(V, H)
-        self.skip = self.gbuf[n:n + 1]
+        if self.sharded:
+            # reduce-scatter input: N chunks of Vs rows (+ 64 floats holding the
+            # skip word, so the sum of every rank's abort flag lands in each
+            # rank's chunk); output: this rank's chunk
+            Vs = self.policy.Vs
+            self.cs = Vs * H + 64
+            self.hg = model_pool.alloc(nodes * self.cs * 4 + self.cs * 4, align=256)
+            allg = model_pool.view(self.hg, torch.float32)[: (nodes + 1) * self.cs]
+            allg.zero_()
+            self.gin = allg[: nodes * self.cs]
+            self.gshard = allg[nodes * self.cs:]
+            self.skip = self.gshard[Vs * H:Vs * H + 1]
+            self.skip_in = self.gin.view(nodes, self.cs)[:, Vs * H]
+            self.grad2d = None
+            self.sumsq = torch.zeros(1, dtype=torch.float64, device=device)
+            self._own_skip = torch.zeros(1, dtype=torch.float32, device=device)
+            self.status_out = self._own_skip
+        else:
+            # f32 gradient + the skip word (one all-reduce buffer), long-lived
+            self.hg = model_pool.alloc((n + 1) * 4, align=256)
+            self.gbuf = model_pool.view(self.hg, torch.float32)[: n + 1]
+            self.grad2d = self.gbuf[:n].view(V, H)
+            self.skip = self.gbuf[n:n + 1]
+            self.status_out = self.skip
         # activations of one update (logits, d loss / d logits, per-token
         # features): an activation pool of the recycled kind, reset per update
         act_bytes = R * (2 * V * 2 + H * 2) + (4 << 20)
@@ -544,7 +587,6 @@ class TrainerWorker:
         self.h_misc = torch.empty(2, dtype=torch.float64, pin_memory=True)  # norm, skip
         self.h_flags = torch.empty(2, dtype=torch.int32, pin_memory=True)
         self.h_skip = torch.empty(1, dtype=torch.float32, pin_memory=True)
-        self.buckets = 4 if reducer.nodes > 1 else 1
         self.version = 0
         self.done_event = None
         self.timing = None  # optional: dict of CUDA event pairs per phase
@@ -564,6 +606,74 @@ class TrainerWorker:
         return device_snapshot(self.policy.weight_bf16().reshape(-1), self.version, out=out,
                                stream=stream)
 
+    def _grad_tail(self, s, ev_t, mx):
+        """One GPU (or the switch-reduced / exact reducers): dW = dl^T x as
+        f32 GEMM output, the mean over nodes, norm, optimizer tail."""
+        from . import _lib
+        torch = __import__("torch")
+        pol, nodes = self.policy, self.reducer.nodes
+        V, H = pol.V, pol.H
+        n = V * H
+        torch.mm(self.dl.t(), self.feats_tok, out_dtype=torch.float32, out=self.grad2d)
+        if ev_t is not None:
+            ev_t["grad1"].record(s)
+        if nodes > 1:  # switch-reduced / exact paths: the mean itself
+            self.gbuf.copy_(self.reducer.reduce(self.gbuf))
+        if ev_t is not None:
+            ev_t["reduce1"].record(s)
+        g = self.gcfg
+        _lib.check(_lib.dvla_grad_norm_f32(self.gbuf.data_ptr(), n, 1.0, self.norm.data_ptr(),
+                                           self.flags.data_ptr(), self.norm_ws.data_ptr(),
+                                           s.cuda_stream), "dvla_grad_norm_f32")
+        _lib.check(_lib.dvla_adam_tail_f32(
+            pol.master.data_ptr(), self.gbuf.data_ptr(), pol.m.data_ptr(), pol.v.data_ptr(),
+            n, pol.step + 1, g.lr, g.beta1, g.beta2, g.opt_eps, 1.0, self.norm.data_ptr(), mx,
+            self.skip.data_ptr(), pol.w16.data_ptr(), self.flags.data_ptr() + 4,
+            s.cuda_stream), "dvla_adam_tail_f32")
+
+    def _grad_tail_sharded(self, s, ev_t, mx):
+        """N learner GPUs, ZeRO-1 (reference runtime.py:788-796 arithmetic):
+        dW row blocks as f32 GEMM outputs straight into the reduce-scatter
+        input -> NCCL reduce-scatter (sum) -> this rank's block / N -> global
+        norm (block sums of squares all-reduced) -> optimizer tail on the
+        block (skipped on every rank when any rank's loss aborted: the skip
+        words are summed with the gradient) -> NCCL all-gather of the bf16
+        blocks -> non-finite flags max-reduced."""
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+        pol, nodes, grp = self.policy, self.reducer.nodes, self.reducer.group
+        V, H, Vs = pol.V, pol.H, pol.Vs
+        nloc = Vs * H
+        gin2 = self.gin.view(nodes, self.cs)
+        for j in range(nodes):
+            a, b = j * Vs, min(V, (j + 1) * Vs)
+            if a < b:
+                torch.mm(self.dl[:, a:b].t(), self.feats_tok, out_dtype=torch.float32,
+                         out=gin2[j, :(b - a) * H].view(b - a, H))
+        self.skip_in.copy_(self._own_skip.expand(nodes))
+        if ev_t is not None:
+            ev_t["grad1"].record(s)
+        dist.reduce_scatter_tensor(self.gshard, self.gin, op=dist.ReduceOp.SUM, group=grp)
+        if ev_t is not None:
+            ev_t["reduce1"].record(s)
+        g = self.gcfg
+        div = float(nodes)
+        _lib.check(_lib.dvla_grad_sumsq_f32(self.gshard.data_ptr(), nloc, div,
+                                            self.sumsq.data_ptr(), self.flags.data_ptr(),
+                                            self.norm_ws.data_ptr(), s.cuda_stream),
+                   "dvla_grad_sumsq_f32")
+        dist.all_reduce(self.sumsq, op=dist.ReduceOp.SUM, group=grp)
+        torch.sqrt(self.sumsq, out=self.norm)
+        _lib.check(_lib.dvla_adam_tail_f32(
+            pol.master.data_ptr(), self.gshard.data_ptr(), pol.m.data_ptr(), pol.v.data_ptr(),
+            nloc, pol.step + 1, g.lr, g.beta1, g.beta2, g.opt_eps, div, self.norm.data_ptr(), mx,
+            self.skip.data_ptr(), pol.w16_own.data_ptr(), self.flags.data_ptr() + 4,
+            s.cuda_stream), "dvla_adam_tail_f32")
+        dist.all_gather_into_tensor(pol.w16pad, pol.w16_own, group=grp)
+        dist.all_reduce(self.flags, op=dist.ReduceOp.MAX, group=grp)
+
     def update(self, batches: list) -> dict:
         """One GRPO update on one epoch of groups (reference runtime.py:768-800)."""
         import torch
@@ -571,9 +681,7 @@ class TrainerWorker:
         from . import _lib
         from .grpo import stats_from_vector
         cfg, pol, s = self.cfg, self.policy, self.stream
-        V, H, C, T = cfg.vocab, cfg.hidden, cfg.chunks, cfg.tokens
-        n = V * H
-        nodes = self.reducer.nodes
+        H = cfg.hidden
         t0 = time.perf_counter()
         ids = [b.group_id for b in batches]
         if len(batches) != self.n_groups:
@@ -601,41 +709,15 @@ class TrainerWorker:
             if ev_t is not None:
                 ev_t["loss1"].record(s)
             _lib.check(_lib.dvla_loss_status(self.loss.stats_dev.data_ptr(),
-                                             self.skip.data_ptr(), s.cuda_stream),
+                                             self.status_out.data_ptr(), s.cuda_stream),
                        "dvla_loss_status")
             self.flags.zero_()
-            # dW = dl^T feats, f32 output, in buckets over V; each bucket's
-            # NCCL sum overlaps the next bucket's GEMM
-            overlap = self.reducer.overlappable(self.gbuf)
-            nb = self.buckets if overlap else 1
-            step = -(-V // nb)
-            works = []
-            for j in range(nb):
-                a, b_ = j * step, min(V, (j + 1) * step)
-                torch.mm(self.dl[:, a:b_].t(), self.feats_tok, out_dtype=torch.float32,
-                         out=self.grad2d[a:b_])
-                if overlap:
-                    hi = b_ * H if b_ < V else n + 1   # the skip word rides the last bucket
-                    works.append(self.reducer.reduce_async(self.gbuf[a * H:hi]))
-            if ev_t is not None:
-                ev_t["grad1"].record(s)
-            for w in works:
-                w.wait()
-            div = float(nodes) if overlap else 1.0
-            if nodes > 1 and not overlap:  # switch-reduced / exact paths: the mean itself
-                self.gbuf.copy_(self.reducer.reduce(self.gbuf))
-            if ev_t is not None:
-                ev_t["reduce1"].record(s)
             g = self.gcfg
             mx = float(g.max_grad_norm) if g.max_grad_norm is not None else 0.0
-            _lib.check(_lib.dvla_grad_norm_f32(self.gbuf.data_ptr(), n, div, self.norm.data_ptr(),
-                                               self.flags.data_ptr(), self.norm_ws.data_ptr(),
-                                               s.cuda_stream), "dvla_grad_norm_f32")
-            _lib.check(_lib.dvla_adam_tail_f32(
-                pol.master.data_ptr(), self.gbuf.data_ptr(), pol.m.data_ptr(), pol.v.data_ptr(),
-                n, pol.step + 1, g.lr, g.beta1, g.beta2, g.opt_eps, div, self.norm.data_ptr(), mx,
-                self.skip.data_ptr(), pol.w16.data_ptr(), self.flags.data_ptr() + 4,
-                s.cuda_stream), "dvla_adam_tail_f32")
+            if self.sharded:
+                self._grad_tail_sharded(s, ev_t, mx)
+            else:
+                self._grad_tail(s, ev_t, mx)
             if ev_t is not None:
                 ev_t["end"].record(s)
             self.h_stats.copy_(self.loss.stats_dev, non_blocking=True)
@@ -649,9 +731,10 @@ class TrainerWorker:
         skipped = float(self.h_skip[0]) != 0.0
         grad_bad = bool(self.h_flags[0])
         norm = float(self.h_misc[0])
-        rw_h = None
         if skipped or grad_bad or not np.isfinite(norm):
             # the device skipped the step: parameters and moments untouched
+            # (loss abort / non-finite loss on any rank, or a non-finite
+            # gradient: reference grpo.py:237-283 -> quarantine)
             stats_from_vector(sv, self.loss.group_ids, self.loss.order,
                               self.n_groups * cfg.group_size)          # local abort -> raises
             if skipped:
@@ -660,8 +743,6 @@ class TrainerWorker:
         rw_h = rw.cpu().numpy().reshape(self.n_groups, cfg.group_size)
         stats = stats_from_vector(sv, self.loss.group_ids, self.loss.order,
                                   self.n_groups * cfg.group_size, rw_h)
-        if not np.isfinite(stats["loss"]):
-            raise GrpoAbort(int(ids[0]), "non-finite loss or gradient")
         if bool(self.h_flags[1]):
             raise RunAbort("non-finite parameters after update",
                            lane=LaneId.TRAINER.value, epoch=self.version)

@@ -276,12 +276,17 @@ def main():
                          hidden=64, epochs=3, seed=11)
     res = run_swimlane(cfg)
     assert res.counters["updates"] == 3
-    for name, t in (("master", res.policy.master), ("w16", res.policy.w16.reshape(-1)),
-                    ("adam_m", res.policy.m)):
-        allw = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(allw, t.contiguous())
-        for r in range(1, world):
-            assert torch.equal(allw[0].view(torch.uint8), allw[r].view(torch.uint8)), (name, r)
+    pol = res.policy
+    t = pol.w16.reshape(-1)
+    allw = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(allw, t.contiguous())
+    for r in range(1, world):
+        assert torch.equal(allw[0].view(torch.int16), allw[r].view(torch.int16)), ("w16", r)
+    # ZeRO-1: each rank steps its own row block of the master weights; the
+    # all-gathered bf16 block is that block's round-to-nearest
+    assert pol.N == world and pol.rank == rank
+    assert torch.equal(pol.w16_own, pol.master.to(torch.bfloat16))
+    assert res.counters["updates"] == 3 and pol.step == 3
     if rank == 0:
         print("SWIMLANE_WEIGHTS_EQUAL_OK", flush=True)
     dist.barrier()
