@@ -805,6 +805,55 @@ def _bench_learner_step(world, rank, dev, barrier, max_over_ranks, steps=10, war
     return out
 
 
+C3_WEIGHT_BYTES = 6_600_000_000     # pi0-3B-shaped bf16 weights (BASELINE config 3)
+
+
+def _bench_disaggregated(world, rank, dev, epochs=8, keep_timeline=False, engine="ce_head"):
+    """BASELINE config 3 layout inside the RL loop (disagg.run_disaggregated):
+    learner ranks {0, 1} (from 4 GPUs; {0} below) and rollout ranks, the
+    C4-shaped action head trained on the rollout ranks' trajectories, and
+    every published version -- the head plus a constant body blob up to the
+    pi0-3B weight volume (6.6 GB) -- pushed over NVLink by the split TMA
+    chains into the rollout ranks' MODEL_COMPUTE replica rings, checksummed
+    on every receiver.  Rank 0 (learner 0) reports."""
+    from paper_2605_13276_b200.disagg import default_learners, run_disaggregated
+    from paper_2605_13276_b200.runtime import SwimlaneConfig
+    cfg = SwimlaneConfig(n_groups=N_GROUPS, group_size=G, chunks=C, tokens=T, vocab=V,
+                         hidden=SWIM_H, epochs=epochs, seed=29)
+    body = max(0, C3_WEIGHT_BYTES - V * SWIM_H * 2)
+    res = run_disaggregated(cfg, verify=True, body_bytes=body, timeout_s=300.0, engine=engine)
+    tl = None
+    if keep_timeline:
+        import torch.distributed as dist
+        tl = [None] * world
+        dist.all_gather_object(tl, res.timeline)
+    if rank != 0:
+        return None
+    sm = res.summary()
+    L = default_learners(world)
+    peak = _nvl_peak()
+    S = V * SWIM_H * 2 + body
+    gbs = S / (sm["receiver_ms_median_max"] / 1e3) / 1e9 if sm["receiver_ms_median_max"] else None
+    return {"layout": f"learners {L}, rollout ranks {[r for r in range(world) if r not in L]}",
+            "engine": engine,
+            "trajectories_per_s_total": sm["trajectories_per_s"],
+            "updates": sm["updates"], "quarantined": sm["quarantined"],
+            "weight_bytes_per_version": V * SWIM_H * 2 + body,
+            "replication_ms_per_iteration_median": sm["receiver_ms_median_max"],
+            "replication_gbs_per_receiver": gbs,
+            "replication_frac_of_nvlink_peak": (gbs / peak) if gbs else None,
+            "source_hop_ms_median": sm["replication_ms_median"],
+            "lane_s_rank0": sm["lane_s"],
+            "nvlink_peak_gbs": peak,
+            "replication_overlapped_with_updates": sm["overlap"],
+            "checksum_mismatches": sm["checksum_mismatches"],
+            **({"timeline": tl} if tl else {}),
+            "timing": "learner 0: host clock between first and last publish (traj/s); "
+                      "replication: CUDA events around each rollout rank's hop launch on its "
+                      "receive stream (launched once the chain heads run) until every chunk "
+                      "landed, median per rank, max over ranks"}
+
+
 def _bench_swimlane(world, rank, dev, max_over_ranks, epochs=8):
     """End-to-end RL samples/s of the four-lane swimlane (BASELINE config 4
     shape: OpenVLA-7B-sized action head V=32,064 x H=4,096, 64 groups x 8
@@ -1072,6 +1121,10 @@ def run_ours(a):
         swim = _bench_swimlane(world, rank, dev, max_over_ranks)
         barrier()
         swim["model"] = _guarded(_swim_model, swim, world, roofline, sampler, optimizer)
+        if world >= 2:
+            barrier()
+            swim["disaggregated"] = _guarded(_bench_disaggregated, world, rank, dev)
+            barrier()
         # the GPU-work bound of one epoch on one GPU: the sampler's device
         # work (the strict-alternation rollout lane) + the learner step
         if isinstance(learner, dict) and "ms_per_step_device" in learner:

@@ -319,6 +319,11 @@ int dvla_snapshot_copy(const void* src, void* dst, int64_t nbytes, int dtype,
 /* Bitwise compare (messages_equal on parameter bytes, wire.py:279-281):
  * out_dev[0] = number of differing 16-byte words, out_dev[1] = first
  * differing byte offset (UINT64_MAX if equal). */
+/* Order-independent checksum of a region (a replica checked against its
+ * source on another GPU): out_dev[0] = sum of its 8-byte little-endian words,
+ * out_dev[1] = sum of word_i * (2 i + 1), both mod 2^64 (a trailing partial
+ * word zero-padded).  8-byte aligned; one read; asynchronous on `stream`. */
+int dvla_checksum64(const void* p, int64_t nbytes, uint64_t* out_dev, void* stream);
 int dvla_bytes_equal(const void* a, const void* b, int64_t nbytes, uint64_t* out_dev,
                      void* stream);
 

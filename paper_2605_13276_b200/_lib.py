@@ -155,6 +155,7 @@ dvla_replicate_chain = _proto("dvla_replicate_chain", [
     C.POINTER(Hop), _i32, _i64, _i64, C.c_uint32, _i32, C.c_uint64, _vp, _vp])
 dvla_snapshot_copy = _proto("dvla_snapshot_copy", [_vp, _vp, _i64, _i32, _vp, _vp])
 dvla_bytes_equal = _proto("dvla_bytes_equal", [_vp, _vp, _i64, _vp, _vp])
+dvla_checksum64 = _proto("dvla_checksum64", [_vp, _i64, _vp, _vp])
 dvla_memcpy_async = _proto("dvla_memcpy_async", [_vp, _vp, _i64, _vp])
 dvla_nccl_init = _proto("dvla_nccl_init", [_i32, C.POINTER(_i32)])
 dvla_nccl_group_start = _proto("dvla_nccl_group_start", [])

@@ -207,6 +207,41 @@ __global__ void bytes_equal_kernel(const uint4* __restrict__ a, const uint4* __r
   if ((threadIdx.x & 31) == 0 && mism) atomicAdd(out, mism);
 }
 
+// Order-independent 64-bit checksum of a region (verification of a replica
+// against its source on another GPU without moving either): over 8-byte
+// words w_i, out[0] += w_i and out[1] += w_i * (2 i + 1) mod 2^64 (the
+// index weight catches swapped or shifted chunks); a byte tail is folded in
+// as one zero-padded word.  One read of the region.
+__global__ void checksum64_kernel(const uint2* __restrict__ w, int64_t nwords,
+                                  unsigned long long* out) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  unsigned long long s0 = 0, s1 = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nwords;
+       i += stride) {
+    const uint2 x = __ldcs(w + i);
+    const unsigned long long v = (static_cast<unsigned long long>(x.y) << 32) | x.x;
+    s0 += v;
+    s1 += v * static_cast<unsigned long long>(2 * i + 1);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out, s0);
+    atomicAdd(out + 1, s1);
+  }
+}
+
+__global__ void checksum64_tail_kernel(const uint8_t* p, int64_t from, int64_t n,
+                                       unsigned long long* out) {
+  unsigned long long v = 0;
+  for (int64_t i = from; i < n; ++i) v |= static_cast<unsigned long long>(p[i]) << (8 * (i - from));
+  const unsigned long long idx = static_cast<unsigned long long>(from / 8);
+  atomicAdd(out, v);
+  atomicAdd(out + 1, v * (2 * idx + 1));
+}
+
 __global__ void bytes_equal_tail_kernel(const uint8_t* a, const uint8_t* b, int64_t from,
                                         int64_t n, unsigned long long* out) {
   const int64_t i = from + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -391,6 +426,23 @@ extern "C" int dvla_bytes_equal(const void* a, const void* b, int64_t nbytes, ui
     bytes_equal_tail_kernel<<<static_cast<unsigned>((nbytes - from + 255) / 256), 256, 0, st>>>(
         static_cast<const uint8_t*>(a), static_cast<const uint8_t*>(b), from, nbytes, out);
   return launch_check("bytes_equal_kernel");
+}
+
+extern "C" int dvla_checksum64(const void* p, int64_t nbytes, uint64_t* out_dev, void* stream) {
+  if (nbytes < 0) return fail(DVLA_ERR_USAGE, "nbytes must be >= 0");
+  if (!out_dev || (!p && nbytes > 0)) return fail(DVLA_ERR_USAGE, "null pointer argument");
+  if (reinterpret_cast<uintptr_t>(p) % 8) return fail(DVLA_ERR_USAGE, "region must be 8-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* out = reinterpret_cast<unsigned long long*>(out_dev);
+  DVLA_CUDA_TRY(cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), st));
+  const int64_t nwords = nbytes / 8;
+  if (nwords > 0)
+    checksum64_kernel<<<grid_for(nwords, 256), 256, 0, st>>>(static_cast<const uint2*>(p), nwords,
+                                                              out);
+  if (nwords * 8 < nbytes)
+    checksum64_tail_kernel<<<1, 1, 0, st>>>(static_cast<const uint8_t*>(p), nwords * 8, nbytes,
+                                            out);
+  return launch_check("checksum64_kernel");
 }
 
 extern "C" int dvla_memcpy_async(void* dst, const void* src, int64_t nbytes, void* stream) {

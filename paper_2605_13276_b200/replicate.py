@@ -86,6 +86,17 @@ def device_snapshot(params, version: int, out=None, stream=None,
                          else dst, ready=ready)
 
 
+def checksum64_async(t, stream=None):
+    """Device u64[2] checksum of a tensor's bytes (dvla_checksum64), on
+    `stream`; compare two GPUs' copies of a region without moving either."""
+    from . import _lib
+    torch = _torch()
+    out = torch.empty(2, dtype=torch.int64, device=t.device)
+    _lib.check(_lib.dvla_checksum64(t.data_ptr(), t.numel() * t.element_size(), out.data_ptr(),
+                                    _stream_ptr(stream)), "dvla_checksum64")
+    return out
+
+
 def bytes_equal(a, b, stream=None) -> tuple[int, int]:
     """(number of differing 16-byte words, first differing byte or -1)."""
     from . import _lib
@@ -604,37 +615,55 @@ class SplitReplicator:
     rank's hops run in one kernel launch (one CTA group per hop)."""
 
     def __init__(self, nbytes: int, chains, n_buffers: int = 2, chunk_bytes=None,
-                 ctas_per_hop: int = 64, group=None):
+                 ctas_per_hop: int = 64, group=None, pool=None, engine: str = "sm"):
         import torch.distributed as dist
         torch = _torch()
         parts = len(chains)
         if parts < 1 or nbytes % (16 * parts):
             raise UsageError("the region must split into 16-byte-aligned equal parts")
+        if engine not in ("sm", "ce", "ce_head"):
+            raise UsageError(f"engine must be 'sm' (TMA kernel), 'ce' (copy engines) or "
+                             f"'ce_head' (copy engines at the chain heads, TMA kernel on the "
+                             f"forwarding hops), got {engine!r}")
         self.rank = dist.get_rank()
         self.chains = [list(c) for c in chains]
         self.nbytes, self.parts, self.nb = int(nbytes), parts, int(n_buffers)
         self.part = self.nbytes // parts
         self.ctas = int(ctas_per_hop)
-        self.chunk = int(chunk_bytes) if chunk_bytes else chain_chunk_bytes(self.part, self.ctas)
+        self.engine = engine
+        if chunk_bytes:
+            self.chunk = int(chunk_bytes)
+        elif engine in ("ce", "ce_head"):   # three stream operations per chunk: keep them few
+            self.chunk = int(min(max(self.part // 64, 4 << 20), 64 << 20)) // 16 * 16
+        else:
+            self.chunk = chain_chunk_bytes(self.part, self.ctas)
         self.n_chunks = (self.part + self.chunk - 1) // self.chunk
         receivers = sorted({r for c in self.chains for r in c[1:]})
         self.err = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.buf = self.flags = None
         handles = None
         if self.rank in receivers:
-            self.buf = _Slab(self.nb * self.nbytes, torch.cuda.current_device())
+            # the replica ring lands in the receiver's MODEL_COMPUTE pool when
+            # one is given (the pool's slab is what is IPC-shared)
+            if pool is not None:
+                self.buf = _PoolRegion(pool, self.nb * self.nbytes)
+            else:
+                self.buf = _Slab(self.nb * self.nbytes, torch.cuda.current_device())
             fb = ((self.nb * parts * self.n_chunks * 4 + 255) // 256) * 256
             self.flags = _Slab(fb, torch.cuda.current_device())
             self.flags.t.zero_()
             torch.cuda.synchronize()
-            handles = (self.buf.ipc(), self.flags.ipc())
+            handles = (self.buf.ipc(), getattr(self.buf, "offset", 0), self.flags.ipc())
         allh = _gather_by_rank(handles, group)
         self.peer = {}
+        self._opened = []
         for c in self.chains:
             if self.rank in c and c.index(self.rank) < len(c) - 1:
                 nxt = c[c.index(self.rank) + 1]
                 if nxt not in self.peer:
-                    self.peer[nxt] = (_open_ipc(allh[nxt][0]), _open_ipc(allh[nxt][1]))
+                    base = _open_ipc(allh[nxt][0])
+                    self._opened.append(base)
+                    self.peer[nxt] = (base + allh[nxt][1], _open_ipc(allh[nxt][2]))
 
     def _flag_off(self, b: int, c: int) -> int:
         return (b * self.parts + c) * self.n_chunks * 4
@@ -650,6 +679,7 @@ class SplitReplicator:
         b = version % self.nb
         epoch = version + 1
         specs = []
+        heads = []   # specs of hops this rank sources as a chain head
         for c, chain in enumerate(self.chains):
             if self.rank not in chain:
                 continue
@@ -664,10 +694,22 @@ class SplitReplicator:
                 wait = self.flags.ptr + self._flag_off(b, c)
             if pos < len(chain) - 1:
                 nb_ptr, nf_ptr = self.peer[chain[pos + 1]]
-                specs.append((s_ptr, nb_ptr + b * self.nbytes + off, wait,
-                              nf_ptr + self._flag_off(b, c)))
+                spec = (s_ptr, nb_ptr + b * self.nbytes + off, wait, nf_ptr + self._flag_off(b, c))
             else:
-                specs.append((None, None, wait, None))
+                spec = (None, None, wait, None)
+            (heads if pos == 0 else specs).append(spec)
+        ce = list(heads) if self.engine in ("ce", "ce_head") else []
+        if self.engine == "ce":
+            ce += specs
+            specs = []
+        elif self.engine == "sm":
+            specs = heads + specs
+        # copy engines: stream-ordered waits, peer copies and flag writes; no
+        # SMs are held while the bytes move (the GEMMs keep them)
+        for s_ptr, d_ptr, wait, nf in ce:
+            _lib.check(_lib.dvla_replicate_hop_ce(s_ptr, d_ptr, wait, nf, self.part,
+                                                  self.chunk, epoch, _stream_ptr(stream)),
+                       "dvla_replicate_hop_ce")
         if not specs:
             return
         _lib.check(_lib.dvla_replicate_chain(_hops(specs), len(specs), self.part, self.chunk,
@@ -682,10 +724,12 @@ class SplitReplicator:
 
     def close(self):
         from . import _lib
-        for bp, fp in self.peer.values():
-            _lib.dvla_ipc_close(bp)
+        for p in self._opened:
+            _lib.dvla_ipc_close(p)
+        for _, fp in self.peer.values():
             _lib.dvla_ipc_close(fp)
         self.peer = {}
+        self._opened = []
 
 
 def replicate_devices(src, dsts, mode: str = "chain", chunk_bytes: int = 0, streams=None):

@@ -498,7 +498,12 @@ class SamplerWorker:
         ev.synchronize()
         meta = {"roll_wall": time.perf_counter() - t0, "epoch": epoch,
                 "behavior_version": snap.version,
-                "success_rate": float(rewards.float().mean().item()) if not poison else 0.0}
+                "success_rate": float(rewards.float().mean().item()) if not poison else 0.0,
+                # the whole epoch as one message (cross-process hand-off)
+                "epoch_batch": GroupBatch(
+                    group_id=base, horizon=C * T, chunk=T, obs=feats.view(n_traj, C, H),
+                    actions=tokens.view(n_traj, C, T), behavior_log_prob=blp.view(n_traj, C),
+                    rewards=rewards, behavior_version=snap.version, tokens=None)}
         return msgs, meta
 
 
@@ -860,6 +865,7 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
     dist_cv = threading.Condition()
 
     def sampler_lane():
+        torch.cuda.set_device(dev)   # the current device is per host thread
         try:
             for epoch in range(cfg.epochs):
                 snap, stal = board.wait_gate()
@@ -878,6 +884,7 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
             monitor.fail(f"sampler: {e!r}", LaneId.SAMPLER.value, -1)
 
     def trainer_lane():
+        torch.cuda.set_device(dev)   # the current device is per host thread
         try:
             for epoch in range(cfg.epochs):
                 batches = [chan.take() for _ in range(cfg.n_groups)]
@@ -925,6 +932,7 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
             monitor.fail(f"trainer: {e!r}", LaneId.TRAINER.value, -1)
 
     def dist_lane():
+        torch.cuda.set_device(dev)   # the current device is per host thread
         try:
             while True:
                 with dist_cv:
@@ -944,6 +952,7 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
             monitor.fail(f"dist: {e!r}", LaneId.WEIGHT_DIST.value, -1)
 
     def recv_lane():
+        torch.cuda.set_device(dev)   # the current device is per host thread
         try:
             while not (board.sampler_done and mailbox._slot is None):
                 snap = mailbox.take_newest(timeout=0.2)

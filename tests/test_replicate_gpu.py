@@ -134,3 +134,25 @@ def test_replicate_devices_single_process(dev, mode):
         replicate_devices(src, dsts, mode=mode, chunk_bytes=(1 << 20) + 16 * it)
         for d in dsts:
             assert bytes_equal(src.to(d.device), d) == (0, -1)
+
+
+def test_checksum64_matches_host_and_sees_swaps(dev):
+    """dvla_checksum64 (the per-version replica check of the disaggregated
+    swimlane): equals the host formula incl. a partial tail word, and
+    changes when two chunks swap (the index-weighted sum)."""
+    import torch
+    from paper_2605_13276_b200.replicate import checksum64_async
+    n = 10_000_005
+    t = torch.randint(0, 256, (n,), dtype=torch.uint8, device=dev)
+    junk = torch.full((64,), -1, dtype=torch.int64, device=dev)   # dirty the allocator cache
+    del junk
+    got = [int(x) & (2**64 - 1) for x in checksum64_async(t).cpu().tolist()]
+    b = t.cpu().numpy().tobytes() + b"\0" * (8 - n % 8)
+    w = np.frombuffer(b, dtype="<u8").astype(object)
+    s0 = int(sum(w)) % 2**64
+    s1 = int(sum(int(x) * (2 * i + 1) for i, x in enumerate(w))) % 2**64
+    assert got == [s0, s1]
+    u = t.clone()
+    u[:4096], u[4096:8192] = t[4096:8192], t[:4096]
+    g2 = [int(x) & (2**64 - 1) for x in checksum64_async(u).cpu().tolist()]
+    assert g2[0] == got[0] and g2[1] != got[1]

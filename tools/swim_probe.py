@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--epochs", type=int, default=8)
     ap.add_argument("--no-swim", action="store_true")
     ap.add_argument("--no-learner", action="store_true")
+    ap.add_argument("--disagg", action="store_true")
     a = ap.parse_args()
     world, rank, local = bench._dist()
     torch.cuda.set_device(local)
@@ -48,6 +49,12 @@ def main():
     if not a.no_swim:
         barrier()
         out["swimlane"] = bench._bench_swimlane(world, rank, dev, mx, epochs=a.epochs)
+    if a.disagg and world > 1:
+        barrier()
+        for eng in ("ce_head", "sm"):
+            barrier()
+            out[f"disaggregated_{eng}"] = bench._bench_disaggregated(
+                world, rank, dev, keep_timeline=True, engine=eng)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
