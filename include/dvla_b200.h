@@ -18,10 +18,12 @@
  *    dvla_last_error() returns a thread-local message.  Status codes map
  *    1:1 onto the reference's exception types (see dvla_status).
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).
- *  - the library holds no global mutable state besides a per-device SM
- *    count cache and kernel attribute flags; calls are thread-safe across
- *    distinct streams (the reference's nogil lane concurrency,
- *    numba_backend.py:1-5).
+ *  - the library's global mutable state: a per-device SM count cache,
+ *    kernel attribute flags, the profiling hooks (dvla_profile_*), and the
+ *    flag buffers + epoch counter of the single-process dvla_replicate
+ *    (guarded by a mutex held for the whole call); everything else is
+ *    per call or per handle.  Calls are thread-safe across distinct
+ *    streams (the reference's nogil lane concurrency, numba_backend.py:1-5).
  */
 #ifndef DVLA_B200_H
 #define DVLA_B200_H

@@ -14,6 +14,8 @@
 // checked by dvla_bytes_equal on every bench run.
 #include <stdlib.h>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "drv.cuh"
 
@@ -536,8 +538,12 @@ struct RepFlags {
   size_t count = 0;
   uint32_t* err = nullptr;
 };
+// The single-process replication's flag buffers and epoch counter (the
+// only mutable library state): every dvla_replicate / dvla_replicate_status
+// call holds g_rep_mutex for its whole (host-side, enqueue-only) duration.
 static RepFlags g_rep_flags[64];
 static uint32_t g_rep_epoch = 0;
+static std::mutex g_rep_mutex;
 }  // namespace dvla
 
 extern "C" int dvla_replicate(int src_dev, const void* src, int n_dst, const int* dst_devs,
@@ -549,6 +555,7 @@ extern "C" int dvla_replicate(int src_dev, const void* src, int n_dst, const int
   if (n_dst == 0 || nbytes == 0) return DVLA_OK;
   if (chunk_bytes <= 0) chunk_bytes = 1 << 20;
   if (chunk_bytes % 16) return fail(DVLA_ERR_USAGE, "chunk_bytes must be a multiple of 16");
+  std::lock_guard<std::mutex> lock(g_rep_mutex);
   int prev = 0;
   DVLA_CUDA_TRY(cudaGetDevice(&prev));
   auto stream_of = [&](int i) {  // i = 0: source, i > 0: destination i - 1
@@ -639,6 +646,7 @@ extern "C" int dvla_replicate(int src_dev, const void* src, int n_dst, const int
 // (synchronous; call after the streams used by dvla_replicate are idle).
 extern "C" int dvla_replicate_status(int* timed_out) {
   if (!timed_out) return fail(DVLA_ERR_USAGE, "null out pointer");
+  std::lock_guard<std::mutex> lock(g_rep_mutex);
   int prev = 0;
   DVLA_CUDA_TRY(cudaGetDevice(&prev));
   *timed_out = 0;

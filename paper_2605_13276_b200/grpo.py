@@ -597,10 +597,18 @@ def grpo_loss(params, batches, cfg: GrpoConfig) -> float:
 
 
 def infer_policy_config(params):
+    """The structural config a params object implies (reference
+    grpo.py:323-330).  The reference fixes act_dim = 2 (its env) and sets
+    chunk = out_dim // 2, which drops a unit for an odd out_dim; here the
+    split keeps chunk * act_dim == out_dim (act_dim 2 when out_dim is even,
+    else 1) -- unflatten only needs out_dim, so even-width heads behave
+    exactly as in the reference."""
     from .policy import PolicyConfig
     hidden, obs_dim = tuple(params.w1.shape)
     out_dim = tuple(params.w2.shape)[0]
-    return PolicyConfig(obs_dim=obs_dim, hidden=hidden, chunk=out_dim // 2, act_dim=2)
+    act_dim = 2 if out_dim % 2 == 0 else 1
+    return PolicyConfig(obs_dim=obs_dim, hidden=hidden, chunk=out_dim // act_dim,
+                        act_dim=act_dim)
 
 
 def grpo_update(params, batches, cfg: GrpoConfig, adam: AdamState, version: int):

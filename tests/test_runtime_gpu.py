@@ -21,9 +21,10 @@ def test_nvlink_broadcast_into_subscriber_regions(dev):
         snap = snapshot_from_params(p, v)
         plane.broadcast(snap)
         torch.cuda.synchronize()
+        plane.check()
         for b in boxes:
             got = b.take_newest()
-            assert got.version == v
+            assert got.version == v and got.ready is not None and got.ready.query()
             assert got.params.data_ptr() == b.region(v).data_ptr()  # zero-copy view
             assert bytes_equal(got.params, p) == (0, -1)
     assert t.copy_counter == 9 and t.bytes_counter == 9 * 4 * n

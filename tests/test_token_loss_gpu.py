@@ -444,3 +444,51 @@ def test_back_to_back_launches_see_their_own_inputs():
         scale = sum(abs(v) for v in ost["coeff"].ravel()) / max(ost["coeff"].size, 1)
         assert abs(sv[_lib.ST_LOSS] - oloss) <= 1e-5 * max(abs(oloss), scale, 1e-12)
         assert_dlogits_close(dl.float().cpu().numpy(), odl.reshape(dl.shape), 1e-2)
+
+
+@pytest.mark.parametrize("priority", [-1, 0])
+def test_fused_kernel_beside_gemms_on_another_stream(priority):
+    """The fused kernel's CTAs wait on each other's published token
+    log-probs, so it needs all of its CTAs resident.  Launched while another
+    stream's GEMMs hold the SMs (the swimlane's sampler beside the trainer),
+    it must still finish -- its CTAs become resident as the GEMM CTAs retire
+    (no deadlock: resident fused CTAs never wait on the GEMM) -- without the
+    spin timeout (ST_KERNEL_ERR) and with the oracle's result, on a
+    high-priority stream (the trainer's) and a default-priority one."""
+    import torch
+    from paper_2605_13276_b200 import grpo
+    dev = torch.device("cuda", 0)
+    x, tokens, blp, rewards, ids = _case(41, 4, 8, 1, 56, 32064, torch.bfloat16)
+    cfg = grpo.GrpoConfig(group_size=8)
+    R, V = 4 * 8 * 56, 32064
+    tl = grpo.TokenLoss(4, 8, 1, 56, V, cfg, dtype=torch.bfloat16, device=dev)
+    tl.set_groups(ids)
+    lg = torch.from_numpy(x.reshape(R, V)).to(dev, torch.bfloat16)
+    tk = torch.from_numpy(tokens.reshape(-1)).to(dev)
+    bl = torch.from_numpy(blp.reshape(-1)).to(dev)
+    rw = torch.from_numpy(rewards.reshape(-1)).to(dev)
+    dl = torch.empty_like(lg)
+    a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+    b = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+    side = torch.cuda.Stream(device=dev)
+    mine = torch.cuda.Stream(device=dev, priority=priority)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    started = torch.cuda.Event()
+    with torch.cuda.stream(side):
+        torch.mm(a, b)
+        started.record(side)
+        for _ in range(11):                          # ~10 ms more GEMM CTAs on every SM
+            torch.mm(a, b)
+    with torch.cuda.stream(mine):
+        mine.wait_event(started)                     # launched while the GEMMs run
+        e0.record(mine)
+        tl.launch(lg, tk, bl, rw, dl, stream=mine)
+        e1.record(mine)
+    torch.cuda.synchronize()
+    st = tl.stats(rewards)                           # raises on ST_KERNEL_ERR (timeout)
+    oloss, odl, ost = O.grpo_token_grad(x, tokens, blp, rewards, ids)
+    scale = float(np.abs(ost["coeff"]).mean())
+    assert abs(st["loss"] - oloss) <= 1e-5 * max(abs(oloss), scale)
+    assert_dlogits_close(dl.float().cpu().numpy(), odl.reshape(R, V), 1e-2)
+    print(f"fused loss beside GEMMs (priority {priority}): {e0.elapsed_time(e1):.2f} ms")
