@@ -270,6 +270,17 @@ int dvla_arena_is_live(dvla_arena* arena, int64_t generation, int64_t serial, in
 int dvla_arena_stats(dvla_arena* arena, int64_t* out);
 /* kernels.alloc_trace_run (numba_backend.py:139-247), host memory in/out;
  * final_out[3] = (total_free, largest_free, n_extents). */
+/* torch's caching allocator on an ENV_AUX arena (torch
+ * temporaries in the recycled pool).  dvla_torch_pool_bind(device, arena,
+ * slab_base) routes every segment a torch.cuda.MemPool built on
+ * dvla_torch_alloc / dvla_torch_free (the CUDAPluggableAllocator signatures;
+ * stream is a cudaStream_t) requests on `device` into the arena's slab
+ * (first fit, 512-byte aligned); arena = NULL unbinds (refused while torch
+ * segments are live).  A bound arena refuses epoch_reset.  alloc returns
+ * NULL when the arena cannot place the segment (torch raises OOM). */
+int dvla_torch_pool_bind(int device, dvla_arena* arena, void* slab_base);
+void* dvla_torch_alloc(size_t size, int device, void* stream);
+void dvla_torch_free(void* ptr, size_t size, int device, void* stream);
 int dvla_arena_trace(int64_t capacity, int64_t n, const uint8_t* is_alloc, const int64_t* size,
                      const int64_t* align, const uint64_t* pick, uint8_t* out_ok,
                      int64_t* out_off, int64_t* final_out);

@@ -49,6 +49,7 @@ struct dvla_arena {
   std::unordered_map<int64_t, Live> live;  // serial -> block
   int64_t next_serial = 1;
   int64_t alloc_count = 0, free_count = 0, failed_allocs = 0, churn_bytes = 0;
+  int torch_bound = 0;   // hosting torch's segments (dvla_torch_pool_bind): no epoch reset
   std::mutex mu;
 };
 
@@ -185,6 +186,9 @@ extern "C" int dvla_arena_epoch_reset(dvla_arena* a) {
     return dvla::fail(DVLA_ERR_POOL_USAGE,
                       "epoch_reset on a %s pool; model allocations are long-lived by contract",
                       kind_name(a->kind));
+  if (a->torch_bound)
+    return dvla::fail(DVLA_ERR_POOL_USAGE,
+                      "epoch_reset on a pool that hosts torch's allocations (unbind it first)");
   a->generation += 1;
   a->live.clear();
   a->free_off.assign(1, 0);
@@ -272,4 +276,75 @@ extern "C" int dvla_arena_trace(int64_t capacity, int64_t n, const uint8_t* is_a
     final_out[2] = static_cast<int64_t>(fs.size());
   }
   return DVLA_OK;
+}
+
+// ---- torch's caching allocator on top of an ENV_AUX arena
+//
+// torch temporaries (activations, concatenations, the
+// sampler's observation tensors) belong in the recycled pool, not in
+// torch's own cudaMalloc segments.  dvla_torch_alloc / dvla_torch_free have
+// the signatures of torch.cuda.memory.CUDAPluggableAllocator; inside a
+// torch.cuda.MemPool built on them, every segment torch requests is placed
+// by the first-fit arena bound to that device (pools.torch_arena) in that
+// arena's device slab.  Torch sub-allocates and caches within its segments.
+namespace {
+struct TorchBinding {
+  dvla_arena* arena = nullptr;
+  uintptr_t base = 0;
+  std::unordered_map<uintptr_t, std::pair<int64_t, int64_t>> live;  // ptr -> (serial, gen)
+  std::mutex mu;
+};
+TorchBinding g_torch[64];
+}  // namespace
+
+extern "C" int dvla_torch_pool_bind(int device, dvla_arena* a, void* base) {
+  if (device < 0 || device >= 64) return dvla::fail(DVLA_ERR_USAGE, "device out of range");
+  TorchBinding& b = g_torch[device];
+  std::lock_guard<std::mutex> g(b.mu);
+  if (a && (!base || a->kind != DVLA_POOL_ENV_AUX))
+    return dvla::fail(DVLA_ERR_USAGE, "torch allocations bind to an ENV_AUX device pool");
+  if (a && b.arena && b.arena != a)
+    return dvla::fail(DVLA_ERR_POOL_USAGE, "device %d already hosts torch in another pool",
+                      device);
+  if (!a && !b.live.empty())
+    return dvla::fail(DVLA_ERR_POOL_USAGE, "%zu torch segments still live in the pool",
+                      b.live.size());
+  if (b.arena) {
+    std::lock_guard<std::mutex> ga(b.arena->mu);
+    b.arena->torch_bound = 0;
+  }
+  b.arena = a;
+  b.base = reinterpret_cast<uintptr_t>(base);
+  if (a) {
+    std::lock_guard<std::mutex> ga(a->mu);
+    a->torch_bound = 1;
+  }
+  return DVLA_OK;
+}
+
+extern "C" void* dvla_torch_alloc(size_t size, int device, void* stream) {
+  (void)stream;
+  if (device < 0 || device >= 64 || size == 0) return nullptr;
+  TorchBinding& b = g_torch[device];
+  std::lock_guard<std::mutex> g(b.mu);
+  if (!b.arena) return nullptr;
+  int64_t off = 0, serial = 0, gen = 0;
+  if (dvla_arena_alloc(b.arena, static_cast<int64_t>(size), 512, &off, &serial, &gen) != DVLA_OK)
+    return nullptr;  // torch reports out of memory for the pool
+  const uintptr_t p = b.base + static_cast<uintptr_t>(off);
+  b.live[p] = {serial, gen};
+  return reinterpret_cast<void*>(p);
+}
+
+extern "C" void dvla_torch_free(void* ptr, size_t size, int device, void* stream) {
+  (void)stream;
+  if (device < 0 || device >= 64 || !ptr) return;
+  TorchBinding& b = g_torch[device];
+  std::lock_guard<std::mutex> g(b.mu);
+  auto it = b.live.find(reinterpret_cast<uintptr_t>(ptr));
+  if (!b.arena || it == b.live.end()) return;
+  const int64_t off = static_cast<int64_t>(reinterpret_cast<uintptr_t>(ptr) - b.base);
+  dvla_arena_free(b.arena, b.arena->pool_id, off, static_cast<int64_t>(size), it->second.second,
+                  it->second.first);
+  b.live.erase(it);
 }

@@ -18,6 +18,7 @@ at every epoch boundary.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass
 from enum import Enum
 
@@ -203,6 +204,97 @@ class Pool:
     def run_trace(self, is_alloc, size, align, pick):
         """Batched trace through the native arena (alloc_trace_run contract)."""
         return arena_trace(self.capacity, is_alloc, size, align, pick)
+
+
+class TorchArena:
+    """Torch's own allocations in an ENV_AUX pool.
+
+    A torch.cuda.MemPool over a CUDAPluggableAllocator whose segments the
+    pool's first-fit arena places in its device slab (dvla_torch_alloc /
+    dvla_torch_free, csrc/arena.cpp): inside `with arena:` every tensor the
+    current thread allocates on the pool's device (activations,
+    concatenations, sampling outputs) lands in the recycled pool instead of
+    torch's private cudaMalloc segments.  Torch caches and sub-allocates
+    within its segments, so the pool is not epoch-reset while bound (the
+    C-ABI refuses it); close() returns the segments and unbinds.  Several
+    lane threads may use one arena at once (one MemPool per thread, all
+    drawing from the arena)."""
+
+    def __init__(self, pool: "Pool"):
+        import torch
+
+        from . import _lib
+        if pool.kind is not PoolKind.ENV_AUX or pool._slab is None:
+            raise PoolUsageError("torch allocations go to an ENV_AUX device pool")
+        self.pool = pool
+        self.device = pool.data.device.index
+        _lib.check(_lib.dvla_torch_pool_bind(self.device, pool._arena, pool.data.data_ptr()),
+                   "dvla_torch_pool_bind")
+        self._alloc = torch.cuda.memory.CUDAPluggableAllocator(
+            str(_lib._LIB_PATH), "dvla_torch_alloc", "dvla_torch_free")
+        # one MemPool per thread (torch records one thread into a pool at a
+        # time); every one of them draws its segments from this arena
+        self._pools: dict = {}
+        self._lock = threading.Lock()
+        self._ctx = threading.local()
+
+    @property
+    def mempool(self):
+        import torch
+        tid = threading.get_ident()
+        with self._lock:
+            mp = self._pools.get(tid)
+            if mp is None:
+                mp = self._pools[tid] = torch.cuda.MemPool(self._alloc.allocator())
+        return mp
+
+    def __enter__(self):
+        import torch
+        ctx = torch.cuda.use_mem_pool(self.mempool, device=self.device)
+        ctx.__enter__()
+        stack = getattr(self._ctx, "stack", None) or []
+        stack.append(ctx)
+        self._ctx.stack = stack
+        return self
+
+    def __exit__(self, *exc):
+        return self._ctx.stack.pop().__exit__(*exc)
+
+    _shared: dict = {}
+
+    @classmethod
+    def shared(cls, device, nbytes: int) -> "TorchArena":
+        """The process's torch arena on `device` (one binding per device),
+        created with an ENV_AUX pool of `nbytes` on first use."""
+        import torch
+        idx = torch.device(device).index
+        if idx is None:
+            idx = torch.cuda.current_device()
+        a = cls._shared.get(idx)
+        if a is None:
+            a = cls(Pool(PoolKind.ENV_AUX, int(nbytes), device=torch.device("cuda", idx)))
+            cls._shared[idx] = a
+        return a
+
+    def holds(self, t) -> bool:
+        """True when tensor t's storage lies in the pool's slab."""
+        base = self.pool.data.data_ptr()
+        return base <= t.data_ptr() < base + self.pool.capacity
+
+    def close(self):
+        """Release torch's segments back to the arena and unbind (every
+        tensor allocated inside must be gone)."""
+        import gc
+
+        import torch
+
+        from . import _lib
+        torch.cuda.synchronize(self.device)
+        with self._lock:
+            self._pools.clear()
+        gc.collect()
+        torch.cuda.empty_cache()
+        _lib.check(_lib.dvla_torch_pool_bind(self.device, None, None), "dvla_torch_pool_bind")
 
 
 def arena_trace(capacity: int, is_alloc, size, align, pick):

@@ -28,6 +28,7 @@ body is out of scope; the hot path is everything after it.
 
 from __future__ import annotations
 
+import contextlib
 import logging
 import math
 import threading
@@ -346,6 +347,9 @@ class SwimlaneConfig:
     seed: int = 0
     watchdog_s: float = 60.0
     max_grad_norm: float | None = None
+    # torch's own temporaries (concatenations, sampling outputs) in an
+    # ENV_AUX pool through a MemPool (pools.TorchArena); 0 = torch's allocator
+    torch_pool_bytes: int = 256 << 20
 
     def validate(self):
         if self.group_size < 2:
@@ -428,8 +432,10 @@ class SamplerWorker:
     run_epoch produces one epoch of device-resident GroupBatch messages with
     the installed weights read in place."""
 
-    def __init__(self, cfg: SwimlaneConfig, node: int, nodes: int, env_pools, stream, device):
+    def __init__(self, cfg: SwimlaneConfig, node: int, nodes: int, env_pools, stream, device,
+                 torch_arena=None):
         import torch
+        self.torch_arena = torch_arena
         self.cfg, self.node, self.nodes = cfg, node, nodes
         self.env_pools, self.stream, self.device = env_pools, stream, device
         H = cfg.hidden
@@ -459,7 +465,7 @@ class SamplerWorker:
             n = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
             return pool.view(pool.alloc(n, align=256), dtype).view(*shape)
 
-        with torch.cuda.stream(self.stream):
+        with (self.torch_arena or contextlib.nullcontext()), torch.cuda.stream(self.stream):
             if getattr(snap, "ready", None) is not None:
                 self.stream.wait_event(snap.ready)  # the snapshot's bytes landed
             W = snap.params.view(V, H)  # installed replica, zero copy
@@ -527,7 +533,7 @@ class TrainerWorker:
     (non-finite parameters)."""
 
     def __init__(self, cfg: SwimlaneConfig, node: int, model_pool, reducer, stream, device,
-                 act_pool=None, n_groups: int | None = None):
+                 act_pool=None, n_groups: int | None = None, torch_arena=None):
         import torch
 
         from . import _lib
@@ -595,6 +601,7 @@ class TrainerWorker:
         self.version = 0
         self.done_event = None
         self.timing = None  # optional: dict of CUDA event pairs per phase
+        self.torch_arena = torch_arena
 
     def _acts(self, R, V, H):
         import torch
@@ -692,7 +699,7 @@ class TrainerWorker:
         if len(batches) != self.n_groups:
             raise ConfigError(f"update expects {self.n_groups} groups, got {len(batches)}")
         ev_t = self.timing
-        with torch.cuda.stream(s):
+        with (self.torch_arena or contextlib.nullcontext()), torch.cuda.stream(s):
             seen = set()
             for b in batches:
                 ev = getattr(b, "ready", None)
@@ -852,8 +859,12 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
     chan = Channel(cfg.queue_capacity * cfg.n_groups,
                    Transport(TransportMode.INPROC, Plane.DATA, name="data"), abort_event=abort)
     reducer = GradReducer(nodes, group)
-    trainer = TrainerWorker(cfg, rank, model_pool, reducer, s_train, dev)
-    sampler = SamplerWorker(cfg, rank, nodes, env_pools, s_sample, dev)
+    tarena = None
+    if cfg.torch_pool_bytes > 0:
+        from .pools import TorchArena
+        tarena = TorchArena.shared(dev, cfg.torch_pool_bytes)
+    trainer = TrainerWorker(cfg, rank, model_pool, reducer, s_train, dev, torch_arena=tarena)
+    sampler = SamplerWorker(cfg, rank, nodes, env_pools, s_sample, dev, torch_arena=tarena)
     # ring of published weights (bf16) in the MODEL_COMPUTE pool
     wbuf = [model_pool.view(model_pool.alloc(n * 2, align=256), torch.bfloat16)
             for _ in range(nbuf)]
@@ -984,6 +995,11 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
     result.staleness_max = board.staleness_max
     result.lane_busy = busy
     result.policy = trainer.policy   # final weights (multi-GPU: identical on every rank)
+    if tarena is not None:
+        st = tarena.pool.stats()
+        result.counters["torch_arena"] = {"capacity": tarena.pool.capacity,
+                                          "segments_allocated": st.alloc_count,
+                                          "live_bytes": st.live_bytes}
     result.counters.update({"updates": board.version, "produced": board.produced,
                             "regressions_ignored": board.regressions_ignored})
     return result

@@ -200,3 +200,32 @@ def test_sampler_and_trainer_workers_against_the_oracle(dev):
     assert trainer.version == 1 and trainer.policy.step == 1
     assert torch.equal(trainer.policy.master, p0) and torch.equal(trainer.policy.m, m0) \
         and torch.equal(trainer.policy.v, v0)
+
+
+def test_torch_arena_places_torch_allocations_in_env_aux(dev):
+    """pools.TorchArena: tensors torch allocates inside
+    `with arena:` live in the ENV_AUX pool's slab, placed by its first-fit
+    arena; the bound pool refuses epoch_reset; the swimlane's temporaries go
+    there (counters)."""
+    import torch
+    from paper_2605_13276_b200.pools import Pool, PoolKind, PoolUsageError, TorchArena
+    from paper_2605_13276_b200.runtime import SwimlaneConfig, run_swimlane
+    arena = TorchArena.shared(dev, 256 << 20)
+    before = arena.pool.stats().alloc_count
+    with arena:
+        a = torch.randn(1 << 20, device=dev)
+        b = torch.cat([a, a]) * 2
+    c = torch.randn(1 << 20, device=dev)          # outside: torch's own segments
+    assert arena.holds(a) and arena.holds(b) and not arena.holds(c)
+    assert arena.pool.stats().alloc_count > before
+    assert torch.equal(b[: 1 << 20], a * 2)
+    with pytest.raises(PoolUsageError):
+        arena.pool.epoch_reset()
+    # another pool cannot take over the device's binding
+    with pytest.raises(Exception):
+        TorchArena(Pool(PoolKind.ENV_AUX, 1 << 20, device=dev))
+    cfg = SwimlaneConfig(n_groups=2, group_size=4, tokens=8, vocab=1024, action_bins=256,
+                         hidden=64, epochs=3, seed=21)
+    res = run_swimlane(cfg, device=dev)
+    assert res.counters["updates"] == 3
+    assert res.counters["torch_arena"]["segments_allocated"] > 0
