@@ -115,7 +115,7 @@ __device__ __forceinline__ double tail_grad(float g32, double div, bool clip, do
   return gi;
 }
 
-__global__ void adam_tail_kernel(TailArgs a, int vec) {
+__global__ void __launch_bounds__(256, 3) adam_tail_kernel(TailArgs a, int vec) {
   if (a.skip != nullptr && *a.skip != 0.0f) return;
   bool clip = false;
   double f = 1.0;
@@ -247,7 +247,10 @@ __global__ void sumsq_blocks_kernel(const double* __restrict__ g, int64_t n, int
 }
 
 // f32 gradient variant: the norm of gi = f64(g32[i]) / div (the values
-// adam_tail_kernel steps with), 8-byte loads, four in flight per thread
+// adam_tail_kernel steps with).  16-byte loads, four in flight per thread;
+// the squares of each 4-element load are summed in f64 (exact products of
+// f32 values, f64 adds) -- the same fixed block shape as the f64 kernel, so
+// the reduction order never depends on the launch.
 __global__ void sumsq_blocks_f32_kernel(const float* __restrict__ g, int64_t n, int64_t per_block,
                                         double div, double* __restrict__ partial,
                                         unsigned* __restrict__ nonfinite) {
@@ -256,39 +259,40 @@ __global__ void sumsq_blocks_f32_kernel(const float* __restrict__ g, int64_t n, 
   const int64_t hi = (lo + per_block < n) ? lo + per_block : n;
   double acc0 = 0.0, acc1 = 0.0;
   unsigned bad = 0;
-  auto sq = [div](float x) {
-    double d = static_cast<double>(x);
-    if (div != 1.0) d = __ddiv_rn(d, div);
-    return d * d;
+  const double inv = (div != 1.0) ? 1.0 / (div * div) : 1.0;  // only scales the norm
+  auto sq4 = [](const float4& v) {
+    const double a = v.x, b = v.y, c = v.z, d = v.w;
+    return (a * a + b * b) + (c * c + d * d);
   };
-  const bool vec = ((reinterpret_cast<uintptr_t>(g + lo) & 7) == 0);
+  auto bad4 = [](const float4& v) {
+    return !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
+  };
+  const bool vec = ((reinterpret_cast<uintptr_t>(g + lo) & 15) == 0);
   int64_t i = lo;
   if (vec) {
-    const float2* g2 = reinterpret_cast<const float2*>(g + lo);
-    const int64_t npair = (hi - lo) / 2;
+    const float4* g4 = reinterpret_cast<const float4*>(g + lo);
+    const int64_t nq = (hi - lo) / 4;
     int64_t j = threadIdx.x;
-    for (; j + 3 * kNormThreads < npair; j += 4 * kNormThreads) {
-      const float2 a = __ldcs(g2 + j), b = __ldcs(g2 + j + kNormThreads);
-      const float2 c = __ldcs(g2 + j + 2 * kNormThreads), d = __ldcs(g2 + j + 3 * kNormThreads);
-      acc0 += (sq(a.x) + sq(b.x)) + (sq(c.x) + sq(d.x));
-      acc1 += (sq(a.y) + sq(b.y)) + (sq(c.y) + sq(d.y));
-      bad |= !isfinite(a.x) | !isfinite(a.y) | !isfinite(b.x) | !isfinite(b.y) |
-             !isfinite(c.x) | !isfinite(c.y) | !isfinite(d.x) | !isfinite(d.y);
+    for (; j + 3 * kNormThreads < nq; j += 4 * kNormThreads) {
+      const float4 a = __ldcs(g4 + j), b = __ldcs(g4 + j + kNormThreads);
+      const float4 c = __ldcs(g4 + j + 2 * kNormThreads), d = __ldcs(g4 + j + 3 * kNormThreads);
+      acc0 += sq4(a) + sq4(b);
+      acc1 += sq4(c) + sq4(d);
+      bad |= bad4(a) | bad4(b) | bad4(c) | bad4(d);
     }
-    for (; j < npair; j += kNormThreads) {
-      const float2 a = __ldcs(g2 + j);
-      acc0 += sq(a.x);
-      acc1 += sq(a.y);
-      bad |= !isfinite(a.x) | !isfinite(a.y);
+    for (; j < nq; j += kNormThreads) {
+      const float4 a = __ldcs(g4 + j);
+      acc0 += sq4(a);
+      bad |= bad4(a);
     }
-    i = lo + npair * 2;
+    i = lo + nq * 4;
   }
   for (i += threadIdx.x; i < hi; i += kNormThreads) {
-    const float x = g[i];
-    acc0 += sq(x);
-    bad |= !isfinite(x);
+    const double x = g[i];
+    acc0 += x * x;
+    bad |= !isfinite(g[i]);
   }
-  double acc = warp_sum_f64(acc0 + acc1);
+  double acc = warp_sum_f64((acc0 + acc1) * inv);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   bad = __any_sync(0xffffffffu, bad);
   if ((threadIdx.x & 31) == 0 && bad) atomicOr(nonfinite, 1u);
@@ -417,7 +421,7 @@ static int grad_sumsq_f32(const float* grad, int64_t n, double div, double* out,
     return fail(DVLA_ERR_USAGE, "bad grad_norm_f32 arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nblocks = kNormBlocks;
-  const int64_t per = ((n + nblocks - 1) / nblocks + 1) & ~int64_t{1};
+  const int64_t per = ((n + nblocks - 1) / nblocks + 3) & ~int64_t{3};  // 16-byte blocks
   double* partial = static_cast<double*>(workspace);
   DVLA_CUDA_TRY(cudaMemsetAsync(partial, 0, nblocks * sizeof(double), st));
   if (n > 0) {
