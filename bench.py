@@ -50,6 +50,7 @@ def _args():
     ap.add_argument("--no-repl", action="store_true")
     ap.add_argument("--no-swimlane", action="store_true")
     ap.add_argument("--no-gauss", action="store_true")
+    ap.add_argument("--no-f32", action="store_true", help="skip the C2 f32 leg")
     ap.add_argument("--fixed-warmup", action="store_true",
                     help="exactly --warmup warm-up steps (for ncu launch lists)")
     return ap.parse_args()
@@ -1105,7 +1106,8 @@ def run_ours(a):
         del h_logits, d_logits
 
     del dl
-    c2_f32 = _guarded(_bench_c2_f32, dev, rank, world, barrier, max_over_ranks)
+    c2_f32 = None if a.no_f32 else _guarded(_bench_c2_f32, dev, rank, world, barrier,
+                                            max_over_ranks)
     repl = None if a.no_repl else _bench_replication(world, rank, dev, barrier, max_over_ranks)
     allreduce = _bench_allreduce(world, dev, barrier, max_over_ranks)
     learner = None if a.no_swimlane else _guarded(_bench_learner_step, world, rank, dev, barrier,
