@@ -327,25 +327,29 @@ def b200_costs(n_groups: int = 64, group_size: int = 8, chunks: int = 1, tokens:
     """Lane costs of the token-head swimlane (runtime.run_swimlane) on B200.
 
     Sampler: logits GEMM [R, H] x [H, V] + one-pass sampling over the logits.
-    Trainer: logits GEMM + fused loss fwd/bwd (2 R V bf16 bytes) + the
-    weight-gradient GEMM + Adam on V*H parameters (48 B each) + the
-    per-parameter passes around it (f32 -> f64 gradient 12 B, non-finite
-    scan 4 B, bf16 weight cast 6 B) + the snapshot copy of the bf16 weights
-    + the [R, H] feature expansion.  Weight replication to ``replicas`` other GPUs
-    over the chain, gradient mean over ``nodes`` GPUs with NCCL."""
+    Trainer (TrainerWorker.update, round 2): logits GEMM + fused loss
+    fwd/bwd (2 R V bf16 bytes) + the head-gradient GEMM (f32 output, 4 n
+    bytes written) + the [R, H] feature expansion + grad norm (4 n / N read)
+    + the optimizer tail on this learner's 1/N of the parameters (46 B each:
+    f32 gradient, f64 moments, f32 master, bf16 copy) + the snapshot copy of
+    the bf16 weights.  With ``nodes`` = N > 1 learners the gradient is
+    reduce-scattered (f32) and the bf16 blocks all-gathered by NCCL
+    (ZeRO-1): (N - 1) / N (4 + 2) n bytes per GPU and direction at the
+    measured bus bandwidth.  Weight replication to ``replicas`` other GPUs
+    over the chain."""
     R = n_groups * group_size * chunks * tokens
     n = vocab * hidden
+    N = max(int(nodes), 1)
     gemm = 2.0 * R * hidden * vocab / (rates.gemm_tflops * 1e12)
     hbm = rates.hbm_gbs * 1e9
     roll = gemm + R * vocab * 2 / (hbm * rates.sample_frac) + rates.launch_overhead_s
     loss = 2 * R * vocab * 2 / (hbm * rates.loss_frac)
-    adam = 48.0 * n / (hbm * rates.adam_frac)
+    tail = 46.0 * n / N / (hbm * rates.adam_frac)
     snap = 2 * n * 2 / hbm
-    passes = (22.0 * n + 2 * R * hidden * 2) / hbm
-    act = 2 * gemm + loss + adam + snap + passes + rates.launch_overhead_s
+    passes = (4.0 * n + 4.0 * n / N + 2 * R * hidden * 2) / hbm
+    act = 2 * gemm + loss + tail + snap + passes + rates.launch_overhead_s
     bcast = (n * 2 / (rates.nvlink_gbs * 1e9)) if replicas else 0.0
-    reduce = (2.0 * (nodes - 1) / nodes * n * 8 / (rates.allreduce_busbw_gbs * 1e9)
-              if nodes > 1 else 0.0)
+    reduce = ((N - 1) / N * n * (4 + 2) / (rates.allreduce_busbw_gbs * 1e9) if N > 1 else 0.0)
     return LaneCosts(rollout_s=roll, actor_s=act, broadcast_s=bcast, reduce_s=reduce,
                      shared_slots=shared_gpu, transitions_per_epoch=R)
 
