@@ -824,8 +824,10 @@ def _bench_disaggregated(world, rank, dev, epochs=8, keep_timeline=False, engine
     body = max(0, C3_WEIGHT_BYTES - V * SWIM_H * 2)
     res = run_disaggregated(cfg, verify=True, body_bytes=body, timeout_s=300.0, engine=engine)
     tl = None
+    import torch.distributed as dist
+    mism = [None] * world
+    dist.all_gather_object(mism, res.mismatched)
     if keep_timeline:
-        import torch.distributed as dist
         tl = [None] * world
         dist.all_gather_object(tl, res.timeline)
     if rank != 0:
@@ -848,6 +850,7 @@ def _bench_disaggregated(world, rank, dev, epochs=8, keep_timeline=False, engine
             "nvlink_peak_gbs": peak,
             "replication_overlapped_with_updates": sm["overlap"],
             "checksum_mismatches": sm["checksum_mismatches"],
+            "mismatched_versions": {r: [m[0] for m in x] for r, x in enumerate(mism) if x},
             **({"timeline": tl} if tl else {}),
             "timing": "learner 0: host clock between first and last publish (traj/s); "
                       "replication: CUDA events around each rollout rank's hop launch on its "

@@ -87,6 +87,7 @@ class DisaggResult:
     recv_ms: list = field(default_factory=list)  # rollout: per-version hop time (CUDA events)
     recv_ms_median_max: float | None = None      # max over rollout ranks of their medians
     timeline: list = field(default_factory=list)  # (event, epoch/version, host monotonic s)
+    mismatched: list = field(default_factory=list)  # rollout: (version, got, want) checksums
 
     def summary(self) -> dict:
         reps = [r["ms"] for r in self.replication]
@@ -291,6 +292,9 @@ def _learner(cfg, rank, L, Rr, assign, k, lgroup, model_pool, chans, rep, store,
         for p in pub:
             p[hb:].copy_(body)
         del body
+    # the initialisation above ran on this thread's default stream, which the
+    # (non-blocking) trainer / weight-dist streams do not order against
+    torch.cuda.synchronize(dev)
     # pub_done[i]: event after which the chain heads (and the checksum) no
     # longer read pub[i]; `pushed` = the newest version whose push has been
     # enqueued (the trainer reuses pub[v % 2] only after v - 2 was enqueued)
@@ -480,8 +484,11 @@ def _rollout(cfg, rank, Rr, assign, chans, rep, store, key, ring, S, verify, poi
                 if verify:
                     with torch.cuda.stream(s_recv):
                         csum = _checksum_async(region)
-                    if _fmt(csum, s_recv) != store.get(key("sum", v), "checksum").decode():
+                    got = _fmt(csum, s_recv)
+                    want = store.get(key("sum", v), "checksum").decode()
+                    if got != want:
                         res.checksum_mismatches += 1
+                        res.mismatched.append((v, got, want))
                 ev = torch.cuda.Event()
                 ev.record(s_recv)
                 snap = ParamSnapshot(version=v, params=region[:V * H * 2].view(torch.bfloat16),

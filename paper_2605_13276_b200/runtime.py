@@ -444,6 +444,7 @@ class SamplerWorker:
                                     cfg.seed + 1)) * 0.05
         self.pos = token_positions(cfg, device)
         self.rng = torch.Generator(device=device).manual_seed(cfg.seed * 7919 + node)
+        torch.cuda.synchronize(device)   # tables built on the default stream
 
     def run_epoch(self, epoch: int, snap: ParamSnapshot, poison: bool = False,
                   group_base: int | None = None):
@@ -602,6 +603,9 @@ class TrainerWorker:
         self.done_event = None
         self.timing = None  # optional: dict of CUDA event pairs per phase
         self.torch_arena = torch_arena
+        # the initial weights / moments were written on the default stream,
+        # which the worker's non-blocking streams do not order against
+        torch.cuda.synchronize(device)
 
     def _acts(self, R, V, H):
         import torch

@@ -39,14 +39,15 @@ def main():
         return t.item() == 0.0
 
     chains = [[0, 2, 3], [1, 3, 2]]
-    for ctas in (64, 74):
-        rep = SplitReplicator(S, chains, n_buffers=1, ctas_per_hop=ctas)
+    engines = os.environ.get("ENGINES", "sm,ce_head,ce").split(",")
+    for engine in engines:
+        rep = SplitReplicator(S, chains, n_buffers=1, ctas_per_hop=64, engine=engine)
         ms = timed(lambda it: rep.broadcast(src if rank in (0, 1) else None, it))
         rep.check()
         ok = ok_all(rank < 2 or bytes_equal(src, rep.replica(0))[0] == 0)
         rep.close()
         if rank == 0:
-            print(f"split 2 learners -> 2 replicas, {ctas} CTAs/hop: {ms:.3f} ms, "
+            print(f"split 2 learners -> 2 replicas, engine {engine}: {ms:.3f} ms, "
                   f"{S / ms / 1e6:.1f} GB/s per replica, bit_exact={ok}", flush=True)
         del rep
     # one learner, chain 0 -> 2 -> 3 (replicas only), the 1-source baseline
