@@ -904,7 +904,7 @@ def _swim_model(swim, world, roofline, sampler, optimizer):
     except Exception:  # noqa: BLE001 - the dataclass default stands
         pass
     rates = sim.B200Rates(hbm_gbs=_peaks()[0], **kw)
-    costs = sim.b200_costs(N_GROUPS, G, C, T, V, 4096, nodes=world, rates=rates)
+    costs = sim.b200_costs(N_GROUPS, G, C, T, V, SWIM_H, nodes=world, rates=rates)
     R = N_GROUPS * G * C * T
     per_traj = N_GROUPS * G / R
     ep = swim["epochs"]
@@ -941,10 +941,13 @@ def _swim_model(swim, world, roofline, sampler, optimizer):
                         shared_slots=True, transitions_per_epoch=R)
     out["calibrated"] = {"rollout_s": cal.rollout_s, "actor_s": cal.actor_s,
                          "async": fit(sim.simulate(cal, "async", **akw), "async")}
-    # the calibrated lanes at 8 GPUs: this run's all-reduce swapped for 8 GPUs'
-    c8 = sim.b200_costs(N_GROUPS, G, C, T, V, 4096, nodes=8, rates=rates)
-    cal8 = sim.LaneCosts(rollout_s=cal.rollout_s,
-                         actor_s=max(cal.actor_s - costs.reduce_s, 1e-6) + c8.reduce_s,
+    # the calibrated lanes at 8 GPUs: the analytic difference of the learner
+    # lane between this run's N and 8 (ZeRO-1: the reduce-scatter /
+    # all-gather grows to 7/8 of the bytes, the optimizer tail shrinks to
+    # 1/8 of the parameters) applied to the live trainer lane
+    c8 = sim.b200_costs(N_GROUPS, G, C, T, V, SWIM_H, nodes=8, rates=rates)
+    d8 = (c8.actor_s + c8.reduce_s) - (costs.actor_s + costs.reduce_s)
+    cal8 = sim.LaneCosts(rollout_s=cal.rollout_s, actor_s=max(cal.actor_s + d8, 1e-6),
                          shared_slots=True, transitions_per_epoch=R)
     r8 = sim.simulate(cal8, "async", **akw)
     out["predicted_8gpu_trajectories_per_s_total"] = r8.throughput * per_traj * 8
