@@ -268,3 +268,48 @@ def test_gauss_loss_one_call_abort_on_nonfinite_reward(dev):
         grpo.grpo_gauss_head_grad(t(means), t(np.zeros(D, np.float32)), t(means),
                                   t(np.zeros((n_groups, G, C), np.float32)), t(rewards),
                                   [9, 4, 6], grpo.GrpoConfig(group_size=G))
+
+
+def test_grpo_loss_matches_golden_and_finite_differences(dev):
+    """grpo.grpo_loss (reference grpo.py:181-214) on the reference's golden
+    cases: equals the reference loss (its inter-backend tolerance), and
+    central finite differences of it (reference tests/helpers.py:58-79:
+    f32-realised steps, h = 1e-3) match grpo_grad's gradient.  The reference
+    pins its gradient against an f64-means loss at 1e-4; this loss rounds
+    the means to f32 exactly as grpo_grad does, so the secants carry f32
+    rounding: 1e-3 norm-wise."""
+    from paper_2605_13276_b200 import grpo
+    from paper_2605_13276_b200.policy import PolicyParams
+    g = golden("grpo_gauss")
+    for tag in ("s0_kl0", "s5_kl0", "s3_kl5"):
+        if f"{tag}_loss" not in g.files:
+            continue
+        params, batches = _case(g, tag)
+        cfg = grpo.GrpoConfig(group_size=4, clip_eps=0.2, adv_epsilon=1e-8, micro_batch=4,
+                              kl_coeff=float(g[f"{tag}_kl"]))
+        loss = grpo.grpo_loss(params, batches, cfg)
+        assert loss == pytest.approx(float(g[f"{tag}_loss"]), abs=1e-6)
+        _, grad, _ = grpo.grpo_grad(params, batches, cfg)
+        names = ("w1", "b1", "w2", "b2", "log_std")
+        flat = np.concatenate([getattr(params, k).ravel().astype(np.float64) for k in names])
+        shapes = [getattr(params, k).shape for k in names]
+
+        def unflat(v):
+            out, i = {}, 0
+            for k, shp in zip(names, shapes):
+                n = int(np.prod(shp))
+                out[k] = v[i:i + n].reshape(shp).astype(np.float32)
+                i += n
+            return PolicyParams(**out)
+
+        fd = np.zeros(flat.size)
+        h = 1e-3
+        for idx in range(flat.size):
+            up, dn = flat.copy(), flat.copy()
+            up[idx] += h
+            dn[idx] -= h
+            pu, pd = unflat(up), unflat(dn)
+            delta = float(np.float32(up[idx])) - float(np.float32(dn[idx]))
+            fd[idx] = (grpo.grpo_loss(pu, batches, cfg) - grpo.grpo_loss(pd, batches, cfg)) / delta
+        err = np.linalg.norm(fd - grad) / np.linalg.norm(grad)
+        assert err < 1e-3, (tag, err)
