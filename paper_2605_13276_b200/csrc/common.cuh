@@ -304,6 +304,12 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+// acc += x on both lanes, in place (keeps a loop-carried accumulator pair in
+// its registers: with a separate destination ptxas moved the sum back into
+// the accumulator every iteration)
+__device__ __forceinline__ void fadd2_acc(uint64_t& acc, uint64_t x) {
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(x));
+}
 // bf16x2 word -> (x_lo, x_hi) * s + t on both lanes, f32
 __device__ __forceinline__ uint64_t bf16x2_fma2(uint32_t w, uint64_t s2, uint64_t t2) {
   return ffma2(f2pack(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u)), s2, t2);

@@ -279,6 +279,9 @@ __device__ __forceinline__ void op_of(int n, int nloc, int L, bool* isB, int* k)
 #ifndef DVLA_POLY_WORDS
 #define DVLA_POLY_WORDS 0
 #endif
+#ifndef DVLA_ACC_INPLACE
+#define DVLA_ACC_INPLACE 1
+#endif
 constexpr int kPolyWords = DVLA_POLY_WORDS;  // bf16 phase-B words per granule on the FMA pipe
 
 // 2^y on both lanes of a packed f32 pair without MUFU: y = j + f with j =
@@ -321,6 +324,7 @@ struct FusedElem<__nv_bfloat16> {
     return bf16x2_max(m, bf16x2_max(bf16x2_max(x.x, x.y), bf16x2_max(x.z, x.w)));
   }
   __device__ static float maxf(uint32_t m) { return fmaxf(bf16lo(m), bf16hi(m)); }
+  __device__ static uint32_t max2(uint32_t a, uint32_t b) { return bf16x2_max(a, b); }
   // acc += 2^(x log2e + off) over the granule (packed f32 pairs)
   __device__ static void exps(const uint4& x, uint64_t l2e2, uint64_t off2, uint64_t (&acc)[4]) {
     const uint32_t w[4] = {x.x, x.y, x.z, x.w};
@@ -328,7 +332,11 @@ struct FusedElem<__nv_bfloat16> {
     for (int j = 0; j < 4; ++j) {
       float y0, y1;
       f2unpack(bf16x2_fma2(w[j], l2e2, off2), y0, y1);
+#if DVLA_ACC_INPLACE
+      fadd2_acc(acc[j], f2pack(ex2f(y0), ex2f(y1)));
+#else
       acc[j] = fadd2(acc[j], f2pack(ex2f(y0), ex2f(y1)));
+#endif
     }
   }
   // -sign(c) 2^(x log2e - K) for the granule, in place.  kPolyWords of the
@@ -368,6 +376,9 @@ struct FusedElem<float> {
                                        fmaxf(__uint_as_float(x.z), __uint_as_float(x.w)))));
   }
   __device__ static float maxf(uint32_t m) { return __uint_as_float(m); }
+  __device__ static uint32_t max2(uint32_t a, uint32_t b) {
+    return __float_as_uint(fmaxf(__uint_as_float(a), __uint_as_float(b)));
+  }
   __device__ static void exps(const uint4& x, uint64_t l2e2, uint64_t off2, uint64_t (&acc)[4]) {
     float y0, y1, y2, y3;
     f2unpack(ffma2(f2pack(__uint_as_float(x.x), __uint_as_float(x.y)), l2e2, off2), y0, y1);
@@ -682,12 +693,38 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
       const uint4* v = reinterpret_cast<const uint4*>(buf(s));
       uint32_t mx = FE::kNegInf;
       uint64_t acc[4] = {0, 0, 0, 0};  // packed (0.f, 0.f)
+#if DVLA_ACC_INPLACE
+      // two granules per iteration into two accumulator sets: each
+      // accumulator is updated in place once per iteration (one set made
+      // ptxas copy the pair sums back every iteration)
+      {
+        uint64_t acc2[4] = {0, 0, 0, 0};
+        uint32_t mx2 = FE::kNegInf;
+        int i = tid;
+        for (; i + kFusedComputeThreads < nvec; i += 2 * kFusedComputeThreads) {
+          const uint4 x = v[i], y = v[i + kFusedComputeThreads];
+          mx = FE::max16(mx, x);
+          mx2 = FE::max16(mx2, y);
+          FE::exps(x, l2e2, 0, acc);
+          FE::exps(y, l2e2, 0, acc2);
+        }
+        if (i < nvec) {
+          const uint4 x = v[i];
+          mx = FE::max16(mx, x);
+          FE::exps(x, l2e2, 0, acc);
+        }
+        mx = FE::max2(mx, mx2);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) fadd2_acc(acc[j], acc2[j]);
+      }
+#else
 #pragma unroll 2
       for (int i = tid; i < nvec; i += kFusedComputeThreads) {
         const uint4 x = v[i];
         mx = FE::max16(mx, x);
         FE::exps(x, l2e2, 0, acc);
       }
+#endif
       const float wmax = warp_max_f32(FE::maxf(mx));
       float m = 0.f;  // frame of this warp's partial
       if (!(wmax <= kFrameHi) || (wmax < kFrameLo && wmax > -INFINITY)) {  // warp-uniform

@@ -6,6 +6,6 @@ for rep in 1 2; do
     if [ "$v" = default ]; then L=""; else L=$v; fi
     printf '%s ' "$(basename "$v")"
     DVLA_B200_LIB=$L python bench.py --steps 200 --warmup 20 --no-e2e --no-cpu --no-repl \
-      --no-swimlane --no-gauss 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); c=d['clocks']; print(round(d['ms_per_step'],4), d['roofline']['kernel_ms'], c['sm_mhz'], c['reasons'], c.get('power_w'))"
+      --no-swimlane --no-gauss --no-f32 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); c=d['clocks']; print(round(d['ms_per_step'],4), d['roofline']['kernel_ms'], c['sm_mhz'], c['reasons'], c.get('power_w'))"
   done
 done
