@@ -274,7 +274,11 @@ __device__ __forceinline__ void op_of(int n, int nloc, int L, bool* isB, int* k)
 #define DVLA_FULL_SPIN 0
 #endif
 #ifndef DVLA_CFULL_WAIT
-#define DVLA_CFULL_WAIT 0
+// compute warps wait for a phase-B coefficient with the hardware try_wait
+// (suspend until the barrier flips) rather than a nanosleep back-off loop:
+// the back-off loop issued ~22 % of the kernel's instructions; sustained
+// power-capped step 0.3-0.6 % faster (round 2, tools/sustained_variants.sh)
+#define DVLA_CFULL_WAIT 1
 #endif
 #ifndef DVLA_POLY_WORDS
 #define DVLA_POLY_WORDS 0
