@@ -387,6 +387,12 @@ def _learner(cfg, rank, L, Rr, assign, k, lgroup, model_pool, chans, rep, store,
                 continue
             intervals["update"].append((t0.elapsed_time(ev_u["start"]),
                                         t0.elapsed_time(ev_u["end"])))
+            names = ("start", "loss0", "loss1", "grad1", "reduce1", "end")
+            res.lane_s.setdefault("update_phases_ms", []).append(
+                {**{n1: round(ev_u[n0].elapsed_time(ev_u[n1]), 3)
+                    for n0, n1 in zip(names, names[1:])},
+                 "host_enqueue_ms": round(1e3 * ev_u["host_enqueue_s"], 3),
+                 "host_wait_ms": round(1e3 * ev_u["host_wait_s"], 3)})
             v = trainer.version
             res.update_stats.append({"version": v, **{kk: st[kk] for kk in (
                 "loss", "mean_ratio", "clip_fraction", "n_chunks", "grad_norm")}})

@@ -284,16 +284,35 @@ class TokenLoss:
         self.lp_tok = ws64[offs[1] // 8: offs[1] // 8 + self.rows]
         self.coeff = ws64[offs[3] // 8: offs[3] // 8 + nq]
         self.set_groups(np.arange(n_groups, dtype=np.int64))
+        self._ids_ev.synchronize()   # usable from any stream from here on
 
-    def set_groups(self, group_ids):
+    def set_groups(self, group_ids, stream=None):
+        """Host group ids -> canonical order; the two small device vectors
+        are refreshed by an asynchronous copy from a pinned staging buffer on
+        `stream` (default: current) -- a pageable copy would block the host
+        until the stream drained (no-op when the ids are unchanged)."""
         torch = _torch()
         ids = np.asarray(group_ids, dtype=np.int64)
         if ids.shape != (self.n_groups,):
             raise UsageError(f"expected {self.n_groups} group ids, got shape {ids.shape}")
+        if getattr(self, "group_ids", None) is not None and np.array_equal(ids, self.group_ids):
+            return
         self.group_ids = ids
         self.order = canonical_order(ids)
-        self.order_dev = torch.from_numpy(self.order).to(self.device)
-        self.ids_dev = torch.from_numpy(ids).to(self.device)
+        if getattr(self, "_ids_host", None) is None:
+            self._ids_host = torch.empty(2, self.n_groups, dtype=torch.int64, pin_memory=True)
+            self._ids_dev = torch.empty(2, self.n_groups, dtype=torch.int64, device=self.device)
+            self.order_dev, self.ids_dev = self._ids_dev[0], self._ids_dev[1]
+            self._ids_ev = None
+        if self._ids_ev is not None:
+            self._ids_ev.synchronize()        # the previous copy has read the staging buffer
+        self._ids_host[0].copy_(torch.from_numpy(self.order))
+        self._ids_host[1].copy_(torch.from_numpy(ids))
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(st):
+            self._ids_dev.copy_(self._ids_host, non_blocking=True)
+            self._ids_ev = torch.cuda.Event()
+            self._ids_ev.record(st)
 
     def _check_tensor(self, t, shape, dtype, name):
         torch = _torch()

@@ -742,7 +742,11 @@ class TrainerWorker:
             self.h_skip.copy_(self.skip, non_blocking=True)
         done = torch.cuda.Event()
         done.record(s)
+        t_enq = time.perf_counter()
         done.synchronize()   # the update's one host synchronisation
+        if ev_t is not None:
+            ev_t["host_enqueue_s"] = t_enq - t0
+            ev_t["host_wait_s"] = time.perf_counter() - t_enq
         sv = self.h_stats.numpy().copy()
         skipped = float(self.h_skip[0]) != 0.0
         grad_bad = bool(self.h_flags[0])

@@ -51,10 +51,10 @@ def main():
         out["swimlane"] = bench._bench_swimlane(world, rank, dev, mx, epochs=a.epochs)
     if a.disagg and world > 1:
         barrier()
-        for eng in ("ce_head", "sm"):
+        for eng, lim in (("ce_head", 1),):
             barrier()
-            out[f"disaggregated_{eng}"] = bench._bench_disaggregated(
-                world, rank, dev, keep_timeline=True, engine=eng)
+            out[f"disaggregated_{eng}_limit{lim}"] = bench._bench_disaggregated(
+                world, rank, dev, keep_timeline=True, engine=eng, staleness_limit=lim)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
