@@ -249,3 +249,38 @@ def test_one_rank_abort_skips_the_update_on_every_rank_gloo():
     res = _run_update_workers(poison_rank=1)
     (_, sk0, _, p0), (_, sk1, _, p1) = res
     assert sk0 and sk1 and p0 == p1
+
+
+def test_disagg_key_board_polls_without_blocking_other_lanes():
+    """disagg._Keys: waits poll the store with the non-blocking check(), so
+    a lane waiting on a key never holds the store client against another
+    lane's set (the deadlock a blocking get caused); timeouts and a peer
+    lane's error surface instead of hanging."""
+    import threading
+    import time as _t
+
+    import torch.distributed as dist
+    from paper_2605_13276_b200.disagg import _Keys
+    store = dist.HashStore()
+    errors = []
+    kb = _Keys(store, "ns/", 2.0, errors)
+    got = {}
+
+    def waiter():
+        got["v"] = kb.get(kb.key("pub", 3), "v3")
+
+    th = threading.Thread(target=waiter)
+    th.start()
+    _t.sleep(0.05)
+    kb.set(kb.key("rel", 2, 0), "1")          # another lane's set goes through
+    kb.set(kb.key("pub", 3), "end")
+    th.join(2.0)
+    assert got["v"] == b"end"
+    kb.wait([kb.key("rel", 2, 0)])
+    t0 = _t.perf_counter()
+    with pytest.raises(TimeoutError):
+        _Keys(store, "ns/", 0.2, errors).wait([kb.key("never")], "never")
+    assert _t.perf_counter() - t0 < 1.0
+    errors.append(RuntimeError("peer lane failed"))
+    with pytest.raises(RuntimeError, match="peer lane failed"):
+        kb.wait([kb.key("never")])
