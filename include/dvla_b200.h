@@ -337,6 +337,11 @@ int dvla_snapshot_copy(const void* src, void* dst, int64_t nbytes, int dtype,
  * out_dev[1] = sum of word_i * (2 i + 1), both mod 2^64 (a trailing partial
  * word zero-padded).  8-byte aligned; one read; asynchronous on `stream`. */
 int dvla_checksum64(const void* p, int64_t nbytes, uint64_t* out_dev, void* stream);
+/* The same terms for a sub-range that starts at 8-byte word `first_word` of
+ * a larger region (index weights 2 (first_word + i) + 1): the checksums of
+ * consecutive sub-ranges add up (mod 2^64) to the whole region's. */
+int dvla_checksum64_at(const void* p, int64_t nbytes, int64_t first_word, uint64_t* out_dev,
+                       void* stream);
 int dvla_bytes_equal(const void* a, const void* b, int64_t nbytes, uint64_t* out_dev,
                      void* stream);
 

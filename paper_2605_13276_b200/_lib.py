@@ -156,6 +156,7 @@ dvla_replicate_chain = _proto("dvla_replicate_chain", [
 dvla_snapshot_copy = _proto("dvla_snapshot_copy", [_vp, _vp, _i64, _i32, _vp, _vp])
 dvla_bytes_equal = _proto("dvla_bytes_equal", [_vp, _vp, _i64, _vp, _vp])
 dvla_checksum64 = _proto("dvla_checksum64", [_vp, _i64, _vp, _vp])
+dvla_checksum64_at = _proto("dvla_checksum64_at", [_vp, _i64, _i64, _vp, _vp])
 dvla_torch_pool_bind = _proto("dvla_torch_pool_bind", [_i32, _vp, _vp])
 dvla_memcpy_async = _proto("dvla_memcpy_async", [_vp, _vp, _i64, _vp])
 dvla_nccl_init = _proto("dvla_nccl_init", [_i32, C.POINTER(_i32)])

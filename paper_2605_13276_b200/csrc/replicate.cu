@@ -214,7 +214,7 @@ __global__ void bytes_equal_kernel(const uint4* __restrict__ a, const uint4* __r
 // words w_i, out[0] += w_i and out[1] += w_i * (2 i + 1) mod 2^64 (the
 // index weight catches swapped or shifted chunks); a byte tail is folded in
 // as one zero-padded word.  One read of the region.
-__global__ void checksum64_kernel(const uint2* __restrict__ w, int64_t nwords,
+__global__ void checksum64_kernel(const uint2* __restrict__ w, int64_t nwords, int64_t first,
                                   unsigned long long* out) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   unsigned long long s0 = 0, s1 = 0;
@@ -223,7 +223,7 @@ __global__ void checksum64_kernel(const uint2* __restrict__ w, int64_t nwords,
     const uint2 x = __ldcs(w + i);
     const unsigned long long v = (static_cast<unsigned long long>(x.y) << 32) | x.x;
     s0 += v;
-    s1 += v * static_cast<unsigned long long>(2 * i + 1);
+    s1 += v * static_cast<unsigned long long>(2 * (first + i) + 1);
   }
   for (int o = 16; o > 0; o >>= 1) {
     s0 += __shfl_xor_sync(0xffffffffu, s0, o);
@@ -235,11 +235,11 @@ __global__ void checksum64_kernel(const uint2* __restrict__ w, int64_t nwords,
   }
 }
 
-__global__ void checksum64_tail_kernel(const uint8_t* p, int64_t from, int64_t n,
+__global__ void checksum64_tail_kernel(const uint8_t* p, int64_t from, int64_t n, int64_t first,
                                        unsigned long long* out) {
   unsigned long long v = 0;
   for (int64_t i = from; i < n; ++i) v |= static_cast<unsigned long long>(p[i]) << (8 * (i - from));
-  const unsigned long long idx = static_cast<unsigned long long>(from / 8);
+  const unsigned long long idx = static_cast<unsigned long long>(first + from / 8);
   atomicAdd(out, v);
   atomicAdd(out + 1, v * (2 * idx + 1));
 }
@@ -430,8 +430,9 @@ extern "C" int dvla_bytes_equal(const void* a, const void* b, int64_t nbytes, ui
   return launch_check("bytes_equal_kernel");
 }
 
-extern "C" int dvla_checksum64(const void* p, int64_t nbytes, uint64_t* out_dev, void* stream) {
-  if (nbytes < 0) return fail(DVLA_ERR_USAGE, "nbytes must be >= 0");
+extern "C" int dvla_checksum64_at(const void* p, int64_t nbytes, int64_t first_word,
+                                  uint64_t* out_dev, void* stream) {
+  if (nbytes < 0 || first_word < 0) return fail(DVLA_ERR_USAGE, "nbytes, first_word must be >= 0");
   if (!out_dev || (!p && nbytes > 0)) return fail(DVLA_ERR_USAGE, "null pointer argument");
   if (reinterpret_cast<uintptr_t>(p) % 8) return fail(DVLA_ERR_USAGE, "region must be 8-byte aligned");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -440,11 +441,15 @@ extern "C" int dvla_checksum64(const void* p, int64_t nbytes, uint64_t* out_dev,
   const int64_t nwords = nbytes / 8;
   if (nwords > 0)
     checksum64_kernel<<<grid_for(nwords, 256), 256, 0, st>>>(static_cast<const uint2*>(p), nwords,
-                                                              out);
+                                                              first_word, out);
   if (nwords * 8 < nbytes)
     checksum64_tail_kernel<<<1, 1, 0, st>>>(static_cast<const uint8_t*>(p), nwords * 8, nbytes,
-                                            out);
+                                            first_word, out);
   return launch_check("checksum64_kernel");
+}
+
+extern "C" int dvla_checksum64(const void* p, int64_t nbytes, uint64_t* out_dev, void* stream) {
+  return dvla_checksum64_at(p, nbytes, 0, out_dev, stream);
 }
 
 extern "C" int dvla_memcpy_async(void* dst, const void* src, int64_t nbytes, void* stream) {

@@ -142,9 +142,15 @@ class _Keys:
 
 
 def _fmt(c, stream) -> str:
-    """The checksum as text; the D2H copy is ordered on `stream` (the one
-    that computed it) and waits for it."""
+    """The checksum as text, once `stream` (the one that computed it) got
+    there.  The wait is an event synchronisation, which releases the GIL: a
+    blocking .cpu() holds it for the whole wait and stalls the other lanes'
+    Python (measured: the trainer lane's enqueue stretched by the ~10 ms the
+    push took)."""
     import torch
+    ev = torch.cuda.Event()
+    ev.record(stream)
+    ev.synchronize()
     with torch.cuda.stream(stream):
         return ",".join(str(int(x)) for x in c.cpu().tolist())
 
@@ -292,6 +298,12 @@ def _learner(cfg, rank, L, Rr, assign, k, lgroup, model_pool, chans, rep, store,
         for p in pub:
             p[hb:].copy_(body)
         del body
+    # the body blob never changes: its share of every version's checksum is
+    # taken once (sub-range checksums add up), so each version only re-reads
+    # the head it rewrote
+    from .replicate import checksum64_async
+    body_sum = (checksum64_async(pub[0][hb:], first_word=hb // 8) if S > hb
+                else torch.zeros(2, dtype=torch.int64, device=dev))
     # the initialisation above ran on this thread's default stream, which the
     # (non-blocking) trainer / weight-dist streams do not order against
     torch.cuda.synchronize(dev)
@@ -322,7 +334,7 @@ def _learner(cfg, rank, L, Rr, assign, k, lgroup, model_pool, chans, rep, store,
         csum = None
         if verify and lead:
             with torch.cuda.stream(s_dist):
-                csum = _checksum_async(pub[b])
+                csum = _checksum_async(pub[b][:hb]) + body_sum   # wraps mod 2^64
         done = torch.cuda.Event()
         done.record(s_dist)
         with cv:

@@ -86,14 +86,17 @@ def device_snapshot(params, version: int, out=None, stream=None,
                          else dst, ready=ready)
 
 
-def checksum64_async(t, stream=None):
-    """Device u64[2] checksum of a tensor's bytes (dvla_checksum64), on
-    `stream`; compare two GPUs' copies of a region without moving either."""
+def checksum64_async(t, stream=None, first_word: int = 0):
+    """Device u64[2] checksum of a tensor's bytes (dvla_checksum64_at), on
+    `stream`; compare two GPUs' copies of a region without moving either.
+    first_word: the tensor's 8-byte-word offset inside a larger region
+    (sub-range checksums add up mod 2^64)."""
     from . import _lib
     torch = _torch()
     out = torch.empty(2, dtype=torch.int64, device=t.device)
-    _lib.check(_lib.dvla_checksum64(t.data_ptr(), t.numel() * t.element_size(), out.data_ptr(),
-                                    _stream_ptr(stream)), "dvla_checksum64")
+    _lib.check(_lib.dvla_checksum64_at(t.data_ptr(), t.numel() * t.element_size(),
+                                       int(first_word), out.data_ptr(), _stream_ptr(stream)),
+               "dvla_checksum64_at")
     return out
 
 

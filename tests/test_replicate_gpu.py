@@ -156,3 +156,16 @@ def test_checksum64_matches_host_and_sees_swaps(dev):
     u[:4096], u[4096:8192] = t[4096:8192], t[:4096]
     g2 = [int(x) & (2**64 - 1) for x in checksum64_async(u).cpu().tolist()]
     assert g2[0] == got[0] and g2[1] != got[1]
+
+
+def test_checksum64_of_sub_ranges_adds_up(dev):
+    """dvla_checksum64_at: the checksums of consecutive sub-ranges (word
+    offsets given) add up, mod 2^64, to the whole region's -- the learner
+    re-checksums only the head of each version and adds the body's once."""
+    import torch
+    from paper_2605_13276_b200.replicate import checksum64_async
+    t = torch.randint(0, 256, (8 * 1_000_003,), dtype=torch.uint8, device=dev)
+    whole = checksum64_async(t)
+    cut = 8 * 123_457
+    parts = checksum64_async(t[:cut]) + checksum64_async(t[cut:], first_word=cut // 8)
+    assert torch.equal(whole, parts)
