@@ -809,7 +809,8 @@ def _bench_learner_step(world, rank, dev, barrier, max_over_ranks, steps=10, war
 C3_WEIGHT_BYTES = 6_600_000_000     # pi0-3B-shaped bf16 weights (BASELINE config 3)
 
 
-def _bench_disaggregated(world, rank, dev, epochs=8, keep_timeline=False, engine="ce_head"):
+def _bench_disaggregated(world, rank, dev, epochs=8, keep_timeline=False, engine="ce_head",
+                         staleness_limit=1):
     """BASELINE config 3 layout inside the RL loop (disagg.run_disaggregated):
     learner ranks {0, 1} (from 4 GPUs; {0} below) and rollout ranks, the
     C4-shaped action head trained on the rollout ranks' trajectories, and
@@ -820,7 +821,7 @@ def _bench_disaggregated(world, rank, dev, epochs=8, keep_timeline=False, engine
     from paper_2605_13276_b200.disagg import default_learners, run_disaggregated
     from paper_2605_13276_b200.runtime import SwimlaneConfig
     cfg = SwimlaneConfig(n_groups=N_GROUPS, group_size=G, chunks=C, tokens=T, vocab=V,
-                         hidden=SWIM_H, epochs=epochs, seed=29)
+                         hidden=SWIM_H, epochs=epochs, seed=29, staleness_limit=staleness_limit)
     body = max(0, C3_WEIGHT_BYTES - V * SWIM_H * 2)
     res = run_disaggregated(cfg, verify=True, body_bytes=body, timeout_s=300.0, engine=engine)
     tl = None
@@ -838,7 +839,7 @@ def _bench_disaggregated(world, rank, dev, epochs=8, keep_timeline=False, engine
     S = V * SWIM_H * 2 + body
     gbs = S / (sm["receiver_ms_median_max"] / 1e3) / 1e9 if sm["receiver_ms_median_max"] else None
     return {"layout": f"learners {L}, rollout ranks {[r for r in range(world) if r not in L]}",
-            "engine": engine,
+            "engine": engine, "staleness_limit": staleness_limit,
             "trajectories_per_s_total": sm["trajectories_per_s"],
             "updates": sm["updates"], "quarantined": sm["quarantined"],
             "weight_bytes_per_version": V * SWIM_H * 2 + body,
@@ -1132,6 +1133,11 @@ def run_ours(a):
         if world >= 2:
             barrier()
             swim["disaggregated"] = _guarded(_bench_disaggregated, world, rank, dev)
+            barrier()
+            # the same layout with one more version of slack in the gate: the
+            # push leaves the rollout epochs' critical path (learner-bound)
+            swim["disaggregated_staleness2"] = _guarded(_bench_disaggregated, world, rank, dev,
+                                                        staleness_limit=2)
             barrier()
         # the GPU-work bound of one epoch on one GPU: the sampler's device
         # work (the strict-alternation rollout lane) + the learner step

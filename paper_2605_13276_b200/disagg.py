@@ -499,14 +499,9 @@ def _rollout(cfg, rank, Rr, assign, chans, rep, store, key, ring, S, verify, poi
                 h1.record(s_recv)
                 hops.append((h0, h1))
                 region = rep.replica(v)
-                if verify:
-                    with torch.cuda.stream(s_recv):
-                        csum = _checksum_async(region)
-                    got = _fmt(csum, s_recv)
-                    want = store.get(key("sum", v), "checksum").decode()
-                    if got != want:
-                        res.checksum_mismatches += 1
-                        res.mismatched.append((v, got, want))
+                # deposit at once: the sampler's stream waits on the hop's
+                # event when it installs the version (device-ordered), so the
+                # host never waits for the bytes before the gate can see them
                 ev = torch.cuda.Event()
                 ev.record(s_recv)
                 snap = ParamSnapshot(version=v, params=region[:V * H * 2].view(torch.bfloat16),
@@ -518,6 +513,15 @@ def _rollout(cfg, rank, Rr, assign, chans, rep, store, key, ring, S, verify, poi
                     if state["done"]:
                         release_below(v)
                     cv.notify_all()
+                if verify:   # the replica against the learner's checksum, off the gate's path
+                    with torch.cuda.stream(s_recv):
+                        csum = _checksum_async(region)
+                    got = _fmt(csum, s_recv)
+                    want = store.get(key("sum", v), "checksum").decode()
+                    if got != want:
+                        res.checksum_mismatches += 1
+                        res.mismatched.append((v, got, want))
+                    res.timeline.append(("verified", v, time.perf_counter()))
                 v += 1
             rep.check()
         except Exception as e:  # noqa: BLE001
