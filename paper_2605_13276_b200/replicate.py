@@ -636,6 +636,8 @@ class SplitReplicator:
         self.engine = engine
         if chunk_bytes:
             self.chunk = int(chunk_bytes)
+        elif engine in ("ce", "ce_head") and all(len(c) == 2 for c in chains):
+            self.chunk = self.part    # single hops: one copy-engine copy, one flag (no pipeline)
         elif engine in ("ce", "ce_head"):   # three stream operations per chunk: keep them few
             self.chunk = int(min(max(self.part // 64, 4 << 20), 64 << 20)) // 16 * 16
         else:
