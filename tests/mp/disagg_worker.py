@@ -25,11 +25,12 @@ def main():
     rank, world = dist.get_rank(), dist.get_world_size()
     from paper_2605_13276_b200.disagg import default_learners, run_disaggregated
     from paper_2605_13276_b200.runtime import SwimlaneConfig
-    L = default_learners(world)
+    L = [int(x) for x in os.environ["DVLA_DISAGG_LEARNERS"].split(",")] \
+        if os.environ.get("DVLA_DISAGG_LEARNERS") else default_learners(world)
     cfg = SwimlaneConfig(n_groups=2, group_size=4, tokens=8, vocab=1024, action_bins=256,
                          hidden=64, epochs=5, seed=13)
     engine = os.environ.get("DVLA_DISAGG_ENGINE", "sm")
-    res = run_disaggregated(cfg, verify=True, body_bytes=3_000_000, engine=engine)
+    res = run_disaggregated(cfg, learners=L, verify=True, body_bytes=3_000_000, engine=engine)
     assert res.checksum_mismatches == 0
     n = cfg.vocab * cfg.hidden
     if res.role == "learner":
@@ -57,7 +58,7 @@ def main():
     # a poisoned epoch on every rollout rank: the learners quarantine it together
     cfg2 = SwimlaneConfig(n_groups=2, group_size=4, tokens=8, vocab=1024, action_bins=256,
                           hidden=64, epochs=4, seed=14)
-    res2 = run_disaggregated(cfg2, verify=True, poison_epochs={2},
+    res2 = run_disaggregated(cfg2, learners=L, verify=True, poison_epochs={2},
                              engine="ce" if engine == "sm" else "sm")
     if res2.role == "learner":
         assert res2.quarantined == 1 and res2.updates == 3, (res2.quarantined, res2.updates)
