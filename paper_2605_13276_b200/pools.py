@@ -291,8 +291,8 @@ class TorchArena:
         from . import _lib
         torch.cuda.synchronize(self.device)
         with self._lock:
-            self._pools.clear()
-        gc.collect()
+            self._pools.clear()      # ~MemPool releases the pool; empty_cache then
+        gc.collect()                 # hands its segments back through dvla_torch_free
         torch.cuda.empty_cache()
         _lib.check(_lib.dvla_torch_pool_bind(self.device, None, None), "dvla_torch_pool_bind")
 

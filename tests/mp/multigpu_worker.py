@@ -256,6 +256,19 @@ def main():
         torch.cuda.synchronize()
     dist.barrier()
     pc.close()
+    # a ring of more than 64 slots (the flag slabs grow with the slot count)
+    pc70 = PeerChannel(producer=0, consumer=1, slot_bytes=64 << 10, slots=70)
+    if rank == 0:
+        for gid in range(75):
+            pc70.put(make_batch(gid, "cuda"))
+        torch.cuda.synchronize()
+    elif rank == 1:
+        for gid in range(75):
+            got = pc70.take()
+            assert got.group_id == gid and torch.equal(got.tokens, make_batch(gid, "cuda").tokens)
+        torch.cuda.synchronize()
+    dist.barrier()
+    pc70.close()
     if rank == 0:
         print("PEER_CHANNEL_OK", flush=True)
 

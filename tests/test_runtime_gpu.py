@@ -229,3 +229,34 @@ def test_torch_arena_places_torch_allocations_in_env_aux(dev):
     res = run_swimlane(cfg, device=dev)
     assert res.counters["updates"] == 3
     assert res.counters["torch_arena"]["segments_allocated"] > 0
+
+
+def test_torch_arena_close_returns_segments_and_unbinds(dev):
+    """TorchArena.close(): torch's segments go back to the arena (live bytes
+    0), the device is unbound and the pool may be epoch-reset again.  Runs
+    in a fresh process (the device's binding is process-wide)."""
+    import subprocess
+    import sys
+    code = r"""
+import sys, torch
+sys.path.insert(0, %r)
+from paper_2605_13276_b200.pools import Pool, PoolKind, TorchArena, PoolUsageError
+dev = torch.device("cuda", 0)
+arena = TorchArena(Pool(PoolKind.ENV_AUX, 64 << 20, device=dev))
+with arena:
+    x = torch.ones(1 << 18, device=dev)
+assert arena.holds(x) and arena.pool.stats().live_bytes > 0
+try:
+    arena.pool.epoch_reset()
+    raise SystemExit("epoch_reset allowed while bound")
+except PoolUsageError:
+    pass
+del x
+arena.close()
+assert arena.pool.stats().live_bytes == 0, arena.pool.stats()
+arena.pool.epoch_reset()
+again = TorchArena(Pool(PoolKind.ENV_AUX, 16 << 20, device=dev))   # the device is free again
+print("CLOSE_OK")
+""" % (__import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))),)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "CLOSE_OK" in r.stdout, r.stdout[-2000:] + r.stderr[:3000]
