@@ -155,7 +155,7 @@ def _fmt(c, stream) -> str:
         return ",".join(str(int(x)) for x in c.cpu().tolist())
 
 
-def run_disaggregated(cfg, learners=None, group=None, verify: bool = True,
+def run_disaggregated(cfg, learners=None, verify: bool = True,
                       poison_epochs=frozenset(), timeout_s: float = 120.0,
                       body_bytes: int = 0, engine: str = "ce_head") -> DisaggResult:
     """Collective: every rank of the job calls it (torch.distributed with
@@ -172,10 +172,10 @@ def run_disaggregated(cfg, learners=None, group=None, verify: bool = True,
     replication holds none of the SMs the learner's GEMMs need, and the
     rollout ranks forward with the TMA chain kernel (their GPUs have idle
     SM time between sampling epochs); "sm" runs the TMA kernel on every hop
-    (measured at 4 GPUs with 6.6 GB versions: the learner's update grows
-    from 12 to 20-24 ms while a version is in flight); "ce" uses copy
+    (measured at 4 GPUs with 6.6 GB versions: ~10 % fewer trajectories/s --
+    the heads' kernel takes SMs from the learner's GEMMs); "ce" uses copy
     engines on every hop (forwarding with per-chunk stream waits is slower:
-    21 ms per version vs 14 for "ce_head")."""
+    15.3 ms per version vs 9.9 for "ce_head", tools/split_sweep.py)."""
     import datetime
 
     import torch
