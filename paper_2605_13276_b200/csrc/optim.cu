@@ -93,6 +93,10 @@ __global__ void adam_kernel(float* __restrict__ p, const double* __restrict__ g,
 // Optional outputs: the new parameters rounded to bf16 (the weights the
 // next forward GEMM and the published snapshot read) and a flag raised
 // when any new parameter is non-finite.
+#ifndef DVLA_ADAM_CTAS
+#define DVLA_ADAM_CTAS 3   // CTAs per SM the tail is compiled for (register budget)
+#endif
+
 struct TailArgs {
   float* p;
   const float* g;
@@ -115,7 +119,7 @@ __device__ __forceinline__ double tail_grad(float g32, double div, bool clip, do
   return gi;
 }
 
-__global__ void __launch_bounds__(256, 3) adam_tail_kernel(TailArgs a, int vec) {
+__global__ void __launch_bounds__(256, DVLA_ADAM_CTAS) adam_tail_kernel(TailArgs a, int vec) {
   if (a.skip != nullptr && *a.skip != 0.0f) return;
   bool clip = false;
   double f = 1.0;
