@@ -524,11 +524,15 @@ class TrainerWorker:
       per-token features -> logits GEMM (cuBLAS, bf16 weights kept by the
       optimizer tail) -> fused token loss fwd+bwd (csrc/token_loss.cu) ->
       skip word (loss abort) -> head gradient dW = dl^T feats as f32 GEMM
-      output, in buckets over V whose NCCL all-reduce overlaps the next
-      bucket's GEMM (the skip word travels with the last bucket, so a rank's
-      abort skips the step on every rank) -> grad norm of the mean ->
-      optimizer tail (clip, Adam, bf16 copy, non-finite flag; skipped on the
-      device on abort or a non-finite gradient).
+      output -> with N learners (NCCL): ZeRO-1, the gradient's row blocks
+      reduce-scattered together with every rank's skip word (so one rank's
+      abort skips the step on every rank), this rank's block stepped, the
+      bf16 blocks all-gathered; with the switch-reduced / exact reducers: the
+      mean of the whole gradient -> grad norm of the mean -> optimizer tail
+      (clip, Adam, bf16 copy, non-finite flag; skipped on the device on
+      abort or a non-finite gradient).  (GradReducer.reduce_async keeps a
+      bucketed all-reduce available; overlapping it with the gradient GEMM
+      measured slower.)
     Aborts surface after the one synchronisation: GrpoAbort (the caller
     quarantines; parameters and Adam state untouched) or RunAbort
     (non-finite parameters)."""
