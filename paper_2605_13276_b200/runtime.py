@@ -102,6 +102,9 @@ class Monitor:
 
 class VersionBoard:
     """Two-ended staleness gate (reference runtime.py:211-564, busy mode).
+    The reference's methods also take the lane clock / virtual timestamps
+    (its virtual-time mode); they are accepted and ignored here (busy mode,
+    real time only).
 
     Sampler end: an epoch may start iff version + produced - processed -
     installed <= limit (wait_gate).  Trainer end: version V+1 may be
@@ -126,7 +129,7 @@ class VersionBoard:
         self.epoch_meta: dict = {}
         self.retired_max = -1   # versions <= this one's buffer has been reused
 
-    def deposit(self, snap: ParamSnapshot):
+    def deposit(self, snap: ParamSnapshot, *_virtual_time):
         with self._c:
             if snap.version <= self.installed or snap.version in self.delivered or \
                     snap.version <= self.retired_max:
@@ -137,7 +140,7 @@ class VersionBoard:
             self.delivered[snap.version] = snap
             self._c.notify_all()
 
-    def boundary(self):
+    def boundary(self, *_clock):
         with self._c:
             self.at_boundary = True
             self._c.notify_all()
@@ -152,13 +155,13 @@ class VersionBoard:
         with self._c:
             return self.epoch_meta.pop(epoch)
 
-    def mark_sampler_done(self):
+    def mark_sampler_done(self, *_clock):
         with self._c:
             self.sampler_done = True
             self.at_boundary = True
             self._c.notify_all()
 
-    def wait_gate(self):
+    def wait_gate(self, *_clock):
         """Block until the gate admits the next epoch; installs the newest
         delivered snapshot first (epoch-boundary install).  Returns
         (snapshot, staleness)."""
@@ -182,7 +185,7 @@ class VersionBoard:
                 self.monitor.beat(LaneId.SAMPLER.value, "gate-wait")
                 self._c.wait(0.05)
 
-    def wait_pacing(self, next_version: int):
+    def wait_pacing(self, next_version: int, *_clock):
         with self._c:
             while True:
                 if self.monitor.abort.is_set():
@@ -194,7 +197,7 @@ class VersionBoard:
                 self.monitor.beat(LaneId.TRAINER.value, "pacing-wait")
                 self._c.wait(0.05)
 
-    def publish(self) -> int:
+    def publish(self, *_clock) -> int:
         with self._c:
             self.version += 1
             self.processed += 1
@@ -203,7 +206,7 @@ class VersionBoard:
             self._c.notify_all()
             return self.version
 
-    def quarantine(self):
+    def quarantine(self, *_clock):
         with self._c:
             self.processed += 1
             self._c.notify_all()
@@ -278,7 +281,42 @@ class GradReducer:
         self.backend = "nvls" if ok.item() == 1.0 else "nccl"
         return self.backend == "nvls"
 
-    def reduce(self, grad):
+    def reduce(self, *args):
+        """The mean of this rank's gradient over the nodes.  Called as
+        reduce(grad), or with the reference's signature reduce(node, round,
+        grad, clock) (runtime.py:596-627: there every node is a thread of one
+        process; here every node is a process, so node / round / clock carry
+        no information)."""
+        if len(args) == 1:
+            grad = args[0]
+        elif len(args) in (3, 4):
+            grad = args[2]
+        else:
+            raise TypeError("reduce(grad) or reduce(node, round, grad, clock)")
+        return self._reduce(grad)
+
+    def reduce_serial(self, rnd: int, grads: list):
+        """Sync-mode path (reference runtime.py:629-637): every node's
+        gradient on hand in one place; each is quantised to the f32 frame,
+        summed in f64 in node order and divided by the node count -- the
+        reference's arithmetic.  numpy in -> numpy out; tensors stay on the
+        first gradient's device."""
+        del rnd
+        if self.nodes == 1 or len(grads) == 1:
+            return grads[0]
+        if isinstance(grads[0], np.ndarray):
+            total = np.zeros(grads[0].shape[0], dtype=np.float64)
+            for g in grads:
+                total += np.asarray(g).astype(np.float32).astype(np.float64)
+            return total / len(grads)
+        import torch
+        dev = grads[0].device
+        total = torch.zeros(grads[0].numel(), dtype=torch.float64, device=dev)
+        for g in grads:
+            total += g.reshape(-1).to(dev).to(torch.float32).to(torch.float64)
+        return total / len(grads)
+
+    def _reduce(self, grad):
         import torch
         import torch.distributed as dist
         if self.nodes == 1:
@@ -295,7 +333,7 @@ class GradReducer:
                 except NativeError:  # raised on every rank alike: fall back together
                     self._ar = None
                     self.backend = "nccl"
-                    return self.reduce(grad)
+                    return self._reduce(grad)
                 self._ar.buf.zero_()
             self._ar.buf[:n].copy_(grad.reshape(-1))  # f32 quantisation (the frame)
             self._ar.allreduce(scale=1.0 / self.nodes)
@@ -694,8 +732,10 @@ class TrainerWorker:
         dist.all_gather_into_tensor(pol.w16pad, pol.w16_own, group=grp)
         dist.all_reduce(self.flags, op=dist.ReduceOp.MAX, group=grp)
 
-    def update(self, batches: list) -> dict:
-        """One GRPO update on one epoch of groups (reference runtime.py:768-800)."""
+    def update(self, batches: list, transport_nodes: int | None = None) -> dict:
+        """One GRPO update on one epoch of groups (reference runtime.py:768-800).
+        transport_nodes: the reference's argument; the node count here is
+        the reducer's (GradReducer.nodes)."""
         import torch
 
         from . import _lib

@@ -284,3 +284,21 @@ def test_disagg_key_board_polls_without_blocking_other_lanes():
     errors.append(RuntimeError("peer lane failed"))
     with pytest.raises(RuntimeError, match="peer lane failed"):
         kb.wait([kb.key("never")])
+
+
+def test_grad_reducer_reference_signatures():
+    """GradReducer keeps the reference's call forms: reduce(node, round,
+    grad, clock) (a no-op on one node) and reduce_serial(round, grads) with
+    the reference arithmetic (f32 frames, f64 sum in node order, / nodes)."""
+    import torch
+    g = np.array([1.0 / 3, 2.0, -1e-9])
+    r = GradReducer(1)
+    assert r.reduce(0, 5, g, None) is g and r.reduce(g) is g
+    r3 = GradReducer(3)
+    gs = [g * (k + 1) for k in range(3)]
+    want = sum(x.astype(np.float32).astype(np.float64) for x in gs) / 3
+    np.testing.assert_array_equal(r3.reduce_serial(0, gs), want)
+    got_t = r3.reduce_serial(0, [torch.from_numpy(x) for x in gs])
+    np.testing.assert_array_equal(got_t.numpy(), want)
+    with pytest.raises(TypeError):
+        r.reduce(1, 2)
