@@ -1139,6 +1139,17 @@ def run_ours(a):
             swim["disaggregated_staleness2"] = _guarded(_bench_disaggregated, world, rank, dev,
                                                         staleness_limit=2)
             barrier()
+            # strict alternation in the same layout (staleness limit 0: every
+            # epoch waits for the previous update's version to arrive)
+            swim["disaggregated_sync"] = _guarded(_bench_disaggregated, world, rank, dev,
+                                                  staleness_limit=0)
+            barrier()
+            try:
+                swim["disaggregated_async_over_sync"] = (
+                    swim["disaggregated"]["trajectories_per_s_total"]
+                    / swim["disaggregated_sync"]["trajectories_per_s_total"])
+            except (TypeError, KeyError, ZeroDivisionError):
+                pass
         # the GPU-work bound of one epoch on one GPU: the sampler's device
         # work (the strict-alternation rollout lane) + the learner step
         if isinstance(learner, dict) and "ms_per_step_device" in learner:

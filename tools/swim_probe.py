@@ -51,7 +51,7 @@ def main():
         out["swimlane"] = bench._bench_swimlane(world, rank, dev, mx, epochs=a.epochs)
     if a.disagg and world > 1:
         barrier()
-        for eng, lim in (("ce_head", 1), ("ce_head", 2)):
+        for eng, lim in (("ce_head", 0), ("ce_head", 1), ("ce_head", 2)):
             barrier()
             out[f"disaggregated_{eng}_limit{lim}"] = bench._bench_disaggregated(
                 world, rank, dev, keep_timeline=True, engine=eng, staleness_limit=lim)
