@@ -221,7 +221,7 @@ constexpr int kWarpStore = kFusedComputeWarps + 2;
 constexpr int kPrepWarp = kFusedComputeWarps + 3;
 constexpr int kFusedThreadsWS = (kFusedComputeWarps + 4) * 32;
 
-constexpr int kLagRounds = 4;  // pieces; measured best on B200 (lag sweep, tools/fused_variants.py)
+constexpr int kLagRounds = 3;  // pieces; measured best on B200 (round 2: tools/lag_ab.sh, 5 alternating sustained pairs)
 constexpr int kRing = 8;       // (lse, target) rows in flight tail -> prep; lag <= 8P - 1
 constexpr float kFrameHi = 64.f;   // fixed-frame sum-exp range of a warp max (see phase A)
 constexpr float kFrameLo = -50.f;
