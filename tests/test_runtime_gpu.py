@@ -260,3 +260,33 @@ print("CLOSE_OK")
 """ % (__import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))),)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "CLOSE_OK" in r.stdout, r.stdout[-2000:] + r.stderr[:3000]
+
+
+def test_nvlink_broadcast_across_devices_one_process(dev):
+    """ControlPlane NVLINK transport with subscribers on two GPUs of one
+    process: hops on the second device run on the plane's own stream with
+    their own timeout word; each mailbox's snapshot carries the event of the
+    hop that wrote it."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs in one process")
+    from paper_2605_13276_b200.core import snapshot_from_params
+    from paper_2605_13276_b200.planes import ControlPlane, Plane, Transport, TransportMode
+    from paper_2605_13276_b200.replicate import bytes_equal
+    n = 2_000_000
+    plane = ControlPlane(Transport(TransportMode.NVLINK, Plane.CONTROL), chunk_bytes=1 << 20,
+                         ctas_per_hop=8)
+    boxes = [plane.subscribe("a", device="cuda:0", nbytes=4 * n),
+             plane.subscribe("b", device="cuda:1", nbytes=4 * n),
+             plane.subscribe("c", device="cuda:1", nbytes=4 * n)]
+    s = torch.cuda.Stream(device="cuda:0")
+    for v in (1, 2, 3):
+        p = torch.randn(n, device="cuda:0") + v
+        plane.broadcast(snapshot_from_params(p, v), stream=s)
+        for b in boxes:
+            got = b.take_newest()
+            got.ready.synchronize()
+            assert got.version == v
+            ref = p.to(got.params.device)
+            assert bytes_equal(got.params, ref) == (0, -1), (b.name, v)
+    plane.check()
