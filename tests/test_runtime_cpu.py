@@ -302,3 +302,40 @@ def test_grad_reducer_reference_signatures():
     np.testing.assert_array_equal(got_t.numpy(), want)
     with pytest.raises(TypeError):
         r.reduce(1, 2)
+
+
+def test_retire_waits_for_a_newer_install_and_blocks_stale_deposits():
+    """VersionBoard.retire (the published-weight ring, run_swimlane): the
+    publisher may reuse version u's slot only once the sampler installed
+    something newer; u (and anything older) is dropped from the pending
+    deliveries and later deposits of it are ignored."""
+    b = _board(limit=1)
+    b.wait_gate()                                    # sampler installed v0 (mid-epoch)
+    done = threading.Event()
+
+    def publisher():
+        b.retire(0)                                  # slot of v0 about to be reused
+        done.set()
+
+    t = threading.Thread(target=publisher)
+    t.start()
+    assert not done.wait(0.2)                        # v0 is installed: must wait
+    b.publish()
+    b.deposit(ParamSnapshot(version=1, params=np.ones(4, np.float32)))
+    b.produce(0, {})
+    b.boundary()
+    b.wait_gate()                                    # installs v1
+    assert done.wait(2.0) and b.installed == 1
+    b.deposit(ParamSnapshot(version=0, params=np.zeros(4, np.float32)))
+    assert b.regressions_ignored == 1
+    # pending deliveries at or below the retired version are dropped
+    b2 = _board(limit=2)
+    b2.deposit(ParamSnapshot(version=1, params=np.zeros(4, np.float32)))
+    b2.deposit(ParamSnapshot(version=2, params=np.zeros(4, np.float32)))
+    b2.installed = 3                                 # (as if v3 were installed)
+    b2.retire(2)
+    assert 1 not in b2.delivered and 2 not in b2.delivered and b2.retired_max == 2
+    # a finished sampler never blocks the publisher
+    b3 = _board(limit=1)
+    b3.mark_sampler_done()
+    b3.retire(0)
