@@ -1285,13 +1285,17 @@ extern "C" int dvla_token_loss_fwd_bwd(const void* logits, int dtype, const int3
     const unsigned grid = static_cast<unsigned>(R < slots ? R : slots);
     cudaEvent_t stop;
     prof_begin(stream, &stop);
-    static const int lag = [] {
+    static const int lag_env = [] {
       const char* e = getenv("DVLA_FUSED_LAG");
-      return e ? atoi(e) : kLagRounds;
+      return e ? atoi(e) : 0;
     }();
     // lag in pieces: >= 2P - 1 so a chunk's two rounds of tails precede its
-    // B ops (deadlock freedom), <= kRing P - 1 for the (lse, target) ring
+    // B ops (deadlock freedom), <= kRing P - 1 for the (lse, target) ring.
+    // Measured defaults (sustained, power-capped): 3 pieces for one-piece
+    // rows (bf16 C2), 4 pieces = 2 rows for two-piece rows (f32 C2: 1.370 vs
+    // 1.423 ms at 3, 1.430 at 5; tools/f32_time.py).
     const int P = geom.pieces;
+    const int lag = lag_env > 0 ? lag_env : (P == 1 ? kLagRounds : (P == 2 ? 4 : 2 * P - 1));
     const int lag_p = std::min(std::max(lag, 2 * P - 1), kRing * P - 1);
     DVLA_CUDA_TRY(launch_maybe_pdl(kern, dim3(grid), dim3(kFusedThreadsWS), geom.smem, stream,
                                    p, geom.stage_bytes, geom.piece_vec, want_dl ? 1 : 0,

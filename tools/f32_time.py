@@ -14,15 +14,18 @@ tl = grpo.TokenLoss(N_GROUPS, G, C, T, V, grpo.GrpoConfig(group_size=G), dtype=t
 tl.launch(logits, tokens, torch.zeros(N_GROUPS * G, device=dev), rw, None)
 blp = (tl.lp_chunk + 0.01).float()
 dl = torch.empty_like(logits)
-for _ in range(3):
+import time
+t_end = time.perf_counter() + float(os.environ.get("WARM_S", "1.0"))   # reach the sustained state
+while time.perf_counter() < t_end:
     tl.launch(logits, tokens, blp, rw, dl)
-torch.cuda.synchronize()
+    torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+n_it = int(os.environ.get("ITERS", "100"))
 e0.record()
-for _ in range(10):
+for _ in range(n_it):
     tl.launch(logits, tokens, blp, rw, dl)
 e1.record()
 torch.cuda.synchronize()
-ms = e0.elapsed_time(e1) / 10
+ms = e0.elapsed_time(e1) / n_it
 algo = 2 * R * V * 4
 print(f"f32 C2 step {ms:.3f} ms  {algo / ms / 1e6:.0f} GB/s algorithmic ({algo/1e9:.2f} GB)")
