@@ -268,7 +268,7 @@ __device__ __forceinline__ void op_of(int n, int nloc, int L, bool* isB, int* k)
 }
 
 #ifndef DVLA_POLL_NS
-#define DVLA_POLL_NS 256  // prep warp: back-off between polls of a chunk's token log-probs
+#define DVLA_POLL_NS 512  // prep warp: back-off between polls of a chunk's token log-probs
 #endif
 #ifndef DVLA_FULL_SPIN
 #define DVLA_FULL_SPIN 0
@@ -282,6 +282,9 @@ __device__ __forceinline__ void op_of(int n, int nloc, int L, bool* isB, int* k)
 #endif
 #ifndef DVLA_POLY_WORDS
 #define DVLA_POLY_WORDS 0
+#endif
+#ifndef DVLA_A_EVICT_LAST
+#define DVLA_A_EVICT_LAST 0   // phase-A loads with an L2 evict_last hint (experiment)
 #endif
 #ifndef DVLA_ACC_INPLACE
 #define DVLA_ACC_INPLACE 1
@@ -456,6 +459,9 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
   if (warp == kWarpLoader) {
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
+#if DVLA_A_EVICT_LAST
+      const uint64_t pol_last = l2_policy_evict_last();
+#endif
       for (int n = 0; n < nops; ++n) {
         const int s = static_cast<int>(n % kFusedStages);
         if (n >= kFusedStages) {
@@ -472,8 +478,13 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
         mbar_arrive_expect_tx(&S.full[s], bytes);
         if (isB)  // second (last) read of the piece: from L2, then evict
           tma_load_1d_evict_first(buf(s), src, bytes, &S.full[s], pol);
+#if DVLA_A_EVICT_LAST
+        else
+          tma_load_1d_evict_first(buf(s), src, bytes, &S.full[s], pol_last);
+#else
         else  // (an evict_last hint here measured no better: the lag keeps rows in L2)
           tma_load_1d(buf(s), src, bytes, &S.full[s]);
+#endif
       }
     }
     return;
