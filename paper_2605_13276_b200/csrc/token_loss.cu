@@ -50,7 +50,14 @@ constexpr int kFusedCtasPerSm = DVLA_FUSED_CTAS;  // resident fused CTAs per SM
 constexpr size_t kFusedSmemCap = (228u * 1024u) / DVLA_FUSED_CTAS - 1024u;
 constexpr int kFusedComputeThreads = kFusedComputeWarps * 32;
 constexpr int kFusedStages = 3;    // SMEM row stages and B coefficient slots
-constexpr int kASlots = 8;         // A-row partial slots (coef-warp slack)
+#ifndef DVLA_A_SLOTS
+#define DVLA_A_SLOTS 8
+#endif
+#ifndef DVLA_B_UNROLL
+#define DVLA_B_UNROLL 2   // phase-B granules per loop iteration
+#endif
+constexpr int kASlots = DVLA_A_SLOTS;  // A-row partial slots (coef-warp slack)
+constexpr int kBUnroll = DVLA_B_UNROLL;
 constexpr uint64_t kSpinTimeoutNs = 4000000000ull;  // 4 s: report, never hang
 
 struct TokParams {
@@ -807,7 +814,7 @@ __global__ void __launch_bounds__(kFusedThreadsWS, kFusedCtasPerSm)
       const float K = S.kval[sb];
       const uint64_t nK2 = f2pack(-K, -K);
       const uint32_t sgn = (mode & 0x80000000u) ? FE::kSign : 0u;
-#pragma unroll 2
+#pragma unroll kBUnroll
       for (int i = tid; i < nvec; i += kFusedComputeThreads) v[i] = FE::grad(v[i], l2e2, nK2, sgn);
       if (owner) FE::put(v, li, val);
     }
