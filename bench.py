@@ -732,13 +732,17 @@ def _bench_c2_f32(dev, rank, world, barrier, max_over_ranks, steps=20):
 SWIM_H = 4096                        # OpenVLA-7B hidden size (the action head's K)
 
 
-def _bench_learner_step(world, rank, dev, barrier, max_over_ranks, steps=10, warmup=3):
+def _bench_learner_step(world, rank, dev, barrier, max_over_ranks, steps=10, warmup=3,
+                        scatter="auto"):
     """The learner step of BASELINE config 4 per GPU, timed as a unit with
     its collective (reference TrainerWorker.update, runtime.py:768-800):
     per-token features -> logits GEMM (V=32,064 x H=4,096 bf16 head) ->
-    fused token loss fwd+bwd -> f32 head-gradient GEMM in 4 buckets whose
-    NCCL all-reduce overlaps the next bucket -> grad norm -> optimizer tail
-    (clip + Adam + bf16 copy + non-finite flag), one host sync per step.
+    fused token loss fwd+bwd -> f32 head-gradient GEMM in row blocks, with
+    N GPUs ZeRO-1: each peer's block pushed over NVLink by a copy engine as
+    it completes, own block last, node-order sum (scatter "peer"; "nccl" =
+    NCCL reduce-scatter after the GEMM) -> grad norm -> optimizer tail on
+    the own block (clip + Adam + bf16 copy + non-finite flag) -> bf16
+    all-gather, one host sync per step.
     CUDA events on the trainer stream, max over ranks; the same 512
     trajectories every step (inputs 1.84 GB of logits > L2)."""
     import torch
@@ -755,7 +759,7 @@ def _bench_learner_step(world, rank, dev, barrier, max_over_ranks, steps=10, war
     s_train = torch.cuda.Stream(device=dev, priority=-1)
     s_sample = torch.cuda.Stream(device=dev)
     import torch.distributed as dist
-    reducer = GradReducer(world, None)
+    reducer = GradReducer(world, None, scatter=scatter)
     trainer = TrainerWorker(cfg, rank, model_pool, reducer, s_train, dev)
     sampler = SamplerWorker(cfg, rank, world, [env_pool], s_sample, dev)
     msgs, _ = sampler.run_epoch(0, trainer.snapshot())
@@ -798,8 +802,14 @@ def _bench_learner_step(world, rank, dev, barrier, max_over_ranks, steps=10, war
                              "achieved_tflops_step": round(flops / (dev_ms / 1e3) / 1e12, 1),
                              "frac_step": round(flops / (dev_ms / 1e3) / 1e12 / tf_peak, 4)},
            "config": f"V={V} x H={SWIM_H} bf16 head, {N_GROUPS}x{G} traj x {T} tokens per GPU; "
-                     f"grad f32 {n * 4 / 1e9:.2f} GB all-reduced over {world} GPU(s)",
+                     f"grad f32 {n * 4 / 1e9:.2f} GB reduce-scattered over {world} GPU(s)",
+           "reduce_scatter": (("peer: copy-engine pushes over NVLink overlapped with the "
+                               "gradient GEMM + node-order f64 sum (exchange.PeerGradExchange)")
+                              if getattr(trainer, "exchange", None) is not None else
+                              ("NCCL reduce_scatter_tensor after the gradient GEMM"
+                               if world > 1 else None)),
            "steps": steps}
+    trainer.close()
     del trainer, sampler, model_pool, env_pool, msgs
     torch.cuda.empty_cache()
     _ = dist
@@ -1119,6 +1129,13 @@ def run_ours(a):
     allreduce = _bench_allreduce(world, dev, barrier, max_over_ranks)
     learner = None if a.no_swimlane else _guarded(_bench_learner_step, world, rank, dev, barrier,
                                                   max_over_ranks)
+    if learner and world > 1 and "value" in learner:
+        # the same step with NCCL's reduce-scatter (the collective-library baseline)
+        alt = _guarded(_bench_learner_step, world, rank, dev, barrier, max_over_ranks,
+                       scatter="nccl")
+        if alt and "value" in alt:
+            learner["nccl_reduce_scatter"] = {k: alt[k] for k in (
+                "value", "ms_per_step_wall", "ms_per_step_device", "phases_ms_rank0")}
     # secondary per-GPU measurements: a failure is reported, never fatal to
     # the headline line
     gauss = None if a.no_gauss else _guarded(_bench_gauss_c3, dev, rank, cpu=not a.no_cpu)

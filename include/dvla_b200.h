@@ -234,6 +234,16 @@ int dvla_grad_norm_f32(const float* grad, int64_t n, double div, double* norm_ou
  * norm: the shards' sums are all-reduced, then the root taken). */
 int dvla_grad_sumsq_f32(const float* grad, int64_t n, double div, double* sumsq_out,
                         uint32_t* nonfinite_out, void* workspace, void* stream);
+/* The peer gradient exchange's reduce-scatter epilogue (runtime.py:618-627:
+ * the nodes' f32 frames summed in f64 in node order): out[i] = f32(sum over
+ * k < n_src, in order, of f64(srcs[k][i])) for i < n_all, and in the same
+ * pass what dvla_grad_sumsq_f32(out, n, div, ...) returns for the first n
+ * (bit-identical; [n, n_all) carries side words such as the skip flags).
+ * srcs: a HOST array of n_src (1..16) device pointers, each and out 16-byte
+ * aligned; workspace as dvla_grad_norm_workspace_bytes(n). */
+int dvla_grad_sum_f32(const float* const* srcs, int n_src, int64_t n, int64_t n_all, double div,
+                      float* out, double* sumsq_out, uint32_t* nonfinite_out, void* workspace,
+                      void* stream);
 int dvla_adam_tail_f32(float* params, const float* grad, double* m, double* v, int64_t n,
                        int64_t step, double lr, double beta1, double beta2, double eps,
                        double div, const double* norm, double max_norm, const float* skip,

@@ -208,6 +208,8 @@ dvla_grad_norm = _proto("dvla_grad_norm", [_vp, _i64, _f64, _vp, _vp, _vp, _vp])
 dvla_f32_nonfinite = _proto("dvla_f32_nonfinite", [_vp, _i64, _vp, _vp])
 dvla_grad_norm_f32 = _proto("dvla_grad_norm_f32", [_vp, _i64, _f64, _vp, _vp, _vp, _vp])
 dvla_grad_sumsq_f32 = _proto("dvla_grad_sumsq_f32", [_vp, _i64, _f64, _vp, _vp, _vp, _vp])
+dvla_grad_sum_f32 = _proto("dvla_grad_sum_f32", [C.POINTER(_vp), _i32, _i64, _i64, _f64, _vp, _vp,
+                                                   _vp, _vp, _vp])
 dvla_adam_tail_f32 = _proto("dvla_adam_tail_f32", [
     _vp, _vp, _vp, _vp, _i64, _i64, _f64, _f64, _f64, _f64, _f64, _vp, _f64, _vp, _vp, _vp, _vp])
 dvla_loss_status = _proto("dvla_loss_status", [_vp, _vp, _vp])

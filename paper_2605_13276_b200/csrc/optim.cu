@@ -308,6 +308,98 @@ __global__ void sumsq_blocks_f32_kernel(const float* __restrict__ g, int64_t n, 
   }
 }
 
+// Reduce-scatter epilogue of the peer gradient exchange (runtime.py:618-627:
+// the nodes' f32 frames summed in f64 in node order): out[i] = f32(sum over
+// p in source order of f64(src[p][i])), and -- in the same pass, with
+// sumsq_blocks_f32_kernel's block shape and per-thread order, so the two
+// give identical partials -- the block sums of squares of out[i] / div.
+constexpr int kMaxSumSrcs = 16;
+struct SumSrcs {
+  const float* p[kMaxSumSrcs];
+};
+
+__device__ __forceinline__ float4 sum_srcs4(const SumSrcs& s, int n_src, int64_t q) {
+  double x = 0.0, y = 0.0, z = 0.0, w = 0.0;
+  for (int k = 0; k < n_src; ++k) {
+    const float4 v = __ldcs(reinterpret_cast<const float4*>(s.p[k]) + q);
+    x += v.x;
+    y += v.y;
+    z += v.z;
+    w += v.w;
+  }
+  return make_float4(static_cast<float>(x), static_cast<float>(y), static_cast<float>(z),
+                     static_cast<float>(w));
+}
+
+__global__ void __launch_bounds__(kNormThreads) sum_sumsq_blocks_f32_kernel(
+    SumSrcs src, int n_src, int64_t n, int64_t n_all, int64_t per_block, double div,
+    float* __restrict__ out, double* __restrict__ partial, unsigned* __restrict__ nonfinite) {
+  __shared__ double red[kNormThreads / 32];
+  if (blockIdx.x == gridDim.x - 1) {   // [n, n_all): summed, outside the norm
+    for (int64_t i = n + threadIdx.x; i < n_all; i += kNormThreads) {
+      double t = 0.0;
+      for (int k = 0; k < n_src; ++k) t += src.p[k][i];
+      out[i] = static_cast<float>(t);
+    }
+  }
+  if (static_cast<int64_t>(blockIdx.x) * per_block >= n) return;
+  const int64_t lo = blockIdx.x * per_block;
+  const int64_t hi = (lo + per_block < n) ? lo + per_block : n;
+  double acc0 = 0.0, acc1 = 0.0;
+  unsigned bad = 0;
+  const double inv = (div != 1.0) ? 1.0 / (div * div) : 1.0;
+  auto sq4 = [](const float4& v) {
+    const double a = v.x, b = v.y, c = v.z, d = v.w;
+    return (a * a + b * b) + (c * c + d * d);
+  };
+  auto bad4 = [](const float4& v) {
+    return !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
+  };
+  // every source and `out` 16-byte aligned (checked on the host)
+  const int64_t q0 = lo / 4;
+  const int64_t nq = (hi - lo) / 4;
+  float4* o4 = reinterpret_cast<float4*>(out);
+  int64_t j = threadIdx.x;
+  for (; j + 3 * kNormThreads < nq; j += 4 * kNormThreads) {
+    const float4 a = sum_srcs4(src, n_src, q0 + j);
+    const float4 b = sum_srcs4(src, n_src, q0 + j + kNormThreads);
+    const float4 c = sum_srcs4(src, n_src, q0 + j + 2 * kNormThreads);
+    const float4 d = sum_srcs4(src, n_src, q0 + j + 3 * kNormThreads);
+    o4[q0 + j] = a;
+    o4[q0 + j + kNormThreads] = b;
+    o4[q0 + j + 2 * kNormThreads] = c;
+    o4[q0 + j + 3 * kNormThreads] = d;
+    acc0 += sq4(a) + sq4(b);
+    acc1 += sq4(c) + sq4(d);
+    bad |= bad4(a) | bad4(b) | bad4(c) | bad4(d);
+  }
+  for (; j < nq; j += kNormThreads) {
+    const float4 a = sum_srcs4(src, n_src, q0 + j);
+    o4[q0 + j] = a;
+    acc0 += sq4(a);
+    bad |= bad4(a);
+  }
+  for (int64_t i = lo + nq * 4 + threadIdx.x; i < hi; i += kNormThreads) {
+    double t = 0.0;
+    for (int k = 0; k < n_src; ++k) t += src.p[k][i];
+    const float f = static_cast<float>(t);
+    out[i] = f;
+    const double x = f;
+    acc0 += x * x;
+    bad |= !isfinite(f);
+  }
+  double acc = warp_sum_f64((acc0 + acc1) * inv);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  bad = __any_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0 && bad) atomicOr(nonfinite, 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kNormThreads / 32; ++w) s += red[w];
+    partial[blockIdx.x] = s;
+  }
+}
+
 // fixed-order finish: thread t sums partials t, t + 1024, ... sequentially,
 // then a warp-shuffle and a 32-entry tree (deterministic, one block)
 constexpr int kFinishThreads = 1024;
@@ -446,6 +538,35 @@ extern "C" int dvla_grad_norm_f32(const float* grad, int64_t n, double div, doub
 extern "C" int dvla_grad_sumsq_f32(const float* grad, int64_t n, double div, double* sumsq_out,
                                    uint32_t* nonfinite_out, void* workspace, void* stream) {
   return grad_sumsq_f32(grad, n, div, sumsq_out, nonfinite_out, workspace, stream, 0);
+}
+
+extern "C" int dvla_grad_sum_f32(const float* const* srcs, int n_src, int64_t n, int64_t n_all,
+                                 double div, float* out, double* sumsq_out,
+                                 uint32_t* nonfinite_out, void* workspace, void* stream) {
+  if (n < 0 || n_all < n || !srcs || n_src < 1 || n_src > kMaxSumSrcs || !out || !sumsq_out ||
+      !nonfinite_out || !workspace || !(div > 0.0))
+    return fail(DVLA_ERR_USAGE, "bad grad_sum_f32 arguments (1 <= n_src <= %d)", kMaxSumSrcs);
+  SumSrcs s{};
+  for (int k = 0; k < n_src; ++k) {
+    if (!srcs[k] || (reinterpret_cast<uintptr_t>(srcs[k]) & 15))
+      return fail(DVLA_ERR_USAGE, "grad_sum_f32: source %d null or not 16-byte aligned", k);
+    s.p[k] = srcs[k];
+  }
+  if (reinterpret_cast<uintptr_t>(out) & 15)
+    return fail(DVLA_ERR_USAGE, "grad_sum_f32: output not 16-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nblocks = kNormBlocks;
+  const int64_t per = ((n + nblocks - 1) / nblocks + 3) & ~int64_t{3};
+  double* partial = static_cast<double*>(workspace);
+  DVLA_CUDA_TRY(cudaMemsetAsync(partial, 0, nblocks * sizeof(double), st));
+  if (n_all > 0) {
+    const int used = n > 0 ? static_cast<int>((n + per - 1) / per) : 1;
+    sum_sumsq_blocks_f32_kernel<<<used, kNormThreads, 0, st>>>(
+        s, n_src, n, n_all, per, div, out, partial, reinterpret_cast<unsigned*>(nonfinite_out));
+    if (int rc = launch_check("sum_sumsq_blocks_f32_kernel")) return rc;
+  }
+  norm_finish_kernel<<<1, kFinishThreads, 0, st>>>(partial, nblocks, sumsq_out, 0);
+  return launch_check("norm_finish_kernel");
 }
 
 extern "C" int dvla_adam_tail_f32(float* params, const float* grad, double* m, double* v,

@@ -1,0 +1,171 @@
+"""Learner-gradient reduce-scatter over NVLink peer memory, overlapped with
+the gradient GEMM (ZeRO-1 path of TrainerWorker.update).
+
+Reference: GradReducer.reduce / reduce_serial (runtime.py:569-637) -- every
+node's gradient travels as an f32 frame (runtime.py:590), the frames are
+summed in f64 in node order and divided by the node count (runtime.py:618-
+627); TrainerWorker.update divides by w and reduces (runtime.py:788).  SURVEY
+§8 a10 / e.
+
+B200 design.  The head gradient dW = dl^T x is a row-blocked GEMM: block j
+(the rows rank j owns under ZeRO-1) is computed by every rank and needed,
+summed, only by rank j.  Each rank computes its blocks in the order
+j = r + 1, r + 2, ..., r (its own block LAST), and as soon as block j is in
+HBM a copy engine pushes it over NVLink into rank j's staging slot for r --
+no SMs are taken from the GEMM, whose remaining blocks hide the transfer
+(rank j's last incoming block is finished one block-GEMM before j's own).
+Then one HBM-bound kernel on rank j sums its own block and the N - 1 staged
+ones in f64 in NODE order (the reference's arithmetic, deterministic) and
+computes the block's sum of squares in the same pass
+(`dvla_grad_sum_f32`).  Per GPU the links carry (N - 1) / N of the gradient
+each way, the same as a ring reduce-scatter, but in one step with no
+SM-driven pipeline.
+
+Synchronisation is stream-ordered, with one u32 flag per peer and direction
+in device memory (the same CUDA IPC + stream memory-operation protocol as
+the copy-engine replication chain, replicate.SplitReplicator):
+  ready[p] on rank j  = step e  after p's push into j's slot p landed
+                                (written by p's copy stream)
+  ack[j]   on rank p  = step e  after j's sum read its slot p
+                                (written by j's trainer stream)
+so a push of step e + 1 never overwrites a slot before the step-e sum read
+it, and a GEMM of step e + 1 never overwrites a block before its step-e push
+(a local event).  Stream waits have no timeout: a rank that stops issuing
+steps stalls its peers, as an NCCL collective would.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+from .core import UsageError
+
+
+class PeerGradExchange:
+    """Reduce-scatter of `gin` ([N, cs] f32, this rank's GEMM output; row j
+    goes to rank j) into rank r's sum, over CUDA IPC + copy engines.
+
+    Collective construction: every rank of `group` calls it (one process
+    per GPU).  `stage_pool` (a device Pool, e.g. MODEL_COMPUTE) holds the
+    N x cs f32 staging slots; per step:
+        begin(s)                       # before anything writes gin
+        for j in order(): GEMM block j into gin[j]; pushed(j, s)
+        finish(s, out, div, sumsq, nonfinite, workspace)
+    """
+
+    def __init__(self, gin, stage_pool, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+        from .replicate import _gather_by_rank, _open_ipc, _PoolRegion, _Slab
+        if gin.dim() != 2 or gin.dtype != torch.float32 or not gin.is_contiguous():
+            raise UsageError("gin must be a contiguous [N, cs] f32 tensor")
+        self.N, self.cs = gin.shape
+        if (self.cs * 4) % 16 or gin.data_ptr() % 16:
+            raise UsageError("gradient blocks must be 16-byte aligned")
+        self.rank = dist.get_rank(group)
+        if dist.get_world_size(group) != self.N:
+            raise UsageError("gin needs one block per rank of the group")
+        self.gin = gin
+        self.dev = gin.device
+        self.group = group
+        N, cs, r = self.N, self.cs, self.rank
+        self.stage = _PoolRegion(stage_pool, N * cs * 4)
+        self.stage_t = self.stage.t[: N * cs * 4].view(torch.float32).view(N, cs)
+        self.flags = _Slab(256, self.dev.index)   # ready[0:N) | ack[32:32+N)
+        self.flags.t.zero_()
+        torch.cuda.synchronize(self.dev)
+        if N > 32:
+            raise UsageError("at most 32 ranks per exchange")
+        # peer access for the copy engines (symmetric; IPC mappings also need it
+        # for direct stores/loads, copies work either way)
+        ranks = (list(range(dist.get_world_size())) if group is None
+                 else dist.get_process_group_ranks(group))
+        devs = _gather_by_rank(self.dev.index, group)
+        for g in ranks:
+            if devs[g] != self.dev.index:
+                _lib.dvla_enable_peer_access(self.dev.index, devs[g])
+        allh = _gather_by_rank((self.stage.ipc(), self.stage.offset, self.flags.ipc()), group)
+        self._opened = []
+        self.peer = {}   # group rank -> (stage base of that rank, flags base of that rank)
+        for p, g in enumerate(ranks):
+            if p == r:
+                continue
+            base = _open_ipc(allh[g][0])
+            fl = _open_ipc(allh[g][2])
+            self._opened += [base, fl]
+            self.peer[p] = (base + allh[g][1], fl)
+        self.copy_stream = torch.cuda.Stream(device=self.dev, priority=-1)
+        self.ev_block = [torch.cuda.Event() for _ in range(N)]
+        self.ev_pushed = None     # the previous step's last push (gin reusable)
+        self.epoch = 0
+        self.srcs = (C.c_void_p * N)(*[
+            (gin[r].data_ptr() if p == r else self.stage_t[p].data_ptr()) for p in range(N)])
+        dist.barrier(group=group)
+
+    def order(self):
+        """Block order for this rank's GEMM: every peer's block first, in
+        the order (r + 1, r + 2, ...), its own block last."""
+        return [(self.rank + k) % self.N for k in range(1, self.N + 1)]
+
+    def begin(self, stream):
+        """Start of a step on the trainer stream: the previous step's pushes
+        must have read gin before the GEMMs overwrite it."""
+        self.epoch += 1
+        if self.ev_pushed is not None:
+            stream.wait_event(self.ev_pushed)
+
+    def pushed(self, j: int, stream):
+        """Block j of gin is complete on `stream`: push it to rank j."""
+        from . import _lib
+        if j == self.rank:
+            return
+        e, c = self.epoch, self.copy_stream
+        self.ev_block[j].record(stream)
+        c.wait_event(self.ev_block[j])
+        stage_j, flags_j = self.peer[j]
+        if e > 1:   # rank j's previous sum has read its slot for us
+            _lib.check(_lib.dvla_stream_wait_u32(self.flags.ptr + 4 * (32 + j), e - 1,
+                                                 c.cuda_stream), "dvla_stream_wait_u32")
+        _lib.check(_lib.dvla_memcpy_async(stage_j + self.rank * self.cs * 4,
+                                          self.gin[j].data_ptr(), self.cs * 4, c.cuda_stream),
+                   "dvla_memcpy_async")
+        _lib.check(_lib.dvla_stream_write_u32(flags_j + 4 * self.rank, e, c.cuda_stream),
+                   "dvla_stream_write_u32")
+        if j == self.order()[-2]:   # the last peer block of the step
+            ev = __import__("torch").cuda.Event()
+            ev.record(c)
+            self.ev_pushed = ev
+
+    def finish(self, stream, out, n_norm: int, div: float, sumsq, nonfinite, workspace):
+        """On `stream` (after this rank's own block): wait for every peer's
+        push, out = f32(f64 sum of the N blocks in node order), *sumsq =
+        sum of (out[:n_norm] / div)^2, then release the slots to the peers."""
+        from . import _lib
+        e, r = self.epoch, self.rank
+        for p in range(self.N):
+            if p != r:
+                _lib.check(_lib.dvla_stream_wait_u32(self.flags.ptr + 4 * p, e,
+                                                     stream.cuda_stream), "dvla_stream_wait_u32")
+        if out.numel() != self.cs or out.dtype != self.gin.dtype:
+            raise UsageError("the reduce-scatter output is one f32 block")
+        _lib.check(_lib.dvla_grad_sum_f32(self.srcs, self.N, int(n_norm), self.cs, float(div),
+                                          out.data_ptr(),
+                                          sumsq.data_ptr(), nonfinite.data_ptr(),
+                                          workspace.data_ptr(), stream.cuda_stream),
+                   "dvla_grad_sum_f32")
+        for p in range(self.N):
+            if p != r:
+                _lib.check(_lib.dvla_stream_write_u32(self.peer[p][1] + 4 * (32 + r), e,
+                                                      stream.cuda_stream),
+                           "dvla_stream_write_u32")
+
+    def close(self):
+        from . import _lib
+        import torch
+        torch.cuda.synchronize(self.dev)
+        for p in self._opened:
+            _lib.dvla_ipc_close(p)
+        self._opened = []
+        self.peer = {}

@@ -254,16 +254,39 @@ class GradReducer:
     nodes the ring wins (569 vs 400 GB/s busbw measured).  Single-node runs
     are a no-op, as in the reference."""
 
-    def __init__(self, nodes: int, group=None, exact: bool = False, backend: str = "nccl"):
+    def __init__(self, nodes: int, group=None, exact: bool = False, backend: str = "nccl",
+                 scatter: str = "auto"):
         if backend not in ("auto", "nccl", "nvls"):
             raise ConfigError(f"unknown gradient reduction backend {backend!r}")
         if exact and backend == "nvls":
             raise ConfigError("exact=True needs the NCCL f64 path")
+        if scatter not in ("auto", "peer", "nccl"):
+            raise ConfigError(f"unknown reduce-scatter transport {scatter!r}")
         self.nodes = nodes
         self.group = group
         self.exact = exact
         self.backend = backend
+        # TrainerWorker's ZeRO-1 reduce-scatter: "peer" = copy-engine pushes
+        # over NVLink overlapped with the gradient GEMM + a node-order f64 sum
+        # (exchange.PeerGradExchange); "nccl" = NCCL reduce_scatter after the
+        # GEMM; "auto" = peer when every rank is on this host's GPUs
+        self.scatter = scatter
         self._ar = None
+
+    def peer_scatter(self) -> bool:
+        """Collective: True when the ZeRO-1 reduce-scatter runs over peer
+        memory (scatter "peer", or "auto" with every rank on one host)."""
+        if self.scatter == "nccl" or self.nodes == 1:
+            return False
+        if self.scatter == "peer":
+            return True
+        import socket
+
+        import torch.distributed as dist
+        from .replicate import _gather_by_rank
+        hosts = set(_gather_by_rank(socket.gethostname(), self.group).values())
+        self.scatter = "peer" if len(hosts) == 1 else "nccl"
+        return self.scatter == "peer"
 
     def _use_nvls(self, grad) -> bool:
         if self.exact or self.backend == "nccl" or self.nodes == 1 or not grad.is_cuda:
@@ -620,6 +643,11 @@ class TrainerWorker:
             self.sumsq = torch.zeros(1, dtype=torch.float64, device=device)
             self._own_skip = torch.zeros(1, dtype=torch.float32, device=device)
             self.status_out = self._own_skip
+            self.exchange = None
+            if reducer.peer_scatter():
+                from .exchange import PeerGradExchange
+                self.exchange = PeerGradExchange(self.gin.view(nodes, self.cs), model_pool,
+                                                 group=reducer.group)
         else:
             # f32 gradient + the skip word (one all-reduce buffer), long-lived
             self.hg = model_pool.alloc((n + 1) * 4, align=256)
@@ -648,6 +676,14 @@ class TrainerWorker:
         # the initial weights / moments were written on the default stream,
         # which the worker's non-blocking streams do not order against
         torch.cuda.synchronize(device)
+
+    def close(self):
+        """Release the peer exchange's IPC mappings (collective with the
+        other learners when sharded)."""
+        ex = getattr(self, "exchange", None)
+        if ex is not None:
+            ex.close()
+            self.exchange = None
 
     def _acts(self, R, V, H):
         import torch
@@ -692,7 +728,9 @@ class TrainerWorker:
     def _grad_tail_sharded(self, s, ev_t, mx):
         """N learner GPUs, ZeRO-1 (reference runtime.py:788-796 arithmetic):
         dW row blocks as f32 GEMM outputs straight into the reduce-scatter
-        input -> NCCL reduce-scatter (sum) -> this rank's block / N -> global
+        input -> reduce-scatter (sum): copy-engine pushes over NVLink as the
+        blocks complete + a node-order f64 sum (exchange.PeerGradExchange),
+        or NCCL reduce_scatter -> this rank's block / N -> global
         norm (block sums of squares all-reduced) -> optimizer tail on the
         block (skipped on every rank when any rank's loss aborted: the skip
         words are summed with the gradient) -> NCCL all-gather of the bf16
@@ -705,23 +743,43 @@ class TrainerWorker:
         V, H, Vs = pol.V, pol.H, pol.Vs
         nloc = Vs * H
         gin2 = self.gin.view(nodes, self.cs)
-        for j in range(nodes):
+        ex = self.exchange
+        div = float(nodes)
+
+        def block(j):
             a, b = j * Vs, min(V, (j + 1) * Vs)
             if a < b:
                 torch.mm(self.dl[:, a:b].t(), self.feats_tok, out_dtype=torch.float32,
                          out=gin2[j, :(b - a) * H].view(b - a, H))
-        self.skip_in.copy_(self._own_skip.expand(nodes))
-        if ev_t is not None:
-            ev_t["grad1"].record(s)
-        dist.reduce_scatter_tensor(self.gshard, self.gin, op=dist.ReduceOp.SUM, group=grp)
-        if ev_t is not None:
-            ev_t["reduce1"].record(s)
+
+        if ex is not None:
+            # peer blocks first, each pushed by a copy engine as it completes,
+            # the own block last (it hides the final pushes); then the
+            # node-order sum + this block's sum of squares in one pass
+            ex.begin(s)
+            self.skip_in.copy_(self._own_skip.expand(nodes))
+            for j in ex.order():
+                block(j)
+                ex.pushed(j, s)
+            if ev_t is not None:
+                ev_t["grad1"].record(s)
+            ex.finish(s, self.gshard, nloc, div, self.sumsq, self.flags, self.norm_ws)
+            if ev_t is not None:
+                ev_t["reduce1"].record(s)
+        else:
+            for j in range(nodes):
+                block(j)
+            self.skip_in.copy_(self._own_skip.expand(nodes))
+            if ev_t is not None:
+                ev_t["grad1"].record(s)
+            dist.reduce_scatter_tensor(self.gshard, self.gin, op=dist.ReduceOp.SUM, group=grp)
+            if ev_t is not None:
+                ev_t["reduce1"].record(s)
+            _lib.check(_lib.dvla_grad_sumsq_f32(self.gshard.data_ptr(), nloc, div,
+                                                self.sumsq.data_ptr(), self.flags.data_ptr(),
+                                                self.norm_ws.data_ptr(), s.cuda_stream),
+                       "dvla_grad_sumsq_f32")
         g = self.gcfg
-        div = float(nodes)
-        _lib.check(_lib.dvla_grad_sumsq_f32(self.gshard.data_ptr(), nloc, div,
-                                            self.sumsq.data_ptr(), self.flags.data_ptr(),
-                                            self.norm_ws.data_ptr(), s.cuda_stream),
-                   "dvla_grad_sumsq_f32")
         dist.all_reduce(self.sumsq, op=dist.ReduceOp.SUM, group=grp)
         torch.sqrt(self.sumsq, out=self.norm)
         _lib.check(_lib.dvla_adam_tail_f32(

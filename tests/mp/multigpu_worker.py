@@ -124,16 +124,27 @@ def _zero1_matches_full_gradient(rank, world):
                 for k in range(cfg.n_groups)]
 
     out = {}
-    for name, red in (("zero1", GradReducer(world)), ("full", GradReducer(world, exact=True))):
+    for name, red in (("zero1", GradReducer(world)),
+                      ("zero1_nccl", GradReducer(world, scatter="nccl")),
+                      ("full", GradReducer(world, exact=True))):
         pool = Pool(PoolKind.MODEL_COMPUTE, 64 << 20, device=dev)
         tr = TrainerWorker(cfg, rank, pool, red, torch.cuda.Stream(device=dev), dev)
-        assert tr.sharded == (name == "zero1")
-        for step in range(2):
+        assert tr.sharded == name.startswith("zero1")
+        if tr.sharded:   # the default reduce-scatter is the peer exchange
+            assert (tr.exchange is not None) == (name == "zero1"), name
+        for step in range(3):
             tr.update(batches(step))
         torch.cuda.synchronize()
         out[name] = (tr.policy.w16.clone(), tr.policy.master.clone(), tr.policy)
+        tr.close()
     w_z, m_z, pol_z = out["zero1"]
     w_f, m_f, _ = out["full"]
+    # peer exchange (node-order f64 sum) vs NCCL reduce-scatter (f32 ring
+    # sum): the same update up to the sum's rounding
+    w_n, m_n, _ = out["zero1_nccl"]
+    dn = (m_z - m_n).abs()
+    assert float((dn > 1e-6).float().mean()) < 1e-3, float((dn > 1e-6).float().mean())
+    assert float((w_z.view(torch.int16) == w_n.view(torch.int16)).float().mean()) > 0.99
     # this rank's master block of the sharded learner vs the same rows of the
     # full one; the bf16 working copies everywhere
     Vs = pol_z.Vs

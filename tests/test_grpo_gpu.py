@@ -313,3 +313,45 @@ def test_grpo_loss_matches_golden_and_finite_differences(dev):
             fd[idx] = (grpo.grpo_loss(pu, batches, cfg) - grpo.grpo_loss(pd, batches, cfg)) / delta
         err = np.linalg.norm(fd - grad) / np.linalg.norm(grad)
         assert err < 1e-3, (tag, err)
+
+
+@pytest.mark.parametrize("n_src,n,extra", [(2, 1 << 20, 64), (4, 1_000_003 // 4 * 4, 64),
+                                           (3, 0, 64), (8, 4096, 0)])
+def test_grad_sum_is_the_node_order_f64_sum(dev, n_src, n, extra):
+    """dvla_grad_sum_f32 (the peer reduce-scatter's epilogue): out = f32 of
+    the f64 sum in source order (reference reduce_serial, runtime.py:618-627),
+    bit-exact; its sum of squares is bit-identical to dvla_grad_sumsq_f32 on
+    the output; the side words past n are summed but stay out of the norm."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2605_13276_b200 import _lib
+    n_all = n + extra
+    g = torch.Generator(device=dev).manual_seed(n_src * 7 + n)
+    srcs = [torch.randn(n_all, device=dev, generator=g) * (10.0 ** k) for k in range(n_src)]
+    out = torch.empty(n_all, device=dev)
+    ws = torch.empty(_lib.dvla_grad_norm_workspace_bytes(max(n, 1)), dtype=torch.uint8,
+                     device=dev)
+    ss, ss2 = (torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(2))
+    bad, bad2 = (torch.zeros(1, dtype=torch.int32, device=dev) for _ in range(2))
+    ptrs = (C.c_void_p * n_src)(*[t.data_ptr() for t in srcs])
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.check(_lib.dvla_grad_sum_f32(ptrs, n_src, n, n_all, 4.0, out.data_ptr(), ss.data_ptr(),
+                                      bad.data_ptr(), ws.data_ptr(), st), "dvla_grad_sum_f32")
+    want = np.zeros(n_all)
+    for t in srcs:
+        want += t.cpu().numpy().astype(np.float64)
+    assert np.array_equal(out.cpu().numpy(), want.astype(np.float32))
+    _lib.check(_lib.dvla_grad_sumsq_f32(out.data_ptr(), n, 4.0, ss2.data_ptr(), bad2.data_ptr(),
+                                        ws.data_ptr(), st), "dvla_grad_sumsq_f32")
+    assert float(ss) == float(ss2)
+    ref = float(((want.astype(np.float32)[:n].astype(np.float64) / 4.0) ** 2).sum())
+    assert float(ss) == pytest.approx(ref, rel=1e-12)
+    assert int(bad) == 0
+    if n:
+        srcs[-1][n // 2] = float("inf")
+        _lib.check(_lib.dvla_grad_sum_f32(ptrs, n_src, n, n_all, 1.0, out.data_ptr(),
+                                          ss.data_ptr(), bad.data_ptr(), ws.data_ptr(), st),
+                   "dvla_grad_sum_f32")
+        assert int(bad) == 1
