@@ -763,9 +763,10 @@ def _bench_learner_step(world, rank, dev, barrier, max_over_ranks, steps=10, war
     trainer = TrainerWorker(cfg, rank, model_pool, reducer, s_train, dev)
     sampler = SamplerWorker(cfg, rank, world, [env_pool], s_sample, dev)
     msgs, _ = sampler.run_epoch(0, trainer.snapshot())
-    names = ("start", "loss0", "loss1", "grad1", "reduce1", "end")
+    names = ("start", "loss0", "loss1", "grad1", "reduce1", "norm1", "adam1", "end")
     phases = {k: 0.0 for k in ("feats_logits_gemm", "loss", "grad_gemm_and_reduce",
-                               "reduce_wait", "norm_adam_tail")}
+                               "reduce_wait", "norm_adam_tail", "tail_norm", "tail_adam",
+                               "tail_gather")}
     for _ in range(warmup):
         trainer.update(msgs)
     barrier()
@@ -782,6 +783,9 @@ def _bench_learner_step(world, rank, dev, barrier, max_over_ranks, steps=10, war
         phases["grad_gemm_and_reduce"] += ev["loss1"].elapsed_time(ev["grad1"])
         phases["reduce_wait"] += ev["grad1"].elapsed_time(ev["reduce1"])
         phases["norm_adam_tail"] += ev["reduce1"].elapsed_time(ev["end"])
+        phases["tail_norm"] += ev["reduce1"].elapsed_time(ev["norm1"])
+        phases["tail_adam"] += ev["norm1"].elapsed_time(ev["adam1"])
+        phases["tail_gather"] += ev["adam1"].elapsed_time(ev["end"])
     trainer.timing = None
     barrier()
     dev_ms = max_over_ranks(sum(devs) / steps)

@@ -53,7 +53,7 @@ class PeerGradExchange:
         finish(s, out, div, sumsq, nonfinite, workspace)
     """
 
-    def __init__(self, gin, stage_pool, group=None):
+    def __init__(self, gin, stage_pool, group=None, wbuf=None):
         import torch
         import torch.distributed as dist
 
@@ -73,7 +73,8 @@ class PeerGradExchange:
         N, cs, r = self.N, self.cs, self.rank
         self.stage = _PoolRegion(stage_pool, N * cs * 4)
         self.stage_t = self.stage.t[: N * cs * 4].view(torch.float32).view(N, cs)
-        self.flags = _Slab(256, self.dev.index)   # ready[0:N) | ack[32:32+N)
+        # ready[0:N) | ack[32:32+N) | weights landed[64:64+N)
+        self.flags = _Slab(512, self.dev.index)
         self.flags.t.zero_()
         torch.cuda.synchronize(self.dev)
         if N > 32:
@@ -86,9 +87,22 @@ class PeerGradExchange:
         for g in ranks:
             if devs[g] != self.dev.index:
                 _lib.dvla_enable_peer_access(self.dev.index, devs[g])
-        allh = _gather_by_rank((self.stage.ipc(), self.stage.offset, self.flags.ipc()), group)
+        # the bf16 weights all-gathered after the optimizer tail (optional):
+        # [N * nloc] in the same pool, rank p's rows at p * nloc
+        self.wbuf = wbuf
+        w_off = None
+        if wbuf is not None:
+            slab = stage_pool._slab
+            w_off = wbuf.data_ptr() - slab.ptr
+            if (wbuf.dtype != torch.bfloat16 or wbuf.numel() % N or w_off < 0
+                    or w_off + wbuf.numel() * 2 > slab.nbytes):
+                raise UsageError("wbuf must be an [N * nloc] bf16 view inside the stage pool")
+            self.nloc = wbuf.numel() // N
+        allh = _gather_by_rank((self.stage.ipc(), self.stage.offset, self.flags.ipc(), w_off),
+                               group)
         self._opened = []
         self.peer = {}   # group rank -> (stage base of that rank, flags base of that rank)
+        self.peer_w = {}  # group rank -> that rank's wbuf
         for p, g in enumerate(ranks):
             if p == r:
                 continue
@@ -96,6 +110,8 @@ class PeerGradExchange:
             fl = _open_ipc(allh[g][2])
             self._opened += [base, fl]
             self.peer[p] = (base + allh[g][1], fl)
+            if allh[g][3] is not None:
+                self.peer_w[p] = base + allh[g][3]
         self.copy_stream = torch.cuda.Stream(device=self.dev, priority=-1)
         self.ev_block = [torch.cuda.Event() for _ in range(N)]
         self.ev_pushed = None     # the previous step's last push (gin reusable)
@@ -160,6 +176,45 @@ class PeerGradExchange:
                 _lib.check(_lib.dvla_stream_write_u32(self.peer[p][1] + 4 * (32 + r), e,
                                                       stream.cuda_stream),
                            "dvla_stream_write_u32")
+
+    def gather_chunk(self, lo: int, hi: int, stream):
+        """Elements [lo, hi) of this rank's weight rows are final on
+        `stream` (an optimizer-tail chunk): a copy engine pushes them into
+        every peer's wbuf while the next chunk is being stepped."""
+        from . import _lib
+        if self.wbuf is None:
+            raise UsageError("this exchange has no weight buffer")
+        if hi <= lo:
+            return
+        c = self.copy_stream
+        ev = __import__("torch").cuda.Event()
+        ev.record(stream)
+        c.wait_event(ev)
+        off = (self.rank * self.nloc + lo) * 2
+        src = self.wbuf.data_ptr() + off
+        for k in range(1, self.N):
+            p = (self.rank + k) % self.N
+            _lib.check(_lib.dvla_memcpy_async(self.peer_w[p] + off, src, (hi - lo) * 2,
+                                              c.cuda_stream), "dvla_memcpy_async")
+
+    def gather_finish(self, stream):
+        """After the last gather_chunk: tell every peer this rank's rows
+        landed, then make `stream` wait until this rank's pushes are done
+        and every peer's rows have landed here."""
+        from . import _lib
+        torch = __import__("torch")
+        e, r, c = self.epoch, self.rank, self.copy_stream
+        for p in range(self.N):
+            if p != r:
+                _lib.check(_lib.dvla_stream_write_u32(self.peer[p][1] + 4 * (64 + r), e,
+                                                      c.cuda_stream), "dvla_stream_write_u32")
+        ev = torch.cuda.Event()
+        ev.record(c)
+        stream.wait_event(ev)
+        for p in range(self.N):
+            if p != r:
+                _lib.check(_lib.dvla_stream_wait_u32(self.flags.ptr + 4 * (64 + p), e,
+                                                     stream.cuda_stream), "dvla_stream_wait_u32")
 
     def close(self):
         from . import _lib

@@ -31,6 +31,7 @@ from __future__ import annotations
 import contextlib
 import logging
 import math
+import os
 import threading
 import time
 from dataclasses import dataclass, field
@@ -647,7 +648,10 @@ class TrainerWorker:
             if reducer.peer_scatter():
                 from .exchange import PeerGradExchange
                 self.exchange = PeerGradExchange(self.gin.view(nodes, self.cs), model_pool,
-                                                 group=reducer.group)
+                                                 group=reducer.group, wbuf=self.policy.w16pad)
+                # optimizer-tail chunks whose bf16 rows are pushed to the peers
+                # while the next chunk is stepped (the all-gather, overlapped)
+                self.gather_chunks = int(os.environ.get("DVLA_GATHER_CHUNKS", "4"))
         else:
             # f32 gradient + the skip word (one all-reduce buffer), long-lived
             self.hg = model_pool.alloc((n + 1) * 4, align=256)
@@ -719,11 +723,15 @@ class TrainerWorker:
         _lib.check(_lib.dvla_grad_norm_f32(self.gbuf.data_ptr(), n, 1.0, self.norm.data_ptr(),
                                            self.flags.data_ptr(), self.norm_ws.data_ptr(),
                                            s.cuda_stream), "dvla_grad_norm_f32")
+        if ev_t is not None and "norm1" in ev_t:
+            ev_t["norm1"].record(s)
         _lib.check(_lib.dvla_adam_tail_f32(
             pol.master.data_ptr(), self.gbuf.data_ptr(), pol.m.data_ptr(), pol.v.data_ptr(),
             n, pol.step + 1, g.lr, g.beta1, g.beta2, g.opt_eps, 1.0, self.norm.data_ptr(), mx,
             self.skip.data_ptr(), pol.w16.data_ptr(), self.flags.data_ptr() + 4,
             s.cuda_stream), "dvla_adam_tail_f32")
+        if ev_t is not None and "adam1" in ev_t:
+            ev_t["adam1"].record(s)
 
     def _grad_tail_sharded(self, s, ev_t, mx):
         """N learner GPUs, ZeRO-1 (reference runtime.py:788-796 arithmetic):
@@ -782,12 +790,33 @@ class TrainerWorker:
         g = self.gcfg
         dist.all_reduce(self.sumsq, op=dist.ReduceOp.SUM, group=grp)
         torch.sqrt(self.sumsq, out=self.norm)
-        _lib.check(_lib.dvla_adam_tail_f32(
-            pol.master.data_ptr(), self.gshard.data_ptr(), pol.m.data_ptr(), pol.v.data_ptr(),
-            nloc, pol.step + 1, g.lr, g.beta1, g.beta2, g.opt_eps, div, self.norm.data_ptr(), mx,
-            self.skip.data_ptr(), pol.w16_own.data_ptr(), self.flags.data_ptr() + 4,
-            s.cuda_stream), "dvla_adam_tail_f32")
-        dist.all_gather_into_tensor(pol.w16pad, pol.w16_own, group=grp)
+        if ev_t is not None and "norm1" in ev_t:
+            ev_t["norm1"].record(s)
+
+        def adam(lo, hi):
+            _lib.check(_lib.dvla_adam_tail_f32(
+                pol.master.data_ptr() + 4 * lo, self.gshard.data_ptr() + 4 * lo,
+                pol.m.data_ptr() + 8 * lo, pol.v.data_ptr() + 8 * lo, hi - lo, pol.step + 1,
+                g.lr, g.beta1, g.beta2, g.opt_eps, div, self.norm.data_ptr(), mx,
+                self.skip.data_ptr(), pol.w16_own.data_ptr() + 2 * lo, self.flags.data_ptr() + 4,
+                s.cuda_stream), "dvla_adam_tail_f32")
+
+        if ex is not None and ex.wbuf is not None:
+            # the all-gather as copy-engine pushes of each stepped chunk
+            k = max(1, self.gather_chunks)
+            step = max(64, (-(-nloc // k) + 63) // 64 * 64)   # 64-element aligned chunks
+            for lo in range(0, nloc, step):
+                hi = min(nloc, lo + step)
+                adam(lo, hi)
+                ex.gather_chunk(lo, hi, s)
+            if ev_t is not None and "adam1" in ev_t:
+                ev_t["adam1"].record(s)
+            ex.gather_finish(s)
+        else:
+            adam(0, nloc)
+            if ev_t is not None and "adam1" in ev_t:
+                ev_t["adam1"].record(s)
+            dist.all_gather_into_tensor(pol.w16pad, pol.w16_own, group=grp)
         dist.all_reduce(self.flags, op=dist.ReduceOp.MAX, group=grp)
 
     def update(self, batches: list, transport_nodes: int | None = None) -> dict:

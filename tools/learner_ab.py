@@ -1,6 +1,6 @@
 """A/B of the ZeRO-1 reduce-scatter transports inside the timed learner step
 (bench._bench_learner_step), alternated REPS times under torchrun:
-python -m torch.distributed.run --nproc-per-node N tools/learner_ab.py [REPS]"""
+python -m torch.distributed.run --nproc-per-node N tools/learner_ab.py [REPS] [scatter:chunks,...]"""
 import json
 import os
 import sys
@@ -30,11 +30,16 @@ def mor(x):
     return float(t)
 
 
+variants = [("peer", "4"), ("peer", "1"), ("nccl", "4")]
+if len(sys.argv) > 2:
+    variants = [tuple(v.split(":")) for v in sys.argv[2].split(",")]
 for rep in range(reps):
-    for sc in ("peer", "nccl"):
+    for sc, gc in variants:
+        os.environ["DVLA_GATHER_CHUNKS"] = gc
         out = bench._bench_learner_step(world, rank, dev, barrier, mor, scatter=sc)
         if rank == 0:
-            print(json.dumps({"rep": rep, "scatter": sc, "value": round(out["value"]),
+            print(json.dumps({"rep": rep, "scatter": sc, "gather_chunks": gc,
+                              "value": round(out["value"]),
                               "ms_wall": round(out["ms_per_step_wall"], 3),
                               "ms_dev": round(out["ms_per_step_device"], 3),
                               "phases": out["phases_ms_rank0"]}), flush=True)
