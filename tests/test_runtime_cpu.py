@@ -7,7 +7,7 @@ import threading
 import numpy as np
 import pytest
 
-from paper_2605_13276_b200.core import ParamSnapshot
+from paper_2605_13276_b200.core import ConfigError, ParamSnapshot
 from paper_2605_13276_b200.runtime import GradReducer, Monitor, VersionBoard
 
 
@@ -70,6 +70,11 @@ def _reduce_worker(rank, world, port, q):
     g = torch.tensor([1.0 + rank, 1e-9 * (rank + 1), -3.0], dtype=torch.float64)
     out_fast = GradReducer(world).reduce(g.clone())
     out_exact = GradReducer(world, exact=True).reduce(g.clone())
+    # ZeRO-1 transport choice: collective, peer memory when every rank is on
+    # this host, NCCL when asked
+    peer = (GradReducer(world).peer_scatter(), GradReducer(world, scatter="nccl").peer_scatter(),
+            GradReducer(world, scatter="peer").peer_scatter())
+    assert peer == (True, False, True), peer
     q.put((rank, out_fast.numpy().tolist(), out_exact.numpy().tolist()))
     dist.destroy_process_group()
 
@@ -302,6 +307,9 @@ def test_grad_reducer_reference_signatures():
     np.testing.assert_array_equal(got_t.numpy(), want)
     with pytest.raises(TypeError):
         r.reduce(1, 2)
+    with pytest.raises(ConfigError, match="reduce-scatter transport"):
+        GradReducer(2, scatter="ring")
+    assert not GradReducer(1).peer_scatter()
 
 
 def test_retire_waits_for_a_newer_install_and_blocks_stale_deposits():
