@@ -439,6 +439,7 @@ def _learner(cfg, rank, L, Rr, assign, k, lgroup, model_pool, chans, rep, store,
         th.join()
         if lead:
             store.set(key("pub", trainer.version + 1), "end")
+        trainer.close()
     res.epochs = cfg.epochs
     n_traj_all = len(Rr) * cfg.n_groups * cfg.group_size
     if len(t_pub) > 1:

@@ -217,10 +217,11 @@ class PeerGradExchange:
                                                      stream.cuda_stream), "dvla_stream_wait_u32")
 
     def close(self):
-        from . import _lib
         import torch
+
+        from .replicate import _close_ipc
         torch.cuda.synchronize(self.dev)
         for p in self._opened:
-            _lib.dvla_ipc_close(p)
+            _close_ipc(p)
         self._opened = []
         self.peer = {}

@@ -172,11 +172,38 @@ class _PoolRegion:
         return buf.raw
 
 
+_IPC_OPEN = {}   # handle bytes -> [mapped pointer, references] (one mapping per process)
+_IPC_PTR = {}    # mapped pointer -> handle bytes
+
+
 def _open_ipc(handle: bytes) -> int:
+    """Map a peer allocation (CUDA IPC).  A process may map an allocation
+    only once (cudaIpcOpenMemHandle refuses a second mapping), so mappings
+    are shared and reference-counted: every _open_ipc pairs with one
+    _close_ipc."""
     from . import _lib
+    ent = _IPC_OPEN.get(handle)
+    if ent is not None:
+        ent[1] += 1
+        return ent[0]
     p = C.c_void_p()
     _lib.check(_lib.dvla_ipc_open(handle, C.byref(p)), "dvla_ipc_open")
+    _IPC_OPEN[handle] = [p.value, 1]
+    _IPC_PTR[p.value] = handle
     return p.value
+
+
+def _close_ipc(ptr: int) -> None:
+    from . import _lib
+    handle = _IPC_PTR.get(ptr)
+    if handle is None:
+        _lib.dvla_ipc_close(ptr)
+        return
+    ent = _IPC_OPEN[handle]
+    ent[1] -= 1
+    if ent[1] == 0:
+        del _IPC_OPEN[handle], _IPC_PTR[ptr]
+        _lib.dvla_ipc_close(ptr)
 
 
 class LocalChain:
@@ -377,7 +404,7 @@ class ChainReplicator:
         from . import _lib
         for p in set(self._opened + [self.next_flags]):
             if p:
-                _lib.dvla_ipc_close(p)
+                _close_ipc(p)
         self._opened = []
         self.next_buf = self.next_flags = None
         self.fan_bufs = []
@@ -730,9 +757,9 @@ class SplitReplicator:
     def close(self):
         from . import _lib
         for p in self._opened:
-            _lib.dvla_ipc_close(p)
+            _close_ipc(p)
         for _, fp in self.peer.values():
-            _lib.dvla_ipc_close(fp)
+            _close_ipc(fp)
         self.peer = {}
         self._opened = []
 

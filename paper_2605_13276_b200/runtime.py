@@ -1119,16 +1119,21 @@ def run_swimlane(cfg: SwimlaneConfig, device=None, group=None, poison_epochs=fro
         (dist_lane, "dist"))]
     for t in lanes:
         t.start()
-    while any(t.is_alive() for t in lanes):
-        time.sleep(0.05)
-        stale = monitor.stale_lanes(cfg.watchdog_s)
-        if stale:
-            monitor.fail(f"watchdog: lanes silent for > {cfg.watchdog_s}s", stale[0], -1)
-        if abort.is_set():
-            for t in lanes:
-                t.join(timeout=2.0)
-            raise RunAbort(monitor.abort_reason or "aborted", lane=monitor.abort_lane,
-                           epoch=monitor.abort_epoch, lane_states=monitor.dump())
+    try:
+        while any(t.is_alive() for t in lanes):
+            time.sleep(0.05)
+            stale = monitor.stale_lanes(cfg.watchdog_s)
+            if stale:
+                monitor.fail(f"watchdog: lanes silent for > {cfg.watchdog_s}s", stale[0], -1)
+            if abort.is_set():
+                for t in lanes:
+                    t.join(timeout=2.0)
+                raise RunAbort(monitor.abort_reason or "aborted", lane=monitor.abort_lane,
+                               epoch=monitor.abort_epoch, lane_states=monitor.dump())
+    finally:
+        # the learners' peer-memory mappings (a later run may be handed the
+        # same peer allocations: an open mapping would collide)
+        trainer.close()
     torch.cuda.synchronize(dev)
     result.wall = time.perf_counter() - t_start
     result.staleness_max = board.staleness_max
