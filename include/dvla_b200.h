@@ -396,6 +396,12 @@ int dvla_nccl_destroy(void);
  * cuStreamWriteValue32 with a memory barrier). */
 int dvla_stream_wait_u32(const uint32_t* addr, uint32_t value, void* stream);
 int dvla_stream_write_u32(uint32_t* addr, uint32_t value, void* stream);
+/* Stream-ordered wait until flags[i] >= target for every bit i set in mask
+ * (i < 32), acquire-polled by one warp; after timeout_ns *err_dev |= 1 and
+ * the stream goes on (the peer exchange's bounded waits: a dead peer is an
+ * error the host reads after its sync, not a hung stream). */
+int dvla_wait_flags_u32(const uint32_t* flags, uint32_t mask, uint32_t target,
+                        uint64_t timeout_ns, uint32_t* err_dev, void* stream);
 
 /* ---- switch-multicast (NVLS) replication ---------------------------------
  * Replaces the same ControlPlane.broadcast -> WeightMailbox.deliver data path

@@ -475,6 +475,36 @@ extern "C" int dvla_stream_wait_u32(const uint32_t* addr, uint32_t value, void* 
   return DVLA_OK;
 }
 
+// Stream-ordered wait on several peer-written flags with a timeout (the
+// bounded form of cuStreamWaitValue32): lane i of one warp acquire-polls
+// flags[i] while bit i of `mask` is set, until flags[i] >= target; on
+// timeout it sets *err and returns, so a dead peer surfaces as an error
+// instead of a hung stream.
+__global__ void wait_flags_kernel(const uint32_t* flags, uint32_t mask, uint32_t target,
+                                  uint64_t timeout_ns, uint32_t* err) {
+  const int i = threadIdx.x;
+  if (!((mask >> i) & 1u)) return;
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t ns = 32;
+  while (ld_acquire_sys(flags + i) < target) {
+    __nanosleep(ns);
+    if (ns < 1024) ns <<= 1;
+    if (globaltimer_ns() - t0 > timeout_ns) {
+      atomicOr(err, 1u);
+      return;
+    }
+  }
+}
+
+extern "C" int dvla_wait_flags_u32(const uint32_t* flags, uint32_t mask, uint32_t target,
+                                   uint64_t timeout_ns, uint32_t* err_dev, void* stream) {
+  if (!flags || !err_dev) return fail(DVLA_ERR_USAGE, "null argument");
+  if (!mask) return DVLA_OK;
+  wait_flags_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(flags, mask, target,
+                                                                     timeout_ns, err_dev);
+  return launch_check("wait_flags_kernel");
+}
+
 extern "C" int dvla_stream_write_u32(uint32_t* addr, uint32_t value, void* stream) {
   if (!addr) return fail(DVLA_ERR_USAGE, "null flag address");
   if (int rc = drv_check()) return rc;

@@ -30,13 +30,15 @@ the copy-engine replication chain, replicate.SplitReplicator):
                                 (written by j's trainer stream)
 so a push of step e + 1 never overwrites a slot before the step-e sum read
 it, and a GEMM of step e + 1 never overwrites a block before its step-e push
-(a local event).  Stream waits have no timeout: a rank that stops issuing
-steps stalls its peers, as an NCCL collective would.
+(a local event).  The flag waits are bounded (`dvla_wait_flags_u32`, one
+polling warp per wait): a peer that stops arriving sets an error word after
+the timeout instead of hanging the stream.
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 from .core import UsageError
 
@@ -53,7 +55,8 @@ class PeerGradExchange:
         finish(s, out, div, sumsq, nonfinite, workspace)
     """
 
-    def __init__(self, gin, stage_pool, group=None, wbuf=None):
+    def __init__(self, gin, stage_pool, group=None, wbuf=None, err=None,
+                 timeout_s: float | None = None):
         import torch
         import torch.distributed as dist
 
@@ -113,6 +116,15 @@ class PeerGradExchange:
             if allh[g][3] is not None:
                 self.peer_w[p] = base + allh[g][3]
         self.copy_stream = torch.cuda.Stream(device=self.dev, priority=-1)
+        # bounded waits: a peer that stops arriving sets this word (device
+        # int32; the caller's, e.g. a slot of TrainerWorker's flags that is
+        # max-reduced and read after its one sync) instead of hanging
+        self.err = err if err is not None else torch.zeros(1, dtype=torch.int32,
+                                                           device=self.dev)
+        if timeout_s is None:
+            timeout_s = float(os.environ.get("DVLA_EXCHANGE_TIMEOUT_S", "120"))
+        self.timeout_ns = int(timeout_s * 1e9)
+        self.peer_mask = ((1 << N) - 1) & ~(1 << r)
         self.ev_block = [torch.cuda.Event() for _ in range(N)]
         self.ev_pushed = None     # the previous step's last push (gin reusable)
         self.epoch = 0
@@ -127,10 +139,20 @@ class PeerGradExchange:
 
     def begin(self, stream):
         """Start of a step on the trainer stream: the previous step's pushes
-        must have read gin before the GEMMs overwrite it."""
+        must have read gin before the GEMMs overwrite it, and (copy stream)
+        every peer's previous sum must have read its slot for this rank
+        before this step's pushes overwrite it."""
         self.epoch += 1
         if self.ev_pushed is not None:
             stream.wait_event(self.ev_pushed)
+        if self.epoch > 1:
+            self._wait(32, self.epoch - 1, self.copy_stream)
+
+    def _wait(self, word: int, target: int, stream):
+        from . import _lib
+        _lib.check(_lib.dvla_wait_flags_u32(self.flags.ptr + 4 * word, self.peer_mask, target,
+                                            self.timeout_ns, self.err.data_ptr(),
+                                            stream.cuda_stream), "dvla_wait_flags_u32")
 
     def pushed(self, j: int, stream):
         """Block j of gin is complete on `stream`: push it to rank j."""
@@ -141,9 +163,6 @@ class PeerGradExchange:
         self.ev_block[j].record(stream)
         c.wait_event(self.ev_block[j])
         stage_j, flags_j = self.peer[j]
-        if e > 1:   # rank j's previous sum has read its slot for us
-            _lib.check(_lib.dvla_stream_wait_u32(self.flags.ptr + 4 * (32 + j), e - 1,
-                                                 c.cuda_stream), "dvla_stream_wait_u32")
         _lib.check(_lib.dvla_memcpy_async(stage_j + self.rank * self.cs * 4,
                                           self.gin[j].data_ptr(), self.cs * 4, c.cuda_stream),
                    "dvla_memcpy_async")
@@ -160,10 +179,7 @@ class PeerGradExchange:
         sum of (out[:n_norm] / div)^2, then release the slots to the peers."""
         from . import _lib
         e, r = self.epoch, self.rank
-        for p in range(self.N):
-            if p != r:
-                _lib.check(_lib.dvla_stream_wait_u32(self.flags.ptr + 4 * p, e,
-                                                     stream.cuda_stream), "dvla_stream_wait_u32")
+        self._wait(0, e, stream)
         if out.numel() != self.cs or out.dtype != self.gin.dtype:
             raise UsageError("the reduce-scatter output is one f32 block")
         _lib.check(_lib.dvla_grad_sum_f32(self.srcs, self.N, int(n_norm), self.cs, float(div),
@@ -211,10 +227,14 @@ class PeerGradExchange:
         ev = torch.cuda.Event()
         ev.record(c)
         stream.wait_event(ev)
-        for p in range(self.N):
-            if p != r:
-                _lib.check(_lib.dvla_stream_wait_u32(self.flags.ptr + 4 * (64 + p), e,
-                                                     stream.cuda_stream), "dvla_stream_wait_u32")
+        self._wait(64, e, stream)
+
+    def check(self):
+        """Host side, after the stream has been synchronised: raise if a
+        bounded wait timed out."""
+        if int(self.err.item()):
+            from ._lib import ReplicationTimeout
+            raise ReplicationTimeout(f"rank {self.rank}: peer gradient exchange timed out")
 
     def close(self):
         import torch

@@ -668,10 +668,13 @@ class TrainerWorker:
         self.norm_ws = torch.empty(_lib.dvla_grad_norm_workspace_bytes(n), dtype=torch.uint8,
                                    device=device)
         self.norm = torch.zeros(1, dtype=torch.float64, device=device)
-        self.flags = torch.zeros(2, dtype=torch.int32, device=device)  # grad / param non-finite
+        # grad / param non-finite, peer-exchange timeout (max-reduced over learners)
+        self.flags = torch.zeros(3, dtype=torch.int32, device=device)
+        if getattr(self, "exchange", None) is not None:
+            self.exchange.err = self.flags[2:3]
         self.h_stats = torch.empty(_lib.ST_LEN, dtype=torch.float64, pin_memory=True)
         self.h_misc = torch.empty(2, dtype=torch.float64, pin_memory=True)  # norm, skip
-        self.h_flags = torch.empty(2, dtype=torch.int32, pin_memory=True)
+        self.h_flags = torch.empty(3, dtype=torch.int32, pin_memory=True)
         self.h_skip = torch.empty(1, dtype=torch.float32, pin_memory=True)
         self.version = 0
         self.done_event = None
@@ -878,6 +881,9 @@ class TrainerWorker:
         if ev_t is not None:
             ev_t["host_enqueue_s"] = t_enq - t0
             ev_t["host_wait_s"] = time.perf_counter() - t_enq
+        if bool(self.h_flags[2]):
+            raise RunAbort("peer gradient exchange timed out (a learner stopped arriving)",
+                           lane=LaneId.TRAINER.value, epoch=self.version)
         sv = self.h_stats.numpy().copy()
         skipped = float(self.h_skip[0]) != 0.0
         grad_bad = bool(self.h_flags[0])

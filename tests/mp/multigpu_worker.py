@@ -162,6 +162,40 @@ def _zero1_matches_full_gradient(rank, world):
     dist.barrier()
 
 
+def _exchange_timeout(rank, world):
+    """The peer exchange's waits are bounded: when the other learners never
+    push, rank 0's sum wait times out, sets the error word and the stream
+    goes on (ReplicationTimeout on check(), no hung stream)."""
+    from paper_2605_13276_b200._lib import ReplicationTimeout
+    from paper_2605_13276_b200.exchange import PeerGradExchange
+    from paper_2605_13276_b200.pools import Pool, PoolKind
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cs = 4096
+    pool = Pool(PoolKind.MODEL_COMPUTE, (world + 1) * cs * 4 * 2 + (1 << 20), device=dev)
+    gin = torch.ones(world, cs, device=dev)
+    ex = PeerGradExchange(gin, pool, timeout_s=0.5)
+    s = torch.cuda.current_stream()
+    if rank == 0:
+        out = torch.empty(cs, device=dev)
+        sq = torch.zeros(1, dtype=torch.float64, device=dev)
+        bad = torch.zeros(1, dtype=torch.int32, device=dev)
+        import paper_2605_13276_b200._lib as L
+        ws = torch.empty(L.dvla_grad_norm_workspace_bytes(cs), dtype=torch.uint8, device=dev)
+        ex.begin(s)
+        for j in ex.order():
+            ex.pushed(j, s)
+        ex.finish(s, out, cs, 1.0, sq, bad, ws)
+        torch.cuda.synchronize()
+        try:
+            ex.check()
+            raise AssertionError("the exchange wait did not time out")
+        except ReplicationTimeout:
+            pass
+    dist.barrier()
+    ex.close()
+    dist.barrier()
+
+
 def main():
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -356,6 +390,9 @@ def main():
     _zero1_matches_full_gradient(rank, world)
     if rank == 0:
         print("ZERO1_OK", flush=True)
+    _exchange_timeout(rank, world)
+    if rank == 0:
+        print("EXCHANGE_TIMEOUT_OK", flush=True)
 
     # (4) swimlane, topology replication with NCCL grad mean: every rank
     # ends with bitwise-identical master weights and bf16 working copies

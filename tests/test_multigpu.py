@@ -28,7 +28,8 @@ def test_multigpu_worker():
            os.path.join(here, "mp", "multigpu_worker.py")]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
-    for tag in ("SHARDED_LOSS_OK", "ZERO1_OK", "SWIMLANE_WEIGHTS_EQUAL_OK", "PEER_CHANNEL_OK",
+    for tag in ("SHARDED_LOSS_OK", "ZERO1_OK", "EXCHANGE_TIMEOUT_OK", "SWIMLANE_WEIGHTS_EQUAL_OK",
+                "PEER_CHANNEL_OK",
                 "MULTIGPU_OK"):
         assert tag in res.stdout, tag
 
