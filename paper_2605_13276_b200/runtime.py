@@ -586,10 +586,13 @@ class TrainerWorker:
       per-token features -> logits GEMM (cuBLAS, bf16 weights kept by the
       optimizer tail) -> fused token loss fwd+bwd (csrc/token_loss.cu) ->
       skip word (loss abort) -> head gradient dW = dl^T feats as f32 GEMM
-      output -> with N learners (NCCL): ZeRO-1, the gradient's row blocks
+      output -> with N learners: ZeRO-1, the gradient's row blocks
       reduce-scattered together with every rank's skip word (so one rank's
-      abort skips the step on every rank), this rank's block stepped, the
-      bf16 blocks all-gathered; with the switch-reduced / exact reducers: the
+      abort skips the step on every rank) -- by copy-engine pushes over
+      NVLink as the blocks complete (exchange.PeerGradExchange) or NCCL --
+      this rank's block stepped, the bf16 blocks all-gathered (pushed chunk
+      by chunk behind the optimizer tail, or NCCL); with the switch-reduced
+      / exact reducers: the
       mean of the whole gradient -> grad norm of the mean -> optimizer tail
       (clip, Adam, bf16 copy, non-finite flag; skipped on the device on
       abort or a non-finite gradient).  (GradReducer.reduce_async keeps a
