@@ -807,6 +807,7 @@ def _bench_learner_step(world, rank, dev, barrier, max_over_ranks, steps=10, war
                              "frac_step": round(flops / (dev_ms / 1e3) / 1e12 / tf_peak, 4)},
            "config": f"V={V} x H={SWIM_H} bf16 head, {N_GROUPS}x{G} traj x {T} tokens per GPU; "
                      f"grad f32 {n * 4 / 1e9:.2f} GB reduce-scattered over {world} GPU(s)",
+           "grad_gemms_per_block": getattr(trainer, "grad_sub", 1),
            "reduce_scatter": (("peer: copy-engine pushes over NVLink overlapped with the "
                                "gradient GEMM + node-order f64 sum (exchange.PeerGradExchange)")
                               if getattr(trainer, "exchange", None) is not None else

@@ -667,6 +667,9 @@ class TrainerWorker:
         act_bytes = R * (2 * V * 2 + H * 2) + (4 << 20)
         self.act_pool = act_pool or Pool(PoolKind.ENV_AUX, act_bytes, device=device)
         self._acts(R, V, H)
+        # GEMMs per owner block of the head gradient (DVLA_GRAD_SUB; DESIGN §6:
+        # at 4 learners two per block measured 0.15 ms faster, at 2 one)
+        self.grad_sub = max(1, int(os.environ.get("DVLA_GRAD_SUB", "1")))
         self.pos = token_positions(cfg, device)
         self.norm_ws = torch.empty(_lib.dvla_grad_norm_workspace_bytes(n), dtype=torch.uint8,
                                    device=device)
@@ -739,6 +742,23 @@ class TrainerWorker:
         if ev_t is not None and "adam1" in ev_t:
             ev_t["adam1"].record(s)
 
+    def _grad_block(self, j: int, sub: int | None = None):
+        """Rows of rank j's block of dW = dl^T x (f32 GEMM output into the
+        reduce-scatter input), as `sub` row-split GEMMs."""
+        import torch
+        pol = self.policy
+        V, H, Vs = pol.V, pol.H, pol.Vs
+        a, b = j * Vs, min(V, (j + 1) * Vs)
+        if a >= b:
+            return
+        sub = self.grad_sub if sub is None else sub
+        gin2 = self.gin.view(self.reducer.nodes, self.cs)
+        step = max(128, (-(-(b - a) // sub) + 127) // 128 * 128)
+        for a2 in range(a, b, step):
+            b2 = min(b, a2 + step)
+            torch.mm(self.dl[:, a2:b2].t(), self.feats_tok, out_dtype=torch.float32,
+                     out=gin2[j, (a2 - a) * H:(b2 - a) * H].view(b2 - a2, H))
+
     def _grad_tail_sharded(self, s, ev_t, mx):
         """N learner GPUs, ZeRO-1 (reference runtime.py:788-796 arithmetic):
         dW row blocks as f32 GEMM outputs straight into the reduce-scatter
@@ -754,17 +774,10 @@ class TrainerWorker:
 
         from . import _lib
         pol, nodes, grp = self.policy, self.reducer.nodes, self.reducer.group
-        V, H, Vs = pol.V, pol.H, pol.Vs
-        nloc = Vs * H
-        gin2 = self.gin.view(nodes, self.cs)
+        nloc = pol.Vs * pol.H
         ex = self.exchange
         div = float(nodes)
-
-        def block(j):
-            a, b = j * Vs, min(V, (j + 1) * Vs)
-            if a < b:
-                torch.mm(self.dl[:, a:b].t(), self.feats_tok, out_dtype=torch.float32,
-                         out=gin2[j, :(b - a) * H].view(b - a, H))
+        block = self._grad_block
 
         if ex is not None:
             # peer blocks first, each pushed by a copy engine as it completes,
