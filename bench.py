@@ -771,6 +771,7 @@ def _bench_learner_step(world, rank, dev, barrier, max_over_ranks, steps=10, war
         trainer.update(msgs)
     barrier()
     walls, devs = [], []
+    host = {"enqueue": 0.0, "wait": 0.0, "wall": 0.0}
     for _ in range(steps):
         ev = {k: torch.cuda.Event(enable_timing=True) for k in names}
         trainer.timing = ev
@@ -778,6 +779,9 @@ def _bench_learner_step(world, rank, dev, barrier, max_over_ranks, steps=10, war
         trainer.update(msgs)       # ends with its one host sync
         walls.append(time.perf_counter() - t0)
         devs.append(ev["start"].elapsed_time(ev["end"]))
+        host["enqueue"] += 1e3 * ev.get("host_enqueue_s", 0.0)
+        host["wait"] += 1e3 * ev.get("host_wait_s", 0.0)
+        host["wall"] += 1e3 * walls[-1]
         phases["feats_logits_gemm"] += ev["start"].elapsed_time(ev["loss0"])
         phases["loss"] += ev["loss0"].elapsed_time(ev["loss1"])
         phases["grad_gemm_and_reduce"] += ev["loss1"].elapsed_time(ev["grad1"])
@@ -800,6 +804,10 @@ def _bench_learner_step(world, rank, dev, barrier, max_over_ranks, steps=10, war
            "value": world * N_GROUPS * G / (wall_ms / 1e3), "unit": UNIT,
            "ms_per_step_wall": wall_ms, "ms_per_step_device": dev_ms,
            "phases_ms_rank0": {k: round(v / steps, 4) for k, v in phases.items()},
+           "host_ms_rank0": {"enqueue": round(host["enqueue"] / steps, 4),
+                             "wait_for_device": round(host["wait"] / steps, 4),
+                             "after_sync": round((host["wall"] - host["enqueue"] - host["wait"])
+                                                 / steps, 4)},
            "gemm_tflop_per_step": flops / 1e12,
            "gemm_roofline": {"bound": "tensor", "peak_tflops": tf_peak,
                              "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",

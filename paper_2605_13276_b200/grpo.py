@@ -204,7 +204,10 @@ def canonical_order(group_ids) -> np.ndarray:
 def _mean_reward(rewards_2d: np.ndarray, order: np.ndarray) -> float:
     """float(np.mean([b.rewards.mean() for b in batches])) in canonical order
     (reference grpo.py:291); host f32 arithmetic, bit-identical."""
-    per = [np.asarray(rewards_2d[k], dtype=np.float32).mean() for k in order]
+    # one row-wise reduction over the groups in canonical order: numpy's
+    # per-row pairwise f32 sums, bit-identical to the per-group .mean()
+    # (tests/test_oracle.py), without a Python loop over the groups
+    per = np.asarray(rewards_2d, dtype=np.float32)[np.asarray(order)].mean(axis=1)
     return float(np.mean(per))
 
 
@@ -227,7 +230,7 @@ def stats_from_vector(sv: np.ndarray, group_ids: np.ndarray, order: np.ndarray,
         "n_traj": int(n_traj),
         "n_groups": int(len(group_ids)),
         "n_chunks": n_chunks,
-        "group_ids": [int(group_ids[k]) for k in order],
+        "group_ids": np.asarray(group_ids, dtype=np.int64)[np.asarray(order)].tolist(),
     }
     if rewards_2d is not None:
         out["mean_reward"] = _mean_reward(rewards_2d, order)

@@ -682,6 +682,7 @@ class TrainerWorker:
         self.h_misc = torch.empty(2, dtype=torch.float64, pin_memory=True)  # norm, skip
         self.h_flags = torch.empty(3, dtype=torch.int32, pin_memory=True)
         self.h_skip = torch.empty(1, dtype=torch.float32, pin_memory=True)
+        self.h_rw = None
         self.version = 0
         self.done_event = None
         self.timing = None  # optional: dict of CUDA event pairs per phase
@@ -869,6 +870,9 @@ class TrainerWorker:
             toks = torch.cat([b.actions.reshape(-1) for b in batches])
             blp = torch.cat([b.behavior_log_prob.reshape(-1) for b in batches])
             rw = torch.cat([b.rewards.reshape(-1) for b in batches])
+            if self.h_rw is None or self.h_rw.dtype != rw.dtype or self.h_rw.shape != rw.shape:
+                self.h_rw = torch.empty(rw.shape, dtype=rw.dtype, pin_memory=True)
+            self.h_rw.copy_(rw, non_blocking=True)   # mean_reward, read after the sync
             if ev_t is not None:
                 ev_t["loss0"].record(s)
             self.loss.launch(self.logits, toks, blp, rw, self.dl, stream=s)
@@ -897,13 +901,14 @@ class TrainerWorker:
         if ev_t is not None:
             ev_t["host_enqueue_s"] = t_enq - t0
             ev_t["host_wait_s"] = time.perf_counter() - t_enq
-        if bool(self.h_flags[2]):
+        hf = self.h_flags.numpy()
+        if hf[2]:
             raise RunAbort("peer gradient exchange timed out (a learner stopped arriving)",
                            lane=LaneId.TRAINER.value, epoch=self.version)
         sv = self.h_stats.numpy().copy()
-        skipped = float(self.h_skip[0]) != 0.0
-        grad_bad = bool(self.h_flags[0])
-        norm = float(self.h_misc[0])
+        skipped = float(self.h_skip.numpy()[0]) != 0.0
+        grad_bad = bool(hf[0])
+        norm = float(self.h_misc.numpy()[0])
         if skipped or grad_bad or not np.isfinite(norm):
             # the device skipped the step: parameters and moments untouched
             # (loss abort / non-finite loss on any rank, or a non-finite
@@ -913,10 +918,10 @@ class TrainerWorker:
             if skipped:
                 raise GrpoAbort(int(ids[0]), "a peer learner's batch aborted the update")
             raise GrpoAbort(int(ids[0]), "non-finite loss or gradient")
-        rw_h = rw.cpu().numpy().reshape(self.n_groups, cfg.group_size)
+        rw_h = self.h_rw.numpy().reshape(self.n_groups, cfg.group_size)
         stats = stats_from_vector(sv, self.loss.group_ids, self.loss.order,
                                   self.n_groups * cfg.group_size, rw_h)
-        if bool(self.h_flags[1]):
+        if hf[1]:
             raise RunAbort("non-finite parameters after update",
                            lane=LaneId.TRAINER.value, epoch=self.version)
         pol.step += 1

@@ -224,3 +224,17 @@ def test_coefficient_condition_widens_only_cancelling_rows():
     coeff = np.array([s.ravel()[0], 1e-6 * s.ravel()[1]])
     rc = row_condition(coeff, s, 3)
     assert rc.shape == (6,) and np.all(rc[:3] == 1.0) and np.allclose(rc[3:], 1e6)
+
+
+def test_mean_reward_matches_the_per_group_definition():
+    """grpo._mean_reward (one row-wise reduction) is bit-identical to the
+    reference's float(np.mean([b.rewards.mean() for b in batches]))
+    (grpo.py:291) in canonical order, for many group sizes."""
+    from paper_2605_13276_b200.grpo import _mean_reward
+    rng = np.random.default_rng(5)
+    for G in list(range(2, 40)) + [64, 127, 128, 129, 300]:
+        for n_groups in (1, 3, 64):
+            r = (rng.standard_normal((n_groups, G)) * rng.uniform(0.01, 100)).astype(np.float32)
+            order = rng.permutation(n_groups)
+            want = float(np.mean([r[k].mean() for k in order]))
+            assert _mean_reward(r, order) == want, (G, n_groups)

@@ -48,5 +48,6 @@ for rep in range(reps):
                               "value": round(out["value"]),
                               "ms_wall": round(out["ms_per_step_wall"], 3),
                               "ms_dev": round(out["ms_per_step_device"], 3),
-                              "phases": out["phases_ms_rank0"]}), flush=True)
+                              "phases": out["phases_ms_rank0"],
+                              "host": out.get("host_ms_rank0")}), flush=True)
 dist.destroy_process_group()
