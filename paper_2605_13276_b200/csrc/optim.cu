@@ -318,29 +318,56 @@ struct SumSrcs {
   const float* p[kMaxSumSrcs];
 };
 
+// NS > 0: the source count at compile time, so every source's load of a
+// granule is issued before the first add (NS loads in flight per granule,
+// 4 NS per thread); NS == 0: runtime count (any n_src up to 16)
+template <int NS>
 __device__ __forceinline__ float4 sum_srcs4(const SumSrcs& s, int n_src, int64_t q) {
+  constexpr int kMax = NS > 0 ? NS : kMaxSumSrcs;
+  float4 v[NS > 0 ? NS : 1];
+  if constexpr (NS > 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) v[k] = __ldcs(reinterpret_cast<const float4*>(s.p[k]) + q);
+  }
   double x = 0.0, y = 0.0, z = 0.0, w = 0.0;
-  for (int k = 0; k < n_src; ++k) {
-    const float4 v = __ldcs(reinterpret_cast<const float4*>(s.p[k]) + q);
-    x += v.x;
-    y += v.y;
-    z += v.z;
-    w += v.w;
+#pragma unroll
+  for (int k = 0; k < kMax; ++k) {
+    if constexpr (NS == 0) {
+      if (k >= n_src) break;
+    }
+    const float4 u = NS > 0 ? v[NS > 0 ? k : 0]
+                            : __ldcs(reinterpret_cast<const float4*>(s.p[k]) + q);
+    x += u.x;
+    y += u.y;
+    z += u.z;
+    w += u.w;
   }
   return make_float4(static_cast<float>(x), static_cast<float>(y), static_cast<float>(z),
                      static_cast<float>(w));
 }
 
+// one element (tails): static source indices, so the pointer table stays in
+// the parameter bank (a runtime index would copy it to local memory)
+template <int NS>
+__device__ __forceinline__ float sum_srcs1(const SumSrcs& s, int n_src, int64_t i) {
+  constexpr int kMax = NS > 0 ? NS : kMaxSumSrcs;
+  double t = 0.0;
+#pragma unroll
+  for (int k = 0; k < kMax; ++k) {
+    if (NS == 0 && k >= n_src) break;
+    t += s.p[k][i];
+  }
+  return static_cast<float>(t);
+}
+
+template <int NS>
 __global__ void __launch_bounds__(kNormThreads) sum_sumsq_blocks_f32_kernel(
     SumSrcs src, int n_src, int64_t n, int64_t n_all, int64_t per_block, double div,
     float* __restrict__ out, double* __restrict__ partial, unsigned* __restrict__ nonfinite) {
   __shared__ double red[kNormThreads / 32];
   if (blockIdx.x == gridDim.x - 1) {   // [n, n_all): summed, outside the norm
-    for (int64_t i = n + threadIdx.x; i < n_all; i += kNormThreads) {
-      double t = 0.0;
-      for (int k = 0; k < n_src; ++k) t += src.p[k][i];
-      out[i] = static_cast<float>(t);
-    }
+    for (int64_t i = n + threadIdx.x; i < n_all; i += kNormThreads)
+      out[i] = sum_srcs1<NS>(src, n_src, i);
   }
   if (static_cast<int64_t>(blockIdx.x) * per_block >= n) return;
   const int64_t lo = blockIdx.x * per_block;
@@ -361,10 +388,10 @@ __global__ void __launch_bounds__(kNormThreads) sum_sumsq_blocks_f32_kernel(
   float4* o4 = reinterpret_cast<float4*>(out);
   int64_t j = threadIdx.x;
   for (; j + 3 * kNormThreads < nq; j += 4 * kNormThreads) {
-    const float4 a = sum_srcs4(src, n_src, q0 + j);
-    const float4 b = sum_srcs4(src, n_src, q0 + j + kNormThreads);
-    const float4 c = sum_srcs4(src, n_src, q0 + j + 2 * kNormThreads);
-    const float4 d = sum_srcs4(src, n_src, q0 + j + 3 * kNormThreads);
+    const float4 a = sum_srcs4<NS>(src, n_src, q0 + j);
+    const float4 b = sum_srcs4<NS>(src, n_src, q0 + j + kNormThreads);
+    const float4 c = sum_srcs4<NS>(src, n_src, q0 + j + 2 * kNormThreads);
+    const float4 d = sum_srcs4<NS>(src, n_src, q0 + j + 3 * kNormThreads);
     o4[q0 + j] = a;
     o4[q0 + j + kNormThreads] = b;
     o4[q0 + j + 2 * kNormThreads] = c;
@@ -374,15 +401,13 @@ __global__ void __launch_bounds__(kNormThreads) sum_sumsq_blocks_f32_kernel(
     bad |= bad4(a) | bad4(b) | bad4(c) | bad4(d);
   }
   for (; j < nq; j += kNormThreads) {
-    const float4 a = sum_srcs4(src, n_src, q0 + j);
+    const float4 a = sum_srcs4<NS>(src, n_src, q0 + j);
     o4[q0 + j] = a;
     acc0 += sq4(a);
     bad |= bad4(a);
   }
   for (int64_t i = lo + nq * 4 + threadIdx.x; i < hi; i += kNormThreads) {
-    double t = 0.0;
-    for (int k = 0; k < n_src; ++k) t += src.p[k][i];
-    const float f = static_cast<float>(t);
+    const float f = sum_srcs1<NS>(src, n_src, i);
     out[i] = f;
     const double x = f;
     acc0 += x * x;
@@ -561,8 +586,17 @@ extern "C" int dvla_grad_sum_f32(const float* const* srcs, int n_src, int64_t n,
   DVLA_CUDA_TRY(cudaMemsetAsync(partial, 0, nblocks * sizeof(double), st));
   if (n_all > 0) {
     const int used = n > 0 ? static_cast<int>((n + per - 1) / per) : 1;
-    sum_sumsq_blocks_f32_kernel<<<used, kNormThreads, 0, st>>>(
-        s, n_src, n, n_all, per, div, out, partial, reinterpret_cast<unsigned*>(nonfinite_out));
+    auto launch = [&](auto kern) {
+      kern<<<used, kNormThreads, 0, st>>>(s, n_src, n, n_all, per, div, out, partial,
+                                          reinterpret_cast<unsigned*>(nonfinite_out));
+    };
+    switch (n_src) {
+      case 2: launch(sum_sumsq_blocks_f32_kernel<2>); break;
+      case 3: launch(sum_sumsq_blocks_f32_kernel<3>); break;
+      case 4: launch(sum_sumsq_blocks_f32_kernel<4>); break;
+      case 8: launch(sum_sumsq_blocks_f32_kernel<8>); break;
+      default: launch(sum_sumsq_blocks_f32_kernel<0>); break;
+    }
     if (int rc = launch_check("sum_sumsq_blocks_f32_kernel")) return rc;
   }
   norm_finish_kernel<<<1, kFinishThreads, 0, st>>>(partial, nblocks, sumsq_out, 0);
