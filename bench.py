@@ -1149,12 +1149,29 @@ def run_ours(a):
         barrier()
         # the last step's result as read back on the host vs the device one
         e2e_ok = bool(torch.equal(h_stats[(e_k[0] - 1) % 2], tl.stats_dev.cpu()))
+        # the bound: a plain pinned host -> device copy of the logits alone
+        h2d_best = 1e9
+        for _ in range(2):
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            slots[0][0].copy_(h_logits, non_blocking=True)
+            c1.record(stream)
+            torch.cuda.synchronize()
+            h2d_best = min(h2d_best, c0.elapsed_time(c1))
+        h2d_gbs = R * V * 2 / (h2d_best / 1e3) / 1e9
         h2d = R * V * 2 + R * 4 + N_GROUPS * G * C * 4 + N_GROUPS * G * 4
         e2e = {"value": world * N_GROUPS * G * e_steps / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": _lib.ST_LEN * 8,
                "steps": e_steps, "ms_per_step": ems / e_steps,
                "pipelining": "two input slots: step k+1's H2D copy overlaps step k's kernel",
-               "result_read_back": e2e_ok}
+               "result_read_back": e2e_ok,
+               "roofline": {"bound": "pcie_h2d", "unit": "GB/s",
+                            "achieved": round(h2d / (ems / e_steps / 1e3) / 1e9, 2),
+                            "peak": round(h2d_gbs, 2),
+                            "frac": round(h2d / (ems / e_steps / 1e3) / 1e9 / h2d_gbs, 4),
+                            "peak_source": "measured in this run: one pinned 1.84 GB "
+                                           "host->device copy, best of 2 (split over 2-8 "
+                                           "streams it is no faster: tools/h2d_probe.py)"}}
         del h_logits, slots
 
     del dl
