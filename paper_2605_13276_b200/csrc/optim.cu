@@ -11,7 +11,28 @@ namespace dvla {
 
 struct AdamConsts {
   double beta1, one_m_beta1, beta2, one_m_beta2, bc1, bc2, lr, eps;
+  double ibc1, ibc2;   // RN(1 / bc1), RN(1 / bc2): host IEEE divisions
 };
+
+// a / b, correctly rounded, for a divisor fixed per launch with y = RN(1/b)
+// computed on the host: q = RN(a y), the remainder r = a - b q exactly (one
+// FMA), then RN(q + r y) -- Markstein's correction, which returns RN(a/b)
+// when y is within half an ulp of 1/b and q within one ulp of a/b.  Three
+// f64 operations instead of __ddiv_rn's reciprocal refinement and range
+// checks; used for |a| in [2^-900, 2^1000] (every intermediate normal for
+// the divisors here, 1e-3 .. 16), the full division elsewhere, the sign of
+// a zero kept (tests/test_grpo_gpu.py: bitwise against numpy on 4M wide
+// inputs per step / node count, subnormal and -0 moments included).
+__device__ __forceinline__ double div_const(double a, double b, double y) {
+  const double aa = fabs(a);
+  if (aa >= 0x1p-900 && aa <= 0x1p+1000) {
+    const double q = __dmul_rn(a, y);
+    const double r = __fma_rn(-q, b, a);
+    return __fma_rn(r, y, q);
+  }
+  if (a == 0.0) return a;
+  return __ddiv_rn(a, b);
+}
 
 // one element, the reference's arithmetic in its order (grpo.py:143-150)
 __device__ __forceinline__ float adam_elem(float p, double gi, double& m, double& v,
@@ -22,8 +43,8 @@ __device__ __forceinline__ float adam_elem(float p, double gi, double& m, double
   vi = __dadd_rn(vi, __dmul_rn(c.one_m_beta2, __dmul_rn(gi, gi)));
   m = mi;
   v = vi;
-  const double mh = __ddiv_rn(mi, c.bc1);
-  const double vh = __ddiv_rn(vi, c.bc2);
+  const double mh = div_const(mi, c.bc1, c.ibc1);
+  const double vh = div_const(vi, c.bc2, c.ibc2);
   const double upd = __dsub_rn(static_cast<double>(p),
                                __ddiv_rn(__dmul_rn(c.lr, mh), __dadd_rn(__dsqrt_rn(vh), c.eps)));
   return __double2float_rn(upd);
@@ -105,6 +126,7 @@ struct TailArgs {
   int64_t n;
   AdamConsts c;
   double div;
+  double idiv;   // RN(1 / div)
   const double* norm;
   double max_norm;
   const float* skip;
@@ -112,9 +134,10 @@ struct TailArgs {
   unsigned* nonfinite;
 };
 
-__device__ __forceinline__ double tail_grad(float g32, double div, bool clip, double f) {
+__device__ __forceinline__ double tail_grad(float g32, double div, double idiv, bool clip,
+                                            double f) {
   double gi = static_cast<double>(g32);
-  if (div != 1.0) gi = __ddiv_rn(gi, div);
+  if (div != 1.0) gi = div_const(gi, div, idiv);
   if (clip) gi = __dmul_rn(gi, f);
   return gi;
 }
@@ -148,10 +171,10 @@ __global__ void __launch_bounds__(256, DVLA_ADAM_CTAS) adam_tail_kernel(TailArgs
       float2 pa = p2[i], pb = p2[i + stride];
       const float2 ga = __ldcs(g2 + i), gb = __ldcs(g2 + i + stride);
       double2 ma = m2[i], mb = m2[i + stride], va = v2[i], vb = v2[i + stride];
-      pa.x = adam_elem(pa.x, tail_grad(ga.x, a.div, clip, f), ma.x, va.x, a.c);
-      pa.y = adam_elem(pa.y, tail_grad(ga.y, a.div, clip, f), ma.y, va.y, a.c);
-      pb.x = adam_elem(pb.x, tail_grad(gb.x, a.div, clip, f), mb.x, vb.x, a.c);
-      pb.y = adam_elem(pb.y, tail_grad(gb.y, a.div, clip, f), mb.y, vb.y, a.c);
+      pa.x = adam_elem(pa.x, tail_grad(ga.x, a.div, a.idiv, clip, f), ma.x, va.x, a.c);
+      pa.y = adam_elem(pa.y, tail_grad(ga.y, a.div, a.idiv, clip, f), ma.y, va.y, a.c);
+      pb.x = adam_elem(pb.x, tail_grad(gb.x, a.div, a.idiv, clip, f), mb.x, vb.x, a.c);
+      pb.y = adam_elem(pb.y, tail_grad(gb.y, a.div, a.idiv, clip, f), mb.y, vb.y, a.c);
       p2[i] = pa;
       p2[i + stride] = pb;
       m2[i] = ma;
@@ -168,8 +191,8 @@ __global__ void __launch_bounds__(256, DVLA_ADAM_CTAS) adam_tail_kernel(TailArgs
       float2 pa = p2[i];
       const float2 ga = __ldcs(g2 + i);
       double2 ma = m2[i], va = v2[i];
-      pa.x = adam_elem(pa.x, tail_grad(ga.x, a.div, clip, f), ma.x, va.x, a.c);
-      pa.y = adam_elem(pa.y, tail_grad(ga.y, a.div, clip, f), ma.y, va.y, a.c);
+      pa.x = adam_elem(pa.x, tail_grad(ga.x, a.div, a.idiv, clip, f), ma.x, va.x, a.c);
+      pa.y = adam_elem(pa.y, tail_grad(ga.y, a.div, a.idiv, clip, f), ma.y, va.y, a.c);
       p2[i] = pa;
       m2[i] = ma;
       v2[i] = va;
@@ -180,7 +203,7 @@ __global__ void __launch_bounds__(256, DVLA_ADAM_CTAS) adam_tail_kernel(TailArgs
   }
   for (int64_t i = done + t0; i < a.n; i += stride) {
     double mi = a.m[i], vi = a.v[i];
-    const float pn = adam_elem(a.p[i], tail_grad(a.g[i], a.div, clip, f), mi, vi, a.c);
+    const float pn = adam_elem(a.p[i], tail_grad(a.g[i], a.div, a.idiv, clip, f), mi, vi, a.c);
     a.p[i] = pn;
     a.m[i] = mi;
     a.v[i] = vi;
@@ -485,7 +508,8 @@ extern "C" int dvla_adam_step(float* params, const double* grad, double* m, doub
     b1p = pow(beta1, static_cast<double>(step));
     b2p = pow(beta2, static_cast<double>(step));
   }
-  const AdamConsts c{beta1, 1.0 - beta1, beta2, 1.0 - beta2, 1.0 - b1p, 1.0 - b2p, lr, eps};
+  const AdamConsts c{beta1, 1.0 - beta1, beta2, 1.0 - beta2, 1.0 - b1p, 1.0 - b2p, lr, eps,
+                     1.0 / (1.0 - b1p), 1.0 / (1.0 - b2p)};
   const int vec = ((reinterpret_cast<uintptr_t>(params) & 7) == 0 &&
                    (reinterpret_cast<uintptr_t>(grad) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(m) & 15) == 0 &&
@@ -614,8 +638,9 @@ extern "C" int dvla_adam_tail_f32(float* params, const float* grad, double* m, d
   const double b1p = pow(beta1, static_cast<double>(step));
   const double b2p = pow(beta2, static_cast<double>(step));
   TailArgs a{params, grad, m, v, n,
-             AdamConsts{beta1, 1.0 - beta1, beta2, 1.0 - beta2, 1.0 - b1p, 1.0 - b2p, lr, eps},
-             div, norm, max_norm, skip, static_cast<__nv_bfloat16*>(bf16_out),
+             AdamConsts{beta1, 1.0 - beta1, beta2, 1.0 - beta2, 1.0 - b1p, 1.0 - b2p, lr, eps,
+                        1.0 / (1.0 - b1p), 1.0 / (1.0 - b2p)},
+             div, 1.0 / div, norm, max_norm, skip, static_cast<__nv_bfloat16*>(bf16_out),
              reinterpret_cast<unsigned*>(nonfinite_out)};
   const int vec = ((reinterpret_cast<uintptr_t>(params) & 7) == 0 &&
                    (reinterpret_cast<uintptr_t>(grad) & 7) == 0 &&

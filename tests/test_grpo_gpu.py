@@ -355,3 +355,59 @@ def test_grad_sum_is_the_node_order_f64_sum(dev, n_src, n, extra):
                                           ss.data_ptr(), bad.data_ptr(), ws.data_ptr(), st),
                    "dvla_grad_sum_f32")
         assert int(bad) == 1
+
+
+def _adam_tail_numpy(p, g32, m, v, t, lr, b1, b2, eps, div, f=None):
+    """The reference update in numpy f64 (grpo.py:137-150, runtime.py:788
+    ÷ nodes, grpo.py:297-301 scaling): every operation correctly rounded."""
+    gi = g32.astype(np.float64)
+    if div != 1.0:
+        gi = gi / div
+    if f is not None:
+        gi = gi * f
+    m2 = b1 * m + (1.0 - b1) * gi
+    v2 = b2 * v + (1.0 - b2) * (gi * gi)
+    mh = m2 / (1.0 - b1 ** t)
+    vh = v2 / (1.0 - b2 ** t)
+    p2 = (p.astype(np.float64) - (lr * mh) / (np.sqrt(vh) + eps)).astype(np.float32)
+    return p2, m2, v2
+
+
+@pytest.mark.parametrize("t,div", [(1, 1.0), (2, 3.0), (5, 4.0), (37, 7.0), (1000, 1.0),
+                                   (30000, 3.0)])
+def test_adam_tail_is_bitwise_on_wide_inputs(dev, t, div):
+    """dvla_adam_tail_f32 (the learner's optimizer tail) against the
+    reference arithmetic in numpy, bit for bit, on 4M elements spanning the
+    f64 range the moments reach (zeros, -0, subnormal moments, 1e-300 ..
+    1e+30) for several steps and node counts."""
+    import torch
+
+    from paper_2605_13276_b200 import _lib
+    rng = np.random.default_rng(t * 10 + int(div))
+    n = 1 << 22
+    p = (rng.standard_normal(n) * 10.0 ** rng.uniform(-6, 2, n)).astype(np.float32)
+    g = (rng.standard_normal(n) * 10.0 ** rng.uniform(-30, 3, n)).astype(np.float32)
+    m = rng.standard_normal(n) * 10.0 ** rng.uniform(-300, 30, n)
+    v = np.abs(rng.standard_normal(n)) * 10.0 ** rng.uniform(-300, 30, n)
+    m[:64], v[:64] = 0.0, 0.0
+    m[64:128] = -0.0
+    m[128:192], v[128:192] = 1e-310, 3e-315           # subnormal f64
+    g[192:256] = 0.0
+    m[256:320] = np.nextafter(2.0, 0.0)               # all-ones significands
+    v[256:320] = np.nextafter(1.0, 0.0)
+    lr, b1, b2, eps = 1e-3, 0.9, 0.999, 1e-8
+    want_p, want_m, want_v = _adam_tail_numpy(p, g, m, v, t, lr, b1, b2, eps, div)
+    tp, tg = torch.from_numpy(p).to(dev), torch.from_numpy(g).to(dev)
+    tm, tv = torch.from_numpy(m).to(dev), torch.from_numpy(v).to(dev)
+    w16 = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.check(_lib.dvla_adam_tail_f32(tp.data_ptr(), tg.data_ptr(), tm.data_ptr(),
+                                       tv.data_ptr(), n, t, lr, b1, b2, eps, div, None, 0.0,
+                                       None, w16.data_ptr(), bad.data_ptr(),
+                                       torch.cuda.current_stream().cuda_stream),
+               "dvla_adam_tail_f32")
+    got_m, got_v, got_p = tm.cpu().numpy(), tv.cpu().numpy(), tp.cpu().numpy()
+    assert np.array_equal(got_m.view(np.int64), want_m.view(np.int64))
+    assert np.array_equal(got_v.view(np.int64), want_v.view(np.int64))
+    assert np.array_equal(got_p.view(np.int32), want_p.view(np.int32))
+    assert torch.equal(w16.cpu(), torch.from_numpy(want_p).bfloat16())
