@@ -938,9 +938,18 @@ def _swim_model(swim, world, roofline, sampler, optimizer):
         f = sim.fit_check(res, {"mode": mode, "throughput": live["transitions_per_s"],
                                 "rollout_time": live["rollout_time"],
                                 "actor_time": live["actor_time"]}, threshold=0.25)
-        return {"predicted_trajectories_per_s": res.throughput * per_traj,
-                "live_trajectories_per_s": live["trajectories_per_s"],
-                "fit": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in f.items()}}
+        out = {"predicted_trajectories_per_s": res.throughput * per_traj,
+               "live_trajectories_per_s": live["trajectories_per_s"],
+               "fit": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in f.items()}}
+        if mode == "async":
+            # both lanes run on one GPU here: a live lane's host time includes
+            # waiting for the GPU the other lane holds, which the DES books as
+            # slot waiting, not lane time -- the overlapped run is judged on
+            # throughput
+            out["fit"]["pass_throughput"] = f["throughput_dev"] <= 0.25
+            out["fit"]["note"] = ("lane times include waiting for the shared GPU; "
+                                  "judged on throughput")
+        return out
 
     # one closed loop per GPU, coupled only through the gradient mean: each
     # GPU is modelled as its own node with the all-reduce inside the trainer
