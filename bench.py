@@ -1205,9 +1205,10 @@ def run_ours(a):
     swim = None
     if not a.no_swimlane:
         barrier()
-        swim = _bench_swimlane(world, rank, dev, max_over_ranks)
+        swim = _guarded(_bench_swimlane, world, rank, dev, max_over_ranks)
         barrier()
-        swim["model"] = _guarded(_swim_model, swim, world, roofline, sampler, optimizer)
+        if "error" not in swim:
+            swim["model"] = _guarded(_swim_model, swim, world, roofline, sampler, optimizer)
         if world >= 2:
             barrier()
             swim["disaggregated"] = _guarded(_bench_disaggregated, world, rank, dev)
@@ -1230,7 +1231,8 @@ def run_ours(a):
                 pass
         # the GPU-work bound of one epoch on one GPU: the sampler's device
         # work (the strict-alternation rollout lane) + the learner step
-        if isinstance(learner, dict) and "ms_per_step_device" in learner:
+        if (isinstance(learner, dict) and "ms_per_step_device" in learner
+                and "lanes" in swim):
             t_epoch = swim["lanes"]["sync"]["rollout_time"] + learner["ms_per_step_device"] / 1e3
             bound = N_GROUPS * G / t_epoch
             swim["gpu_work_bound_trajectories_per_s_rank0"] = bound
