@@ -402,6 +402,18 @@ int dvla_stream_write_u32(uint32_t* addr, uint32_t value, void* stream);
  * error the host reads after its sync, not a hung stream). */
 int dvla_wait_flags_u32(const uint32_t* flags, uint32_t mask, uint32_t target,
                         uint64_t timeout_ns, uint32_t* err_dev, void* stream);
+/* k (1..4) scalars reduced across the n (<= 32) ranks of a peer exchange
+ * through IPC-mapped peer memory, in rank order, identical on every rank:
+ * kind 0 = f64 sum, kind 1 = u32 max.  This rank's values (`local`, device)
+ * go to slot [rank] of every peer's slot array (peer_slots[p], [n][k]
+ * values, mapped here) and the epoch to peer_flags[p][rank]; the local
+ * flags my_flags[p] (written by peer p) are acquire-polled, bounded by
+ * timeout_ns (then *err_dev |= 1); out[0, k) = the reduction.  One warp,
+ * stream-ordered; epochs increase by one per call. */
+int dvla_peer_reduce(int kind, const void* local, int k, void* const* peer_slots,
+                     uint32_t* const* peer_flags, int rank, int n, const void* my_slots,
+                     const uint32_t* my_flags, uint32_t epoch, uint64_t timeout_ns,
+                     uint32_t* err_dev, void* out, void* stream);
 
 /* ---- switch-multicast (NVLS) replication ---------------------------------
  * Replaces the same ControlPlane.broadcast -> WeightMailbox.deliver data path

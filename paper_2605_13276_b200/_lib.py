@@ -173,6 +173,9 @@ dvla_stream_wait_u32 = _proto("dvla_stream_wait_u32", [_vp, C.c_uint32, _vp])
 dvla_stream_write_u32 = _proto("dvla_stream_write_u32", [_vp, C.c_uint32, _vp])
 dvla_wait_flags_u32 = _proto("dvla_wait_flags_u32", [_vp, C.c_uint32, C.c_uint32, C.c_uint64, _vp,
                                                        _vp])
+dvla_peer_reduce = _proto("dvla_peer_reduce", [_i32, _vp, _i32, C.POINTER(_vp), C.POINTER(_vp), _i32,
+                                                 _i32, _vp, _vp, C.c_uint32, C.c_uint64, _vp, _vp,
+                                                 _vp])
 dvla_mc_supported = _proto("dvla_mc_supported", [_i32, C.POINTER(_i32)])
 dvla_mc_create = _proto("dvla_mc_create", [_i32, _sz, C.POINTER(_i32), C.POINTER(_sz),
                                            C.POINTER(_pp)])

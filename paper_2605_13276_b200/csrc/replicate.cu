@@ -505,6 +505,103 @@ extern "C" int dvla_wait_flags_u32(const uint32_t* flags, uint32_t mask, uint32_
   return launch_check("wait_flags_kernel");
 }
 
+// A few scalars reduced across the N ranks of a peer exchange over
+// IPC-mapped peer memory, in rank order (every rank computes the same
+// value): the learner's global sum of squares (f64 sum) and its abort /
+// non-finite words (u32 max) without a collective library call.  Lane 0
+// stores this rank's k values into slot [rank] of every peer's slot array,
+// fences, and release-stores the epoch into every peer's flag [rank];
+// lane p acquire-polls the local flag [p] (bounded: a timeout ORs *err);
+// then lane 0 reduces the n contributions in rank order into out[0, k).
+constexpr int kPeerMax = 32;
+constexpr int kScalMax = 4;
+struct PeerScalarTable {
+  void* slots[kPeerMax];      // rank p's slot array ([n][k] values), mapped here
+  uint32_t* flags[kPeerMax];  // rank p's flag array ([n] u32), mapped here
+};
+
+template <class T>
+__global__ void peer_reduce_kernel(const T* local, int k, PeerScalarTable peers, int rank, int n,
+                                   const T* my_slots, const uint32_t* my_flags, uint32_t epoch,
+                                   uint64_t timeout_ns, uint32_t* err, T* out) {
+  const int lane = threadIdx.x;
+  T mine[kScalMax];
+  for (int j = 0; j < k; ++j) mine[j] = local[j];
+  if (lane == 0) {
+    for (int p = 0; p < n; ++p) {
+      if (p == rank) continue;
+      T* dst = static_cast<T*>(peers.slots[p]) + rank * k;
+      for (int j = 0; j < k; ++j) dst[j] = mine[j];
+    }
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    for (int p = 0; p < n; ++p)
+      if (p != rank) st_release_sys(peers.flags[p] + rank, epoch);
+  }
+  if (lane < n && lane != rank) {
+    const uint64_t t0 = globaltimer_ns();
+    uint32_t ns = 32;
+    while (ld_acquire_sys(my_flags + lane) < epoch) {
+      __nanosleep(ns);
+      if (ns < 512) ns <<= 1;
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        atomicOr(err, 1u);
+        break;
+      }
+    }
+  }
+  __syncwarp();
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  if (lane == 0) {
+    for (int j = 0; j < k; ++j) {
+      T acc = T(0);
+      for (int p = 0; p < n; ++p) {
+        const T v = (p == rank) ? mine[j]
+                                : *reinterpret_cast<const volatile T*>(my_slots + p * k + j);
+        if constexpr (sizeof(T) == 8) {
+          acc += v;                      // f64 sum in rank order
+        } else {
+          acc = acc > v ? acc : v;       // u32 max
+        }
+      }
+      if constexpr (sizeof(T) == 8) {
+        out[j] = acc;
+      } else {  // keep what this launch's own timeout may have ORed in place
+        const T cur = *reinterpret_cast<volatile T*>(out + j);
+        out[j] = acc > cur ? acc : cur;
+      }
+    }
+  }
+}
+
+extern "C" int dvla_peer_reduce(int kind, const void* local, int k, void* const* peer_slots,
+                                uint32_t* const* peer_flags, int rank, int n,
+                                const void* my_slots, const uint32_t* my_flags, uint32_t epoch,
+                                uint64_t timeout_ns, uint32_t* err_dev, void* out,
+                                void* stream) {
+  if (!local || !peer_slots || !peer_flags || !my_slots || !my_flags || !err_dev || !out ||
+      k < 1 || k > kScalMax || n < 1 || n > kPeerMax || rank < 0 || rank >= n ||
+      (kind != 0 && kind != 1))
+    return fail(DVLA_ERR_USAGE, "dvla_peer_reduce: bad arguments");
+  PeerScalarTable t{};
+  for (int p = 0; p < n; ++p) {
+    if (p != rank && (!peer_slots[p] || !peer_flags[p]))
+      return fail(DVLA_ERR_USAGE, "dvla_peer_reduce: missing peer %d mapping", p);
+    t.slots[p] = peer_slots[p];
+    t.flags[p] = peer_flags[p];
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (kind == 0)
+    peer_reduce_kernel<double><<<1, 32, 0, st>>>(
+        static_cast<const double*>(local), k, t, rank, n, static_cast<const double*>(my_slots),
+        my_flags, epoch, timeout_ns, err_dev, static_cast<double*>(out));
+  else
+    peer_reduce_kernel<uint32_t><<<1, 32, 0, st>>>(
+        static_cast<const uint32_t*>(local), k, t, rank, n,
+        static_cast<const uint32_t*>(my_slots), my_flags, epoch, timeout_ns, err_dev,
+        static_cast<uint32_t*>(out));
+  return launch_check("peer_reduce_kernel");
+}
+
 extern "C" int dvla_stream_write_u32(uint32_t* addr, uint32_t value, void* stream) {
   if (!addr) return fail(DVLA_ERR_USAGE, "null flag address");
   if (int rc = drv_check()) return rc;

@@ -76,8 +76,10 @@ class PeerGradExchange:
         N, cs, r = self.N, self.cs, self.rank
         self.stage = _PoolRegion(stage_pool, N * cs * 4)
         self.stage_t = self.stage.t[: N * cs * 4].view(torch.float32).view(N, cs)
-        # ready[0:N) | ack[32:32+N) | weights landed[64:64+N)
-        self.flags = _Slab(512, self.dev.index)
+        # u32 words: ready[0:N) | ack[32:32+N) | weights landed[64:64+N) |
+        # scalar-sum flags [96:96+N) | scalar-max flags [128:128+N); bytes
+        # [1024, 2048): f64 scalar-sum slots [N][k]; [2048, 2560): u32 max slots
+        self.flags = _Slab(4096, self.dev.index)
         self.flags.t.zero_()
         torch.cuda.synchronize(self.dev)
         if N > 32:
@@ -128,6 +130,15 @@ class PeerGradExchange:
         self.ev_block = [torch.cuda.Event() for _ in range(N)]
         self.ev_pushed = None     # the previous step's last push (gin reusable)
         self.epoch = 0
+        # peer tables of the scalar reductions (the own entry unused)
+        self._sum_slots = (C.c_void_p * N)(*[self.peer[p][1] + 1024 if p != r else 0
+                                              for p in range(N)])
+        self._sum_flags = (C.c_void_p * N)(*[self.peer[p][1] + 4 * 96 if p != r else 0
+                                              for p in range(N)])
+        self._max_slots = (C.c_void_p * N)(*[self.peer[p][1] + 2048 if p != r else 0
+                                              for p in range(N)])
+        self._max_flags = (C.c_void_p * N)(*[self.peer[p][1] + 4 * 128 if p != r else 0
+                                              for p in range(N)])
         self.srcs = (C.c_void_p * N)(*[
             (gin[r].data_ptr() if p == r else self.stage_t[p].data_ptr()) for p in range(N)])
         dist.barrier(group=group)
@@ -228,6 +239,25 @@ class PeerGradExchange:
         ev.record(c)
         stream.wait_event(ev)
         self._wait(64, e, stream)
+
+    def reduce_sum_f64(self, vals, stream):
+        """vals (device f64, k <= 4 values) <- their sum over the ranks in
+        rank order, identical on every rank (in place; once per step)."""
+        self._reduce(0, vals, 1024, 96, self._sum_slots, self._sum_flags, stream)
+
+    def reduce_max_u32(self, vals, stream):
+        """vals (device int32/uint32 flags, k <= 4) <- their max over the
+        ranks (in place; once per step)."""
+        self._reduce(1, vals, 2048, 128, self._max_slots, self._max_flags, stream)
+
+    def _reduce(self, kind, vals, slot_off, flag_word, peer_slots, peer_flags, stream):
+        from . import _lib
+        k = vals.numel()
+        _lib.check(_lib.dvla_peer_reduce(kind, vals.data_ptr(), k, peer_slots, peer_flags,
+                                         self.rank, self.N, self.flags.ptr + slot_off,
+                                         self.flags.ptr + 4 * flag_word, self.epoch,
+                                         self.timeout_ns, self.err.data_ptr(), vals.data_ptr(),
+                                         stream.cuda_stream), "dvla_peer_reduce")
 
     def check(self):
         """Host side, after the stream has been synchronised: raise if a

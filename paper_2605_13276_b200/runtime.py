@@ -766,10 +766,13 @@ class TrainerWorker:
         input -> reduce-scatter (sum): copy-engine pushes over NVLink as the
         blocks complete + a node-order f64 sum (exchange.PeerGradExchange),
         or NCCL reduce_scatter -> this rank's block / N -> global
-        norm (block sums of squares all-reduced) -> optimizer tail on the
-        block (skipped on every rank when any rank's loss aborted: the skip
-        words are summed with the gradient) -> NCCL all-gather of the bf16
-        blocks -> non-finite flags max-reduced."""
+        norm (block sums of squares summed over the ranks: in rank order over
+        NVLink with the exchange, else NCCL) -> optimizer tail on the block
+        (skipped on every rank when any rank's loss aborted: the skip words
+        are summed with the gradient) -> all-gather of the bf16 blocks
+        (pushed per optimizer chunk, or NCCL) -> non-finite / timeout flags
+        max-reduced (over NVLink with the exchange, else NCCL).  With the
+        exchange the step makes no collective-library call."""
         import torch
         import torch.distributed as dist
 
@@ -808,7 +811,10 @@ class TrainerWorker:
                                                 self.norm_ws.data_ptr(), s.cuda_stream),
                        "dvla_grad_sumsq_f32")
         g = self.gcfg
-        dist.all_reduce(self.sumsq, op=dist.ReduceOp.SUM, group=grp)
+        if ex is not None:   # the blocks' sums of squares, rank order, over NVLink
+            ex.reduce_sum_f64(self.sumsq, s)
+        else:
+            dist.all_reduce(self.sumsq, op=dist.ReduceOp.SUM, group=grp)
         torch.sqrt(self.sumsq, out=self.norm)
         if ev_t is not None and "norm1" in ev_t:
             ev_t["norm1"].record(s)
@@ -837,7 +843,10 @@ class TrainerWorker:
             if ev_t is not None and "adam1" in ev_t:
                 ev_t["adam1"].record(s)
             dist.all_gather_into_tensor(pol.w16pad, pol.w16_own, group=grp)
-        dist.all_reduce(self.flags, op=dist.ReduceOp.MAX, group=grp)
+        if ex is not None:   # abort / non-finite / timeout words, max over the learners
+            ex.reduce_max_u32(self.flags, s)
+        else:
+            dist.all_reduce(self.flags, op=dist.ReduceOp.MAX, group=grp)
 
     def update(self, batches: list, transport_nodes: int | None = None) -> dict:
         """One GRPO update on one epoch of groups (reference runtime.py:768-800).

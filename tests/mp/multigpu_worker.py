@@ -132,11 +132,21 @@ def _zero1_matches_full_gradient(rank, world):
         assert tr.sharded == name.startswith("zero1")
         if tr.sharded:   # the default reduce-scatter is the peer exchange
             assert (tr.exchange is not None) == (name == "zero1"), name
-        for step in range(3):
-            tr.update(batches(step))
+        norms = [tr.update(batches(step))["grad_norm"] for step in range(3)]
         torch.cuda.synchronize()
         out[name] = (tr.policy.w16.clone(), tr.policy.master.clone(), tr.policy)
+        out[name + "_norms"] = norms
         tr.close()
+    # the global gradient norm (peer: block sums of squares reduced in rank
+    # order over NVLink; NCCL's all-reduce; the exact path's full gradient)
+    # agrees on every rank and across the paths
+    allnorms = [None] * world
+    dist.all_gather_object(allnorms, out["zero1_norms"])
+    assert all(nm == allnorms[0] for nm in allnorms), allnorms
+    for a_, b_ in zip(out["zero1_norms"], out["full_norms"]):
+        assert abs(a_ - b_) <= 1e-5 * abs(b_), (a_, b_)
+    for a_, b_ in zip(out["zero1_norms"], out["zero1_nccl_norms"]):
+        assert abs(a_ - b_) <= 1e-6 * abs(b_), (a_, b_)
     w_z, m_z, pol_z = out["zero1"]
     w_f, m_f, _ = out["full"]
     # peer exchange (node-order f64 sum) vs NCCL reduce-scatter (f32 ring

@@ -37,13 +37,14 @@ for rep in range(reps):
     for v in variants:
         sc, gc = v[0], v[1]
         os.environ["DVLA_GATHER_CHUNKS"] = gc
-        if len(v) > 2:
+        if len(v) > 2 and v[2]:
             os.environ["DVLA_GRAD_SUB"] = v[2]
         else:
             os.environ.pop("DVLA_GRAD_SUB", None)
         out = bench._bench_learner_step(world, rank, dev, barrier, mor, scatter=sc)
         if rank == 0:
-            print(json.dumps({"rep": rep, "scatter": sc, "gather_chunks": gc,
+            print(json.dumps({"rep": rep, "scatter": sc + ":" + ":".join(v[2:]),
+                              "gather_chunks": gc,
                               "grad_sub": out.get("grad_gemms_per_block"),
                               "value": round(out["value"]),
                               "ms_wall": round(out["ms_per_step_wall"], 3),
