@@ -172,6 +172,36 @@ def _zero1_matches_full_gradient(rank, world):
     dist.barrier()
 
 
+def _exchange_scalars(rank, world):
+    """The exchange's scalar reductions: f64 sums in rank order and u32
+    maxima, identical on every rank, over several epochs."""
+    from paper_2605_13276_b200.exchange import PeerGradExchange
+    from paper_2605_13276_b200.pools import Pool, PoolKind
+    dev = torch.device("cuda", torch.cuda.current_device())
+    pool = Pool(PoolKind.MODEL_COMPUTE, (world + 1) * 4096 * 4 + (1 << 20), device=dev)
+    ex = PeerGradExchange(torch.zeros(world, 4096, device=dev), pool)
+    s = torch.cuda.current_stream()
+    for step in range(1, 4):
+        ex.epoch += 1
+        v = torch.tensor([rank + 0.1 * step, 1e-300 * (rank + 1)], dtype=torch.float64,
+                         device=dev)
+        f = torch.tensor([7 * step if rank == world - 1 else 0, rank, 0], dtype=torch.int32,
+                         device=dev)
+        ex.reduce_sum_f64(v, s)
+        ex.reduce_max_u32(f, s)
+        torch.cuda.synchronize()
+        want0 = 0.0
+        for r in range(world):
+            want0 += r + 0.1 * step
+        assert v[0].item() == want0, (v[0].item(), want0)
+        assert v[1].item() == sum(1e-300 * (r + 1) for r in range(world))
+        assert f.tolist() == [7 * step, world - 1, 0], f.tolist()
+    ex.check()
+    dist.barrier()
+    ex.close()
+    dist.barrier()
+
+
 def _exchange_timeout(rank, world):
     """The peer exchange's waits are bounded: when the other learners never
     push, rank 0's sum wait times out, sets the error word and the stream
@@ -400,6 +430,7 @@ def main():
     _zero1_matches_full_gradient(rank, world)
     if rank == 0:
         print("ZERO1_OK", flush=True)
+    _exchange_scalars(rank, world)
     _exchange_timeout(rank, world)
     if rank == 0:
         print("EXCHANGE_TIMEOUT_OK", flush=True)
