@@ -9,11 +9,12 @@ summed in f64 in node order and divided by the node count (runtime.py:618-
 
 B200 design.  The head gradient dW = dl^T x is a row-blocked GEMM: block j
 (the rows rank j owns under ZeRO-1) is computed by every rank and needed,
-summed, only by rank j.  Each rank computes its blocks in the order
-j = r + 1, r + 2, ..., r (its own block LAST), and as soon as block j is in
-HBM a copy engine pushes it over NVLink into rank j's staging slot for r --
-no SMs are taken from the GEMM, whose remaining blocks hide the transfer
-(rank j's last incoming block is finished one block-GEMM before j's own).
+summed, only by rank j.  Each rank computes the peers' blocks first (as
+the one or two contiguous runs of rows around its own block, one GEMM
+each) and its own block LAST; as soon as a run is in HBM a copy engine
+pushes each of its blocks over NVLink into the owner's staging slot for r
+-- no SMs are taken from the GEMMs, and the own block's GEMM hides the
+last pushes.
 Then one HBM-bound kernel on rank j sums its own block and the N - 1 staged
 ones in f64 in NODE order (the reference's arithmetic, deterministic) and
 computes the block's sum of squares in the same pass
@@ -51,8 +52,9 @@ class PeerGradExchange:
     per GPU).  `stage_pool` (a device Pool, e.g. MODEL_COMPUTE) holds the
     N x cs f32 staging slots; per step:
         begin(s)                       # before anything writes gin
-        for j in order(): GEMM block j into gin[j]; pushed(j, s)
-        finish(s, out, div, sumsq, nonfinite, workspace)
+        GEMMs into gin's blocks, the own block last (order(): one per block);
+        pushed(j, s) for each peer block j as soon as it is complete
+        finish(s, out, n_norm, div, sumsq, nonfinite, workspace)
     """
 
     def __init__(self, gin, stage_pool, group=None, wbuf=None, err=None,
@@ -130,6 +132,7 @@ class PeerGradExchange:
         self.ev_block = [torch.cuda.Event() for _ in range(N)]
         self.ev_pushed = None     # the previous step's last push (gin reusable)
         self.epoch = 0
+        self._npushed = 0
         # peer tables of the scalar reductions (the own entry unused)
         self._sum_slots = (C.c_void_p * N)(*[self.peer[p][1] + 1024 if p != r else 0
                                               for p in range(N)])
@@ -154,6 +157,7 @@ class PeerGradExchange:
         every peer's previous sum must have read its slot for this rank
         before this step's pushes overwrite it."""
         self.epoch += 1
+        self._npushed = 0
         if self.ev_pushed is not None:
             stream.wait_event(self.ev_pushed)
         if self.epoch > 1:
@@ -179,7 +183,8 @@ class PeerGradExchange:
                    "dvla_memcpy_async")
         _lib.check(_lib.dvla_stream_write_u32(flags_j + 4 * self.rank, e, c.cuda_stream),
                    "dvla_stream_write_u32")
-        if j == self.order()[-2]:   # the last peer block of the step
+        self._npushed += 1
+        if self._npushed == self.N - 1:   # the last peer block of the step
             ev = __import__("torch").cuda.Event()
             ev.record(c)
             self.ev_pushed = ev

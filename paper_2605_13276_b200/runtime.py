@@ -622,6 +622,7 @@ class TrainerWorker:
             shard = (dist.get_rank(reducer.group), nodes)
         else:
             shard = None
+        self.reducer_rank = shard[0] if shard else 0
         self.policy = TokenPolicy(cfg, model_pool, device, shard=shard)
         self.gcfg = GrpoConfig(group_size=cfg.group_size, lr=cfg.lr,
                                max_grad_norm=cfg.max_grad_norm)
@@ -631,20 +632,22 @@ class TrainerWorker:
         self.loss = TokenLoss(self.n_groups, G, C, T, V, self.gcfg, dtype=torch.bfloat16,
                               device=device)
         if self.sharded:
-            # reduce-scatter input: N chunks of Vs rows (+ 64 floats holding the
-            # skip word, so the sum of every rank's abort flag lands in each
-            # rank's chunk); output: this rank's chunk
+            # reduce-scatter input: the gradient's N*Vs rows contiguous (rank j's
+            # block = rows [j Vs, (j+1) Vs); rows past V stay zero), so a GEMM
+            # can cover several owners' blocks at once; output: this rank's
+            # block.  The skip words (loss aborts) travel with the block sums
+            # of squares: scal = [sum of squares, skip] summed over the ranks.
             Vs = self.policy.Vs
-            self.cs = Vs * H + 64
+            self.cs = Vs * H
             self.hg = model_pool.alloc(nodes * self.cs * 4 + self.cs * 4, align=256)
             allg = model_pool.view(self.hg, torch.float32)[: (nodes + 1) * self.cs]
             allg.zero_()
             self.gin = allg[: nodes * self.cs]
             self.gshard = allg[nodes * self.cs:]
-            self.skip = self.gshard[Vs * H:Vs * H + 1]
-            self.skip_in = self.gin.view(nodes, self.cs)[:, Vs * H]
             self.grad2d = None
-            self.sumsq = torch.zeros(1, dtype=torch.float64, device=device)
+            self.scal = torch.zeros(2, dtype=torch.float64, device=device)
+            self.sumsq = self.scal[0:1]
+            self.skip = torch.zeros(1, dtype=torch.float32, device=device)
             self._own_skip = torch.zeros(1, dtype=torch.float32, device=device)
             self.status_out = self._own_skip
             self.exchange = None
@@ -743,22 +746,32 @@ class TrainerWorker:
         if ev_t is not None and "adam1" in ev_t:
             ev_t["adam1"].record(s)
 
-    def _grad_block(self, j: int, sub: int | None = None):
-        """Rows of rank j's block of dW = dl^T x (f32 GEMM output into the
-        reduce-scatter input), as `sub` row-split GEMMs."""
+    def _grad_rows(self, a: int, b: int):
+        """Rows [a, b) of dW = dl^T x (f32 GEMM output into the contiguous
+        reduce-scatter input), as `grad_sub` row-split GEMMs."""
         import torch
-        pol = self.policy
-        V, H, Vs = pol.V, pol.H, pol.Vs
-        a, b = j * Vs, min(V, (j + 1) * Vs)
+        b = min(b, self.policy.V)
         if a >= b:
             return
-        sub = self.grad_sub if sub is None else sub
-        gin2 = self.gin.view(self.reducer.nodes, self.cs)
-        step = max(128, (-(-(b - a) // sub) + 127) // 128 * 128)
+        H = self.policy.H
+        rows = self.gin.view(-1, H)
+        step = max(128, (-(-(b - a) // self.grad_sub) + 127) // 128 * 128)
         for a2 in range(a, b, step):
             b2 = min(b, a2 + step)
             torch.mm(self.dl[:, a2:b2].t(), self.feats_tok, out_dtype=torch.float32,
-                     out=gin2[j, (a2 - a) * H:(b2 - a) * H].view(b2 - a2, H))
+                     out=rows[a2:b2])
+
+    def _grad_segments(self):
+        """The head-gradient GEMMs of this rank under ZeRO-1, in issue order:
+        (first block, end block) ranges of owner blocks -- the peers' blocks
+        as the (at most two) contiguous runs around the own block, larger run
+        first, each one GEMM (an owner block alone is a less efficient GEMM
+        shape on B200: DESIGN.md §6), then the own block, whose GEMM hides
+        the last pushes."""
+        N, r = self.reducer.nodes, self.reducer_rank
+        runs = [(r + 1, N), (0, r)]
+        runs = sorted([x for x in runs if x[1] > x[0]], key=lambda x: x[0] - x[1])
+        return runs + [(r, r + 1)]
 
     def _grad_tail_sharded(self, s, ev_t, mx):
         """N learner GPUs, ZeRO-1 (reference runtime.py:788-796 arithmetic):
@@ -778,43 +791,44 @@ class TrainerWorker:
 
         from . import _lib
         pol, nodes, grp = self.policy, self.reducer.nodes, self.reducer.group
-        nloc = pol.Vs * pol.H
+        Vs = pol.Vs
+        nloc = Vs * pol.H
         ex = self.exchange
         div = float(nodes)
-        block = self._grad_block
 
         if ex is not None:
-            # peer blocks first, each pushed by a copy engine as it completes,
-            # the own block last (it hides the final pushes); then the
-            # node-order sum + this block's sum of squares in one pass
+            # peer blocks first, pushed by a copy engine as each GEMM run
+            # completes, the own block last (it hides the final pushes); then
+            # the node-order sum + this block's sum of squares in one pass
             ex.begin(s)
-            self.skip_in.copy_(self._own_skip.expand(nodes))
-            for j in ex.order():
-                block(j)
-                ex.pushed(j, s)
+            for j0, j1 in self._grad_segments():
+                self._grad_rows(j0 * Vs, j1 * Vs)
+                for j in range(j0, j1):
+                    ex.pushed(j, s)
             if ev_t is not None:
                 ev_t["grad1"].record(s)
             ex.finish(s, self.gshard, nloc, div, self.sumsq, self.flags, self.norm_ws)
-            if ev_t is not None:
-                ev_t["reduce1"].record(s)
         else:
-            for j in range(nodes):
-                block(j)
-            self.skip_in.copy_(self._own_skip.expand(nodes))
+            self._grad_rows(0, nodes * Vs)     # one GEMM: the rows are contiguous
             if ev_t is not None:
                 ev_t["grad1"].record(s)
             dist.reduce_scatter_tensor(self.gshard, self.gin, op=dist.ReduceOp.SUM, group=grp)
-            if ev_t is not None:
-                ev_t["reduce1"].record(s)
             _lib.check(_lib.dvla_grad_sumsq_f32(self.gshard.data_ptr(), nloc, div,
                                                 self.sumsq.data_ptr(), self.flags.data_ptr(),
                                                 self.norm_ws.data_ptr(), s.cuda_stream),
                        "dvla_grad_sumsq_f32")
+        if ev_t is not None:
+            ev_t["reduce1"].record(s)
         g = self.gcfg
-        if ex is not None:   # the blocks' sums of squares, rank order, over NVLink
-            ex.reduce_sum_f64(self.sumsq, s)
+        # [sum of squares, skip] summed over the ranks: the global norm and
+        # the number of ranks whose loss aborted (any -> the step is skipped
+        # on every rank)
+        self.scal[1:2].copy_(self._own_skip)
+        if ex is not None:   # rank order, over NVLink
+            ex.reduce_sum_f64(self.scal, s)
         else:
-            dist.all_reduce(self.sumsq, op=dist.ReduceOp.SUM, group=grp)
+            dist.all_reduce(self.scal, op=dist.ReduceOp.SUM, group=grp)
+        self.skip.copy_(self.scal[1:2])
         torch.sqrt(self.sumsq, out=self.norm)
         if ev_t is not None and "norm1" in ev_t:
             ev_t["norm1"].record(s)

@@ -194,8 +194,14 @@ def _exchange_scalars(rank, world):
         for r in range(world):
             want0 += r + 0.1 * step
         assert v[0].item() == want0, (v[0].item(), want0)
-        assert v[1].item() == sum(1e-300 * (r + 1) for r in range(world))
+        want1 = 0.0   # left to right (Python's sum() compensates since 3.12)
+        for r in range(world):
+            want1 += 1e-300 * (r + 1)
+        assert v[1].item() == want1, (v.tolist(), want1, step)
         assert f.tolist() == [7 * step, world - 1, 0], f.tolist()
+        # (in the learner the next step's writes are ordered after this
+        # read by the exchange's own flags; here a barrier stands in)
+        dist.barrier()
     ex.check()
     dist.barrier()
     ex.close()
