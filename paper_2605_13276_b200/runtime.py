@@ -673,6 +673,7 @@ class TrainerWorker:
         # GEMMs per owner block of the head gradient (DVLA_GRAD_SUB; DESIGN §6:
         # at 4 learners two per block measured 0.15 ms faster, at 2 one)
         self.grad_sub = max(1, int(os.environ.get("DVLA_GRAD_SUB", "1")))
+        self.grad_plan = os.environ.get("DVLA_GRAD_PLAN", "halves")
         self.pos = token_positions(cfg, device)
         self.norm_ws = torch.empty(_lib.dvla_grad_norm_workspace_bytes(n), dtype=torch.uint8,
                                    device=device)
@@ -762,13 +763,22 @@ class TrainerWorker:
                      out=rows[a2:b2])
 
     def _grad_segments(self):
-        """The head-gradient GEMMs of this rank under ZeRO-1, in issue order:
-        (first block, end block) ranges of owner blocks -- the peers' blocks
-        as the (at most two) contiguous runs around the own block, larger run
-        first, each one GEMM (an owner block alone is a less efficient GEMM
-        shape on B200: DESIGN.md §6), then the own block, whose GEMM hides
-        the last pushes."""
+        """The head-gradient GEMMs of this rank under ZeRO-1, in issue order,
+        as (first block, end block) ranges of owner blocks; every peer block
+        a GEMM completes is pushed right after it.
+          "halves" (default): the owner blocks in two halves, each one GEMM
+            of ~V/2 rows (an efficient shape; a single owner block of V/N rows
+            is not on B200 at 4 learners: DESIGN.md §6) -- the other half
+            first, its pushes hidden by the own half's GEMM;
+          "runs": the peers' blocks as the (at most two) contiguous runs
+            around the own block, larger first, then the own block alone
+            (every push hidden, but smaller GEMMs)."""
         N, r = self.reducer.nodes, self.reducer_rank
+        if self.grad_plan == "halves" and N > 2:
+            h = N // 2
+            halves = [(0, h), (h, N)]
+            own = 0 if r < h else 1
+            return [halves[1 - own], halves[own]]
         runs = [(r + 1, N), (0, r)]
         runs = sorted([x for x in runs if x[1] > x[0]], key=lambda x: x[0] - x[1])
         return runs + [(r, r + 1)]
@@ -804,7 +814,8 @@ class TrainerWorker:
             for j0, j1 in self._grad_segments():
                 self._grad_rows(j0 * Vs, j1 * Vs)
                 for j in range(j0, j1):
-                    ex.pushed(j, s)
+                    if j != self.reducer_rank:
+                        ex.pushed(j, s)
             if ev_t is not None:
                 ev_t["grad1"].record(s)
             ex.finish(s, self.gshard, nloc, div, self.sumsq, self.flags, self.norm_ws)
