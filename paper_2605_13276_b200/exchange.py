@@ -9,12 +9,12 @@ summed in f64 in node order and divided by the node count (runtime.py:618-
 
 B200 design.  The head gradient dW = dl^T x is a row-blocked GEMM: block j
 (the rows rank j owns under ZeRO-1) is computed by every rank and needed,
-summed, only by rank j.  Each rank computes the peers' blocks first (as
-the one or two contiguous runs of rows around its own block, one GEMM
-each) and its own block LAST; as soon as a run is in HBM a copy engine
-pushes each of its blocks over NVLink into the owner's staging slot for r
--- no SMs are taken from the GEMMs, and the own block's GEMM hides the
-last pushes.
+summed, only by rank j.  Each rank computes its gradient in a few large
+GEMMs ordered so that its own block comes last (TrainerWorker's plans: the
+other half of the blocks, then its own half; or the peer runs, then its
+own block); as soon as a GEMM is in HBM a copy engine pushes each of its
+peer blocks over NVLink into the owner's staging slot for r -- no SMs are
+taken from the GEMMs, and the last GEMM hides the earlier pushes.
 Then one HBM-bound kernel on rank j sums its own block and the N - 1 staged
 ones in f64 in NODE order (the reference's arithmetic, deterministic) and
 computes the block's sum of squares in the same pass
