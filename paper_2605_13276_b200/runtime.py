@@ -789,10 +789,10 @@ class TrainerWorker:
         input -> reduce-scatter (sum): copy-engine pushes over NVLink as the
         blocks complete + a node-order f64 sum (exchange.PeerGradExchange),
         or NCCL reduce_scatter -> this rank's block / N -> global
-        norm (block sums of squares summed over the ranks: in rank order over
-        NVLink with the exchange, else NCCL) -> optimizer tail on the block
-        (skipped on every rank when any rank's loss aborted: the skip words
-        are summed with the gradient) -> all-gather of the bf16 blocks
+        norm (block sums of squares summed over the ranks together with the
+        skip words: in rank order over NVLink with the exchange, else NCCL)
+        -> optimizer tail on the block (skipped on every rank when any
+        rank's loss aborted) -> all-gather of the bf16 blocks
         (pushed per optimizer chunk, or NCCL) -> non-finite / timeout flags
         max-reduced (over NVLink with the exchange, else NCCL).  With the
         exchange the step makes no collective-library call."""
@@ -807,9 +807,9 @@ class TrainerWorker:
         div = float(nodes)
 
         if ex is not None:
-            # peer blocks first, pushed by a copy engine as each GEMM run
-            # completes, the own block last (it hides the final pushes); then
-            # the node-order sum + this block's sum of squares in one pass
+            # the GEMMs of _grad_segments (own block last); each finished peer
+            # block pushed by a copy engine while the next GEMM runs; then the
+            # node-order sum + this block's sum of squares in one pass
             ex.begin(s)
             for j0, j1 in self._grad_segments():
                 self._grad_rows(j0 * Vs, j1 * Vs)
