@@ -125,13 +125,17 @@ def _zero1_matches_full_gradient(rank, world):
 
     out = {}
     for name, red in (("zero1", GradReducer(world)),
+                      ("zero1_runs", GradReducer(world)),
                       ("zero1_nccl", GradReducer(world, scatter="nccl")),
                       ("full", GradReducer(world, exact=True))):
         pool = Pool(PoolKind.MODEL_COMPUTE, 64 << 20, device=dev)
+        if name == "zero1_runs":   # the other GEMM plan of the peer exchange
+            os.environ["DVLA_GRAD_PLAN"] = "runs"
         tr = TrainerWorker(cfg, rank, pool, red, torch.cuda.Stream(device=dev), dev)
+        os.environ.pop("DVLA_GRAD_PLAN", None)
         assert tr.sharded == name.startswith("zero1")
         if tr.sharded:   # the default reduce-scatter is the peer exchange
-            assert (tr.exchange is not None) == (name == "zero1"), name
+            assert (tr.exchange is not None) == (name != "zero1_nccl"), name
         norms = [tr.update(batches(step))["grad_norm"] for step in range(3)]
         torch.cuda.synchronize()
         out[name] = (tr.policy.w16.clone(), tr.policy.master.clone(), tr.policy)
@@ -152,6 +156,9 @@ def _zero1_matches_full_gradient(rank, world):
     # peer exchange (node-order f64 sum) vs NCCL reduce-scatter (f32 ring
     # sum): the same update up to the sum's rounding
     w_n, m_n, _ = out["zero1_nccl"]
+    w_u, m_u, _ = out["zero1_runs"]
+    du = (m_z - m_u).abs()
+    assert float((du > 1e-6).float().mean()) < 1e-3, float((du > 1e-6).float().mean())
     dn = (m_z - m_n).abs()
     assert float((dn > 1e-6).float().mean()) < 1e-3, float((dn > 1e-6).float().mean())
     assert float((w_z.view(torch.int16) == w_n.view(torch.int16)).float().mean()) > 0.99
