@@ -323,7 +323,8 @@ class B200Rates:
 
 def b200_costs(n_groups: int = 64, group_size: int = 8, chunks: int = 1, tokens: int = 56,
                vocab: int = 32064, hidden: int = 4096, replicas: int = 0, nodes: int = 1,
-               rates: B200Rates = B200Rates(), shared_gpu: bool = True) -> LaneCosts:
+               rates: B200Rates = B200Rates(), shared_gpu: bool = True,
+               peer_exchange: bool = True, gather_chunks: int = 4) -> LaneCosts:
     """Lane costs of the token-head swimlane (runtime.run_swimlane) on B200.
 
     Sampler: logits GEMM [R, H] x [H, V] + one-pass sampling over the logits.
@@ -333,10 +334,14 @@ def b200_costs(n_groups: int = 64, group_size: int = 8, chunks: int = 1, tokens:
     + the optimizer tail on this learner's 1/N of the parameters (46 B each:
     f32 gradient, f64 moments, f32 master, bf16 copy) + the snapshot copy of
     the bf16 weights.  With ``nodes`` = N > 1 learners the gradient is
-    reduce-scattered (f32) and the bf16 blocks all-gathered by NCCL
-    (ZeRO-1): (N - 1) / N (4 + 2) n bytes per GPU and direction at the
-    measured bus bandwidth.  Weight replication to ``replicas`` other GPUs
-    over the chain."""
+    reduce-scattered (f32) and the bf16 blocks all-gathered (ZeRO-1):
+    with ``peer_exchange`` (exchange.PeerGradExchange, the default) both are
+    copy-engine pushes under the gradient GEMM / optimizer tail, so only the
+    own half's peer blocks (pushed after the last GEMM), the last optimizer
+    chunk's pushes and the node-order sum (N + 1 blocks read / written)
+    remain exposed; with NCCL, (N - 1) / N (4 + 2) n bytes per GPU and
+    direction at the measured bus bandwidth.  Weight replication to
+    ``replicas`` other GPUs over the chain."""
     R = n_groups * group_size * chunks * tokens
     n = vocab * hidden
     N = max(int(nodes), 1)
@@ -349,7 +354,14 @@ def b200_costs(n_groups: int = 64, group_size: int = 8, chunks: int = 1, tokens:
     passes = (4.0 * n + 4.0 * n / N + 2 * R * hidden * 2) / hbm
     act = 2 * gemm + loss + tail + snap + passes + rates.launch_overhead_s
     bcast = (n * 2 / (rates.nvlink_gbs * 1e9)) if replicas else 0.0
-    reduce = ((N - 1) / N * n * (4 + 2) / (rates.allreduce_busbw_gbs * 1e9) if N > 1 else 0.0)
+    if N == 1:
+        reduce = 0.0
+    elif peer_exchange:
+        own_half = N // 2 if N > 2 else 1
+        pushes = (own_half - 1) * 4.0 * n / N + (N - 1) * 2.0 * n / N / max(gather_chunks, 1)
+        reduce = pushes / (rates.nvlink_gbs * 1e9) + (N + 1) * 4.0 * n / N / hbm
+    else:
+        reduce = (N - 1) / N * n * (4 + 2) / (rates.allreduce_busbw_gbs * 1e9)
     return LaneCosts(rollout_s=roll, actor_s=act, broadcast_s=bcast, reduce_s=reduce,
                      shared_slots=shared_gpu, transitions_per_epoch=R)
 
