@@ -347,3 +347,27 @@ def test_retire_waits_for_a_newer_install_and_blocks_stale_deposits():
     b3 = _board(limit=1)
     b3.mark_sampler_done()
     b3.retire(0)
+
+
+def test_zero1_gemm_plans_cover_every_block_once_own_last():
+    """TrainerWorker._grad_segments: every owner block in exactly one GEMM
+    range, ranges contiguous, the range holding the own block issued last
+    (its GEMM hides the earlier pushes), for both plans and N = 2..8."""
+    from types import SimpleNamespace
+
+    from paper_2605_13276_b200.runtime import TrainerWorker
+    for plan in ("halves", "runs"):
+        for N in range(2, 9):
+            for r in range(N):
+                me = SimpleNamespace(reducer=SimpleNamespace(nodes=N), reducer_rank=r,
+                                     grad_plan=plan)
+                segs = TrainerWorker._grad_segments(me)
+                blocks = [j for a, b in segs for j in range(a, b)]
+                assert sorted(blocks) == list(range(N)), (plan, N, r, segs)
+                assert all(b > a for a, b in segs)
+                a, b = segs[-1]
+                assert a <= r < b, (plan, N, r, segs)
+                if plan == "halves" and N > 2:
+                    assert len(segs) == 2
+                if plan == "runs" or N == 2:
+                    assert segs[-1] == (r, r + 1)
