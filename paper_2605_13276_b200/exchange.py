@@ -72,6 +72,8 @@ class PeerGradExchange:
         self.rank = dist.get_rank(group)
         if dist.get_world_size(group) != self.N:
             raise UsageError("gin needs one block per rank of the group")
+        if self.N > 32:
+            raise UsageError("at most 32 ranks per exchange")
         self.gin = gin
         self.dev = gin.device
         self.group = group
@@ -84,8 +86,6 @@ class PeerGradExchange:
         self.flags = _Slab(4096, self.dev.index)
         self.flags.t.zero_()
         torch.cuda.synchronize(self.dev)
-        if N > 32:
-            raise UsageError("at most 32 ranks per exchange")
         # peer access for the copy engines (symmetric; IPC mappings also need it
         # for direct stores/loads, copies work either way)
         ranks = (list(range(dist.get_world_size())) if group is None
