@@ -248,6 +248,16 @@ int dvla_adam_tail_f32(float* params, const float* grad, double* m, double* v, i
                        int64_t step, double lr, double beta1, double beta2, double eps,
                        double div, const double* norm, double max_norm, const float* skip,
                        void* bf16_out, uint32_t* nonfinite_out, void* stream);
+/* dvla_adam_tail_f32 whose bf16 copy is also stored into n_peers (<= 31)
+ * other learners' working copies (device pointers mapped here, e.g. CUDA
+ * IPC, at the same element offset): the ZeRO-1 all-gather fused into the
+ * optimizer tail over NVLink.  The stores are fenced system-wide before
+ * the kernel completes; signal the peers after it (stream order). */
+int dvla_adam_tail_f32_bcast(float* params, const float* grad, double* m, double* v, int64_t n,
+                             int64_t step, double lr, double beta1, double beta2, double eps,
+                             double div, const double* norm, double max_norm, const float* skip,
+                             void* bf16_out, void* const* bf16_peers, int n_peers,
+                             uint32_t* nonfinite_out, void* stream);
 int dvla_loss_status(const double* stats, float* skip_out, void* stream);
 
 /* --------------------------------------------------- dual-pool arena */

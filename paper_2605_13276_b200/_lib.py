@@ -217,6 +217,9 @@ dvla_grad_sum_f32 = _proto("dvla_grad_sum_f32", [C.POINTER(_vp), _i32, _i64, _i6
                                                    _vp, _vp, _vp])
 dvla_adam_tail_f32 = _proto("dvla_adam_tail_f32", [
     _vp, _vp, _vp, _vp, _i64, _i64, _f64, _f64, _f64, _f64, _f64, _vp, _f64, _vp, _vp, _vp, _vp])
+dvla_adam_tail_f32_bcast = _proto("dvla_adam_tail_f32_bcast", [
+    _vp, _vp, _vp, _vp, _i64, _i64, _f64, _f64, _f64, _f64, _f64, _vp, _f64, _vp, _vp,
+    C.POINTER(_vp), _i32, _vp, _vp])
 dvla_loss_status = _proto("dvla_loss_status", [_vp, _vp, _vp])
 
 # ---------------------------------------------------- rollout token sampling

@@ -142,7 +142,20 @@ __device__ __forceinline__ double tail_grad(float g32, double div, double idiv, 
   return gi;
 }
 
-__global__ void __launch_bounds__(256, DVLA_ADAM_CTAS) adam_tail_kernel(TailArgs a, int vec) {
+// kPeers: the bf16 copy is also stored straight into every peer learner's
+// working copy (IPC-mapped, same element offset) -- the ZeRO-1 all-gather
+// fused into the optimizer tail: a warp's 128 contiguous bytes go out as one
+// NVLink write per peer while the kernel streams its 46 B / parameter from
+// HBM.
+constexpr int kMaxBf16Peers = 31;
+struct Bf16Peers {
+  __nv_bfloat16* p[kMaxBf16Peers];
+  int n;
+};
+
+template <bool kPeers>
+__global__ void __launch_bounds__(256, DVLA_ADAM_CTAS)
+    adam_tail_kernel(TailArgs a, int vec, Bf16Peers peers) {
   if (a.skip != nullptr && *a.skip != 0.0f) return;
   bool clip = false;
   double f = 1.0;
@@ -182,8 +195,19 @@ __global__ void __launch_bounds__(256, DVLA_ADAM_CTAS) adam_tail_kernel(TailArgs
       v2[i] = va;
       v2[i + stride] = vb;
       if (w2 != nullptr) {
-        w2[i] = __floats2bfloat162_rn(pa.x, pa.y);
-        w2[i + stride] = __floats2bfloat162_rn(pb.x, pb.y);
+        const __nv_bfloat162 ba = __floats2bfloat162_rn(pa.x, pa.y);
+        const __nv_bfloat162 bb = __floats2bfloat162_rn(pb.x, pb.y);
+        w2[i] = ba;
+        w2[i + stride] = bb;
+        if constexpr (kPeers) {
+#pragma unroll
+          for (int q = 0; q < kMaxBf16Peers; ++q) {   // static indices: no local copy
+            if (q >= peers.n) break;
+            __nv_bfloat162* r2 = reinterpret_cast<__nv_bfloat162*>(peers.p[q]);
+            r2[i] = ba;
+            r2[i + stride] = bb;
+          }
+        }
       }
       bad |= !isfinite(pa.x) | !isfinite(pa.y) | !isfinite(pb.x) | !isfinite(pb.y);
     }
@@ -196,7 +220,17 @@ __global__ void __launch_bounds__(256, DVLA_ADAM_CTAS) adam_tail_kernel(TailArgs
       p2[i] = pa;
       m2[i] = ma;
       v2[i] = va;
-      if (w2 != nullptr) w2[i] = __floats2bfloat162_rn(pa.x, pa.y);
+      if (w2 != nullptr) {
+        const __nv_bfloat162 ba = __floats2bfloat162_rn(pa.x, pa.y);
+        w2[i] = ba;
+        if constexpr (kPeers) {
+#pragma unroll
+          for (int q = 0; q < kMaxBf16Peers; ++q) {
+            if (q >= peers.n) break;
+            reinterpret_cast<__nv_bfloat162*>(peers.p[q])[i] = ba;
+          }
+        }
+      }
       bad |= !isfinite(pa.x) | !isfinite(pa.y);
     }
     done = npair * 2;
@@ -207,11 +241,22 @@ __global__ void __launch_bounds__(256, DVLA_ADAM_CTAS) adam_tail_kernel(TailArgs
     a.p[i] = pn;
     a.m[i] = mi;
     a.v[i] = vi;
-    if (a.w16 != nullptr) a.w16[i] = __float2bfloat16_rn(pn);
+    if (a.w16 != nullptr) {
+      const __nv_bfloat16 bn = __float2bfloat16_rn(pn);
+      a.w16[i] = bn;
+      if constexpr (kPeers) {
+#pragma unroll
+        for (int q = 0; q < kMaxBf16Peers; ++q) {
+          if (q >= peers.n) break;
+          peers.p[q][i] = bn;
+        }
+      }
+    }
     bad |= !isfinite(pn);
   }
   if (a.nonfinite != nullptr && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
     atomicOr(a.nonfinite, 1u);
+  if constexpr (kPeers) __threadfence_system();   // peer stores visible before completion
 }
 
 // skip word for adam_tail_kernel from the fused loss's stats vector: 1.0
@@ -647,8 +692,43 @@ extern "C" int dvla_adam_tail_f32(float* params, const float* grad, double* m, d
                    (reinterpret_cast<uintptr_t>(m) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(v) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(bf16_out) & 3) == 0) ? 1 : 0;
-  adam_tail_kernel<<<grid_n(vec ? (n + 1) / 2 : n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      a, vec);
+  adam_tail_kernel<false><<<grid_n(vec ? (n + 1) / 2 : n), 256, 0,
+                             static_cast<cudaStream_t>(stream)>>>(a, vec, Bf16Peers{});
+  return launch_check("adam_tail_kernel");
+}
+
+extern "C" int dvla_adam_tail_f32_bcast(float* params, const float* grad, double* m, double* v,
+                                        int64_t n, int64_t step, double lr, double beta1,
+                                        double beta2, double eps, double div, const double* norm,
+                                        double max_norm, const float* skip, void* bf16_out,
+                                        void* const* bf16_peers, int n_peers,
+                                        uint32_t* nonfinite_out, void* stream) {
+  if (n < 0 || step < 1 || !(div > 0.0) || !bf16_out || n_peers < 0 ||
+      n_peers > kMaxBf16Peers || (n_peers > 0 && !bf16_peers))
+    return fail(DVLA_ERR_USAGE, "adam_tail_bcast: bad arguments (n_peers <= %d)", kMaxBf16Peers);
+  if (n == 0) return DVLA_OK;
+  Bf16Peers peers{};
+  peers.n = n_peers;
+  for (int q = 0; q < n_peers; ++q) {
+    if (!bf16_peers[q] || (reinterpret_cast<uintptr_t>(bf16_peers[q]) & 3) !=
+                              (reinterpret_cast<uintptr_t>(bf16_out) & 3))
+      return fail(DVLA_ERR_USAGE, "adam_tail_bcast: peer %d copy null or misaligned", q);
+    peers.p[q] = static_cast<__nv_bfloat16*>(bf16_peers[q]);
+  }
+  const double b1p = pow(beta1, static_cast<double>(step));
+  const double b2p = pow(beta2, static_cast<double>(step));
+  TailArgs a{params, grad, m, v, n,
+             AdamConsts{beta1, 1.0 - beta1, beta2, 1.0 - beta2, 1.0 - b1p, 1.0 - b2p, lr, eps,
+                        1.0 / (1.0 - b1p), 1.0 / (1.0 - b2p)},
+             div, 1.0 / div, norm, max_norm, skip, static_cast<__nv_bfloat16*>(bf16_out),
+             reinterpret_cast<unsigned*>(nonfinite_out)};
+  const int vec = ((reinterpret_cast<uintptr_t>(params) & 7) == 0 &&
+                   (reinterpret_cast<uintptr_t>(grad) & 7) == 0 &&
+                   (reinterpret_cast<uintptr_t>(m) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(v) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(bf16_out) & 3) == 0) ? 1 : 0;
+  adam_tail_kernel<true><<<grid_n(vec ? (n + 1) / 2 : n), 256, 0,
+                            static_cast<cudaStream_t>(stream)>>>(a, vec, peers);
   return launch_check("adam_tail_kernel");
 }
 

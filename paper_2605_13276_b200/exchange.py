@@ -229,20 +229,34 @@ class PeerGradExchange:
             _lib.check(_lib.dvla_memcpy_async(self.peer_w[p] + off, src, (hi - lo) * 2,
                                               c.cuda_stream), "dvla_memcpy_async")
 
-    def gather_finish(self, stream):
-        """After the last gather_chunk: tell every peer this rank's rows
-        landed, then make `stream` wait until this rank's pushes are done
-        and every peer's rows have landed here."""
+    def peer_rows(self, lo: int = 0):
+        """Device pointers (a ctypes array, one per peer) to element `lo` of
+        this rank's rows inside every peer's wbuf: the targets of an
+        optimizer tail that stores its bf16 rows straight into the peers
+        (dvla_adam_tail_f32_bcast)."""
+        if self.wbuf is None:
+            raise UsageError("this exchange has no weight buffer")
+        off = (self.rank * self.nloc + lo) * 2
+        peers = [p for p in range(self.N) if p != self.rank]
+        return (C.c_void_p * max(len(peers), 1))(*[self.peer_w[p] + off for p in peers])
+
+    def gather_finish(self, stream, by_kernel: bool = False):
+        """After the last gather_chunk (or, by_kernel, after the optimizer
+        tail that stored the rows into the peers itself, on `stream`): tell
+        every peer this rank's rows landed, then make `stream` wait until
+        this rank's pushes are done and every peer's rows have landed here."""
         from . import _lib
         torch = __import__("torch")
-        e, r, c = self.epoch, self.rank, self.copy_stream
+        e, r = self.epoch, self.rank
+        c = stream if by_kernel else self.copy_stream
         for p in range(self.N):
             if p != r:
                 _lib.check(_lib.dvla_stream_write_u32(self.peer[p][1] + 4 * (64 + r), e,
                                                       c.cuda_stream), "dvla_stream_write_u32")
-        ev = torch.cuda.Event()
-        ev.record(c)
-        stream.wait_event(ev)
+        if not by_kernel:
+            ev = torch.cuda.Event()
+            ev.record(c)
+            stream.wait_event(ev)
         self._wait(64, e, stream)
 
     def reduce_sum_f64(self, vals, stream):

@@ -655,9 +655,12 @@ class TrainerWorker:
                 from .exchange import PeerGradExchange
                 self.exchange = PeerGradExchange(self.gin.view(nodes, self.cs), model_pool,
                                                  group=reducer.group, wbuf=self.policy.w16pad)
-                # optimizer-tail chunks whose bf16 rows are pushed to the peers
-                # while the next chunk is stepped (the all-gather, overlapped)
+                # the bf16 all-gather: "kernel" = the optimizer tail stores its
+                # rows into the peers' working copies itself; "ce" = copy-engine
+                # pushes of each optimizer-tail chunk while the next is stepped
+                self.gather_mode = os.environ.get("DVLA_GATHER_MODE", "kernel")
                 self.gather_chunks = int(os.environ.get("DVLA_GATHER_CHUNKS", "4"))
+                self._peer_rows = self.exchange.peer_rows(0)
         else:
             # f32 gradient + the skip word (one all-reduce buffer), long-lived
             self.hg = model_pool.alloc((n + 1) * 4, align=256)
@@ -852,7 +855,19 @@ class TrainerWorker:
                 self.skip.data_ptr(), pol.w16_own.data_ptr() + 2 * lo, self.flags.data_ptr() + 4,
                 s.cuda_stream), "dvla_adam_tail_f32")
 
-        if ex is not None and ex.wbuf is not None:
+        if ex is not None and ex.wbuf is not None and self.gather_mode == "kernel":
+            # the all-gather inside the optimizer tail: its bf16 rows stored
+            # into every peer's working copy by the same kernel
+            _lib.check(_lib.dvla_adam_tail_f32_bcast(
+                pol.master.data_ptr(), self.gshard.data_ptr(), pol.m.data_ptr(),
+                pol.v.data_ptr(), nloc, pol.step + 1, g.lr, g.beta1, g.beta2, g.opt_eps, div,
+                self.norm.data_ptr(), mx, self.skip.data_ptr(), pol.w16_own.data_ptr(),
+                self._peer_rows, nodes - 1, self.flags.data_ptr() + 4, s.cuda_stream),
+                "dvla_adam_tail_f32_bcast")
+            if ev_t is not None and "adam1" in ev_t:
+                ev_t["adam1"].record(s)
+            ex.gather_finish(s, by_kernel=True)
+        elif ex is not None and ex.wbuf is not None:
             # the all-gather as copy-engine pushes of each stepped chunk
             k = max(1, self.gather_chunks)
             step = max(64, (-(-nloc // k) + 63) // 64 * 64)   # 64-element aligned chunks

@@ -125,14 +125,18 @@ def _zero1_matches_full_gradient(rank, world):
 
     out = {}
     for name, red in (("zero1", GradReducer(world)),
+                      ("zero1_ce_gather", GradReducer(world)),
                       ("zero1_runs", GradReducer(world)),
                       ("zero1_nccl", GradReducer(world, scatter="nccl")),
                       ("full", GradReducer(world, exact=True))):
         pool = Pool(PoolKind.MODEL_COMPUTE, 64 << 20, device=dev)
         if name == "zero1_runs":   # the other GEMM plan of the peer exchange
             os.environ["DVLA_GRAD_PLAN"] = "runs"
+        if name == "zero1_ce_gather":   # the all-gather by copy-engine pushes
+            os.environ["DVLA_GATHER_MODE"] = "ce"
         tr = TrainerWorker(cfg, rank, pool, red, torch.cuda.Stream(device=dev), dev)
         os.environ.pop("DVLA_GRAD_PLAN", None)
+        os.environ.pop("DVLA_GATHER_MODE", None)
         assert tr.sharded == name.startswith("zero1")
         if tr.sharded:   # the default reduce-scatter is the peer exchange
             assert (tr.exchange is not None) == (name != "zero1_nccl"), name
@@ -156,6 +160,11 @@ def _zero1_matches_full_gradient(rank, world):
     # peer exchange (node-order f64 sum) vs NCCL reduce-scatter (f32 ring
     # sum): the same update up to the sum's rounding
     w_n, m_n, _ = out["zero1_nccl"]
+    # the optimizer tail storing its bf16 rows into the peers (default) and
+    # the copy-engine pushes deliver the same bytes
+    w_c, m_c, _ = out["zero1_ce_gather"]
+    assert torch.equal(w_c.view(torch.int16), w_z.view(torch.int16))
+    assert torch.equal(m_c, m_z)
     w_u, m_u, _ = out["zero1_runs"]
     du = (m_z - m_u).abs()
     assert float((du > 1e-6).float().mean()) < 1e-3, float((du > 1e-6).float().mean())

@@ -37,10 +37,14 @@ for rep in range(reps):
     for v in variants:
         sc, gc = v[0], v[1]
         os.environ["DVLA_GATHER_CHUNKS"] = gc
-        if len(v) > 3:
+        if len(v) > 3 and v[3]:
             os.environ["DVLA_GRAD_PLAN"] = v[3]
         else:
             os.environ.pop("DVLA_GRAD_PLAN", None)
+        if len(v) > 4:
+            os.environ["DVLA_GATHER_MODE"] = v[4]
+        else:
+            os.environ.pop("DVLA_GATHER_MODE", None)
         if len(v) > 2 and v[2]:
             os.environ["DVLA_GRAD_SUB"] = v[2]
         else:
