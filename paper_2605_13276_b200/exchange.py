@@ -22,6 +22,11 @@ computes the block's sum of squares in the same pass
 each way, the same as a ring reduce-scatter, but in one step with no
 SM-driven pipeline.
 
+The bf16 weight all-gather after the optimizer tail either rides in the
+tail kernel itself (it stores its rows into every peer's working copy
+through the mappings, `peer_rows`, then `gather_finish(by_kernel=True)`)
+or goes as copy-engine pushes per optimizer chunk (`gather_chunk`).
+
 Synchronisation is stream-ordered, with one u32 flag per peer and direction
 in device memory (the same CUDA IPC + stream memory-operation protocol as
 the copy-engine replication chain, replicate.SplitReplicator):

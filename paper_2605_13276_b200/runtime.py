@@ -795,8 +795,9 @@ class TrainerWorker:
         norm (block sums of squares summed over the ranks together with the
         skip words: in rank order over NVLink with the exchange, else NCCL)
         -> optimizer tail on the block (skipped on every rank when any
-        rank's loss aborted) -> all-gather of the bf16 blocks
-        (pushed per optimizer chunk, or NCCL) -> non-finite / timeout flags
+        rank's loss aborted) -> all-gather of the bf16 blocks (stored into
+        the peers by the optimizer-tail kernel itself, or pushed per
+        optimizer chunk by the copy engines, or NCCL) -> non-finite / timeout flags
         max-reduced (over NVLink with the exchange, else NCCL).  With the
         exchange the step makes no collective-library call."""
         import torch
