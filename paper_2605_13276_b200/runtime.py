@@ -767,24 +767,44 @@ class TrainerWorker:
 
     def _grad_segments(self):
         """The head-gradient GEMMs of this rank under ZeRO-1, in issue order,
-        as (first block, end block) ranges of owner blocks; every peer block
-        a GEMM completes is pushed right after it.
-          "halves" (default): the owner blocks in two halves, each one GEMM
-            of ~V/2 rows (an efficient shape; a single owner block of V/N rows
-            is not on B200 at 4 learners: DESIGN.md §6) -- the other half
-            first, its pushes hidden by the own half's GEMM;
+        as (first row, end row, peer blocks complete after this GEMM); every
+        peer block a GEMM completes is pushed right after it, and the last
+        GEMM (part or all of the own block) hides the last pushes.
+          "halves" (default): the owner blocks in two halves, each ~V/2 rows
+            (a single owner block of V/N rows is a less efficient GEMM shape
+            on B200 at 4 learners: DESIGN.md §6) -- the other half first;
+            then, when the own block sits at an end of its half, the half
+            minus the own block's outer half as one GEMM (its peer blocks
+            pushed under the next one) and that outer half last;
+          "halves1": the same with the own half as one GEMM (its peer blocks
+            pushed after it, exposed);
           "runs": the peers' blocks as the (at most two) contiguous runs
-            around the own block, larger first, then the own block alone
-            (every push hidden, but smaller GEMMs)."""
+            around the own block, larger first, then the own block alone."""
         N, r = self.reducer.nodes, self.reducer_rank
-        if self.grad_plan == "halves" and N > 2:
+        Vs = self.policy.Vs
+        plan = self.grad_plan
+        if plan in ("halves", "halves1") and N > 2:
             h = N // 2
             halves = [(0, h), (h, N)]
             own = 0 if r < h else 1
-            return [halves[1 - own], halves[own]]
+            oa, ob = halves[1 - own]
+            segs = [(oa * Vs, ob * Vs, list(range(oa, ob)))]
+            ha, hb = halves[own]
+            mates = [j for j in range(ha, hb) if j != r]
+            cut = (Vs // 2 + 127) // 128 * 128      # the own block's outer part
+            if plan == "halves" and mates and r in (ha, hb - 1) and 0 < cut < Vs:
+                if r == ha:   # own block first in its half: its lower rows last
+                    segs += [(r * Vs + cut, hb * Vs, mates), (r * Vs, r * Vs + cut, [])]
+                else:         # own block last in its half: its upper rows last
+                    segs += [(ha * Vs, r * Vs + Vs - cut, mates),
+                             (r * Vs + Vs - cut, (r + 1) * Vs, [])]
+            else:
+                segs += [(ha * Vs, hb * Vs, mates)]
+            return segs
         runs = [(r + 1, N), (0, r)]
         runs = sorted([x for x in runs if x[1] > x[0]], key=lambda x: x[0] - x[1])
-        return runs + [(r, r + 1)]
+        return ([(a * Vs, b * Vs, list(range(a, b))) for a, b in runs]
+                + [(r * Vs, (r + 1) * Vs, [])])
 
     def _grad_tail_sharded(self, s, ev_t, mx):
         """N learner GPUs, ZeRO-1 (reference runtime.py:788-796 arithmetic):
@@ -815,11 +835,10 @@ class TrainerWorker:
             # block pushed by a copy engine while the next GEMM runs; then the
             # node-order sum + this block's sum of squares in one pass
             ex.begin(s)
-            for j0, j1 in self._grad_segments():
-                self._grad_rows(j0 * Vs, j1 * Vs)
-                for j in range(j0, j1):
-                    if j != self.reducer_rank:
-                        ex.pushed(j, s)
+            for ra, rb, done in self._grad_segments():
+                self._grad_rows(ra, rb)
+                for j in done:
+                    ex.pushed(j, s)
             if ev_t is not None:
                 ev_t["grad1"].record(s)
             ex.finish(s, self.gshard, nloc, div, self.sumsq, self.flags, self.norm_ws)

@@ -350,24 +350,38 @@ def test_retire_waits_for_a_newer_install_and_blocks_stale_deposits():
 
 
 def test_zero1_gemm_plans_cover_every_block_once_own_last():
-    """TrainerWorker._grad_segments: every owner block in exactly one GEMM
-    range, ranges contiguous, the range holding the own block issued last
-    (its GEMM hides the earlier pushes), for both plans and N = 2..8."""
+    """TrainerWorker._grad_segments: the GEMM row ranges tile [0, N Vs)
+    exactly once; every peer block is pushed exactly once, after the GEMM
+    that completes it; the last GEMM computes only own rows (it hides the
+    earlier pushes), for every plan and N = 2..8."""
     from types import SimpleNamespace
 
     from paper_2605_13276_b200.runtime import TrainerWorker
-    for plan in ("halves", "runs"):
+    Vs = 1000
+    for plan in ("halves", "halves1", "runs"):
         for N in range(2, 9):
             for r in range(N):
                 me = SimpleNamespace(reducer=SimpleNamespace(nodes=N), reducer_rank=r,
-                                     grad_plan=plan)
+                                     grad_plan=plan, policy=SimpleNamespace(Vs=Vs))
                 segs = TrainerWorker._grad_segments(me)
-                blocks = [j for a, b in segs for j in range(a, b)]
-                assert sorted(blocks) == list(range(N)), (plan, N, r, segs)
-                assert all(b > a for a, b in segs)
-                a, b = segs[-1]
-                assert a <= r < b, (plan, N, r, segs)
-                if plan == "halves" and N > 2:
-                    assert len(segs) == 2
-                if plan == "runs" or N == 2:
-                    assert segs[-1] == (r, r + 1)
+                rows = sorted((a, b) for a, b, _ in segs)
+                assert rows[0][0] == 0 and rows[-1][1] == N * Vs, (plan, N, r, segs)
+                assert all(x[1] == y[0] for x, y in zip(rows, rows[1:])), (plan, N, r, segs)
+                pushed, done_rows = [], set()
+                for a, b, blocks in segs:
+                    done_rows.update(range(a // 10, b // 10))   # 10-row granules
+                    for j in blocks:
+                        assert j != r
+                        assert set(range(j * Vs // 10, (j + 1) * Vs // 10)) <= done_rows
+                        pushed.append(j)
+                assert sorted(pushed) == [j for j in range(N) if j != r], (plan, N, r, segs)
+                a, b, blocks = segs[-1]
+                assert a < (r + 1) * Vs and b > r * Vs, (plan, N, r, segs)   # own rows last
+                h = N // 2
+                split = plan == "halves" and N > 2 and r in (0, h - 1, h, N - 1) and (
+                    (N - h if r >= h else h) > 1)
+                if plan == "runs" or N == 2 or split:
+                    # the last GEMM is own rows only: every push is hidden
+                    assert r * Vs <= a and b <= (r + 1) * Vs and not blocks, (plan, N, r, segs)
+                if plan != "runs" and N > 2:
+                    assert len(segs) in (2, 3)
