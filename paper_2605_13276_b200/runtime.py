@@ -283,7 +283,6 @@ class GradReducer:
             return True
         import socket
 
-        import torch.distributed as dist
         from .replicate import _gather_by_rank
         hosts = set(_gather_by_rank(socket.gethostname(), self.group).values())
         self.scatter = "peer" if len(hosts) == 1 else "nccl"
