@@ -816,11 +816,18 @@ def _bench_learner_step(world, rank, dev, barrier, max_over_ranks, steps=10, war
            "config": f"V={V} x H={SWIM_H} bf16 head, {N_GROUPS}x{G} traj x {T} tokens per GPU; "
                      f"grad f32 {n * 4 / 1e9:.2f} GB reduce-scattered over {world} GPU(s)",
            "grad_gemms_per_block": getattr(trainer, "grad_sub", 1),
-           "reduce_scatter": (("peer: copy-engine pushes over NVLink overlapped with the "
-                               "gradient GEMM + node-order f64 sum (exchange.PeerGradExchange)")
+           "reduce_scatter": (("peer (exchange.PeerGradExchange): gradient GEMMs in plan "
+                               f"'{getattr(trainer, 'grad_plan', '')}', each finished peer "
+                               "block pushed over NVLink by a copy engine under the next GEMM, "
+                               "node-order f64 sum; norm / abort scalars reduced over peer "
+                               "memory; bf16 all-gather "
+                               + ("stored into the peers by the optimizer-tail kernel"
+                                  if getattr(trainer, "gather_mode", "") == "kernel" else
+                                  "as copy-engine pushes per optimizer chunk")
+                               + "; no collective-library call")
                               if getattr(trainer, "exchange", None) is not None else
-                              ("NCCL reduce_scatter_tensor after the gradient GEMM"
-                               if world > 1 else None)),
+                              ("NCCL: one gradient GEMM, reduce_scatter_tensor, all-reduce of "
+                               "the scalars, all_gather_into_tensor" if world > 1 else None)),
            "steps": steps}
     trainer.close()
     del trainer, sampler, model_pool, env_pool, msgs
