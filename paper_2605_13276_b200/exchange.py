@@ -83,47 +83,70 @@ class PeerGradExchange:
         self.dev = gin.device
         self.group = group
         N, cs, r = self.N, self.cs, self.rank
-        self.stage = _PoolRegion(stage_pool, N * cs * 4)
-        self.stage_t = self.stage.t[: N * cs * 4].view(torch.float32).view(N, cs)
-        # u32 words: ready[0:N) | ack[32:32+N) | weights landed[64:64+N) |
-        # scalar-sum flags [96:96+N) | scalar-max flags [128:128+N); bytes
-        # [1024, 2048): f64 scalar-sum slots [N][k]; [2048, 2560): u32 max slots
-        self.flags = _Slab(4096, self.dev.index)
-        self.flags.t.zero_()
-        torch.cuda.synchronize(self.dev)
-        # peer access for the copy engines (symmetric; IPC mappings also need it
-        # for direct stores/loads, copies work either way)
-        ranks = (list(range(dist.get_world_size())) if group is None
-                 else dist.get_process_group_ranks(group))
-        devs = _gather_by_rank(self.dev.index, group)
-        for g in ranks:
-            if devs[g] != self.dev.index:
-                _lib.dvla_enable_peer_access(self.dev.index, devs[g])
-        # the bf16 weights all-gathered after the optimizer tail (optional):
-        # [N * nloc] in the same pool, rank p's rows at p * nloc
-        self.wbuf = wbuf
-        w_off = None
-        if wbuf is not None:
-            slab = stage_pool._slab
-            w_off = wbuf.data_ptr() - slab.ptr
-            if (wbuf.dtype != torch.bfloat16 or wbuf.numel() % N or w_off < 0
-                    or w_off + wbuf.numel() * 2 > slab.nbytes):
-                raise UsageError("wbuf must be an [N * nloc] bf16 view inside the stage pool")
-            self.nloc = wbuf.numel() // N
-        allh = _gather_by_rank((self.stage.ipc(), self.stage.offset, self.flags.ipc(), w_off),
-                               group)
         self._opened = []
         self.peer = {}   # group rank -> (stage base of that rank, flags base of that rank)
         self.peer_w = {}  # group rank -> that rank's wbuf
-        for p, g in enumerate(ranks):
-            if p == r:
-                continue
-            base = _open_ipc(allh[g][0])
-            fl = _open_ipc(allh[g][2])
-            self._opened += [base, fl]
-            self.peer[p] = (base + allh[g][1], fl)
-            if allh[g][3] is not None:
-                self.peer_w[p] = base + allh[g][3]
+        ranks = (list(range(dist.get_world_size())) if group is None
+                 else dist.get_process_group_ranks(group))
+
+        def agree(err):
+            """Every setup phase ends with an agreement: a failure on any rank
+            (out of pool memory, no IPC / peer access ...) raises the same
+            NativeError on every rank, so the caller can fall back together
+            instead of leaving the others in a collective."""
+            errs = [e for e in _gather_by_rank(err, group).values() if e]
+            if errs:
+                self.close()
+                raise _lib.NativeError("peer gradient exchange setup failed: "
+                                       + "; ".join(errs))
+
+        err = None
+        try:
+            if os.environ.get("DVLA_TEST_EXCHANGE_FAIL_RANK") == str(r):
+                raise RuntimeError("injected failure (DVLA_TEST_EXCHANGE_FAIL_RANK)")
+            self.stage = _PoolRegion(stage_pool, N * cs * 4)
+            self.stage_t = self.stage.t[: N * cs * 4].view(torch.float32).view(N, cs)
+            # u32 words: ready[0:N) | ack[32:32+N) | weights landed[64:64+N) |
+            # scalar-sum flags [96:96+N) | scalar-max flags [128:128+N); bytes
+            # [1024, 2048): f64 scalar-sum slots [N][k]; [2048, 2560): u32 max slots
+            self.flags = _Slab(4096, self.dev.index)
+            self.flags.t.zero_()
+            torch.cuda.synchronize(self.dev)
+            # the bf16 weights all-gathered after the optimizer tail
+            # (optional): [N * nloc] in the same pool, rank p's rows at p * nloc
+            self.wbuf = wbuf
+            w_off = None
+            if wbuf is not None:
+                slab = stage_pool._slab
+                w_off = wbuf.data_ptr() - slab.ptr
+                if (wbuf.dtype != torch.bfloat16 or wbuf.numel() % N or w_off < 0
+                        or w_off + wbuf.numel() * 2 > slab.nbytes):
+                    raise UsageError("wbuf must be an [N * nloc] bf16 view inside the pool")
+                self.nloc = wbuf.numel() // N
+            mine = (self.dev.index, self.stage.ipc(), self.stage.offset, self.flags.ipc(), w_off)
+        except Exception as e:  # noqa: BLE001 - agreed on below
+            err, mine = f"rank {r}: {e}", None
+        agree(err)
+        allh = _gather_by_rank(mine, group)
+        try:
+            # peer access for the copy engines and the kernels' peer stores
+            # (IPC mappings enable it lazily too)
+            for g in ranks:
+                if allh[g][0] != self.dev.index:
+                    _lib.dvla_enable_peer_access(self.dev.index, allh[g][0])
+            for p, g in enumerate(ranks):
+                if p == r:
+                    continue
+                base = _open_ipc(allh[g][1])
+                self._opened.append(base)
+                fl = _open_ipc(allh[g][3])
+                self._opened.append(fl)
+                self.peer[p] = (base + allh[g][2], fl)
+                if allh[g][4] is not None:
+                    self.peer_w[p] = base + allh[g][4]
+        except Exception as e:  # noqa: BLE001 - agreed on below
+            err = f"rank {r}: {e}"
+        agree(err)
         self.copy_stream = torch.cuda.Stream(device=self.dev, priority=-1)
         # bounded waits: a peer that stops arriving sets this word (device
         # int32; the caller's, e.g. a slot of TrainerWorker's flags that is
@@ -295,7 +318,7 @@ class PeerGradExchange:
 
         from .replicate import _close_ipc
         torch.cuda.synchronize(self.dev)
-        for p in self._opened:
+        for p in getattr(self, "_opened", []):
             _close_ipc(p)
         self._opened = []
         self.peer = {}

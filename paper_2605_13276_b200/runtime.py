@@ -651,9 +651,16 @@ class TrainerWorker:
             self.status_out = self._own_skip
             self.exchange = None
             if reducer.peer_scatter():
+                from ._lib import NativeError
                 from .exchange import PeerGradExchange
-                self.exchange = PeerGradExchange(self.gin.view(nodes, self.cs), model_pool,
-                                                 group=reducer.group, wbuf=self.policy.w16pad)
+                try:
+                    self.exchange = PeerGradExchange(self.gin.view(nodes, self.cs), model_pool,
+                                                     group=reducer.group,
+                                                     wbuf=self.policy.w16pad)
+                except NativeError as e:   # raised on every rank alike: NCCL together
+                    log.warning("peer gradient exchange unavailable (%s); NCCL collectives", e)
+                    reducer.scatter = "nccl"
+            if self.exchange is not None:
                 # the bf16 all-gather: "kernel" = the optimizer tail stores its
                 # rows into the peers' working copies itself; "ce" = copy-engine
                 # pushes of each optimizer-tail chunk while the next is stepped

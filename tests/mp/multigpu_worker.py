@@ -224,6 +224,41 @@ def _exchange_scalars(rank, world):
     dist.barrier()
 
 
+def _exchange_setup_failure_falls_back_to_nccl(rank, world):
+    """A setup failure on one rank (injected on the last one) makes every
+    learner fall back to NCCL's collectives together, and the update runs."""
+    from paper_2605_13276_b200.pools import Pool, PoolKind
+    from paper_2605_13276_b200.runtime import GradReducer, SwimlaneConfig, TrainerWorker
+    from paper_2605_13276_b200.grpo import GroupBatch
+    cfg = SwimlaneConfig(n_groups=2, group_size=4, tokens=8, vocab=512, action_bins=256,
+                         hidden=64, seed=5)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    os.environ["DVLA_TEST_EXCHANGE_FAIL_RANK"] = str(world - 1)
+    try:
+        red = GradReducer(world)
+        tr = TrainerWorker(cfg, rank, Pool(PoolKind.MODEL_COMPUTE, 64 << 20, device=dev), red,
+                           torch.cuda.Stream(device=dev), dev)
+    finally:
+        os.environ.pop("DVLA_TEST_EXCHANGE_FAIL_RANK", None)
+    assert tr.sharded and tr.exchange is None and red.scatter == "nccl"
+    G, T, H, V = cfg.group_size, cfg.tokens, cfg.hidden, cfg.vocab
+    g = torch.Generator(device=dev).manual_seed(rank)
+    n = cfg.n_groups * G
+    feats = torch.randn(n, 1, H, device=dev, generator=g).to(torch.bfloat16)
+    toks = torch.randint(0, V, (n, 1, T), device=dev, generator=g, dtype=torch.int32)
+    blp = (torch.randn(n, 1, device=dev, generator=g) - 40.0).float()
+    rw = torch.rand(n, device=dev, generator=g)
+    batches = [GroupBatch(group_id=rank * cfg.n_groups + k, horizon=T, chunk=T,
+                          obs=feats[k * G:(k + 1) * G], actions=toks[k * G:(k + 1) * G],
+                          behavior_log_prob=blp[k * G:(k + 1) * G],
+                          rewards=rw[k * G:(k + 1) * G], behavior_version=0,
+                          tokens=toks[k * G:(k + 1) * G]) for k in range(cfg.n_groups)]
+    st = tr.update(batches)
+    assert st["version"] == 1 and np.isfinite(st["grad_norm"])
+    tr.close()
+    dist.barrier()
+
+
 def _exchange_timeout(rank, world):
     """The peer exchange's waits are bounded: when the other learners never
     push, rank 0's sum wait times out, sets the error word and the stream
@@ -453,6 +488,7 @@ def main():
     if rank == 0:
         print("ZERO1_OK", flush=True)
     _exchange_scalars(rank, world)
+    _exchange_setup_failure_falls_back_to_nccl(rank, world)
     _exchange_timeout(rank, world)
     if rank == 0:
         print("EXCHANGE_TIMEOUT_OK", flush=True)
